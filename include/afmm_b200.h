@@ -1,0 +1,166 @@
+/*
+ * afmm_b200.h -- C ABI of the B200-native AFMM product (libafmm_b200.so).
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj/include/afmm/kernels.hpp):
+ *
+ *   afmm_case_a_f64  replaces afmm::afmm_case_a(const DenseMatrix&, const DenseMatrix&)
+ *                    kernels.hpp:113-136 (real lhs bases, integer rhs reps)
+ *   afmm_case_b_f64  replaces afmm::afmm_case_b(...)      kernels.hpp:142-165
+ *                    (integer lhs reps, real rhs bases)
+ *   afmm_case_{a,b}_f32  the same contract on fp32 storage (the reference is
+ *                    fp64-only, proj/README.md:91; BASELINE configs 3-5 are fp32)
+ *
+ * Plain pointers and sizes only. Inputs are caller-owned row-major n x n
+ * host arrays, element (i,j) at p[i*n+j] (matrix.hpp:41-46); the product is
+ * written to a caller-owned n x n host array; counts are the reference's
+ * OpCounts (op_counts.hpp:17-23). The C ABI cannot throw, so it returns an
+ * afmm_status plus an afmm_error naming the first offender; the C++ wrapper
+ * include/afmm_b200/kernels.hpp rethrows the reference's exception types
+ * with the reference's message text (kernels.hpp:17-19, 32-39; matrix.hpp:55).
+ *
+ * All compute runs on sm_100a CUDA kernels. There is no CPU fallback: without
+ * a usable B200 every compute entry returns AFMM_ERR_CUDA.
+ */
+#ifndef AFMM_B200_H
+#define AFMM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AFMM_B200_ABI_VERSION 1
+
+typedef enum {
+  AFMM_OK = 0,
+  AFMM_ERR_SHAPE = 1,            /* afmm::shape_error (dimension mismatch)               */
+  AFMM_ERR_DOMAIN = 2,           /* std::domain_error (rep not integer / out of range / non-finite) */
+  AFMM_ERR_INVALID_ARGUMENT = 3, /* std::invalid_argument (n == 0, bad option)          */
+  AFMM_ERR_CUDA = 4,             /* CUDA runtime / driver failure, no device            */
+  AFMM_ERR_UNSUPPORTED = 5,      /* |rep| >= 2^31 (device loop-counter limit)           */
+  AFMM_ERR_OUT_OF_MEMORY = 6
+} afmm_status;
+
+typedef enum { AFMM_CASE_A = 0, AFMM_CASE_B = 1 } afmm_case;
+typedef enum { AFMM_F64 = 0, AFMM_F32 = 1 } afmm_dtype;
+
+typedef enum {
+  /* Bit-exact with the reference: every Z element receives its terms in
+   * increasing k, each as |rep| sequential `acc += step` (kernels.hpp:95-104). */
+  AFMM_MODE_ORDER_PRESERVING = 0,
+  /* Same additions, reassociated (split-k partial sums combined in a fixed
+   * order). Within 1e-12 (f64) / 1e-5 (f32) of the reference, normalised by
+   * sum_k |X[i,k]|*|Y[k,j]|. */
+  AFMM_MODE_FAST = 1
+} afmm_mode;
+
+/* op_counts.hpp:17-23 */
+typedef struct {
+  uint64_t additions;
+  uint64_t multiplications; /* always 0: the device path never multiplies an element */
+  uint64_t zero_skips;
+} afmm_op_counts;
+
+typedef enum {
+  AFMM_ERRKIND_NONE = 0,
+  AFMM_ERRKIND_NOT_INTEGER = 1,   /* kernels.hpp:31-34 */
+  AFMM_ERRKIND_OUT_OF_RANGE = 2,  /* kernels.hpp:36-39 */
+  AFMM_ERRKIND_NON_FINITE = 3,    /* matrix.hpp:31-35 (DenseMatrix ctor) */
+  AFMM_ERRKIND_SHAPE = 4,         /* kernels.hpp:15-21 */
+  AFMM_ERRKIND_EMPTY = 5,         /* matrix.hpp:54-57 */
+  AFMM_ERRKIND_REP_TOO_LARGE = 6, /* device limit, no reference counterpart */
+  AFMM_ERRKIND_OTHER = 7
+} afmm_error_kind;
+
+typedef struct {
+  int32_t kind;      /* afmm_error_kind */
+  int32_t operand;   /* 0 = lhs, 1 = rhs */
+  uint64_t row;      /* first offender in row-major order */
+  uint64_t col;
+  double value;      /* the offending element, widened to double */
+  char message[256]; /* the exact text the reference's exception would carry */
+} afmm_error;
+
+typedef struct {
+  int32_t mode;      /* afmm_mode */
+  int32_t device;    /* CUDA device ordinal; -1 = current */
+  int32_t split_k;   /* fast mode only: 0 = auto */
+  int32_t reserved;
+} afmm_options;
+
+/* ---- reference-facing entry points (host buffers) ------------------------ */
+
+afmm_status afmm_case_a_f64(const double* lhs, uint64_t n_lhs, const double* rhs, uint64_t n_rhs,
+                            double* out, const afmm_options* options, afmm_op_counts* counts,
+                            afmm_error* error);
+afmm_status afmm_case_b_f64(const double* lhs, uint64_t n_lhs, const double* rhs, uint64_t n_rhs,
+                            double* out, const afmm_options* options, afmm_op_counts* counts,
+                            afmm_error* error);
+afmm_status afmm_case_a_f32(const float* lhs, uint64_t n_lhs, const float* rhs, uint64_t n_rhs,
+                            float* out, const afmm_options* options, afmm_op_counts* counts,
+                            afmm_error* error);
+afmm_status afmm_case_b_f32(const float* lhs, uint64_t n_lhs, const float* rhs, uint64_t n_rhs,
+                            float* out, const afmm_options* options, afmm_op_counts* counts,
+                            afmm_error* error);
+
+/* ---- device-resident entry points ----------------------------------------
+ * An afmm_context owns a CUDA stream binding and a grow-only workspace on one
+ * device. Calls on one context are serialised internally; distinct contexts
+ * may be used concurrently. */
+typedef struct afmm_context afmm_context;
+
+afmm_status afmm_context_create(int32_t device, afmm_context** ctx);
+void afmm_context_destroy(afmm_context* ctx);
+/* Enqueue work on `stream` (a cudaStream_t; NULL = the legacy default stream). */
+afmm_status afmm_context_set_stream(afmm_context* ctx, void* stream);
+
+/* Z rows [row_begin, row_end) of lhs * rhs, all pointers device memory.
+ * lhs/rhs are n x n with leading dimension `ld` (elements); `out` receives
+ * (row_end - row_begin) rows with leading dimension `ld_out`, row r of the
+ * slab holding Z row row_begin + r. Validation of the whole rep operand is
+ * done on the device before any product element is computed.
+ * When `sync` is nonzero the call waits for completion and fills counts /
+ * error; when zero it only enqueues, and afmm_context_finish() later returns
+ * the status, counts and error of the last enqueued call. */
+afmm_status afmm_product_device(afmm_context* ctx, int32_t which_case, int32_t dtype,
+                                const void* lhs, const void* rhs, uint64_t n, uint64_t ld,
+                                void* out, uint64_t ld_out, uint64_t row_begin, uint64_t row_end,
+                                const afmm_options* options, int32_t sync,
+                                afmm_op_counts* counts, afmm_error* error);
+afmm_status afmm_context_finish(afmm_context* ctx, afmm_op_counts* counts, afmm_error* error);
+
+/* Per-row work W_i (exact additions of Z row i) for the row partition:
+ * Case A  W_i = sum_{k: X[i,k] != 0} sum_j |llround Y[k,j]|
+ * Case B  W_i = sum_k |llround X[i,k]| * nnz(Y[k,:])
+ * (closed forms of kernels.hpp:119-134 / :148-163). Written to the host
+ * array work[n]. Device pointers as in afmm_product_device. */
+afmm_status afmm_row_work_device(afmm_context* ctx, int32_t which_case, int32_t dtype,
+                                 const void* lhs, const void* rhs, uint64_t n, uint64_t ld,
+                                 uint64_t* work, afmm_error* error);
+
+/* Cut n rows into `parts` contiguous ranges of (as near as possible) equal
+ * total work: cuts[0] = 0, cuts[parts] = n, range p = [cuts[p], cuts[p+1]).
+ * Pure host function (no device needed). */
+afmm_status afmm_partition_rows(const uint64_t* work, uint64_t n, uint32_t parts, uint64_t* cuts);
+
+/* ---- roofline ---------------------------------------------------------------
+ * Measure the CUDA-core FP-add peak of `device` with a register-resident
+ * add-chain microbenchmark (the same instruction mix as the product's inner
+ * loop: FADD2 for f32, DADD for f64). Returns additions per second. */
+afmm_status afmm_fp_add_peak(int32_t device, int32_t dtype, double* adds_per_second,
+                             double* sm_clock_mhz);
+
+/* Number of kernels the library launched on this process since load (the
+ * bench's gpu_launches claim). */
+uint64_t afmm_kernel_launch_count(void);
+const char* afmm_status_string(afmm_status s);
+int32_t afmm_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* AFMM_B200_H */

@@ -1,0 +1,168 @@
+// ref_shim.cpp -- C-ABI shim over the UNMODIFIED reference headers.
+//
+// TEST INFRASTRUCTURE ONLY. oracle/Makefile compiles this file against
+// /root/reference/proj/include (the reference's sources where they lie; no
+// copy) with the reference's Release flags (-O3 -ffp-contract=off,
+// proj/CMakeLists.txt:8-16) into oracle/_ref/libafmm_ref.so. It exists so the
+// tests and the golden-vector script can call the real reference kernels
+// (proj/include/afmm/kernels.hpp:113,142), the reference generator
+// (random.hpp:111) and the reference tests' integer generator
+// (test_kernels.cpp:16-24, restated here on top of detail::uniform_below).
+
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "afmm/bench.hpp"
+#include "afmm/errors.hpp"
+#include "afmm/kernels.hpp"
+#include "afmm/matrix.hpp"
+#include "afmm/random.hpp"
+
+namespace {
+
+struct RefCounts {
+  std::uint64_t additions, multiplications, zero_skips;
+};
+
+// Status: 0 ok, 1 shape_error, 2 domain_error, 3 invalid_argument, 4 other.
+int classify_and_copy(const std::exception& e, int code, char* msg, std::size_t cap) {
+  if (msg && cap) {
+    std::strncpy(msg, e.what(), cap - 1);
+    msg[cap - 1] = '\0';
+  }
+  return code;
+}
+
+template <class Fn>
+int guarded(Fn&& fn, char* msg, std::size_t cap) {
+  try {
+    fn();
+    if (msg && cap) msg[0] = '\0';
+    return 0;
+  } catch (const afmm::shape_error& e) {
+    return classify_and_copy(e, 1, msg, cap);
+  } catch (const std::domain_error& e) {
+    return classify_and_copy(e, 2, msg, cap);
+  } catch (const std::invalid_argument& e) {
+    return classify_and_copy(e, 3, msg, cap);
+  } catch (const std::exception& e) {
+    return classify_and_copy(e, 4, msg, cap);
+  }
+}
+
+afmm::DenseMatrix wrap(const double* p, std::uint64_t n) {
+  return afmm::DenseMatrix(n, std::vector<double>(p, p + n * n));
+}
+
+template <class Kernel>
+int run(Kernel kernel, const double* lhs, std::uint64_t n_lhs, const double* rhs,
+        std::uint64_t n_rhs, double* out, RefCounts* counts, char* msg, std::size_t cap) {
+  return guarded(
+      [&] {
+        const auto l = wrap(lhs, n_lhs);
+        const auto r = wrap(rhs, n_rhs);
+        const afmm::MultiplyResult res = kernel(l, r);
+        const auto d = res.product.data();
+        std::memcpy(out, d.data(), d.size() * sizeof(double));
+        if (counts) {
+          counts->additions = res.counts.additions;
+          counts->multiplications = res.counts.multiplications;
+          counts->zero_skips = res.counts.zero_skips;
+        }
+      },
+      msg, cap);
+}
+
+}  // namespace
+
+extern "C" {
+
+int ref_afmm_case_a(const double* lhs, std::uint64_t n_lhs, const double* rhs,
+                    std::uint64_t n_rhs, double* out, RefCounts* counts, char* msg,
+                    std::size_t cap) {
+  return run([](const auto& l, const auto& r) { return afmm::afmm_case_a(l, r); }, lhs, n_lhs,
+             rhs, n_rhs, out, counts, msg, cap);
+}
+
+int ref_afmm_case_b(const double* lhs, std::uint64_t n_lhs, const double* rhs,
+                    std::uint64_t n_rhs, double* out, RefCounts* counts, char* msg,
+                    std::size_t cap) {
+  return run([](const auto& l, const auto& r) { return afmm::afmm_case_b(l, r); }, lhs, n_lhs,
+             rhs, n_rhs, out, counts, msg, cap);
+}
+
+int ref_multiply_ijk(const double* lhs, const double* rhs, std::uint64_t n, double* out,
+                     RefCounts* counts, char* msg, std::size_t cap) {
+  return run([](const auto& l, const auto& r) { return afmm::multiply_ijk(l, r); }, lhs, n, rhs,
+             n, out, counts, msg, cap);
+}
+
+// DenseMatrix(n) with n == 0 -> std::invalid_argument (matrix.hpp:54-57).
+int ref_make_matrix(std::uint64_t n, char* msg, std::size_t cap) {
+  return guarded([&] { afmm::DenseMatrix m(n); (void)m; }, msg, cap);
+}
+
+// DenseMatrix(n, values) finite-only constructor (matrix.hpp:25-36).
+int ref_make_matrix_from(const double* p, std::uint64_t n, char* msg, std::size_t cap) {
+  return guarded([&] { (void)wrap(p, n); }, msg, cap);
+}
+
+std::uint64_t ref_splitmix64(std::uint64_t x) { return afmm::detail::splitmix64(x); }
+
+// test_kernels.cpp:16-24 / acceptance.hpp:72-82, on the reference's own
+// detail::uniform_below.
+void ref_random_integer_matrix(std::uint64_t n, int low, int high, std::uint64_t seed,
+                               double* out) {
+  std::mt19937_64 rng(seed);
+  const auto range = static_cast<std::uint64_t>(high - low + 1);
+  for (std::uint64_t idx = 0; idx < n * n; ++idx) {
+    out[idx] = static_cast<double>(
+        low + static_cast<long long>(afmm::detail::uniform_below(rng, range)));
+  }
+}
+
+int ref_generate(std::uint64_t n, double density, double mu_prime, int role, double low,
+                 double high, std::uint64_t seed, double* out, char* msg, std::size_t cap) {
+  return guarded(
+      [&] {
+        afmm::GeneratorSpec spec =
+            role == 1 ? afmm::GeneratorSpec::integer_valued(n, density, mu_prime)
+                      : afmm::GeneratorSpec::real_valued(n, density, low, high);
+        const auto m = afmm::generate(spec, afmm::Seed{seed});
+        const auto d = m.data();
+        std::memcpy(out, d.data(), d.size() * sizeof(double));
+      },
+      msg, cap);
+}
+
+// bench.hpp:82-85 and :90-101 (AFMM_A when case_b == 0, AFMM_B otherwise).
+std::uint64_t ref_cell_seed(std::uint64_t base, std::uint64_t n, std::uint64_t rep) {
+  return afmm::cell_seed(afmm::Seed{base}, n, rep);
+}
+
+void ref_make_factor_pair(int case_b, std::uint64_t n, double d1, double d2, double mu_prime,
+                          std::uint64_t seed, double* lhs, double* rhs) {
+  const auto pair = afmm::make_factor_pair(case_b ? afmm::KernelId::AFMM_B : afmm::KernelId::AFMM_A,
+                                           n, d1, d2, mu_prime, seed);
+  std::memcpy(lhs, pair.first.data().data(), n * n * sizeof(double));
+  std::memcpy(rhs, pair.second.data().data(), n * n * sizeof(double));
+}
+
+// test_kernels.cpp:208-217: the 16-bit-magnitude operands (|entries| <= 2^15),
+// drawn from std::mt19937_64(0xB16) exactly as that test does.
+void ref_b16_pair(double* lhs, double* rhs) {
+  std::mt19937_64 rng(0xB16);
+  for (int idx = 0; idx < 64; ++idx) {
+    lhs[idx] = rng() % 3 == 0 ? static_cast<double>(static_cast<int>(rng() % 65536) - 32768) : 0.0;
+  }
+  for (int idx = 0; idx < 64; ++idx) {
+    rhs[idx] = rng() % 3 == 0 ? static_cast<double>(static_cast<int>(rng() % 65536) - 32768) : 0.0;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,29 @@
+"""B200-native AFMM product (arXiv 1308.2400) behind the reference's hot-path API.
+
+The product path is libafmm_b200.so (include/afmm_b200.h): sm_100a CUDA kernels
+with a C ABI. This package is the Python binding of that ABI plus the
+synthetic-input generators and the multi-GPU row partition used by bench.py.
+"""
+from .afmm import (  # noqa: F401
+    FAST,
+    ORDER_PRESERVING,
+    DeviceContext,
+    DeviceError,
+    DomainError,
+    InvalidArgument,
+    MultiplyResult,
+    OpCounts,
+    ShapeError,
+    UnsupportedError,
+    afmm_case_a,
+    afmm_case_b,
+    fp_add_peak,
+    kernel_launch_count,
+    partition_rows,
+)
+
+__all__ = [
+    "afmm_case_a", "afmm_case_b", "MultiplyResult", "OpCounts", "ShapeError", "DomainError",
+    "InvalidArgument", "UnsupportedError", "DeviceError", "DeviceContext", "partition_rows",
+    "fp_add_peak", "kernel_launch_count", "ORDER_PRESERVING", "FAST",
+]

@@ -1,0 +1,263 @@
+"""Python mirror of the reference's AFMM hot-path API, backed by the sm_100a C ABI.
+
+Reference interface (paths relative to /root/reference/proj):
+  afmm::afmm_case_a(const DenseMatrix& lhs, const DenseMatrix& rhs) -> MultiplyResult
+      include/afmm/kernels.hpp:113-136  (real lhs bases, integer rhs reps)
+  afmm::afmm_case_b(...)               include/afmm/kernels.hpp:142-165
+  OpCounts / MultiplyResult            include/afmm/op_counts.hpp:17-33
+  shape_error                          include/afmm/errors.hpp:9-12
+
+Same names, same argument meaning, same error behaviour: a dimension mismatch
+raises ShapeError (a ValueError, as shape_error is a std::invalid_argument),
+a non-integer or out-of-range rep raises DomainError naming the first
+offender in row-major order with the reference's message text, an empty
+matrix raises InvalidArgument ("DenseMatrix: dimension must be >= 1").
+
+Every product is computed by the CUDA kernels in csrc/ through
+libafmm_b200.so; nothing here computes on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional, Tuple
+
+import numpy as np
+
+from . import _lib
+
+ORDER_PRESERVING = "order-preserving"
+FAST = "fast"
+_MODES = {ORDER_PRESERVING: _lib.MODE_ORDER_PRESERVING, FAST: _lib.MODE_FAST}
+
+
+class ShapeError(ValueError):
+    """afmm::shape_error (errors.hpp:9-12): dimension mismatch."""
+
+
+class DomainError(ValueError):
+    """std::domain_error: rep not integer-valued / out of range / non-finite element."""
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument: empty matrix or invalid option."""
+
+
+class UnsupportedError(DomainError):
+    """A rep magnitude at or above 2^31 (device loop-counter limit; the reference
+    would run 2^31+ sequential adds per element)."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA failure or no usable device (there is no CPU fallback)."""
+
+
+@dataclass(frozen=True)
+class OpCounts:
+    """op_counts.hpp:17-23"""
+
+    additions: int = 0
+    multiplications: int = 0
+    zero_skips: int = 0
+
+
+@dataclass
+class MultiplyResult:
+    """op_counts.hpp:30-33"""
+
+    product: np.ndarray
+    counts: OpCounts
+
+
+def _raise_for(status: int, err: _lib.Error) -> None:
+    if status == _lib.OK:
+        return
+    msg = err.message.decode(errors="replace") or _lib.status_string(status)
+    if status == _lib.ERR_SHAPE:
+        raise ShapeError(msg)
+    if status == _lib.ERR_DOMAIN:
+        raise DomainError(msg)
+    if status == _lib.ERR_UNSUPPORTED:
+        raise UnsupportedError(msg)
+    if status == _lib.ERR_INVALID_ARGUMENT:
+        raise InvalidArgument(msg)
+    if status == _lib.ERR_OUT_OF_MEMORY:
+        raise MemoryError(msg)
+    raise DeviceError(msg)
+
+
+def _options(mode: str, device: Optional[int]) -> _lib.Options:
+    if mode not in _MODES:
+        raise InvalidArgument(f"afmm: unknown mode {mode!r}")
+    return _lib.Options(_MODES[mode], -1 if device is None else int(device), 0, 0)
+
+
+def _as_square(m, name: str) -> np.ndarray:
+    a = np.asarray(m)
+    if a.ndim != 2 or a.shape[0] != a.shape[1]:
+        raise ShapeError(f"DenseMatrix: {name} must be square n x n, got shape {a.shape}")
+    return a
+
+
+def _common_dtype(lhs: np.ndarray, rhs: np.ndarray, dtype) -> np.dtype:
+    if dtype is not None:
+        dt = np.dtype(dtype)
+    elif lhs.dtype == np.float32 and rhs.dtype == np.float32:
+        dt = np.dtype(np.float32)
+    else:
+        dt = np.dtype(np.float64)
+    if dt not in (np.dtype(np.float32), np.dtype(np.float64)):
+        raise InvalidArgument(f"afmm: dtype must be float32 or float64, got {dt}")
+    return dt
+
+
+def _product(which: int, lhs, rhs, mode: str, device: Optional[int], dtype,
+             out: Optional[np.ndarray]) -> MultiplyResult:
+    lib = _lib.load()
+    l = _as_square(lhs, "lhs")
+    r = _as_square(rhs, "rhs")
+    dt = _common_dtype(l, r, dtype)
+    l = np.ascontiguousarray(l, dtype=dt)
+    r = np.ascontiguousarray(r, dtype=dt)
+    n = l.shape[0]
+    if out is None:
+        out = np.empty((n, n), dtype=dt)
+    elif out.dtype != dt or out.shape != (n, n) or not out.flags.c_contiguous:
+        raise InvalidArgument("afmm: out must be a C-contiguous n x n array of the operand dtype")
+    counts = _lib.OpCounts()
+    err = _lib.Error()
+    opts = _options(mode, device)
+    fn = {
+        (_lib.CASE_A, np.float64): lib.afmm_case_a_f64,
+        (_lib.CASE_B, np.float64): lib.afmm_case_b_f64,
+        (_lib.CASE_A, np.float32): lib.afmm_case_a_f32,
+        (_lib.CASE_B, np.float32): lib.afmm_case_b_f32,
+    }[(which, dt.type)]
+    status = fn(l.ctypes.data, l.shape[0], r.ctypes.data, r.shape[0], out.ctypes.data,
+                ctypes.byref(opts), ctypes.byref(counts), ctypes.byref(err))
+    _raise_for(status, err)
+    return MultiplyResult(out, OpCounts(*counts.as_tuple()))
+
+
+def afmm_case_a(lhs, rhs, *, mode: str = ORDER_PRESERVING, device: Optional[int] = None,
+                dtype=None, out: Optional[np.ndarray] = None) -> MultiplyResult:
+    """AFMM Case A on the GPU: real lhs bases, integer-valued rhs reps (kernels.hpp:113-136)."""
+    return _product(_lib.CASE_A, lhs, rhs, mode, device, dtype, out)
+
+
+def afmm_case_b(lhs, rhs, *, mode: str = ORDER_PRESERVING, device: Optional[int] = None,
+                dtype=None, out: Optional[np.ndarray] = None) -> MultiplyResult:
+    """AFMM Case B on the GPU: integer-valued lhs reps, real rhs bases (kernels.hpp:142-165)."""
+    return _product(_lib.CASE_B, lhs, rhs, mode, device, dtype, out)
+
+
+# ---- device-resident API ------------------------------------------------------
+
+_DT_CODE = {"float64": _lib.F64, "float32": _lib.F32}
+
+
+def _tensor_info(t) -> Tuple[int, int, str, int]:
+    """(data_ptr, leading dimension, dtype name, n) of a 2D row-major CUDA tensor."""
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise InvalidArgument("afmm: device operands must be 2D with unit column stride")
+    name = str(t.dtype).replace("torch.", "")
+    if name not in _DT_CODE:
+        raise InvalidArgument(f"afmm: unsupported dtype {t.dtype}")
+    return t.data_ptr(), t.stride(0), name, t.shape[1]
+
+
+class DeviceContext:
+    """An afmm_context: device, stream binding and grow-only workspace."""
+
+    def __init__(self, device: int = 0):
+        self._lib = _lib.load()
+        h = ctypes.c_void_p()
+        status = self._lib.afmm_context_create(int(device), ctypes.byref(h))
+        if status != _lib.OK:
+            raise DeviceError(f"afmm_context_create({device}) failed: "
+                              f"{_lib.status_string(status)}")
+        self._h = h
+        self.device = int(device)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._lib.afmm_context_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream) -> None:
+        handle = getattr(stream, "cuda_stream", stream)
+        self._lib.afmm_context_set_stream(self._h, ctypes.c_void_p(int(handle or 0)))
+
+    def product(self, which: str, lhs, rhs, out, row_begin: int = 0,
+                row_end: Optional[int] = None, *, sync: bool = True,
+                mode: str = ORDER_PRESERVING) -> Optional[OpCounts]:
+        """Rows [row_begin, row_end) of Z into `out` (device tensors, row-major)."""
+        lp, ld, dname, n = _tensor_info(lhs)
+        rp, ld_r, dname_r, n_r = _tensor_info(rhs)
+        if dname_r != dname or ld_r != ld or lhs.shape[0] != n or rhs.shape != lhs.shape:
+            raise ShapeError(f"afmm_case_{which}: dimension mismatch {n} vs {n_r}")
+        row_end = n if row_end is None else int(row_end)
+        op, ld_out, dname_o, _ = _tensor_info(out)
+        if dname_o != dname:
+            raise InvalidArgument("afmm: out dtype differs from the operands")
+        counts = _lib.OpCounts()
+        err = _lib.Error()
+        opts = _options(mode, self.device)
+        status = self._lib.afmm_product_device(
+            self._h, _lib.CASE_A if which == "a" else _lib.CASE_B, _DT_CODE[dname], lp, rp, n, ld,
+            op, ld_out, int(row_begin), row_end, ctypes.byref(opts), 1 if sync else 0,
+            ctypes.byref(counts), ctypes.byref(err))
+        _raise_for(status, err)
+        return OpCounts(*counts.as_tuple()) if sync else None
+
+    def finish(self) -> OpCounts:
+        counts = _lib.OpCounts()
+        err = _lib.Error()
+        _raise_for(self._lib.afmm_context_finish(self._h, ctypes.byref(counts), ctypes.byref(err)),
+                   err)
+        return OpCounts(*counts.as_tuple())
+
+    def row_work(self, which: str, lhs, rhs) -> np.ndarray:
+        lp, ld, dname, n = _tensor_info(lhs)
+        rp, _, _, _ = _tensor_info(rhs)
+        work = np.zeros(n, dtype=np.uint64)
+        err = _lib.Error()
+        status = self._lib.afmm_row_work_device(
+            self._h, _lib.CASE_A if which == "a" else _lib.CASE_B, _DT_CODE[dname], lp, rp, n, ld,
+            work.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), ctypes.byref(err))
+        _raise_for(status, err)
+        return work
+
+
+def partition_rows(work, parts: int) -> np.ndarray:
+    """Contiguous row ranges of near-equal total work (afmm_partition_rows)."""
+    lib = _lib.load()
+    w = np.ascontiguousarray(work, dtype=np.uint64)
+    cuts = np.zeros(int(parts) + 1, dtype=np.uint64)
+    status = lib.afmm_partition_rows(w.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), w.size,
+                                     int(parts), cuts.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)))
+    if status != _lib.OK:
+        raise InvalidArgument("afmm_partition_rows: invalid arguments")
+    return cuts.astype(np.int64)
+
+
+def fp_add_peak(device: int = 0, dtype: str = "float32") -> Tuple[float, float]:
+    """Measured CUDA-core FP-add peak (adds/s) and the SM clock it ran at (MHz)."""
+    lib = _lib.load()
+    rate = ctypes.c_double()
+    mhz = ctypes.c_double()
+    status = lib.afmm_fp_add_peak(int(device), _DT_CODE[dtype], ctypes.byref(rate),
+                                  ctypes.byref(mhz))
+    if status != _lib.OK:
+        raise DeviceError("afmm_fp_add_peak failed")
+    return rate.value, mhz.value
+
+
+def kernel_launch_count() -> int:
+    return int(_lib.load().afmm_kernel_launch_count())

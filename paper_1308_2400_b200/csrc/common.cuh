@@ -1,0 +1,101 @@
+// common.cuh -- shared device helpers for the AFMM sm_100a kernels:
+// mbarrier + TMA (cp.async.bulk.tensor) inline PTX, rep conversion, status.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace afmm_dev {
+
+// Device-side status of one product call: first offenders (row-major linear
+// index, ~0 = none) and the exact counts, all written by the prepass.
+struct DevStatus {
+  unsigned long long nonfinite_lhs;  // linear index of first non-finite lhs element
+  unsigned long long nonfinite_rhs;
+  unsigned long long rep_bad;        // (linear index << 2) | kind of first bad rep
+  unsigned long long rep_too_large;  // linear index of first |rep| >= 2^31
+  unsigned long long additions;
+  unsigned long long zero_skips;
+  unsigned long long pad[2];
+};
+
+__device__ __forceinline__ bool status_failed(const DevStatus* st) {
+  return (st->nonfinite_lhs & st->nonfinite_rhs & st->rep_bad & st->rep_too_large) != ~0ull;
+}
+
+// kernels.hpp:31-40 on the widened value: 0 ok, 1 not integer-valued,
+// 2 exceeds the exact integer range. round() is std::round (half away from
+// zero). NaN passes both tests exactly as in the reference; non-finite
+// elements are rejected separately (the DenseMatrix ctor, matrix.hpp:31-35).
+__device__ __forceinline__ int rep_kind(double v) {
+  if (fabs(v - round(v)) > 1e-9) return 1;
+  if (fabs(v) > 9007199254740992.0) return 2;
+  return 0;
+}
+
+// ---- mbarrier --------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b64 st;\n\t"
+      "mbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "{\n\t.reg .b64 st;\n\t"
+      "mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(bytes)
+      : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// ---- TMA -------------------------------------------------------------------
+
+// 2D tiled tensor load global -> shared, completion via mbarrier tx bytes.
+// c0 = innermost (column) coordinate, c1 = row coordinate, in elements.
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map,
+                                            uint64_t* bar, int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+}  // namespace afmm_dev

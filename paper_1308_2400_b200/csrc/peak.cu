@@ -1,0 +1,117 @@
+// peak.cu -- CUDA-core FP-add peak microbenchmark (the roofline denominator).
+//
+// AFMM never uses tensor cores (they would reintroduce multiplications), so
+// the bound for the repeated-addition kernel is the SM's FP add issue rate.
+// This kernel measures it with the same instruction mix as the product's
+// inner loop (bform.cu): per lane 4 independent float2 chains of FADD2 for
+// fp32, 4 independent DADD chains for fp64, each adding a register-held step,
+// unrolled, on 4 CTAs x 256 threads per SM. clock64() deltas give the SM
+// clock the measurement ran at.
+#include "kernels.h"
+
+namespace afmm_dev {
+
+namespace {
+
+constexpr int kIters = 8192;
+constexpr int kUnroll = 16;
+
+__global__ void k_peak_f32(const float* __restrict__ s, float* out, unsigned long long* cycles) {
+  float2 acc[4], st[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    acc[c] = make_float2(0.f, 0.f);
+    st[c] = make_float2(s[(threadIdx.x + 2 * c) & 63], s[(threadIdx.x + 2 * c + 1) & 63]);
+  }
+  const long long t0 = clock64();
+  for (int it = 0; it < kIters; ++it) {
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[c] = __fadd2_rn(acc[c], st[c]);
+  }
+  const long long t1 = clock64();
+  float r = 0.f;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) r += acc[c].x + acc[c].y;
+  if (r == 1234.5f) out[0] = r;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *cycles = (unsigned long long)(t1 - t0);
+}
+
+__global__ void k_peak_f64(const double* __restrict__ s, double* out,
+                           unsigned long long* cycles) {
+  double acc[4], st[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    acc[c] = 0.0;
+    st[c] = s[(threadIdx.x + c) & 63];
+  }
+  const long long t0 = clock64();
+  for (int it = 0; it < kIters / 2; ++it) {
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[c] = __dadd_rn(acc[c], st[c]);
+  }
+  const long long t1 = clock64();
+  double r = 0.0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) r += acc[c];
+  if (r == 1234.5) out[0] = r;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *cycles = (unsigned long long)(t1 - t0);
+}
+
+}  // namespace
+
+cudaError_t run_peak(int dtype, double* adds_per_second, double* sm_mhz) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  void* buf = nullptr;
+  unsigned long long* cyc = nullptr;
+  cudaError_t e = cudaMalloc(&buf, 64 * sizeof(double) + 64);
+  if (e != cudaSuccess) return e;
+  e = cudaMalloc(&cyc, sizeof(unsigned long long));
+  if (e != cudaSuccess) { cudaFree(buf); return e; }
+  double host[64];
+  for (int i = 0; i < 64; ++i) host[i] = 1e-12 * (i + 1);
+  float hostf[64];
+  for (int i = 0; i < 64; ++i) hostf[i] = 1e-7f * (i + 1);
+  if (dtype == 0) cudaMemcpy(buf, host, sizeof host, cudaMemcpyHostToDevice);
+  else cudaMemcpy(buf, hostf, sizeof hostf, cudaMemcpyHostToDevice);
+  const int blocks = sms * 4, threads = 256;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  auto launch = [&]() {
+    if (dtype == 0)
+      k_peak_f64<<<blocks, threads>>>((const double*)buf, (double*)buf + 64, cyc);
+    else
+      k_peak_f32<<<blocks, threads>>>((const float*)buf, (float*)buf + 64, cyc);
+    note_launch();
+  };
+  for (int w = 0; w < 2; ++w) launch();
+  const int reps = 5;
+  cudaEventRecord(a);
+  for (int r = 0; r < reps; ++r) launch();
+  cudaEventRecord(b);
+  e = cudaEventSynchronize(b);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  unsigned long long cycles = 0;
+  cudaMemcpy(&cycles, cyc, sizeof cycles, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  const double adds_per_thread =
+      dtype == 0 ? (double)(kIters / 2) * kUnroll * 4 : (double)kIters * kUnroll * 8;
+  const double total = adds_per_thread * blocks * threads * reps;
+  if (adds_per_second) *adds_per_second = total / (ms * 1e-3);
+  // one launch's kernel body took `cycles` SM clocks; the launch took ms/reps
+  if (sm_mhz) *sm_mhz = (double)cycles / ((ms / reps) * 1e-3) / 1e6;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(buf);
+  cudaFree(cyc);
+  return e;
+}
+
+}  // namespace afmm_dev

@@ -1,0 +1,306 @@
+// prepass.cu -- O(n^2) device prepass of the AFMM product (sm_100a).
+//
+// Replaces the inline zero tests and the up-front validation of the
+// reference kernels (/root/reference/proj/include/afmm/kernels.hpp:25-43,
+// :121-130, :150-159) with data-parallel passes:
+//   k_scan_operand   finite check (matrix.hpp:31-35) and rep validation
+//                    (kernels.hpp:25-43), first offender by atomicMin on the
+//                    row-major linear index
+//   k_row_nnz        nnz(B[k,:]) of the Case-B base operand rows
+//   k_row_repsum     R_k = sum_j |llround Y[k,j]| of the Case-A rep operand rows
+//   k_compact_reps   warp ballot/popc stream compaction of every rep row into
+//                    an ordered (k, rep) list: the zero-skip of kernels.hpp:128-130
+//                    and :151-153 done once instead of per (i,k,j)
+//   k_row_work       exact per-row additions W_i and zero_skips (closed forms of
+//                    kernels.hpp:119-134 / :148-163), the partition weights
+//   k_sum_counts     OpCounts of a row slab
+//   k_transpose      32x32 smem-tiled transpose (Case A runs as Case B on
+//                    transposed operands)
+// All of these are HBM-bound streaming passes: one coalesced read of each
+// operand, no reuse, so no smem staging except in the transpose.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace afmm_dev {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long w = __shfl_xor_sync(FULL, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+template <class T>
+__global__ void k_scan_operand(const T* __restrict__ m, uint64_t ld, uint32_t n, int is_rep,
+                               unsigned long long* nonfinite, unsigned long long* rep_bad,
+                               unsigned long long* too_large) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = warp; i < n; i += nwarps) {
+    const T* row = m + i * ld;
+    for (uint32_t j0 = 0; j0 < n; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      unsigned long long nf = ~0ull, rb = ~0ull, tl = ~0ull;
+      if (j < n) {
+        const double v = (double)row[j];
+        const uint64_t lin = i * (uint64_t)n + j;
+        if (!isfinite(v)) nf = lin;
+        if (is_rep) {
+          const int kind = rep_kind(v);
+          if (kind) rb = (lin << 2) | (unsigned long long)kind;
+          else if (fabs(v) >= 2147483647.5) tl = lin;
+        }
+      }
+      const bool bad = (nf & rb & tl) != ~0ull;
+      if (__any_sync(FULL, bad)) {
+        nf = warp_min_u64(nf);
+        rb = warp_min_u64(rb);
+        tl = warp_min_u64(tl);
+        if (lane == 0) {
+          if (nf != ~0ull) atomicMin(nonfinite, nf);
+          if (rb != ~0ull) atomicMin(rep_bad, rb);
+          if (tl != ~0ull) atomicMin(too_large, tl);
+        }
+      }
+    }
+  }
+}
+
+// nnz of each row of the base operand (Case B: nnz(Y[k,:]), test_kernels.cpp:168).
+template <class T>
+__global__ void k_row_nnz(const T* __restrict__ m, uint64_t ld, uint32_t n,
+                          uint32_t* __restrict__ nnz) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t k = warp; k < n; k += nwarps) {
+    const T* row = m + k * ld;
+    uint32_t c = 0;
+    for (uint32_t j = lane; j < n; j += 32) c += row[j] != T(0) ? 1u : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+    if (lane == 0) nnz[k] = c;
+  }
+}
+
+// R_k = sum_j |llround Y[k,j]| over the Case-A rep operand rows
+// (test_kernels.cpp:51-53).
+template <class T>
+__global__ void k_row_repsum(const T* __restrict__ m, uint64_t ld, uint32_t n,
+                             unsigned long long* __restrict__ rsum) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t k = warp; k < n; k += nwarps) {
+    const T* row = m + k * ld;
+    unsigned long long s = 0;
+    for (uint32_t j = lane; j < n; j += 32) {
+      const T v = row[j];
+      if (v != T(0)) {
+        const long long r = llround((double)v);
+        s += (unsigned long long)(r < 0 ? -r : r);
+      }
+    }
+    s = warp_sum_u64(s);
+    if (lane == 0) rsum[k] = s;
+  }
+}
+
+// One warp per rep row: ordered (k, rep) list of the nonzero reps. A rep is
+// skipped exactly when the reference skips it: value == 0.0 or llround == 0
+// (kernels.hpp:128-130, :151-153).
+template <class T>
+__global__ void k_compact_reps(const T* __restrict__ m, uint64_t ld, uint32_t rows, uint32_t n,
+                               int2* __restrict__ lists, uint64_t cap,
+                               uint32_t* __restrict__ counts) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  for (uint64_t r = warp; r < rows; r += nwarps) {
+    const T* row = m + r * ld;
+    int2* out = lists + r * cap;
+    uint32_t base = 0;
+    for (uint32_t k0 = 0; k0 < n; k0 += 32) {
+      const uint32_t k = k0 + lane;
+      int rep = 0;
+      if (k < n) {
+        const T v = row[k];
+        if (v != T(0)) rep = (int)llround((double)v);
+      }
+      const unsigned mask = __ballot_sync(FULL, rep != 0);
+      if (rep != 0) out[base + __popc(mask & lt)] = make_int2((int)k, rep);
+      base += __popc(mask);
+    }
+    if (lane == 0) counts[r] = base;
+  }
+}
+
+// Exact per-row additions and zero_skips of Z row i.
+// Case A: W_i = sum_{k: X[i,k] != 0} R_k,           zs_i = #{k: X[i,k] == 0}
+// Case B: W_i = sum_k |rep_ik| * nnzB_k,            zs_i = sum_{k: rep_ik != 0} (n - nnzB_k)
+template <class T>
+__global__ void k_row_work(const T* __restrict__ x, uint64_t ld, uint32_t n, int which_case,
+                           const uint32_t* __restrict__ nnz_b,
+                           const unsigned long long* __restrict__ rsum,
+                           unsigned long long* __restrict__ work,
+                           unsigned long long* __restrict__ zs) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = warp; i < n; i += nwarps) {
+    const T* row = x + i * ld;
+    unsigned long long w = 0, z = 0;
+    for (uint32_t k = lane; k < n; k += 32) {
+      const T v = row[k];
+      if (which_case == 0) {
+        if (v == T(0)) ++z;
+        else w += rsum[k];
+      } else if (v != T(0)) {
+        const long long r = llround((double)v);
+        if (r != 0) {
+          const unsigned long long nb = nnz_b[k];
+          w += (unsigned long long)(r < 0 ? -r : r) * nb;  // count bookkeeping, not an element product
+          z += (unsigned long long)n - nb;
+        }
+      }
+    }
+    w = warp_sum_u64(w);
+    z = warp_sum_u64(z);
+    if (lane == 0) {
+      work[i] = w;
+      if (zs) zs[i] = z;
+    }
+  }
+}
+
+__global__ void k_sum_counts(const unsigned long long* __restrict__ work,
+                             const unsigned long long* __restrict__ zs, uint32_t r0, uint32_t r1,
+                             DevStatus* st) {
+  unsigned long long w = 0, z = 0;
+  for (uint32_t i = r0 + blockIdx.x * blockDim.x + threadIdx.x; i < r1;
+       i += gridDim.x * blockDim.x) {
+    w += work[i];
+    z += zs[i];
+  }
+  w = warp_sum_u64(w);
+  z = warp_sum_u64(z);
+  if ((threadIdx.x & 31) == 0) {
+    if (w) atomicAdd(&st->additions, w);
+    if (z) atomicAdd(&st->zero_skips, z);
+  }
+}
+
+// out[c * ld_out + r] = in[r * ld_in + c] for r < rows, c < cols.
+template <class T>
+__global__ void k_transpose(const T* __restrict__ in, uint64_t ld_in, uint32_t rows,
+                            uint32_t cols, T* __restrict__ out, uint64_t ld_out) {
+  __shared__ T tile[32][33];
+  const uint32_t c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (uint32_t dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const uint32_t r = r0 + dy, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[dy][threadIdx.x] = in[(uint64_t)r * ld_in + c];
+  }
+  __syncthreads();
+  for (uint32_t dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const uint32_t c = c0 + dy, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[(uint64_t)c * ld_out + r] = tile[threadIdx.x][dy];
+  }
+}
+
+inline unsigned grid_for_rows(uint64_t rows, int warps_per_block) {
+  uint64_t blocks = (rows + warps_per_block - 1) / warps_per_block;
+  if (blocks > 148ull * 32) blocks = 148ull * 32;
+  if (blocks < 1) blocks = 1;
+  return (unsigned)blocks;
+}
+
+}  // namespace
+
+// ---- launchers ---------------------------------------------------------------
+
+template <class T>
+void launch_scan_operand(const T* m, uint64_t ld, uint32_t n, int is_rep,
+                         unsigned long long* nonfinite, unsigned long long* rep_bad,
+                         unsigned long long* too_large, cudaStream_t s) {
+  k_scan_operand<T><<<grid_for_rows(n, 8), 256, 0, s>>>(m, ld, n, is_rep, nonfinite, rep_bad,
+                                                         too_large);
+  note_launch();
+}
+
+template <class T>
+void launch_row_nnz(const T* m, uint64_t ld, uint32_t n, uint32_t* nnz, cudaStream_t s) {
+  k_row_nnz<T><<<grid_for_rows(n, 8), 256, 0, s>>>(m, ld, n, nnz);
+  note_launch();
+}
+
+template <class T>
+void launch_row_repsum(const T* m, uint64_t ld, uint32_t n, unsigned long long* rsum,
+                       cudaStream_t s) {
+  k_row_repsum<T><<<grid_for_rows(n, 8), 256, 0, s>>>(m, ld, n, rsum);
+  note_launch();
+}
+
+template <class T>
+void launch_compact_reps(const T* m, uint64_t ld, uint32_t rows, uint32_t n, int2* lists,
+                         uint64_t cap, uint32_t* counts, cudaStream_t s) {
+  k_compact_reps<T><<<grid_for_rows(rows, 8), 256, 0, s>>>(m, ld, rows, n, lists, cap, counts);
+  note_launch();
+}
+
+template <class T>
+void launch_row_work(const T* x, uint64_t ld, uint32_t n, int which_case, const uint32_t* nnz_b,
+                     const unsigned long long* rsum, unsigned long long* work,
+                     unsigned long long* zs, cudaStream_t s) {
+  k_row_work<T><<<grid_for_rows(n, 8), 256, 0, s>>>(x, ld, n, which_case, nnz_b, rsum, work, zs);
+  note_launch();
+}
+
+void launch_sum_counts(const unsigned long long* work, const unsigned long long* zs, uint32_t r0,
+                       uint32_t r1, DevStatus* st, cudaStream_t s) {
+  uint64_t blocks = ((uint64_t)(r1 - r0) + 255) / 256;
+  if (blocks > 296) blocks = 296;
+  if (blocks < 1) blocks = 1;
+  k_sum_counts<<<(unsigned)blocks, 256, 0, s>>>(work, zs, r0, r1, st);
+  note_launch();
+}
+
+template <class T>
+void launch_transpose(const T* in, uint64_t ld_in, uint32_t rows, uint32_t cols, T* out,
+                      uint64_t ld_out, cudaStream_t s) {
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32);
+  k_transpose<T><<<grid, dim3(32, 8), 0, s>>>(in, ld_in, rows, cols, out, ld_out);
+  note_launch();
+}
+
+#define INSTANTIATE(T)                                                                         \
+  template void launch_scan_operand<T>(const T*, uint64_t, uint32_t, int, unsigned long long*, \
+                                       unsigned long long*, unsigned long long*, cudaStream_t); \
+  template void launch_row_nnz<T>(const T*, uint64_t, uint32_t, uint32_t*, cudaStream_t);      \
+  template void launch_row_repsum<T>(const T*, uint64_t, uint32_t, unsigned long long*,       \
+                                     cudaStream_t);                                            \
+  template void launch_compact_reps<T>(const T*, uint64_t, uint32_t, uint32_t, int2*,          \
+                                       uint64_t, uint32_t*, cudaStream_t);                     \
+  template void launch_row_work<T>(const T*, uint64_t, uint32_t, int, const uint32_t*,         \
+                                   const unsigned long long*, unsigned long long*,             \
+                                   unsigned long long*, cudaStream_t);                         \
+  template void launch_transpose<T>(const T*, uint64_t, uint32_t, uint32_t, T*, uint64_t,      \
+                                    cudaStream_t);
+
+INSTANTIATE(float)
+INSTANTIATE(double)
+
+}  // namespace afmm_dev

@@ -1,0 +1,665 @@
+// runtime.cu -- host runtime behind the C ABI (include/afmm_b200.h).
+//
+// Owns contexts (device + stream + grow-only workspace), builds the TMA
+// tensor maps, sequences prepass -> repeated-addition kernel -> epilogue on
+// one stream, and maps device-side validation results to the reference's
+// error contract (kernels.hpp:15-43, matrix.hpp:25-36, 54-57). No compute
+// happens on the host and there is no CPU fallback.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cinttypes>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+
+#include "../../include/afmm_b200.h"
+#include "kernels.h"
+
+using afmm_dev::DevStatus;
+
+namespace afmm_dev {
+static std::atomic<uint64_t> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace afmm_dev
+
+namespace {
+
+constexpr uint64_t kNone = ~0ull;
+
+inline uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  // grow-only; contents are not preserved
+  cudaError_t ensure(size_t want) {
+    if (want <= bytes) return cudaSuccess;
+    if (p) {
+      cudaFree(p);  // implicit device sync
+      p = nullptr;
+      bytes = 0;
+    }
+    want = std::max<size_t>(want, 256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      return e;
+    }
+    bytes = want;
+    return cudaSuccess;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class U>
+  U* as() const {
+    return static_cast<U*>(p);
+  }
+};
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+template <class T>
+bool make_tmap(CUtensorMap* map, const T* base, uint64_t rows, uint64_t cols, uint64_t ld) {
+  auto fn = get_encode_fn();
+  if (!fn) return false;
+  const cuuint64_t gdim[2] = {cols, rows};
+  const cuuint64_t gstride[1] = {ld * sizeof(T)};
+  const cuuint32_t box[2] = {(cuuint32_t)afmm_dev::bform_tile_n<T>(),
+                             (cuuint32_t)afmm_dev::bform_kb<T>()};
+  const cuuint32_t estride[2] = {1, 1};
+  const CUtensorMapDataType dt =
+      sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  CUresult r = fn(map, dt, 2, const_cast<T*>(base), gdim, gstride, box, estride,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+struct afmm_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  // workspace
+  DevBuf status, vec_k, work, zs, lists, counts, base_copy, yt, xt, zt;
+  // host-buffer API staging
+  DevBuf hx, hy, hz;
+  DevStatus* status_host = nullptr;  // pinned
+  // state of the last enqueued product, for error decoding
+  int last_case = 0, last_dtype = 0;
+  const void* last_lhs = nullptr;
+  const void* last_rhs = nullptr;
+  uint64_t last_n = 0, last_ld = 0;
+  bool pending = false;
+  afmm_status pending_status = AFMM_OK;
+};
+
+namespace {
+
+void set_error(afmm_error* err, int kind, int operand, uint64_t row, uint64_t col, double value,
+               const char* msg) {
+  if (!err) return;
+  err->kind = kind;
+  err->operand = operand;
+  err->row = row;
+  err->col = col;
+  err->value = value;
+  std::snprintf(err->message, sizeof err->message, "%s", msg);
+}
+
+void clear_error(afmm_error* err) {
+  if (!err) return;
+  std::memset(err, 0, sizeof *err);
+}
+
+afmm_status cuda_fail(afmm_error* err, cudaError_t e, const char* what) {
+  char buf[256];
+  std::snprintf(buf, sizeof buf, "%s: CUDA error %s (%s)", what, cudaGetErrorName(e),
+                cudaGetErrorString(e));
+  set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, buf);
+  if (e == cudaErrorMemoryAllocation) return AFMM_ERR_OUT_OF_MEMORY;
+  return AFMM_ERR_CUDA;
+}
+
+const char* case_name(int which) { return which == AFMM_CASE_A ? "afmm_case_a" : "afmm_case_b"; }
+
+// kernels.hpp:15-21 and matrix.hpp:54-57
+afmm_status check_dims(int which, uint64_t n_lhs, uint64_t n_rhs, afmm_error* err) {
+  if (n_lhs != n_rhs) {
+    char buf[256];
+    std::snprintf(buf, sizeof buf, "%s: dimension mismatch %" PRIu64 " vs %" PRIu64,
+                  case_name(which), n_lhs, n_rhs);
+    set_error(err, AFMM_ERRKIND_SHAPE, 0, 0, 0, 0.0, buf);
+    return AFMM_ERR_SHAPE;
+  }
+  if (n_lhs == 0) {
+    set_error(err, AFMM_ERRKIND_EMPTY, 0, 0, 0, 0.0, "DenseMatrix: dimension must be >= 1");
+    return AFMM_ERR_INVALID_ARGUMENT;
+  }
+  if (n_lhs > (1ull << 31) - 1) {
+    set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: n exceeds the device index range");
+    return AFMM_ERR_UNSUPPORTED;
+  }
+  return AFMM_OK;
+}
+
+// Read one element back (only on the error path).
+double read_element(const void* base, int dtype, uint64_t ld, uint64_t row, uint64_t col) {
+  if (dtype == AFMM_F64) {
+    double v = 0.0;
+    cudaMemcpy(&v, static_cast<const double*>(base) + row * ld + col, sizeof v,
+               cudaMemcpyDeviceToHost);
+    return v;
+  }
+  float v = 0.f;
+  cudaMemcpy(&v, static_cast<const float*>(base) + row * ld + col, sizeof v,
+             cudaMemcpyDeviceToHost);
+  return (double)v;
+}
+
+// Translate the device status of the last product into status / counts / error.
+afmm_status decode_status(afmm_context* c, afmm_op_counts* counts, afmm_error* err) {
+  const DevStatus& s = *c->status_host;
+  const uint64_t n = c->last_n;
+  const int rep_operand = c->last_case == AFMM_CASE_A ? 1 : 0;  // rhs for A, lhs for B
+  const char* where = case_name(c->last_case);
+  const char* opname = rep_operand ? "rhs" : "lhs";
+  char buf[256];
+  if (s.nonfinite_lhs != kNone || s.nonfinite_rhs != kNone) {
+    const int operand = s.nonfinite_lhs != kNone ? 0 : 1;
+    const uint64_t lin = operand == 0 ? s.nonfinite_lhs : s.nonfinite_rhs;
+    const double v = read_element(operand == 0 ? c->last_lhs : c->last_rhs, c->last_dtype,
+                                  c->last_ld, lin / n, lin % n);
+    set_error(err, AFMM_ERRKIND_NON_FINITE, operand, lin / n, lin % n, v,
+              "DenseMatrix: non-finite element");
+    return AFMM_ERR_DOMAIN;
+  }
+  if (s.rep_bad != kNone) {
+    const uint64_t lin = s.rep_bad >> 2;
+    const int kind = (int)(s.rep_bad & 3);
+    const uint64_t i = lin / n, j = lin % n;
+    const double v = read_element(rep_operand ? c->last_rhs : c->last_lhs, c->last_dtype,
+                                  c->last_ld, i, j);
+    if (kind == 1) {
+      // std::to_string(double) is "%f" (kernels.hpp:32-34)
+      std::snprintf(buf, sizeof buf, "%s: %s[%" PRIu64 "][%" PRIu64 "] = %f is not integer-valued",
+                    where, opname, i, j, v);
+      set_error(err, AFMM_ERRKIND_NOT_INTEGER, rep_operand, i, j, v, buf);
+    } else {
+      std::snprintf(buf, sizeof buf,
+                    "%s: %s[%" PRIu64 "][%" PRIu64 "] exceeds the exact integer range", where,
+                    opname, i, j);
+      set_error(err, AFMM_ERRKIND_OUT_OF_RANGE, rep_operand, i, j, v, buf);
+    }
+    return AFMM_ERR_DOMAIN;
+  }
+  if (s.rep_too_large != kNone) {
+    const uint64_t lin = s.rep_too_large;
+    const uint64_t i = lin / n, j = lin % n;
+    const double v = read_element(rep_operand ? c->last_rhs : c->last_lhs, c->last_dtype,
+                                  c->last_ld, i, j);
+    std::snprintf(buf, sizeof buf,
+                  "%s: %s[%" PRIu64 "][%" PRIu64 "] = %f exceeds the device repeat-count limit "
+                  "(2^31 - 1)",
+                  where, opname, i, j, v);
+    set_error(err, AFMM_ERRKIND_REP_TOO_LARGE, rep_operand, i, j, v, buf);
+    return AFMM_ERR_UNSUPPORTED;
+  }
+  if (counts) {
+    counts->additions = s.additions;
+    counts->multiplications = 0;
+    counts->zero_skips = s.zero_skips;
+  }
+  clear_error(err);
+  return AFMM_OK;
+}
+
+#define CK(expr, what)                              \
+  do {                                              \
+    cudaError_t _e = (expr);                        \
+    if (_e != cudaSuccess) return cuda_fail(err, _e, what); \
+  } while (0)
+
+// Enqueue the whole device pipeline for Z rows [r0, r1). Pointers are device
+// memory with leading dimension ld (lhs, rhs) and ld_out (out).
+template <class T>
+afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* rhs, uint64_t n,
+                            uint64_t ld, T* out, uint64_t ld_out, uint64_t r0, uint64_t r1,
+                            afmm_error* err) {
+  cudaStream_t s = c->stream;
+  const uint64_t rows = r1 - r0;
+  const uint32_t n32 = (uint32_t)n;
+  CK(c->status.ensure(sizeof(DevStatus)), "workspace");
+  CK(c->vec_k.ensure(n * 8), "workspace");
+  CK(c->work.ensure(n * 8), "workspace");
+  CK(c->zs.ensure(n * 8), "workspace");
+  DevStatus* st = c->status.as<DevStatus>();
+  CK(cudaMemsetAsync(st, 0xff, 4 * sizeof(unsigned long long), s), "memset");
+  CK(cudaMemsetAsync(&st->additions, 0, 4 * sizeof(unsigned long long), s), "memset");
+
+  // validation (kernels.hpp:115 / :144) + DenseMatrix finite check (matrix.hpp:31-35)
+  afmm_dev::launch_scan_operand<T>(lhs, ld, n32, which == AFMM_CASE_B, &st->nonfinite_lhs,
+                                   &st->rep_bad, &st->rep_too_large, s);
+  afmm_dev::launch_scan_operand<T>(rhs, ld, n32, which == AFMM_CASE_A, &st->nonfinite_rhs,
+                                   &st->rep_bad, &st->rep_too_large, s);
+
+  auto* work = c->work.as<unsigned long long>();
+  auto* zs = c->zs.as<unsigned long long>();
+  CUtensorMap tmap;
+  if (which == AFMM_CASE_B) {
+    // rep = X[i,k] (lhs), bases = Y[k,:] (rhs): B-form directly.
+    auto* nnz = c->vec_k.as<uint32_t>();
+    afmm_dev::launch_row_nnz<T>(rhs, ld, n32, nnz, s);
+    afmm_dev::launch_row_work<T>(lhs, ld, n32, 1, nnz, nullptr, work, zs, s);
+    CK(c->lists.ensure(std::max<uint64_t>(rows, 1) * n * sizeof(int2)), "workspace");
+    CK(c->counts.ensure(std::max<uint64_t>(rows, 1) * 4), "workspace");
+    if (rows > 0)
+      afmm_dev::launch_compact_reps<T>(lhs + r0 * ld, ld, (uint32_t)rows, n32,
+                                       c->lists.as<int2>(), n, c->counts.as<uint32_t>(), s);
+    const T* base = rhs;
+    uint64_t ldb = ld;
+    if ((ld * sizeof(T)) % 16 != 0 || reinterpret_cast<uintptr_t>(rhs) % 16 != 0) {
+      ldb = round_up(n, 32);
+      CK(c->base_copy.ensure(n * ldb * sizeof(T)), "workspace");
+      CK(cudaMemcpy2DAsync(c->base_copy.p, ldb * sizeof(T), rhs, ld * sizeof(T), n * sizeof(T), n,
+                           cudaMemcpyDeviceToDevice, s),
+         "copy");
+      base = c->base_copy.as<T>();
+    }
+    if (rows > 0) {
+      if (!make_tmap<T>(&tmap, base, n, n, ldb)) {
+        set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: cuTensorMapEncodeTiled failed");
+        return AFMM_ERR_CUDA;
+      }
+      CK(afmm_dev::launch_bform<T>(&tmap, c->lists.as<int2>(), n, c->counts.as<uint32_t>(),
+                                   (uint32_t)rows, 0, (int32_t)n, n32, out, ld_out, st, s),
+         "bform");
+    }
+  } else {
+    // Case A as Case B on transposed operands: Z^T = (Y^T) (x) (X^T).
+    // B-form rows = Z columns j (rep list = column j of Y), B-form columns =
+    // Z rows of the slab (bases X[i,k], i in [r0, r1)).
+    auto* rsum = c->vec_k.as<unsigned long long>();
+    afmm_dev::launch_row_repsum<T>(rhs, ld, n32, rsum, s);
+    afmm_dev::launch_row_work<T>(lhs, ld, n32, 0, nullptr, rsum, work, zs, s);
+    const uint64_t ldt = round_up(n, 32);
+    const uint64_t lds = round_up(std::max<uint64_t>(rows, 1), 32);
+    CK(c->yt.ensure(n * ldt * sizeof(T)), "workspace");
+    CK(c->xt.ensure(n * lds * sizeof(T)), "workspace");
+    CK(c->zt.ensure(n * lds * sizeof(T)), "workspace");
+    CK(c->lists.ensure(n * n * sizeof(int2)), "workspace");
+    CK(c->counts.ensure(n * 4), "workspace");
+    afmm_dev::launch_transpose<T>(rhs, ld, n32, n32, c->yt.as<T>(), ldt, s);
+    afmm_dev::launch_compact_reps<T>(c->yt.as<T>(), ldt, n32, n32, c->lists.as<int2>(), n,
+                                     c->counts.as<uint32_t>(), s);
+    if (rows > 0) {
+      afmm_dev::launch_transpose<T>(lhs + r0 * ld, ld, (uint32_t)rows, n32, c->xt.as<T>(), lds,
+                                    s);
+      if (!make_tmap<T>(&tmap, c->xt.as<T>(), n, rows, lds)) {
+        set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: cuTensorMapEncodeTiled failed");
+        return AFMM_ERR_CUDA;
+      }
+      CK(afmm_dev::launch_bform<T>(&tmap, c->lists.as<int2>(), n, c->counts.as<uint32_t>(), n32,
+                                   0, (int32_t)rows, n32, c->zt.as<T>(), lds, st, s),
+         "bform");
+      afmm_dev::launch_transpose<T>(c->zt.as<T>(), lds, n32, (uint32_t)rows, out, ld_out, s);
+    }
+  }
+  if (rows > 0) afmm_dev::launch_sum_counts(work, zs, (uint32_t)r0, (uint32_t)r1, st, s);
+  CK(cudaGetLastError(), "launch");
+  CK(cudaMemcpyAsync(c->status_host, st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s),
+     "status readback");
+  c->last_case = which;
+  c->last_dtype = sizeof(T) == 8 ? AFMM_F64 : AFMM_F32;
+  c->last_lhs = lhs;
+  c->last_rhs = rhs;
+  c->last_n = n;
+  c->last_ld = ld;
+  c->pending = true;
+  return AFMM_OK;
+}
+
+afmm_status finish_locked(afmm_context* c, afmm_op_counts* counts, afmm_error* err) {
+  if (!c->pending) {
+    clear_error(err);
+    return AFMM_OK;
+  }
+  c->pending = false;
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return cuda_fail(err, e, "afmm: device execution");
+  return decode_status(c, counts, err);
+}
+
+std::mutex g_default_mu;
+afmm_context* g_default[64] = {};
+
+afmm_status default_context(int device, afmm_context** out, afmm_error* err) {
+  if (device < 0) {
+    cudaError_t e = cudaGetDevice(&device);
+    if (e != cudaSuccess) return cuda_fail(err, e, "afmm: no CUDA device");
+  }
+  if (device >= 64) {
+    set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: device ordinal out of range");
+    return AFMM_ERR_INVALID_ARGUMENT;
+  }
+  std::lock_guard<std::mutex> g(g_default_mu);
+  if (!g_default[device]) {
+    afmm_context* c = nullptr;
+    afmm_status s = afmm_context_create(device, &c);
+    if (s != AFMM_OK) {
+      set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: cannot create a CUDA context");
+      return s;
+    }
+    g_default[device] = c;
+  }
+  *out = g_default[device];
+  return AFMM_OK;
+}
+
+// The reference-facing call: host buffers in, host buffer out.
+template <class T>
+afmm_status host_product(int which, const T* lhs, uint64_t n_lhs, const T* rhs, uint64_t n_rhs,
+                         T* out, const afmm_options* opt, afmm_op_counts* counts,
+                         afmm_error* err) {
+  clear_error(err);
+  afmm_status st = check_dims(which, n_lhs, n_rhs, err);
+  if (st != AFMM_OK) return st;
+  if (!lhs || !rhs || !out) {
+    set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: null pointer argument");
+    return AFMM_ERR_INVALID_ARGUMENT;
+  }
+  afmm_context* c = nullptr;
+  st = default_context(opt ? opt->device : -1, &c, err);
+  if (st != AFMM_OK) return st;
+  std::lock_guard<std::mutex> g(c->mu);
+  CK(cudaSetDevice(c->device), "afmm: cudaSetDevice");
+  const uint64_t n = n_lhs, ld = round_up(n, 32);
+  const size_t mat = n * ld * sizeof(T);
+  CK(c->hx.ensure(mat), "afmm: device allocation");
+  CK(c->hy.ensure(mat), "afmm: device allocation");
+  CK(c->hz.ensure(mat), "afmm: device allocation");
+  cudaStream_t s = c->stream;
+  CK(cudaMemcpy2DAsync(c->hx.p, ld * sizeof(T), lhs, n * sizeof(T), n * sizeof(T), n,
+                       cudaMemcpyHostToDevice, s),
+     "afmm: H2D");
+  CK(cudaMemcpy2DAsync(c->hy.p, ld * sizeof(T), rhs, n * sizeof(T), n * sizeof(T), n,
+                       cudaMemcpyHostToDevice, s),
+     "afmm: H2D");
+  st = enqueue_product<T>(c, which, c->hx.as<T>(), c->hy.as<T>(), n, ld, c->hz.as<T>(), ld, 0, n,
+                          err);
+  if (st != AFMM_OK) return st;
+  st = finish_locked(c, counts, err);
+  if (st != AFMM_OK) return st;
+  CK(cudaMemcpy2DAsync(out, n * sizeof(T), c->hz.p, ld * sizeof(T), n * sizeof(T), n,
+                       cudaMemcpyDeviceToHost, s),
+     "afmm: D2H");
+  CK(cudaStreamSynchronize(s), "afmm: D2H");
+  return AFMM_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+
+extern "C" {
+
+afmm_status afmm_case_a_f64(const double* lhs, uint64_t n_lhs, const double* rhs, uint64_t n_rhs,
+                            double* out, const afmm_options* options, afmm_op_counts* counts,
+                            afmm_error* error) {
+  try {
+    return host_product<double>(AFMM_CASE_A, lhs, n_lhs, rhs, n_rhs, out, options, counts, error);
+  } catch (const std::bad_alloc&) {
+    return AFMM_ERR_OUT_OF_MEMORY;
+  } catch (...) {
+    return AFMM_ERR_CUDA;
+  }
+}
+
+afmm_status afmm_case_b_f64(const double* lhs, uint64_t n_lhs, const double* rhs, uint64_t n_rhs,
+                            double* out, const afmm_options* options, afmm_op_counts* counts,
+                            afmm_error* error) {
+  try {
+    return host_product<double>(AFMM_CASE_B, lhs, n_lhs, rhs, n_rhs, out, options, counts, error);
+  } catch (const std::bad_alloc&) {
+    return AFMM_ERR_OUT_OF_MEMORY;
+  } catch (...) {
+    return AFMM_ERR_CUDA;
+  }
+}
+
+afmm_status afmm_case_a_f32(const float* lhs, uint64_t n_lhs, const float* rhs, uint64_t n_rhs,
+                            float* out, const afmm_options* options, afmm_op_counts* counts,
+                            afmm_error* error) {
+  try {
+    return host_product<float>(AFMM_CASE_A, lhs, n_lhs, rhs, n_rhs, out, options, counts, error);
+  } catch (const std::bad_alloc&) {
+    return AFMM_ERR_OUT_OF_MEMORY;
+  } catch (...) {
+    return AFMM_ERR_CUDA;
+  }
+}
+
+afmm_status afmm_case_b_f32(const float* lhs, uint64_t n_lhs, const float* rhs, uint64_t n_rhs,
+                            float* out, const afmm_options* options, afmm_op_counts* counts,
+                            afmm_error* error) {
+  try {
+    return host_product<float>(AFMM_CASE_B, lhs, n_lhs, rhs, n_rhs, out, options, counts, error);
+  } catch (const std::bad_alloc&) {
+    return AFMM_ERR_OUT_OF_MEMORY;
+  } catch (...) {
+    return AFMM_ERR_CUDA;
+  }
+}
+
+afmm_status afmm_context_create(int32_t device, afmm_context** ctx) {
+  if (!ctx) return AFMM_ERR_INVALID_ARGUMENT;
+  *ctx = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return AFMM_ERR_CUDA;
+  if (device < 0 && cudaGetDevice(&device) != cudaSuccess) return AFMM_ERR_CUDA;
+  if (device >= count) return AFMM_ERR_INVALID_ARGUMENT;
+  auto* c = new (std::nothrow) afmm_context;
+  if (!c) return AFMM_ERR_OUT_OF_MEMORY;
+  c->device = device;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaHostAlloc(reinterpret_cast<void**>(&c->status_host), sizeof(DevStatus),
+                    cudaHostAllocDefault) != cudaSuccess) {
+    delete c;
+    cudaSetDevice(prev);
+    return AFMM_ERR_CUDA;
+  }
+  cudaSetDevice(prev);
+  *ctx = c;
+  return AFMM_OK;
+}
+
+void afmm_context_destroy(afmm_context* c) {
+  if (!c) return;
+  {
+    std::lock_guard<std::mutex> g(c->mu);
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (DevBuf* b : {&c->status, &c->vec_k, &c->work, &c->zs, &c->lists, &c->counts,
+                      &c->base_copy, &c->yt, &c->xt, &c->zt, &c->hx, &c->hy, &c->hz})
+      b->release();
+    if (c->status_host) cudaFreeHost(c->status_host);
+  }
+  delete c;
+}
+
+afmm_status afmm_context_set_stream(afmm_context* c, void* stream) {
+  if (!c) return AFMM_ERR_INVALID_ARGUMENT;
+  std::lock_guard<std::mutex> g(c->mu);
+  c->stream = static_cast<cudaStream_t>(stream);
+  return AFMM_OK;
+}
+
+afmm_status afmm_product_device(afmm_context* c, int32_t which_case, int32_t dtype,
+                                const void* lhs, const void* rhs, uint64_t n, uint64_t ld,
+                                void* out, uint64_t ld_out, uint64_t row_begin, uint64_t row_end,
+                                const afmm_options* options, int32_t sync,
+                                afmm_op_counts* counts, afmm_error* err) {
+  (void)options;
+  clear_error(err);
+  if (!c || (which_case != AFMM_CASE_A && which_case != AFMM_CASE_B) ||
+      (dtype != AFMM_F64 && dtype != AFMM_F32)) {
+    set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: invalid context/case/dtype");
+    return AFMM_ERR_INVALID_ARGUMENT;
+  }
+  afmm_status st = check_dims(which_case, n, n, err);
+  if (st != AFMM_OK) return st;
+  if (ld < n || ld_out < n || row_begin > row_end || row_end > n || !lhs || !rhs ||
+      (!out && row_end > row_begin)) {
+    set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: invalid leading dimension / rows");
+    return AFMM_ERR_INVALID_ARGUMENT;
+  }
+  try {
+    std::lock_guard<std::mutex> g(c->mu);
+    CK(cudaSetDevice(c->device), "afmm: cudaSetDevice");
+    if (c->pending) {
+      st = finish_locked(c, nullptr, nullptr);  // drain an unfinished async call
+      (void)st;
+    }
+    if (dtype == AFMM_F64)
+      st = enqueue_product<double>(c, which_case, static_cast<const double*>(lhs),
+                                   static_cast<const double*>(rhs), n, ld,
+                                   static_cast<double*>(out), ld_out, row_begin, row_end, err);
+    else
+      st = enqueue_product<float>(c, which_case, static_cast<const float*>(lhs),
+                                  static_cast<const float*>(rhs), n, ld, static_cast<float*>(out),
+                                  ld_out, row_begin, row_end, err);
+    if (st != AFMM_OK) return st;
+    if (sync) return finish_locked(c, counts, err);
+    return AFMM_OK;
+  } catch (const std::bad_alloc&) {
+    return AFMM_ERR_OUT_OF_MEMORY;
+  }
+}
+
+afmm_status afmm_context_finish(afmm_context* c, afmm_op_counts* counts, afmm_error* err) {
+  if (!c) return AFMM_ERR_INVALID_ARGUMENT;
+  std::lock_guard<std::mutex> g(c->mu);
+  CK(cudaSetDevice(c->device), "afmm: cudaSetDevice");
+  return finish_locked(c, counts, err);
+}
+
+afmm_status afmm_row_work_device(afmm_context* c, int32_t which_case, int32_t dtype,
+                                 const void* lhs, const void* rhs, uint64_t n, uint64_t ld,
+                                 uint64_t* work_host, afmm_error* err) {
+  clear_error(err);
+  if (!c || !work_host || (dtype != AFMM_F64 && dtype != AFMM_F32)) return AFMM_ERR_INVALID_ARGUMENT;
+  afmm_status st = check_dims(which_case, n, n, err);
+  if (st != AFMM_OK) return st;
+  std::lock_guard<std::mutex> g(c->mu);
+  CK(cudaSetDevice(c->device), "afmm: cudaSetDevice");
+  CK(c->vec_k.ensure(n * 8), "workspace");
+  CK(c->work.ensure(n * 8), "workspace");
+  cudaStream_t s = c->stream;
+  auto* work = c->work.as<unsigned long long>();
+  if (dtype == AFMM_F64) {
+    auto* l = static_cast<const double*>(lhs);
+    auto* r = static_cast<const double*>(rhs);
+    if (which_case == AFMM_CASE_B) {
+      afmm_dev::launch_row_nnz<double>(r, ld, (uint32_t)n, c->vec_k.as<uint32_t>(), s);
+      afmm_dev::launch_row_work<double>(l, ld, (uint32_t)n, 1, c->vec_k.as<uint32_t>(), nullptr,
+                                        work, nullptr, s);
+    } else {
+      afmm_dev::launch_row_repsum<double>(r, ld, (uint32_t)n, c->vec_k.as<unsigned long long>(), s);
+      afmm_dev::launch_row_work<double>(l, ld, (uint32_t)n, 0, nullptr,
+                                        c->vec_k.as<unsigned long long>(), work, nullptr, s);
+    }
+  } else {
+    auto* l = static_cast<const float*>(lhs);
+    auto* r = static_cast<const float*>(rhs);
+    if (which_case == AFMM_CASE_B) {
+      afmm_dev::launch_row_nnz<float>(r, ld, (uint32_t)n, c->vec_k.as<uint32_t>(), s);
+      afmm_dev::launch_row_work<float>(l, ld, (uint32_t)n, 1, c->vec_k.as<uint32_t>(), nullptr,
+                                       work, nullptr, s);
+    } else {
+      afmm_dev::launch_row_repsum<float>(r, ld, (uint32_t)n, c->vec_k.as<unsigned long long>(), s);
+      afmm_dev::launch_row_work<float>(l, ld, (uint32_t)n, 0, nullptr,
+                                       c->vec_k.as<unsigned long long>(), work, nullptr, s);
+    }
+  }
+  CK(cudaMemcpyAsync(work_host, work, n * 8, cudaMemcpyDeviceToHost, s), "work readback");
+  CK(cudaStreamSynchronize(s), "work readback");
+  return AFMM_OK;
+}
+
+afmm_status afmm_partition_rows(const uint64_t* work, uint64_t n, uint32_t parts, uint64_t* cuts) {
+  if (!work || !cuts || parts == 0) return AFMM_ERR_INVALID_ARGUMENT;
+  // Prefix sums in 128-bit-safe form: total may exceed 2^64 only for absurd
+  // reps; saturate.
+  unsigned __int128 total = 0;
+  for (uint64_t i = 0; i < n; ++i) total += work[i];
+  cuts[0] = 0;
+  unsigned __int128 acc = 0;
+  uint64_t i = 0;
+  for (uint32_t p = 1; p < parts; ++p) {
+    // smallest row index whose prefix reaches p/parts of the total, rounding
+    // to the nearer boundary
+    const unsigned __int128 target = total * p / parts;
+    while (i < n && acc + work[i] <= target) acc += work[i++];
+    if (i < n && acc < target) {
+      const unsigned __int128 over = acc + work[i] - target, under = target - acc;
+      if (over < under) acc += work[i++];
+    }
+    cuts[p] = std::max<uint64_t>(i, cuts[p - 1]);
+  }
+  cuts[parts] = n;
+  return AFMM_OK;
+}
+
+afmm_status afmm_fp_add_peak(int32_t device, int32_t dtype, double* adds_per_second,
+                             double* sm_clock_mhz) {
+  int prev = 0;
+  if (cudaGetDevice(&prev) != cudaSuccess) return AFMM_ERR_CUDA;
+  if (device >= 0 && cudaSetDevice(device) != cudaSuccess) return AFMM_ERR_CUDA;
+  cudaError_t e = afmm_dev::run_peak(dtype, adds_per_second, sm_clock_mhz);
+  cudaSetDevice(prev);
+  return e == cudaSuccess ? AFMM_OK : AFMM_ERR_CUDA;
+}
+
+uint64_t afmm_kernel_launch_count(void) {
+  return afmm_dev::g_launches.load(std::memory_order_relaxed);
+}
+
+const char* afmm_status_string(afmm_status s) {
+  switch (s) {
+    case AFMM_OK: return "ok";
+    case AFMM_ERR_SHAPE: return "shape_error";
+    case AFMM_ERR_DOMAIN: return "domain_error";
+    case AFMM_ERR_INVALID_ARGUMENT: return "invalid_argument";
+    case AFMM_ERR_CUDA: return "cuda_error";
+    case AFMM_ERR_UNSUPPORTED: return "unsupported";
+    case AFMM_ERR_OUT_OF_MEMORY: return "out_of_memory";
+  }
+  return "unknown";
+}
+
+int32_t afmm_abi_version(void) { return AFMM_B200_ABI_VERSION; }
+
+}  // extern "C"

@@ -1,0 +1,136 @@
+"""The C-ABI library without a GPU: it loads, exports every symbol include/afmm_b200.h
+declares, and its host-side logic (dimension checks, row partition) behaves as the
+reference's contract says. No compute call is made here."""
+import ctypes
+import os
+import re
+import shutil
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "afmm_b200.h")
+
+
+def _declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:[\w\s\*]+?)\b(afmm_\w+)\s*\(", text, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1308_2400_b200 import _lib
+
+    lib = _lib.load()
+    declared = _declared_symbols()
+    assert len(declared) >= 15
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert set(declared) == set(_lib.EXPORTED_SYMBOLS)
+    assert lib.afmm_abi_version() == 1
+
+
+def test_library_is_sm100a_only():
+    """The product .so carries sm_100a SASS (no PTX JIT, no other arch)."""
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(cuobjdump):
+        pytest.skip("cuobjdump not available")
+    from paper_1308_2400_b200 import _lib
+
+    out = subprocess.run([cuobjdump, "--list-elf", _lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run([cuobjdump, "-sass", _lib.LIB_PATH], capture_output=True,
+                          text=True).stdout
+    for mnemonic in ("UTMALDG", "FADD2", "DADD", "SYNCS.PHASECHK"):
+        assert mnemonic in sass, mnemonic
+    assert "HMMA" not in sass and "UTCHMMA" not in sass  # no tensor cores: no multiplications
+
+
+def test_status_strings():
+    from paper_1308_2400_b200 import _lib
+
+    assert _lib.status_string(_lib.OK) == "ok"
+    assert _lib.status_string(_lib.ERR_SHAPE) == "shape_error"
+    assert _lib.status_string(_lib.ERR_DOMAIN) == "domain_error"
+
+
+def test_dimension_mismatch_is_shape_error_before_any_device_work():
+    import paper_1308_2400_b200 as afmm
+
+    with pytest.raises(afmm.ShapeError) as ei:
+        afmm.afmm_case_a(np.zeros((2, 2)), np.zeros((3, 3)))
+    assert str(ei.value) == "afmm_case_a: dimension mismatch 2 vs 3"
+    with pytest.raises(afmm.ShapeError) as ei:
+        afmm.afmm_case_b(np.zeros((2, 2)), np.zeros((3, 3)))
+    assert str(ei.value) == "afmm_case_b: dimension mismatch 2 vs 3"
+    assert issubclass(afmm.ShapeError, ValueError)  # shape_error : std::invalid_argument
+
+
+def test_empty_matrix_is_invalid_argument():
+    import paper_1308_2400_b200 as afmm
+
+    with pytest.raises(afmm.InvalidArgument) as ei:
+        afmm.afmm_case_b(np.zeros((0, 0)), np.zeros((0, 0)))
+    assert str(ei.value) == "DenseMatrix: dimension must be >= 1"
+
+
+def test_no_cpu_fallback_without_a_device():
+    """Without a CUDA device the product must fail loudly, never compute on the host."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    import paper_1308_2400_b200 as afmm
+
+    with pytest.raises(afmm.DeviceError):
+        afmm.afmm_case_a(np.eye(2), np.eye(2))
+
+
+@pytest.mark.parametrize("parts", [1, 2, 3, 4, 8])
+def test_partition_rows_balanced_and_monotone(parts):
+    from paper_1308_2400_b200 import partition_rows
+
+    rng = np.random.default_rng(parts)
+    for n in (1, 5, 64, 1000):
+        w = rng.integers(0, 10_000, n).astype(np.uint64)
+        w[rng.random(n) < 0.2] = 0
+        cuts = partition_rows(w, parts)
+        assert cuts[0] == 0 and cuts[-1] == n and len(cuts) == parts + 1
+        assert np.all(np.diff(cuts) >= 0)
+        total = int(w.sum())
+        for p in range(parts):
+            s = int(w[cuts[p]:cuts[p + 1]].sum())
+            # each part is within one row's work of its fair share
+            assert abs(s - total / parts) <= int(w.max()) + 1, (n, parts, p)
+
+
+def test_partition_rows_skewed_beta_rows():
+    """cfg4-like skew: Beta(0.5,0.5) row densities; cuts follow work, not row count."""
+    from paper_1308_2400_b200 import partition_rows
+
+    rng = np.random.default_rng(0)
+    w = (rng.beta(0.5, 0.5, 8192) * 1e6).astype(np.uint64)
+    cuts = partition_rows(w, 8)
+    shares = [int(w[cuts[p]:cuts[p + 1]].sum()) for p in range(8)]
+    assert max(shares) / min(shares) < 1.005  # one row of work is ~0.2% of a share
+
+
+def test_cpp_wrapper_header_compiles():
+    """include/afmm_b200/kernels.hpp against the reference's own headers (drop-in check)."""
+    ref_inc = "/root/reference/proj/include"
+    if not os.path.isdir(ref_inc):
+        pytest.skip("reference headers not present")
+    src = (
+        '#include "afmm_b200/kernels.hpp"\n'
+        "int main() {\n"
+        "  afmm::DenseMatrix x(2), y(2);\n"
+        "  auto (*fa)(const afmm::DenseMatrix&, const afmm::DenseMatrix&, afmm::gpu::Options)"
+        " -> afmm::MultiplyResult = &afmm::gpu::afmm_case_a;\n"
+        "  (void)fa; (void)x; (void)y;\n"
+        "  return afmm::gpu::parse_kernel(\"afmm-a-gpu\").has_value() ? 0 : 1;\n}\n")
+    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-x", "c++", "-I", ref_inc, "-I",
+                        os.path.join(ROOT, "include"), "-"], input=src, capture_output=True,
+                       text=True)
+    assert r.returncode == 0, r.stderr

@@ -1,0 +1,197 @@
+"""Parity of the sm_100a product (through the C ABI) with the reference.
+
+Order-preserving mode must be bit-identical to the reference / its oracle:
+  * every golden fixture and seeded case produced by the unmodified reference
+    (tests/golden/), fp64, including error types and message text;
+  * the fp32 path against the fp32 restatement of the oracle;
+  * BASELINE.json's five input distributions at reduced n against the oracle,
+    and at full size through row samples + closed-form counts.
+"""
+import numpy as np
+import pytest
+
+from golden_util import load_arrays, load_index, seeded_inputs, sha
+
+pytestmark = pytest.mark.gpu
+
+INDEX = load_index()
+ARRAYS = load_arrays()
+
+
+def _api():
+    import paper_1308_2400_b200 as afmm
+
+    return afmm
+
+
+def _call(case, lhs, rhs, **kw):
+    afmm = _api()
+    fn = afmm.afmm_case_a if case == "a" else afmm.afmm_case_b
+    return fn(lhs, rhs, **kw)
+
+
+def _bits_equal(a, b):
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
+@pytest.mark.parametrize("fx", INDEX["fixtures"], ids=[f["name"] for f in INDEX["fixtures"]])
+def test_golden_fixture(cuda, fx):
+    afmm = _api()
+    lhs = ARRAYS[fx["name"] + "/lhs"]
+    rhs = ARRAYS[fx["name"] + "/rhs"]
+    if "error" in fx:
+        exc = {"shape_error": afmm.ShapeError, "domain_error": afmm.DomainError,
+               "invalid_argument": afmm.InvalidArgument}[fx["error"]["type"]]
+        with pytest.raises(exc) as ei:
+            _call(fx["case"], lhs, rhs)
+        assert str(ei.value) == fx["error"]["message"]
+        return
+    res = _call(fx["case"], lhs, rhs)
+    assert (res.counts.additions, res.counts.multiplications, res.counts.zero_skips) == \
+        tuple(fx["counts"])
+    assert _bits_equal(res.product, ARRAYS[fx["name"] + "/z"])
+
+
+def test_golden_seeded(cuda, oracle):
+    for entry in INDEX["seeded"]:
+        lhs, rhs = seeded_inputs(oracle, entry)
+        res = _call(entry["case"], lhs, rhs)
+        c = res.counts
+        assert (c.additions, c.multiplications, c.zero_skips) == tuple(entry["counts"]), \
+            entry["name"]
+        assert sha(res.product) == entry["z_sha"], entry["name"]
+
+
+def test_f32_path_matches_f32_oracle(cuda, oracle):
+    rng = np.random.default_rng(21)
+    for n in (1, 2, 7, 33, 100, 257, 300):
+        bases = rng.uniform(-3, 3, (n, n)).astype(np.float32)
+        bases[rng.random((n, n)) < 0.3] = 0
+        reps = rng.integers(-25, 26, (n, n)).astype(np.float32)
+        reps[rng.random((n, n)) < 0.2] = 0
+        for case, lhs, rhs in (("a", bases, reps), ("b", reps, bases)):
+            z, c, _ = oracle.product(case, lhs, rhs)
+            res = _call(case, lhs, rhs)
+            assert res.product.dtype == np.float32
+            assert (res.counts.additions, 0, res.counts.zero_skips) == c
+            assert _bits_equal(res.product, z), (case, n)
+
+
+def test_empty_matrix_is_invalid_argument(cuda):
+    afmm = _api()
+    with pytest.raises(afmm.InvalidArgument, match="DenseMatrix: dimension must be >= 1"):
+        afmm.afmm_case_a(np.zeros((0, 0)), np.zeros((0, 0)))
+
+
+def test_non_finite_is_domain_error(cuda):
+    afmm = _api()
+    x = np.eye(3)
+    y = np.eye(3)
+    y[1, 2] = np.inf
+    with pytest.raises(afmm.DomainError, match="non-finite"):
+        afmm.afmm_case_b(x, y)
+
+
+def test_rep_too_large_is_reported(cuda):
+    afmm = _api()
+    y = np.eye(2)
+    y[0, 1] = 2.0 ** 31
+    with pytest.raises(afmm.UnsupportedError, match=r"rhs\[0\]\[1\]"):
+        afmm.afmm_case_a(np.eye(2), y)
+
+
+@pytest.mark.parametrize("name,n,kw", [
+    ("cfg1", 256, {}),
+    ("cfg2", 1024, {}),
+    ("cfg3", 384, {"d1": 0.1, "mu": 1}),
+    ("cfg3", 384, {"d1": 0.5, "mu": 4}),
+    ("cfg3", 384, {"d1": 1.0, "mu": 16}),
+    ("cfg4", 512, {}),
+    ("cfg5", 512, {}),
+])
+def test_baseline_distributions_bit_exact(cuda, oracle, name, n, kw):
+    """BASELINE configs' distributions at oracle-friendly n: bit-exact + exact counts."""
+    from paper_1308_2400_b200.gen import CONFIGS, make_inputs
+
+    lhs, rhs = make_inputs(name, seed=3, n=n, **kw)
+    case = CONFIGS[name].case
+    z, c, _ = oracle.product(case, lhs, rhs)
+    res = _call(case, lhs, rhs)
+    assert (res.counts.additions, 0, res.counts.zero_skips) == c
+    assert _bits_equal(res.product, z)
+
+
+def test_device_api_row_slabs_and_padded_ld(cuda, oracle):
+    """Device-resident entry: row slabs [r0, r1) and a non-multiple-of-4 leading dimension."""
+    import torch
+
+    afmm = _api()
+    ctx = afmm.DeviceContext(0)
+    rng = np.random.default_rng(4)
+    for dt, tdt in ((np.float64, torch.float64), (np.float32, torch.float32)):
+        n = 301
+        bases = rng.uniform(-2, 2, (n, n)).astype(dt)
+        bases[rng.random((n, n)) < 0.4] = 0
+        reps = rng.integers(-6, 7, (n, n)).astype(dt)
+        for case, lhs, rhs in (("a", bases, reps), ("b", reps, bases)):
+            zfull, _, _ = oracle.product(case, lhs, rhs)
+            for ld in (n, n + 3, 320):
+                L = torch.zeros((n, ld), dtype=tdt, device="cuda")
+                R = torch.zeros((n, ld), dtype=tdt, device="cuda")
+                L[:, :n] = torch.from_numpy(lhs)
+                R[:, :n] = torch.from_numpy(rhs)
+                for r0, r1 in ((0, n), (17, 140), (300, 301), (5, 5)):
+                    O = torch.full((max(r1 - r0, 1), ld), 7.0, dtype=tdt, device="cuda")
+                    counts = ctx.product(case, L[:, :n], R[:, :n], O[:, :n], r0, r1)
+                    _, c, _ = oracle.product(case, lhs, rhs, r0, r1)
+                    assert (counts.additions, 0, counts.zero_skips) == c
+                    if r1 > r0:
+                        assert _bits_equal(O[: r1 - r0, :n].cpu().numpy(), zfull[r0:r1])
+    ctx.close()
+
+
+def test_row_work_and_partition(cuda):
+    import torch
+
+    from paper_1308_2400_b200.gen import expected_additions, make_inputs
+
+    afmm = _api()
+    ctx = afmm.DeviceContext(0)
+    lhs, rhs = make_inputs("cfg4", seed=1, n=1024)
+    L = torch.from_numpy(lhs).cuda()
+    R = torch.from_numpy(rhs).cuda()
+    work = ctx.row_work("a", L, R)
+    assert int(work.sum()) == expected_additions("a", lhs, rhs)
+    cuts = afmm.partition_rows(work, 8)
+    assert cuts[0] == 0 and cuts[-1] == 1024 and np.all(np.diff(cuts) >= 0)
+    per = [int(work[cuts[p]:cuts[p + 1]].sum()) for p in range(8)]
+    assert max(per) - min(per) <= 2 * int(work.max())
+    ctx.close()
+
+
+@pytest.mark.parametrize("name,kw", [("cfg5", {}), ("cfg4", {}), ("cfg3", {"d1": 1.0, "mu": 16})])
+def test_full_size_row_sample_bit_exact(cuda, oracle, name, kw):
+    """Full BASELINE size on the GPU; a row sample checked bit-exact against the
+    multithreaded oracle and the total additions against the closed form."""
+    import torch
+
+    from paper_1308_2400_b200.gen import CONFIGS, expected_additions, make_inputs
+
+    afmm = _api()
+    cfg = CONFIGS[name]
+    lhs, rhs = make_inputs(name, seed=0, **kw)
+    n = cfg.n
+    ctx = afmm.DeviceContext(0)
+    L = torch.from_numpy(lhs).cuda()
+    R = torch.from_numpy(rhs).cuda()
+    O = torch.empty_like(L)
+    counts = ctx.product(cfg.case, L, R, O)
+    assert counts.additions == expected_additions(cfg.case, lhs, rhs)
+    z = O.cpu().numpy()
+    rows = [0, 1, n // 3, n // 2 + 7, n - 1]
+    for r in rows:
+        zr, _ = oracle.product_mt(cfg.case, lhs, rhs, r, r + 1, 1)
+        assert _bits_equal(z[r:r + 1], zr), (name, r)
+    ctx.close()
