@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""bench.py -- effective additions/sec of the B200 AFMM product (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5] [--impl b200|reference]
+
+A step is one AFMM product over the workload's synthetic operands (BASELINE.json
+config; default cfg5 = Case-B n=16384 fp32, ~4.3e13 additions, the config the
+metric's 1/2/4/8-GPU scaling is specified on). Under torchrun each rank owns one
+GPU; the rows are partitioned by work and Z is gathered to rank 0 over NCCL
+inside the step.
+
+  value  adds/s with operands resident in HBM (CUDA events, max over ranks)
+  e2e    the same metric through the reference-facing C-ABI call with pinned HOST
+         buffers (H2D of X and Y + product + D2H of Z inside the timed region)
+  roofline  the repeated-addition kernel's effective adds/s (per-launch CUDA events
+         around k_bform on its stream) against the MEASURED CUDA-core FP-add peak
+         (afmm_fp_add_peak microbenchmark, same process, same GPU)
+  cpu_baseline  the oracle port (bit-identical to the reference, tests/test_oracle.py)
+         on the host cores over a stated row sample
+
+--impl reference times the reference's CPU algorithm (the oracle port, all host
+threads) on a bounded row sample of the same workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "effective additions/sec (sum |rep| over nonzero bases)"
+UNIT = "adds/s"
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--config", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    p.add_argument("--d1", type=float, default=1.0, help="cfg3 sweep point")
+    p.add_argument("--mu", type=int, default=16, help="cfg3 sweep point")
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0,
+                   help="target CPU time of one baseline sample")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (NVML)
+# ---------------------------------------------------------------------------
+
+_REASONS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+    0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+    0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+}
+
+
+class ClockSampler(threading.Thread):
+    def __init__(self, device: int, period: float = 0.1):
+        super().__init__(daemon=True)
+        self.device = device
+        self.period = period
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._halt = threading.Event()
+        self.ok = False
+
+    def run(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+            while not self._halt.is_set():
+                self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                try:
+                    mask = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except Exception:
+                    mask = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                for bit, name in _REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+                time.sleep(self.period)
+        except Exception as e:  # NVML missing: report, do not fail the bench
+            self.error = repr(e)
+
+    def stop(self):
+        self._halt.set()
+        self.join(timeout=2)
+        return {
+            "sm_mhz": statistics.median(self.samples) if self.samples else None,
+            "sm_max_mhz": self.max_mhz,
+            "reasons": sorted(self.reasons),
+            "samples": len(self.samples),
+        }
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port on a row sample
+# ---------------------------------------------------------------------------
+
+def cpu_sample_rate(case, lhs, rhs, threads, target_s, blocks_hint=None):
+    """Time the multithreaded oracle port on row blocks spread over the matrix.
+
+    Returns (adds/s, description, total_adds, seconds)."""
+    from oracle.oracle import Oracle
+
+    oracle = Oracle()
+    n = lhs.shape[0]
+    # calibrate with one block of `threads` rows in the middle
+    r0 = n // 2
+    t0 = time.perf_counter()
+    _, c = oracle.product_mt(case, lhs, rhs, r0, min(n, r0 + threads), threads)
+    dt = time.perf_counter() - t0
+    blocks = blocks_hint or max(1, min(64, int(target_s / max(dt, 1e-3))))
+    starts = np.linspace(0, max(n - threads, 0), blocks).astype(int)
+    adds = 0
+    t0 = time.perf_counter()
+    for s in starts:
+        _, c = oracle.product_mt(case, lhs, rhs, int(s), min(n, int(s) + threads), threads)
+        adds += c[0]
+    secs = time.perf_counter() - t0
+    rows = blocks * min(threads, n)
+    desc = (f"{rows} of {n} rows ({blocks} blocks of {min(threads, n)} consecutive rows spread "
+            f"evenly), {adds:.4e} additions, {secs:.1f} s")
+    return adds / secs, desc, adds, secs, blocks
+
+
+def run_reference_arm(args, rank):
+    """--impl reference: the reference's CPU algorithm (oracle port, bit-identical to the
+    unmodified reference per tests/test_oracle.py), all host threads, rank 0 only."""
+    if rank != 0:
+        return
+    from paper_1308_2400_b200.gen import CONFIGS, make_inputs
+
+    cfg = CONFIGS[args.config]
+    lhs, rhs = make_inputs(args.config, seed=args.seed, d1=args.d1, mu=args.mu)
+    threads = os.cpu_count() or 1
+    # size one step to ~target seconds
+    _, _, _, _, blocks = cpu_sample_rate(cfg.case, lhs, rhs, threads, args.cpu_seconds * 0.4)
+    for _ in range(max(0, min(args.warmup, 1))):
+        cpu_sample_rate(cfg.case, lhs, rhs, threads, 0, blocks_hint=1)
+    adds = 0
+    secs = 0.0
+    desc = ""
+    for _ in range(args.steps):
+        _, desc, a, s, _ = cpu_sample_rate(cfg.case, lhs, rhs, threads, 0, blocks_hint=blocks)
+        adds += a
+        secs += s
+    value = adds / secs
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64 (reference is fp64-only; fp32 configs run the fp32 restatement)"
+        if cfg.dtype == "float32" else "f64",
+        "data": "synthetic (seeded numpy, BASELINE.json distributions)",
+        "config": _config_dict(args, cfg),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": "per step: " + desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _config_dict(args, cfg):
+    d = {"workload": f"{cfg.name}: {cfg.description}", "case": cfg.case, "n": cfg.n,
+         "mode": "order-preserving (bit-exact)", "parallelism": f"row-partition x{args.gpus}",
+         "l2": "operands larger than L2" if cfg.n >= 4096 else "L2 flushed between steps"}
+    if cfg.name == "cfg3":
+        d["d1"] = args.d1
+        d["mu"] = args.mu
+    return d
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1308_2400_b200 as afmm
+    from paper_1308_2400_b200.distributed import ShardedProduct, gather_rows
+    from paper_1308_2400_b200.gen import CONFIGS, make_inputs
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.barrier()
+    cfg = CONFIGS[args.config]
+    tdt = torch.float32 if cfg.dtype == "float32" else torch.float64
+    es = 4 if cfg.dtype == "float32" else 8
+
+    lhs, rhs = make_inputs(args.config, seed=args.seed, d1=args.d1, mu=args.mu)
+    n = cfg.n
+    dev = torch.device("cuda", local)
+    L = torch.from_numpy(lhs).to(dev)
+    R = torch.from_numpy(rhs).to(dev)
+    Z = torch.empty((n, n), dtype=tdt, device=dev)  # rank 0: full result; others: slab scratch
+    ctx = afmm.DeviceContext(local)
+    ctx.enable_timing(True)
+    sharded = ShardedProduct(ctx, dist if world > 1 else None, rank, world)
+    peak, peak_mhz = afmm.fp_add_peak(local, cfg.dtype)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev) if n < 4096 else None
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step():
+        return sharded.run(cfg.case, L, R, Z, Z)
+
+    for _ in range(args.warmup):
+        counts = step()
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed loop ----
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    sampler.start()
+    launches0 = afmm.kernel_launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    total_ms = 0.0
+    kernel_ms = []
+    rank_adds = 0
+    for _ in range(args.steps):
+        if flush is not None:
+            flush.fill_(1.0)  # evict the operands from L2 between steps (untimed)
+            torch.cuda.synchronize()
+        e0.record()
+        counts = step()
+        e1.record()
+        torch.cuda.synchronize()
+        total_ms += e0.elapsed_time(e1)
+        kernel_ms.append(ctx.last_timing()[1])
+        rank_adds = counts.additions
+    torch.cuda.synchronize()
+    barrier()
+    launches = afmm.kernel_launch_count() - launches0
+    clocks = sampler.stop()
+
+    t = torch.tensor([total_ms, float(rank_adds)], dtype=torch.float64, device=dev)
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        total_ms = float(tmax[0])
+        job_adds = int(tsum[1])
+    else:
+        job_adds = rank_adds
+    ms_per_step = total_ms / args.steps
+    value = job_adds / (ms_per_step * 1e-3)
+
+    # ---- roofline of the repeated-addition kernel (this rank's launch) ----
+    kms = statistics.median(kernel_ms)
+    achieved = rank_adds / (kms * 1e-3)
+    traffic = _ncu_traffic(args.config)
+    roofline = {
+        "bound": "fp-add (CUDA-core FADD2/DADD issue; no tensor cores, no HBM bound)",
+        "kernel": "k_bform",
+        "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tadd/s",
+        "frac": achieved / peak,
+        "peak_source": f"measured in-process by afmm_fp_add_peak ({'FADD2' if es == 4 else 'DADD'}"
+                       f" chains) at {peak_mhz:.0f} MHz",
+        "algorithmic_units_per_launch": rank_adds,
+        "kernel_ms": kms,
+        "step_share": kms / ms_per_step if world == 1 else None,
+        "traffic": traffic,
+    }
+
+    # ---- end to end through the reference-facing API ----
+    e2e = None
+    if not args.no_e2e:
+        e2e = _e2e(args, afmm, dist, torch, world, rank, local, cfg, lhs, rhs, es, job_adds,
+                   sharded, L, R, Z)
+
+    # ---- CPU baseline ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        rate, desc, _, _, _ = cpu_sample_rate(cfg.case, lhs, rhs, threads, args.cpu_seconds)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": desc + "; oracle/afmm_oracle.c restatement (bit-identical to the "
+                                "unmodified reference, tests/test_oracle.py), -O2 "
+                                "-ffp-contract=off, pthreads over rows"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32" if es == 4 else "f64",
+            "data": "synthetic (seeded numpy PCG64, BASELINE.json distributions; no dataset)",
+            "config": _config_dict(args, cfg),
+            "frac_of_fp_add_peak": value / (peak * world),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _e2e(args, afmm, dist, torch, world, rank, local, cfg, lhs, rhs, es, job_adds, sharded, L,
+         R, Z):
+    """Same metric with pinned host operands copied in and Z copied out every step."""
+    n = cfg.n
+    hl = torch.from_numpy(lhs).pin_memory()
+    hr = torch.from_numpy(rhs).pin_memory()
+    hz = torch.empty((n, n), dtype=hl.dtype).pin_memory()
+    hl_np, hr_np, hz_np = hl.numpy(), hr.numpy(), hz.numpy()
+    fn = afmm.afmm_case_a if cfg.case == "a" else afmm.afmm_case_b
+
+    def step():
+        if world == 1:
+            # the reference-facing call: afmm_case_{a,b}_{f32,f64}(host ptrs) via the C ABI
+            fn(hl_np, hr_np, device=local, out=hz_np)
+        else:
+            L.copy_(hl, non_blocking=True)
+            R.copy_(hr, non_blocking=True)
+            sharded.run(cfg.case, L, R, Z, Z)
+            if rank == 0:
+                hz.copy_(Z, non_blocking=True)
+            torch.cuda.synchronize()
+
+    reps = max(1, min(args.steps, 5))
+    for _ in range(1):
+        step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        step()
+    torch.cuda.synchronize()
+    secs = (time.perf_counter() - t0) / reps
+    if world > 1:
+        t = torch.tensor([secs], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        secs = float(t[0])
+    return {"value": job_adds / secs, "unit": UNIT,
+            "h2d_bytes_per_step": 2 * n * n * es * world, "d2h_bytes_per_step": n * n * es,
+            "ms_per_step": secs * 1e3, "steps": reps,
+            "api": "afmm_case_%s_%s (C ABI, host buffers)" % (cfg.case, "f32" if es == 4 else "f64")
+            if world == 1 else "per-rank H2D + row-sharded product + NCCL gather + D2H on rank 0"}
+
+
+def _ncu_traffic(config):
+    """dram bytes per launch of k_bform from the committed ncu --set full capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        entry = d.get(config)
+        return entry
+    except (OSError, ValueError):
+        return None
+
+
+if __name__ == "__main__":
+    main()

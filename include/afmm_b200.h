@@ -132,6 +132,14 @@ afmm_status afmm_product_device(afmm_context* ctx, int32_t which_case, int32_t d
                                 afmm_op_counts* counts, afmm_error* error);
 afmm_status afmm_context_finish(afmm_context* ctx, afmm_op_counts* counts, afmm_error* error);
 
+/* Record CUDA events around the phases of each product on the context's
+ * stream (prepass, repeated-addition kernel, epilogue). After
+ * afmm_context_finish(), afmm_context_last_timing() returns the milliseconds
+ * of the last product's phases; -1 when timing is off. */
+afmm_status afmm_context_enable_timing(afmm_context* ctx, int32_t enable);
+afmm_status afmm_context_last_timing(afmm_context* ctx, float* prepass_ms, float* compute_ms,
+                                     float* epilogue_ms);
+
 /* Per-row work W_i (exact additions of Z row i) for the row partition:
  * Case A  W_i = sum_{k: X[i,k] != 0} sum_j |llround Y[k,j]|
  * Case B  W_i = sum_k |llround X[i,k]| * nnz(Y[k,:])

@@ -216,6 +216,15 @@ class DeviceContext:
         _raise_for(status, err)
         return OpCounts(*counts.as_tuple()) if sync else None
 
+    def enable_timing(self, enable: bool = True) -> None:
+        self._lib.afmm_context_enable_timing(self._h, 1 if enable else 0)
+
+    def last_timing(self) -> Tuple[float, float, float]:
+        """(prepass, repeated-addition kernel, epilogue) milliseconds of the last product."""
+        v = [ctypes.c_float() for _ in range(3)]
+        self._lib.afmm_context_last_timing(self._h, *[ctypes.byref(x) for x in v])
+        return tuple(x.value for x in v)
+
     def finish(self) -> OpCounts:
         counts = _lib.OpCounts()
         err = _lib.Error()

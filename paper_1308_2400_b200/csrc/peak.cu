@@ -5,8 +5,8 @@
 // This kernel measures it with the same instruction mix as the product's
 // inner loop (bform.cu): per lane 4 independent float2 chains of FADD2 for
 // fp32, 4 independent DADD chains for fp64, each adding a register-held step,
-// unrolled, on 4 CTAs x 256 threads per SM. clock64() deltas give the SM
-// clock the measurement ran at.
+// unrolled, on 4 CTAs x 256 threads per SM. clock64() against %globaltimer
+// in the same thread gives the SM clock the measurement ran at.
 #include "kernels.h"
 
 namespace afmm_dev {
@@ -16,13 +16,20 @@ namespace {
 constexpr int kIters = 8192;
 constexpr int kUnroll = 16;
 
-__global__ void k_peak_f32(const float* __restrict__ s, float* out, unsigned long long* cycles) {
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void k_peak_f32(const float* __restrict__ s, float* out, unsigned long long* clk) {
   float2 acc[4], st[4];
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     acc[c] = make_float2(0.f, 0.f);
     st[c] = make_float2(s[(threadIdx.x + 2 * c) & 63], s[(threadIdx.x + 2 * c + 1) & 63]);
   }
+  const unsigned long long g0 = global_ns();
   const long long t0 = clock64();
   for (int it = 0; it < kIters; ++it) {
 #pragma unroll
@@ -31,21 +38,25 @@ __global__ void k_peak_f32(const float* __restrict__ s, float* out, unsigned lon
       for (int c = 0; c < 4; ++c) acc[c] = __fadd2_rn(acc[c], st[c]);
   }
   const long long t1 = clock64();
+  const unsigned long long g1 = global_ns();
   float r = 0.f;
 #pragma unroll
   for (int c = 0; c < 4; ++c) r += acc[c].x + acc[c].y;
   if (r == 1234.5f) out[0] = r;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *cycles = (unsigned long long)(t1 - t0);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    clk[0] = (unsigned long long)(t1 - t0);
+    clk[1] = g1 - g0;
+  }
 }
 
-__global__ void k_peak_f64(const double* __restrict__ s, double* out,
-                           unsigned long long* cycles) {
+__global__ void k_peak_f64(const double* __restrict__ s, double* out, unsigned long long* clk) {
   double acc[4], st[4];
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     acc[c] = 0.0;
     st[c] = s[(threadIdx.x + c) & 63];
   }
+  const unsigned long long g0 = global_ns();
   const long long t0 = clock64();
   for (int it = 0; it < kIters / 2; ++it) {
 #pragma unroll
@@ -54,11 +65,15 @@ __global__ void k_peak_f64(const double* __restrict__ s, double* out,
       for (int c = 0; c < 4; ++c) acc[c] = __dadd_rn(acc[c], st[c]);
   }
   const long long t1 = clock64();
+  const unsigned long long g1 = global_ns();
   double r = 0.0;
 #pragma unroll
   for (int c = 0; c < 4; ++c) r += acc[c];
   if (r == 1234.5) out[0] = r;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *cycles = (unsigned long long)(t1 - t0);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    clk[0] = (unsigned long long)(t1 - t0);
+    clk[1] = g1 - g0;
+  }
 }
 
 }  // namespace
@@ -68,11 +83,14 @@ cudaError_t run_peak(int dtype, double* adds_per_second, double* sm_mhz) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   void* buf = nullptr;
-  unsigned long long* cyc = nullptr;
+  unsigned long long* clk = nullptr;
   cudaError_t e = cudaMalloc(&buf, 64 * sizeof(double) + 64);
   if (e != cudaSuccess) return e;
-  e = cudaMalloc(&cyc, sizeof(unsigned long long));
-  if (e != cudaSuccess) { cudaFree(buf); return e; }
+  e = cudaMalloc(&clk, 2 * sizeof(unsigned long long));
+  if (e != cudaSuccess) {
+    cudaFree(buf);
+    return e;
+  }
   double host[64];
   for (int i = 0; i < 64; ++i) host[i] = 1e-12 * (i + 1);
   float hostf[64];
@@ -85,9 +103,9 @@ cudaError_t run_peak(int dtype, double* adds_per_second, double* sm_mhz) {
   cudaEventCreate(&b);
   auto launch = [&]() {
     if (dtype == 0)
-      k_peak_f64<<<blocks, threads>>>((const double*)buf, (double*)buf + 64, cyc);
+      k_peak_f64<<<blocks, threads>>>((const double*)buf, (double*)buf + 64, clk);
     else
-      k_peak_f32<<<blocks, threads>>>((const float*)buf, (float*)buf + 64, cyc);
+      k_peak_f32<<<blocks, threads>>>((const float*)buf, (float*)buf + 64, clk);
     note_launch();
   };
   for (int w = 0; w < 2; ++w) launch();
@@ -98,19 +116,18 @@ cudaError_t run_peak(int dtype, double* adds_per_second, double* sm_mhz) {
   e = cudaEventSynchronize(b);
   float ms = 0.f;
   cudaEventElapsedTime(&ms, a, b);
-  unsigned long long cycles = 0;
-  cudaMemcpy(&cycles, cyc, sizeof cycles, cudaMemcpyDeviceToHost);
+  unsigned long long hc[2] = {0, 0};
+  cudaMemcpy(hc, clk, sizeof hc, cudaMemcpyDeviceToHost);
   if (e == cudaSuccess) e = cudaGetLastError();
   const double adds_per_thread =
       dtype == 0 ? (double)(kIters / 2) * kUnroll * 4 : (double)kIters * kUnroll * 8;
   const double total = adds_per_thread * blocks * threads * reps;
   if (adds_per_second) *adds_per_second = total / (ms * 1e-3);
-  // one launch's kernel body took `cycles` SM clocks; the launch took ms/reps
-  if (sm_mhz) *sm_mhz = (double)cycles / ((ms / reps) * 1e-3) / 1e6;
+  if (sm_mhz) *sm_mhz = hc[1] ? (double)hc[0] / (double)hc[1] * 1e3 : 0.0;
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   cudaFree(buf);
-  cudaFree(cyc);
+  cudaFree(clk);
   return e;
 }
 

@@ -110,7 +110,13 @@ struct afmm_context {
   const void* last_rhs = nullptr;
   uint64_t last_n = 0, last_ld = 0;
   bool pending = false;
-  afmm_status pending_status = AFMM_OK;
+  // optional phase timing: ev[0] start, ev[1] before compute, ev[2] after compute, ev[3] end
+  bool timing = false;
+  bool timed_last = false;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  void mark(int i) {
+    if (timing) cudaEventRecord(ev[i], stream);
+  }
 };
 
 namespace {
@@ -253,6 +259,8 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
   CK(c->work.ensure(n * 8), "workspace");
   CK(c->zs.ensure(n * 8), "workspace");
   DevStatus* st = c->status.as<DevStatus>();
+  c->timed_last = c->timing;
+  c->mark(0);
   CK(cudaMemsetAsync(st, 0xff, 4 * sizeof(unsigned long long), s), "memset");
   CK(cudaMemsetAsync(&st->additions, 0, 4 * sizeof(unsigned long long), s), "memset");
 
@@ -285,6 +293,7 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
          "copy");
       base = c->base_copy.as<T>();
     }
+    c->mark(1);
     if (rows > 0) {
       if (!make_tmap<T>(&tmap, base, n, n, ldb)) {
         set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: cuTensorMapEncodeTiled failed");
@@ -294,6 +303,7 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
                                    (uint32_t)rows, 0, (int32_t)n, n32, out, ld_out, st, s),
          "bform");
     }
+    c->mark(2);
   } else {
     // Case A as Case B on transposed operands: Z^T = (Y^T) (x) (X^T).
     // B-form rows = Z columns j (rep list = column j of Y), B-form columns =
@@ -318,13 +328,19 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
         set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: cuTensorMapEncodeTiled failed");
         return AFMM_ERR_CUDA;
       }
+      c->mark(1);
       CK(afmm_dev::launch_bform<T>(&tmap, c->lists.as<int2>(), n, c->counts.as<uint32_t>(), n32,
                                    0, (int32_t)rows, n32, c->zt.as<T>(), lds, st, s),
          "bform");
+      c->mark(2);
       afmm_dev::launch_transpose<T>(c->zt.as<T>(), lds, n32, (uint32_t)rows, out, ld_out, s);
+    } else {
+      c->mark(1);
+      c->mark(2);
     }
   }
   if (rows > 0) afmm_dev::launch_sum_counts(work, zs, (uint32_t)r0, (uint32_t)r1, st, s);
+  c->mark(3);
   CK(cudaGetLastError(), "launch");
   CK(cudaMemcpyAsync(c->status_host, st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s),
      "status readback");
@@ -506,6 +522,8 @@ void afmm_context_destroy(afmm_context* c) {
                       &c->base_copy, &c->yt, &c->xt, &c->zt, &c->hx, &c->hy, &c->hz})
       b->release();
     if (c->status_host) cudaFreeHost(c->status_host);
+    for (cudaEvent_t& e : c->ev)
+      if (e) cudaEventDestroy(e);
   }
   delete c;
 }
@@ -564,6 +582,39 @@ afmm_status afmm_context_finish(afmm_context* c, afmm_op_counts* counts, afmm_er
   std::lock_guard<std::mutex> g(c->mu);
   CK(cudaSetDevice(c->device), "afmm: cudaSetDevice");
   return finish_locked(c, counts, err);
+}
+
+afmm_status afmm_context_enable_timing(afmm_context* c, int32_t enable) {
+  if (!c) return AFMM_ERR_INVALID_ARGUMENT;
+  std::lock_guard<std::mutex> g(c->mu);
+  if (enable && !c->ev[0]) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(c->device);
+    for (cudaEvent_t& e : c->ev)
+      if (cudaEventCreate(&e) != cudaSuccess) {
+        cudaSetDevice(prev);
+        return AFMM_ERR_CUDA;
+      }
+    cudaSetDevice(prev);
+  }
+  c->timing = enable != 0;
+  return AFMM_OK;
+}
+
+afmm_status afmm_context_last_timing(afmm_context* c, float* prepass_ms, float* compute_ms,
+                                     float* epilogue_ms) {
+  if (!c) return AFMM_ERR_INVALID_ARGUMENT;
+  std::lock_guard<std::mutex> g(c->mu);
+  float v[3] = {-1.f, -1.f, -1.f};
+  if (c->timed_last && !c->pending) {
+    for (int i = 0; i < 3; ++i)
+      if (cudaEventElapsedTime(&v[i], c->ev[i], c->ev[i + 1]) != cudaSuccess) v[i] = -1.f;
+  }
+  if (prepass_ms) *prepass_ms = v[0];
+  if (compute_ms) *compute_ms = v[1];
+  if (epilogue_ms) *epilogue_ms = v[2];
+  return AFMM_OK;
 }
 
 afmm_status afmm_row_work_device(afmm_context* c, int32_t which_case, int32_t dtype,
