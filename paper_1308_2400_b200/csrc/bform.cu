@@ -17,13 +17,19 @@
 //     the tile is shared by all CW rows of the CTA (CW-fold reuse from smem).
 //   * Each consumer walks its row's compacted (k, rep) list (built by the
 //     prepass, zero reps already skipped), waits for the stage holding row k,
-//     loads its C bases with two conflict-free 128-bit LDS and runs the
+//     loads its C bases with conflict-free 128-bit LDS and runs the
 //     warp-uniform rep loop: |rep| x (C/2) FADD2 (fp32) or |rep| x C DADD
-//     (fp64). Since the rep is uniform across the warp there is no
-//     divergence; zero bases are added as +0/-0, which is bit-neutral
-//     (the accumulator is never -0) and never counted.
+//     (fp64). The rep is uniform across the warp, so there is no divergence;
+//     zero bases are added as +0/-0, which is bit-neutral (the accumulator is
+//     never -0) and never counted.
 //   * Warps release a stage by arriving on its empty barrier; they may drift
 //     up to STAGES blocks apart, which absorbs per-row work imbalance.
+//
+// Issue-slot budget: FADD2 and DADD occupy their pipe for 2 cycles per warp
+// instruction, so one non-FP instruction per FP instruction issues for free.
+// The entry path therefore uses only ALU/LSU instructions (SHF/LOP3/LEA, LDS,
+// SHFL; sign flips by LOP3), and the rep loop has no predicated FP tail
+// (a predicated-off FADD2 still occupies the pipe).
 #include "common.cuh"
 #include "kernels.h"
 
@@ -33,147 +39,146 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-template <class T>
-struct BformCfg;
-
-template <>
-struct BformCfg<float> {
-  // 8 columns per lane (4 x float2)
-  static constexpr int TILE_N = 256;   // columns per CTA
-};
-
-template <>
-struct BformCfg<double> {
-  // 4 columns per lane (2 x double2)
-  static constexpr int TILE_N = 128;
-};
-
-constexpr int KB = 16;       // k rows per stage
+constexpr int KB = 8;        // k rows per stage
 constexpr int STAGES = 6;    // smem ring depth
 constexpr int CW = 16;       // consumer warps (output rows) per CTA
+constexpr int ROW_BYTES = 2048;  // bytes of one staged k row: TILE_N * sizeof(T)
+constexpr int STAGE_BYTES = KB * ROW_BYTES;
+constexpr int G = ROW_BYTES / 32 / 16;  // 128-bit vectors per lane per k row (= 4)
 
 template <class T>
-__host__ __device__ constexpr size_t stage_bytes() {
-  return (size_t)KB * BformCfg<T>::TILE_N * sizeof(T);
-}
+struct BformCfg {
+  static constexpr int TILE_N = ROW_BYTES / sizeof(T);  // 512 fp32 / 256 fp64 columns
+};
 
-template <class T>
 __host__ __device__ constexpr size_t bform_smem_bytes() {
-  return 1024 /*alignment slack*/ + STAGES * stage_bytes<T>() + 2 * STAGES * sizeof(uint64_t);
+  return 1024 /*alignment slack*/ + (size_t)STAGES * STAGE_BYTES + 2 * STAGES * sizeof(uint64_t);
 }
 
-// ---- per-element-type inner loops -----------------------------------------
+__device__ __forceinline__ float4 lds128f(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
+}
 
+__device__ __forceinline__ double2 lds128d(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ float negf(float x) {
+  return __int_as_float(__float_as_int(x) ^ 0x80000000);  // LOP3, exact -x
+}
+
+__device__ __forceinline__ double negd(double x) {
+  return __longlong_as_double(__double_as_longlong(x) ^ 0x8000000000000000ll);
+}
+
+// Lane l owns, for g = 0..G-1, the 16-byte column group at byte g*512 + l*16
+// of each staged k row: every 128-bit LDS across the warp reads 512
+// contiguous bytes (no bank conflict).
 struct AccF32 {
-  float2 a[4];
+  float2 a[2 * G];
   __device__ __forceinline__ void zero() {
 #pragma unroll
-    for (int c = 0; c < 4; ++c) a[c] = make_float2(0.f, 0.f);
+    for (int c = 0; c < 2 * G; ++c) a[c] = make_float2(0.f, 0.f);
   }
-  // Lane owns columns {4l..4l+3} and {128+4l..128+4l+3} of the tile, so each
-  // 128-bit LDS across the warp reads 512 contiguous bytes (no bank conflict).
-  __device__ __forceinline__ void run(const float* row, uint32_t lane, int rep) {
-    const float4 v0 = *reinterpret_cast<const float4*>(row + 4 * lane);
-    const float4 v1 = *reinterpret_cast<const float4*>(row + 128 + 4 * lane);
-    float2 b[4] = {make_float2(v0.x, v0.y), make_float2(v0.z, v0.w), make_float2(v1.x, v1.y),
-                   make_float2(v1.z, v1.w)};
+  __device__ __forceinline__ void run(uint32_t row_addr, int rep) {
+    float2 b[2 * G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float4 v = lds128f(row_addr + g * 512);
+      b[2 * g] = make_float2(v.x, v.y);
+      b[2 * g + 1] = make_float2(v.z, v.w);
+    }
     uint32_t t = (uint32_t)rep;
     if (rep < 0) {
-      // step = -base (kernels.hpp:97): exact negation
+      // step = -base (kernels.hpp:97)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) b[c] = make_float2(-b[c].x, -b[c].y);
-      t = (uint32_t)(-rep);
+      for (int c = 0; c < 2 * G; ++c) b[c] = make_float2(negf(b[c].x), negf(b[c].y));
+      t = 0u - t;
     }
+#pragma unroll 1
     while (t >= 4) {
 #pragma unroll
       for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) a[c] = __fadd2_rn(a[c], b[c]);
+        for (int c = 0; c < 2 * G; ++c) a[c] = __fadd2_rn(a[c], b[c]);
       t -= 4;
     }
-    if (t & 2) {
+#pragma unroll 1
+    while (t != 0) {
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) a[c] = __fadd2_rn(a[c], b[c]);
-    }
-    if (t & 1) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) a[c] = __fadd2_rn(a[c], b[c]);
+      for (int c = 0; c < 2 * G; ++c) a[c] = __fadd2_rn(a[c], b[c]);
+      t -= 1;
     }
   }
   __device__ __forceinline__ void store(float* out_row, int32_t oc0, int32_t ncols, uint32_t lane,
                                         bool vec_ok) {
-    const int32_t c0 = oc0 + 4 * (int32_t)lane;
-    const int32_t c1 = oc0 + 128 + 4 * (int32_t)lane;
-    const float v[8] = {a[0].x, a[0].y, a[1].x, a[1].y, a[2].x, a[2].y, a[3].x, a[3].y};
-    if (vec_ok && c0 + 3 < ncols) {
-      *reinterpret_cast<float4*>(out_row + c0) = make_float4(v[0], v[1], v[2], v[3]);
-    } else {
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (c0 + e < ncols) out_row[c0 + e] = v[e];
-    }
-    if (vec_ok && c1 + 3 < ncols) {
-      *reinterpret_cast<float4*>(out_row + c1) = make_float4(v[4], v[5], v[6], v[7]);
-    } else {
+    for (int g = 0; g < G; ++g) {
+      const int32_t c = oc0 + g * 128 + 4 * (int32_t)lane;
+      const float v[4] = {a[2 * g].x, a[2 * g].y, a[2 * g + 1].x, a[2 * g + 1].y};
+      if (vec_ok && c + 3 < ncols) {
+        *reinterpret_cast<float4*>(out_row + c) = make_float4(v[0], v[1], v[2], v[3]);
+      } else {
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (c1 + e < ncols) out_row[c1 + e] = v[4 + e];
+        for (int e = 0; e < 4; ++e)
+          if (c + e < ncols) out_row[c + e] = v[e];
+      }
     }
   }
 };
 
 struct AccF64 {
-  double a[4];
+  double a[2 * G];
   __device__ __forceinline__ void zero() {
 #pragma unroll
-    for (int c = 0; c < 4; ++c) a[c] = 0.0;
+    for (int c = 0; c < 2 * G; ++c) a[c] = 0.0;
   }
-  // Lane owns columns {2l, 2l+1} and {64+2l, 64+2l+1}.
-  __device__ __forceinline__ void run(const double* row, uint32_t lane, int rep) {
-    const double2 v0 = *reinterpret_cast<const double2*>(row + 2 * lane);
-    const double2 v1 = *reinterpret_cast<const double2*>(row + 64 + 2 * lane);
-    double b[4] = {v0.x, v0.y, v1.x, v1.y};
+  __device__ __forceinline__ void run(uint32_t row_addr, int rep) {
+    double b[2 * G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const double2 v = lds128d(row_addr + g * 512);
+      b[2 * g] = v.x;
+      b[2 * g + 1] = v.y;
+    }
     uint32_t t = (uint32_t)rep;
     if (rep < 0) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) b[c] = -b[c];
-      t = (uint32_t)(-rep);
+      for (int c = 0; c < 2 * G; ++c) b[c] = negd(b[c]);
+      t = 0u - t;
     }
+#pragma unroll 1
     while (t >= 4) {
 #pragma unroll
       for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) a[c] = __dadd_rn(a[c], b[c]);
+        for (int c = 0; c < 2 * G; ++c) a[c] = __dadd_rn(a[c], b[c]);
       t -= 4;
     }
-    if (t & 2) {
+#pragma unroll 1
+    while (t != 0) {
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) a[c] = __dadd_rn(a[c], b[c]);
-    }
-    if (t & 1) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) a[c] = __dadd_rn(a[c], b[c]);
+      for (int c = 0; c < 2 * G; ++c) a[c] = __dadd_rn(a[c], b[c]);
+      t -= 1;
     }
   }
   __device__ __forceinline__ void store(double* out_row, int32_t oc0, int32_t ncols,
                                         uint32_t lane, bool vec_ok) {
-    const int32_t c0 = oc0 + 2 * (int32_t)lane;
-    const int32_t c1 = oc0 + 64 + 2 * (int32_t)lane;
-    if (vec_ok && c0 + 1 < ncols) {
-      *reinterpret_cast<double2*>(out_row + c0) = make_double2(a[0], a[1]);
-    } else {
-      if (c0 < ncols) out_row[c0] = a[0];
-      if (c0 + 1 < ncols) out_row[c0 + 1] = a[1];
-    }
-    if (vec_ok && c1 + 1 < ncols) {
-      *reinterpret_cast<double2*>(out_row + c1) = make_double2(a[2], a[3]);
-    } else {
-      if (c1 < ncols) out_row[c1] = a[2];
-      if (c1 + 1 < ncols) out_row[c1 + 1] = a[3];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int32_t c = oc0 + g * 64 + 2 * (int32_t)lane;
+      if (vec_ok && c + 1 < ncols) {
+        *reinterpret_cast<double2*>(out_row + c) = make_double2(a[2 * g], a[2 * g + 1]);
+      } else {
+        if (c < ncols) out_row[c] = a[2 * g];
+        if (c + 1 < ncols) out_row[c + 1] = a[2 * g + 1];
+      }
     }
   }
 };
@@ -200,11 +205,11 @@ __global__ void __launch_bounds__((CW + 1) * 32, 2)
   using Cfg = BformCfg<T>;
   extern __shared__ unsigned char smem_raw[];
   // 1024-byte aligned ring; pointer arithmetic on the smem pointer itself keeps
-  // the shared address space visible to the compiler (LDS, not generic LD).
+  // the shared address space visible to the compiler.
   unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  T* tiles = reinterpret_cast<T*>(base);
-  uint64_t* full = reinterpret_cast<uint64_t*>(base + STAGES * stage_bytes<T>());
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
+  const uint32_t ring = smem_u32(base);
 
   if (status_failed(st)) return;  // validation failed: compute nothing (kernels.hpp:115,144)
 
@@ -227,8 +232,8 @@ __global__ void __launch_bounds__((CW + 1) * 32, 2)
       uint32_t slot = 0, phase = 0;
       for (uint32_t kb = 0; kb < nkb; ++kb) {
         if (kb >= STAGES) mbar_wait(&empty[slot], phase ^ 1);
-        mbar_arrive_expect_tx(&full[slot], (uint32_t)stage_bytes<T>());
-        tma_load_2d(tiles + (size_t)slot * KB * Cfg::TILE_N, &tmap, &full[slot], col0 + tile_c,
+        mbar_arrive_expect_tx(&full[slot], (uint32_t)STAGE_BYTES);
+        tma_load_2d(base + slot * STAGE_BYTES, &tmap, &full[slot], col0 + tile_c,
                     (int32_t)(kb * KB));
         if (++slot == STAGES) {
           slot = 0;
@@ -248,15 +253,19 @@ __global__ void __launch_bounds__((CW + 1) * 32, 2)
   acc.zero();
 
   // (kb_cur, slot, phase): the k block currently held, its ring slot and the
-  // parity of that slot's current fill.
+  // parity of that slot's current fill; stage_addr = smem address of the slot
+  // plus this lane's first 16-byte column group.
   uint32_t kb_cur = 0, slot = 0, phase = 0;
+  uint32_t stage_addr = ring + lane * 16;
   auto advance = [&]() {
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
     ++kb_cur;
+    stage_addr += STAGE_BYTES;
     if (++slot == STAGES) {
       slot = 0;
       phase ^= 1;
+      stage_addr -= STAGES * STAGE_BYTES;
     }
   };
   mbar_wait(&full[0], 0);
@@ -266,15 +275,14 @@ __global__ void __launch_bounds__((CW + 1) * 32, 2)
     const int2 nxt = pn < cnt ? lst[pn] : make_int2(0, 0);  // prefetch next chunk
     const uint32_t m = cnt - p < 32u ? cnt - p : 32u;
     for (uint32_t q = 0; q < m; ++q) {
-      const int k = __shfl_sync(FULL, cur.x, q);
+      const uint32_t k = (uint32_t)__shfl_sync(FULL, cur.x, q);
       const int rep = __shfl_sync(FULL, cur.y, q);
-      const uint32_t kb = (uint32_t)k / KB;
+      const uint32_t kb = k / KB;
       while (kb_cur < kb) {
         advance();
         mbar_wait(&full[slot], phase);
       }
-      const T* row = tiles + ((size_t)slot * KB + ((uint32_t)k % KB)) * Cfg::TILE_N;
-      acc.run(row, lane, rep);
+      acc.run(stage_addr + (k % KB) * ROW_BYTES, rep);
     }
     cur = nxt;
   }
@@ -305,7 +313,7 @@ cudaError_t launch_bform(const CUtensorMap* tmap, const int2* lists, uint64_t ca
                          const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,
                          uint32_t nk, T* out, uint64_t ld_out, const DevStatus* st,
                          cudaStream_t s) {
-  const size_t smem = bform_smem_bytes<T>();
+  const size_t smem = bform_smem_bytes();
   // set on every call: the attribute is per device and costs ~1 us
   cudaError_t e =
       cudaFuncSetAttribute(k_bform<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
