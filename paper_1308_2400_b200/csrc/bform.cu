@@ -42,13 +42,24 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int KB = 8;        // k rows per stage
 constexpr int STAGES = 6;    // smem ring depth
 constexpr int CW = 16;       // consumer warps (output rows) per CTA
-constexpr int ROW_BYTES = 2048;  // bytes of one staged k row: TILE_N * sizeof(T)
+constexpr int ROW_BYTES = 2048;  // bytes of one k row of the tile: TILE_N * sizeof(T)
+// A TMA box is at most 256 elements wide, so a stage is NBOX boxes of
+// KB x BOX_BYTES laid out box-major: [box][k row][BOX_BYTES].
+constexpr int BOX_BYTES = 1024;
+constexpr int NBOX = ROW_BYTES / BOX_BYTES;
 constexpr int STAGE_BYTES = KB * ROW_BYTES;
 constexpr int G = ROW_BYTES / 32 / 16;  // 128-bit vectors per lane per k row (= 4)
 
+// smem byte offset of vector group g (0..G-1) of a k row, relative to the row's
+// address in box 0 (the 512-byte warp-wide groups are two per box row).
+__device__ __forceinline__ constexpr uint32_t group_off(int g) {
+  return (uint32_t)((g >> 1) * KB * BOX_BYTES + (g & 1) * 512);
+}
+
 template <class T>
 struct BformCfg {
-  static constexpr int TILE_N = ROW_BYTES / sizeof(T);  // 512 fp32 / 256 fp64 columns
+  static constexpr int TILE_N = ROW_BYTES / sizeof(T);     // 512 fp32 / 256 fp64 columns
+  static constexpr int BOX_N = BOX_BYTES / sizeof(T);      // 256 fp32 / 128 fp64 columns
 };
 
 __host__ __device__ constexpr size_t bform_smem_bytes() {
@@ -90,7 +101,7 @@ struct AccF32 {
     float2 b[2 * G];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const float4 v = lds128f(row_addr + g * 512);
+      const float4 v = lds128f(row_addr + group_off(g));
       b[2 * g] = make_float2(v.x, v.y);
       b[2 * g + 1] = make_float2(v.z, v.w);
     }
@@ -143,7 +154,7 @@ struct AccF64 {
     double b[2 * G];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const double2 v = lds128d(row_addr + g * 512);
+      const double2 v = lds128d(row_addr + group_off(g));
       b[2 * g] = v.x;
       b[2 * g + 1] = v.y;
     }
@@ -233,8 +244,10 @@ __global__ void __launch_bounds__((CW + 1) * 32, 2)
       for (uint32_t kb = 0; kb < nkb; ++kb) {
         if (kb >= STAGES) mbar_wait(&empty[slot], phase ^ 1);
         mbar_arrive_expect_tx(&full[slot], (uint32_t)STAGE_BYTES);
-        tma_load_2d(base + slot * STAGE_BYTES, &tmap, &full[slot], col0 + tile_c,
-                    (int32_t)(kb * KB));
+#pragma unroll
+        for (int h = 0; h < NBOX; ++h)
+          tma_load_2d(base + slot * STAGE_BYTES + h * KB * BOX_BYTES, &tmap, &full[slot],
+                      col0 + tile_c + h * Cfg::BOX_N, (int32_t)(kb * KB));
         if (++slot == STAGES) {
           slot = 0;
           phase ^= 1;
@@ -282,7 +295,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 2)
         advance();
         mbar_wait(&full[slot], phase);
       }
-      acc.run(stage_addr + (k % KB) * ROW_BYTES, rep);
+      acc.run(stage_addr + (k % KB) * BOX_BYTES, rep);
     }
     cur = nxt;
   }
@@ -301,6 +314,11 @@ __global__ void __launch_bounds__((CW + 1) * 32, 2)
 template <class T>
 int bform_tile_n() {
   return BformCfg<T>::TILE_N;
+}
+
+template <class T>
+int bform_box_cols() {
+  return BformCfg<T>::BOX_N;
 }
 
 template <class T>
@@ -328,6 +346,8 @@ cudaError_t launch_bform(const CUtensorMap* tmap, const int2* lists, uint64_t ca
   return cudaGetLastError();
 }
 
+template int bform_box_cols<float>();
+template int bform_box_cols<double>();
 template int bform_tile_n<float>();
 template int bform_tile_n<double>();
 template int bform_kb<float>();

@@ -39,6 +39,8 @@ int bform_tile_n();
 template <class T>
 int bform_kb();
 template <class T>
+int bform_box_cols();
+template <class T>
 cudaError_t launch_bform(const CUtensorMap* tmap, const int2* lists, uint64_t cap,
                          const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,
                          uint32_t nk, T* out, uint64_t ld_out, const DevStatus* st,

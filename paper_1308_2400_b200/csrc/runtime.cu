@@ -82,7 +82,7 @@ bool make_tmap(CUtensorMap* map, const T* base, uint64_t rows, uint64_t cols, ui
   if (!fn) return false;
   const cuuint64_t gdim[2] = {cols, rows};
   const cuuint64_t gstride[1] = {ld * sizeof(T)};
-  const cuuint32_t box[2] = {(cuuint32_t)afmm_dev::bform_tile_n<T>(),
+  const cuuint32_t box[2] = {(cuuint32_t)afmm_dev::bform_box_cols<T>(),
                              (cuuint32_t)afmm_dev::bform_kb<T>()};
   const cuuint32_t estride[2] = {1, 1};
   const CUtensorMapDataType dt =
