@@ -9,11 +9,12 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
 NVFLAGS += -fmad=false -ftz=false -prec-div=true -prec-sqrt=true
 
 CSRC := paper_1308_2400_b200/csrc
-SRCS := $(CSRC)/runtime.cu $(CSRC)/prepass.cu $(CSRC)/bform.cu $(CSRC)/peak.cu
+SRCS := $(CSRC)/runtime.cu $(CSRC)/prepass.cu $(CSRC)/bform.cu $(CSRC)/bform_l1.cu $(CSRC)/peak.cu
 OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
 LIB := paper_1308_2400_b200/libafmm_b200.so
+REF_INC ?= /root/reference/proj/include
 
-all: $(LIB) oracle
+all: $(LIB) oracle $(if $(wildcard $(REF_INC)/afmm/kernels.hpp),cpptest)
 
 build/%.o: $(CSRC)/%.cu $(CSRC)/common.cuh $(CSRC)/kernels.h include/afmm_b200.h
 	@mkdir -p build
@@ -25,6 +26,15 @@ $(LIB): $(OBJS)
 oracle:
 	$(MAKE) -C oracle
 
+# The reference's kernel tests restated against the drop-in C++ front end
+# (needs the reference headers, so it is built in the build container; the
+# binary travels to the GPU box with the snapshot).
+cpptest: build/test_gpu_kernels
+build/test_gpu_kernels: tests/cpp/test_gpu_kernels.cpp include/afmm_b200/kernels.hpp include/afmm_b200.h $(LIB)
+	@mkdir -p build
+	g++ -std=c++20 -O2 -ffp-contract=off -I$(REF_INC) -Iinclude -o $@ $< \
+	    -L paper_1308_2400_b200 -lafmm_b200 -Wl,-rpath,'$$ORIGIN/../paper_1308_2400_b200'
+
 sass: $(LIB)
 	/usr/local/cuda/bin/cuobjdump -sass $(LIB) > build/libafmm_b200.sass
 
@@ -32,4 +42,4 @@ clean:
 	rm -rf build $(LIB)
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle clean sass
+.PHONY: all oracle clean sass cpptest

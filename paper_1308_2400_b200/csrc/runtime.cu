@@ -11,6 +11,7 @@
 #include <atomic>
 #include <cinttypes>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -28,6 +29,14 @@ void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 namespace {
 
 constexpr uint64_t kNone = ~0ull;
+constexpr int kVariantL1 = 0;    // decoupled warps, L1-cached base loads (bform_l1.cu)
+constexpr int kVariantRing = 1;  // TMA smem ring shared by the CTA (bform.cu)
+
+int variant_from_env() {
+  const char* v = std::getenv("AFMM_BFORM");
+  if (v && std::strcmp(v, "ring") == 0) return kVariantRing;
+  return kVariantL1;
+}
 
 inline uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
 
@@ -110,6 +119,8 @@ struct afmm_context {
   const void* last_rhs = nullptr;
   uint64_t last_n = 0, last_ld = 0;
   bool pending = false;
+  uint64_t list_cap = 0;
+  int variant = 0;  // kVariantL1 / kVariantRing (AFMM_BFORM=ring|l1)
   // optional phase timing: ev[0] start, ev[1] before compute, ev[2] after compute, ev[3] end
   bool timing = false;
   bool timed_last = false;
@@ -245,6 +256,32 @@ afmm_status decode_status(afmm_context* c, afmm_op_counts* counts, afmm_error* e
     if (_e != cudaSuccess) return cuda_fail(err, _e, what); \
   } while (0)
 
+// The repeated-addition kernel over B-form rows [0, nrows) (their rep lists
+// are in c->lists / c->counts) and base columns [col0, col0 + ncols) of the
+// base matrix (kb_rows x b_cols, leading dimension ldb).
+template <class T>
+afmm_status launch_compute(afmm_context* c, const T* base, uint64_t kb_rows, uint64_t b_cols,
+                           uint64_t ldb, uint32_t nrows, int32_t col0, int32_t ncols, T* out,
+                           uint64_t ld_out, DevStatus* st, afmm_error* err) {
+  if (c->variant == kVariantRing) {
+    CUtensorMap tmap;
+    if (!make_tmap<T>(&tmap, base, kb_rows, b_cols, ldb)) {
+      set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: cuTensorMapEncodeTiled failed");
+      return AFMM_ERR_CUDA;
+    }
+    CK(afmm_dev::launch_bform<T>(&tmap, c->lists.as<int2>(), c->list_cap,
+                                 c->counts.as<uint32_t>(), nrows, col0, ncols, (uint32_t)kb_rows,
+                                 out, ld_out, st, c->stream),
+       "bform");
+  } else {
+    CK(afmm_dev::launch_bform_l1<T>(base, ldb, c->lists.as<int2>(), c->list_cap,
+                                    c->counts.as<uint32_t>(), nrows, col0, ncols, out, ld_out, st,
+                                    c->stream),
+       "bform_l1");
+  }
+  return AFMM_OK;
+}
+
 // Enqueue the whole device pipeline for Z rows [r0, r1). Pointers are device
 // memory with leading dimension ld (lhs, rhs) and ld_out (out).
 template <class T>
@@ -259,6 +296,7 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
   CK(c->work.ensure(n * 8), "workspace");
   CK(c->zs.ensure(n * 8), "workspace");
   DevStatus* st = c->status.as<DevStatus>();
+  c->list_cap = n;
   c->timed_last = c->timing;
   c->mark(0);
   CK(cudaMemsetAsync(st, 0xff, 4 * sizeof(unsigned long long), s), "memset");
@@ -272,7 +310,6 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
 
   auto* work = c->work.as<unsigned long long>();
   auto* zs = c->zs.as<unsigned long long>();
-  CUtensorMap tmap;
   if (which == AFMM_CASE_B) {
     // rep = X[i,k] (lhs), bases = Y[k,:] (rhs): B-form directly.
     auto* nnz = c->vec_k.as<uint32_t>();
@@ -295,13 +332,9 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
     }
     c->mark(1);
     if (rows > 0) {
-      if (!make_tmap<T>(&tmap, base, n, n, ldb)) {
-        set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: cuTensorMapEncodeTiled failed");
-        return AFMM_ERR_CUDA;
-      }
-      CK(afmm_dev::launch_bform<T>(&tmap, c->lists.as<int2>(), n, c->counts.as<uint32_t>(),
-                                   (uint32_t)rows, 0, (int32_t)n, n32, out, ld_out, st, s),
-         "bform");
+      afmm_status cs = launch_compute<T>(c, base, n, n, ldb, (uint32_t)rows, 0, (int32_t)n, out,
+                                         ld_out, st, err);
+      if (cs != AFMM_OK) return cs;
     }
     c->mark(2);
   } else {
@@ -324,14 +357,10 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
     if (rows > 0) {
       afmm_dev::launch_transpose<T>(lhs + r0 * ld, ld, (uint32_t)rows, n32, c->xt.as<T>(), lds,
                                     s);
-      if (!make_tmap<T>(&tmap, c->xt.as<T>(), n, rows, lds)) {
-        set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: cuTensorMapEncodeTiled failed");
-        return AFMM_ERR_CUDA;
-      }
       c->mark(1);
-      CK(afmm_dev::launch_bform<T>(&tmap, c->lists.as<int2>(), n, c->counts.as<uint32_t>(), n32,
-                                   0, (int32_t)rows, n32, c->zt.as<T>(), lds, st, s),
-         "bform");
+      afmm_status cs = launch_compute<T>(c, c->xt.as<T>(), n, rows, lds, n32, 0, (int32_t)rows,
+                                         c->zt.as<T>(), lds, st, err);
+      if (cs != AFMM_OK) return cs;
       c->mark(2);
       afmm_dev::launch_transpose<T>(c->zt.as<T>(), lds, n32, (uint32_t)rows, out, ld_out, s);
     } else {
@@ -498,6 +527,7 @@ afmm_status afmm_context_create(int32_t device, afmm_context** ctx) {
   auto* c = new (std::nothrow) afmm_context;
   if (!c) return AFMM_ERR_OUT_OF_MEMORY;
   c->device = device;
+  c->variant = variant_from_env();
   int prev = 0;
   cudaGetDevice(&prev);
   if (cudaSetDevice(device) != cudaSuccess ||

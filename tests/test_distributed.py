@@ -1,0 +1,92 @@
+"""The N>1 row-sharded path on CPU: world size 2 over gloo.
+
+The sharding logic (per-row work -> equal-work cuts -> per-rank slab -> gather to
+rank 0) is the same code bench.py runs over NCCL; here the per-rank compute is
+the CPU oracle standing in for the GPU (the only GPU in this pool is used by
+the gpu-marked tests), so what is tested is the partition and the exchange:
+rank 0 must end up with exactly the single-process product.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+class OracleContext:
+    """Test double of afmm.DeviceContext (same row_work / product signatures)."""
+
+    def __init__(self):
+        from oracle.oracle import Oracle
+
+        self.oracle = Oracle()
+
+    def row_work(self, which, lhs, rhs):
+        l, r = lhs.numpy(), rhs.numpy()
+        if which == "a":
+            rsum = np.abs(np.rint(r)).sum(axis=1)
+            return ((l != 0) * rsum[None, :]).sum(axis=1).astype(np.uint64)
+        nnz = (r != 0).sum(axis=1)
+        return (np.abs(np.rint(l)) * nnz[None, :]).sum(axis=1).astype(np.uint64)
+
+    def product(self, which, lhs, rhs, out, r0, r1):
+        z, counts, err = self.oracle.product(which, lhs.numpy(), rhs.numpy(), r0, r1)
+        assert err is None
+        if r1 > r0:
+            out[: r1 - r0].copy_(torch.from_numpy(z))
+        from paper_1308_2400_b200 import OpCounts
+
+        return OpCounts(*counts)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, case, n, result_path):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1308_2400_b200.distributed import ShardedProduct
+    from paper_1308_2400_b200.gen import make_inputs
+
+    name = "cfg4" if case == "a" else "cfg5"
+    lhs, rhs = make_inputs(name, seed=5, n=n)
+    L, R = torch.from_numpy(lhs), torch.from_numpy(rhs)
+    Z = torch.full((n, n), float("nan"), dtype=L.dtype)
+    sp = ShardedProduct(OracleContext(), dist, rank, world)
+    counts = sp.run(case, L, R, Z, torch.empty_like(Z))
+    adds = torch.tensor([counts.additions], dtype=torch.float64)
+    dist.all_reduce(adds)
+    if rank == 0:
+        np.save(result_path, Z.numpy())
+        np.save(result_path + ".meta.npy", np.array([adds.item(), *sp.cuts], dtype=np.float64))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case,n", [("a", 96), ("b", 130)])
+def test_two_rank_gloo_sharded_product_matches_single_process(tmp_path, case, n, oracle):
+    from paper_1308_2400_b200.gen import expected_additions, make_inputs
+
+    out = str(tmp_path / "z.npy")
+    mp.spawn(_worker, args=(2, _free_port(), case, n, out), nprocs=2, join=True)
+    z = np.load(out)
+    meta = np.load(out + ".meta.npy")
+    name = "cfg4" if case == "a" else "cfg5"
+    lhs, rhs = make_inputs(name, seed=5, n=n)
+    ref, counts, _ = oracle.product(case, lhs, rhs)
+    assert np.array_equal(z.view(np.uint8), ref.view(np.uint8))
+    assert int(meta[0]) == counts[0] == expected_additions(case, lhs, rhs)
+    cuts = meta[1:].astype(int)
+    assert cuts[0] == 0 and cuts[-1] == n and 0 < cuts[1] < n

@@ -195,3 +195,27 @@ def test_full_size_row_sample_bit_exact(cuda, oracle, name, kw):
         zr, _ = oracle.product_mt(cfg.case, lhs, rhs, r, r + 1, 1)
         assert _bits_equal(z[r:r + 1], zr), (name, r)
     ctx.close()
+
+
+@pytest.mark.parametrize("variant", ["ring", "l1"])
+def test_both_kernel_variants_bit_exact(cuda, oracle, variant, monkeypatch):
+    """k_bform (TMA smem ring) and k_bform_l1 (decoupled warps) give identical bits."""
+    import torch
+
+    from paper_1308_2400_b200.gen import CONFIGS, make_inputs
+
+    monkeypatch.setenv("AFMM_BFORM", variant)
+    afmm = _api()
+    ctx = afmm.DeviceContext(0)  # reads AFMM_BFORM at creation
+    for name, n, kw in (("cfg1", 200, {}), ("cfg2", 333, {}), ("cfg3", 515, {"d1": 0.5, "mu": 4}),
+                        ("cfg5", 600, {})):
+        lhs, rhs = make_inputs(name, seed=11, n=n, **kw)
+        case = CONFIGS[name].case
+        z, c, _ = oracle.product(case, lhs, rhs)
+        L = torch.from_numpy(lhs).cuda()
+        R = torch.from_numpy(rhs).cuda()
+        O = torch.empty_like(L)
+        counts = ctx.product(case, L, R, O)
+        assert (counts.additions, 0, counts.zero_skips) == c
+        assert _bits_equal(O.cpu().numpy(), z), (variant, name)
+    ctx.close()
