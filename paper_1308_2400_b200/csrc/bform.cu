@@ -309,7 +309,211 @@ __global__ void __launch_bounds__((CW + 1) * 32, 2)
   if (b < nrows) acc.store(out + (uint64_t)b * ld_out, tile_c, ncols, lane, vec_ok != 0);
 }
 
+// ---------------------------------------------------------------------------
+// k_bform_dyn: the same TMA ring, but the CTA's rows are not pinned to warps.
+//
+// ncu on k_bform showed ~9% of warp samples spinning on stage barriers: a
+// row's cumulative work is a random walk in k, and with one row per warp the
+// ring's slack (STAGES blocks) is regularly exhausted by the slowest warp.
+// Here the unit of work is an ITEM = (k block b, row w). Items are handed out
+// from a CTA-wide counter in b-major order, so any warp takes whichever row is
+// next; a row's accumulators live in registers for the duration of an item
+// and in a 16 x TILE_N smem tile between items. Per-row order is kept by a
+// per-row "next block" flag (item (w, b) starts only after (w, b-1) has
+// stored its accumulators), so every element still receives its terms in
+// increasing k, exactly as kernels.hpp:148-163.
+// ---------------------------------------------------------------------------
+
+constexpr int DYN_STAGES = 4;  // power of two
+constexpr int DYN_ROWS = 16;   // rows per CTA (power of two)
+constexpr int DYN_CW = 16;     // consumer warps per CTA
+constexpr int ZS_BYTES = DYN_ROWS * ROW_BYTES;
+
+__host__ __device__ constexpr size_t bform_dyn_smem_bytes() {
+  return 1024 + (size_t)DYN_STAGES * STAGE_BYTES + ZS_BYTES + 2 * DYN_STAGES * sizeof(uint64_t) +
+         (2 * DYN_ROWS + 4) * sizeof(uint32_t);
+}
+
+__device__ __forceinline__ void sts128(uint32_t addr, float a, float b, float c, float d) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
+}
+__device__ __forceinline__ void sts128d(uint32_t addr, double a, double b) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(a), "d"(b) : "memory");
+}
+
+__device__ __forceinline__ void save_acc(const AccF32& acc, uint32_t z) {
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+    sts128(z + g * 512, acc.a[2 * g].x, acc.a[2 * g].y, acc.a[2 * g + 1].x, acc.a[2 * g + 1].y);
+}
+__device__ __forceinline__ void load_acc(AccF32& acc, uint32_t z) {
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const float4 v = lds128f(z + g * 512);
+    acc.a[2 * g] = make_float2(v.x, v.y);
+    acc.a[2 * g + 1] = make_float2(v.z, v.w);
+  }
+}
+__device__ __forceinline__ void save_acc(const AccF64& acc, uint32_t z) {
+#pragma unroll
+  for (int g = 0; g < G; ++g) sts128d(z + g * 512, acc.a[2 * g], acc.a[2 * g + 1]);
+}
+__device__ __forceinline__ void load_acc(AccF64& acc, uint32_t z) {
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const double2 v = lds128d(z + g * 512);
+    acc.a[2 * g] = v.x;
+    acc.a[2 * g + 1] = v.y;
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__((DYN_CW + 1) * 32, 2)
+    k_bform_dyn(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ lists,
+                uint64_t cap, const uint32_t* __restrict__ counts, uint32_t nrows, int32_t col0,
+                int32_t ncols, uint32_t nkb, T* __restrict__ out, uint64_t ld_out, int vec_ok,
+                const DevStatus* __restrict__ st) {
+  using Cfg = BformCfg<T>;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char* zs = base + DYN_STAGES * STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(zs + ZS_BYTES);
+  uint64_t* empty = full + DYN_STAGES;
+  volatile uint32_t* row_next = reinterpret_cast<volatile uint32_t*>(empty + DYN_STAGES);
+  uint32_t* cursor = const_cast<uint32_t*>(row_next + DYN_ROWS);
+  uint32_t* item_ctr = cursor + DYN_ROWS;
+  const uint32_t ring = smem_u32(base);
+  const uint32_t zs_addr = smem_u32(zs);
+
+  if (status_failed(st)) return;  // validation failed: compute nothing (kernels.hpp:115,144)
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t tile_c = blockIdx.y * Cfg::TILE_N;
+  const uint32_t row0 = blockIdx.x * DYN_ROWS;
+  const uint32_t rows_here = nrows - row0 < (uint32_t)DYN_ROWS ? nrows - row0 : DYN_ROWS;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < DYN_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], DYN_ROWS);
+    }
+    *item_ctr = 0;
+    fence_barrier_init();
+  }
+  if (threadIdx.x < DYN_ROWS) {
+    row_next[threadIdx.x] = 0;
+    cursor[threadIdx.x] = 0;
+  }
+  __syncthreads();
+
+  if (warp == DYN_CW) {
+    // ---- TMA producer ----
+    if (lane == 0) {
+      prefetch_tensormap(&tmap);
+      for (uint32_t kb = 0; kb < nkb; ++kb) {
+        const uint32_t slot = kb & (DYN_STAGES - 1);
+        if (kb >= DYN_STAGES) mbar_wait(&empty[slot], ((kb / DYN_STAGES) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[slot], (uint32_t)STAGE_BYTES);
+#pragma unroll
+        for (int h = 0; h < NBOX; ++h)
+          tma_load_2d(base + slot * STAGE_BYTES + h * KB * BOX_BYTES, &tmap, &full[slot],
+                      col0 + tile_c + h * Cfg::BOX_N, (int32_t)(kb * KB));
+      }
+    }
+    return;
+  }
+
+  // ---- consumers: items (b, w) in b-major order ----
+  const uint32_t total = nkb * DYN_ROWS;
+  typename AccOf<T>::type acc;
+  while (true) {
+    uint32_t id = 0;
+    if (lane == 0) id = atomicAdd(item_ctr, 1u);
+    id = __shfl_sync(FULL, id, 0);
+    if (id >= total) break;
+    const uint32_t b = id / DYN_ROWS, w = id % DYN_ROWS;
+    const uint32_t slot = b & (DYN_STAGES - 1);
+    mbar_wait(&full[slot], (b / DYN_STAGES) & 1);
+    if (w < rows_here) {
+      // per-row order: (w, b-1) must have stored its accumulators
+      while (row_next[w] != b) {
+      }
+      __threadfence_block();
+      const uint32_t zrow = zs_addr + w * ROW_BYTES + lane * 16;
+      if (b == 0) acc.zero();
+      else load_acc(acc, zrow);
+      const uint32_t r = row0 + w;
+      const uint32_t cnt = counts[r];
+      const int2* lst = lists + (uint64_t)r * cap;
+      uint32_t p = cursor[w];
+      const uint32_t kend = (b + 1) * KB;
+      const uint32_t stage_addr = ring + slot * STAGE_BYTES + lane * 16;
+      while (p < cnt) {
+        const int2 e = p + lane < cnt ? lst[p + lane] : make_int2(0x7fffffff, 0);
+        // entries of this block among the 32 fetched (lists are sorted by k)
+        const unsigned in_blk = __ballot_sync(FULL, (uint32_t)e.x < kend);
+        const uint32_t m = __popc(in_blk);
+        for (uint32_t q = 0; q < m; ++q) {
+          const uint32_t k = (uint32_t)__shfl_sync(FULL, e.x, q);
+          const int rep = __shfl_sync(FULL, e.y, q);
+          acc.run(stage_addr + (k % KB) * BOX_BYTES, rep);
+        }
+        p += m;
+        if (m < 32) break;
+      }
+      save_acc(acc, zrow);
+      __syncwarp();
+      if (lane == 0) {
+        cursor[w] = p;
+        __threadfence_block();
+        row_next[w] = b + 1;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+  }
+
+  // all items done -> write the Z tile out (named barrier over the consumers)
+  asm volatile("bar.sync 1, %0;" ::"r"(DYN_CW * 32) : "memory");
+  for (uint32_t w = warp; w < rows_here; w += DYN_CW) {
+    load_acc(acc, zs_addr + w * ROW_BYTES + lane * 16);
+    acc.store(out + (uint64_t)(row0 + w) * ld_out, tile_c, ncols, lane, vec_ok != 0);
+  }
+}
+
 }  // namespace
+
+template <class T>
+cudaError_t launch_bform_dyn(const CUtensorMap* tmap, const int2* lists, uint64_t cap,
+                             const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,
+                             uint32_t nk, T* out, uint64_t ld_out, const DevStatus* st,
+                             cudaStream_t s) {
+  const size_t smem = bform_dyn_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(k_bform_dyn<T>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const uint32_t nkb = (nk + KB - 1) / KB;
+  const bool vec_ok = (ld_out * sizeof(T)) % 16 == 0 &&
+                      (reinterpret_cast<uintptr_t>(out) % 16) == 0;
+  dim3 grid((nrows + DYN_ROWS - 1) / DYN_ROWS,
+            (ncols + BformCfg<T>::TILE_N - 1) / BformCfg<T>::TILE_N);
+  k_bform_dyn<T><<<grid, (DYN_CW + 1) * 32, smem, s>>>(*tmap, lists, cap, counts, nrows, col0,
+                                                       ncols, nkb, out, ld_out, vec_ok ? 1 : 0,
+                                                       st);
+  note_launch();
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_bform_dyn<float>(const CUtensorMap*, const int2*, uint64_t,
+                                             const uint32_t*, uint32_t, int32_t, int32_t,
+                                             uint32_t, float*, uint64_t, const DevStatus*,
+                                             cudaStream_t);
+template cudaError_t launch_bform_dyn<double>(const CUtensorMap*, const int2*, uint64_t,
+                                              const uint32_t*, uint32_t, int32_t, int32_t,
+                                              uint32_t, double*, uint64_t, const DevStatus*,
+                                              cudaStream_t);
 
 template <class T>
 int bform_tile_n() {

@@ -47,6 +47,11 @@ cudaError_t launch_bform(const CUtensorMap* tmap, const int2* lists, uint64_t ca
                          cudaStream_t s);
 
 template <class T>
+cudaError_t launch_bform_dyn(const CUtensorMap* tmap, const int2* lists, uint64_t cap,
+                             const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,
+                             uint32_t nk, T* out, uint64_t ld_out, const DevStatus* st,
+                             cudaStream_t s);
+template <class T>
 cudaError_t launch_bform_l1(const T* base, uint64_t ldb, const int2* lists, uint64_t cap,
                             const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,
                             T* out, uint64_t ld_out, const DevStatus* st, cudaStream_t s);

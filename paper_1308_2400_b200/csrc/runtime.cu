@@ -29,13 +29,17 @@ void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 namespace {
 
 constexpr uint64_t kNone = ~0ull;
-constexpr int kVariantL1 = 0;    // decoupled warps, L1-cached base loads (bform_l1.cu)
-constexpr int kVariantRing = 1;  // TMA smem ring shared by the CTA (bform.cu)
+constexpr int kVariantDyn = 0;   // TMA smem ring + dynamic (block, row) items (bform.cu)
+constexpr int kVariantRing = 1;  // TMA smem ring, one row pinned per warp (bform.cu)
+constexpr int kVariantL1 = 2;    // decoupled warps, L1-cached base loads (bform_l1.cu)
 
+// AFMM_BFORM=dyn|ring|l1 selects the repeated-addition kernel (all three are
+// bit-identical; tests/test_gpu_parity.py runs each). Default: dyn.
 int variant_from_env() {
   const char* v = std::getenv("AFMM_BFORM");
   if (v && std::strcmp(v, "ring") == 0) return kVariantRing;
-  return kVariantL1;
+  if (v && std::strcmp(v, "l1") == 0) return kVariantL1;
+  return kVariantDyn;
 }
 
 inline uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
@@ -120,7 +124,7 @@ struct afmm_context {
   uint64_t last_n = 0, last_ld = 0;
   bool pending = false;
   uint64_t list_cap = 0;
-  int variant = 0;  // kVariantL1 / kVariantRing (AFMM_BFORM=ring|l1)
+  int variant = 0;  // kVariantDyn / kVariantRing / kVariantL1 (AFMM_BFORM)
   // optional phase timing: ev[0] start, ev[1] before compute, ev[2] after compute, ev[3] end
   bool timing = false;
   bool timed_last = false;
@@ -263,16 +267,22 @@ template <class T>
 afmm_status launch_compute(afmm_context* c, const T* base, uint64_t kb_rows, uint64_t b_cols,
                            uint64_t ldb, uint32_t nrows, int32_t col0, int32_t ncols, T* out,
                            uint64_t ld_out, DevStatus* st, afmm_error* err) {
-  if (c->variant == kVariantRing) {
+  if (c->variant == kVariantRing || c->variant == kVariantDyn) {
     CUtensorMap tmap;
     if (!make_tmap<T>(&tmap, base, kb_rows, b_cols, ldb)) {
       set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: cuTensorMapEncodeTiled failed");
       return AFMM_ERR_CUDA;
     }
-    CK(afmm_dev::launch_bform<T>(&tmap, c->lists.as<int2>(), c->list_cap,
-                                 c->counts.as<uint32_t>(), nrows, col0, ncols, (uint32_t)kb_rows,
-                                 out, ld_out, st, c->stream),
-       "bform");
+    if (c->variant == kVariantDyn)
+      CK(afmm_dev::launch_bform_dyn<T>(&tmap, c->lists.as<int2>(), c->list_cap,
+                                       c->counts.as<uint32_t>(), nrows, col0, ncols,
+                                       (uint32_t)kb_rows, out, ld_out, st, c->stream),
+         "bform_dyn");
+    else
+      CK(afmm_dev::launch_bform<T>(&tmap, c->lists.as<int2>(), c->list_cap,
+                                   c->counts.as<uint32_t>(), nrows, col0, ncols,
+                                   (uint32_t)kb_rows, out, ld_out, st, c->stream),
+         "bform");
   } else {
     CK(afmm_dev::launch_bform_l1<T>(base, ldb, c->lists.as<int2>(), c->list_cap,
                                     c->counts.as<uint32_t>(), nrows, col0, ncols, out, ld_out, st,
