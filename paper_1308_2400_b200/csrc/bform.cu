@@ -1,4 +1,4 @@
-// bform.cu -- the repeated-addition kernel (sm_100a, CUDA cores only).
+// bform.cu -- the repeated-addition kernels (sm_100a, CUDA cores only).
 //
 // Computes Z' = R' (x) B' in the reference's order-preserving form: for every
 // output element, the terms arrive in increasing k and each is |rep|
@@ -8,28 +8,31 @@
 // same kernel on transposed operands (afmm_case_a(X,Y) = afmm_case_b(Y^T,X^T)^T,
 // same per-element add sequence).
 //
-// Structure (one CTA = CW consumer warps + 1 TMA producer warp):
+// k_bform (one CTA = CW consumer warps + 1 TMA producer warp):
 //   * CTA tile = CW output rows x TILE_N output columns; each consumer warp
-//     owns one output row, each lane C columns held in registers for the
-//     whole k sweep (register-resident Z tile).
+//     owns one output row, each lane 8*G fp32 / 4*G fp64 columns held in
+//     registers for the whole k sweep (register-resident Z tile).
 //   * The producer streams KB x TILE_N tiles of the base matrix B' through a
 //     STAGES-deep smem ring with cp.async.bulk.tensor (TMA) + mbarriers;
 //     the tile is shared by all CW rows of the CTA (CW-fold reuse from smem).
 //   * Each consumer walks its row's compacted (k, rep) list (built by the
 //     prepass, zero reps already skipped), waits for the stage holding row k,
-//     loads its C bases with conflict-free 128-bit LDS and runs the
-//     warp-uniform rep loop: |rep| x (C/2) FADD2 (fp32) or |rep| x C DADD
+//     loads its bases with conflict-free 128-bit LDS and runs the
+//     warp-uniform rep loop: |rep| x 4G FADD2 (fp32) or |rep| x 8G... DADD
 //     (fp64). The rep is uniform across the warp, so there is no divergence;
 //     zero bases are added as +0/-0, which is bit-neutral (the accumulator is
 //     never -0) and never counted.
 //   * Warps release a stage by arriving on its empty barrier; they may drift
-//     up to STAGES blocks apart, which absorbs per-row work imbalance.
+//     up to STAGES blocks apart.
 //
 // Issue-slot budget: FADD2 and DADD occupy their pipe for 2 cycles per warp
 // instruction, so one non-FP instruction per FP instruction issues for free.
-// The entry path therefore uses only ALU/LSU instructions (SHF/LOP3/LEA, LDS,
-// SHFL; sign flips by LOP3), and the rep loop has no predicated FP tail
-// (a predicated-off FADD2 still occupies the pipe).
+// The entry path uses ALU/LSU instructions (SHF/LOP3, LDS, SHFL) and the rep
+// loop has no predicated FP tail (a predicated-off FADD2 still occupies the
+// pipe). The next entry's (k, rep) broadcast is issued before the current rep
+// loop so its shuffle latency is hidden. Wider tiles (G = 8: 1024 fp32
+// columns, 32 accumulators per lane) amortise the per-entry overhead over
+// twice the adds, which matters for small reps (tools/sweep.py).
 #include "common.cuh"
 #include "kernels.h"
 
@@ -39,32 +42,25 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-constexpr int KB = 8;        // k rows per stage
-constexpr int STAGES = 6;    // smem ring depth
-constexpr int CW = 16;       // consumer warps (output rows) per CTA
-constexpr int ROW_BYTES = 2048;  // bytes of one k row of the tile: TILE_N * sizeof(T)
-// A TMA box is at most 256 elements wide, so a stage is NBOX boxes of
+constexpr int KB = 8;  // k rows per stage
+// A TMA box is at most 256 elements wide, so a stage is G/2 boxes of
 // KB x BOX_BYTES laid out box-major: [box][k row][BOX_BYTES].
 constexpr int BOX_BYTES = 1024;
-constexpr int NBOX = ROW_BYTES / BOX_BYTES;
-constexpr int STAGE_BYTES = KB * ROW_BYTES;
-constexpr int G = ROW_BYTES / 32 / 16;  // 128-bit vectors per lane per k row (= 4)
 
-// smem byte offset of vector group g (0..G-1) of a k row, relative to the row's
-// address in box 0 (the 512-byte warp-wide groups are two per box row).
+// smem byte offset of 128-bit group g of a k row, relative to the row's address
+// in box 0 (each 1 KB box row holds two warp-wide 512-byte groups).
 __device__ __forceinline__ constexpr uint32_t group_off(int g) {
   return (uint32_t)((g >> 1) * KB * BOX_BYTES + (g & 1) * 512);
 }
 
-template <class T>
-struct BformCfg {
-  static constexpr int TILE_N = ROW_BYTES / sizeof(T);     // 512 fp32 / 256 fp64 columns
-  static constexpr int BOX_N = BOX_BYTES / sizeof(T);      // 256 fp32 / 128 fp64 columns
+template <class T, int G>
+struct Geo {
+  static constexpr int ROW_BYTES = G * 512;                // one k row of the CTA tile
+  static constexpr int STAGE_BYTES = KB * ROW_BYTES;
+  static constexpr int TILE_N = ROW_BYTES / sizeof(T);     // columns per CTA
+  static constexpr int BOX_N = BOX_BYTES / sizeof(T);      // columns per TMA box
+  static constexpr int NBOX = ROW_BYTES / BOX_BYTES;
 };
-
-__host__ __device__ constexpr size_t bform_smem_bytes() {
-  return 1024 /*alignment slack*/ + (size_t)STAGES * STAGE_BYTES + 2 * STAGES * sizeof(uint64_t);
-}
 
 __device__ __forceinline__ float4 lds128f(uint32_t addr) {
   float4 v;
@@ -80,18 +76,31 @@ __device__ __forceinline__ double2 lds128d(uint32_t addr) {
   return v;
 }
 
-__device__ __forceinline__ float negf(float x) {
-  return __int_as_float(__float_as_int(x) ^ 0x80000000);  // LOP3, exact -x
+__device__ __forceinline__ void sts128(uint32_t addr, float a, float b, float c, float d) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
+}
+__device__ __forceinline__ void sts128d(uint32_t addr, double a, double b) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(a), "d"(b) : "memory");
 }
 
+__device__ __forceinline__ float negf(float x) {
+  return __int_as_float(__float_as_int(x) ^ 0x80000000);  // exact -x
+}
 __device__ __forceinline__ double negd(double x) {
   return __longlong_as_double(__double_as_longlong(x) ^ 0x8000000000000000ll);
 }
 
-// Lane l owns, for g = 0..G-1, the 16-byte column group at byte g*512 + l*16
-// of each staged k row: every 128-bit LDS across the warp reads 512
-// contiguous bytes (no bank conflict).
-struct AccF32 {
+// Lane l owns, for g = 0..G-1, the 16-byte column group at byte
+// (g>>1)*KB*BOX_BYTES + (g&1)*512 + l*16 of each staged k row: every 128-bit
+// LDS across the warp reads 512 contiguous bytes (no bank conflict). In
+// output columns that is tile_col + g*128 + 4l (fp32) / g*64 + 2l (fp64).
+template <class T, int G>
+struct Acc;
+
+template <int G>
+struct Acc<float, G> {
   float2 a[2 * G];
   __device__ __forceinline__ void zero() {
 #pragma unroll
@@ -127,8 +136,21 @@ struct AccF32 {
       t -= 1;
     }
   }
+  __device__ __forceinline__ void save(uint32_t z) const {
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      sts128(z + g * 512, a[2 * g].x, a[2 * g].y, a[2 * g + 1].x, a[2 * g + 1].y);
+  }
+  __device__ __forceinline__ void load(uint32_t z) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float4 v = lds128f(z + g * 512);
+      a[2 * g] = make_float2(v.x, v.y);
+      a[2 * g + 1] = make_float2(v.z, v.w);
+    }
+  }
   __device__ __forceinline__ void store(float* out_row, int32_t oc0, int32_t ncols, uint32_t lane,
-                                        bool vec_ok) {
+                                        bool vec_ok) const {
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const int32_t c = oc0 + g * 128 + 4 * (int32_t)lane;
@@ -144,7 +166,8 @@ struct AccF32 {
   }
 };
 
-struct AccF64 {
+template <int G>
+struct Acc<double, G> {
   double a[2 * G];
   __device__ __forceinline__ void zero() {
 #pragma unroll
@@ -179,8 +202,20 @@ struct AccF64 {
       t -= 1;
     }
   }
+  __device__ __forceinline__ void save(uint32_t z) const {
+#pragma unroll
+    for (int g = 0; g < G; ++g) sts128d(z + g * 512, a[2 * g], a[2 * g + 1]);
+  }
+  __device__ __forceinline__ void load(uint32_t z) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const double2 v = lds128d(z + g * 512);
+      a[2 * g] = v.x;
+      a[2 * g + 1] = v.y;
+    }
+  }
   __device__ __forceinline__ void store(double* out_row, int32_t oc0, int32_t ncols,
-                                        uint32_t lane, bool vec_ok) {
+                                        uint32_t lane, bool vec_ok) const {
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const int32_t c = oc0 + g * 64 + 2 * (int32_t)lane;
@@ -194,38 +229,55 @@ struct AccF64 {
   }
 };
 
-template <class T>
-struct AccOf;
-template <>
-struct AccOf<float> {
-  using type = AccF32;
-};
-template <>
-struct AccOf<double> {
-  using type = AccF64;
-};
+template <class T, int G, int STAGES>
+__host__ __device__ constexpr size_t ring_smem_bytes() {
+  return 1024 /*alignment slack*/ + (size_t)STAGES * Geo<T, G>::STAGE_BYTES +
+         2 * STAGES * sizeof(uint64_t);
+}
+
+// TMA producer loop (one elected thread): block kb goes to slot kb % STAGES
+// after all consumers released the block STAGES earlier.
+template <class T, int G, int STAGES>
+__device__ __forceinline__ void produce(const CUtensorMap* tmap, unsigned char* ring,
+                                        uint64_t* full, uint64_t* empty, int32_t col, uint32_t nkb) {
+  using Gm = Geo<T, G>;
+  prefetch_tensormap(tmap);
+  uint32_t slot = 0, phase = 0;
+  for (uint32_t kb = 0; kb < nkb; ++kb) {
+    if (kb >= STAGES) mbar_wait(&empty[slot], phase ^ 1);
+    mbar_arrive_expect_tx(&full[slot], (uint32_t)Gm::STAGE_BYTES);
+#pragma unroll
+    for (int h = 0; h < Gm::NBOX; ++h)
+      tma_load_2d(ring + slot * Gm::STAGE_BYTES + h * KB * BOX_BYTES, tmap, &full[slot],
+                  col + h * Gm::BOX_N, (int32_t)(kb * KB));
+    if (++slot == STAGES) {
+      slot = 0;
+      phase ^= 1;
+    }
+  }
+}
 
 // lists: row b's entries at lists[b * cap .. b * cap + counts[b]) in increasing k.
 // Output row b, column (col0 + c) -> out[b * ld_out + c], c < ncols.
-template <class T>
-__global__ void __launch_bounds__((CW + 1) * 32, 2)
+template <class T, int G, int CW, int STAGES, int MINB>
+__global__ void __launch_bounds__((CW + 1) * 32, MINB)
     k_bform(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ lists,
             uint64_t cap, const uint32_t* __restrict__ counts, uint32_t nrows, int32_t col0,
             int32_t ncols, uint32_t nkb, T* __restrict__ out, uint64_t ld_out, int vec_ok,
             const DevStatus* __restrict__ st) {
-  using Cfg = BformCfg<T>;
+  using Gm = Geo<T, G>;
   extern __shared__ unsigned char smem_raw[];
   // 1024-byte aligned ring; pointer arithmetic on the smem pointer itself keeps
   // the shared address space visible to the compiler.
   unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(base + STAGES * STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + STAGES * Gm::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   const uint32_t ring = smem_u32(base);
 
   if (status_failed(st)) return;  // validation failed: compute nothing (kernels.hpp:115,144)
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t tile_c = blockIdx.y * Cfg::TILE_N;  // relative to col0
+  const int32_t tile_c = blockIdx.y * Gm::TILE_N;  // relative to col0
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -237,23 +289,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 2)
   __syncthreads();
 
   if (warp == CW) {
-    // ---- TMA producer ----
-    if (lane == 0) {
-      prefetch_tensormap(&tmap);
-      uint32_t slot = 0, phase = 0;
-      for (uint32_t kb = 0; kb < nkb; ++kb) {
-        if (kb >= STAGES) mbar_wait(&empty[slot], phase ^ 1);
-        mbar_arrive_expect_tx(&full[slot], (uint32_t)STAGE_BYTES);
-#pragma unroll
-        for (int h = 0; h < NBOX; ++h)
-          tma_load_2d(base + slot * STAGE_BYTES + h * KB * BOX_BYTES, &tmap, &full[slot],
-                      col0 + tile_c + h * Cfg::BOX_N, (int32_t)(kb * KB));
-        if (++slot == STAGES) {
-          slot = 0;
-          phase ^= 1;
-        }
-      }
-    }
+    if (lane == 0) produce<T, G, STAGES>(&tmap, base, full, empty, col0 + tile_c, nkb);
     return;
   }
 
@@ -262,7 +298,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 2)
   const uint32_t cnt = b < nrows ? counts[b] : 0u;
   const int2* lst = lists + (uint64_t)(b < nrows ? b : 0) * cap;
 
-  typename AccOf<T>::type acc;
+  Acc<T, G> acc;
   acc.zero();
 
   // (kb_cur, slot, phase): the k block currently held, its ring slot and the
@@ -274,30 +310,36 @@ __global__ void __launch_bounds__((CW + 1) * 32, 2)
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
     ++kb_cur;
-    stage_addr += STAGE_BYTES;
+    stage_addr += Gm::STAGE_BYTES;
     if (++slot == STAGES) {
       slot = 0;
       phase ^= 1;
-      stage_addr -= STAGES * STAGE_BYTES;
+      stage_addr -= STAGES * Gm::STAGE_BYTES;
     }
   };
   mbar_wait(&full[0], 0);
   int2 cur = lane < cnt ? lst[lane] : make_int2(0, 0);
-  for (uint32_t p = 0; p < cnt; p += 32) {
-    const uint32_t pn = p + 32 + lane;
-    const int2 nxt = pn < cnt ? lst[pn] : make_int2(0, 0);  // prefetch next chunk
-    const uint32_t m = cnt - p < 32u ? cnt - p : 32u;
-    for (uint32_t q = 0; q < m; ++q) {
-      const uint32_t k = (uint32_t)__shfl_sync(FULL, cur.x, q);
-      const int rep = __shfl_sync(FULL, cur.y, q);
-      const uint32_t kb = k / KB;
-      while (kb_cur < kb) {
-        advance();
-        mbar_wait(&full[slot], phase);
-      }
-      acc.run(stage_addr + (k % KB) * BOX_BYTES, rep);
+  int2 nxt = 32 + lane < cnt ? lst[32 + lane] : make_int2(0, 0);
+  // entry e = (k, rep) broadcast one entry ahead of its use
+  uint32_t k = (uint32_t)__shfl_sync(FULL, cur.x, 0);
+  int rep = __shfl_sync(FULL, cur.y, 0);
+  for (uint32_t e = 0; e < cnt; ++e) {
+    const uint32_t f = e + 1;
+    if ((f & 31u) == 0) {  // next entry starts a new chunk of 32
+      cur = nxt;
+      const uint32_t pn = f + 32 + lane;
+      nxt = pn < cnt ? lst[pn] : make_int2(0, 0);
     }
-    cur = nxt;
+    const uint32_t k_n = (uint32_t)__shfl_sync(FULL, cur.x, f & 31u);
+    const int rep_n = __shfl_sync(FULL, cur.y, f & 31u);
+    const uint32_t kb = k / KB;
+    while (kb_cur < kb) {
+      advance();
+      mbar_wait(&full[slot], phase);
+    }
+    acc.run(stage_addr + (k % KB) * BOX_BYTES, rep);
+    k = k_n;
+    rep = rep_n;
   }
   // release the remaining stages in order
   while (true) {
@@ -311,62 +353,26 @@ __global__ void __launch_bounds__((CW + 1) * 32, 2)
 
 // ---------------------------------------------------------------------------
 // k_bform_dyn: the same TMA ring, but the CTA's rows are not pinned to warps.
-//
-// ncu on k_bform showed ~9% of warp samples spinning on stage barriers: a
-// row's cumulative work is a random walk in k, and with one row per warp the
-// ring's slack (STAGES blocks) is regularly exhausted by the slowest warp.
-// Here the unit of work is an ITEM = (k block b, row w). Items are handed out
-// from a CTA-wide counter in b-major order, so any warp takes whichever row is
-// next; a row's accumulators live in registers for the duration of an item
-// and in a 16 x TILE_N smem tile between items. Per-row order is kept by a
-// per-row "next block" flag (item (w, b) starts only after (w, b-1) has
-// stored its accumulators), so every element still receives its terms in
-// increasing k, exactly as kernels.hpp:148-163.
+// The unit of work is an ITEM = (k block b, row w), handed out from a CTA-wide
+// counter in b-major order, so any warp takes whichever row is next; a row's
+// accumulators live in registers for the duration of an item and in a
+// ROWS x TILE_N smem tile between items. Per-row order is kept by a per-row
+// "next block" flag (item (w, b) starts only after (w, b-1) has stored its
+// accumulators), so every element still receives its terms in increasing k
+// (kernels.hpp:148-163). Measured: equal to k_bform for large reps, slower for
+// small ones (per-item overhead); kept as a selectable variant.
 // ---------------------------------------------------------------------------
 
+constexpr int DYN_G = 4;
 constexpr int DYN_STAGES = 4;  // power of two
 constexpr int DYN_ROWS = 16;   // rows per CTA (power of two)
 constexpr int DYN_CW = 16;     // consumer warps per CTA
-constexpr int ZS_BYTES = DYN_ROWS * ROW_BYTES;
 
-__host__ __device__ constexpr size_t bform_dyn_smem_bytes() {
-  return 1024 + (size_t)DYN_STAGES * STAGE_BYTES + ZS_BYTES + 2 * DYN_STAGES * sizeof(uint64_t) +
+template <class T>
+__host__ __device__ constexpr size_t dyn_smem_bytes() {
+  return 1024 + (size_t)DYN_STAGES * Geo<T, DYN_G>::STAGE_BYTES +
+         (size_t)DYN_ROWS * Geo<T, DYN_G>::ROW_BYTES + 2 * DYN_STAGES * sizeof(uint64_t) +
          (2 * DYN_ROWS + 4) * sizeof(uint32_t);
-}
-
-__device__ __forceinline__ void sts128(uint32_t addr, float a, float b, float c, float d) {
-  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c),
-               "f"(d)
-               : "memory");
-}
-__device__ __forceinline__ void sts128d(uint32_t addr, double a, double b) {
-  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(a), "d"(b) : "memory");
-}
-
-__device__ __forceinline__ void save_acc(const AccF32& acc, uint32_t z) {
-#pragma unroll
-  for (int g = 0; g < G; ++g)
-    sts128(z + g * 512, acc.a[2 * g].x, acc.a[2 * g].y, acc.a[2 * g + 1].x, acc.a[2 * g + 1].y);
-}
-__device__ __forceinline__ void load_acc(AccF32& acc, uint32_t z) {
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    const float4 v = lds128f(z + g * 512);
-    acc.a[2 * g] = make_float2(v.x, v.y);
-    acc.a[2 * g + 1] = make_float2(v.z, v.w);
-  }
-}
-__device__ __forceinline__ void save_acc(const AccF64& acc, uint32_t z) {
-#pragma unroll
-  for (int g = 0; g < G; ++g) sts128d(z + g * 512, acc.a[2 * g], acc.a[2 * g + 1]);
-}
-__device__ __forceinline__ void load_acc(AccF64& acc, uint32_t z) {
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    const double2 v = lds128d(z + g * 512);
-    acc.a[2 * g] = v.x;
-    acc.a[2 * g + 1] = v.y;
-  }
 }
 
 template <class T>
@@ -375,11 +381,11 @@ __global__ void __launch_bounds__((DYN_CW + 1) * 32, 2)
                 uint64_t cap, const uint32_t* __restrict__ counts, uint32_t nrows, int32_t col0,
                 int32_t ncols, uint32_t nkb, T* __restrict__ out, uint64_t ld_out, int vec_ok,
                 const DevStatus* __restrict__ st) {
-  using Cfg = BformCfg<T>;
+  using Gm = Geo<T, DYN_G>;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  unsigned char* zs = base + DYN_STAGES * STAGE_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(zs + ZS_BYTES);
+  unsigned char* zs = base + DYN_STAGES * Gm::STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(zs + DYN_ROWS * Gm::ROW_BYTES);
   uint64_t* empty = full + DYN_STAGES;
   volatile uint32_t* row_next = reinterpret_cast<volatile uint32_t*>(empty + DYN_STAGES);
   uint32_t* cursor = const_cast<uint32_t*>(row_next + DYN_ROWS);
@@ -387,10 +393,10 @@ __global__ void __launch_bounds__((DYN_CW + 1) * 32, 2)
   const uint32_t ring = smem_u32(base);
   const uint32_t zs_addr = smem_u32(zs);
 
-  if (status_failed(st)) return;  // validation failed: compute nothing (kernels.hpp:115,144)
+  if (status_failed(st)) return;
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t tile_c = blockIdx.y * Cfg::TILE_N;
+  const int32_t tile_c = blockIdx.y * Gm::TILE_N;
   const uint32_t row0 = blockIdx.x * DYN_ROWS;
   const uint32_t rows_here = nrows - row0 < (uint32_t)DYN_ROWS ? nrows - row0 : DYN_ROWS;
 
@@ -409,25 +415,12 @@ __global__ void __launch_bounds__((DYN_CW + 1) * 32, 2)
   __syncthreads();
 
   if (warp == DYN_CW) {
-    // ---- TMA producer ----
-    if (lane == 0) {
-      prefetch_tensormap(&tmap);
-      for (uint32_t kb = 0; kb < nkb; ++kb) {
-        const uint32_t slot = kb & (DYN_STAGES - 1);
-        if (kb >= DYN_STAGES) mbar_wait(&empty[slot], ((kb / DYN_STAGES) & 1) ^ 1);
-        mbar_arrive_expect_tx(&full[slot], (uint32_t)STAGE_BYTES);
-#pragma unroll
-        for (int h = 0; h < NBOX; ++h)
-          tma_load_2d(base + slot * STAGE_BYTES + h * KB * BOX_BYTES, &tmap, &full[slot],
-                      col0 + tile_c + h * Cfg::BOX_N, (int32_t)(kb * KB));
-      }
-    }
+    if (lane == 0) produce<T, DYN_G, DYN_STAGES>(&tmap, base, full, empty, col0 + tile_c, nkb);
     return;
   }
 
-  // ---- consumers: items (b, w) in b-major order ----
   const uint32_t total = nkb * DYN_ROWS;
-  typename AccOf<T>::type acc;
+  Acc<T, DYN_G> acc;
   while (true) {
     uint32_t id = 0;
     if (lane == 0) id = atomicAdd(item_ctr, 1u);
@@ -437,22 +430,20 @@ __global__ void __launch_bounds__((DYN_CW + 1) * 32, 2)
     const uint32_t slot = b & (DYN_STAGES - 1);
     mbar_wait(&full[slot], (b / DYN_STAGES) & 1);
     if (w < rows_here) {
-      // per-row order: (w, b-1) must have stored its accumulators
       while (row_next[w] != b) {
       }
       __threadfence_block();
-      const uint32_t zrow = zs_addr + w * ROW_BYTES + lane * 16;
+      const uint32_t zrow = zs_addr + w * Gm::ROW_BYTES + lane * 16;
       if (b == 0) acc.zero();
-      else load_acc(acc, zrow);
+      else acc.load(zrow);
       const uint32_t r = row0 + w;
       const uint32_t cnt = counts[r];
       const int2* lst = lists + (uint64_t)r * cap;
       uint32_t p = cursor[w];
       const uint32_t kend = (b + 1) * KB;
-      const uint32_t stage_addr = ring + slot * STAGE_BYTES + lane * 16;
+      const uint32_t stage_addr = ring + slot * Gm::STAGE_BYTES + lane * 16;
       while (p < cnt) {
         const int2 e = p + lane < cnt ? lst[p + lane] : make_int2(0x7fffffff, 0);
-        // entries of this block among the 32 fetched (lists are sorted by k)
         const unsigned in_blk = __ballot_sync(FULL, (uint32_t)e.x < kend);
         const uint32_t m = __popc(in_blk);
         for (uint32_t q = 0; q < m; ++q) {
@@ -463,7 +454,7 @@ __global__ void __launch_bounds__((DYN_CW + 1) * 32, 2)
         p += m;
         if (m < 32) break;
       }
-      save_acc(acc, zrow);
+      acc.save(zrow);
       __syncwarp();
       if (lane == 0) {
         cursor[w] = p;
@@ -475,22 +466,57 @@ __global__ void __launch_bounds__((DYN_CW + 1) * 32, 2)
     if (lane == 0) mbar_arrive(&empty[slot]);
   }
 
-  // all items done -> write the Z tile out (named barrier over the consumers)
   asm volatile("bar.sync 1, %0;" ::"r"(DYN_CW * 32) : "memory");
   for (uint32_t w = warp; w < rows_here; w += DYN_CW) {
-    load_acc(acc, zs_addr + w * ROW_BYTES + lane * 16);
+    acc.load(zs_addr + w * Gm::ROW_BYTES + lane * 16);
     acc.store(out + (uint64_t)(row0 + w) * ld_out, tile_c, ncols, lane, vec_ok != 0);
   }
 }
 
+template <class T, int G, int CW, int STAGES, int MINB>
+cudaError_t launch_ring(const CUtensorMap* tmap, const int2* lists, uint64_t cap,
+                        const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,
+                        uint32_t nk, T* out, uint64_t ld_out, const DevStatus* st,
+                        cudaStream_t s) {
+  auto kern = k_bform<T, G, CW, STAGES, MINB>;
+  const size_t smem = ring_smem_bytes<T, G, STAGES>();
+  // set on every call: the attribute is per device and costs ~1 us
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  const uint32_t nkb = (nk + KB - 1) / KB;
+  const bool vec_ok = (ld_out * sizeof(T)) % 16 == 0 &&
+                      (reinterpret_cast<uintptr_t>(out) % 16) == 0;
+  dim3 grid((nrows + CW - 1) / CW, (ncols + Geo<T, G>::TILE_N - 1) / Geo<T, G>::TILE_N);
+  kern<<<grid, (CW + 1) * 32, smem, s>>>(*tmap, lists, cap, counts, nrows, col0, ncols, nkb, out,
+                                         ld_out, vec_ok ? 1 : 0, st);
+  note_launch();
+  return cudaGetLastError();
+}
+
 }  // namespace
+
+int bform_box_bytes() { return BOX_BYTES; }
+int bform_kb() { return KB; }
+
+template <class T>
+cudaError_t launch_bform(int shape, const CUtensorMap* tmap, const int2* lists, uint64_t cap,
+                         const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,
+                         uint32_t nk, T* out, uint64_t ld_out, const DevStatus* st,
+                         cudaStream_t s) {
+  if (shape == kShapeWide)  // 1024 fp32 / 512 fp64 columns, 1 CTA per SM
+    return launch_ring<T, 8, 16, 6, 1>(tmap, lists, cap, counts, nrows, col0, ncols, nk, out,
+                                       ld_out, st, s);
+  return launch_ring<T, 4, 16, 6, 2>(tmap, lists, cap, counts, nrows, col0, ncols, nk, out,
+                                     ld_out, st, s);
+}
 
 template <class T>
 cudaError_t launch_bform_dyn(const CUtensorMap* tmap, const int2* lists, uint64_t cap,
                              const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,
                              uint32_t nk, T* out, uint64_t ld_out, const DevStatus* st,
                              cudaStream_t s) {
-  const size_t smem = bform_dyn_smem_bytes();
+  const size_t smem = dyn_smem_bytes<T>();
   cudaError_t e = cudaFuncSetAttribute(k_bform_dyn<T>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -498,7 +524,7 @@ cudaError_t launch_bform_dyn(const CUtensorMap* tmap, const int2* lists, uint64_
   const bool vec_ok = (ld_out * sizeof(T)) % 16 == 0 &&
                       (reinterpret_cast<uintptr_t>(out) % 16) == 0;
   dim3 grid((nrows + DYN_ROWS - 1) / DYN_ROWS,
-            (ncols + BformCfg<T>::TILE_N - 1) / BformCfg<T>::TILE_N);
+            (ncols + Geo<T, DYN_G>::TILE_N - 1) / Geo<T, DYN_G>::TILE_N);
   k_bform_dyn<T><<<grid, (DYN_CW + 1) * 32, smem, s>>>(*tmap, lists, cap, counts, nrows, col0,
                                                        ncols, nkb, out, ld_out, vec_ok ? 1 : 0,
                                                        st);
@@ -506,6 +532,12 @@ cudaError_t launch_bform_dyn(const CUtensorMap* tmap, const int2* lists, uint64_
   return cudaGetLastError();
 }
 
+template cudaError_t launch_bform<float>(int, const CUtensorMap*, const int2*, uint64_t,
+                                         const uint32_t*, uint32_t, int32_t, int32_t, uint32_t,
+                                         float*, uint64_t, const DevStatus*, cudaStream_t);
+template cudaError_t launch_bform<double>(int, const CUtensorMap*, const int2*, uint64_t,
+                                          const uint32_t*, uint32_t, int32_t, int32_t, uint32_t,
+                                          double*, uint64_t, const DevStatus*, cudaStream_t);
 template cudaError_t launch_bform_dyn<float>(const CUtensorMap*, const int2*, uint64_t,
                                              const uint32_t*, uint32_t, int32_t, int32_t,
                                              uint32_t, float*, uint64_t, const DevStatus*,
@@ -514,53 +546,5 @@ template cudaError_t launch_bform_dyn<double>(const CUtensorMap*, const int2*, u
                                               const uint32_t*, uint32_t, int32_t, int32_t,
                                               uint32_t, double*, uint64_t, const DevStatus*,
                                               cudaStream_t);
-
-template <class T>
-int bform_tile_n() {
-  return BformCfg<T>::TILE_N;
-}
-
-template <class T>
-int bform_box_cols() {
-  return BformCfg<T>::BOX_N;
-}
-
-template <class T>
-int bform_kb() {
-  return KB;
-}
-
-template <class T>
-cudaError_t launch_bform(const CUtensorMap* tmap, const int2* lists, uint64_t cap,
-                         const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,
-                         uint32_t nk, T* out, uint64_t ld_out, const DevStatus* st,
-                         cudaStream_t s) {
-  const size_t smem = bform_smem_bytes();
-  // set on every call: the attribute is per device and costs ~1 us
-  cudaError_t e =
-      cudaFuncSetAttribute(k_bform<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  const uint32_t nkb = (nk + KB - 1) / KB;
-  const bool vec_ok = (ld_out * sizeof(T)) % 16 == 0 &&
-                      (reinterpret_cast<uintptr_t>(out) % 16) == 0;
-  dim3 grid((nrows + CW - 1) / CW, (ncols + BformCfg<T>::TILE_N - 1) / BformCfg<T>::TILE_N);
-  k_bform<T><<<grid, (CW + 1) * 32, smem, s>>>(*tmap, lists, cap, counts, nrows, col0, ncols, nkb,
-                                               out, ld_out, vec_ok ? 1 : 0, st);
-  note_launch();
-  return cudaGetLastError();
-}
-
-template int bform_box_cols<float>();
-template int bform_box_cols<double>();
-template int bform_tile_n<float>();
-template int bform_tile_n<double>();
-template int bform_kb<float>();
-template int bform_kb<double>();
-template cudaError_t launch_bform<float>(const CUtensorMap*, const int2*, uint64_t,
-                                         const uint32_t*, uint32_t, int32_t, int32_t, uint32_t,
-                                         float*, uint64_t, const DevStatus*, cudaStream_t);
-template cudaError_t launch_bform<double>(const CUtensorMap*, const int2*, uint64_t,
-                                          const uint32_t*, uint32_t, int32_t, int32_t, uint32_t,
-                                          double*, uint64_t, const DevStatus*, cudaStream_t);
 
 }  // namespace afmm_dev

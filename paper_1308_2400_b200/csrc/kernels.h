@@ -34,14 +34,17 @@ template <class T>
 void launch_transpose(const T* in, uint64_t ld_in, uint32_t rows, uint32_t cols, T* out,
                       uint64_t ld_out, cudaStream_t s);
 
-template <class T>
-int bform_tile_n();
-template <class T>
+// TMA geometry shared by the ring kernels: boxes of bform_kb() rows x
+// bform_box_bytes() bytes.
 int bform_kb();
+int bform_box_bytes();
+
+// k_bform tile shapes: narrow = 512 fp32 / 256 fp64 columns per CTA, 2 CTAs
+// per SM; wide = 1024 / 512 columns, 32 accumulators per lane, 1 CTA per SM.
+constexpr int kShapeNarrow = 0;
+constexpr int kShapeWide = 1;
 template <class T>
-int bform_box_cols();
-template <class T>
-cudaError_t launch_bform(const CUtensorMap* tmap, const int2* lists, uint64_t cap,
+cudaError_t launch_bform(int shape, const CUtensorMap* tmap, const int2* lists, uint64_t cap,
                          const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,
                          uint32_t nk, T* out, uint64_t ld_out, const DevStatus* st,
                          cudaStream_t s);

@@ -29,17 +29,19 @@ void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 namespace {
 
 constexpr uint64_t kNone = ~0ull;
-constexpr int kVariantDyn = 0;   // TMA smem ring + dynamic (block, row) items (bform.cu)
-constexpr int kVariantRing = 1;  // TMA smem ring, one row pinned per warp (bform.cu)
-constexpr int kVariantL1 = 2;    // decoupled warps, L1-cached base loads (bform_l1.cu)
+constexpr int kVariantWide = 0;  // TMA smem ring, 1024-column tiles (bform.cu, default)
+constexpr int kVariantRing = 1;  // TMA smem ring, 512-column tiles (bform.cu)
+constexpr int kVariantDyn = 2;   // TMA smem ring + dynamic (block, row) items (bform.cu)
+constexpr int kVariantL1 = 3;    // decoupled warps, L1-cached base loads (bform_l1.cu)
 
-// AFMM_BFORM=dyn|ring|l1 selects the repeated-addition kernel (all three are
-// bit-identical; tests/test_gpu_parity.py runs each). Default: dyn.
+// AFMM_BFORM=wide|ring|dyn|l1 selects the repeated-addition kernel (all are
+// bit-identical; tests/test_gpu_parity.py runs each).
 int variant_from_env() {
   const char* v = std::getenv("AFMM_BFORM");
   if (v && std::strcmp(v, "ring") == 0) return kVariantRing;
+  if (v && std::strcmp(v, "dyn") == 0) return kVariantDyn;
   if (v && std::strcmp(v, "l1") == 0) return kVariantL1;
-  return kVariantDyn;
+  return kVariantWide;
 }
 
 inline uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
@@ -95,8 +97,8 @@ bool make_tmap(CUtensorMap* map, const T* base, uint64_t rows, uint64_t cols, ui
   if (!fn) return false;
   const cuuint64_t gdim[2] = {cols, rows};
   const cuuint64_t gstride[1] = {ld * sizeof(T)};
-  const cuuint32_t box[2] = {(cuuint32_t)afmm_dev::bform_box_cols<T>(),
-                             (cuuint32_t)afmm_dev::bform_kb<T>()};
+  const cuuint32_t box[2] = {(cuuint32_t)(afmm_dev::bform_box_bytes() / sizeof(T)),
+                             (cuuint32_t)afmm_dev::bform_kb()};
   const cuuint32_t estride[2] = {1, 1};
   const CUtensorMapDataType dt =
       sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
@@ -124,7 +126,7 @@ struct afmm_context {
   uint64_t last_n = 0, last_ld = 0;
   bool pending = false;
   uint64_t list_cap = 0;
-  int variant = 0;  // kVariantDyn / kVariantRing / kVariantL1 (AFMM_BFORM)
+  int variant = 0;  // kVariant* (AFMM_BFORM)
   // optional phase timing: ev[0] start, ev[1] before compute, ev[2] after compute, ev[3] end
   bool timing = false;
   bool timed_last = false;
@@ -267,7 +269,7 @@ template <class T>
 afmm_status launch_compute(afmm_context* c, const T* base, uint64_t kb_rows, uint64_t b_cols,
                            uint64_t ldb, uint32_t nrows, int32_t col0, int32_t ncols, T* out,
                            uint64_t ld_out, DevStatus* st, afmm_error* err) {
-  if (c->variant == kVariantRing || c->variant == kVariantDyn) {
+  if (c->variant != kVariantL1) {
     CUtensorMap tmap;
     if (!make_tmap<T>(&tmap, base, kb_rows, b_cols, ldb)) {
       set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: cuTensorMapEncodeTiled failed");
@@ -279,9 +281,10 @@ afmm_status launch_compute(afmm_context* c, const T* base, uint64_t kb_rows, uin
                                        (uint32_t)kb_rows, out, ld_out, st, c->stream),
          "bform_dyn");
     else
-      CK(afmm_dev::launch_bform<T>(&tmap, c->lists.as<int2>(), c->list_cap,
-                                   c->counts.as<uint32_t>(), nrows, col0, ncols,
-                                   (uint32_t)kb_rows, out, ld_out, st, c->stream),
+      CK(afmm_dev::launch_bform<T>(
+             c->variant == kVariantWide ? afmm_dev::kShapeWide : afmm_dev::kShapeNarrow, &tmap,
+             c->lists.as<int2>(), c->list_cap, c->counts.as<uint32_t>(), nrows, col0, ncols,
+             (uint32_t)kb_rows, out, ld_out, st, c->stream),
          "bform");
   } else {
     CK(afmm_dev::launch_bform_l1<T>(base, ldb, c->lists.as<int2>(), c->list_cap,

@@ -197,7 +197,7 @@ def test_full_size_row_sample_bit_exact(cuda, oracle, name, kw):
     ctx.close()
 
 
-@pytest.mark.parametrize("variant", ["dyn", "ring", "l1"])
+@pytest.mark.parametrize("variant", ["wide", "ring", "dyn", "l1"])
 def test_both_kernel_variants_bit_exact(cuda, oracle, variant, monkeypatch):
     """k_bform (TMA smem ring) and k_bform_l1 (decoupled warps) give identical bits."""
     import torch
