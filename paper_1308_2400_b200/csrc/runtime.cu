@@ -29,7 +29,8 @@ void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 namespace {
 
 constexpr uint64_t kNone = ~0ull;
-constexpr int kVariantWide = 0;  // TMA smem ring, 1024-column tiles (bform.cu, default)
+constexpr int kVariantAuto = -1; // wide when the problem fills the GPU with wide tiles, else ring
+constexpr int kVariantWide = 0;  // TMA smem ring, 1024-column tiles (bform.cu)
 constexpr int kVariantRing = 1;  // TMA smem ring, 512-column tiles (bform.cu)
 constexpr int kVariantDyn = 2;   // TMA smem ring + dynamic (block, row) items (bform.cu)
 constexpr int kVariantL1 = 3;    // decoupled warps, L1-cached base loads (bform_l1.cu)
@@ -41,7 +42,8 @@ int variant_from_env() {
   if (v && std::strcmp(v, "ring") == 0) return kVariantRing;
   if (v && std::strcmp(v, "dyn") == 0) return kVariantDyn;
   if (v && std::strcmp(v, "l1") == 0) return kVariantL1;
-  return kVariantWide;
+  if (v && std::strcmp(v, "wide") == 0) return kVariantWide;
+  return kVariantAuto;
 }
 
 inline uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
@@ -280,12 +282,17 @@ afmm_status launch_compute(afmm_context* c, const T* base, uint64_t kb_rows, uin
                                        c->counts.as<uint32_t>(), nrows, col0, ncols,
                                        (uint32_t)kb_rows, out, ld_out, st, c->stream),
          "bform_dyn");
-    else
+    else {
+      // wide tiles (1 CTA/SM, 16 rows x 4 KB) need >= ~2 waves of CTAs to pay off
+      const uint64_t wide_ctas = (nrows + 15) / 16 * ((ncols * sizeof(T) + 4095) / 4096);
+      const bool wide = c->variant == kVariantWide ||
+                        (c->variant == kVariantAuto && wide_ctas >= 2 * 148);
       CK(afmm_dev::launch_bform<T>(
-             c->variant == kVariantWide ? afmm_dev::kShapeWide : afmm_dev::kShapeNarrow, &tmap,
+             wide ? afmm_dev::kShapeWide : afmm_dev::kShapeNarrow, &tmap,
              c->lists.as<int2>(), c->list_cap, c->counts.as<uint32_t>(), nrows, col0, ncols,
              (uint32_t)kb_rows, out, ld_out, st, c->stream),
          "bform");
+    }
   } else {
     CK(afmm_dev::launch_bform_l1<T>(base, ldb, c->lists.as<int2>(), c->list_cap,
                                     c->counts.as<uint32_t>(), nrows, col0, ncols, out, ld_out, st,
