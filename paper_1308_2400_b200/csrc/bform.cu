@@ -235,11 +235,13 @@ __host__ __device__ constexpr size_t ring_smem_bytes() {
          2 * STAGES * sizeof(uint64_t);
 }
 
-// TMA producer loop (one elected thread): block kb goes to slot kb % STAGES
-// after all consumers released the block STAGES earlier.
+// TMA producer loop (one elected thread): the i-th block of the slice
+// (k block kb_lo + i) goes to slot i % STAGES after all consumers released
+// the block STAGES earlier.
 template <class T, int G, int STAGES>
 __device__ __forceinline__ void produce(const CUtensorMap* tmap, unsigned char* ring,
-                                        uint64_t* full, uint64_t* empty, int32_t col, uint32_t nkb) {
+                                        uint64_t* full, uint64_t* empty, int32_t col, uint32_t nkb,
+                                        uint32_t kb_lo = 0) {
   using Gm = Geo<T, G>;
   prefetch_tensormap(tmap);
   uint32_t slot = 0, phase = 0;
@@ -249,7 +251,7 @@ __device__ __forceinline__ void produce(const CUtensorMap* tmap, unsigned char* 
 #pragma unroll
     for (int h = 0; h < Gm::NBOX; ++h)
       tma_load_2d(ring + slot * Gm::STAGE_BYTES + h * KB * BOX_BYTES, tmap, &full[slot],
-                  col + h * Gm::BOX_N, (int32_t)(kb * KB));
+                  col + h * Gm::BOX_N, (int32_t)((kb_lo + kb) * KB));
     if (++slot == STAGES) {
       slot = 0;
       phase ^= 1;
@@ -257,14 +259,29 @@ __device__ __forceinline__ void produce(const CUtensorMap* tmap, unsigned char* 
   }
 }
 
+// First list index with k >= key (lists are sorted by k); every lane computes
+// the same answer from broadcast loads.
+__device__ __forceinline__ uint32_t lower_bound_k(const int2* lst, uint32_t cnt, uint32_t key) {
+  uint32_t lo = 0, hi = cnt;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if ((uint32_t)lst[mid].x < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
 // lists: row b's entries at lists[b * cap .. b * cap + counts[b]) in increasing k.
 // Output row b, column (col0 + c) -> out[b * ld_out + c], c < ncols.
+// k slice: blockIdx.z selects slice z = [z*slice_blocks, (z+1)*slice_blocks)
+// of the nkb_total k blocks and writes to out + z * slice_stride (fast-mode
+// split-k; one slice = the whole k range in order-preserving mode).
 template <class T, int G, int CW, int STAGES, int MINB>
 __global__ void __launch_bounds__((CW + 1) * 32, MINB)
     k_bform(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ lists,
             uint64_t cap, const uint32_t* __restrict__ counts, uint32_t nrows, int32_t col0,
-            int32_t ncols, uint32_t nkb, T* __restrict__ out, uint64_t ld_out, int vec_ok,
-            const DevStatus* __restrict__ st) {
+            int32_t ncols, uint32_t nkb_total, uint32_t slice_blocks, uint64_t slice_stride,
+            T* __restrict__ out, uint64_t ld_out, int vec_ok, const DevStatus* __restrict__ st) {
   using Gm = Geo<T, G>;
   extern __shared__ unsigned char smem_raw[];
   // 1024-byte aligned ring; pointer arithmetic on the smem pointer itself keeps
@@ -278,6 +295,10 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t tile_c = blockIdx.y * Gm::TILE_N;  // relative to col0
+  const uint32_t kb_lo = blockIdx.z * slice_blocks;
+  const uint32_t kb_hi = min(nkb_total, kb_lo + slice_blocks);
+  const uint32_t nkb = kb_hi - kb_lo;
+  out += blockIdx.z * slice_stride;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -289,14 +310,21 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
   __syncthreads();
 
   if (warp == CW) {
-    if (lane == 0) produce<T, G, STAGES>(&tmap, base, full, empty, col0 + tile_c, nkb);
+    if (lane == 0) produce<T, G, STAGES>(&tmap, base, full, empty, col0 + tile_c, nkb, kb_lo);
     return;
   }
 
   // ---- consumers: one output row per warp ----
   const uint32_t b = blockIdx.x * CW + warp;
-  const uint32_t cnt = b < nrows ? counts[b] : 0u;
+  uint32_t cnt = b < nrows ? counts[b] : 0u;
   const int2* lst = lists + (uint64_t)(b < nrows ? b : 0) * cap;
+  if (gridDim.z > 1) {
+    // this slice's entries: [lower_bound(kb_lo*KB), lower_bound(kb_hi*KB))
+    const uint32_t p0 = lower_bound_k(lst, cnt, kb_lo * KB);
+    const uint32_t p1 = kb_hi == nkb_total ? cnt : lower_bound_k(lst, cnt, kb_hi * KB);
+    lst += p0;
+    cnt = p1 - p0;
+  }
 
   Acc<T, G> acc;
   acc.zero();
@@ -332,7 +360,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
     }
     const uint32_t k_n = (uint32_t)__shfl_sync(FULL, cur.x, f & 31u);
     const int rep_n = __shfl_sync(FULL, cur.y, f & 31u);
-    const uint32_t kb = k / KB;
+    const uint32_t kb = k / KB - kb_lo;  // block index within the slice
     while (kb_cur < kb) {
       advance();
       mbar_wait(&full[slot], phase);
@@ -476,8 +504,8 @@ __global__ void __launch_bounds__((DYN_CW + 1) * 32, 2)
 template <class T, int G, int CW, int STAGES, int MINB>
 cudaError_t launch_ring(const CUtensorMap* tmap, const int2* lists, uint64_t cap,
                         const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,
-                        uint32_t nk, T* out, uint64_t ld_out, const DevStatus* st,
-                        cudaStream_t s) {
+                        uint32_t nk, uint32_t* splits, uint64_t slice_stride, T* out,
+                        uint64_t ld_out, const DevStatus* st, cudaStream_t s) {
   auto kern = k_bform<T, G, CW, STAGES, MINB>;
   const size_t smem = ring_smem_bytes<T, G, STAGES>();
   // set on every call: the attribute is per device and costs ~1 us
@@ -485,11 +513,17 @@ cudaError_t launch_ring(const CUtensorMap* tmap, const int2* lists, uint64_t cap
                                        (int)smem);
   if (e != cudaSuccess) return e;
   const uint32_t nkb = (nk + KB - 1) / KB;
+  uint32_t want = *splits < 1 ? 1 : *splits;
+  if (want > nkb) want = nkb;
+  const uint32_t slice_blocks = (nkb + want - 1) / want;
+  *splits = (nkb + slice_blocks - 1) / slice_blocks;
   const bool vec_ok = (ld_out * sizeof(T)) % 16 == 0 &&
-                      (reinterpret_cast<uintptr_t>(out) % 16) == 0;
-  dim3 grid((nrows + CW - 1) / CW, (ncols + Geo<T, G>::TILE_N - 1) / Geo<T, G>::TILE_N);
-  kern<<<grid, (CW + 1) * 32, smem, s>>>(*tmap, lists, cap, counts, nrows, col0, ncols, nkb, out,
-                                         ld_out, vec_ok ? 1 : 0, st);
+                      (reinterpret_cast<uintptr_t>(out) % 16) == 0 &&
+                      (slice_stride * sizeof(T)) % 16 == 0;
+  dim3 grid((nrows + CW - 1) / CW, (ncols + Geo<T, G>::TILE_N - 1) / Geo<T, G>::TILE_N, *splits);
+  kern<<<grid, (CW + 1) * 32, smem, s>>>(*tmap, lists, cap, counts, nrows, col0, ncols, nkb,
+                                         slice_blocks, slice_stride, out, ld_out,
+                                         vec_ok ? 1 : 0, st);
   note_launch();
   return cudaGetLastError();
 }
@@ -502,13 +536,13 @@ int bform_kb() { return KB; }
 template <class T>
 cudaError_t launch_bform(int shape, const CUtensorMap* tmap, const int2* lists, uint64_t cap,
                          const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,
-                         uint32_t nk, T* out, uint64_t ld_out, const DevStatus* st,
-                         cudaStream_t s) {
+                         uint32_t nk, uint32_t* splits, uint64_t slice_stride, T* out,
+                         uint64_t ld_out, const DevStatus* st, cudaStream_t s) {
   if (shape == kShapeWide)  // 1024 fp32 / 512 fp64 columns, 1 CTA per SM
-    return launch_ring<T, 8, 16, 6, 1>(tmap, lists, cap, counts, nrows, col0, ncols, nk, out,
-                                       ld_out, st, s);
-  return launch_ring<T, 4, 16, 6, 2>(tmap, lists, cap, counts, nrows, col0, ncols, nk, out,
-                                     ld_out, st, s);
+    return launch_ring<T, 8, 16, 6, 1>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits,
+                                       slice_stride, out, ld_out, st, s);
+  return launch_ring<T, 4, 16, 6, 2>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits,
+                                     slice_stride, out, ld_out, st, s);
 }
 
 template <class T>
@@ -534,10 +568,12 @@ cudaError_t launch_bform_dyn(const CUtensorMap* tmap, const int2* lists, uint64_
 
 template cudaError_t launch_bform<float>(int, const CUtensorMap*, const int2*, uint64_t,
                                          const uint32_t*, uint32_t, int32_t, int32_t, uint32_t,
-                                         float*, uint64_t, const DevStatus*, cudaStream_t);
+                                         uint32_t*, uint64_t, float*, uint64_t, const DevStatus*,
+                                         cudaStream_t);
 template cudaError_t launch_bform<double>(int, const CUtensorMap*, const int2*, uint64_t,
                                           const uint32_t*, uint32_t, int32_t, int32_t, uint32_t,
-                                          double*, uint64_t, const DevStatus*, cudaStream_t);
+                                          uint32_t*, uint64_t, double*, uint64_t,
+                                          const DevStatus*, cudaStream_t);
 template cudaError_t launch_bform_dyn<float>(const CUtensorMap*, const int2*, uint64_t,
                                              const uint32_t*, uint32_t, int32_t, int32_t,
                                              uint32_t, float*, uint64_t, const DevStatus*,

@@ -43,11 +43,18 @@ int bform_box_bytes();
 // per SM; wide = 1024 / 512 columns, 32 accumulators per lane, 1 CTA per SM.
 constexpr int kShapeNarrow = 0;
 constexpr int kShapeWide = 1;
+// *splits: requested k slices in, slices launched out (1 = order-preserving).
+// Slice z writes its partial product to out + z * slice_stride.
 template <class T>
 cudaError_t launch_bform(int shape, const CUtensorMap* tmap, const int2* lists, uint64_t cap,
                          const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,
-                         uint32_t nk, T* out, uint64_t ld_out, const DevStatus* st,
-                         cudaStream_t s);
+                         uint32_t nk, uint32_t* splits, uint64_t slice_stride, T* out,
+                         uint64_t ld_out, const DevStatus* st, cudaStream_t s);
+
+// out[r*ld_out + c] = sum over z (ascending) of part[z*stride + r*ld_part + c]
+template <class T>
+void launch_reduce_slices(const T* part, uint64_t stride, uint64_t ld_part, uint32_t splits,
+                          uint32_t rows, uint32_t cols, T* out, uint64_t ld_out, cudaStream_t s);
 
 template <class T>
 cudaError_t launch_bform_dyn(const CUtensorMap* tmap, const int2* lists, uint64_t cap,

@@ -221,6 +221,24 @@ __global__ void k_transpose(const T* __restrict__ in, uint64_t ld_in, uint32_t r
   }
 }
 
+// Fast mode: combine the k-slice partial products in ascending slice order
+// (deterministic; the reassociation the fast mode allows is exactly this
+// regrouping of each element's k-sum).
+template <class T>
+__global__ void k_reduce_slices(const T* __restrict__ part, uint64_t stride, uint64_t ld_part,
+                                uint32_t splits, uint32_t rows, uint32_t cols,
+                                T* __restrict__ out, uint64_t ld_out) {
+  const uint64_t total = (uint64_t)rows * cols;
+  for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = idx / cols, c = idx % cols;
+    const T* p = part + r * ld_part + c;
+    T acc = p[0];
+    for (uint32_t z = 1; z < splits; ++z) acc = acc + p[z * stride];
+    out[r * ld_out + c] = acc;
+  }
+}
+
 inline unsigned grid_for_rows(uint64_t rows, int warps_per_block) {
   uint64_t blocks = (rows + warps_per_block - 1) / warps_per_block;
   if (blocks > 148ull * 32) blocks = 148ull * 32;
@@ -286,7 +304,20 @@ void launch_transpose(const T* in, uint64_t ld_in, uint32_t rows, uint32_t cols,
   note_launch();
 }
 
+template <class T>
+void launch_reduce_slices(const T* part, uint64_t stride, uint64_t ld_part, uint32_t splits,
+                          uint32_t rows, uint32_t cols, T* out, uint64_t ld_out, cudaStream_t s) {
+  uint64_t blocks = ((uint64_t)rows * cols + 255) / 256;
+  if (blocks > 148ull * 16) blocks = 148ull * 16;
+  if (blocks < 1) blocks = 1;
+  k_reduce_slices<T><<<(unsigned)blocks, 256, 0, s>>>(part, stride, ld_part, splits, rows, cols,
+                                                      out, ld_out);
+  note_launch();
+}
+
 #define INSTANTIATE(T)                                                                         \
+  template void launch_reduce_slices<T>(const T*, uint64_t, uint64_t, uint32_t, uint32_t,     \
+                                        uint32_t, T*, uint64_t, cudaStream_t);                 \
   template void launch_scan_operand<T>(const T*, uint64_t, uint32_t, int, unsigned long long*, \
                                        unsigned long long*, unsigned long long*, cudaStream_t); \
   template void launch_row_nnz<T>(const T*, uint64_t, uint32_t, uint32_t*, cudaStream_t);      \

@@ -117,7 +117,7 @@ struct afmm_context {
   cudaStream_t stream = nullptr;
   std::mutex mu;
   // workspace
-  DevBuf status, vec_k, work, zs, lists, counts, base_copy, yt, xt, zt;
+  DevBuf status, vec_k, work, zs, lists, counts, base_copy, yt, xt, zt, part;
   // host-buffer API staging
   DevBuf hx, hy, hz;
   DevStatus* status_host = nullptr;  // pinned
@@ -268,9 +268,38 @@ afmm_status decode_status(afmm_context* c, afmm_op_counts* counts, afmm_error* e
 // are in c->lists / c->counts) and base columns [col0, col0 + ncols) of the
 // base matrix (kb_rows x b_cols, leading dimension ldb).
 template <class T>
-afmm_status launch_compute(afmm_context* c, const T* base, uint64_t kb_rows, uint64_t b_cols,
-                           uint64_t ldb, uint32_t nrows, int32_t col0, int32_t ncols, T* out,
-                           uint64_t ld_out, DevStatus* st, afmm_error* err) {
+afmm_status launch_compute(afmm_context* c, int mode, const T* base, uint64_t kb_rows,
+                           uint64_t b_cols, uint64_t ldb, uint32_t nrows, int32_t col0,
+                           int32_t ncols, T* out, uint64_t ld_out, DevStatus* st,
+                           afmm_error* err) {
+  // Fast mode (reassociated): split the k range into slices when the tile grid
+  // alone cannot fill the GPU (2 CTAs x 148 SMs), then add the slice partials
+  // in a fixed order. Each slice is still the exact repeated-addition chain.
+  const uint64_t narrow_ctas = (nrows + 15) / 16 * ((ncols * sizeof(T) + 2047) / 2048);
+  const uint64_t nkb = (kb_rows + afmm_dev::bform_kb() - 1) / afmm_dev::bform_kb();
+  uint32_t splits = 1;
+  if (mode == AFMM_MODE_FAST && (c->variant == kVariantAuto || c->variant == kVariantRing)) {
+    uint64_t want = (4 * 148) / std::max<uint64_t>(narrow_ctas, 1);
+    want = std::min<uint64_t>(want, std::max<uint64_t>(nkb / 4, 1));
+    splits = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, 32));
+  }
+  if (splits > 1) {
+    CUtensorMap tmap;
+    if (!make_tmap<T>(&tmap, base, kb_rows, b_cols, ldb)) {
+      set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: cuTensorMapEncodeTiled failed");
+      return AFMM_ERR_CUDA;
+    }
+    const uint64_t ldp = round_up((uint64_t)ncols, 32);
+    const uint64_t stride = (uint64_t)nrows * ldp;
+    CK(c->part.ensure(stride * splits * sizeof(T)), "workspace");
+    CK(afmm_dev::launch_bform<T>(afmm_dev::kShapeNarrow, &tmap, c->lists.as<int2>(), c->list_cap,
+                                 c->counts.as<uint32_t>(), nrows, col0, ncols, (uint32_t)kb_rows,
+                                 &splits, stride, c->part.as<T>(), ldp, st, c->stream),
+       "bform");
+    afmm_dev::launch_reduce_slices<T>(c->part.as<T>(), stride, ldp, splits, nrows,
+                                      (uint32_t)ncols, out, ld_out, c->stream);
+    return AFMM_OK;
+  }
   if (c->variant != kVariantL1) {
     CUtensorMap tmap;
     if (!make_tmap<T>(&tmap, base, kb_rows, b_cols, ldb)) {
@@ -287,10 +316,11 @@ afmm_status launch_compute(afmm_context* c, const T* base, uint64_t kb_rows, uin
       const uint64_t wide_ctas = (nrows + 15) / 16 * ((ncols * sizeof(T) + 4095) / 4096);
       const bool wide = c->variant == kVariantWide ||
                         (c->variant == kVariantAuto && wide_ctas >= 2 * 148);
+      uint32_t one = 1;
       CK(afmm_dev::launch_bform<T>(
              wide ? afmm_dev::kShapeWide : afmm_dev::kShapeNarrow, &tmap,
              c->lists.as<int2>(), c->list_cap, c->counts.as<uint32_t>(), nrows, col0, ncols,
-             (uint32_t)kb_rows, out, ld_out, st, c->stream),
+             (uint32_t)kb_rows, &one, 0, out, ld_out, st, c->stream),
          "bform");
     }
   } else {
@@ -307,7 +337,7 @@ afmm_status launch_compute(afmm_context* c, const T* base, uint64_t kb_rows, uin
 template <class T>
 afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* rhs, uint64_t n,
                             uint64_t ld, T* out, uint64_t ld_out, uint64_t r0, uint64_t r1,
-                            afmm_error* err) {
+                            int mode, afmm_error* err) {
   cudaStream_t s = c->stream;
   const uint64_t rows = r1 - r0;
   const uint32_t n32 = (uint32_t)n;
@@ -352,7 +382,7 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
     }
     c->mark(1);
     if (rows > 0) {
-      afmm_status cs = launch_compute<T>(c, base, n, n, ldb, (uint32_t)rows, 0, (int32_t)n, out,
+      afmm_status cs = launch_compute<T>(c, mode, base, n, n, ldb, (uint32_t)rows, 0, (int32_t)n, out,
                                          ld_out, st, err);
       if (cs != AFMM_OK) return cs;
     }
@@ -378,7 +408,7 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
       afmm_dev::launch_transpose<T>(lhs + r0 * ld, ld, (uint32_t)rows, n32, c->xt.as<T>(), lds,
                                     s);
       c->mark(1);
-      afmm_status cs = launch_compute<T>(c, c->xt.as<T>(), n, rows, lds, n32, 0, (int32_t)rows,
+      afmm_status cs = launch_compute<T>(c, mode, c->xt.as<T>(), n, rows, lds, n32, 0, (int32_t)rows,
                                          c->zt.as<T>(), lds, st, err);
       if (cs != AFMM_OK) return cs;
       c->mark(2);
@@ -470,7 +500,7 @@ afmm_status host_product(int which, const T* lhs, uint64_t n_lhs, const T* rhs, 
                        cudaMemcpyHostToDevice, s),
      "afmm: H2D");
   st = enqueue_product<T>(c, which, c->hx.as<T>(), c->hy.as<T>(), n, ld, c->hz.as<T>(), ld, 0, n,
-                          err);
+                          opt ? opt->mode : AFMM_MODE_ORDER_PRESERVING, err);
   if (st != AFMM_OK) return st;
   st = finish_locked(c, counts, err);
   if (st != AFMM_OK) return st;
@@ -569,7 +599,7 @@ void afmm_context_destroy(afmm_context* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     for (DevBuf* b : {&c->status, &c->vec_k, &c->work, &c->zs, &c->lists, &c->counts,
-                      &c->base_copy, &c->yt, &c->xt, &c->zt, &c->hx, &c->hy, &c->hz})
+                      &c->base_copy, &c->yt, &c->xt, &c->zt, &c->part, &c->hx, &c->hy, &c->hz})
       b->release();
     if (c->status_host) cudaFreeHost(c->status_host);
     for (cudaEvent_t& e : c->ev)
@@ -590,8 +620,8 @@ afmm_status afmm_product_device(afmm_context* c, int32_t which_case, int32_t dty
                                 void* out, uint64_t ld_out, uint64_t row_begin, uint64_t row_end,
                                 const afmm_options* options, int32_t sync,
                                 afmm_op_counts* counts, afmm_error* err) {
-  (void)options;
   clear_error(err);
+  const int mode = options ? options->mode : AFMM_MODE_ORDER_PRESERVING;
   if (!c || (which_case != AFMM_CASE_A && which_case != AFMM_CASE_B) ||
       (dtype != AFMM_F64 && dtype != AFMM_F32)) {
     set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: invalid context/case/dtype");
@@ -614,11 +644,12 @@ afmm_status afmm_product_device(afmm_context* c, int32_t which_case, int32_t dty
     if (dtype == AFMM_F64)
       st = enqueue_product<double>(c, which_case, static_cast<const double*>(lhs),
                                    static_cast<const double*>(rhs), n, ld,
-                                   static_cast<double*>(out), ld_out, row_begin, row_end, err);
+                                   static_cast<double*>(out), ld_out, row_begin, row_end, mode,
+                                   err);
     else
       st = enqueue_product<float>(c, which_case, static_cast<const float*>(lhs),
                                   static_cast<const float*>(rhs), n, ld, static_cast<float*>(out),
-                                  ld_out, row_begin, row_end, err);
+                                  ld_out, row_begin, row_end, mode, err);
     if (st != AFMM_OK) return st;
     if (sync) return finish_locked(c, counts, err);
     return AFMM_OK;

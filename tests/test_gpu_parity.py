@@ -197,6 +197,28 @@ def test_full_size_row_sample_bit_exact(cuda, oracle, name, kw):
     ctx.close()
 
 
+@pytest.mark.parametrize("name,n,kw", [
+    ("cfg1", 256, {}), ("cfg2", 1024, {}), ("cfg3", 512, {"d1": 0.5, "mu": 4}),
+    ("cfg4", 384, {}), ("cfg5", 640, {}),
+])
+def test_fast_mode_within_tolerance(cuda, oracle, name, n, kw):
+    """Reassociated fast mode (split-k): within 1e-12 (f64) / 1e-5 (f32) of the fp64
+    reference, normalised by sum_k |X[i,k]| |Y[k,j]| (the checker may multiply; the
+    kernel may not), with the same OpCounts as the reference."""
+    from paper_1308_2400_b200.gen import CONFIGS, make_inputs
+
+    lhs, rhs = make_inputs(name, seed=13, n=n, **kw)
+    case = CONFIGS[name].case
+    l64, r64 = lhs.astype(np.float64), rhs.astype(np.float64)
+    z64, c64 = oracle.product_mt(case, l64, r64, 0, n, 8)
+    res = _call(case, lhs, rhs, mode="fast")
+    assert (res.counts.additions, 0, res.counts.zero_skips) == c64
+    norm = np.abs(l64) @ np.abs(r64)
+    err = np.abs(res.product.astype(np.float64) - z64) / np.maximum(norm, 1e-300)
+    tol = 1e-12 if lhs.dtype == np.float64 else 1e-5
+    assert float(err.max()) <= tol, (name, float(err.max()))
+
+
 @pytest.mark.parametrize("variant", ["wide", "ring", "dyn", "l1"])
 def test_both_kernel_variants_bit_exact(cuda, oracle, variant, monkeypatch):
     """k_bform (TMA smem ring) and k_bform_l1 (decoupled warps) give identical bits."""
