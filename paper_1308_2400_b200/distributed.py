@@ -52,12 +52,13 @@ class ShardedProduct:
         self.world = world
         self.cuts: Optional[np.ndarray] = None
 
-    def run(self, case: str, lhs, rhs, z_full, slab_buf) -> OpCounts:
+    def run(self, case: str, lhs, rhs, z_full, slab_buf,
+            mode: str = "order-preserving") -> OpCounts:
         """lhs, rhs: full n x n device tensors on every rank; z_full: n x n on rank 0;
         slab_buf: a scratch n x n tensor on ranks > 0. Returns this rank's counts."""
         n = lhs.shape[0]
         if self.world == 1:
-            counts = self.ctx.product(case, lhs, rhs, z_full, 0, n)
+            counts = self.ctx.product(case, lhs, rhs, z_full, 0, n, mode=mode)
             self.cuts = np.array([0, n])
             return counts
         work = self.ctx.row_work(case, lhs, rhs)
@@ -65,6 +66,6 @@ class ShardedProduct:
         self.cuts = cuts
         r0, r1 = int(cuts[self.rank]), int(cuts[self.rank + 1])
         out = z_full[r0:r1] if self.rank == 0 else slab_buf[: max(r1 - r0, 1)]
-        counts = self.ctx.product(case, lhs, rhs, out, r0, r1)
+        counts = self.ctx.product(case, lhs, rhs, out, r0, r1, mode=mode)
         gather_rows(self.dist, z_full, out[: r1 - r0], cuts, self.rank, self.world)
         return counts

@@ -32,7 +32,7 @@ class OracleContext:
         nnz = (r != 0).sum(axis=1)
         return (np.abs(np.rint(l)) * nnz[None, :]).sum(axis=1).astype(np.uint64)
 
-    def product(self, which, lhs, rhs, out, r0, r1):
+    def product(self, which, lhs, rhs, out, r0, r1, mode="order-preserving"):
         z, counts, err = self.oracle.product(which, lhs.numpy(), rhs.numpy(), r0, r1)
         assert err is None
         if r1 > r0:
