@@ -8,20 +8,23 @@
 
 namespace afmm_dev {
 
-// Device-side status of one product call: first offenders (row-major linear
-// index, ~0 = none) and the exact counts, all written by the prepass.
+// Device-side status of one product call: first offenders and the exact
+// counts, all written by the prepass. Offenders are stored INVERTED (~key,
+// reduced with atomicMax) so that an all-zero struct means "no error, zero
+// counts" and one memset initialises everything.
 struct DevStatus {
-  unsigned long long nonfinite_lhs;  // linear index of first non-finite lhs element
-  unsigned long long nonfinite_rhs;
-  unsigned long long rep_bad;        // (linear index << 2) | kind of first bad rep
-  unsigned long long rep_too_large;  // linear index of first |rep| >= 2^31
+  unsigned long long nonfinite_lhs_inv;  // ~(linear index) of first non-finite lhs element
+  unsigned long long nonfinite_rhs_inv;
+  unsigned long long rep_bad_inv;        // ~((linear index << 2) | kind) of first bad rep
+  unsigned long long rep_too_large_inv;  // ~(linear index) of first |rep| >= 2^31
   unsigned long long additions;
   unsigned long long zero_skips;
   unsigned long long pad[2];
 };
 
 __device__ __forceinline__ bool status_failed(const DevStatus* st) {
-  return (st->nonfinite_lhs & st->nonfinite_rhs & st->rep_bad & st->rep_too_large) != ~0ull;
+  return (st->nonfinite_lhs_inv | st->nonfinite_rhs_inv | st->rep_bad_inv |
+          st->rep_too_large_inv) != 0ull;
 }
 
 // kernels.hpp:31-40 on the widened value: 0 ok, 1 not integer-valued,

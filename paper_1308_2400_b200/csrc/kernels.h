@@ -12,24 +12,22 @@ namespace afmm_dev {
 
 void note_launch();  // counts library kernel launches (runtime.cu)
 
+// Both operands: finite check, rep validation (into st), and the per-k vector
+// (Case B: nnz[k] of rhs rows; Case A: rsum[k] of rhs rows). which_case: 0 = A, 1 = B.
 template <class T>
-void launch_scan_operand(const T* m, uint64_t ld, uint32_t n, int is_rep,
-                         unsigned long long* nonfinite, unsigned long long* rep_bad,
-                         unsigned long long* too_large, cudaStream_t s);
+void launch_scan_stats(const T* lhs, const T* rhs, uint64_t ld, uint32_t n, int which_case,
+                       DevStatus* st, uint32_t* nnz, unsigned long long* rsum, cudaStream_t s);
+// Rows of X: work[i] for all rows; slab [r0, r1) adds OpCounts to st and, for
+// Case B with lists != nullptr, gets its compacted (k, rep) lists.
 template <class T>
-void launch_row_nnz(const T* m, uint64_t ld, uint32_t n, uint32_t* nnz, cudaStream_t s);
+void launch_rows(const T* x, uint64_t ld, uint32_t n, int which_case, const uint32_t* nnz,
+                 const unsigned long long* rsum, uint32_t r0, uint32_t r1, int2* lists,
+                 uint64_t cap, uint32_t* counts, unsigned long long* work, DevStatus* st,
+                 cudaStream_t s);
+// Case A rep lists: list j = compacted column j of Y.
 template <class T>
-void launch_row_repsum(const T* m, uint64_t ld, uint32_t n, unsigned long long* rsum,
-                       cudaStream_t s);
-template <class T>
-void launch_compact_reps(const T* m, uint64_t ld, uint32_t rows, uint32_t n, int2* lists,
-                         uint64_t cap, uint32_t* counts, cudaStream_t s);
-template <class T>
-void launch_row_work(const T* x, uint64_t ld, uint32_t n, int which_case, const uint32_t* nnz_b,
-                     const unsigned long long* rsum, unsigned long long* work,
-                     unsigned long long* zs, cudaStream_t s);
-void launch_sum_counts(const unsigned long long* work, const unsigned long long* zs, uint32_t r0,
-                       uint32_t r1, DevStatus* st, cudaStream_t s);
+void launch_transpose_compact(const T* y, uint64_t ld, uint32_t n, int2* lists, uint64_t cap,
+                              uint32_t* counts, cudaStream_t s);
 template <class T>
 void launch_transpose(const T* in, uint64_t ld_in, uint32_t rows, uint32_t cols, T* out,
                       uint64_t ld_out, cudaStream_t s);

@@ -2,22 +2,26 @@
 //
 // Replaces the inline zero tests and the up-front validation of the
 // reference kernels (/root/reference/proj/include/afmm/kernels.hpp:25-43,
-// :121-130, :150-159) with data-parallel passes:
-//   k_scan_operand   finite check (matrix.hpp:31-35) and rep validation
-//                    (kernels.hpp:25-43), first offender by atomicMin on the
-//                    row-major linear index
-//   k_row_nnz        nnz(B[k,:]) of the Case-B base operand rows
-//   k_row_repsum     R_k = sum_j |llround Y[k,j]| of the Case-A rep operand rows
-//   k_compact_reps   warp ballot/popc stream compaction of every rep row into
-//                    an ordered (k, rep) list: the zero-skip of kernels.hpp:128-130
-//                    and :151-153 done once instead of per (i,k,j)
-//   k_row_work       exact per-row additions W_i and zero_skips (closed forms of
-//                    kernels.hpp:119-134 / :148-163), the partition weights
-//   k_sum_counts     OpCounts of a row slab
-//   k_transpose      32x32 smem-tiled transpose (Case A runs as Case B on
-//                    transposed operands)
-// All of these are HBM-bound streaming passes: one coalesced read of each
-// operand, no reuse, so no smem staging except in the transpose.
+// :121-130, :150-159) with three streaming passes (one warp per matrix row,
+// 128-bit loads, one read of each operand):
+//
+//   k_scan_stats   both operands: finite check (matrix.hpp:31-35), rep
+//                  validation of the rep operand (kernels.hpp:25-43; first
+//                  offender by atomicMax on the inverted row-major index), and
+//                  the per-k vector the work formulas need: nnz(Y[k,:]) (Case B)
+//                  or R_k = sum_j |llround Y[k,j]| (Case A)
+//   k_rows         per row i of X: exact additions W_i and zero_skips (closed
+//                  forms of kernels.hpp:119-134 / :148-163), the slab's OpCounts,
+//                  and (Case B) the warp-scan stream compaction of the row's
+//                  nonzero reps into an ordered (k, rep) list: the zero-skip of
+//                  kernels.hpp:151-153 done once instead of per (i,k,j)
+//   k_transpose_compact  (Case A) the same compaction for the columns of Y,
+//                  through 32x33 smem tiles (the rep list of B-form row j is
+//                  column j of Y)
+//
+// plus k_transpose (Case A operand/result transposes) and k_reduce_slices
+// (fast-mode split-k combine). All are HBM-bound; none does FP arithmetic on
+// the product.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -27,11 +31,11 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const unsigned long long w = __shfl_xor_sync(FULL, v, o);
-    v = w < v ? w : v;
+    v = w > v ? w : v;
   }
   return v;
 }
@@ -42,165 +46,202 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
   return v;
 }
 
-template <class T>
-__global__ void k_scan_operand(const T* __restrict__ m, uint64_t ld, uint32_t n, int is_rep,
-                               unsigned long long* nonfinite, unsigned long long* rep_bad,
-                               unsigned long long* too_large) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t i = warp; i < n; i += nwarps) {
-    const T* row = m + i * ld;
-    for (uint32_t j0 = 0; j0 < n; j0 += 32) {
-      const uint32_t j = j0 + lane;
-      unsigned long long nf = ~0ull, rb = ~0ull, tl = ~0ull;
-      if (j < n) {
-        const double v = (double)row[j];
-        const uint64_t lin = i * (uint64_t)n + j;
-        if (!isfinite(v)) nf = lin;
-        if (is_rep) {
-          const int kind = rep_kind(v);
-          if (kind) rb = (lin << 2) | (unsigned long long)kind;
-          else if (fabs(v) >= 2147483647.5) tl = lin;
-        }
-      }
-      const bool bad = (nf & rb & tl) != ~0ull;
-      if (__any_sync(FULL, bad)) {
-        nf = warp_min_u64(nf);
-        rb = warp_min_u64(rb);
-        tl = warp_min_u64(tl);
-        if (lane == 0) {
-          if (nf != ~0ull) atomicMin(nonfinite, nf);
-          if (rb != ~0ull) atomicMin(rep_bad, rb);
-          if (tl != ~0ull) atomicMin(too_large, tl);
-        }
-      }
-    }
-  }
-}
-
-// nnz of each row of the base operand (Case B: nnz(Y[k,:]), test_kernels.cpp:168).
-template <class T>
-__global__ void k_row_nnz(const T* __restrict__ m, uint64_t ld, uint32_t n,
-                          uint32_t* __restrict__ nnz) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t k = warp; k < n; k += nwarps) {
-    const T* row = m + k * ld;
-    uint32_t c = 0;
-    for (uint32_t j = lane; j < n; j += 32) c += row[j] != T(0) ? 1u : 0u;
+__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, uint32_t lane, uint32_t* total) {
+  uint32_t x = v;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
-    if (lane == 0) nnz[k] = c;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, x, o);
+    if (lane >= (uint32_t)o) x += y;
+  }
+  *total = __shfl_sync(FULL, x, 31);
+  return x - v;
+}
+
+// Four consecutive row elements j..j+3 (zeros beyond n). `vec` = row base and
+// leading dimension allow 128-bit loads.
+template <class T>
+__device__ __forceinline__ void load4(const T* row, uint32_t j, uint32_t n, bool vec, T v[4]) {
+  if (vec && j + 3 < n) {
+    if constexpr (sizeof(T) == 4) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(row + j));
+      v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else {
+      const double2 a = __ldg(reinterpret_cast<const double2*>(row + j));
+      const double2 b = __ldg(reinterpret_cast<const double2*>(row + j + 2));
+      v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) v[e] = j + e < n ? row[j + e] : T(0);
   }
 }
 
-// R_k = sum_j |llround Y[k,j]| over the Case-A rep operand rows
-// (test_kernels.cpp:51-53).
+__device__ __forceinline__ long long abs_ll(long long r) { return r < 0 ? -r : r; }
+
+// warp task t < n: lhs row t; t >= n: rhs row t - n.
 template <class T>
-__global__ void k_row_repsum(const T* __restrict__ m, uint64_t ld, uint32_t n,
-                             unsigned long long* __restrict__ rsum) {
+__global__ void k_scan_stats(const T* __restrict__ lhs, const T* __restrict__ rhs, uint64_t ld,
+                             uint32_t n, int which_case, int vec, DevStatus* st,
+                             uint32_t* __restrict__ nnz, unsigned long long* __restrict__ rsum) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t k = warp; k < n; k += nwarps) {
-    const T* row = m + k * ld;
+  for (uint64_t t = warp; t < 2ull * n; t += nwarps) {
+    const bool is_rhs = t >= n;
+    const uint64_t i = is_rhs ? t - n : t;
+    const T* row = (is_rhs ? rhs : lhs) + i * ld;
+    // Case A validates rhs (kernels.hpp:115), Case B lhs (:144)
+    const bool is_rep = is_rhs == (which_case == 0);
+    unsigned long long nf = 0, rb = 0, tl = 0;  // inverted keys, 0 = none
+    uint32_t cnt = 0;
     unsigned long long s = 0;
-    for (uint32_t j = lane; j < n; j += 32) {
-      const T v = row[j];
-      if (v != T(0)) {
-        const long long r = llround((double)v);
-        s += (unsigned long long)(r < 0 ? -r : r);
+    for (uint32_t j0 = 4 * lane; j0 < n; j0 += 128) {
+      T v[4];
+      load4(row, j0, n, vec != 0, v);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t j = j0 + e;
+        if (j >= n) break;
+        const double d = (double)v[e];
+        const unsigned long long lin = i * (uint64_t)n + j;
+        if (!isfinite(d) && nf == 0) nf = ~lin;  // ascending j: the first one is the minimum
+        if (is_rep) {
+          const int kind = rep_kind(d);
+          if (kind && rb == 0) rb = ~((lin << 2) | (unsigned long long)kind);
+          else if (!kind && tl == 0 && fabs(d) >= 2147483647.5) tl = ~lin;
+        }
+        if (is_rhs) {
+          cnt += v[e] != T(0) ? 1u : 0u;
+          if (v[e] != T(0)) s += (unsigned long long)abs_ll(llround(d));
+        }
       }
     }
-    s = warp_sum_u64(s);
-    if (lane == 0) rsum[k] = s;
+    if (__any_sync(FULL, (nf | rb | tl) != 0)) {
+      nf = warp_max_u64(nf);
+      rb = warp_max_u64(rb);
+      tl = warp_max_u64(tl);
+      if (lane == 0) {
+        if (nf) atomicMax(is_rhs ? &st->nonfinite_rhs_inv : &st->nonfinite_lhs_inv, nf);
+        if (rb) atomicMax(&st->rep_bad_inv, rb);
+        if (tl) atomicMax(&st->rep_too_large_inv, tl);
+      }
+    }
+    if (is_rhs) {
+      if (which_case == 1) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+        if (lane == 0) nnz[i] = cnt;
+      } else {
+        s = warp_sum_u64(s);
+        if (lane == 0) rsum[i] = s;
+      }
+    }
   }
 }
 
-// One warp per rep row: ordered (k, rep) list of the nonzero reps. A rep is
-// skipped exactly when the reference skips it: value == 0.0 or llround == 0
-// (kernels.hpp:128-130, :151-153).
+// Per row i of X (all n rows): W_i -> work[i]; rows in [r0, r1) add to the
+// slab OpCounts and (Case B, lists != nullptr) get their compacted rep list.
+// Case A: W_i = sum_{k: X[i,k] != 0} R_k, zs_i = #{k: X[i,k] == 0}
+// Case B: W_i = sum_k |rep_ik| nnz_k,    zs_i = sum_{k: rep_ik != 0} (n - nnz_k)
+// A rep is skipped exactly when the reference skips it: value == 0.0 or
+// llround == 0 (kernels.hpp:151-153).
 template <class T>
-__global__ void k_compact_reps(const T* __restrict__ m, uint64_t ld, uint32_t rows, uint32_t n,
-                               int2* __restrict__ lists, uint64_t cap,
-                               uint32_t* __restrict__ counts) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  const unsigned lt = (1u << lane) - 1u;
-  for (uint64_t r = warp; r < rows; r += nwarps) {
-    const T* row = m + r * ld;
-    int2* out = lists + r * cap;
-    uint32_t base = 0;
-    for (uint32_t k0 = 0; k0 < n; k0 += 32) {
-      const uint32_t k = k0 + lane;
-      int rep = 0;
-      if (k < n) {
-        const T v = row[k];
-        if (v != T(0)) rep = (int)llround((double)v);
-      }
-      const unsigned mask = __ballot_sync(FULL, rep != 0);
-      if (rep != 0) out[base + __popc(mask & lt)] = make_int2((int)k, rep);
-      base += __popc(mask);
-    }
-    if (lane == 0) counts[r] = base;
-  }
-}
-
-// Exact per-row additions and zero_skips of Z row i.
-// Case A: W_i = sum_{k: X[i,k] != 0} R_k,           zs_i = #{k: X[i,k] == 0}
-// Case B: W_i = sum_k |rep_ik| * nnzB_k,            zs_i = sum_{k: rep_ik != 0} (n - nnzB_k)
-template <class T>
-__global__ void k_row_work(const T* __restrict__ x, uint64_t ld, uint32_t n, int which_case,
-                           const uint32_t* __restrict__ nnz_b,
-                           const unsigned long long* __restrict__ rsum,
-                           unsigned long long* __restrict__ work,
-                           unsigned long long* __restrict__ zs) {
+__global__ void k_rows(const T* __restrict__ x, uint64_t ld, uint32_t n, int which_case, int vec,
+                       const uint32_t* __restrict__ nnz,
+                       const unsigned long long* __restrict__ rsum, uint32_t r0, uint32_t r1,
+                       int2* __restrict__ lists, uint64_t cap, uint32_t* __restrict__ counts,
+                       unsigned long long* __restrict__ work, DevStatus* st) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t i = warp; i < n; i += nwarps) {
     const T* row = x + i * ld;
+    const bool in_slab = i >= r0 && i < r1;
+    const bool compact = which_case == 1 && in_slab && lists != nullptr;
+    int2* out = compact ? lists + (i - r0) * cap : nullptr;
     unsigned long long w = 0, z = 0;
-    for (uint32_t k = lane; k < n; k += 32) {
-      const T v = row[k];
-      if (which_case == 0) {
-        if (v == T(0)) ++z;
-        else w += rsum[k];
-      } else if (v != T(0)) {
-        const long long r = llround((double)v);
-        if (r != 0) {
-          const unsigned long long nb = nnz_b[k];
-          w += (unsigned long long)(r < 0 ? -r : r) * nb;  // count bookkeeping, not an element product
+    uint32_t base = 0;
+    for (uint32_t c0 = 0; c0 < n; c0 += 128) {  // warp-uniform trip count (the scan below)
+      const uint32_t j0 = c0 + 4 * lane;
+      T v[4];
+      load4(row, j0, n, vec != 0, v);
+      long long rep[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t j = j0 + e;
+        rep[e] = 0;
+        if (j < n && v[e] != T(0)) rep[e] = llround((double)v[e]);
+        if (which_case == 0) {
+          if (j < n) {
+            if (v[e] == T(0)) ++z;
+            else w += rsum[j];
+          }
+        } else if (rep[e] != 0) {
+          const unsigned long long nb = nnz[j];
+          w += (unsigned long long)abs_ll(rep[e]) * nb;  // count bookkeeping, not an element product
           z += (unsigned long long)n - nb;
         }
+      }
+      if (compact) {
+        const uint32_t mine = (rep[0] != 0) + (rep[1] != 0) + (rep[2] != 0) + (rep[3] != 0);
+        uint32_t total;
+        uint32_t pos = base + warp_excl_scan(mine, lane, &total);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (rep[e] != 0) out[pos++] = make_int2((int)(j0 + e), (int)rep[e]);
+        base += total;
       }
     }
     w = warp_sum_u64(w);
     z = warp_sum_u64(z);
     if (lane == 0) {
       work[i] = w;
-      if (zs) zs[i] = z;
+      if (in_slab) {
+        if (w) atomicAdd(&st->additions, w);
+        if (z) atomicAdd(&st->zero_skips, z);
+        if (compact) counts[i - r0] = base;
+      }
     }
   }
 }
 
-__global__ void k_sum_counts(const unsigned long long* __restrict__ work,
-                             const unsigned long long* __restrict__ zs, uint32_t r0, uint32_t r1,
-                             DevStatus* st) {
-  unsigned long long w = 0, z = 0;
-  for (uint32_t i = r0 + blockIdx.x * blockDim.x + threadIdx.x; i < r1;
-       i += gridDim.x * blockDim.x) {
-    w += work[i];
-    z += zs[i];
+// Case A rep lists: B-form row j = column j of Y. A block owns 32 columns and
+// walks k in 32-row tiles through smem; warp w compacts columns 4w..4w+3.
+template <class T>
+__global__ void __launch_bounds__(256) k_transpose_compact(const T* __restrict__ y, uint64_t ld,
+                                                           uint32_t n, int2* __restrict__ lists,
+                                                           uint64_t cap,
+                                                           uint32_t* __restrict__ counts) {
+  __shared__ T tile[32][33];
+  const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const uint32_t j0 = blockIdx.x * 32;
+  const unsigned lt = (1u << tx) - 1u;
+  uint32_t base[4] = {0, 0, 0, 0};
+  for (uint32_t k0 = 0; k0 < n; k0 += 32) {
+    for (uint32_t dy = ty; dy < 32; dy += 8) {
+      const uint32_t k = k0 + dy, j = j0 + tx;
+      tile[dy][tx] = (k < n && j < n) ? y[(uint64_t)k * ld + j] : T(0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t jj = ty * 4 + q, j = j0 + jj;
+      const T v = tile[tx][jj];  // Y[k0 + tx, j]
+      int rep = 0;
+      if (v != T(0) && k0 + tx < n) rep = (int)llround((double)v);
+      const unsigned m = __ballot_sync(FULL, rep != 0);
+      if (rep != 0 && j < n) lists[(uint64_t)j * cap + base[q] + __popc(m & lt)] =
+          make_int2((int)(k0 + tx), rep);
+      base[q] += __popc(m);
+    }
+    __syncthreads();
   }
-  w = warp_sum_u64(w);
-  z = warp_sum_u64(z);
-  if ((threadIdx.x & 31) == 0) {
-    if (w) atomicAdd(&st->additions, w);
-    if (z) atomicAdd(&st->zero_skips, z);
+  if (tx == 0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t j = j0 + ty * 4 + q;
+      if (j < n) counts[j] = base[q];
+    }
   }
 }
 
@@ -239,11 +280,16 @@ __global__ void k_reduce_slices(const T* __restrict__ part, uint64_t stride, uin
   }
 }
 
-inline unsigned grid_for_rows(uint64_t rows, int warps_per_block) {
-  uint64_t blocks = (rows + warps_per_block - 1) / warps_per_block;
-  if (blocks > 148ull * 32) blocks = 148ull * 32;
+inline unsigned grid_for_warps(uint64_t tasks, int warps_per_block) {
+  uint64_t blocks = (tasks + warps_per_block - 1) / warps_per_block;
+  if (blocks > 148ull * 16) blocks = 148ull * 16;
   if (blocks < 1) blocks = 1;
   return (unsigned)blocks;
+}
+
+template <class T>
+int vec_ok(const T* p, uint64_t ld) {
+  return (reinterpret_cast<uintptr_t>(p) % 16 == 0 && (ld * sizeof(T)) % 16 == 0) ? 1 : 0;
 }
 
 }  // namespace
@@ -251,48 +297,28 @@ inline unsigned grid_for_rows(uint64_t rows, int warps_per_block) {
 // ---- launchers ---------------------------------------------------------------
 
 template <class T>
-void launch_scan_operand(const T* m, uint64_t ld, uint32_t n, int is_rep,
-                         unsigned long long* nonfinite, unsigned long long* rep_bad,
-                         unsigned long long* too_large, cudaStream_t s) {
-  k_scan_operand<T><<<grid_for_rows(n, 8), 256, 0, s>>>(m, ld, n, is_rep, nonfinite, rep_bad,
-                                                         too_large);
+void launch_scan_stats(const T* lhs, const T* rhs, uint64_t ld, uint32_t n, int which_case,
+                       DevStatus* st, uint32_t* nnz, unsigned long long* rsum, cudaStream_t s) {
+  const int vec = vec_ok(lhs, ld) & vec_ok(rhs, ld);
+  k_scan_stats<T><<<grid_for_warps(2ull * n, 8), 256, 0, s>>>(lhs, rhs, ld, n, which_case, vec,
+                                                               st, nnz, rsum);
   note_launch();
 }
 
 template <class T>
-void launch_row_nnz(const T* m, uint64_t ld, uint32_t n, uint32_t* nnz, cudaStream_t s) {
-  k_row_nnz<T><<<grid_for_rows(n, 8), 256, 0, s>>>(m, ld, n, nnz);
+void launch_rows(const T* x, uint64_t ld, uint32_t n, int which_case, const uint32_t* nnz,
+                 const unsigned long long* rsum, uint32_t r0, uint32_t r1, int2* lists,
+                 uint64_t cap, uint32_t* counts, unsigned long long* work, DevStatus* st,
+                 cudaStream_t s) {
+  k_rows<T><<<grid_for_warps(n, 8), 256, 0, s>>>(x, ld, n, which_case, vec_ok(x, ld), nnz, rsum,
+                                                  r0, r1, lists, cap, counts, work, st);
   note_launch();
 }
 
 template <class T>
-void launch_row_repsum(const T* m, uint64_t ld, uint32_t n, unsigned long long* rsum,
-                       cudaStream_t s) {
-  k_row_repsum<T><<<grid_for_rows(n, 8), 256, 0, s>>>(m, ld, n, rsum);
-  note_launch();
-}
-
-template <class T>
-void launch_compact_reps(const T* m, uint64_t ld, uint32_t rows, uint32_t n, int2* lists,
-                         uint64_t cap, uint32_t* counts, cudaStream_t s) {
-  k_compact_reps<T><<<grid_for_rows(rows, 8), 256, 0, s>>>(m, ld, rows, n, lists, cap, counts);
-  note_launch();
-}
-
-template <class T>
-void launch_row_work(const T* x, uint64_t ld, uint32_t n, int which_case, const uint32_t* nnz_b,
-                     const unsigned long long* rsum, unsigned long long* work,
-                     unsigned long long* zs, cudaStream_t s) {
-  k_row_work<T><<<grid_for_rows(n, 8), 256, 0, s>>>(x, ld, n, which_case, nnz_b, rsum, work, zs);
-  note_launch();
-}
-
-void launch_sum_counts(const unsigned long long* work, const unsigned long long* zs, uint32_t r0,
-                       uint32_t r1, DevStatus* st, cudaStream_t s) {
-  uint64_t blocks = ((uint64_t)(r1 - r0) + 255) / 256;
-  if (blocks > 296) blocks = 296;
-  if (blocks < 1) blocks = 1;
-  k_sum_counts<<<(unsigned)blocks, 256, 0, s>>>(work, zs, r0, r1, st);
+void launch_transpose_compact(const T* y, uint64_t ld, uint32_t n, int2* lists, uint64_t cap,
+                              uint32_t* counts, cudaStream_t s) {
+  k_transpose_compact<T><<<(n + 31) / 32, 256, 0, s>>>(y, ld, n, lists, cap, counts);
   note_launch();
 }
 
@@ -316,20 +342,17 @@ void launch_reduce_slices(const T* part, uint64_t stride, uint64_t ld_part, uint
 }
 
 #define INSTANTIATE(T)                                                                         \
-  template void launch_reduce_slices<T>(const T*, uint64_t, uint64_t, uint32_t, uint32_t,     \
-                                        uint32_t, T*, uint64_t, cudaStream_t);                 \
-  template void launch_scan_operand<T>(const T*, uint64_t, uint32_t, int, unsigned long long*, \
-                                       unsigned long long*, unsigned long long*, cudaStream_t); \
-  template void launch_row_nnz<T>(const T*, uint64_t, uint32_t, uint32_t*, cudaStream_t);      \
-  template void launch_row_repsum<T>(const T*, uint64_t, uint32_t, unsigned long long*,       \
-                                     cudaStream_t);                                            \
-  template void launch_compact_reps<T>(const T*, uint64_t, uint32_t, uint32_t, int2*,          \
-                                       uint64_t, uint32_t*, cudaStream_t);                     \
-  template void launch_row_work<T>(const T*, uint64_t, uint32_t, int, const uint32_t*,         \
-                                   const unsigned long long*, unsigned long long*,             \
-                                   unsigned long long*, cudaStream_t);                         \
+  template void launch_scan_stats<T>(const T*, const T*, uint64_t, uint32_t, int, DevStatus*,  \
+                                     uint32_t*, unsigned long long*, cudaStream_t);            \
+  template void launch_rows<T>(const T*, uint64_t, uint32_t, int, const uint32_t*,             \
+                               const unsigned long long*, uint32_t, uint32_t, int2*, uint64_t, \
+                               uint32_t*, unsigned long long*, DevStatus*, cudaStream_t);      \
+  template void launch_transpose_compact<T>(const T*, uint64_t, uint32_t, int2*, uint64_t,     \
+                                            uint32_t*, cudaStream_t);                          \
   template void launch_transpose<T>(const T*, uint64_t, uint32_t, uint32_t, T*, uint64_t,      \
-                                    cudaStream_t);
+                                    cudaStream_t);                                             \
+  template void launch_reduce_slices<T>(const T*, uint64_t, uint64_t, uint32_t, uint32_t,     \
+                                        uint32_t, T*, uint64_t, cudaStream_t);
 
 INSTANTIATE(float)
 INSTANTIATE(double)

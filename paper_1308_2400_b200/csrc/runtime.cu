@@ -117,7 +117,7 @@ struct afmm_context {
   cudaStream_t stream = nullptr;
   std::mutex mu;
   // workspace
-  DevBuf status, vec_k, work, zs, lists, counts, base_copy, yt, xt, zt, part;
+  DevBuf status, vec_k, work, lists, counts, base_copy, xt, zt, part;
   // host-buffer API staging
   DevBuf hx, hy, hz;
   DevStatus* status_host = nullptr;  // pinned
@@ -209,18 +209,22 @@ afmm_status decode_status(afmm_context* c, afmm_op_counts* counts, afmm_error* e
   const char* where = case_name(c->last_case);
   const char* opname = rep_operand ? "rhs" : "lhs";
   char buf[256];
-  if (s.nonfinite_lhs != kNone || s.nonfinite_rhs != kNone) {
-    const int operand = s.nonfinite_lhs != kNone ? 0 : 1;
-    const uint64_t lin = operand == 0 ? s.nonfinite_lhs : s.nonfinite_rhs;
+  // offenders are stored inverted (0 = none); see DevStatus
+  auto key = [](unsigned long long inv) { return inv ? ~inv : kNone; };
+  const uint64_t nf_lhs = key(s.nonfinite_lhs_inv), nf_rhs = key(s.nonfinite_rhs_inv);
+  const uint64_t rep_bad = key(s.rep_bad_inv), rep_too_large = key(s.rep_too_large_inv);
+  if (nf_lhs != kNone || nf_rhs != kNone) {
+    const int operand = nf_lhs != kNone ? 0 : 1;
+    const uint64_t lin = operand == 0 ? nf_lhs : nf_rhs;
     const double v = read_element(operand == 0 ? c->last_lhs : c->last_rhs, c->last_dtype,
                                   c->last_ld, lin / n, lin % n);
     set_error(err, AFMM_ERRKIND_NON_FINITE, operand, lin / n, lin % n, v,
               "DenseMatrix: non-finite element");
     return AFMM_ERR_DOMAIN;
   }
-  if (s.rep_bad != kNone) {
-    const uint64_t lin = s.rep_bad >> 2;
-    const int kind = (int)(s.rep_bad & 3);
+  if (rep_bad != kNone) {
+    const uint64_t lin = rep_bad >> 2;
+    const int kind = (int)(rep_bad & 3);
     const uint64_t i = lin / n, j = lin % n;
     const double v = read_element(rep_operand ? c->last_rhs : c->last_lhs, c->last_dtype,
                                   c->last_ld, i, j);
@@ -237,8 +241,8 @@ afmm_status decode_status(afmm_context* c, afmm_op_counts* counts, afmm_error* e
     }
     return AFMM_ERR_DOMAIN;
   }
-  if (s.rep_too_large != kNone) {
-    const uint64_t lin = s.rep_too_large;
+  if (rep_too_large != kNone) {
+    const uint64_t lin = rep_too_large;
     const uint64_t i = lin / n, j = lin % n;
     const double v = read_element(rep_operand ? c->last_rhs : c->last_lhs, c->last_dtype,
                                   c->last_ld, i, j);
@@ -344,32 +348,26 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
   CK(c->status.ensure(sizeof(DevStatus)), "workspace");
   CK(c->vec_k.ensure(n * 8), "workspace");
   CK(c->work.ensure(n * 8), "workspace");
-  CK(c->zs.ensure(n * 8), "workspace");
   DevStatus* st = c->status.as<DevStatus>();
   c->list_cap = n;
   c->timed_last = c->timing;
   c->mark(0);
-  CK(cudaMemsetAsync(st, 0xff, 4 * sizeof(unsigned long long), s), "memset");
-  CK(cudaMemsetAsync(&st->additions, 0, 4 * sizeof(unsigned long long), s), "memset");
+  CK(cudaMemsetAsync(st, 0, sizeof(DevStatus), s), "memset");
 
   // validation (kernels.hpp:115 / :144) + DenseMatrix finite check (matrix.hpp:31-35)
-  afmm_dev::launch_scan_operand<T>(lhs, ld, n32, which == AFMM_CASE_B, &st->nonfinite_lhs,
-                                   &st->rep_bad, &st->rep_too_large, s);
-  afmm_dev::launch_scan_operand<T>(rhs, ld, n32, which == AFMM_CASE_A, &st->nonfinite_rhs,
-                                   &st->rep_bad, &st->rep_too_large, s);
+  // + the per-k vector of the work formulas, one pass over both operands
+  auto* nnz = c->vec_k.as<uint32_t>();
+  auto* rsum = c->vec_k.as<unsigned long long>();
+  afmm_dev::launch_scan_stats<T>(lhs, rhs, ld, n32, which == AFMM_CASE_B ? 1 : 0, st, nnz, rsum,
+                                 s);
 
   auto* work = c->work.as<unsigned long long>();
-  auto* zs = c->zs.as<unsigned long long>();
   if (which == AFMM_CASE_B) {
     // rep = X[i,k] (lhs), bases = Y[k,:] (rhs): B-form directly.
-    auto* nnz = c->vec_k.as<uint32_t>();
-    afmm_dev::launch_row_nnz<T>(rhs, ld, n32, nnz, s);
-    afmm_dev::launch_row_work<T>(lhs, ld, n32, 1, nnz, nullptr, work, zs, s);
     CK(c->lists.ensure(std::max<uint64_t>(rows, 1) * n * sizeof(int2)), "workspace");
     CK(c->counts.ensure(std::max<uint64_t>(rows, 1) * 4), "workspace");
-    if (rows > 0)
-      afmm_dev::launch_compact_reps<T>(lhs + r0 * ld, ld, (uint32_t)rows, n32,
-                                       c->lists.as<int2>(), n, c->counts.as<uint32_t>(), s);
+    afmm_dev::launch_rows<T>(lhs, ld, n32, 1, nnz, nullptr, (uint32_t)r0, (uint32_t)r1,
+                             c->lists.as<int2>(), n, c->counts.as<uint32_t>(), work, st, s);
     const T* base = rhs;
     uint64_t ldb = ld;
     if ((ld * sizeof(T)) % 16 != 0 || reinterpret_cast<uintptr_t>(rhs) % 16 != 0) {
@@ -391,19 +389,15 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
     // Case A as Case B on transposed operands: Z^T = (Y^T) (x) (X^T).
     // B-form rows = Z columns j (rep list = column j of Y), B-form columns =
     // Z rows of the slab (bases X[i,k], i in [r0, r1)).
-    auto* rsum = c->vec_k.as<unsigned long long>();
-    afmm_dev::launch_row_repsum<T>(rhs, ld, n32, rsum, s);
-    afmm_dev::launch_row_work<T>(lhs, ld, n32, 0, nullptr, rsum, work, zs, s);
-    const uint64_t ldt = round_up(n, 32);
     const uint64_t lds = round_up(std::max<uint64_t>(rows, 1), 32);
-    CK(c->yt.ensure(n * ldt * sizeof(T)), "workspace");
     CK(c->xt.ensure(n * lds * sizeof(T)), "workspace");
     CK(c->zt.ensure(n * lds * sizeof(T)), "workspace");
     CK(c->lists.ensure(n * n * sizeof(int2)), "workspace");
     CK(c->counts.ensure(n * 4), "workspace");
-    afmm_dev::launch_transpose<T>(rhs, ld, n32, n32, c->yt.as<T>(), ldt, s);
-    afmm_dev::launch_compact_reps<T>(c->yt.as<T>(), ldt, n32, n32, c->lists.as<int2>(), n,
-                                     c->counts.as<uint32_t>(), s);
+    afmm_dev::launch_rows<T>(lhs, ld, n32, 0, nullptr, rsum, (uint32_t)r0, (uint32_t)r1, nullptr,
+                             0, nullptr, work, st, s);
+    afmm_dev::launch_transpose_compact<T>(rhs, ld, n32, c->lists.as<int2>(), n,
+                                          c->counts.as<uint32_t>(), s);
     if (rows > 0) {
       afmm_dev::launch_transpose<T>(lhs + r0 * ld, ld, (uint32_t)rows, n32, c->xt.as<T>(), lds,
                                     s);
@@ -418,7 +412,6 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
       c->mark(2);
     }
   }
-  if (rows > 0) afmm_dev::launch_sum_counts(work, zs, (uint32_t)r0, (uint32_t)r1, st, s);
   c->mark(3);
   CK(cudaGetLastError(), "launch");
   CK(cudaMemcpyAsync(c->status_host, st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s),
@@ -598,8 +591,8 @@ void afmm_context_destroy(afmm_context* c) {
     std::lock_guard<std::mutex> g(c->mu);
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    for (DevBuf* b : {&c->status, &c->vec_k, &c->work, &c->zs, &c->lists, &c->counts,
-                      &c->base_copy, &c->yt, &c->xt, &c->zt, &c->part, &c->hx, &c->hy, &c->hz})
+    for (DevBuf* b : {&c->status, &c->vec_k, &c->work, &c->lists, &c->counts, &c->base_copy,
+                      &c->xt, &c->zt, &c->part, &c->hx, &c->hy, &c->hz})
       b->release();
     if (c->status_host) cudaFreeHost(c->status_host);
     for (cudaEvent_t& e : c->ev)
@@ -709,32 +702,26 @@ afmm_status afmm_row_work_device(afmm_context* c, int32_t which_case, int32_t dt
   CK(cudaSetDevice(c->device), "afmm: cudaSetDevice");
   CK(c->vec_k.ensure(n * 8), "workspace");
   CK(c->work.ensure(n * 8), "workspace");
+  CK(c->status.ensure(sizeof(DevStatus)), "workspace");
   cudaStream_t s = c->stream;
   auto* work = c->work.as<unsigned long long>();
+  DevStatus* dst = c->status.as<DevStatus>();
+  CK(cudaMemsetAsync(dst, 0, sizeof(DevStatus), s), "memset");
+  const int cb = which_case == AFMM_CASE_B ? 1 : 0;
+  auto* nnz = c->vec_k.as<uint32_t>();
+  auto* rsum = c->vec_k.as<unsigned long long>();
   if (dtype == AFMM_F64) {
     auto* l = static_cast<const double*>(lhs);
     auto* r = static_cast<const double*>(rhs);
-    if (which_case == AFMM_CASE_B) {
-      afmm_dev::launch_row_nnz<double>(r, ld, (uint32_t)n, c->vec_k.as<uint32_t>(), s);
-      afmm_dev::launch_row_work<double>(l, ld, (uint32_t)n, 1, c->vec_k.as<uint32_t>(), nullptr,
-                                        work, nullptr, s);
-    } else {
-      afmm_dev::launch_row_repsum<double>(r, ld, (uint32_t)n, c->vec_k.as<unsigned long long>(), s);
-      afmm_dev::launch_row_work<double>(l, ld, (uint32_t)n, 0, nullptr,
-                                        c->vec_k.as<unsigned long long>(), work, nullptr, s);
-    }
+    afmm_dev::launch_scan_stats<double>(l, r, ld, (uint32_t)n, cb, dst, nnz, rsum, s);
+    afmm_dev::launch_rows<double>(l, ld, (uint32_t)n, cb, nnz, rsum, 0, 0, nullptr, 0, nullptr,
+                                  work, dst, s);
   } else {
     auto* l = static_cast<const float*>(lhs);
     auto* r = static_cast<const float*>(rhs);
-    if (which_case == AFMM_CASE_B) {
-      afmm_dev::launch_row_nnz<float>(r, ld, (uint32_t)n, c->vec_k.as<uint32_t>(), s);
-      afmm_dev::launch_row_work<float>(l, ld, (uint32_t)n, 1, c->vec_k.as<uint32_t>(), nullptr,
-                                       work, nullptr, s);
-    } else {
-      afmm_dev::launch_row_repsum<float>(r, ld, (uint32_t)n, c->vec_k.as<unsigned long long>(), s);
-      afmm_dev::launch_row_work<float>(l, ld, (uint32_t)n, 0, nullptr,
-                                       c->vec_k.as<unsigned long long>(), work, nullptr, s);
-    }
+    afmm_dev::launch_scan_stats<float>(l, r, ld, (uint32_t)n, cb, dst, nnz, rsum, s);
+    afmm_dev::launch_rows<float>(l, ld, (uint32_t)n, cb, nnz, rsum, 0, 0, nullptr, 0, nullptr,
+                                 work, dst, s);
   }
   CK(cudaMemcpyAsync(work_host, work, n * 8, cudaMemcpyDeviceToHost, s), "work readback");
   CK(cudaStreamSynchronize(s), "work readback");
