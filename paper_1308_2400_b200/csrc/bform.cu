@@ -541,6 +541,9 @@ cudaError_t launch_bform(int shape, const CUtensorMap* tmap, const int2* lists, 
   if (shape == kShapeWide)  // 1024 fp32 / 512 fp64 columns, 1 CTA per SM
     return launch_ring<T, 8, 16, 6, 1>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits,
                                        slice_stride, out, ld_out, st, s);
+  if (shape == kShapeSmall)  // 256 fp32 / 128 fp64 columns x 4 rows, up to 8 CTAs per SM
+    return launch_ring<T, 2, 4, 3, 8>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits,
+                                      slice_stride, out, ld_out, st, s);
   return launch_ring<T, 4, 16, 6, 2>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits,
                                      slice_stride, out, ld_out, st, s);
 }

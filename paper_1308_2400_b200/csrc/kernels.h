@@ -39,8 +39,11 @@ int bform_box_bytes();
 
 // k_bform tile shapes: narrow = 512 fp32 / 256 fp64 columns per CTA, 2 CTAs
 // per SM; wide = 1024 / 512 columns, 32 accumulators per lane, 1 CTA per SM.
+// small = 256 / 128 columns x 4 rows per CTA, for problems too small to fill
+// the GPU with the larger tiles.
 constexpr int kShapeNarrow = 0;
 constexpr int kShapeWide = 1;
+constexpr int kShapeSmall = 2;
 // *splits: requested k slices in, slices launched out (1 = order-preserving).
 // Slice z writes its partial product to out + z * slice_stride.
 template <class T>

@@ -34,6 +34,7 @@ constexpr int kVariantWide = 0;  // TMA smem ring, 1024-column tiles (bform.cu)
 constexpr int kVariantRing = 1;  // TMA smem ring, 512-column tiles (bform.cu)
 constexpr int kVariantDyn = 2;   // TMA smem ring + dynamic (block, row) items (bform.cu)
 constexpr int kVariantL1 = 3;    // decoupled warps, L1-cached base loads (bform_l1.cu)
+constexpr int kVariantSmall = 4; // TMA smem ring, 1 KB-wide x 4-row CTA tiles (bform.cu)
 
 // AFMM_BFORM=wide|ring|dyn|l1 selects the repeated-addition kernel (all are
 // bit-identical; tests/test_gpu_parity.py runs each).
@@ -43,6 +44,7 @@ int variant_from_env() {
   if (v && std::strcmp(v, "dyn") == 0) return kVariantDyn;
   if (v && std::strcmp(v, "l1") == 0) return kVariantL1;
   if (v && std::strcmp(v, "wide") == 0) return kVariantWide;
+  if (v && std::strcmp(v, "small") == 0) return kVariantSmall;
   return kVariantAuto;
 }
 
@@ -276,14 +278,32 @@ afmm_status launch_compute(afmm_context* c, int mode, const T* base, uint64_t kb
                            uint64_t b_cols, uint64_t ldb, uint32_t nrows, int32_t col0,
                            int32_t ncols, T* out, uint64_t ld_out, DevStatus* st,
                            afmm_error* err) {
+  // Tile shape: the widest one whose grid still fills the GPU (per-entry
+  // overhead is amortised over more adds in wider tiles; small problems need
+  // the parallelism of narrow/small tiles). CTA slots per GPU: wide 148
+  // (1/SM), narrow 296 (2/SM), small 1184 (8/SM).
+  const uint64_t cbytes = (uint64_t)ncols * sizeof(T);
+  const uint64_t wide_ctas = (nrows + 15) / 16 * ((cbytes + 4095) / 4096);
+  const uint64_t narrow_ctas = (nrows + 15) / 16 * ((cbytes + 2047) / 2048);
+  const uint64_t small_ctas = (nrows + 3) / 4 * ((cbytes + 1023) / 1024);
+  int shape = afmm_dev::kShapeNarrow;
+  uint64_t ctas = narrow_ctas, slots = 296;
+  if (c->variant == kVariantWide || (c->variant == kVariantAuto && wide_ctas >= 2 * 148)) {
+    shape = afmm_dev::kShapeWide;
+    ctas = wide_ctas;
+    slots = 148;
+  } else if (c->variant == kVariantSmall || (c->variant == kVariantAuto && narrow_ctas < 296)) {
+    shape = afmm_dev::kShapeSmall;
+    ctas = small_ctas;
+    slots = 1184;
+  }
   // Fast mode (reassociated): split the k range into slices when the tile grid
-  // alone cannot fill the GPU (2 CTAs x 148 SMs), then add the slice partials
-  // in a fixed order. Each slice is still the exact repeated-addition chain.
-  const uint64_t narrow_ctas = (nrows + 15) / 16 * ((ncols * sizeof(T) + 2047) / 2048);
+  // alone cannot fill 2 waves, then add the slice partials in a fixed order.
+  // Each slice is still the exact repeated-addition chain.
   const uint64_t nkb = (kb_rows + afmm_dev::bform_kb() - 1) / afmm_dev::bform_kb();
   uint32_t splits = 1;
-  if (mode == AFMM_MODE_FAST && (c->variant == kVariantAuto || c->variant == kVariantRing)) {
-    uint64_t want = (4 * 148) / std::max<uint64_t>(narrow_ctas, 1);
+  if (mode == AFMM_MODE_FAST && c->variant != kVariantDyn && c->variant != kVariantL1) {
+    uint64_t want = (2 * slots + ctas - 1) / std::max<uint64_t>(ctas, 1);
     want = std::min<uint64_t>(want, std::max<uint64_t>(nkb / 4, 1));
     splits = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, 32));
   }
@@ -296,7 +316,7 @@ afmm_status launch_compute(afmm_context* c, int mode, const T* base, uint64_t kb
     const uint64_t ldp = round_up((uint64_t)ncols, 32);
     const uint64_t stride = (uint64_t)nrows * ldp;
     CK(c->part.ensure(stride * splits * sizeof(T)), "workspace");
-    CK(afmm_dev::launch_bform<T>(afmm_dev::kShapeNarrow, &tmap, c->lists.as<int2>(), c->list_cap,
+    CK(afmm_dev::launch_bform<T>(shape, &tmap, c->lists.as<int2>(), c->list_cap,
                                  c->counts.as<uint32_t>(), nrows, col0, ncols, (uint32_t)kb_rows,
                                  &splits, stride, c->part.as<T>(), ldp, st, c->stream),
        "bform");
@@ -316,15 +336,10 @@ afmm_status launch_compute(afmm_context* c, int mode, const T* base, uint64_t kb
                                        (uint32_t)kb_rows, out, ld_out, st, c->stream),
          "bform_dyn");
     else {
-      // wide tiles (1 CTA/SM, 16 rows x 4 KB) need >= ~2 waves of CTAs to pay off
-      const uint64_t wide_ctas = (nrows + 15) / 16 * ((ncols * sizeof(T) + 4095) / 4096);
-      const bool wide = c->variant == kVariantWide ||
-                        (c->variant == kVariantAuto && wide_ctas >= 2 * 148);
       uint32_t one = 1;
-      CK(afmm_dev::launch_bform<T>(
-             wide ? afmm_dev::kShapeWide : afmm_dev::kShapeNarrow, &tmap,
-             c->lists.as<int2>(), c->list_cap, c->counts.as<uint32_t>(), nrows, col0, ncols,
-             (uint32_t)kb_rows, &one, 0, out, ld_out, st, c->stream),
+      CK(afmm_dev::launch_bform<T>(shape, &tmap, c->lists.as<int2>(), c->list_cap,
+                                   c->counts.as<uint32_t>(), nrows, col0, ncols,
+                                   (uint32_t)kb_rows, &one, 0, out, ld_out, st, c->stream),
          "bform");
     }
   } else {
