@@ -292,7 +292,7 @@ afmm_status launch_compute(afmm_context* c, int mode, const T* base, uint64_t kb
     shape = afmm_dev::kShapeWide;
     ctas = wide_ctas;
     slots = 148;
-  } else if (c->variant == kVariantSmall || (c->variant == kVariantAuto && narrow_ctas < 296)) {
+  } else if (c->variant == kVariantSmall || (c->variant == kVariantAuto && narrow_ctas < 148)) {
     shape = afmm_dev::kShapeSmall;
     ctas = small_ctas;
     slots = 1184;
