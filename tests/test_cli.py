@@ -1,0 +1,68 @@
+"""The `afmm_gpu` CLI (tools/afmm_gpu_cli.cpp): the reference CLI's gen/mul flow with
+the B200 kernel ids, restating proj/tests/cli_smoke.cmake:25-34 and :54-57 (integer
+inputs -> the repeated-addition product is byte-identical to the classical one in
+the reference text format; usage errors exit non-zero)."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CLI = os.path.join(ROOT, "build", "afmm_gpu")
+
+
+def _run(*args, cwd):
+    return subprocess.run([CLI, *args], cwd=cwd, capture_output=True, text=True, timeout=300)
+
+
+def _need_cli():
+    if not os.path.exists(CLI):
+        pytest.skip("build/afmm_gpu not built (needs the reference headers at build time)")
+
+
+def test_cli_gen_and_cpu_kernels(tmp_path):
+    _need_cli()
+    assert _run("gen", "--n", "12", "--density", "0.7", "--role", "int", "--mu", "2", "--seed",
+                "7", "--out", "lhs.mat", cwd=tmp_path).returncode == 0
+    assert _run("gen", "--n", "12", "--density", "0.5", "--role", "int", "--mu", "3", "--seed",
+                "8", "--out", "rhs.mat", cwd=tmp_path).returncode == 0
+    r = _run("mul", "lhs.mat", "rhs.mat", "--kernel", "ijk", "--out", "p_ijk.mat", cwd=tmp_path)
+    assert r.returncode == 0 and "multiplications=1728" in r.stdout
+    r = _run("mul", "lhs.mat", "rhs.mat", "--kernel", "afmm-a", "--out", "p_a.mat", cwd=tmp_path)
+    assert r.returncode == 0
+    assert (tmp_path / "p_a.mat").read_bytes() == (tmp_path / "p_ijk.mat").read_bytes()
+    # usage errors (cli_smoke.cmake:54-57)
+    assert _run("mul", "lhs.mat", "missing.mat", "--kernel", "ijk", cwd=tmp_path).returncode != 0
+    assert _run("mul", "lhs.mat", "rhs.mat", "--kernel", "nosuch", cwd=tmp_path).returncode != 0
+    assert _run("frobnicate", cwd=tmp_path).returncode != 0
+
+
+@pytest.mark.gpu
+def test_cli_gpu_kernels_byte_identical(cuda, tmp_path):
+    _need_cli()
+    assert _run("gen", "--n", "12", "--density", "0.7", "--role", "int", "--mu", "2", "--seed",
+                "7", "--out", "lhs.mat", cwd=tmp_path).returncode == 0
+    assert _run("gen", "--n", "12", "--density", "0.5", "--role", "int", "--mu", "3", "--seed",
+                "8", "--out", "rhs.mat", cwd=tmp_path).returncode == 0
+    outs = {}
+    for k in ("ijk", "afmm-a", "afmm-b", "afmm-a-gpu", "afmm-b-gpu"):
+        r = _run("mul", "lhs.mat", "rhs.mat", "--kernel", k, "--out", f"p_{k}.mat", cwd=tmp_path)
+        assert r.returncode == 0, r.stderr
+        outs[k] = ((tmp_path / f"p_{k}.mat").read_bytes(), r.stdout.strip())
+    for k in ("afmm-a", "afmm-b", "afmm-a-gpu", "afmm-b-gpu"):
+        assert outs[k][0] == outs["ijk"][0], k
+    assert outs["afmm-a-gpu"][1] == outs["afmm-a"][1]  # identical OpCounts line
+    assert outs["afmm-b-gpu"][1] == outs["afmm-b"][1]
+    # real-by-integer, bit-exact against the reference CPU kernel in text form
+    assert _run("gen", "--n", "40", "--density", "0.8", "--seed", "3", "--out", "x.mat",
+                cwd=tmp_path).returncode == 0
+    assert _run("gen", "--n", "40", "--density", "0.6", "--role", "int", "--mu", "7", "--seed",
+                "4", "--out", "y.mat", cwd=tmp_path).returncode == 0
+    ra = _run("mul", "x.mat", "y.mat", "--kernel", "afmm-a", "--out", "za.mat", cwd=tmp_path)
+    rg = _run("mul", "x.mat", "y.mat", "--kernel", "afmm-a-gpu", "--out", "zg.mat", cwd=tmp_path)
+    assert ra.returncode == 0 and rg.returncode == 0
+    assert (tmp_path / "za.mat").read_bytes() == (tmp_path / "zg.mat").read_bytes()
+    assert ra.stdout == rg.stdout
+    # non-integer rep -> the reference's domain_error text, exit code 2
+    r = _run("mul", "y.mat", "x.mat", "--kernel", "afmm-a-gpu", cwd=tmp_path)
+    assert r.returncode == 2 and "is not integer-valued" in r.stderr

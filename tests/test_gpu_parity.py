@@ -197,6 +197,29 @@ def test_full_size_row_sample_bit_exact(cuda, oracle, name, kw):
     ctx.close()
 
 
+@pytest.mark.parametrize("case,n,dt", [("a", 3001, np.float32), ("b", 5003, np.float32),
+                                        ("a", 1537, np.float64), ("b", 2049, np.float64)])
+def test_ragged_sizes_every_tile_shape(cuda, oracle, case, n, dt):
+    """n not a multiple of any tile width (wide/narrow/small boundaries), signed reps,
+    -0.0 / tiny bases; bit-exact on a row sample spanning the last partial tiles."""
+    rng = np.random.default_rng(n)
+    bases = rng.uniform(-3, 3, (n, n)).astype(dt)
+    u = rng.random((n, n))
+    bases[u < 0.3] = 0
+    bases[(u >= 0.3) & (u < 0.32)] = -0.0
+    bases[(u >= 0.32) & (u < 0.34)] = 1e-30
+    reps = rng.integers(-12, 13, (n, n)).astype(dt)
+    lhs, rhs = (bases, reps) if case == "a" else (reps, bases)
+    res = _call(case, lhs, rhs)
+    rows = [0, 1, n // 2, n - 2, n - 1]
+    for r in rows:
+        zr, c = oracle.product_mt(case, lhs, rhs, r, r + 1, 1)
+        assert _bits_equal(res.product[r:r + 1], zr), (case, n, r)
+    from paper_1308_2400_b200.gen import expected_additions
+
+    assert res.counts.additions == expected_additions(case, lhs, rhs)
+
+
 @pytest.mark.parametrize("name,n,kw", [
     ("cfg1", 256, {}), ("cfg2", 1024, {}), ("cfg3", 512, {"d1": 0.5, "mu": 4}),
     ("cfg4", 384, {}), ("cfg5", 640, {}),
