@@ -101,24 +101,31 @@ struct Acc;
 
 template <int G>
 struct Acc<float, G> {
+  struct Bases {
+    float2 b[2 * G];
+  };
   float2 a[2 * G];
   __device__ __forceinline__ void zero() {
 #pragma unroll
     for (int c = 0; c < 2 * G; ++c) a[c] = make_float2(0.f, 0.f);
   }
-  __device__ __forceinline__ void run(uint32_t row_addr, int rep) {
-    float2 b[2 * G];
+  __device__ __forceinline__ static Bases load_bases(uint32_t row_addr) {
+    Bases s;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const float4 v = lds128f(row_addr + group_off(g));
-      b[2 * g] = make_float2(v.x, v.y);
-      b[2 * g + 1] = make_float2(v.z, v.w);
+      s.b[2 * g] = make_float2(v.x, v.y);
+      s.b[2 * g + 1] = make_float2(v.z, v.w);
     }
+    return s;
+  }
+  // |rep| sequential `acc += step` per column, step = rep >= 0 ? base : -base
+  // (kernels.hpp:95-104).
+  __device__ __forceinline__ void add(Bases s, int rep) {
     uint32_t t = (uint32_t)rep;
     if (rep < 0) {
-      // step = -base (kernels.hpp:97)
 #pragma unroll
-      for (int c = 0; c < 2 * G; ++c) b[c] = make_float2(negf(b[c].x), negf(b[c].y));
+      for (int c = 0; c < 2 * G; ++c) s.b[c] = make_float2(negf(s.b[c].x), negf(s.b[c].y));
       t = 0u - t;
     }
 #pragma unroll 1
@@ -126,16 +133,17 @@ struct Acc<float, G> {
 #pragma unroll
       for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int c = 0; c < 2 * G; ++c) a[c] = __fadd2_rn(a[c], b[c]);
+        for (int c = 0; c < 2 * G; ++c) a[c] = __fadd2_rn(a[c], s.b[c]);
       t -= 4;
     }
 #pragma unroll 1
     while (t != 0) {
 #pragma unroll
-      for (int c = 0; c < 2 * G; ++c) a[c] = __fadd2_rn(a[c], b[c]);
+      for (int c = 0; c < 2 * G; ++c) a[c] = __fadd2_rn(a[c], s.b[c]);
       t -= 1;
     }
   }
+  __device__ __forceinline__ void run(uint32_t row_addr, int rep) { add(load_bases(row_addr), rep); }
   __device__ __forceinline__ void save(uint32_t z) const {
 #pragma unroll
     for (int g = 0; g < G; ++g)
@@ -173,18 +181,24 @@ struct Acc<double, G> {
 #pragma unroll
     for (int c = 0; c < 2 * G; ++c) a[c] = 0.0;
   }
-  __device__ __forceinline__ void run(uint32_t row_addr, int rep) {
+  struct Bases {
     double b[2 * G];
+  };
+  __device__ __forceinline__ static Bases load_bases(uint32_t row_addr) {
+    Bases s;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const double2 v = lds128d(row_addr + group_off(g));
-      b[2 * g] = v.x;
-      b[2 * g + 1] = v.y;
+      s.b[2 * g] = v.x;
+      s.b[2 * g + 1] = v.y;
     }
+    return s;
+  }
+  __device__ __forceinline__ void add(Bases s, int rep) {
     uint32_t t = (uint32_t)rep;
     if (rep < 0) {
 #pragma unroll
-      for (int c = 0; c < 2 * G; ++c) b[c] = negd(b[c]);
+      for (int c = 0; c < 2 * G; ++c) s.b[c] = negd(s.b[c]);
       t = 0u - t;
     }
 #pragma unroll 1
@@ -192,16 +206,17 @@ struct Acc<double, G> {
 #pragma unroll
       for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int c = 0; c < 2 * G; ++c) a[c] = __dadd_rn(a[c], b[c]);
+        for (int c = 0; c < 2 * G; ++c) a[c] = __dadd_rn(a[c], s.b[c]);
       t -= 4;
     }
 #pragma unroll 1
     while (t != 0) {
 #pragma unroll
-      for (int c = 0; c < 2 * G; ++c) a[c] = __dadd_rn(a[c], b[c]);
+      for (int c = 0; c < 2 * G; ++c) a[c] = __dadd_rn(a[c], s.b[c]);
       t -= 1;
     }
   }
+  __device__ __forceinline__ void run(uint32_t row_addr, int rep) { add(load_bases(row_addr), rep); }
   __device__ __forceinline__ void save(uint32_t z) const {
 #pragma unroll
     for (int g = 0; g < G; ++g) sts128d(z + g * 512, a[2 * g], a[2 * g + 1]);
@@ -380,6 +395,128 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
 }
 
 // ---------------------------------------------------------------------------
+// k_bform_mr: RW output rows per warp over a DENSE rep tile.
+//
+// For small reps the per-entry cost of k_bform is the shared-memory read of
+// the bases (TILE_N * sizeof(T) bytes per warp per entry, at 128 B/clk/SM),
+// not the adds: with |rep| = 1 a 512-column fp32 entry moves 2 KB from smem
+// for 16 FADD2. Here each warp owns RW rows, walks k densely, reads the RW
+// reps of the current k with one broadcast LDS from a staged dense rep tile,
+// and loads the bases once for all RW rows. The rep tile ([k][row] int32,
+// built by the prepass) arrives through the same TMA ring as the bases.
+// Per element the order is unchanged: k ascending, |rep| sequential adds.
+// ---------------------------------------------------------------------------
+
+constexpr int MR_RW = 4;       // rows per warp
+// 15 consumers + 1 producer = 16 warps, so the register allocator can give each
+// thread 128 registers (4 x 16 accumulators + 16 bases); 17 warps cap it at 96.
+constexpr int MR_CW = 15;
+constexpr int MR_ROWS = MR_RW * MR_CW;  // 60 rows per CTA: a 240-byte int32 rep box row
+constexpr int MR_STAGES = 8;
+
+template <class T, int G>
+__host__ __device__ constexpr size_t mr_smem_bytes() {
+  return 1024 + (size_t)MR_STAGES * (Geo<T, G>::STAGE_BYTES + KB * MR_ROWS * 4) +
+         2 * MR_STAGES * sizeof(uint64_t);
+}
+
+__device__ __forceinline__ int4 lds128i(uint32_t addr) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr));
+  return v;
+}
+
+// rmap: dense reps R'[k][row] (int32, rows = B-form rows, inner dimension).
+template <class T, int G>
+__global__ void __launch_bounds__((MR_CW + 1) * 32, 1)
+    k_bform_mr(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap rmap,
+               uint32_t nrows, int32_t col0, int32_t ncols, uint32_t nk, uint32_t nkb,
+               T* __restrict__ out, uint64_t ld_out, int vec_ok,
+               const DevStatus* __restrict__ st) {
+  using Gm = Geo<T, G>;
+  constexpr int REP_STAGE = KB * MR_ROWS * 4;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char* reps = base + MR_STAGES * Gm::STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(reps + MR_STAGES * REP_STAGE);
+  uint64_t* empty = full + MR_STAGES;
+  const uint32_t ring = smem_u32(base), rring = smem_u32(reps);
+
+  if (status_failed(st)) return;  // validation failed: compute nothing (kernels.hpp:115,144)
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t tile_c = blockIdx.y * Gm::TILE_N;
+  const uint32_t row0 = blockIdx.x * MR_ROWS;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < MR_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], MR_CW);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == MR_CW) {
+    if (lane == 0) {
+      prefetch_tensormap(&tmap);
+      prefetch_tensormap(&rmap);
+      uint32_t slot = 0, phase = 0;
+      for (uint32_t kb = 0; kb < nkb; ++kb) {
+        if (kb >= MR_STAGES) mbar_wait(&empty[slot], phase ^ 1);
+        mbar_arrive_expect_tx(&full[slot], (uint32_t)(Gm::STAGE_BYTES + REP_STAGE));
+#pragma unroll
+        for (int h = 0; h < Gm::NBOX; ++h)
+          tma_load_2d(base + slot * Gm::STAGE_BYTES + h * KB * BOX_BYTES, &tmap, &full[slot],
+                      col0 + tile_c + h * Gm::BOX_N, (int32_t)(kb * KB));
+        tma_load_2d(reps + slot * REP_STAGE, &rmap, &full[slot], (int32_t)row0,
+                    (int32_t)(kb * KB));
+        if (++slot == MR_STAGES) {
+          slot = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    return;
+  }
+
+  Acc<T, G> acc[MR_RW];
+#pragma unroll
+  for (int w = 0; w < MR_RW; ++w) acc[w].zero();
+
+  uint32_t slot = 0, phase = 0;
+  for (uint32_t kb = 0; kb < nkb; ++kb) {
+    mbar_wait(&full[slot], phase);
+    const uint32_t bstage = ring + slot * Gm::STAGE_BYTES + lane * 16;
+    const uint32_t rstage = rring + slot * REP_STAGE + warp * (MR_RW * 4);
+    const uint32_t kk_end = nk - kb * KB < (uint32_t)KB ? nk - kb * KB : (uint32_t)KB;
+    for (uint32_t kk = 0; kk < kk_end; ++kk) {
+      const int4 r = lds128i(rstage + kk * (MR_ROWS * 4));  // this warp's RW reps at k
+      if ((r.x | r.y | r.z | r.w) == 0) continue;
+      const typename Acc<T, G>::Bases b = Acc<T, G>::load_bases(bstage + kk * BOX_BYTES);
+      if (r.x) acc[0].add(b, r.x);
+      if (r.y) acc[1].add(b, r.y);
+      if (r.z) acc[2].add(b, r.z);
+      if (r.w) acc[3].add(b, r.w);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+    if (++slot == MR_STAGES) {
+      slot = 0;
+      phase ^= 1;
+    }
+  }
+
+#pragma unroll
+  for (int w = 0; w < MR_RW; ++w) {
+    const uint32_t row = row0 + warp * MR_RW + w;
+    if (row < nrows) acc[w].store(out + (uint64_t)row * ld_out, tile_c, ncols, lane, vec_ok != 0);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // k_bform_dyn: the same TMA ring, but the CTA's rows are not pinned to warps.
 // The unit of work is an ITEM = (k block b, row w), handed out from a CTA-wide
 // counter in b-major order, so any warp takes whichever row is next; a row's
@@ -539,7 +676,8 @@ cudaError_t launch_bform(int shape, const CUtensorMap* tmap, const int2* lists, 
                          uint32_t nk, uint32_t* splits, uint64_t slice_stride, T* out,
                          uint64_t ld_out, const DevStatus* st, cudaStream_t s) {
   if (shape == kShapeWide)  // 1024 fp32 / 512 fp64 columns, 1 CTA per SM
-    return launch_ring<T, 8, 16, 6, 1>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits,
+    // 15 consumers + producer = 16 warps: 128 registers per thread, no spills
+    return launch_ring<T, 8, 15, 6, 1>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits,
                                        slice_stride, out, ld_out, st, s);
   if (shape == kShapeSmall)  // 256 fp32 / 128 fp64 columns x 4 rows, up to 8 CTAs per SM
     return launch_ring<T, 2, 4, 3, 8>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits,
@@ -547,6 +685,35 @@ cudaError_t launch_bform(int shape, const CUtensorMap* tmap, const int2* lists, 
   return launch_ring<T, 4, 16, 6, 2>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits,
                                      slice_stride, out, ld_out, st, s);
 }
+
+int bform_mr_rows() { return MR_ROWS; }
+
+template <class T>
+cudaError_t launch_bform_mr(const CUtensorMap* tmap, const CUtensorMap* rmap, uint32_t nrows,
+                            int32_t col0, int32_t ncols, uint32_t nk, T* out, uint64_t ld_out,
+                            const DevStatus* st, cudaStream_t s) {
+  constexpr int G = 4;
+  auto kern = k_bform_mr<T, G>;
+  const size_t smem = mr_smem_bytes<T, G>();
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  const uint32_t nkb = (nk + KB - 1) / KB;
+  const bool vec_ok = (ld_out * sizeof(T)) % 16 == 0 &&
+                      (reinterpret_cast<uintptr_t>(out) % 16) == 0;
+  dim3 grid((nrows + MR_ROWS - 1) / MR_ROWS, (ncols + Geo<T, G>::TILE_N - 1) / Geo<T, G>::TILE_N);
+  kern<<<grid, (MR_CW + 1) * 32, smem, s>>>(*tmap, *rmap, nrows, col0, ncols, nk, nkb, out,
+                                            ld_out, vec_ok ? 1 : 0, st);
+  note_launch();
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_bform_mr<float>(const CUtensorMap*, const CUtensorMap*, uint32_t,
+                                            int32_t, int32_t, uint32_t, float*, uint64_t,
+                                            const DevStatus*, cudaStream_t);
+template cudaError_t launch_bform_mr<double>(const CUtensorMap*, const CUtensorMap*, uint32_t,
+                                             int32_t, int32_t, uint32_t, double*, uint64_t,
+                                             const DevStatus*, cudaStream_t);
 
 template <class T>
 cudaError_t launch_bform_dyn(const CUtensorMap* tmap, const int2* lists, uint64_t cap,

@@ -57,6 +57,18 @@ template <class T>
 void launch_reduce_slices(const T* part, uint64_t stride, uint64_t ld_part, uint32_t splits,
                           uint32_t rows, uint32_t cols, T* out, uint64_t ld_out, cudaStream_t s);
 
+// Multi-row dense-rep kernel: rmap = int32 reps R'[k][row] (row inner),
+// box bform_mr_rows() x bform_kb().
+int bform_mr_rows();
+template <class T>
+cudaError_t launch_bform_mr(const CUtensorMap* tmap, const CUtensorMap* rmap, uint32_t nrows,
+                            int32_t col0, int32_t ncols, uint32_t nk, T* out, uint64_t ld_out,
+                            const DevStatus* st, cudaStream_t s);
+// Dense int32 reps: dst[r * ld_dst + c] = llround(src[r][c]) (transpose = 0)
+// or llround(src[c][r]) (transpose = 1) over an rows x cols destination.
+template <class T>
+void launch_reps_dense(const T* src, uint64_t ld_src, uint32_t rows, uint32_t cols,
+                       int transpose, int32_t* dst, uint64_t ld_dst, cudaStream_t s);
 template <class T>
 cudaError_t launch_bform_dyn(const CUtensorMap* tmap, const int2* lists, uint64_t cap,
                              const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,

@@ -245,6 +245,42 @@ __global__ void __launch_bounds__(256) k_transpose_compact(const T* __restrict__
   }
 }
 
+// Dense int32 reps for k_bform_mr: dst[r][c] = llround(src[r][c]) or, with
+// transpose, llround(src[c][r]); zero reps stay 0 (value == 0.0 or llround == 0
+// both skip, kernels.hpp:128-130 / :151-153). 32x33 smem tiles.
+template <class T>
+__global__ void k_reps_dense(const T* __restrict__ src, uint64_t ld_src, uint32_t rows,
+                             uint32_t cols, int transpose, int32_t* __restrict__ dst,
+                             uint64_t ld_dst) {
+  __shared__ int32_t tile[32][33];
+  const uint32_t c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  // destination tile rows [r0, r0+32) x cols [c0, c0+32)
+  for (uint32_t dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    int32_t v = 0;
+    if (transpose) {
+      // read src row (c0 + dy), columns r0 + tx  -> dst[r0 + tx][c0 + dy]
+      const uint32_t sr = c0 + dy, sc = r0 + threadIdx.x;
+      if (sr < cols && sc < rows) {
+        const T x = src[(uint64_t)sr * ld_src + sc];
+        if (x != T(0)) v = (int32_t)llround((double)x);
+      }
+    } else {
+      const uint32_t sr = r0 + dy, sc = c0 + threadIdx.x;
+      if (sr < rows && sc < cols) {
+        const T x = src[(uint64_t)sr * ld_src + sc];
+        if (x != T(0)) v = (int32_t)llround((double)x);
+      }
+    }
+    tile[dy][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (uint32_t dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const uint32_t r = r0 + dy, c = c0 + threadIdx.x;
+    if (r < rows && c < cols)
+      dst[(uint64_t)r * ld_dst + c] = transpose ? tile[threadIdx.x][dy] : tile[dy][threadIdx.x];
+  }
+}
+
 // out[c * ld_out + r] = in[r * ld_in + c] for r < rows, c < cols.
 template <class T>
 __global__ void k_transpose(const T* __restrict__ in, uint64_t ld_in, uint32_t rows,
@@ -331,6 +367,14 @@ void launch_transpose(const T* in, uint64_t ld_in, uint32_t rows, uint32_t cols,
 }
 
 template <class T>
+void launch_reps_dense(const T* src, uint64_t ld_src, uint32_t rows, uint32_t cols,
+                       int transpose, int32_t* dst, uint64_t ld_dst, cudaStream_t s) {
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32);
+  k_reps_dense<T><<<grid, dim3(32, 8), 0, s>>>(src, ld_src, rows, cols, transpose, dst, ld_dst);
+  note_launch();
+}
+
+template <class T>
 void launch_reduce_slices(const T* part, uint64_t stride, uint64_t ld_part, uint32_t splits,
                           uint32_t rows, uint32_t cols, T* out, uint64_t ld_out, cudaStream_t s) {
   uint64_t blocks = ((uint64_t)rows * cols + 255) / 256;
@@ -351,6 +395,8 @@ void launch_reduce_slices(const T* part, uint64_t stride, uint64_t ld_part, uint
                                             uint32_t*, cudaStream_t);                          \
   template void launch_transpose<T>(const T*, uint64_t, uint32_t, uint32_t, T*, uint64_t,      \
                                     cudaStream_t);                                             \
+  template void launch_reps_dense<T>(const T*, uint64_t, uint32_t, uint32_t, int, int32_t*,    \
+                                     uint64_t, cudaStream_t);                                  \
   template void launch_reduce_slices<T>(const T*, uint64_t, uint64_t, uint32_t, uint32_t,     \
                                         uint32_t, T*, uint64_t, cudaStream_t);
 

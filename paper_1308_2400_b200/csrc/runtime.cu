@@ -35,6 +35,7 @@ constexpr int kVariantRing = 1;  // TMA smem ring, 512-column tiles (bform.cu)
 constexpr int kVariantDyn = 2;   // TMA smem ring + dynamic (block, row) items (bform.cu)
 constexpr int kVariantL1 = 3;    // decoupled warps, L1-cached base loads (bform_l1.cu)
 constexpr int kVariantSmall = 4; // TMA smem ring, 1 KB-wide x 4-row CTA tiles (bform.cu)
+constexpr int kVariantMR = 5;    // 4 rows per warp over a dense rep tile (bform.cu)
 
 // AFMM_BFORM=wide|ring|dyn|l1 selects the repeated-addition kernel (all are
 // bit-identical; tests/test_gpu_parity.py runs each).
@@ -45,6 +46,7 @@ int variant_from_env() {
   if (v && std::strcmp(v, "l1") == 0) return kVariantL1;
   if (v && std::strcmp(v, "wide") == 0) return kVariantWide;
   if (v && std::strcmp(v, "small") == 0) return kVariantSmall;
+  if (v && std::strcmp(v, "mr") == 0) return kVariantMR;
   return kVariantAuto;
 }
 
@@ -112,6 +114,24 @@ bool make_tmap(CUtensorMap* map, const T* base, uint64_t rows, uint64_t cols, ui
   return r == CUDA_SUCCESS;
 }
 
+// Dense int32 reps R'[k][row] for k_bform_mr: box = 64 rows x KB k's,
+// out-of-range rows read as 0 (no adds).
+bool make_rep_tmap(CUtensorMap* map, const int32_t* reps, uint64_t nk, uint64_t rows,
+                   uint64_t ld) {
+  auto fn = get_encode_fn();
+  if (!fn) return false;
+  const cuuint64_t gdim[2] = {rows, nk};
+  const cuuint64_t gstride[1] = {ld * sizeof(int32_t)};
+  const cuuint32_t box[2] = {(cuuint32_t)afmm_dev::bform_mr_rows(),
+                             (cuuint32_t)afmm_dev::bform_kb()};
+  const cuuint32_t estride[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, const_cast<int32_t*>(reps), gdim,
+                  gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 struct afmm_context {
@@ -119,7 +139,7 @@ struct afmm_context {
   cudaStream_t stream = nullptr;
   std::mutex mu;
   // workspace
-  DevBuf status, vec_k, work, lists, counts, base_copy, xt, zt, part;
+  DevBuf status, vec_k, work, lists, counts, base_copy, xt, zt, part, reps;
   // host-buffer API staging
   DevBuf hx, hy, hz;
   DevStatus* status_host = nullptr;  // pinned
@@ -277,7 +297,21 @@ template <class T>
 afmm_status launch_compute(afmm_context* c, int mode, const T* base, uint64_t kb_rows,
                            uint64_t b_cols, uint64_t ldb, uint32_t nrows, int32_t col0,
                            int32_t ncols, T* out, uint64_t ld_out, DevStatus* st,
-                           afmm_error* err) {
+                           afmm_error* err, const int32_t* reps_dense = nullptr,
+                           uint64_t ld_reps = 0) {
+  if (reps_dense) {
+    // multi-row dense-rep kernel (small reps)
+    CUtensorMap tmap, rmap;
+    if (!make_tmap<T>(&tmap, base, kb_rows, b_cols, ldb) ||
+        !make_rep_tmap(&rmap, reps_dense, kb_rows, nrows, ld_reps)) {
+      set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: cuTensorMapEncodeTiled failed");
+      return AFMM_ERR_CUDA;
+    }
+    CK(afmm_dev::launch_bform_mr<T>(&tmap, &rmap, nrows, col0, ncols, (uint32_t)kb_rows, out,
+                                    ld_out, st, c->stream),
+       "bform_mr");
+    return AFMM_OK;
+  }
   // Tile shape: the widest one whose grid still fills the GPU (per-entry
   // overhead is amortised over more adds in wider tiles; small problems need
   // the parallelism of narrow/small tiles). CTA slots per GPU: wide 148
@@ -393,10 +427,19 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
          "copy");
       base = c->base_copy.as<T>();
     }
+    const bool use_mr = c->variant == kVariantMR && rows > 0;
+    uint64_t ld_r = 0;
+    if (use_mr) {  // dense reps R'[k][i - r0] = llround(X[i][k]) for the slab
+      ld_r = round_up(rows, 4);
+      CK(c->reps.ensure(n * ld_r * sizeof(int32_t)), "workspace");
+      afmm_dev::launch_reps_dense<T>(lhs + r0 * ld, ld, n32, (uint32_t)rows, 1,
+                                     c->reps.as<int32_t>(), ld_r, s);
+    }
     c->mark(1);
     if (rows > 0) {
       afmm_status cs = launch_compute<T>(c, mode, base, n, n, ldb, (uint32_t)rows, 0, (int32_t)n, out,
-                                         ld_out, st, err);
+                                         ld_out, st, err, use_mr ? c->reps.as<int32_t>() : nullptr,
+                                         ld_r);
       if (cs != AFMM_OK) return cs;
     }
     c->mark(2);
@@ -411,14 +454,22 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
     CK(c->counts.ensure(n * 4), "workspace");
     afmm_dev::launch_rows<T>(lhs, ld, n32, 0, nullptr, rsum, (uint32_t)r0, (uint32_t)r1, nullptr,
                              0, nullptr, work, st, s);
-    afmm_dev::launch_transpose_compact<T>(rhs, ld, n32, c->lists.as<int2>(), n,
-                                          c->counts.as<uint32_t>(), s);
+    const bool use_mr = c->variant == kVariantMR && rows > 0;
+    const uint64_t ld_r = round_up(n, 4);
+    if (use_mr) {  // dense reps R'[k][j] = llround(Y[k][j]): Y itself, converted
+      CK(c->reps.ensure(n * ld_r * sizeof(int32_t)), "workspace");
+      afmm_dev::launch_reps_dense<T>(rhs, ld, n32, n32, 0, c->reps.as<int32_t>(), ld_r, s);
+    } else {
+      afmm_dev::launch_transpose_compact<T>(rhs, ld, n32, c->lists.as<int2>(), n,
+                                            c->counts.as<uint32_t>(), s);
+    }
     if (rows > 0) {
       afmm_dev::launch_transpose<T>(lhs + r0 * ld, ld, (uint32_t)rows, n32, c->xt.as<T>(), lds,
                                     s);
       c->mark(1);
       afmm_status cs = launch_compute<T>(c, mode, c->xt.as<T>(), n, rows, lds, n32, 0, (int32_t)rows,
-                                         c->zt.as<T>(), lds, st, err);
+                                         c->zt.as<T>(), lds, st, err,
+                                         use_mr ? c->reps.as<int32_t>() : nullptr, ld_r);
       if (cs != AFMM_OK) return cs;
       c->mark(2);
       afmm_dev::launch_transpose<T>(c->zt.as<T>(), lds, n32, (uint32_t)rows, out, ld_out, s);
@@ -607,7 +658,7 @@ void afmm_context_destroy(afmm_context* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     for (DevBuf* b : {&c->status, &c->vec_k, &c->work, &c->lists, &c->counts, &c->base_copy,
-                      &c->xt, &c->zt, &c->part, &c->hx, &c->hy, &c->hz})
+                      &c->xt, &c->zt, &c->part, &c->reps, &c->hx, &c->hy, &c->hz})
       b->release();
     if (c->status_host) cudaFreeHost(c->status_host);
     for (cudaEvent_t& e : c->ev)
