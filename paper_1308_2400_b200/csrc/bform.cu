@@ -85,13 +85,6 @@ __device__ __forceinline__ void sts128d(uint32_t addr, double a, double b) {
   asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(a), "d"(b) : "memory");
 }
 
-__device__ __forceinline__ float negf(float x) {
-  return __int_as_float(__float_as_int(x) ^ 0x80000000);  // exact -x
-}
-__device__ __forceinline__ double negd(double x) {
-  return __longlong_as_double(__double_as_longlong(x) ^ 0x8000000000000000ll);
-}
-
 // Lane l owns, for g = 0..G-1, the 16-byte column group at byte
 // (g>>1)*KB*BOX_BYTES + (g&1)*512 + l*16 of each staged k row: every 128-bit
 // LDS across the warp reads 512 contiguous bytes (no bank conflict). In
@@ -119,29 +112,33 @@ struct Acc<float, G> {
     }
     return s;
   }
-  // |rep| sequential `acc += step` per column, step = rep >= 0 ? base : -base
-  // (kernels.hpp:95-104).
-  __device__ __forceinline__ void add(Bases s, int rep) {
-    uint32_t t = (uint32_t)rep;
-    if (rep < 0) {
-#pragma unroll
-      for (int c = 0; c < 2 * G; ++c) s.b[c] = make_float2(negf(s.b[c].x), negf(s.b[c].y));
-      t = 0u - t;
-    }
+  // t sequential `acc += step` per column; NEG: step = -base (kernels.hpp:97),
+  // applied as the FADD2 operand-negate modifier (exact), so the shared bases
+  // are never copied or rewritten.
+  template <bool NEG>
+  __device__ __forceinline__ void add_n(const Bases& s, uint32_t t) {
 #pragma unroll 1
     while (t >= 4) {
 #pragma unroll
       for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int c = 0; c < 2 * G; ++c) a[c] = __fadd2_rn(a[c], s.b[c]);
+        for (int c = 0; c < 2 * G; ++c)
+          a[c] = __fadd2_rn(a[c], NEG ? make_float2(-s.b[c].x, -s.b[c].y) : s.b[c]);
       t -= 4;
     }
 #pragma unroll 1
     while (t != 0) {
 #pragma unroll
-      for (int c = 0; c < 2 * G; ++c) a[c] = __fadd2_rn(a[c], s.b[c]);
+      for (int c = 0; c < 2 * G; ++c)
+        a[c] = __fadd2_rn(a[c], NEG ? make_float2(-s.b[c].x, -s.b[c].y) : s.b[c]);
       t -= 1;
     }
+  }
+  // |rep| sequential `acc += step` per column, step = rep >= 0 ? base : -base
+  // (kernels.hpp:95-104).
+  __device__ __forceinline__ void add(const Bases& s, int rep) {
+    if (rep >= 0) add_n<false>(s, (uint32_t)rep);
+    else add_n<true>(s, 0u - (uint32_t)rep);
   }
   __device__ __forceinline__ void run(uint32_t row_addr, int rep) { add(load_bases(row_addr), rep); }
   __device__ __forceinline__ void save(uint32_t z) const {
@@ -194,27 +191,26 @@ struct Acc<double, G> {
     }
     return s;
   }
-  __device__ __forceinline__ void add(Bases s, int rep) {
-    uint32_t t = (uint32_t)rep;
-    if (rep < 0) {
-#pragma unroll
-      for (int c = 0; c < 2 * G; ++c) s.b[c] = negd(s.b[c]);
-      t = 0u - t;
-    }
+  template <bool NEG>
+  __device__ __forceinline__ void add_n(const Bases& s, uint32_t t) {
 #pragma unroll 1
     while (t >= 4) {
 #pragma unroll
       for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int c = 0; c < 2 * G; ++c) a[c] = __dadd_rn(a[c], s.b[c]);
+        for (int c = 0; c < 2 * G; ++c) a[c] = __dadd_rn(a[c], NEG ? -s.b[c] : s.b[c]);
       t -= 4;
     }
 #pragma unroll 1
     while (t != 0) {
 #pragma unroll
-      for (int c = 0; c < 2 * G; ++c) a[c] = __dadd_rn(a[c], s.b[c]);
+      for (int c = 0; c < 2 * G; ++c) a[c] = __dadd_rn(a[c], NEG ? -s.b[c] : s.b[c]);
       t -= 1;
     }
+  }
+  __device__ __forceinline__ void add(const Bases& s, int rep) {
+    if (rep >= 0) add_n<false>(s, (uint32_t)rep);
+    else add_n<true>(s, 0u - (uint32_t)rep);
   }
   __device__ __forceinline__ void run(uint32_t row_addr, int rep) { add(load_bases(row_addr), rep); }
   __device__ __forceinline__ void save(uint32_t z) const {
