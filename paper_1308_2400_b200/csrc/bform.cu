@@ -8,17 +8,18 @@
 // same kernel on transposed operands (afmm_case_a(X,Y) = afmm_case_b(Y^T,X^T)^T,
 // same per-element add sequence).
 //
-// k_bform (one CTA = CW consumer warps + 1 TMA producer warp):
-//   * CTA tile = CW output rows x TILE_N output columns; each consumer warp
-//     owns one output row, each lane 8*G fp32 / 4*G fp64 columns held in
-//     registers for the whole k sweep (register-resident Z tile).
-//   * The producer streams KB x TILE_N tiles of the base matrix B' through a
-//     STAGES-deep smem ring with cp.async.bulk.tensor (TMA) + mbarriers;
-//     the tile is shared by all CW rows of the CTA (CW-fold reuse from smem).
-//   * Each consumer walks its row's compacted (k, rep) list (built by the
+// k_bform (one CTA = CW warps, each owning one output row):
+//   * CTA tile = CW output rows x TILE_N output columns; each lane holds
+//     8*G fp32 / 4*G fp64 columns in registers for the whole k sweep
+//     (register-resident Z tile).
+//   * KB x TILE_N tiles of the base matrix B' stream through a STAGES-deep
+//     smem ring with cp.async.bulk.tensor (TMA) + mbarriers; the tile is
+//     shared by all CW rows of the CTA (CW-fold reuse from smem). The loads
+//     are issued by lane 0 of warp 0 (Pump) without a dedicated producer warp.
+//   * Each warp walks its row's compacted (k, rep) list (built by the
 //     prepass, zero reps already skipped), waits for the stage holding row k,
 //     loads its bases with conflict-free 128-bit LDS and runs the
-//     warp-uniform rep loop: |rep| x 4G FADD2 (fp32) or |rep| x 8G... DADD
+//     warp-uniform rep loop: |rep| x 4G FADD2 (fp32) or |rep| x 4G DADD
 //     (fp64). The rep is uniform across the warp, so there is no divergence;
 //     zero bases are added as +0/-0, which is bit-neutral (the accumulator is
 //     never -0) and never counted.
@@ -74,15 +75,6 @@ __device__ __forceinline__ double2 lds128d(uint32_t addr) {
   double2 v;
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
   return v;
-}
-
-__device__ __forceinline__ void sts128(uint32_t addr, float a, float b, float c, float d) {
-  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c),
-               "f"(d)
-               : "memory");
-}
-__device__ __forceinline__ void sts128d(uint32_t addr, double a, double b) {
-  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(a), "d"(b) : "memory");
 }
 
 // Lane l owns, for g = 0..G-1, the 16-byte column group at byte
@@ -141,19 +133,6 @@ struct Acc<float, G> {
     else add_n<true>(s, 0u - (uint32_t)rep);
   }
   __device__ __forceinline__ void run(uint32_t row_addr, int rep) { add(load_bases(row_addr), rep); }
-  __device__ __forceinline__ void save(uint32_t z) const {
-#pragma unroll
-    for (int g = 0; g < G; ++g)
-      sts128(z + g * 512, a[2 * g].x, a[2 * g].y, a[2 * g + 1].x, a[2 * g + 1].y);
-  }
-  __device__ __forceinline__ void load(uint32_t z) {
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const float4 v = lds128f(z + g * 512);
-      a[2 * g] = make_float2(v.x, v.y);
-      a[2 * g + 1] = make_float2(v.z, v.w);
-    }
-  }
   __device__ __forceinline__ void store(float* out_row, int32_t oc0, int32_t ncols, uint32_t lane,
                                         bool vec_ok) const {
 #pragma unroll
@@ -213,18 +192,6 @@ struct Acc<double, G> {
     else add_n<true>(s, 0u - (uint32_t)rep);
   }
   __device__ __forceinline__ void run(uint32_t row_addr, int rep) { add(load_bases(row_addr), rep); }
-  __device__ __forceinline__ void save(uint32_t z) const {
-#pragma unroll
-    for (int g = 0; g < G; ++g) sts128d(z + g * 512, a[2 * g], a[2 * g + 1]);
-  }
-  __device__ __forceinline__ void load(uint32_t z) {
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const double2 v = lds128d(z + g * 512);
-      a[2 * g] = v.x;
-      a[2 * g + 1] = v.y;
-    }
-  }
   __device__ __forceinline__ void store(double* out_row, int32_t oc0, int32_t ncols,
                                         uint32_t lane, bool vec_ok) const {
 #pragma unroll
@@ -246,29 +213,62 @@ __host__ __device__ constexpr size_t ring_smem_bytes() {
          2 * STAGES * sizeof(uint64_t);
 }
 
-// TMA producer loop (one elected thread): the i-th block of the slice
-// (k block kb_lo + i) goes to slot i % STAGES after all consumers released
-// the block STAGES earlier.
+// The TMA "pump", run by lane 0 of consumer warp 0 (there is no dedicated
+// producer warp: 16 consumer warps split evenly over the 4 SM sub-partitions
+// and keep a 128-register budget). pump() issues, without blocking, every
+// load whose ring slot has been released by all consumers: the i-th block of
+// the slice (k block kb_lo + i) goes to slot i % STAGES once the block
+// STAGES earlier is released. Warp 0 calls it after each of its releases and
+// while it waits for data, so the block the slowest warp needs is always
+// issued (its slot only depends on blocks every warp has passed).
 template <class T, int G, int STAGES>
-__device__ __forceinline__ void produce(const CUtensorMap* tmap, unsigned char* ring,
-                                        uint64_t* full, uint64_t* empty, int32_t col, uint32_t nkb,
-                                        uint32_t kb_lo = 0) {
+struct Pump {
   using Gm = Geo<T, G>;
-  prefetch_tensormap(tmap);
-  uint32_t slot = 0, phase = 0;
-  for (uint32_t kb = 0; kb < nkb; ++kb) {
-    if (kb >= STAGES) mbar_wait(&empty[slot], phase ^ 1);
-    mbar_arrive_expect_tx(&full[slot], (uint32_t)Gm::STAGE_BYTES);
+  const CUtensorMap* tmap;
+  const CUtensorMap* rmap;  // optional dense-rep map (k_bform_mr)
+  unsigned char* ring;
+  unsigned char* rring;
+  uint64_t* full;
+  uint64_t* empty;
+  int32_t col;
+  int32_t rrow;
+  uint32_t nkb;
+  uint32_t kb_lo;
+  uint32_t rep_stage_bytes;
+  uint32_t next;
+  __device__ __forceinline__ void pump() {
+    while (next < nkb) {
+      const uint32_t slot = next % STAGES;
+      if (next >= STAGES && !mbar_test_wait(&empty[slot], ((next / STAGES) - 1) & 1)) return;
+      mbar_arrive_expect_tx(&full[slot], (uint32_t)Gm::STAGE_BYTES + rep_stage_bytes);
+      const int32_t krow = (int32_t)((kb_lo + next) * KB);
 #pragma unroll
-    for (int h = 0; h < Gm::NBOX; ++h)
-      tma_load_2d(ring + slot * Gm::STAGE_BYTES + h * KB * BOX_BYTES, tmap, &full[slot],
-                  col + h * Gm::BOX_N, (int32_t)((kb_lo + kb) * KB));
-    if (++slot == STAGES) {
-      slot = 0;
-      phase ^= 1;
+      for (int h = 0; h < Gm::NBOX; ++h)
+        tma_load_2d(ring + slot * Gm::STAGE_BYTES + h * KB * BOX_BYTES, tmap, &full[slot],
+                    col + h * Gm::BOX_N, krow);
+      if (rmap) tma_load_2d(rring + slot * rep_stage_bytes, rmap, &full[slot], rrow, krow);
+      ++next;
     }
   }
-}
+  // consumer wait for a filled slot; warp 0 keeps pumping while it waits
+  __device__ __forceinline__ void wait_full(uint32_t warp, uint32_t lane, uint32_t slot,
+                                            uint32_t phase) {
+    if (warp == 0) {
+      while (!mbar_test_wait(&full[slot], phase)) {
+        if (lane == 0) pump();
+      }
+    } else {
+      mbar_wait(&full[slot], phase);
+    }
+  }
+  __device__ __forceinline__ void release(uint32_t warp, uint32_t lane, uint32_t slot) {
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&empty[slot]);
+      if (warp == 0) pump();
+    }
+  }
+};
 
 // First list index with k >= key (lists are sorted by k); every lane computes
 // the same answer from broadcast loads.
@@ -288,7 +288,7 @@ __device__ __forceinline__ uint32_t lower_bound_k(const int2* lst, uint32_t cnt,
 // of the nkb_total k blocks and writes to out + z * slice_stride (fast-mode
 // split-k; one slice = the whole k range in order-preserving mode).
 template <class T, int G, int CW, int STAGES, int MINB>
-__global__ void __launch_bounds__((CW + 1) * 32, MINB)
+__global__ void __launch_bounds__(CW * 32, MINB)
     k_bform(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ lists,
             uint64_t cap, const uint32_t* __restrict__ counts, uint32_t nrows, int32_t col0,
             int32_t ncols, uint32_t nkb_total, uint32_t slice_blocks, uint64_t slice_stride,
@@ -320,9 +320,11 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
   }
   __syncthreads();
 
-  if (warp == CW) {
-    if (lane == 0) produce<T, G, STAGES>(&tmap, base, full, empty, col0 + tile_c, nkb, kb_lo);
-    return;
+  Pump<T, G, STAGES> pump{&tmap, nullptr, base, nullptr, full, empty, col0 + tile_c, 0,
+                          nkb, kb_lo, 0, 0};
+  if (warp == 0 && lane == 0) {
+    prefetch_tensormap(&tmap);
+    pump.pump();
   }
 
   // ---- consumers: one output row per warp ----
@@ -346,8 +348,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
   uint32_t kb_cur = 0, slot = 0, phase = 0;
   uint32_t stage_addr = ring + lane * 16;
   auto advance = [&]() {
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[slot]);
+    pump.release(warp, lane, slot);
     ++kb_cur;
     stage_addr += Gm::STAGE_BYTES;
     if (++slot == STAGES) {
@@ -356,7 +357,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
       stage_addr -= STAGES * Gm::STAGE_BYTES;
     }
   };
-  mbar_wait(&full[0], 0);
+  pump.wait_full(warp, lane, 0, 0);
   int2 cur = lane < cnt ? lst[lane] : make_int2(0, 0);
   int2 nxt = 32 + lane < cnt ? lst[32 + lane] : make_int2(0, 0);
   // entry e = (k, rep) broadcast one entry ahead of its use
@@ -374,7 +375,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
     const uint32_t kb = k / KB - kb_lo;  // block index within the slice
     while (kb_cur < kb) {
       advance();
-      mbar_wait(&full[slot], phase);
+      pump.wait_full(warp, lane, slot, phase);
     }
     acc.run(stage_addr + (k % KB) * BOX_BYTES, rep);
     k = k_n;
@@ -384,7 +385,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
   while (true) {
     advance();
     if (kb_cur >= nkb) break;
-    mbar_wait(&full[slot], phase);
+    pump.wait_full(warp, lane, slot, phase);
   }
 
   if (b < nrows) acc.store(out + (uint64_t)b * ld_out, tile_c, ncols, lane, vec_ok != 0);
@@ -404,10 +405,10 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
 // ---------------------------------------------------------------------------
 
 constexpr int MR_RW = 4;       // rows per warp
-// 15 consumers + 1 producer = 16 warps, so the register allocator can give each
-// thread 128 registers (4 x 16 accumulators + 16 bases); 17 warps cap it at 96.
-constexpr int MR_CW = 15;
-constexpr int MR_ROWS = MR_RW * MR_CW;  // 60 rows per CTA: a 240-byte int32 rep box row
+// 16 warps (no producer warp, see Pump): 4 per SM sub-partition and a
+// 128-register budget (4 x 16 accumulators + 16 bases); 17 warps cap it at 96.
+constexpr int MR_CW = 16;
+constexpr int MR_ROWS = MR_RW * MR_CW;  // 64 rows per CTA: a 256-byte int32 rep box row
 constexpr int MR_STAGES = 8;
 
 template <class T, int G>
@@ -426,7 +427,7 @@ __device__ __forceinline__ int4 lds128i(uint32_t addr) {
 
 // rmap: dense reps R'[k][row] (int32, rows = B-form rows, inner dimension).
 template <class T, int G>
-__global__ void __launch_bounds__((MR_CW + 1) * 32, 1)
+__global__ void __launch_bounds__(MR_CW * 32, 1)
     k_bform_mr(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap rmap,
                uint32_t nrows, int32_t col0, int32_t ncols, uint32_t nk, uint32_t nkb,
                T* __restrict__ out, uint64_t ld_out, int vec_ok,
@@ -455,27 +456,12 @@ __global__ void __launch_bounds__((MR_CW + 1) * 32, 1)
   }
   __syncthreads();
 
-  if (warp == MR_CW) {
-    if (lane == 0) {
-      prefetch_tensormap(&tmap);
-      prefetch_tensormap(&rmap);
-      uint32_t slot = 0, phase = 0;
-      for (uint32_t kb = 0; kb < nkb; ++kb) {
-        if (kb >= MR_STAGES) mbar_wait(&empty[slot], phase ^ 1);
-        mbar_arrive_expect_tx(&full[slot], (uint32_t)(Gm::STAGE_BYTES + REP_STAGE));
-#pragma unroll
-        for (int h = 0; h < Gm::NBOX; ++h)
-          tma_load_2d(base + slot * Gm::STAGE_BYTES + h * KB * BOX_BYTES, &tmap, &full[slot],
-                      col0 + tile_c + h * Gm::BOX_N, (int32_t)(kb * KB));
-        tma_load_2d(reps + slot * REP_STAGE, &rmap, &full[slot], (int32_t)row0,
-                    (int32_t)(kb * KB));
-        if (++slot == MR_STAGES) {
-          slot = 0;
-          phase ^= 1;
-        }
-      }
-    }
-    return;
+  Pump<T, G, MR_STAGES> pump{&tmap, &rmap, base, reps, full, empty, col0 + tile_c, (int32_t)row0,
+                             nkb, 0, (uint32_t)REP_STAGE, 0};
+  if (warp == 0 && lane == 0) {
+    prefetch_tensormap(&tmap);
+    prefetch_tensormap(&rmap);
+    pump.pump();
   }
 
   Acc<T, G> acc[MR_RW];
@@ -484,7 +470,7 @@ __global__ void __launch_bounds__((MR_CW + 1) * 32, 1)
 
   uint32_t slot = 0, phase = 0;
   for (uint32_t kb = 0; kb < nkb; ++kb) {
-    mbar_wait(&full[slot], phase);
+    pump.wait_full(warp, lane, slot, phase);
     const uint32_t bstage = ring + slot * Gm::STAGE_BYTES + lane * 16;
     const uint32_t rstage = rring + slot * REP_STAGE + warp * (MR_RW * 4);
     const uint32_t kk_end = nk - kb * KB < (uint32_t)KB ? nk - kb * KB : (uint32_t)KB;
@@ -497,8 +483,7 @@ __global__ void __launch_bounds__((MR_CW + 1) * 32, 1)
       if (r.z) acc[2].add(b, r.z);
       if (r.w) acc[3].add(b, r.w);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[slot]);
+    pump.release(warp, lane, slot);
     if (++slot == MR_STAGES) {
       slot = 0;
       phase ^= 1;
@@ -509,128 +494,6 @@ __global__ void __launch_bounds__((MR_CW + 1) * 32, 1)
   for (int w = 0; w < MR_RW; ++w) {
     const uint32_t row = row0 + warp * MR_RW + w;
     if (row < nrows) acc[w].store(out + (uint64_t)row * ld_out, tile_c, ncols, lane, vec_ok != 0);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// k_bform_dyn: the same TMA ring, but the CTA's rows are not pinned to warps.
-// The unit of work is an ITEM = (k block b, row w), handed out from a CTA-wide
-// counter in b-major order, so any warp takes whichever row is next; a row's
-// accumulators live in registers for the duration of an item and in a
-// ROWS x TILE_N smem tile between items. Per-row order is kept by a per-row
-// "next block" flag (item (w, b) starts only after (w, b-1) has stored its
-// accumulators), so every element still receives its terms in increasing k
-// (kernels.hpp:148-163). Measured: equal to k_bform for large reps, slower for
-// small ones (per-item overhead); kept as a selectable variant.
-// ---------------------------------------------------------------------------
-
-constexpr int DYN_G = 4;
-constexpr int DYN_STAGES = 4;  // power of two
-constexpr int DYN_ROWS = 16;   // rows per CTA (power of two)
-constexpr int DYN_CW = 16;     // consumer warps per CTA
-
-template <class T>
-__host__ __device__ constexpr size_t dyn_smem_bytes() {
-  return 1024 + (size_t)DYN_STAGES * Geo<T, DYN_G>::STAGE_BYTES +
-         (size_t)DYN_ROWS * Geo<T, DYN_G>::ROW_BYTES + 2 * DYN_STAGES * sizeof(uint64_t) +
-         (2 * DYN_ROWS + 4) * sizeof(uint32_t);
-}
-
-template <class T>
-__global__ void __launch_bounds__((DYN_CW + 1) * 32, 2)
-    k_bform_dyn(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ lists,
-                uint64_t cap, const uint32_t* __restrict__ counts, uint32_t nrows, int32_t col0,
-                int32_t ncols, uint32_t nkb, T* __restrict__ out, uint64_t ld_out, int vec_ok,
-                const DevStatus* __restrict__ st) {
-  using Gm = Geo<T, DYN_G>;
-  extern __shared__ unsigned char smem_raw[];
-  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  unsigned char* zs = base + DYN_STAGES * Gm::STAGE_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(zs + DYN_ROWS * Gm::ROW_BYTES);
-  uint64_t* empty = full + DYN_STAGES;
-  volatile uint32_t* row_next = reinterpret_cast<volatile uint32_t*>(empty + DYN_STAGES);
-  uint32_t* cursor = const_cast<uint32_t*>(row_next + DYN_ROWS);
-  uint32_t* item_ctr = cursor + DYN_ROWS;
-  const uint32_t ring = smem_u32(base);
-  const uint32_t zs_addr = smem_u32(zs);
-
-  if (status_failed(st)) return;
-
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t tile_c = blockIdx.y * Gm::TILE_N;
-  const uint32_t row0 = blockIdx.x * DYN_ROWS;
-  const uint32_t rows_here = nrows - row0 < (uint32_t)DYN_ROWS ? nrows - row0 : DYN_ROWS;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < DYN_STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], DYN_ROWS);
-    }
-    *item_ctr = 0;
-    fence_barrier_init();
-  }
-  if (threadIdx.x < DYN_ROWS) {
-    row_next[threadIdx.x] = 0;
-    cursor[threadIdx.x] = 0;
-  }
-  __syncthreads();
-
-  if (warp == DYN_CW) {
-    if (lane == 0) produce<T, DYN_G, DYN_STAGES>(&tmap, base, full, empty, col0 + tile_c, nkb);
-    return;
-  }
-
-  const uint32_t total = nkb * DYN_ROWS;
-  Acc<T, DYN_G> acc;
-  while (true) {
-    uint32_t id = 0;
-    if (lane == 0) id = atomicAdd(item_ctr, 1u);
-    id = __shfl_sync(FULL, id, 0);
-    if (id >= total) break;
-    const uint32_t b = id / DYN_ROWS, w = id % DYN_ROWS;
-    const uint32_t slot = b & (DYN_STAGES - 1);
-    mbar_wait(&full[slot], (b / DYN_STAGES) & 1);
-    if (w < rows_here) {
-      while (row_next[w] != b) {
-      }
-      __threadfence_block();
-      const uint32_t zrow = zs_addr + w * Gm::ROW_BYTES + lane * 16;
-      if (b == 0) acc.zero();
-      else acc.load(zrow);
-      const uint32_t r = row0 + w;
-      const uint32_t cnt = counts[r];
-      const int2* lst = lists + (uint64_t)r * cap;
-      uint32_t p = cursor[w];
-      const uint32_t kend = (b + 1) * KB;
-      const uint32_t stage_addr = ring + slot * Gm::STAGE_BYTES + lane * 16;
-      while (p < cnt) {
-        const int2 e = p + lane < cnt ? lst[p + lane] : make_int2(0x7fffffff, 0);
-        const unsigned in_blk = __ballot_sync(FULL, (uint32_t)e.x < kend);
-        const uint32_t m = __popc(in_blk);
-        for (uint32_t q = 0; q < m; ++q) {
-          const uint32_t k = (uint32_t)__shfl_sync(FULL, e.x, q);
-          const int rep = __shfl_sync(FULL, e.y, q);
-          acc.run(stage_addr + (k % KB) * BOX_BYTES, rep);
-        }
-        p += m;
-        if (m < 32) break;
-      }
-      acc.save(zrow);
-      __syncwarp();
-      if (lane == 0) {
-        cursor[w] = p;
-        __threadfence_block();
-        row_next[w] = b + 1;
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[slot]);
-  }
-
-  asm volatile("bar.sync 1, %0;" ::"r"(DYN_CW * 32) : "memory");
-  for (uint32_t w = warp; w < rows_here; w += DYN_CW) {
-    acc.load(zs_addr + w * Gm::ROW_BYTES + lane * 16);
-    acc.store(out + (uint64_t)(row0 + w) * ld_out, tile_c, ncols, lane, vec_ok != 0);
   }
 }
 
@@ -654,7 +517,7 @@ cudaError_t launch_ring(const CUtensorMap* tmap, const int2* lists, uint64_t cap
                       (reinterpret_cast<uintptr_t>(out) % 16) == 0 &&
                       (slice_stride * sizeof(T)) % 16 == 0;
   dim3 grid((nrows + CW - 1) / CW, (ncols + Geo<T, G>::TILE_N - 1) / Geo<T, G>::TILE_N, *splits);
-  kern<<<grid, (CW + 1) * 32, smem, s>>>(*tmap, lists, cap, counts, nrows, col0, ncols, nkb,
+  kern<<<grid, CW * 32, smem, s>>>(*tmap, lists, cap, counts, nrows, col0, ncols, nkb,
                                          slice_blocks, slice_stride, out, ld_out,
                                          vec_ok ? 1 : 0, st);
   note_launch();
@@ -672,8 +535,8 @@ cudaError_t launch_bform(int shape, const CUtensorMap* tmap, const int2* lists, 
                          uint32_t nk, uint32_t* splits, uint64_t slice_stride, T* out,
                          uint64_t ld_out, const DevStatus* st, cudaStream_t s) {
   if (shape == kShapeWide)  // 1024 fp32 / 512 fp64 columns, 1 CTA per SM
-    // 15 consumers + producer = 16 warps: 128 registers per thread, no spills
-    return launch_ring<T, 8, 15, 6, 1>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits,
+    // 16 warps (no producer warp): 128 registers per thread, no spills
+    return launch_ring<T, 8, 16, 6, 1>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits,
                                        slice_stride, out, ld_out, st, s);
   if (shape == kShapeSmall)  // 256 fp32 / 128 fp64 columns x 4 rows, up to 8 CTAs per SM
     return launch_ring<T, 2, 4, 3, 8>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits,
@@ -681,6 +544,15 @@ cudaError_t launch_bform(int shape, const CUtensorMap* tmap, const int2* lists, 
   return launch_ring<T, 4, 16, 6, 2>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits,
                                      slice_stride, out, ld_out, st, s);
 }
+
+template cudaError_t launch_bform<float>(int, const CUtensorMap*, const int2*, uint64_t,
+                                         const uint32_t*, uint32_t, int32_t, int32_t, uint32_t,
+                                         uint32_t*, uint64_t, float*, uint64_t, const DevStatus*,
+                                         cudaStream_t);
+template cudaError_t launch_bform<double>(int, const CUtensorMap*, const int2*, uint64_t,
+                                          const uint32_t*, uint32_t, int32_t, int32_t, uint32_t,
+                                          uint32_t*, uint64_t, double*, uint64_t,
+                                          const DevStatus*, cudaStream_t);
 
 int bform_mr_rows() { return MR_ROWS; }
 
@@ -698,7 +570,7 @@ cudaError_t launch_bform_mr(const CUtensorMap* tmap, const CUtensorMap* rmap, ui
   const bool vec_ok = (ld_out * sizeof(T)) % 16 == 0 &&
                       (reinterpret_cast<uintptr_t>(out) % 16) == 0;
   dim3 grid((nrows + MR_ROWS - 1) / MR_ROWS, (ncols + Geo<T, G>::TILE_N - 1) / Geo<T, G>::TILE_N);
-  kern<<<grid, (MR_CW + 1) * 32, smem, s>>>(*tmap, *rmap, nrows, col0, ncols, nk, nkb, out,
+  kern<<<grid, MR_CW * 32, smem, s>>>(*tmap, *rmap, nrows, col0, ncols, nk, nkb, out,
                                             ld_out, vec_ok ? 1 : 0, st);
   note_launch();
   return cudaGetLastError();
@@ -710,43 +582,5 @@ template cudaError_t launch_bform_mr<float>(const CUtensorMap*, const CUtensorMa
 template cudaError_t launch_bform_mr<double>(const CUtensorMap*, const CUtensorMap*, uint32_t,
                                              int32_t, int32_t, uint32_t, double*, uint64_t,
                                              const DevStatus*, cudaStream_t);
-
-template <class T>
-cudaError_t launch_bform_dyn(const CUtensorMap* tmap, const int2* lists, uint64_t cap,
-                             const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,
-                             uint32_t nk, T* out, uint64_t ld_out, const DevStatus* st,
-                             cudaStream_t s) {
-  const size_t smem = dyn_smem_bytes<T>();
-  cudaError_t e = cudaFuncSetAttribute(k_bform_dyn<T>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  const uint32_t nkb = (nk + KB - 1) / KB;
-  const bool vec_ok = (ld_out * sizeof(T)) % 16 == 0 &&
-                      (reinterpret_cast<uintptr_t>(out) % 16) == 0;
-  dim3 grid((nrows + DYN_ROWS - 1) / DYN_ROWS,
-            (ncols + Geo<T, DYN_G>::TILE_N - 1) / Geo<T, DYN_G>::TILE_N);
-  k_bform_dyn<T><<<grid, (DYN_CW + 1) * 32, smem, s>>>(*tmap, lists, cap, counts, nrows, col0,
-                                                       ncols, nkb, out, ld_out, vec_ok ? 1 : 0,
-                                                       st);
-  note_launch();
-  return cudaGetLastError();
-}
-
-template cudaError_t launch_bform<float>(int, const CUtensorMap*, const int2*, uint64_t,
-                                         const uint32_t*, uint32_t, int32_t, int32_t, uint32_t,
-                                         uint32_t*, uint64_t, float*, uint64_t, const DevStatus*,
-                                         cudaStream_t);
-template cudaError_t launch_bform<double>(int, const CUtensorMap*, const int2*, uint64_t,
-                                          const uint32_t*, uint32_t, int32_t, int32_t, uint32_t,
-                                          uint32_t*, uint64_t, double*, uint64_t,
-                                          const DevStatus*, cudaStream_t);
-template cudaError_t launch_bform_dyn<float>(const CUtensorMap*, const int2*, uint64_t,
-                                             const uint32_t*, uint32_t, int32_t, int32_t,
-                                             uint32_t, float*, uint64_t, const DevStatus*,
-                                             cudaStream_t);
-template cudaError_t launch_bform_dyn<double>(const CUtensorMap*, const int2*, uint64_t,
-                                              const uint32_t*, uint32_t, int32_t, int32_t,
-                                              uint32_t, double*, uint64_t, const DevStatus*,
-                                              cudaStream_t);
 
 }  // namespace afmm_dev

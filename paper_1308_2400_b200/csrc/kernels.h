@@ -69,15 +69,6 @@ cudaError_t launch_bform_mr(const CUtensorMap* tmap, const CUtensorMap* rmap, ui
 template <class T>
 void launch_reps_dense(const T* src, uint64_t ld_src, uint32_t rows, uint32_t cols,
                        int transpose, int32_t* dst, uint64_t ld_dst, cudaStream_t s);
-template <class T>
-cudaError_t launch_bform_dyn(const CUtensorMap* tmap, const int2* lists, uint64_t cap,
-                             const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,
-                             uint32_t nk, T* out, uint64_t ld_out, const DevStatus* st,
-                             cudaStream_t s);
-template <class T>
-cudaError_t launch_bform_l1(const T* base, uint64_t ldb, const int2* lists, uint64_t cap,
-                            const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,
-                            T* out, uint64_t ld_out, const DevStatus* st, cudaStream_t s);
 
 // FP-add peak microbenchmark (peak.cu)
 cudaError_t run_peak(int dtype, double* adds_per_second, double* sm_mhz);

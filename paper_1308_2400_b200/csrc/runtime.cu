@@ -29,21 +29,17 @@ void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 namespace {
 
 constexpr uint64_t kNone = ~0ull;
-constexpr int kVariantAuto = -1; // wide when the problem fills the GPU with wide tiles, else ring
+constexpr int kVariantAuto = -1; // shape chosen from the problem (launch_compute)
 constexpr int kVariantWide = 0;  // TMA smem ring, 1024-column tiles (bform.cu)
 constexpr int kVariantRing = 1;  // TMA smem ring, 512-column tiles (bform.cu)
-constexpr int kVariantDyn = 2;   // TMA smem ring + dynamic (block, row) items (bform.cu)
-constexpr int kVariantL1 = 3;    // decoupled warps, L1-cached base loads (bform_l1.cu)
 constexpr int kVariantSmall = 4; // TMA smem ring, 1 KB-wide x 4-row CTA tiles (bform.cu)
 constexpr int kVariantMR = 5;    // 4 rows per warp over a dense rep tile (bform.cu)
 
-// AFMM_BFORM=wide|ring|dyn|l1 selects the repeated-addition kernel (all are
-// bit-identical; tests/test_gpu_parity.py runs each).
+// AFMM_BFORM=wide|ring|small|mr forces one repeated-addition kernel (all are
+// bit-identical; tests/test_gpu_parity.py runs each). Default: auto.
 int variant_from_env() {
   const char* v = std::getenv("AFMM_BFORM");
   if (v && std::strcmp(v, "ring") == 0) return kVariantRing;
-  if (v && std::strcmp(v, "dyn") == 0) return kVariantDyn;
-  if (v && std::strcmp(v, "l1") == 0) return kVariantL1;
   if (v && std::strcmp(v, "wide") == 0) return kVariantWide;
   if (v && std::strcmp(v, "small") == 0) return kVariantSmall;
   if (v && std::strcmp(v, "mr") == 0) return kVariantMR;
@@ -336,17 +332,17 @@ afmm_status launch_compute(afmm_context* c, int mode, const T* base, uint64_t kb
   // Each slice is still the exact repeated-addition chain.
   const uint64_t nkb = (kb_rows + afmm_dev::bform_kb() - 1) / afmm_dev::bform_kb();
   uint32_t splits = 1;
-  if (mode == AFMM_MODE_FAST && c->variant != kVariantDyn && c->variant != kVariantL1) {
+  if (mode == AFMM_MODE_FAST) {
     uint64_t want = (2 * slots + ctas - 1) / std::max<uint64_t>(ctas, 1);
     want = std::min<uint64_t>(want, std::max<uint64_t>(nkb / 4, 1));
     splits = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, 32));
   }
+  CUtensorMap tmap;
+  if (!make_tmap<T>(&tmap, base, kb_rows, b_cols, ldb)) {
+    set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: cuTensorMapEncodeTiled failed");
+    return AFMM_ERR_CUDA;
+  }
   if (splits > 1) {
-    CUtensorMap tmap;
-    if (!make_tmap<T>(&tmap, base, kb_rows, b_cols, ldb)) {
-      set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: cuTensorMapEncodeTiled failed");
-      return AFMM_ERR_CUDA;
-    }
     const uint64_t ldp = round_up((uint64_t)ncols, 32);
     const uint64_t stride = (uint64_t)nrows * ldp;
     CK(c->part.ensure(stride * splits * sizeof(T)), "workspace");
@@ -358,30 +354,11 @@ afmm_status launch_compute(afmm_context* c, int mode, const T* base, uint64_t kb
                                       (uint32_t)ncols, out, ld_out, c->stream);
     return AFMM_OK;
   }
-  if (c->variant != kVariantL1) {
-    CUtensorMap tmap;
-    if (!make_tmap<T>(&tmap, base, kb_rows, b_cols, ldb)) {
-      set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: cuTensorMapEncodeTiled failed");
-      return AFMM_ERR_CUDA;
-    }
-    if (c->variant == kVariantDyn)
-      CK(afmm_dev::launch_bform_dyn<T>(&tmap, c->lists.as<int2>(), c->list_cap,
-                                       c->counts.as<uint32_t>(), nrows, col0, ncols,
-                                       (uint32_t)kb_rows, out, ld_out, st, c->stream),
-         "bform_dyn");
-    else {
-      uint32_t one = 1;
-      CK(afmm_dev::launch_bform<T>(shape, &tmap, c->lists.as<int2>(), c->list_cap,
-                                   c->counts.as<uint32_t>(), nrows, col0, ncols,
-                                   (uint32_t)kb_rows, &one, 0, out, ld_out, st, c->stream),
-         "bform");
-    }
-  } else {
-    CK(afmm_dev::launch_bform_l1<T>(base, ldb, c->lists.as<int2>(), c->list_cap,
-                                    c->counts.as<uint32_t>(), nrows, col0, ncols, out, ld_out, st,
-                                    c->stream),
-       "bform_l1");
-  }
+  uint32_t one = 1;
+  CK(afmm_dev::launch_bform<T>(shape, &tmap, c->lists.as<int2>(), c->list_cap,
+                               c->counts.as<uint32_t>(), nrows, col0, ncols, (uint32_t)kb_rows,
+                               &one, 0, out, ld_out, st, c->stream),
+     "bform");
   return AFMM_OK;
 }
 
