@@ -254,8 +254,9 @@ struct Pump {
   __device__ __forceinline__ void wait_full(uint32_t warp, uint32_t lane, uint32_t slot,
                                             uint32_t phase) {
     if (warp == 0) {
-      while (!mbar_test_wait(&full[slot], phase)) {
+      while (true) {
         if (lane == 0) pump();
+        if (mbar_try_wait(&full[slot], phase)) break;  // suspends briefly, no hot spin
       }
     } else {
       mbar_wait(&full[slot], phase);
@@ -378,6 +379,10 @@ __global__ void __launch_bounds__(CW * 32, MINB)
       pump.wait_full(warp, lane, slot, phase);
     }
     acc.run(stage_addr + (k % KB) * BOX_BYTES, rep);
+    // Rows progress unevenly, so the slot the slowest warp frees must be
+    // refilled promptly: warp 0 polls the ring after every entry, not only
+    // at its own block boundaries.
+    if (warp == 0 && lane == 0) pump.pump();
     k = k_n;
     rep = rep_n;
   }
