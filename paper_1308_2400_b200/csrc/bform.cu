@@ -8,14 +8,14 @@
 // same kernel on transposed operands (afmm_case_a(X,Y) = afmm_case_b(Y^T,X^T)^T,
 // same per-element add sequence).
 //
-// k_bform (one CTA = CW warps, each owning one output row):
+// k_bform (one CTA = CW consumer warps, each owning one output row, + 1 TMA
+// producer warp):
 //   * CTA tile = CW output rows x TILE_N output columns; each lane holds
 //     8*G fp32 / 4*G fp64 columns in registers for the whole k sweep
 //     (register-resident Z tile).
 //   * KB x TILE_N tiles of the base matrix B' stream through a STAGES-deep
 //     smem ring with cp.async.bulk.tensor (TMA) + mbarriers; the tile is
-//     shared by all CW rows of the CTA (CW-fold reuse from smem). The loads
-//     are issued by lane 0 of warp 0 (Pump) without a dedicated producer warp.
+//     shared by all CW rows of the CTA (CW-fold reuse from smem).
 //   * Each warp walks its row's compacted (k, rep) list (built by the
 //     prepass, zero reps already skipped), waits for the stage holding row k,
 //     loads its bases with conflict-free 128-bit LDS and runs the
@@ -289,7 +289,7 @@ __device__ __forceinline__ uint32_t lower_bound_k(const int2* lst, uint32_t cnt,
 // of the nkb_total k blocks and writes to out + z * slice_stride (fast-mode
 // split-k; one slice = the whole k range in order-preserving mode).
 template <class T, int G, int CW, int STAGES, int MINB>
-__global__ void __launch_bounds__(CW * 32, MINB)
+__global__ void __launch_bounds__((CW + 1) * 32, MINB)
     k_bform(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ lists,
             uint64_t cap, const uint32_t* __restrict__ counts, uint32_t nrows, int32_t col0,
             int32_t ncols, uint32_t nkb_total, uint32_t slice_blocks, uint64_t slice_stride,
@@ -321,11 +321,21 @@ __global__ void __launch_bounds__(CW * 32, MINB)
   }
   __syncthreads();
 
-  Pump<T, G, STAGES> pump{&tmap, nullptr, base, nullptr, full, empty, col0 + tile_c, 0,
-                          nkb, kb_lo, 0, 0};
-  if (warp == 0 && lane == 0) {
-    prefetch_tensormap(&tmap);
-    pump.pump();
+  if (warp == CW) {
+    // ---- dedicated TMA producer warp ----
+    // (Unlike k_bform_mr, the list-walking warps progress unevenly; an
+    // in-warp pump makes warp 0 the ring's bottleneck: measured 2-3x slower.)
+    if (lane == 0) {
+      Pump<T, G, STAGES> pump{&tmap, nullptr, base, nullptr, full, empty, col0 + tile_c, 0,
+                              nkb, kb_lo, 0, 0};
+      prefetch_tensormap(&tmap);
+      while (true) {
+        pump.pump();
+        if (pump.next >= nkb) break;
+        mbar_wait(&empty[pump.next % STAGES], ((pump.next / STAGES) - 1) & 1);
+      }
+    }
+    return;
   }
 
   // ---- consumers: one output row per warp ----
@@ -349,7 +359,8 @@ __global__ void __launch_bounds__(CW * 32, MINB)
   uint32_t kb_cur = 0, slot = 0, phase = 0;
   uint32_t stage_addr = ring + lane * 16;
   auto advance = [&]() {
-    pump.release(warp, lane, slot);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
     ++kb_cur;
     stage_addr += Gm::STAGE_BYTES;
     if (++slot == STAGES) {
@@ -358,7 +369,7 @@ __global__ void __launch_bounds__(CW * 32, MINB)
       stage_addr -= STAGES * Gm::STAGE_BYTES;
     }
   };
-  pump.wait_full(warp, lane, 0, 0);
+  mbar_wait(&full[0], 0);
   int2 cur = lane < cnt ? lst[lane] : make_int2(0, 0);
   int2 nxt = 32 + lane < cnt ? lst[32 + lane] : make_int2(0, 0);
   // entry e = (k, rep) broadcast one entry ahead of its use
@@ -376,13 +387,9 @@ __global__ void __launch_bounds__(CW * 32, MINB)
     const uint32_t kb = k / KB - kb_lo;  // block index within the slice
     while (kb_cur < kb) {
       advance();
-      pump.wait_full(warp, lane, slot, phase);
+      mbar_wait(&full[slot], phase);
     }
     acc.run(stage_addr + (k % KB) * BOX_BYTES, rep);
-    // Rows progress unevenly, so the slot the slowest warp frees must be
-    // refilled promptly: warp 0 polls the ring after every entry, not only
-    // at its own block boundaries.
-    if (warp == 0 && lane == 0) pump.pump();
     k = k_n;
     rep = rep_n;
   }
@@ -390,7 +397,7 @@ __global__ void __launch_bounds__(CW * 32, MINB)
   while (true) {
     advance();
     if (kb_cur >= nkb) break;
-    pump.wait_full(warp, lane, slot, phase);
+    mbar_wait(&full[slot], phase);
   }
 
   if (b < nrows) acc.store(out + (uint64_t)b * ld_out, tile_c, ncols, lane, vec_ok != 0);
@@ -522,7 +529,7 @@ cudaError_t launch_ring(const CUtensorMap* tmap, const int2* lists, uint64_t cap
                       (reinterpret_cast<uintptr_t>(out) % 16) == 0 &&
                       (slice_stride * sizeof(T)) % 16 == 0;
   dim3 grid((nrows + CW - 1) / CW, (ncols + Geo<T, G>::TILE_N - 1) / Geo<T, G>::TILE_N, *splits);
-  kern<<<grid, CW * 32, smem, s>>>(*tmap, lists, cap, counts, nrows, col0, ncols, nkb,
+  kern<<<grid, (CW + 1) * 32, smem, s>>>(*tmap, lists, cap, counts, nrows, col0, ncols, nkb,
                                          slice_blocks, slice_stride, out, ld_out,
                                          vec_ok ? 1 : 0, st);
   note_launch();
@@ -540,7 +547,7 @@ cudaError_t launch_bform(int shape, const CUtensorMap* tmap, const int2* lists, 
                          uint32_t nk, uint32_t* splits, uint64_t slice_stride, T* out,
                          uint64_t ld_out, const DevStatus* st, cudaStream_t s) {
   if (shape == kShapeWide)  // 1024 fp32 / 512 fp64 columns, 1 CTA per SM
-    // 16 warps (no producer warp): 128 registers per thread, no spills
+    // 16 consumers + producer (17 warps: a 96-register budget)
     return launch_ring<T, 8, 16, 6, 1>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits,
                                        slice_stride, out, ld_out, st, s);
   if (shape == kShapeSmall)  // 256 fp32 / 128 fp64 columns x 4 rows, up to 8 CTAs per SM
