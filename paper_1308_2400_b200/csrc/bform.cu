@@ -550,6 +550,9 @@ cudaError_t launch_bform(int shape, const CUtensorMap* tmap, const int2* lists, 
     // 16 consumers + producer (17 warps: a 96-register budget)
     return launch_ring<T, 8, 16, 6, 1>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits,
                                        slice_stride, out, ld_out, st, s);
+  if (shape == kShapeWide12)  // 12 consumers + producer: 128-register budget, 3 per SMSP
+    return launch_ring<T, 8, 12, 6, 1>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits,
+                                       slice_stride, out, ld_out, st, s);
   if (shape == kShapeSmall)  // 256 fp32 / 128 fp64 columns x 4 rows, up to 8 CTAs per SM
     return launch_ring<T, 2, 4, 3, 8>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits,
                                       slice_stride, out, ld_out, st, s);
