@@ -213,14 +213,13 @@ __host__ __device__ constexpr size_t ring_smem_bytes() {
          2 * STAGES * sizeof(uint64_t);
 }
 
-// The TMA "pump", run by lane 0 of consumer warp 0 (there is no dedicated
-// producer warp: 16 consumer warps split evenly over the 4 SM sub-partitions
-// and keep a 128-register budget). pump() issues, without blocking, every
-// load whose ring slot has been released by all consumers: the i-th block of
-// the slice (k block kb_lo + i) goes to slot i % STAGES once the block
-// STAGES earlier is released. Warp 0 calls it after each of its releases and
-// while it waits for data, so the block the slowest warp needs is always
-// issued (its slot only depends on blocks every warp has passed).
+// TMA issue logic of the producer warp (lane 0). pump() issues, without
+// blocking, every load whose ring slot has been released by all consumers:
+// the i-th block of the slice (k block kb_lo + i) goes to slot i % STAGES
+// once the block STAGES earlier is released. The producer alternates pump()
+// with a suspending wait on the next slot's empty barrier. (An in-consumer
+// variant that let warp 0 pump between its own entries was measured 2-3x
+// slower: the pumping warp becomes the ring's slowest consumer.)
 template <class T, int G, int STAGES>
 struct Pump {
   using Gm = Geo<T, G>;
@@ -248,25 +247,6 @@ struct Pump {
                     col + h * Gm::BOX_N, krow);
       if (rmap) tma_load_2d(rring + slot * rep_stage_bytes, rmap, &full[slot], rrow, krow);
       ++next;
-    }
-  }
-  // consumer wait for a filled slot; warp 0 keeps pumping while it waits
-  __device__ __forceinline__ void wait_full(uint32_t warp, uint32_t lane, uint32_t slot,
-                                            uint32_t phase) {
-    if (warp == 0) {
-      while (true) {
-        if (lane == 0) pump();
-        if (mbar_try_wait(&full[slot], phase)) break;  // suspends briefly, no hot spin
-      }
-    } else {
-      mbar_wait(&full[slot], phase);
-    }
-  }
-  __device__ __forceinline__ void release(uint32_t warp, uint32_t lane, uint32_t slot) {
-    __syncwarp();
-    if (lane == 0) {
-      mbar_arrive(&empty[slot]);
-      if (warp == 0) pump();
     }
   }
 };
@@ -417,10 +397,10 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
 // ---------------------------------------------------------------------------
 
 constexpr int MR_RW = 4;       // rows per warp
-// 16 warps (no producer warp, see Pump): 4 per SM sub-partition and a
+// 12 consumer warps + 1 producer: 3 consumers per SM sub-partition and a
 // 128-register budget (4 x 16 accumulators + 16 bases); 17 warps cap it at 96.
-constexpr int MR_CW = 16;
-constexpr int MR_ROWS = MR_RW * MR_CW;  // 64 rows per CTA: a 256-byte int32 rep box row
+constexpr int MR_CW = 12;
+constexpr int MR_ROWS = MR_RW * MR_CW;  // 48 rows per CTA: a 192-byte int32 rep box row
 constexpr int MR_STAGES = 8;
 
 template <class T, int G>
@@ -439,7 +419,7 @@ __device__ __forceinline__ int4 lds128i(uint32_t addr) {
 
 // rmap: dense reps R'[k][row] (int32, rows = B-form rows, inner dimension).
 template <class T, int G>
-__global__ void __launch_bounds__(MR_CW * 32, 1)
+__global__ void __launch_bounds__((MR_CW + 1) * 32, 1)
     k_bform_mr(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap rmap,
                uint32_t nrows, int32_t col0, int32_t ncols, uint32_t nk, uint32_t nkb,
                T* __restrict__ out, uint64_t ld_out, int vec_ok,
@@ -468,12 +448,20 @@ __global__ void __launch_bounds__(MR_CW * 32, 1)
   }
   __syncthreads();
 
-  Pump<T, G, MR_STAGES> pump{&tmap, &rmap, base, reps, full, empty, col0 + tile_c, (int32_t)row0,
-                             nkb, 0, (uint32_t)REP_STAGE, 0};
-  if (warp == 0 && lane == 0) {
-    prefetch_tensormap(&tmap);
-    prefetch_tensormap(&rmap);
-    pump.pump();
+  if (warp == MR_CW) {
+    // ---- dedicated TMA producer warp: base tile + dense rep tile per stage ----
+    if (lane == 0) {
+      Pump<T, G, MR_STAGES> pump{&tmap, &rmap, base, reps, full, empty, col0 + tile_c,
+                                 (int32_t)row0, nkb, 0, (uint32_t)REP_STAGE, 0};
+      prefetch_tensormap(&tmap);
+      prefetch_tensormap(&rmap);
+      while (true) {
+        pump.pump();
+        if (pump.next >= nkb) break;
+        mbar_wait(&empty[pump.next % MR_STAGES], ((pump.next / MR_STAGES) - 1) & 1);
+      }
+    }
+    return;
   }
 
   Acc<T, G> acc[MR_RW];
@@ -482,7 +470,7 @@ __global__ void __launch_bounds__(MR_CW * 32, 1)
 
   uint32_t slot = 0, phase = 0;
   for (uint32_t kb = 0; kb < nkb; ++kb) {
-    pump.wait_full(warp, lane, slot, phase);
+    mbar_wait(&full[slot], phase);
     const uint32_t bstage = ring + slot * Gm::STAGE_BYTES + lane * 16;
     const uint32_t rstage = rring + slot * REP_STAGE + warp * (MR_RW * 4);
     const uint32_t kk_end = nk - kb * KB < (uint32_t)KB ? nk - kb * KB : (uint32_t)KB;
@@ -495,7 +483,8 @@ __global__ void __launch_bounds__(MR_CW * 32, 1)
       if (r.z) acc[2].add(b, r.z);
       if (r.w) acc[3].add(b, r.w);
     }
-    pump.release(warp, lane, slot);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
     if (++slot == MR_STAGES) {
       slot = 0;
       phase ^= 1;
@@ -547,10 +536,9 @@ cudaError_t launch_bform(int shape, const CUtensorMap* tmap, const int2* lists, 
                          uint32_t nk, uint32_t* splits, uint64_t slice_stride, T* out,
                          uint64_t ld_out, const DevStatus* st, cudaStream_t s) {
   if (shape == kShapeWide)  // 1024 fp32 / 512 fp64 columns, 1 CTA per SM
-    // 16 consumers + producer (17 warps: a 96-register budget)
-    return launch_ring<T, 8, 16, 6, 1>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits,
-                                       slice_stride, out, ld_out, st, s);
-  if (shape == kShapeWide12)  // 12 consumers + producer: 128-register budget, 3 per SMSP
+    // 12 consumers + producer: 3 consumers per SM sub-partition and a
+    // 128-register budget (16 consumers + producer = 17 warps caps it at 96
+    // and spills; measured 88% vs 90% of peak at rep 16, tools/sweep.py)
     return launch_ring<T, 8, 12, 6, 1>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits,
                                        slice_stride, out, ld_out, st, s);
   if (shape == kShapeSmall)  // 256 fp32 / 128 fp64 columns x 4 rows, up to 8 CTAs per SM
@@ -585,7 +573,7 @@ cudaError_t launch_bform_mr(const CUtensorMap* tmap, const CUtensorMap* rmap, ui
   const bool vec_ok = (ld_out * sizeof(T)) % 16 == 0 &&
                       (reinterpret_cast<uintptr_t>(out) % 16) == 0;
   dim3 grid((nrows + MR_ROWS - 1) / MR_ROWS, (ncols + Geo<T, G>::TILE_N - 1) / Geo<T, G>::TILE_N);
-  kern<<<grid, MR_CW * 32, smem, s>>>(*tmap, *rmap, nrows, col0, ncols, nk, nkb, out,
+  kern<<<grid, (MR_CW + 1) * 32, smem, s>>>(*tmap, *rmap, nrows, col0, ncols, nk, nkb, out,
                                             ld_out, vec_ok ? 1 : 0, st);
   note_launch();
   return cudaGetLastError();

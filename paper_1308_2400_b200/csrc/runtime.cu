@@ -34,7 +34,6 @@ constexpr int kVariantWide = 0;  // TMA smem ring, 1024-column tiles (bform.cu)
 constexpr int kVariantRing = 1;  // TMA smem ring, 512-column tiles (bform.cu)
 constexpr int kVariantSmall = 4; // TMA smem ring, 1 KB-wide x 4-row CTA tiles (bform.cu)
 constexpr int kVariantMR = 5;    // 4 rows per warp over a dense rep tile (bform.cu)
-constexpr int kVariantWide12 = 6;  // wide tiles with 12 consumer warps (experimental)
 
 // AFMM_BFORM=wide|ring|small|mr forces one repeated-addition kernel (all are
 // bit-identical; tests/test_gpu_parity.py runs each). Default: auto.
@@ -44,7 +43,6 @@ int variant_from_env() {
   if (v && std::strcmp(v, "wide") == 0) return kVariantWide;
   if (v && std::strcmp(v, "small") == 0) return kVariantSmall;
   if (v && std::strcmp(v, "mr") == 0) return kVariantMR;
-  if (v && std::strcmp(v, "wide12") == 0) return kVariantWide12;
   return kVariantAuto;
 }
 
@@ -315,16 +313,13 @@ afmm_status launch_compute(afmm_context* c, int mode, const T* base, uint64_t kb
   // the parallelism of narrow/small tiles). CTA slots per GPU: wide 148
   // (1/SM), narrow 296 (2/SM), small 1184 (8/SM).
   const uint64_t cbytes = (uint64_t)ncols * sizeof(T);
-  const uint64_t wide_ctas = (nrows + 15) / 16 * ((cbytes + 4095) / 4096);
+  const uint64_t wide_ctas =
+      (nrows + afmm_dev::kWideRows - 1) / afmm_dev::kWideRows * ((cbytes + 4095) / 4096);
   const uint64_t narrow_ctas = (nrows + 15) / 16 * ((cbytes + 2047) / 2048);
   const uint64_t small_ctas = (nrows + 3) / 4 * ((cbytes + 1023) / 1024);
   int shape = afmm_dev::kShapeNarrow;
   uint64_t ctas = narrow_ctas, slots = 296;
-  if (c->variant == kVariantWide12) {
-    shape = afmm_dev::kShapeWide12;
-    ctas = wide_ctas;
-    slots = 148;
-  } else if (c->variant == kVariantWide ||
+  if (c->variant == kVariantWide ||
              (c->variant == kVariantAuto && wide_ctas >= 2 * 148)) {
     shape = afmm_dev::kShapeWide;
     ctas = wide_ctas;
