@@ -535,12 +535,15 @@ cudaError_t launch_bform(int shape, const CUtensorMap* tmap, const int2* lists, 
                          const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,
                          uint32_t nk, uint32_t* splits, uint64_t slice_stride, T* out,
                          uint64_t ld_out, const DevStatus* st, cudaStream_t s) {
-  if (shape == kShapeWide)  // 1024 fp32 / 512 fp64 columns, 1 CTA per SM
-    // 12 consumers + producer: 3 consumers per SM sub-partition and a
-    // 128-register budget (16 consumers + producer = 17 warps caps it at 96
-    // and spills; measured 88% vs 90% of peak at rep 16, tools/sweep.py)
-    return launch_ring<T, 8, 12, 6, 1>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits,
-                                       slice_stride, out, ld_out, st, s);
+  if (shape == kShapeWide)
+    // 1024 fp32 / 512 fp64 columns x 8 rows, 8 consumers + producer, 3-stage
+    // ring, 2 CTAs per SM. Measured against 12 or 16 consumers at 1 CTA/SM
+    // (tools/sweep.py, sweep_var.py): equal per-SM throughput (90% of peak at
+    // rep 16), but 2x finer CTAs, so far less wave-quantisation tail (cfg3
+    // n=4096: 87% vs 82%). 16 consumers + producer (17 warps) would cap the
+    // registers at 96 and spill.
+    return launch_ring<T, 8, kWideRows, 3, 2>(tmap, lists, cap, counts, nrows, col0, ncols, nk,
+                                              splits, slice_stride, out, ld_out, st, s);
   if (shape == kShapeSmall)  // 256 fp32 / 128 fp64 columns x 4 rows, up to 8 CTAs per SM
     return launch_ring<T, 2, 4, 3, 8>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits,
                                       slice_stride, out, ld_out, st, s);

@@ -310,8 +310,8 @@ afmm_status launch_compute(afmm_context* c, int mode, const T* base, uint64_t kb
   }
   // Tile shape: the widest one whose grid still fills the GPU (per-entry
   // overhead is amortised over more adds in wider tiles; small problems need
-  // the parallelism of narrow/small tiles). CTA slots per GPU: wide 148
-  // (1/SM), narrow 296 (2/SM), small 1184 (8/SM).
+  // the parallelism of narrow/small tiles). CTA slots per GPU: wide 296
+  // (2/SM), narrow 296 (2/SM), small 1184 (8/SM).
   const uint64_t cbytes = (uint64_t)ncols * sizeof(T);
   const uint64_t wide_ctas =
       (nrows + afmm_dev::kWideRows - 1) / afmm_dev::kWideRows * ((cbytes + 4095) / 4096);
@@ -320,10 +320,10 @@ afmm_status launch_compute(afmm_context* c, int mode, const T* base, uint64_t kb
   int shape = afmm_dev::kShapeNarrow;
   uint64_t ctas = narrow_ctas, slots = 296;
   if (c->variant == kVariantWide ||
-             (c->variant == kVariantAuto && wide_ctas >= 2 * 148)) {
+             (c->variant == kVariantAuto && wide_ctas >= 2 * 296)) {
     shape = afmm_dev::kShapeWide;
     ctas = wide_ctas;
-    slots = 148;
+    slots = 296;
   } else if (c->variant == kVariantSmall || (c->variant == kVariantAuto && narrow_ctas < 148)) {
     shape = afmm_dev::kShapeSmall;
     ctas = small_ctas;
