@@ -132,7 +132,51 @@ struct Acc<float, G> {
     if (rep >= 0) add_n<false>(s, (uint32_t)rep);
     else add_n<true>(s, 0u - (uint32_t)rep);
   }
-  __device__ __forceinline__ void run(uint32_t row_addr, int rep) { add(load_bases(row_addr), rep); }
+  // The same on column groups [G0, G1) only, with just those bases live.
+  template <bool NEG, int G0, int G1>
+  __device__ __forceinline__ void add_range(const float2* b, uint32_t t) {
+#pragma unroll 1
+    while (t >= 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int c = 2 * G0; c < 2 * G1; ++c)
+          a[c] = __fadd2_rn(a[c], NEG ? make_float2(-b[c - 2 * G0].x, -b[c - 2 * G0].y)
+                                      : b[c - 2 * G0]);
+      t -= 4;
+    }
+#pragma unroll 1
+    while (t != 0) {
+#pragma unroll
+      for (int c = 2 * G0; c < 2 * G1; ++c)
+        a[c] = __fadd2_rn(a[c], NEG ? make_float2(-b[c - 2 * G0].x, -b[c - 2 * G0].y)
+                                    : b[c - 2 * G0]);
+      t -= 1;
+    }
+  }
+  template <int G0, int G1>
+  __device__ __forceinline__ void run_range(uint32_t row_addr, int rep) {
+    float2 b[2 * (G1 - G0)];
+#pragma unroll
+    for (int g = G0; g < G1; ++g) {
+      const float4 v = lds128f(row_addr + group_off(g));
+      b[2 * (g - G0)] = make_float2(v.x, v.y);
+      b[2 * (g - G0) + 1] = make_float2(v.z, v.w);
+    }
+    if (rep >= 0) add_range<false, G0, G1>(b, (uint32_t)rep);
+    else add_range<true, G0, G1>(b, 0u - (uint32_t)rep);
+  }
+  // One list entry. Wide tiles (G = 8) run in two halves so that only 16 base
+  // registers are live next to the 32 accumulators (register budget of 2
+  // CTAs/SM); the extra loop per entry is noise at the reps where G = 8 is used.
+  __device__ __forceinline__ void run(uint32_t row_addr, int rep) {
+    if constexpr (G > 4) {
+      run_range<0, G / 2>(row_addr, rep);
+      run_range<G / 2, G>(row_addr, rep);
+    } else {
+      run_range<0, G>(row_addr, rep);
+    }
+  }
   __device__ __forceinline__ void store(float* out_row, int32_t oc0, int32_t ncols, uint32_t lane,
                                         bool vec_ok) const {
 #pragma unroll
@@ -191,7 +235,45 @@ struct Acc<double, G> {
     if (rep >= 0) add_n<false>(s, (uint32_t)rep);
     else add_n<true>(s, 0u - (uint32_t)rep);
   }
-  __device__ __forceinline__ void run(uint32_t row_addr, int rep) { add(load_bases(row_addr), rep); }
+  template <bool NEG, int G0, int G1>
+  __device__ __forceinline__ void add_range(const double* b, uint32_t t) {
+#pragma unroll 1
+    while (t >= 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int c = 2 * G0; c < 2 * G1; ++c)
+          a[c] = __dadd_rn(a[c], NEG ? -b[c - 2 * G0] : b[c - 2 * G0]);
+      t -= 4;
+    }
+#pragma unroll 1
+    while (t != 0) {
+#pragma unroll
+      for (int c = 2 * G0; c < 2 * G1; ++c)
+        a[c] = __dadd_rn(a[c], NEG ? -b[c - 2 * G0] : b[c - 2 * G0]);
+      t -= 1;
+    }
+  }
+  template <int G0, int G1>
+  __device__ __forceinline__ void run_range(uint32_t row_addr, int rep) {
+    double b[2 * (G1 - G0)];
+#pragma unroll
+    for (int g = G0; g < G1; ++g) {
+      const double2 v = lds128d(row_addr + group_off(g));
+      b[2 * (g - G0)] = v.x;
+      b[2 * (g - G0) + 1] = v.y;
+    }
+    if (rep >= 0) add_range<false, G0, G1>(b, (uint32_t)rep);
+    else add_range<true, G0, G1>(b, 0u - (uint32_t)rep);
+  }
+  __device__ __forceinline__ void run(uint32_t row_addr, int rep) {
+    if constexpr (G > 4) {
+      run_range<0, G / 2>(row_addr, rep);
+      run_range<G / 2, G>(row_addr, rep);
+    } else {
+      run_range<0, G>(row_addr, rep);
+    }
+  }
   __device__ __forceinline__ void store(double* out_row, int32_t oc0, int32_t ncols,
                                         uint32_t lane, bool vec_ok) const {
 #pragma unroll
@@ -285,7 +367,10 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
 
   if (status_failed(st)) return;  // validation failed: compute nothing (kernels.hpp:115,144)
 
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // %laneid through asm volatile: under register pressure ptxas otherwise
+  // re-derives the lane from S2R SR_TID inside the entry loop (a ~30-cycle
+  // stall per entry, ncu source view at rep 1).
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const int32_t tile_c = blockIdx.y * Gm::TILE_N;  // relative to col0
   const uint32_t kb_lo = blockIdx.z * slice_blocks;
   const uint32_t kb_hi = min(nkb_total, kb_lo + slice_blocks);
@@ -332,15 +417,18 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
 
   Acc<T, G> acc;
   acc.zero();
+  // loop invariants pinned in registers (see pin())
+  const uint32_t k_lo = pin(kb_lo * KB);
+  const uint32_t full0 = pin(smem_u32(full)), empty0 = pin(smem_u32(empty));
 
   // (kb_cur, slot, phase): the k block currently held, its ring slot and the
   // parity of that slot's current fill; stage_addr = smem address of the slot
   // plus this lane's first 16-byte column group.
   uint32_t kb_cur = 0, slot = 0, phase = 0;
-  uint32_t stage_addr = ring + lane * 16;
+  uint32_t stage_addr = pin(ring + lane * 16);
   auto advance = [&]() {
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[slot]);
+    if (lane == 0) mbar_arrive_at(empty0 + slot * 8);
     ++kb_cur;
     stage_addr += Gm::STAGE_BYTES;
     if (++slot == STAGES) {
@@ -349,7 +437,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
       stage_addr -= STAGES * Gm::STAGE_BYTES;
     }
   };
-  mbar_wait(&full[0], 0);
+  mbar_wait_at(full0, 0);
   int2 cur = lane < cnt ? lst[lane] : make_int2(0, 0);
   int2 nxt = 32 + lane < cnt ? lst[32 + lane] : make_int2(0, 0);
   // entry e = (k, rep) broadcast one entry ahead of its use
@@ -364,10 +452,10 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
     }
     const uint32_t k_n = (uint32_t)__shfl_sync(FULL, cur.x, f & 31u);
     const int rep_n = __shfl_sync(FULL, cur.y, f & 31u);
-    const uint32_t kb = k / KB - kb_lo;  // block index within the slice
+    const uint32_t kb = (k - k_lo) / KB;  // block index within the slice
     while (kb_cur < kb) {
       advance();
-      mbar_wait(&full[slot], phase);
+      mbar_wait_at(full0 + slot * 8, phase);
     }
     acc.run(stage_addr + (k % KB) * BOX_BYTES, rep);
     k = k_n;
@@ -377,7 +465,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
   while (true) {
     advance();
     if (kb_cur >= nkb) break;
-    mbar_wait(&full[slot], phase);
+    mbar_wait_at(full0 + slot * 8, phase);
   }
 
   if (b < nrows) acc.store(out + (uint64_t)b * ld_out, tile_c, ncols, lane, vec_ok != 0);

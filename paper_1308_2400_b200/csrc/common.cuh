@@ -37,6 +37,21 @@ __device__ __forceinline__ int rep_kind(double v) {
   return 0;
 }
 
+// Lane index that the compiler cannot rematerialise (an asm volatile result
+// stays in its register instead of being re-read from SR_TID in hot loops).
+__device__ __forceinline__ uint32_t lane_id() {
+  uint32_t l;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(l));
+  return l;
+}
+
+// Make a value opaque to the compiler so it stays in a register instead of
+// being re-derived (S2UR SR_CTAID / SR_CgaCtaId + address math) in hot loops.
+__device__ __forceinline__ uint32_t pin(uint32_t v) {
+  asm volatile("" : "+r"(v));
+  return v;
+}
+
 // ---- mbarrier --------------------------------------------------------------
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -81,6 +96,27 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// Same operations on a precomputed shared-memory address.
+__device__ __forceinline__ void mbar_arrive_at(uint32_t addr) {
+  asm volatile(
+      "{\n\t.reg .b64 st;\n\t"
+      "mbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(addr)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_at(uint32_t addr, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
   }
 }
 
