@@ -335,7 +335,7 @@ __device__ __forceinline__ uint32_t lower_bound_k(const int2* lst, uint32_t cnt,
 // k slice: blockIdx.z selects slice z = [z*slice_blocks, (z+1)*slice_blocks)
 // of the nkb_total k blocks and writes to out + z * slice_stride (fast-mode
 // split-k; one slice = the whole k range in order-preserving mode).
-template <class T, int G, int CW, int STAGES, int MINB>
+template <class T, int G, int CW, int STAGES, int MINB, bool SPLIT>
 __global__ void __launch_bounds__((CW + 1) * 32, MINB)
     k_bform(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ lists,
             uint64_t cap, const uint32_t* __restrict__ counts, uint32_t nrows, int32_t col0,
@@ -357,10 +357,12 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
   // stall per entry, ncu source view at rep 1).
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const int32_t tile_c = blockIdx.y * Gm::TILE_N;  // relative to col0
-  const uint32_t kb_lo = blockIdx.z * slice_blocks;
+  // SPLIT = false (order-preserving mode): one slice, k_lo = 0 at compile time
+  // (a runtime k_lo was rematerialised from S2UR SR_CTAID.Z + LDC every entry).
+  const uint32_t kb_lo = SPLIT ? blockIdx.z * slice_blocks : 0u;
   const uint32_t kb_hi = min(nkb_total, kb_lo + slice_blocks);
   const uint32_t nkb = kb_hi - kb_lo;
-  out += blockIdx.z * slice_stride;
+  if (SPLIT) out += blockIdx.z * slice_stride;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -382,7 +384,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
       while (true) {
         pump.pump();
         if (pump.next >= nkb) break;
-        mbar_wait(&empty[pump.next % STAGES], ((pump.next / STAGES) - 1) & 1);
+        mbar_sleep_wait_at(smem_u32(&empty[pump.next % STAGES]), ((pump.next / STAGES) - 1) & 1);
       }
     }
     return;
@@ -392,7 +394,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
   const uint32_t b = blockIdx.x * CW + warp;
   uint32_t cnt = b < nrows ? counts[b] : 0u;
   const int2* lst = lists + (uint64_t)(b < nrows ? b : 0) * cap;
-  if (gridDim.z > 1) {
+  if (SPLIT) {
     // this slice's entries: [lower_bound(kb_lo*KB), lower_bound(kb_hi*KB))
     const uint32_t p0 = lower_bound_k(lst, cnt, kb_lo * KB);
     const uint32_t p1 = kb_hi == nkb_total ? cnt : lower_bound_k(lst, cnt, kb_hi * KB);
@@ -421,7 +423,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
       stage_addr -= STAGES * Gm::STAGE_BYTES;
     }
   };
-  mbar_wait_at(full0, 0);
+  mbar_sleep_wait_at(full0, 0);
   int2 cur = lane < cnt ? lst[lane] : make_int2(0, 0);
   int2 nxt = 32 + lane < cnt ? lst[32 + lane] : make_int2(0, 0);
   // entry e = (k, rep) broadcast one entry ahead of its use
@@ -439,7 +441,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
     const uint32_t kb = (k - k_lo) / KB;  // block index within the slice
     while (kb_cur < kb) {
       advance();
-      mbar_wait_at(full0 + slot * 8, phase);
+      mbar_sleep_wait_at(full0 + slot * 8, phase);
     }
     acc.run(stage_addr + (k % KB) * BOX_BYTES, rep);
     k = k_n;
@@ -449,7 +451,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
   while (true) {
     advance();
     if (kb_cur >= nkb) break;
-    mbar_wait_at(full0 + slot * 8, phase);
+    mbar_sleep_wait_at(full0 + slot * 8, phase);
   }
 
   if (b < nrows) acc.store(out + (uint64_t)b * ld_out, tile_c, ncols, lane, vec_ok != 0);
@@ -530,7 +532,8 @@ __global__ void __launch_bounds__((MR_CW + 1) * 32, 1)
       while (true) {
         pump.pump();
         if (pump.next >= nkb) break;
-        mbar_wait(&empty[pump.next % MR_STAGES], ((pump.next / MR_STAGES) - 1) & 1);
+        mbar_sleep_wait_at(smem_u32(&empty[pump.next % MR_STAGES]),
+                           ((pump.next / MR_STAGES) - 1) & 1);
       }
     }
     return;
@@ -542,7 +545,7 @@ __global__ void __launch_bounds__((MR_CW + 1) * 32, 1)
 
   uint32_t slot = 0, phase = 0;
   for (uint32_t kb = 0; kb < nkb; ++kb) {
-    mbar_wait(&full[slot], phase);
+    mbar_sleep_wait_at(smem_u32(&full[slot]), phase);
     const uint32_t bstage = ring + slot * Gm::STAGE_BYTES + lane * 16;
     const uint32_t rstage = rring + slot * REP_STAGE + warp * (MR_RW * 4);
     const uint32_t kk_end = nk - kb * KB < (uint32_t)KB ? nk - kb * KB : (uint32_t)KB;
@@ -575,15 +578,16 @@ cudaError_t launch_ring(const CUtensorMap* tmap, const int2* lists, uint64_t cap
                         const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,
                         uint32_t nk, uint32_t* splits, uint64_t slice_stride, T* out,
                         uint64_t ld_out, const DevStatus* st, cudaStream_t s) {
-  auto kern = k_bform<T, G, CW, STAGES, MINB>;
+  const uint32_t nkb = (nk + KB - 1) / KB;
+  uint32_t want = *splits < 1 ? 1 : *splits;
+  if (want > nkb) want = nkb;
+  auto kern = want > 1 ? k_bform<T, G, CW, STAGES, MINB, true>
+                       : k_bform<T, G, CW, STAGES, MINB, false>;
   const size_t smem = ring_smem_bytes<T, G, STAGES>();
   // set on every call: the attribute is per device and costs ~1 us
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  const uint32_t nkb = (nk + KB - 1) / KB;
-  uint32_t want = *splits < 1 ? 1 : *splits;
-  if (want > nkb) want = nkb;
   const uint32_t slice_blocks = (nkb + want - 1) / want;
   *splits = (nkb + slice_blocks - 1) / slice_blocks;
   const bool vec_ok = (ld_out * sizeof(T)) % 16 == 0 &&
