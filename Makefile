@@ -47,3 +47,9 @@ clean:
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean sass cpptest
+
+# Kernel timing experiments (never the product): build/exp/<name>/libafmm_b200.so
+# with extra defines, selected at run time through AFMM_LIB.
+exp-%:
+	@mkdir -p build/exp/$*
+	$(NVCC) $(NVFLAGS) $(EXPDEFS) -shared -o build/exp/$*/libafmm_b200.so $(SRCS)

@@ -11,7 +11,8 @@ import os
 from ctypes import POINTER, c_char, c_double, c_int32, c_uint32, c_uint64, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libafmm_b200.so")
+# AFMM_LIB overrides the in-tree library (kernel experiments built under build/).
+LIB_PATH = os.environ.get("AFMM_LIB") or os.path.join(_HERE, "libafmm_b200.so")
 
 # afmm_status
 OK = 0

@@ -43,7 +43,19 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+#ifndef AFMM_EXP_KB
 constexpr int KB = 8;  // k rows per stage
+#else
+constexpr int KB = AFMM_EXP_KB;  // timing experiments (Makefile exp-%)
+#endif
+#ifndef AFMM_EXP_REP_UNROLL
+constexpr int REP_UNROLL = 4;  // rep-loop unroll (adds per column per trip)
+#else
+constexpr int REP_UNROLL = AFMM_EXP_REP_UNROLL;
+#endif
+#ifndef AFMM_EXP_WIDE_STAGES
+#define AFMM_EXP_WIDE_STAGES 3
+#endif
 // A TMA box is at most 256 elements wide, so a stage is G/2 boxes of
 // KB x BOX_BYTES laid out box-major: [box][k row][BOX_BYTES].
 constexpr int BOX_BYTES = 1024;
@@ -81,6 +93,54 @@ __device__ __forceinline__ double2 lds128d(uint32_t addr) {
 // (g>>1)*KB*BOX_BYTES + (g&1)*512 + l*16 of each staged k row: every 128-bit
 // LDS across the warp reads 512 contiguous bytes (no bank conflict). In
 // output columns that is tile_col + g*128 + 4l (fp32) / g*64 + 2l (fp64).
+// ---- tensor memory (TMEM) ---------------------------------------------------
+
+// 32 lanes x 32 columns of 32-bit words -> 32 registers per thread (lane t of
+// the warp's TMEM lane quadrant, 32 consecutive columns), then wait.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// smem -> TMEM copy of a 32-row x 16-byte matrix, replicated into all four
+// 32-lane quadrants (row r -> lane r of every quadrant, 4 columns).
+__device__ __forceinline__ void tmem_cp_32x128b_x4(uint32_t taddr, uint64_t desc) {
+  asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(desc)
+               : "memory");
+}
+
+// Arrive on an mbarrier once all previously issued tcgen05 async operations of
+// this thread (here: the copies) have completed.
+__device__ __forceinline__ void tmem_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+
+// tcgen05 shared-memory matrix descriptor, no swizzle: 8-row x 16-byte core
+// matrices stored contiguously (128 B apart), version 1 (sm_100).
+__device__ __forceinline__ uint64_t smem_desc_128(uint32_t saddr) {
+  const uint64_t start = (saddr >> 4) & 0x3fffu;
+  const uint64_t lbo = 128u >> 4, sbo = 128u >> 4;
+  return start | (lbo << 16) | (sbo << 32) | (1ull << 46);
+}
+
 template <class T, int G>
 struct Acc;
 
@@ -136,14 +196,14 @@ struct Acc<float, G> {
   template <bool NEG, int G0, int G1>
   __device__ __forceinline__ void add_range(const float2* b, uint32_t t) {
 #pragma unroll 1
-    while (t >= 4) {
+    while (t >= REP_UNROLL) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < REP_UNROLL; ++u)
 #pragma unroll
         for (int c = 2 * G0; c < 2 * G1; ++c)
           a[c] = __fadd2_rn(a[c], NEG ? make_float2(-b[c - 2 * G0].x, -b[c - 2 * G0].y)
                                       : b[c - 2 * G0]);
-      t -= 4;
+      t -= REP_UNROLL;
     }
 #pragma unroll 1
     while (t != 0) {
@@ -169,6 +229,19 @@ struct Acc<float, G> {
   // One list entry, all G column groups in one rep loop. (Splitting wide tiles
   // into two half-width loops to save 16 base registers was measured 3% slower.)
   __device__ __forceinline__ void run(uint32_t row_addr, int rep) { run_range<0, G>(row_addr, rep); }
+  // The same entry with the bases read from tensor memory (k_bform_tm): the
+  // lane's 4G words sit in 4G consecutive TMEM columns in LDS order.
+  __device__ __forceinline__ void run_tm(uint32_t taddr, int rep) {
+    static_assert(G == 8, "TMEM bases: 32 columns per lane");
+    uint32_t r[32];
+    tmem_ld32(taddr, r);
+    float2 b[2 * G];
+#pragma unroll
+    for (int c = 0; c < 2 * G; ++c)
+      b[c] = make_float2(__uint_as_float(r[2 * c]), __uint_as_float(r[2 * c + 1]));
+    if (rep >= 0) add_range<false, 0, G>(b, (uint32_t)rep);
+    else add_range<true, 0, G>(b, 0u - (uint32_t)rep);
+  }
   __device__ __forceinline__ void store(float* out_row, int32_t oc0, int32_t ncols, uint32_t lane,
                                         bool vec_ok) const {
 #pragma unroll
@@ -230,13 +303,13 @@ struct Acc<double, G> {
   template <bool NEG, int G0, int G1>
   __device__ __forceinline__ void add_range(const double* b, uint32_t t) {
 #pragma unroll 1
-    while (t >= 4) {
+    while (t >= REP_UNROLL) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < REP_UNROLL; ++u)
 #pragma unroll
         for (int c = 2 * G0; c < 2 * G1; ++c)
           a[c] = __dadd_rn(a[c], NEG ? -b[c - 2 * G0] : b[c - 2 * G0]);
-      t -= 4;
+      t -= REP_UNROLL;
     }
 #pragma unroll 1
     while (t != 0) {
@@ -259,6 +332,17 @@ struct Acc<double, G> {
     else add_range<true, G0, G1>(b, 0u - (uint32_t)rep);
   }
   __device__ __forceinline__ void run(uint32_t row_addr, int rep) { run_range<0, G>(row_addr, rep); }
+  __device__ __forceinline__ void run_tm(uint32_t taddr, int rep) {
+    static_assert(G == 8, "TMEM bases: 32 columns per lane");
+    uint32_t r[32];
+    tmem_ld32(taddr, r);
+    double b[2 * G];
+#pragma unroll
+    for (int c = 0; c < 2 * G; ++c)
+      b[c] = __hiloint2double((int)r[2 * c + 1], (int)r[2 * c]);
+    if (rep >= 0) add_range<false, 0, G>(b, (uint32_t)rep);
+    else add_range<true, 0, G>(b, 0u - (uint32_t)rep);
+  }
   __device__ __forceinline__ void store(double* out_row, int32_t oc0, int32_t ncols,
                                         uint32_t lane, bool vec_ok) const {
 #pragma unroll
@@ -274,9 +358,39 @@ struct Acc<double, G> {
   }
 };
 
+// Rows per CTA (<= cw) that minimise (waves x rows per CTA), i.e. the busiest
+// SM's share of rows when every SM holds `per_sm` CTAs: a last wave that is
+// mostly empty costs as much as a full one (n = 1024 fp64, 16-row CTAs, 4
+// column tiles: 256 CTAs on 296 slots; 14-row CTAs fill exactly one wave).
+// Keeps cw unless trimming gains more than 3%.
+inline uint32_t balanced_rows(uint32_t nrows, uint32_t tiles, uint32_t cw, uint32_t per_sm) {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const uint64_t slots = (uint64_t)sms * per_sm;
+  auto cost = [&](uint32_t r) {
+    const uint64_t ctas = (uint64_t)((nrows + r - 1) / r) * tiles;
+    return ((ctas + slots - 1) / slots) * (uint64_t)r;
+  };
+  uint32_t best = cw;
+  uint64_t best_cost = cost(cw);
+  for (uint32_t r = cw - 1; r >= 1 && 2 * r >= cw; --r) {
+    const uint64_t c = cost(r);
+    if (c * 100 < best_cost * 97) {
+      best = r;
+      best_cost = c;
+    }
+  }
+  return best;
+}
+
 template <class T, int G, int STAGES>
 __host__ __device__ constexpr size_t ring_smem_bytes() {
-  return 1024 /*alignment slack*/ + (size_t)STAGES * Geo<T, G>::STAGE_BYTES +
+  return 128 /*alignment slack*/ + (size_t)STAGES * Geo<T, G>::STAGE_BYTES +
          2 * STAGES * sizeof(uint64_t);
 }
 
@@ -338,14 +452,15 @@ __device__ __forceinline__ uint32_t lower_bound_k(const int2* lst, uint32_t cnt,
 template <class T, int G, int CW, int STAGES, int MINB, bool SPLIT>
 __global__ void __launch_bounds__((CW + 1) * 32, MINB)
     k_bform(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ lists,
-            uint64_t cap, const uint32_t* __restrict__ counts, uint32_t nrows, int32_t col0,
-            int32_t ncols, uint32_t nkb_total, uint32_t slice_blocks, uint64_t slice_stride,
+            uint64_t cap, const uint32_t* __restrict__ counts, uint32_t nrows, uint32_t rpc,
+            int32_t col0, int32_t ncols, uint32_t nkb_total, uint32_t slice_blocks, uint64_t slice_stride,
             T* __restrict__ out, uint64_t ld_out, int vec_ok, const DevStatus* __restrict__ st) {
   using Gm = Geo<T, G>;
   extern __shared__ unsigned char smem_raw[];
-  // 1024-byte aligned ring; pointer arithmetic on the smem pointer itself keeps
-  // the shared address space visible to the compiler.
-  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  // 128-byte aligned ring (TMA destination without swizzle); pointer arithmetic
+  // on the smem pointer itself keeps the shared address space visible to the
+  // compiler.
+  unsigned char* base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   uint64_t* full = reinterpret_cast<uint64_t*>(base + STAGES * Gm::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   const uint32_t ring = smem_u32(base);
@@ -391,7 +506,9 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
   }
 
   // ---- consumers: one output row per warp ----
-  const uint32_t b = blockIdx.x * CW + warp;
+  // rpc <= CW rows per CTA (the launcher trims it to balance the last wave);
+  // warps past it walk no entries but still release every stage.
+  const uint32_t b = warp < rpc ? blockIdx.x * rpc + warp : nrows;
   uint32_t cnt = b < nrows ? counts[b] : 0u;
   const int2* lst = lists + (uint64_t)(b < nrows ? b : 0) * cap;
   if (SPLIT) {
@@ -455,6 +572,260 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
   }
 
   if (b < nrows) acc.store(out + (uint64_t)b * ld_out, tile_c, ncols, lane, vec_ok != 0);
+}
+
+// ---------------------------------------------------------------------------
+// k_bform_tm: k_bform with the bases served from tensor memory.
+//
+// At small reps k_bform is bound by the shared-memory data pipe (ncu at rep 1:
+// L1TEX wavefronts 97%, FMA pipe 28%): each of the CTA's warps re-reads every
+// staged base row with 128-bit LDS at 128 B/clk/SM. TMEM reads into registers
+// run at >= 450 B/clk/SM (tools/tmem_probe.cu), so here
+//   * warp CW (TMA) streams KB x 1024-byte-row tiles of B' into an SST-deep
+//     smem ring (as in k_bform);
+//   * warp CW+1 (copy) moves each landed tile into one of TST TMEM stages with
+//     tcgen05.cp 32x128b.warpx4 (each 512-byte column group -> 4 columns of all
+//     128 lanes, i.e. one copy per lane quadrant), then tcgen05.commit arrives on
+//     the stage's full barrier and on the smem slot's empty barrier;
+//   * the CW consumer warps walk their rows' lists as in k_bform but fetch an
+//     entry's 32 bases per lane with one tcgen05.ld 32x32b.x32 from their lane
+//     quadrant, releasing TMEM stages through per-stage empty barriers.
+// CW = 14 consumers + 2 producers (4 warps per SM sub-partition, 128-register
+// budget), one CTA per SM owning all 512 TMEM columns: TM_TST = 4 stages of
+// TM_TKB = 4 k rows x 32 columns. Per element the order is unchanged (one
+// chain, k ascending, |rep| adds).
+//
+// Measured (tools/exp_time.py): equal to k_bform at rep >= 4 and slower at
+// rep 1-2 (0.20 vs 0.23 of peak): the replicating copy (one 32x128b.warpx4
+// per 512 bytes) cannot refill TMEM as fast as 14 warps drain it, so the
+// consumers wait on the stage-full barrier (ncu: 32% of warp samples). Kept
+// as an opt-in variant (AFMM_BFORM=tmem) with full parity coverage.
+// ---------------------------------------------------------------------------
+
+constexpr int TM_TKB = 4;           // k rows per TMEM stage (half an smem stage)
+constexpr int TM_TST = 4;           // TMEM stages
+constexpr int TM_COLS = 512;        // TMEM columns allocated (whole SM)
+constexpr int TM_STAGE_COLS = TM_TKB * 32;
+static_assert(KB % TM_TKB == 0, "TMEM stage must divide the smem stage");
+
+template <class T, int CW, int SST>
+__host__ __device__ constexpr size_t tm_smem_bytes() {
+  return 128 + (size_t)SST * Geo<T, 8>::STAGE_BYTES +
+         (2 * SST + 2 * TM_TST) * sizeof(uint64_t) + 16;
+}
+
+template <class T, int CW, int SST, bool SPLIT>
+__global__ void __launch_bounds__((CW + 2) * 32, 1)
+    k_bform_tm(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ lists,
+               uint64_t cap, const uint32_t* __restrict__ counts, uint32_t nrows, uint32_t rpc,
+               int32_t col0, int32_t ncols, uint32_t nkb_total, uint32_t slice_blocks, uint64_t slice_stride,
+               T* __restrict__ out, uint64_t ld_out, int vec_ok,
+               const DevStatus* __restrict__ st) {
+  constexpr int G = 8;
+  using Gm = Geo<T, G>;
+  static_assert(TM_TST * TM_STAGE_COLS <= TM_COLS, "TMEM stages");
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  uint64_t* sfull = reinterpret_cast<uint64_t*>(base + SST * Gm::STAGE_BYTES);
+  uint64_t* sempty = sfull + SST;
+  uint64_t* tfull = sempty + SST;
+  uint64_t* tempty = tfull + TM_TST;
+  uint32_t* tbase_slot = reinterpret_cast<uint32_t*>(tempty + TM_TST);
+  const uint32_t ring = smem_u32(base);
+
+  if (status_failed(st)) return;  // validation failed: compute nothing (kernels.hpp:115,144)
+
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  const int32_t tile_c = blockIdx.y * Gm::TILE_N;
+  const uint32_t kb_lo = SPLIT ? blockIdx.z * slice_blocks : 0u;
+  const uint32_t kb_hi = min(nkb_total, kb_lo + slice_blocks);
+  const uint32_t nkb = kb_hi - kb_lo;
+  if (SPLIT) out += blockIdx.z * slice_stride;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < SST; ++i) {
+      mbar_init(&sfull[i], 1);
+      mbar_init(&sempty[i], 1);
+    }
+    for (int i = 0; i < TM_TST; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], CW);
+    }
+    fence_barrier_init();
+  }
+  if (warp == CW + 1) {  // the copy warp owns the TMEM allocation
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tbase_slot)),
+                 "n"(TM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tbase = *tbase_slot;
+
+  if (warp == CW) {
+    // ---- TMA producer: global -> smem ring ----
+    if (lane == 0) {
+      prefetch_tensormap(&tmap);
+      for (uint32_t i = 0; i < nkb; ++i) {
+        const uint32_t slot = i % SST;
+        if (i >= SST) mbar_sleep_wait_at(smem_u32(&sempty[slot]), ((i / SST) - 1) & 1);
+        mbar_arrive_expect_tx(&sfull[slot], (uint32_t)Gm::STAGE_BYTES);
+        const int32_t krow = (int32_t)((kb_lo + i) * KB);
+#pragma unroll
+        for (int h = 0; h < Gm::NBOX; ++h)
+          tma_load_2d(base + slot * Gm::STAGE_BYTES + h * KB * BOX_BYTES, &tmap, &sfull[slot],
+                      col0 + tile_c + h * Gm::BOX_N, krow);
+      }
+    }
+    return;
+  }
+
+  if (warp == CW + 1) {
+    // ---- copy warp: smem ring -> TMEM stages ----
+    if (lane == 0) {
+      for (uint32_t i = 0; i < nkb; ++i) {
+        const uint32_t slot = i % SST;
+        mbar_sleep_wait_at(smem_u32(&sfull[slot]), (i / SST) & 1);
+        const uint32_t src = ring + slot * Gm::STAGE_BYTES;
+#pragma unroll 1
+        for (int h = 0; h < KB / TM_TKB; ++h) {
+          const uint32_t j = i * (KB / TM_TKB) + h, ts = j % TM_TST;
+          if (j >= TM_TST) mbar_sleep_wait_at(smem_u32(&tempty[ts]), ((j / TM_TST) - 1) & 1);
+          tmem_fence_after();
+          const uint32_t dst = tbase + ts * TM_STAGE_COLS;
+#pragma unroll 1
+          for (int kk = 0; kk < TM_TKB; ++kk)
+#pragma unroll
+            for (int g = 0; g < G; ++g)
+              tmem_cp_32x128b_x4(
+                  dst + kk * 32 + g * 4,
+                  smem_desc_128(src + group_off(g) + (h * TM_TKB + kk) * BOX_BYTES));
+          tmem_commit(smem_u32(&tfull[ts]));
+        }
+        tmem_commit(smem_u32(&sempty[slot]));
+      }
+    }
+    __syncwarp();
+    // wait for the consumers, then free TMEM
+    asm volatile("bar.sync 1, %0;" ::"n"((CW + 1) * 32) : "memory");
+    tmem_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(TM_COLS)
+                 : "memory");
+    return;
+  }
+
+  // ---- consumers: one output row per warp ----
+  // rpc <= CW rows per CTA (the launcher trims it to balance the last wave);
+  // warps past it walk no entries but still release every stage.
+  const uint32_t b = warp < rpc ? blockIdx.x * rpc + warp : nrows;
+  uint32_t cnt = b < nrows ? counts[b] : 0u;
+  const int2* lst = lists + (uint64_t)(b < nrows ? b : 0) * cap;
+  if (SPLIT) {
+    const uint32_t p0 = lower_bound_k(lst, cnt, kb_lo * KB);
+    const uint32_t p1 = kb_hi == nkb_total ? cnt : lower_bound_k(lst, cnt, kb_hi * KB);
+    lst += p0;
+    cnt = p1 - p0;
+  }
+
+  Acc<T, G> acc;
+  acc.zero();
+  const uint32_t k_lo = kb_lo * KB;
+  const uint32_t tfull0 = smem_u32(tfull), tempty0 = smem_u32(tempty);
+  // this warp's lane quadrant of the current TMEM stage
+  const uint32_t tq = tbase + (((warp & 3u) * 32u) << 16);
+  uint32_t kb_cur = 0, ts = 0, phase = 0;
+  uint32_t stage_t = tq;
+  auto advance = [&]() {
+    tmem_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive_at(tempty0 + ts * 8);
+    ++kb_cur;
+    stage_t += TM_STAGE_COLS;
+    if (++ts == TM_TST) {
+      ts = 0;
+      phase ^= 1;
+      stage_t = tq;
+    }
+  };
+  mbar_sleep_wait_at(tfull0, 0);
+  tmem_fence_after();
+  int2 cur = lane < cnt ? lst[lane] : make_int2(0, 0);
+  int2 nxt = 32 + lane < cnt ? lst[32 + lane] : make_int2(0, 0);
+  uint32_t k = (uint32_t)__shfl_sync(FULL, cur.x, 0);
+  int rep = __shfl_sync(FULL, cur.y, 0);
+  for (uint32_t e = 0; e < cnt; ++e) {
+    const uint32_t f = e + 1;
+    if ((f & 31u) == 0) {
+      cur = nxt;
+      const uint32_t pn = f + 32 + lane;
+      nxt = pn < cnt ? lst[pn] : make_int2(0, 0);
+    }
+    const uint32_t k_n = (uint32_t)__shfl_sync(FULL, cur.x, f & 31u);
+    const int rep_n = __shfl_sync(FULL, cur.y, f & 31u);
+    const uint32_t kb = (k - k_lo) / TM_TKB;  // TMEM block within the slice
+    while (kb_cur < kb) {
+      advance();
+      mbar_sleep_wait_at(tfull0 + ts * 8, phase);
+      tmem_fence_after();
+    }
+    acc.run_tm(stage_t + (k % TM_TKB) * 32, rep);
+    k = k_n;
+    rep = rep_n;
+  }
+  while (true) {
+    advance();
+    if (kb_cur >= nkb * (KB / TM_TKB)) break;
+    mbar_sleep_wait_at(tfull0 + ts * 8, phase);
+  }
+  tmem_fence_before();
+  asm volatile("bar.sync 1, %0;" ::"n"((CW + 1) * 32) : "memory");
+
+  if (b < nrows) acc.store(out + (uint64_t)b * ld_out, tile_c, ncols, lane, vec_ok != 0);
+}
+
+template <class T, bool SPLIT>
+cudaError_t launch_tm_impl(const CUtensorMap* tmap, const int2* lists, uint64_t cap,
+                           const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,
+                           uint32_t nkb, uint32_t slice_blocks, uint32_t splits,
+                           uint64_t slice_stride, T* out, uint64_t ld_out, bool vec_ok,
+                           const DevStatus* st, cudaStream_t s) {
+  constexpr int CW = kTmemRows, SST = 4;
+  auto kern = k_bform_tm<T, CW, SST, SPLIT>;
+  const size_t smem = tm_smem_bytes<T, CW, SST>();
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  const uint32_t tiles = (ncols + Geo<T, 8>::TILE_N - 1) / Geo<T, 8>::TILE_N;
+  const uint32_t rpc = balanced_rows(nrows, tiles * splits, CW, 1);
+  dim3 grid((nrows + rpc - 1) / rpc, tiles, splits);
+  kern<<<grid, (CW + 2) * 32, smem, s>>>(*tmap, lists, cap, counts, nrows, rpc, col0, ncols, nkb,
+                                         slice_blocks, slice_stride, out, ld_out,
+                                         vec_ok ? 1 : 0, st);
+  note_launch();
+  return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t launch_tm(const CUtensorMap* tmap, const int2* lists, uint64_t cap,
+                      const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,
+                      uint32_t nk, uint32_t* splits, uint64_t slice_stride, T* out,
+                      uint64_t ld_out, const DevStatus* st, cudaStream_t s) {
+  const uint32_t nkb = (nk + KB - 1) / KB;
+  uint32_t want = *splits < 1 ? 1 : *splits;
+  if (want > nkb) want = nkb;
+  const uint32_t slice_blocks = (nkb + want - 1) / want;
+  *splits = (nkb + slice_blocks - 1) / slice_blocks;
+  const bool vec_ok = (ld_out * sizeof(T)) % 16 == 0 &&
+                      (reinterpret_cast<uintptr_t>(out) % 16) == 0 &&
+                      (slice_stride * sizeof(T)) % 16 == 0;
+  if (*splits > 1)
+    return launch_tm_impl<T, true>(tmap, lists, cap, counts, nrows, col0, ncols, nkb,
+                                   slice_blocks, *splits, slice_stride, out, ld_out, vec_ok, st, s);
+  return launch_tm_impl<T, false>(tmap, lists, cap, counts, nrows, col0, ncols, nkb, slice_blocks,
+                                  1, slice_stride, out, ld_out, vec_ok, st, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -593,8 +964,10 @@ cudaError_t launch_ring(const CUtensorMap* tmap, const int2* lists, uint64_t cap
   const bool vec_ok = (ld_out * sizeof(T)) % 16 == 0 &&
                       (reinterpret_cast<uintptr_t>(out) % 16) == 0 &&
                       (slice_stride * sizeof(T)) % 16 == 0;
-  dim3 grid((nrows + CW - 1) / CW, (ncols + Geo<T, G>::TILE_N - 1) / Geo<T, G>::TILE_N, *splits);
-  kern<<<grid, (CW + 1) * 32, smem, s>>>(*tmap, lists, cap, counts, nrows, col0, ncols, nkb,
+  const uint32_t tiles = (ncols + Geo<T, G>::TILE_N - 1) / Geo<T, G>::TILE_N;
+  const uint32_t rpc = balanced_rows(nrows, tiles * *splits, CW, MINB);
+  dim3 grid((nrows + rpc - 1) / rpc, tiles, *splits);
+  kern<<<grid, (CW + 1) * 32, smem, s>>>(*tmap, lists, cap, counts, nrows, rpc, col0, ncols, nkb,
                                          slice_blocks, slice_stride, out, ld_out,
                                          vec_ok ? 1 : 0, st);
   note_launch();
@@ -618,8 +991,12 @@ cudaError_t launch_bform(int shape, const CUtensorMap* tmap, const int2* lists, 
     // rep 16), but 2x finer CTAs, so far less wave-quantisation tail (cfg3
     // n=4096: 87% vs 82%). 16 consumers + producer (17 warps) would cap the
     // registers at 96 and spill.
-    return launch_ring<T, 8, kWideRows, 3, 2>(tmap, lists, cap, counts, nrows, col0, ncols, nk,
+    return launch_ring<T, 8, kWideRows, AFMM_EXP_WIDE_STAGES, 2>(tmap, lists, cap, counts, nrows, col0, ncols, nk,
                                               splits, slice_stride, out, ld_out, st, s);
+  if (shape == kShapeTmem)
+    // 1024 fp32 / 512 fp64 columns x 16 rows, bases from tensor memory, 1 CTA per SM
+    return launch_tm<T>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits, slice_stride,
+                        out, ld_out, st, s);
   if (shape == kShapeSmall)  // 256 fp32 / 128 fp64 columns x 4 rows, up to 8 CTAs per SM
     return launch_ring<T, 2, 4, 3, 8>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits,
                                       slice_stride, out, ld_out, st, s);

@@ -44,7 +44,9 @@ int bform_box_bytes();
 constexpr int kShapeNarrow = 0;
 constexpr int kShapeWide = 1;
 constexpr int kShapeSmall = 2;
+constexpr int kShapeTmem = 3;
 constexpr int kWideRows = 8;  // rows per wide CTA
+constexpr int kTmemRows = 14; // rows per TMEM-fed CTA (14 + 2 warps: 128-register budget)
 // *splits: requested k slices in, slices launched out (1 = order-preserving).
 // Slice z writes its partial product to out + z * slice_stride.
 template <class T>

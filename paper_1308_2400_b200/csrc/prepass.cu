@@ -217,12 +217,23 @@ __global__ void __launch_bounds__(256) k_transpose_compact(const T* __restrict__
   const uint32_t j0 = blockIdx.x * 32;
   const unsigned lt = (1u << tx) - 1u;
   uint32_t base[4] = {0, 0, 0, 0};
-  for (uint32_t k0 = 0; k0 < n; k0 += 32) {
-    for (uint32_t dy = ty; dy < 32; dy += 8) {
-      const uint32_t k = k0 + dy, j = j0 + tx;
-      tile[dy][tx] = (k < n && j < n) ? y[(uint64_t)k * ld + j] : T(0);
+  // the next 32-row tile is loaded into registers while this one is compacted
+  // (the block walks k serially, so unhidden load latency is its whole cost
+  // at small n)
+  T pre[4];
+  auto fetch = [&](uint32_t k0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t k = k0 + ty + 8 * q, j = j0 + tx;
+      pre[q] = (k < n && j < n) ? y[(uint64_t)k * ld + j] : T(0);
     }
+  };
+  fetch(0);
+  for (uint32_t k0 = 0; k0 < n; k0 += 32) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tile[ty + 8 * q][tx] = pre[q];
     __syncthreads();
+    if (k0 + 32 < n) fetch(k0 + 32);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const uint32_t jj = ty * 4 + q, j = j0 + jj;

@@ -34,6 +34,7 @@ constexpr int kVariantWide = 0;  // TMA smem ring, 1024-column tiles (bform.cu)
 constexpr int kVariantRing = 1;  // TMA smem ring, 512-column tiles (bform.cu)
 constexpr int kVariantSmall = 4; // TMA smem ring, 1 KB-wide x 4-row CTA tiles (bform.cu)
 constexpr int kVariantMR = 5;    // 4 rows per warp over a dense rep tile (bform.cu)
+constexpr int kVariantTmem = 7;  // bases served from tensor memory (bform.cu)
 
 // AFMM_BFORM=wide|ring|small|mr forces one repeated-addition kernel (all are
 // bit-identical; tests/test_gpu_parity.py runs each). Default: auto.
@@ -43,6 +44,7 @@ int variant_from_env() {
   if (v && std::strcmp(v, "wide") == 0) return kVariantWide;
   if (v && std::strcmp(v, "small") == 0) return kVariantSmall;
   if (v && std::strcmp(v, "mr") == 0) return kVariantMR;
+  if (v && std::strcmp(v, "tmem") == 0) return kVariantTmem;
   return kVariantAuto;
 }
 
@@ -319,8 +321,15 @@ afmm_status launch_compute(afmm_context* c, int mode, const T* base, uint64_t kb
   const uint64_t small_ctas = (nrows + 3) / 4 * ((cbytes + 1023) / 1024);
   int shape = afmm_dev::kShapeNarrow;
   uint64_t ctas = narrow_ctas, slots = 296;
-  if (c->variant == kVariantWide ||
-             (c->variant == kVariantAuto && wide_ctas >= 2 * 296)) {
+  if (c->variant == kVariantTmem) {
+    shape = afmm_dev::kShapeTmem;
+    ctas = (nrows + afmm_dev::kTmemRows - 1) / afmm_dev::kTmemRows * ((cbytes + 4095) / 4096);
+    slots = 148;
+  } else if (c->variant == kVariantWide ||
+             (c->variant == kVariantAuto && 4 * wide_ctas >= 3 * 296)) {
+    // (launch_ring trims the rows per CTA so a partial last wave costs little;
+    // wide tiles need about one wave of CTAs: 256 of them at n = 1024 fp64 run
+    // 7% faster than 256 narrow ones)
     shape = afmm_dev::kShapeWide;
     ctas = wide_ctas;
     slots = 296;

@@ -242,7 +242,7 @@ def test_fast_mode_within_tolerance(cuda, oracle, name, n, kw):
     assert float(err.max()) <= tol, (name, float(err.max()))
 
 
-@pytest.mark.parametrize("variant", ["wide", "ring", "small", "mr"])
+@pytest.mark.parametrize("variant", ["wide", "ring", "small", "mr", "tmem"])
 def test_both_kernel_variants_bit_exact(cuda, oracle, variant, monkeypatch):
     """k_bform (TMA smem ring) and k_bform_l1 (decoupled warps) give identical bits."""
     import torch
