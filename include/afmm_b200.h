@@ -140,6 +140,12 @@ afmm_status afmm_context_enable_timing(afmm_context* ctx, int32_t enable);
 afmm_status afmm_context_last_timing(afmm_context* ctx, float* prepass_ms, float* compute_ms,
                                      float* epilogue_ms);
 
+/* Repeated-addition kernel of the context's last product: 0 = B-form
+ * (k_bform: rep uniform per warp; Case B directly, Case A on transposed
+ * operands), 1 = A-form (k_aform: Case A with the base uniform per warp,
+ * chosen for sparse X). */
+int32_t afmm_context_last_form(afmm_context* ctx);
+
 /* Per-row work W_i (exact additions of Z row i) for the row partition:
  * Case A  W_i = sum_{k: X[i,k] != 0} sum_j |llround Y[k,j]|
  * Case B  W_i = sum_k |llround X[i,k]| * nnz(Y[k,:])

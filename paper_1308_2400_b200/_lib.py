@@ -86,6 +86,7 @@ _SIGNATURES = {
     "afmm_context_enable_timing": (c_int32, [c_void_p, c_int32]),
     "afmm_context_last_timing": (c_int32, [c_void_p, POINTER(ctypes.c_float),
                                            POINTER(ctypes.c_float), POINTER(ctypes.c_float)]),
+    "afmm_context_last_form": (c_int32, [c_void_p]),
     "afmm_row_work_device": (c_int32, [c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_uint64,
                                        c_uint64, POINTER(c_uint64), POINTER(Error)]),
     "afmm_partition_rows": (c_int32, [POINTER(c_uint64), c_uint64, c_uint32, POINTER(c_uint64)]),

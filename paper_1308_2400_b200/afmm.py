@@ -225,6 +225,11 @@ class DeviceContext:
         self._lib.afmm_context_last_timing(self._h, *[ctypes.byref(x) for x in v])
         return tuple(x.value for x in v)
 
+    def last_form(self) -> str:
+        """Kernel of the last product: "bform" (rep uniform per warp) or "aform"
+        (Case A, base uniform per warp)."""
+        return "aform" if self._lib.afmm_context_last_form(self._h) == 1 else "bform"
+
     def finish(self) -> OpCounts:
         counts = _lib.OpCounts()
         err = _lib.Error()

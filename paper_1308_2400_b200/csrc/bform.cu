@@ -829,6 +829,231 @@ cudaError_t launch_tm(const CUtensorMap* tmap, const int2* lists, uint64_t cap,
 }
 
 // ---------------------------------------------------------------------------
+// k_aform: Case A with the base uniform per warp ("A-form").
+//
+// The B-form runs Case A on transposed operands, so its lanes are Z rows and
+// every zero base X[i,k] leaves a lane idle: at density d1 the FP pipe does at
+// most d1 useful work (cfg3 d1 = 0.1: 3-9% of peak). Here a warp owns Z row i
+// in the reference's own orientation (kernels.hpp:118-135): it walks row i's
+// compacted nonzero bases (k, X[i,k]) -- zero bases are skipped for the whole
+// warp, as the reference skips them -- and each lane holds CPL columns j of
+// Z[i,:]. The reps Y[k,j] now differ per lane, so the rep loop runs the
+// warp-uniform trip count R = max |Y[k,j]| over the CTA's column tile
+// (precomputed per (k, tile)), and iteration t adds the base to exactly the
+// columns with |Y[k,j]| >= t: one setp.ge.f16x2 tests two columns' fp16 counts
+// (exact up to 2048) and sets two predicates for two predicated FADDs. Each
+// element still receives its |rep| adds consecutively (iterations 1..|rep|)
+// at its k, in k order: the reference's order, bit for bit. The counts arrive
+// as fp16 tiles through a TMA ring (2 bytes per element instead of 4).
+// Cost ~ R x (CPL/2 setp + CPL FADD) per entry: useful while the zero-base
+// waste of the B-form is larger (sparse X).
+// ---------------------------------------------------------------------------
+
+template <class T>
+struct AformGeo {
+  static constexpr int CPL = sizeof(T) == 4 ? 32 : 16;  // columns per lane
+  static constexpr int TILE = 32 * CPL;                 // columns per CTA
+  static constexpr int NBOX = TILE / 256;               // 256-half TMA boxes per k row
+  static constexpr int STAGE_BYTES = KB * TILE * 2;
+  static constexpr int NPAIR = CPL / 2;                 // f16x2 count registers per lane
+  static constexpr int NGRP = CPL / 8;                  // 128-bit count loads per entry
+};
+
+__device__ __forceinline__ uint32_t h2_of(int t) {
+  uint32_t r;
+  asm("{\n\t.reg .f16 h;\n\tcvt.rn.f16.s32 h, %1;\n\tmov.b32 %0, {h, h};\n\t}"
+      : "=r"(r)
+      : "r"(t));
+  return r;
+}
+
+// columns (2p, 2p+1): add b where count >= th (both halves of th equal t)
+__device__ __forceinline__ void padd_ge(float& a0, float& a1, uint32_t cnt, uint32_t th, float b) {
+  asm("{\n\t.reg .pred p, q;\n\tsetp.ge.f16x2 p|q, %2, %3;\n\t"
+      "@p add.rn.f32 %0, %0, %4;\n\t@q add.rn.f32 %1, %1, %4;\n\t}"
+      : "+f"(a0), "+f"(a1)
+      : "r"(cnt), "r"(th), "f"(b));
+}
+// add nb (= -base) where count <= thn (= -t): the negative reps
+__device__ __forceinline__ void padd_le(float& a0, float& a1, uint32_t cnt, uint32_t thn, float nb) {
+  asm("{\n\t.reg .pred p, q;\n\tsetp.le.f16x2 p|q, %2, %3;\n\t"
+      "@p add.rn.f32 %0, %0, %4;\n\t@q add.rn.f32 %1, %1, %4;\n\t}"
+      : "+f"(a0), "+f"(a1)
+      : "r"(cnt), "r"(thn), "f"(nb));
+}
+__device__ __forceinline__ void padd_ge(double& a0, double& a1, uint32_t cnt, uint32_t th,
+                                        double b) {
+  asm("{\n\t.reg .pred p, q;\n\tsetp.ge.f16x2 p|q, %2, %3;\n\t"
+      "@p add.rn.f64 %0, %0, %4;\n\t@q add.rn.f64 %1, %1, %4;\n\t}"
+      : "+d"(a0), "+d"(a1)
+      : "r"(cnt), "r"(th), "d"(b));
+}
+__device__ __forceinline__ void padd_le(double& a0, double& a1, uint32_t cnt, uint32_t thn,
+                                        double nb) {
+  asm("{\n\t.reg .pred p, q;\n\tsetp.le.f16x2 p|q, %2, %3;\n\t"
+      "@p add.rn.f64 %0, %0, %4;\n\t@q add.rn.f64 %1, %1, %4;\n\t}"
+      : "+d"(a0), "+d"(a1)
+      : "r"(cnt), "r"(thn), "d"(nb));
+}
+
+__device__ __forceinline__ float entry_base(int2 e) { return __int_as_float(e.y); }
+__device__ __forceinline__ double entry_base(int4 e) { return __hiloint2double(e.w, e.z); }
+__device__ __forceinline__ int2 shfl_entry(int2 v, uint32_t src) {
+  return make_int2(__shfl_sync(FULL, v.x, src), __shfl_sync(FULL, v.y, src));
+}
+__device__ __forceinline__ int4 shfl_entry(int4 v, uint32_t src) {
+  return make_int4(__shfl_sync(FULL, v.x, src), 0, __shfl_sync(FULL, v.z, src),
+                   __shfl_sync(FULL, v.w, src));
+}
+
+template <class T, int CW, int STAGES, int MINB>
+__global__ void __launch_bounds__((CW + 1) * 32, MINB)
+    k_aform(const __grid_constant__ CUtensorMap cmap,
+            const typename AEntry<T>::type* __restrict__ lists, uint64_t cap,
+            const uint32_t* __restrict__ counts, uint32_t nrows, uint32_t rpc, uint32_t ncols,
+            uint32_t nkb, const uint16_t* __restrict__ rmax, uint32_t ntiles,
+            T* __restrict__ out, uint64_t ld_out, int vec_ok, const DevStatus* __restrict__ st) {
+  using Ag = AformGeo<T>;
+  using E = typename AEntry<T>::type;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + STAGES * Ag::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  const uint32_t ring = smem_u32(base);
+
+  if (status_failed(st)) return;  // validation failed: compute nothing (kernels.hpp:115)
+
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  const uint32_t tile = blockIdx.y;
+  const int32_t tile_c = (int32_t)(tile * Ag::TILE);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], CW);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == CW) {
+    // ---- TMA producer: fp16 count tiles ----
+    if (lane == 0) {
+      prefetch_tensormap(&cmap);
+      for (uint32_t i = 0; i < nkb; ++i) {
+        const uint32_t slot = i % STAGES;
+        if (i >= STAGES) mbar_sleep_wait_at(smem_u32(&empty[slot]), ((i / STAGES) - 1) & 1);
+        mbar_arrive_expect_tx(&full[slot], (uint32_t)Ag::STAGE_BYTES);
+#pragma unroll
+        for (int bx = 0; bx < Ag::NBOX; ++bx)
+          tma_load_2d(base + slot * Ag::STAGE_BYTES + bx * KB * 512, &cmap, &full[slot],
+                      tile_c + bx * 256, (int32_t)(i * KB));
+      }
+    }
+    return;
+  }
+
+  // ---- consumers: one Z row per warp ----
+  const uint32_t b = warp < rpc ? blockIdx.x * rpc + warp : nrows;
+  const uint32_t cnt = b < nrows ? counts[b] : 0u;
+  const E* lst = lists + (uint64_t)(b < nrows ? b : 0) * cap;
+  T acc[Ag::CPL];
+#pragma unroll
+  for (int c = 0; c < Ag::CPL; ++c) acc[c] = T(0);
+
+  const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty);
+  uint32_t kb_cur = 0, slot = 0, phase = 0;
+  uint32_t stage_addr = ring + lane * 16;
+  auto advance = [&]() {
+    __syncwarp();
+    if (lane == 0) mbar_arrive_at(empty0 + slot * 8);
+    ++kb_cur;
+    stage_addr += Ag::STAGE_BYTES;
+    if (++slot == STAGES) {
+      slot = 0;
+      phase ^= 1;
+      stage_addr -= STAGES * Ag::STAGE_BYTES;
+    }
+  };
+  const uint16_t* rm_col = rmax + tile;
+  mbar_sleep_wait_at(full0, 0);
+  E cur = lane < cnt ? lst[lane] : E{};
+  E nxt = 32 + lane < cnt ? lst[32 + lane] : E{};
+  E ent = shfl_entry(cur, 0);
+  uint32_t rm = cnt ? __ldg(rm_col + (uint64_t)(uint32_t)ent.x * ntiles) : 0u;
+  for (uint32_t e = 0; e < cnt; ++e) {
+    const uint32_t f = e + 1;
+    if ((f & 31u) == 0) {
+      cur = nxt;
+      const uint32_t pn = f + 32 + lane;
+      nxt = pn < cnt ? lst[pn] : E{};
+    }
+    const E ent_n = shfl_entry(cur, f & 31u);
+    const uint32_t rm_n = f < cnt ? __ldg(rm_col + (uint64_t)(uint32_t)ent_n.x * ntiles) : 0u;
+    const uint32_t k = (uint32_t)ent.x;
+    const uint32_t kb = k / KB;
+    while (kb_cur < kb) {
+      advance();
+      mbar_sleep_wait_at(full0 + slot * 8, phase);
+    }
+    const int R = (int)(rm & 0x7fffu);
+    if (R != 0) {
+      uint32_t c2[Ag::NPAIR];
+#pragma unroll
+      for (int g = 0; g < Ag::NGRP; ++g) {
+        uint32_t v0, v1, v2, v3;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
+                     : "r"(stage_addr + g * KB * 512 + (k % KB) * 512));
+        c2[4 * g] = v0;
+        c2[4 * g + 1] = v1;
+        c2[4 * g + 2] = v2;
+        c2[4 * g + 3] = v3;
+      }
+      const T bv = entry_base(ent);
+      if ((rm & 0x8000u) == 0) {
+#pragma unroll 1
+        for (int t = 1; t <= R; ++t) {
+          const uint32_t th = h2_of(t);
+#pragma unroll
+          for (int p = 0; p < Ag::NPAIR; ++p) padd_ge(acc[2 * p], acc[2 * p + 1], c2[p], th, bv);
+        }
+      } else {  // the tile row holds negative reps: step = -base there (kernels.hpp:97)
+        const T nb = -bv;
+#pragma unroll 1
+        for (int t = 1; t <= R; ++t) {
+          const uint32_t th = h2_of(t), thn = h2_of(-t);
+#pragma unroll
+          for (int p = 0; p < Ag::NPAIR; ++p) {
+            padd_ge(acc[2 * p], acc[2 * p + 1], c2[p], th, bv);
+            padd_le(acc[2 * p], acc[2 * p + 1], c2[p], thn, nb);
+          }
+        }
+      }
+    }
+    ent = ent_n;
+    rm = rm_n;
+  }
+  while (true) {
+    advance();
+    if (kb_cur >= nkb) break;
+    mbar_sleep_wait_at(full0 + slot * 8, phase);
+  }
+
+  if (b < nrows) {
+    T* orow = out + (uint64_t)b * ld_out;
+#pragma unroll
+    for (int g = 0; g < Ag::NGRP; ++g) {
+      const uint32_t c0 = (uint32_t)tile_c + g * 256 + 8 * lane;
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (c0 + e < ncols) orow[c0 + e] = acc[8 * g + e];
+    }
+  }
+  (void)vec_ok;
+}
+
+// ---------------------------------------------------------------------------
 // k_bform_mr: RW output rows per warp over a DENSE rep tile.
 //
 // For small reps the per-entry cost of k_bform is the shared-memory read of
@@ -1012,6 +1237,39 @@ template cudaError_t launch_bform<double>(int, const CUtensorMap*, const int2*, 
                                           const uint32_t*, uint32_t, int32_t, int32_t, uint32_t,
                                           uint32_t*, uint64_t, double*, uint64_t,
                                           const DevStatus*, cudaStream_t);
+
+template <class T>
+cudaError_t launch_aform(const CUtensorMap* cmap, const typename AEntry<T>::type* lists,
+                         uint64_t cap, const uint32_t* counts, uint32_t nrows, uint32_t ncols,
+                         uint32_t nk, const uint16_t* rmax, T* out, uint64_t ld_out,
+                         const DevStatus* st, cudaStream_t s) {
+  using Ag = AformGeo<T>;
+  static_assert(Ag::TILE == (int)aform_tile_cols<T>(), "A-form tile width");
+  constexpr int CW = kAformRows, STAGES = 6;
+  auto kern = k_aform<T, CW, STAGES, 2>;
+  const size_t smem = 128 + (size_t)STAGES * Ag::STAGE_BYTES + 2 * STAGES * sizeof(uint64_t);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  const uint32_t nkb = (nk + KB - 1) / KB;
+  const uint32_t tiles = (ncols + Ag::TILE - 1) / Ag::TILE;
+  const uint32_t rpc = balanced_rows(nrows, tiles, CW, 2);
+  const bool vec_ok = (ld_out * sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(out) % 16) == 0;
+  dim3 grid((nrows + rpc - 1) / rpc, tiles);
+  kern<<<grid, (CW + 1) * 32, smem, s>>>(*cmap, lists, cap, counts, nrows, rpc, ncols, nkb, rmax,
+                                         tiles, out, ld_out, vec_ok ? 1 : 0, st);
+  note_launch();
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_aform<float>(const CUtensorMap*, const int2*, uint64_t,
+                                         const uint32_t*, uint32_t, uint32_t, uint32_t,
+                                         const uint16_t*, float*, uint64_t, const DevStatus*,
+                                         cudaStream_t);
+template cudaError_t launch_aform<double>(const CUtensorMap*, const int4*, uint64_t,
+                                          const uint32_t*, uint32_t, uint32_t, uint32_t,
+                                          const uint16_t*, double*, uint64_t, const DevStatus*,
+                                          cudaStream_t);
 
 int bform_mr_rows() { return MR_ROWS; }
 

@@ -22,6 +22,18 @@ struct DevStatus {
   unsigned long long pad[2];
 };
 
+// A-form list entry: (k, base) of a nonzero base X[i,k] (k_aform).
+template <class T>
+struct AEntry;
+template <>
+struct AEntry<float> {
+  using type = int2;  // {k, float bits}
+};
+template <>
+struct AEntry<double> {
+  using type = int4;  // {k, 0, low word, high word}
+};
+
 __device__ __forceinline__ bool status_failed(const DevStatus* st) {
   return (st->nonfinite_lhs_inv | st->nonfinite_rhs_inv | st->rep_bad_inv |
           st->rep_too_large_inv) != 0ull;

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -31,6 +32,30 @@ void launch_transpose_compact(const T* y, uint64_t ld, uint32_t n, int2* lists, 
 template <class T>
 void launch_transpose(const T* in, uint64_t ld_in, uint32_t rows, uint32_t cols, T* out,
                       uint64_t ld_out, cudaStream_t s);
+
+// ---- A-form (Case A, base uniform per warp; aform in bform.cu) ----
+// fp16 rep counts of Y (|rep| <= 2048) + per (k, tile) max |rep| | neg flag.
+// fstats (optional, 4 x u64, accumulated): nonzero reps, sum of trip counts,
+// reps beyond 2048, sum of |rep|.
+template <class T>
+void launch_counts_f16(const T* y, uint64_t ld, uint32_t n, uint32_t tile_cols, __half* cnt,
+                       uint64_t ldc, uint16_t* rmax, unsigned long long* fstats, cudaStream_t s);
+// Compacted nonzero bases (k, X[i,k]) of rows [r0, r1).
+template <class T>
+void launch_acompact(const T* x, uint64_t ld, uint32_t n, uint32_t r0, uint32_t r1,
+                     typename AEntry<T>::type* lists, uint64_t cap, uint32_t* counts,
+                     cudaStream_t s);
+// Columns per A-form CTA tile (also the rmax tile width).
+template <class T>
+constexpr uint32_t aform_tile_cols() { return sizeof(T) == 4 ? 1024u : 512u; }
+constexpr int kAformRows = 8;  // rows (warps) per A-form CTA
+constexpr uint32_t kAformMaxRep = 2048;  // fp16 counts are exact up to here
+// Z rows = list rows [0, nrows); cmap = fp16 count tensor map (box 256 x KB).
+template <class T>
+cudaError_t launch_aform(const CUtensorMap* cmap, const typename AEntry<T>::type* lists,
+                         uint64_t cap, const uint32_t* counts, uint32_t nrows, uint32_t ncols,
+                         uint32_t nk, const uint16_t* rmax, T* out, uint64_t ld_out,
+                         const DevStatus* st, cudaStream_t s);
 
 // TMA geometry shared by the ring kernels: boxes of bform_kb() rows x
 // bform_box_bytes() bytes.

@@ -22,6 +22,8 @@
 // plus k_transpose (Case A operand/result transposes) and k_reduce_slices
 // (fast-mode split-k combine). All are HBM-bound; none does FP arithmetic on
 // the product.
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -256,6 +258,98 @@ __global__ void __launch_bounds__(256) k_transpose_compact(const T* __restrict__
   }
 }
 
+// ---- A-form prepass (k_aform, Case A with the base uniform per warp) ----
+
+// A-form rep counts: cnt[k][j] = llround(Y[k,j]) as fp16 (exact for |rep| <=
+// 2048, the A-form's eligibility bound; 0 for zero reps, kernels.hpp:128-130),
+// and per (k, column tile) the largest |rep| (the warp-uniform trip count of
+// the predicated add loop) with bit 15 set when the tile row holds a negative
+// rep. One warp per (k, tile).
+// fstats (optional): [0] nonzero reps, [1] sum of the per-(k, tile) trip counts,
+// [2] reps beyond 2048, [3] sum of |rep| -- the A-form / B-form cost inputs.
+template <class T>
+__global__ void k_counts_f16(const T* __restrict__ y, uint64_t ld, uint32_t n, uint32_t tile_cols,
+                             uint32_t ntiles, __half* __restrict__ cnt, uint64_t ldc,
+                             uint16_t* __restrict__ rmax, unsigned long long* __restrict__ fstats) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t task = warp; task < (uint64_t)n * ntiles; task += nwarps) {
+    const uint64_t k = task / ntiles;
+    const uint32_t t = (uint32_t)(task % ntiles);
+    uint32_t mx = 0, neg = 0, nz = 0, big = 0;
+    unsigned long long sum = 0;
+    for (uint32_t c = t * tile_cols + lane; c < (t + 1) * tile_cols && c < n; c += 32) {
+      const T v = y[k * ld + c];
+      long long r = v != T(0) ? llround((double)v) : 0;
+      nz += r != 0 ? 1u : 0u;
+      sum += (unsigned long long)abs_ll(r);
+      if (r > 2048 || r < -2048) {
+        big += 1;
+        r = r > 0 ? 2048 : -2048;
+      }
+      cnt[k * ldc + c] = __int2half_rn((int)r);
+      const uint32_t a = (uint32_t)(r < 0 ? -r : r);
+      mx = a > mx ? a : mx;
+      neg |= r < 0 ? 1u : 0u;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint32_t m = __shfl_xor_sync(FULL, mx, o);
+      mx = m > mx ? m : mx;
+      neg |= __shfl_xor_sync(FULL, neg, o);
+      nz += __shfl_xor_sync(FULL, nz, o);
+      big += __shfl_xor_sync(FULL, big, o);
+    }
+    sum = warp_sum_u64(sum);
+    if (lane == 0) {
+      rmax[k * ntiles + t] = (uint16_t)(mx | (neg ? 0x8000u : 0u));
+      if (fstats) {
+        if (nz) atomicAdd(&fstats[0], (unsigned long long)nz);
+        if (mx) atomicAdd(&fstats[1], (unsigned long long)mx);
+        if (big) atomicAdd(&fstats[2], (unsigned long long)big);
+        if (sum) atomicAdd(&fstats[3], sum);
+      }
+    }
+  }
+}
+
+// A-form lists: row i in [r0, r1) of X -> its nonzero bases (k, X[i,k]) in
+// increasing k (the zero-base skip of kernels.hpp:121-125 done once).
+template <class T>
+__global__ void k_acompact(const T* __restrict__ x, uint64_t ld, uint32_t n, int vec, uint32_t r0,
+                           uint32_t r1, typename AEntry<T>::type* __restrict__ lists,
+                           uint64_t cap, uint32_t* __restrict__ counts) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = r0 + warp; i < r1; i += nwarps) {
+    const T* row = x + i * ld;
+    auto* out = lists + (i - r0) * cap;
+    uint32_t base = 0;
+    for (uint32_t c0 = 0; c0 < n; c0 += 128) {
+      const uint32_t j0 = c0 + 4 * lane;
+      T v[4];
+      load4(row, j0, n, vec != 0, v);
+      const uint32_t mine = (v[0] != T(0)) + (v[1] != T(0)) + (v[2] != T(0)) + (v[3] != T(0));
+      uint32_t total;
+      uint32_t pos = base + warp_excl_scan(mine, lane, &total);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (v[e] == T(0)) continue;
+        if constexpr (sizeof(T) == 4) {
+          out[pos++] = make_int2((int)(j0 + e), __float_as_int((float)v[e]));
+        } else {
+          const double d = (double)v[e];
+          out[pos++] = make_int4((int)(j0 + e), 0, __double2loint(d), __double2hiint(d));
+        }
+      }
+      base += total;
+    }
+    if (lane == 0) counts[i - r0] = base;
+  }
+}
+
 // Dense int32 reps for k_bform_mr: dst[r][c] = llround(src[r][c]) or, with
 // transpose, llround(src[c][r]); zero reps stay 0 (value == 0.0 or llround == 0
 // both skip, kernels.hpp:128-130 / :151-153). 32x33 smem tiles.
@@ -363,6 +457,24 @@ void launch_rows(const T* x, uint64_t ld, uint32_t n, int which_case, const uint
 }
 
 template <class T>
+void launch_counts_f16(const T* y, uint64_t ld, uint32_t n, uint32_t tile_cols, __half* cnt,
+                       uint64_t ldc, uint16_t* rmax, unsigned long long* fstats, cudaStream_t s) {
+  const uint32_t ntiles = (n + tile_cols - 1) / tile_cols;
+  k_counts_f16<T><<<grid_for_warps((uint64_t)n * ntiles, 8), 256, 0, s>>>(
+      y, ld, n, tile_cols, ntiles, cnt, ldc, rmax, fstats);
+  note_launch();
+}
+
+template <class T>
+void launch_acompact(const T* x, uint64_t ld, uint32_t n, uint32_t r0, uint32_t r1,
+                     typename AEntry<T>::type* lists, uint64_t cap, uint32_t* counts,
+                     cudaStream_t s) {
+  k_acompact<T><<<grid_for_warps(r1 - r0, 8), 256, 0, s>>>(x, ld, n, vec_ok(x, ld), r0, r1, lists,
+                                                          cap, counts);
+  note_launch();
+}
+
+template <class T>
 void launch_transpose_compact(const T* y, uint64_t ld, uint32_t n, int2* lists, uint64_t cap,
                               uint32_t* counts, cudaStream_t s) {
   k_transpose_compact<T><<<(n + 31) / 32, 256, 0, s>>>(y, ld, n, lists, cap, counts);
@@ -402,6 +514,10 @@ void launch_reduce_slices(const T* part, uint64_t stride, uint64_t ld_part, uint
   template void launch_rows<T>(const T*, uint64_t, uint32_t, int, const uint32_t*,             \
                                const unsigned long long*, uint32_t, uint32_t, int2*, uint64_t, \
                                uint32_t*, unsigned long long*, DevStatus*, cudaStream_t);      \
+  template void launch_counts_f16<T>(const T*, uint64_t, uint32_t, uint32_t, __half*, uint64_t, \
+                                     uint16_t*, unsigned long long*, cudaStream_t);            \
+  template void launch_acompact<T>(const T*, uint64_t, uint32_t, uint32_t, uint32_t,           \
+                                   typename AEntry<T>::type*, uint64_t, uint32_t*, cudaStream_t); \
   template void launch_transpose_compact<T>(const T*, uint64_t, uint32_t, int2*, uint64_t,     \
                                             uint32_t*, cudaStream_t);                          \
   template void launch_transpose<T>(const T*, uint64_t, uint32_t, uint32_t, T*, uint64_t,      \

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cinttypes>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -35,6 +36,7 @@ constexpr int kVariantRing = 1;  // TMA smem ring, 512-column tiles (bform.cu)
 constexpr int kVariantSmall = 4; // TMA smem ring, 1 KB-wide x 4-row CTA tiles (bform.cu)
 constexpr int kVariantMR = 5;    // 4 rows per warp over a dense rep tile (bform.cu)
 constexpr int kVariantTmem = 7;  // bases served from tensor memory (bform.cu)
+constexpr int kVariantAForm = 8; // Case A with the base uniform per warp (k_aform, bform.cu)
 
 // AFMM_BFORM=wide|ring|small|mr forces one repeated-addition kernel (all are
 // bit-identical; tests/test_gpu_parity.py runs each). Default: auto.
@@ -45,6 +47,7 @@ int variant_from_env() {
   if (v && std::strcmp(v, "small") == 0) return kVariantSmall;
   if (v && std::strcmp(v, "mr") == 0) return kVariantMR;
   if (v && std::strcmp(v, "tmem") == 0) return kVariantTmem;
+  if (v && std::strcmp(v, "aform") == 0) return kVariantAForm;
   return kVariantAuto;
 }
 
@@ -112,6 +115,23 @@ bool make_tmap(CUtensorMap* map, const T* base, uint64_t rows, uint64_t cols, ui
   return r == CUDA_SUCCESS;
 }
 
+// fp16 rep counts for k_aform: box = 256 columns x KB rows, out-of-range
+// columns read as 0 (no adds).
+bool make_count_tmap(CUtensorMap* map, const __half* cnt, uint64_t rows, uint64_t cols,
+                     uint64_t ldc) {
+  auto fn = get_encode_fn();
+  if (!fn) return false;
+  const cuuint64_t gdim[2] = {cols, rows};
+  const cuuint64_t gstride[1] = {ldc * sizeof(__half)};
+  const cuuint32_t box[2] = {256, (cuuint32_t)afmm_dev::bform_kb()};
+  const cuuint32_t estride[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(cnt), gdim,
+                  gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // Dense int32 reps R'[k][row] for k_bform_mr: box = 64 rows x KB k's,
 // out-of-range rows read as 0 (no adds).
 bool make_rep_tmap(CUtensorMap* map, const int32_t* reps, uint64_t nk, uint64_t rows,
@@ -137,10 +157,11 @@ struct afmm_context {
   cudaStream_t stream = nullptr;
   std::mutex mu;
   // workspace
-  DevBuf status, vec_k, work, lists, counts, base_copy, xt, zt, part, reps;
+  DevBuf status, vec_k, work, lists, counts, base_copy, xt, zt, part, reps, cnt16, rmax, fstats;
   // host-buffer API staging
   DevBuf hx, hy, hz;
   DevStatus* status_host = nullptr;  // pinned
+  unsigned long long* fstats_host = nullptr;  // pinned, 4 words (A-form / B-form choice)
   // state of the last enqueued product, for error decoding
   int last_case = 0, last_dtype = 0;
   const void* last_lhs = nullptr;
@@ -149,6 +170,7 @@ struct afmm_context {
   bool pending = false;
   uint64_t list_cap = 0;
   int variant = 0;  // kVariant* (AFMM_BFORM)
+  int last_form = 0;  // repeated-addition kernel of the last Case A call: 0 B-form, 1 A-form
   // optional phase timing: ev[0] start, ev[1] before compute, ev[2] after compute, ev[3] end
   bool timing = false;
   bool timed_last = false;
@@ -287,6 +309,30 @@ afmm_status decode_status(afmm_context* c, afmm_op_counts* counts, afmm_error* e
     cudaError_t _e = (expr);                        \
     if (_e != cudaSuccess) return cuda_fail(err, _e, what); \
   } while (0)
+
+// Case A kernel choice from the prepass statistics (cycles per SM
+// sub-partition, fitted on B200 to tools/exp_time.py / quick_time.py runs of
+// cfg3 and cfg4):
+//   A-form: ~75 cycles per (nonzero base, column tile) entry + ~54 (fp32) /
+//           ~45 (fp64) per predicated iteration; the trip count of an entry is
+//           the tile's max |rep| at its k, so the iterations are
+//           (nonzero bases per k) x (sum over k and tiles of the trip counts);
+//   B-form: 32 cycles per rep step per tile entry + ~56 per entry (~100 when
+//           the mean rep is below 3: the smem-bound regime, tools/sweep.py).
+// The B-form wins unless the zero bases it adds (1 - d1 of its lanes) cost
+// more than the A-form's divergent trip counts.
+bool prefer_aform(size_t elem, uint64_t n, uint64_t rows, uint64_t nnz_x, uint64_t nnz_y,
+                  uint64_t trip_sum, uint64_t rep_sum) {
+  if (rows == 0 || nnz_y == 0) return false;
+  const double tile_a = elem == 4 ? 1024.0 : 512.0, tile_b = elem == 4 ? 1024.0 : 512.0;
+  const double it_a = elem == 4 ? 54.0 : 45.0;
+  const double tiles_a = std::ceil((double)n / tile_a), tiles_b = std::ceil((double)rows / tile_b);
+  const double cyc_a = 75.0 * (double)nnz_x * tiles_a + it_a * ((double)nnz_x / (double)n) *
+                                                           (double)trip_sum;
+  const double rbar = (double)rep_sum / (double)nnz_y;
+  const double cyc_b = tiles_b * (32.0 * (double)rep_sum + (rbar < 3.0 ? 100.0 : 56.0) * nnz_y);
+  return cyc_a < 0.85 * cyc_b;
+}
 
 // The repeated-addition kernel over B-form rows [0, nrows) (their rep lists
 // are in c->lists / c->counts) and base columns [col0, col0 + ncols) of the
@@ -432,6 +478,60 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
     }
     c->mark(2);
   } else {
+    // A-form or B-form: forced (AFMM_BFORM=aform / any B-form variant), or for
+    // n >= 1024 chosen from the prepass statistics read back here (a short
+    // host wait for the validation pass; the compute stays asynchronous).
+    using E = typename afmm_dev::AEntry<T>::type;
+    const uint32_t tc = afmm_dev::aform_tile_cols<T>();
+    const uint64_t ntiles = (n + tc - 1) / tc, ldc = round_up(n, 64);
+    bool aform = false;
+    const bool consider = rows > 0 && (c->variant == kVariantAForm ||
+                                       (c->variant == kVariantAuto && n >= 1024));
+    afmm_dev::launch_rows<T>(lhs, ld, n32, 0, nullptr, rsum, (uint32_t)r0, (uint32_t)r1, nullptr, 0,
+                             nullptr, work, st, s);
+    if (consider) {
+      CK(c->cnt16.ensure(n * ldc * sizeof(__half)), "workspace");
+      CK(c->rmax.ensure(n * ntiles * sizeof(uint16_t)), "workspace");
+      CK(c->fstats.ensure(4 * sizeof(unsigned long long)), "workspace");
+      auto* fs = c->fstats.as<unsigned long long>();
+      CK(cudaMemsetAsync(fs, 0, 4 * sizeof(unsigned long long), s), "memset");
+      afmm_dev::launch_counts_f16<T>(rhs, ld, n32, tc, c->cnt16.as<__half>(), ldc,
+                                     c->rmax.as<uint16_t>(), fs, s);
+      CK(cudaMemcpyAsync(c->status_host, st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s),
+         "statistics readback");
+      CK(cudaMemcpyAsync(c->fstats_host, fs, 4 * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToHost, s),
+         "statistics readback");
+      CK(cudaStreamSynchronize(s), "statistics readback");
+      const DevStatus& hs = *c->status_host;
+      const bool failed = (hs.nonfinite_lhs_inv | hs.nonfinite_rhs_inv | hs.rep_bad_inv |
+                           hs.rep_too_large_inv) != 0;
+      const unsigned long long* f = c->fstats_host;
+      if (!failed && f[2] == 0) {  // every |rep| <= 2048 (exact fp16 counts)
+        const uint64_t nnz_x = rows * n - hs.zero_skips;
+        aform = c->variant == kVariantAForm ||
+                prefer_aform(sizeof(T), n, rows, nnz_x, f[0], f[1], f[3]);
+      }
+    }
+    c->last_form = aform ? 1 : 0;
+    if (aform) {
+      // A-form: the reference's own orientation, zero bases skipped per warp
+      CK(c->lists.ensure(rows * n * sizeof(E)), "workspace");
+      CK(c->counts.ensure(rows * 4), "workspace");
+      afmm_dev::launch_acompact<T>(lhs, ld, n32, (uint32_t)r0, (uint32_t)r1, c->lists.as<E>(), n,
+                                   c->counts.as<uint32_t>(), s);
+      CUtensorMap cmap;
+      if (!make_count_tmap(&cmap, c->cnt16.as<__half>(), n, n, ldc)) {
+        set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: cuTensorMapEncodeTiled failed");
+        return AFMM_ERR_CUDA;
+      }
+      c->mark(1);
+      CK(afmm_dev::launch_aform<T>(&cmap, c->lists.as<E>(), n, c->counts.as<uint32_t>(),
+                                   (uint32_t)rows, n32, n32, c->rmax.as<uint16_t>(), out, ld_out,
+                                   st, s),
+         "aform");
+      c->mark(2);
+    } else {
     // Case A as Case B on transposed operands: Z^T = (Y^T) (x) (X^T).
     // B-form rows = Z columns j (rep list = column j of Y), B-form columns =
     // Z rows of the slab (bases X[i,k], i in [r0, r1)).
@@ -440,8 +540,6 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
     CK(c->zt.ensure(n * lds * sizeof(T)), "workspace");
     CK(c->lists.ensure(n * n * sizeof(int2)), "workspace");
     CK(c->counts.ensure(n * 4), "workspace");
-    afmm_dev::launch_rows<T>(lhs, ld, n32, 0, nullptr, rsum, (uint32_t)r0, (uint32_t)r1, nullptr,
-                             0, nullptr, work, st, s);
     const bool use_mr = c->variant == kVariantMR && rows > 0;
     const uint64_t ld_r = round_up(n, 4);
     if (use_mr) {  // dense reps R'[k][j] = llround(Y[k][j]): Y itself, converted
@@ -464,6 +562,7 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
     } else {
       c->mark(1);
       c->mark(2);
+    }
     }
   }
   c->mark(3);
@@ -629,7 +728,10 @@ afmm_status afmm_context_create(int32_t device, afmm_context** ctx) {
   cudaGetDevice(&prev);
   if (cudaSetDevice(device) != cudaSuccess ||
       cudaHostAlloc(reinterpret_cast<void**>(&c->status_host), sizeof(DevStatus),
+                    cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc(reinterpret_cast<void**>(&c->fstats_host), 4 * sizeof(unsigned long long),
                     cudaHostAllocDefault) != cudaSuccess) {
+    if (c->status_host) cudaFreeHost(c->status_host);
     delete c;
     cudaSetDevice(prev);
     return AFMM_ERR_CUDA;
@@ -646,9 +748,11 @@ void afmm_context_destroy(afmm_context* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     for (DevBuf* b : {&c->status, &c->vec_k, &c->work, &c->lists, &c->counts, &c->base_copy,
-                      &c->xt, &c->zt, &c->part, &c->reps, &c->hx, &c->hy, &c->hz})
+                      &c->xt, &c->zt, &c->part, &c->reps, &c->cnt16, &c->rmax, &c->fstats,
+                      &c->hx, &c->hy, &c->hz})
       b->release();
     if (c->status_host) cudaFreeHost(c->status_host);
+    if (c->fstats_host) cudaFreeHost(c->fstats_host);
     for (cudaEvent_t& e : c->ev)
       if (e) cudaEventDestroy(e);
   }
@@ -743,6 +847,12 @@ afmm_status afmm_context_last_timing(afmm_context* c, float* prepass_ms, float* 
   if (compute_ms) *compute_ms = v[1];
   if (epilogue_ms) *epilogue_ms = v[2];
   return AFMM_OK;
+}
+
+int32_t afmm_context_last_form(afmm_context* c) {
+  if (!c) return -1;
+  std::lock_guard<std::mutex> g(c->mu);
+  return c->last_case == AFMM_CASE_A ? c->last_form : 0;
 }
 
 afmm_status afmm_row_work_device(afmm_context* c, int32_t which_case, int32_t dtype,

@@ -171,7 +171,8 @@ def test_row_work_and_partition(cuda):
     ctx.close()
 
 
-@pytest.mark.parametrize("name,kw", [("cfg5", {}), ("cfg4", {}), ("cfg3", {"d1": 1.0, "mu": 16})])
+@pytest.mark.parametrize("name,kw", [("cfg5", {}), ("cfg4", {}), ("cfg3", {"d1": 1.0, "mu": 16}),
+                                     ("cfg3", {"d1": 0.1, "mu": 4})])
 def test_full_size_row_sample_bit_exact(cuda, oracle, name, kw):
     """Full BASELINE size on the GPU; a row sample checked bit-exact against the
     multithreaded oracle and the total additions against the closed form."""
@@ -194,6 +195,33 @@ def test_full_size_row_sample_bit_exact(cuda, oracle, name, kw):
     for r in rows:
         zr, _ = oracle.product_mt(cfg.case, lhs, rhs, r, r + 1, 1)
         assert _bits_equal(z[r:r + 1], zr), (name, r)
+    ctx.close()
+
+
+@pytest.mark.parametrize("d1,mu,dt,form", [(0.1, 1, np.float32, "aform"),
+                                           (0.1, 16, np.float64, "aform"),
+                                           (1.0, 16, np.float32, "bform")])
+def test_case_a_kernel_choice_bit_exact(cuda, oracle, d1, mu, dt, form):
+    """Case A picks the A-form (base uniform per warp, zero bases skipped) for
+    sparse X and the B-form for dense X; both are bit-exact with the reference
+    order on every row, counts included."""
+    import torch
+
+    from paper_1308_2400_b200.gen import make_inputs
+
+    afmm = _api()
+    lhs, rhs = make_inputs("cfg3", seed=21, n=1280, d1=d1, mu=mu)
+    lhs, rhs = lhs.astype(dt), rhs.astype(dt)
+    n = lhs.shape[0]
+    ctx = afmm.DeviceContext(0)
+    L = torch.from_numpy(lhs).cuda()
+    R = torch.from_numpy(rhs).cuda()
+    O = torch.empty_like(L)
+    counts = ctx.product("a", L, R, O)
+    assert ctx.last_form() == form
+    z, c = oracle.product_mt("a", lhs, rhs, 0, n, 16)
+    assert (counts.additions, 0, counts.zero_skips) == c
+    assert _bits_equal(O.cpu().numpy(), z)
     ctx.close()
 
 
@@ -242,7 +270,7 @@ def test_fast_mode_within_tolerance(cuda, oracle, name, n, kw):
     assert float(err.max()) <= tol, (name, float(err.max()))
 
 
-@pytest.mark.parametrize("variant", ["wide", "ring", "small", "mr", "tmem"])
+@pytest.mark.parametrize("variant", ["wide", "ring", "small", "mr", "tmem", "aform"])
 def test_both_kernel_variants_bit_exact(cuda, oracle, variant, monkeypatch):
     """k_bform (TMA smem ring) and k_bform_l1 (decoupled warps) give identical bits."""
     import torch
