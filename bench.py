@@ -288,10 +288,15 @@ def main():
     # ---- roofline of the repeated-addition kernel (this rank's launch) ----
     kms = statistics.median(kernel_ms)
     achieved = rank_adds / (kms * 1e-3)
-    traffic = _ncu_traffic(args.config)
+    traffic = _ncu_traffic(args.config if args.config != "cfg3"
+                           else f"cfg3_d{args.d1:g}_mu{args.mu}")
+    form = ctx.last_form() if cfg.case == "a" else "bform"
     roofline = {
-        "bound": "fp-add (CUDA-core FADD2/DADD issue; no tensor cores, no HBM bound)",
-        "kernel": "k_bform",
+        "bound": "fp-add",
+        "bound_detail": "CUDA-core FP add issue (FADD2/DADD; FADD under predicates in the "
+                        "A-form): no tensor cores (they would multiply), far right of the HBM "
+                        "ridge",
+        "kernel": "k_aform" if form == "aform" else "k_bform",
         "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tadd/s",
         "frac": achieved / peak,
         "peak_source": f"measured in-process by afmm_fp_add_peak ({'FADD2' if es == 4 else 'DADD'}"

@@ -225,6 +225,33 @@ def test_case_a_kernel_choice_bit_exact(cuda, oracle, d1, mu, dt, form):
     ctx.close()
 
 
+@pytest.mark.parametrize("big", [False, True])
+def test_case_a_form_signed_and_large_reps(cuda, oracle, big):
+    """Sparse X with signed reps: the A-form's negative-tile path (step = -base,
+    kernels.hpp:97) when every |rep| <= 2048, the B-form when some rep exceeds
+    the fp16-exact range; bit-exact either way."""
+    import torch
+
+    afmm = _api()
+    rng = np.random.default_rng(8)
+    n = 1100
+    x = (rng.random((n, n)) * 2 - 1) * (rng.random((n, n)) < 0.05)
+    y = rng.integers(-6, 7, (n, n)).astype(np.float64)
+    if big:
+        y[rng.integers(0, n, 5), rng.integers(0, n, 5)] = 2049.0
+    x[x == 0] = 0
+    ctx = afmm.DeviceContext(0)
+    L = torch.from_numpy(x).cuda()
+    R = torch.from_numpy(y).cuda()
+    O = torch.empty_like(L)
+    counts = ctx.product("a", L, R, O)
+    assert ctx.last_form() == ("bform" if big else "aform")
+    z, c = oracle.product_mt("a", x, y, 0, n, 16)
+    assert (counts.additions, 0, counts.zero_skips) == c
+    assert _bits_equal(O.cpu().numpy(), z)
+    ctx.close()
+
+
 @pytest.mark.parametrize("case,n,dt", [("a", 3001, np.float32), ("b", 5003, np.float32),
                                         ("a", 1537, np.float64), ("b", 2049, np.float64)])
 def test_ragged_sizes_every_tile_shape(cuda, oracle, case, n, dt):

@@ -29,5 +29,6 @@ ctx = afmm.DeviceContext(0)
 ctx.enable_timing(True)
 for _ in range(a.reps):
     c = ctx.product(cfg.case, L, R, O)
-    print(a.config, c, "phases ms (prepass, kernel, epilogue):", ctx.last_timing(), flush=True)
+    print(a.config, c, "kernel", ctx.last_form(), "phases ms (prepass, kernel, epilogue):",
+          ctx.last_timing(), flush=True)
 ctx.close()
