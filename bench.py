@@ -296,7 +296,7 @@ def main():
         "bound_detail": "CUDA-core FP add issue (FADD2/DADD; FADD under predicates in the "
                         "A-form): no tensor cores (they would multiply), far right of the HBM "
                         "ridge",
-        "kernel": "k_aform" if form == "aform" else "k_bform",
+        "kernel": {"aform": "k_aform", "split": "k_aform+k_bform"}.get(form, "k_bform"),
         "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tadd/s",
         "frac": achieved / peak,
         "peak_source": f"measured in-process by afmm_fp_add_peak ({'FADD2' if es == 4 else 'DADD'}"

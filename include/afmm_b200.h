@@ -143,7 +143,8 @@ afmm_status afmm_context_last_timing(afmm_context* ctx, float* prepass_ms, float
 /* Repeated-addition kernel of the context's last product: 0 = B-form
  * (k_bform: rep uniform per warp; Case B directly, Case A on transposed
  * operands), 1 = A-form (k_aform: Case A with the base uniform per warp,
- * chosen for sparse X). */
+ * chosen for sparse X), 2 = Case A rows split between the two (the sparsest
+ * rows in the A-form). */
 int32_t afmm_context_last_form(afmm_context* ctx);
 
 /* Per-row work W_i (exact additions of Z row i) for the row partition:

@@ -226,9 +226,10 @@ class DeviceContext:
         return tuple(x.value for x in v)
 
     def last_form(self) -> str:
-        """Kernel of the last product: "bform" (rep uniform per warp) or "aform"
-        (Case A, base uniform per warp)."""
-        return "aform" if self._lib.afmm_context_last_form(self._h) == 1 else "bform"
+        """Kernel(s) of the last product: "bform" (rep uniform per warp), "aform"
+        (Case A, base uniform per warp) or "split" (Case A rows divided between
+        the two)."""
+        return {1: "aform", 2: "split"}.get(self._lib.afmm_context_last_form(self._h), "bform")
 
     def finish(self) -> OpCounts:
         counts = _lib.OpCounts()

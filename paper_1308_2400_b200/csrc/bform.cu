@@ -912,7 +912,8 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
             const typename AEntry<T>::type* __restrict__ lists, uint64_t cap,
             const uint32_t* __restrict__ counts, uint32_t nrows, uint32_t rpc, uint32_t ncols,
             uint32_t nkb, const uint16_t* __restrict__ rmax, uint32_t ntiles,
-            T* __restrict__ out, uint64_t ld_out, int vec_ok, const DevStatus* __restrict__ st) {
+            T* __restrict__ out, uint64_t ld_out, const uint32_t* __restrict__ row_idx,
+            const DevStatus* __restrict__ st) {
   using Ag = AformGeo<T>;
   using E = typename AEntry<T>::type;
   extern __shared__ unsigned char smem_raw[];
@@ -955,8 +956,9 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
 
   // ---- consumers: one Z row per warp ----
   const uint32_t b = warp < rpc ? blockIdx.x * rpc + warp : nrows;
-  const uint32_t cnt = b < nrows ? counts[b] : 0u;
-  const E* lst = lists + (uint64_t)(b < nrows ? b : 0) * cap;
+  const uint32_t q = b < nrows ? (row_idx ? row_idx[b] : b) : 0u;  // list / Z row
+  const uint32_t cnt = b < nrows ? counts[q] : 0u;
+  const E* lst = lists + (uint64_t)q * cap;
   T acc[Ag::CPL];
 #pragma unroll
   for (int c = 0; c < Ag::CPL; ++c) acc[c] = T(0);
@@ -1041,7 +1043,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
   }
 
   if (b < nrows) {
-    T* orow = out + (uint64_t)b * ld_out;
+    T* orow = out + (uint64_t)q * ld_out;
 #pragma unroll
     for (int g = 0; g < Ag::NGRP; ++g) {
       const uint32_t c0 = (uint32_t)tile_c + g * 256 + 8 * lane;
@@ -1050,7 +1052,6 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
         if (c0 + e < ncols) orow[c0 + e] = acc[8 * g + e];
     }
   }
-  (void)vec_ok;
 }
 
 // ---------------------------------------------------------------------------
@@ -1242,7 +1243,7 @@ template <class T>
 cudaError_t launch_aform(const CUtensorMap* cmap, const typename AEntry<T>::type* lists,
                          uint64_t cap, const uint32_t* counts, uint32_t nrows, uint32_t ncols,
                          uint32_t nk, const uint16_t* rmax, T* out, uint64_t ld_out,
-                         const DevStatus* st, cudaStream_t s) {
+                         const uint32_t* row_idx, const DevStatus* st, cudaStream_t s) {
   using Ag = AformGeo<T>;
   static_assert(Ag::TILE == (int)aform_tile_cols<T>(), "A-form tile width");
   constexpr int CW = kAformRows, STAGES = 6;
@@ -1254,22 +1255,21 @@ cudaError_t launch_aform(const CUtensorMap* cmap, const typename AEntry<T>::type
   const uint32_t nkb = (nk + KB - 1) / KB;
   const uint32_t tiles = (ncols + Ag::TILE - 1) / Ag::TILE;
   const uint32_t rpc = balanced_rows(nrows, tiles, CW, 2);
-  const bool vec_ok = (ld_out * sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(out) % 16) == 0;
   dim3 grid((nrows + rpc - 1) / rpc, tiles);
   kern<<<grid, (CW + 1) * 32, smem, s>>>(*cmap, lists, cap, counts, nrows, rpc, ncols, nkb, rmax,
-                                         tiles, out, ld_out, vec_ok ? 1 : 0, st);
+                                         tiles, out, ld_out, row_idx, st);
   note_launch();
   return cudaGetLastError();
 }
 
 template cudaError_t launch_aform<float>(const CUtensorMap*, const int2*, uint64_t,
                                          const uint32_t*, uint32_t, uint32_t, uint32_t,
-                                         const uint16_t*, float*, uint64_t, const DevStatus*,
-                                         cudaStream_t);
+                                         const uint16_t*, float*, uint64_t, const uint32_t*,
+                                         const DevStatus*, cudaStream_t);
 template cudaError_t launch_aform<double>(const CUtensorMap*, const int4*, uint64_t,
                                           const uint32_t*, uint32_t, uint32_t, uint32_t,
-                                          const uint16_t*, double*, uint64_t, const DevStatus*,
-                                          cudaStream_t);
+                                          const uint16_t*, double*, uint64_t, const uint32_t*,
+                                          const DevStatus*, cudaStream_t);
 
 int bform_mr_rows() { return MR_ROWS; }
 

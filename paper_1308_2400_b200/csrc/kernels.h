@@ -20,18 +20,21 @@ void launch_scan_stats(const T* lhs, const T* rhs, uint64_t ld, uint32_t n, int 
                        DevStatus* st, uint32_t* nnz, unsigned long long* rsum, cudaStream_t s);
 // Rows of X: work[i] for all rows; slab [r0, r1) adds OpCounts to st and, for
 // Case B with lists != nullptr, gets its compacted (k, rep) lists.
+// nnz_row (optional, Case A): nonzero bases of each slab row.
 template <class T>
 void launch_rows(const T* x, uint64_t ld, uint32_t n, int which_case, const uint32_t* nnz,
                  const unsigned long long* rsum, uint32_t r0, uint32_t r1, int2* lists,
                  uint64_t cap, uint32_t* counts, unsigned long long* work, DevStatus* st,
-                 cudaStream_t s);
+                 cudaStream_t s, uint32_t* nnz_row = nullptr);
 // Case A rep lists: list j = compacted column j of Y.
 template <class T>
 void launch_transpose_compact(const T* y, uint64_t ld, uint32_t n, int2* lists, uint64_t cap,
                               uint32_t* counts, cudaStream_t s);
+// out[oc][r] = in[ir][c] with optional row maps ir = in_rows[r], oc = out_rows[c].
 template <class T>
 void launch_transpose(const T* in, uint64_t ld_in, uint32_t rows, uint32_t cols, T* out,
-                      uint64_t ld_out, cudaStream_t s);
+                      uint64_t ld_out, cudaStream_t s, const uint32_t* in_rows = nullptr,
+                      const uint32_t* out_rows = nullptr);
 
 // ---- A-form (Case A, base uniform per warp; aform in bform.cu) ----
 // fp16 rep counts of Y (|rep| <= 2048) + per (k, tile) max |rep| | neg flag.
@@ -40,22 +43,24 @@ void launch_transpose(const T* in, uint64_t ld_in, uint32_t rows, uint32_t cols,
 template <class T>
 void launch_counts_f16(const T* y, uint64_t ld, uint32_t n, uint32_t tile_cols, __half* cnt,
                        uint64_t ldc, uint16_t* rmax, unsigned long long* fstats, cudaStream_t s);
-// Compacted nonzero bases (k, X[i,k]) of rows [r0, r1).
+// Compacted nonzero bases (k, X[r0 + q, k]) of slab rows q = rows_idx[t]
+// (or t), t < ntask, into lists row q / counts[q].
 template <class T>
-void launch_acompact(const T* x, uint64_t ld, uint32_t n, uint32_t r0, uint32_t r1,
-                     typename AEntry<T>::type* lists, uint64_t cap, uint32_t* counts,
-                     cudaStream_t s);
+void launch_acompact(const T* x, uint64_t ld, uint32_t n, uint32_t r0, uint32_t ntask,
+                     const uint32_t* rows_idx, typename AEntry<T>::type* lists, uint64_t cap,
+                     uint32_t* counts, cudaStream_t s);
 // Columns per A-form CTA tile (also the rmax tile width).
 template <class T>
 constexpr uint32_t aform_tile_cols() { return sizeof(T) == 4 ? 1024u : 512u; }
 constexpr int kAformRows = 8;  // rows (warps) per A-form CTA
 constexpr uint32_t kAformMaxRep = 2048;  // fp16 counts are exact up to here
-// Z rows = list rows [0, nrows); cmap = fp16 count tensor map (box 256 x KB).
+// Warp b computes Z row q = row_idx ? row_idx[b] : b (its list is lists row q,
+// its output out row q), b < nrows; cmap = fp16 count tensor map (box 256 x KB).
 template <class T>
 cudaError_t launch_aform(const CUtensorMap* cmap, const typename AEntry<T>::type* lists,
                          uint64_t cap, const uint32_t* counts, uint32_t nrows, uint32_t ncols,
                          uint32_t nk, const uint16_t* rmax, T* out, uint64_t ld_out,
-                         const DevStatus* st, cudaStream_t s);
+                         const uint32_t* row_idx, const DevStatus* st, cudaStream_t s);
 
 // TMA geometry shared by the ring kernels: boxes of bform_kb() rows x
 // bform_box_bytes() bytes.

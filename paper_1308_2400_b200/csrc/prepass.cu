@@ -152,7 +152,8 @@ __global__ void k_rows(const T* __restrict__ x, uint64_t ld, uint32_t n, int whi
                        const uint32_t* __restrict__ nnz,
                        const unsigned long long* __restrict__ rsum, uint32_t r0, uint32_t r1,
                        int2* __restrict__ lists, uint64_t cap, uint32_t* __restrict__ counts,
-                       unsigned long long* __restrict__ work, DevStatus* st) {
+                       unsigned long long* __restrict__ work, DevStatus* st,
+                       uint32_t* __restrict__ nnz_row) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -202,6 +203,8 @@ __global__ void k_rows(const T* __restrict__ x, uint64_t ld, uint32_t n, int whi
         if (w) atomicAdd(&st->additions, w);
         if (z) atomicAdd(&st->zero_skips, z);
         if (compact) counts[i - r0] = base;
+        // Case A: nonzero bases of the row (its A-form cost)
+        if (nnz_row && which_case == 0) nnz_row[i - r0] = n - (uint32_t)z;
       }
     }
   }
@@ -316,16 +319,20 @@ __global__ void k_counts_f16(const T* __restrict__ y, uint64_t ld, uint32_t n, u
 
 // A-form lists: row i in [r0, r1) of X -> its nonzero bases (k, X[i,k]) in
 // increasing k (the zero-base skip of kernels.hpp:121-125 done once).
+// rows_idx (optional): task t compacts slab row rows_idx[t] (else t); lists
+// and counts are indexed by slab row either way.
 template <class T>
 __global__ void k_acompact(const T* __restrict__ x, uint64_t ld, uint32_t n, int vec, uint32_t r0,
-                           uint32_t r1, typename AEntry<T>::type* __restrict__ lists,
-                           uint64_t cap, uint32_t* __restrict__ counts) {
+                           uint32_t ntask, const uint32_t* __restrict__ rows_idx,
+                           typename AEntry<T>::type* __restrict__ lists, uint64_t cap,
+                           uint32_t* __restrict__ counts) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t i = r0 + warp; i < r1; i += nwarps) {
-    const T* row = x + i * ld;
-    auto* out = lists + (i - r0) * cap;
+  for (uint64_t t = warp; t < ntask; t += nwarps) {
+    const uint64_t q = rows_idx ? rows_idx[t] : t;  // slab row
+    const T* row = x + (r0 + q) * ld;
+    auto* out = lists + q * cap;
     uint32_t base = 0;
     for (uint32_t c0 = 0; c0 < n; c0 += 128) {
       const uint32_t j0 = c0 + 4 * lane;
@@ -346,7 +353,7 @@ __global__ void k_acompact(const T* __restrict__ x, uint64_t ld, uint32_t n, int
       }
       base += total;
     }
-    if (lane == 0) counts[i - r0] = base;
+    if (lane == 0) counts[q] = base;
   }
 }
 
@@ -386,20 +393,30 @@ __global__ void k_reps_dense(const T* __restrict__ src, uint64_t ld_src, uint32_
   }
 }
 
-// out[c * ld_out + r] = in[r * ld_in + c] for r < rows, c < cols.
+// out[oc * ld_out + r] = in[ir * ld_in + c] for r < rows, c < cols, with
+// ir = in_rows ? in_rows[r] : r and oc = out_rows ? out_rows[c] : c (the row
+// maps gather / scatter the rows of a Case A split between the two kernels).
 template <class T>
 __global__ void k_transpose(const T* __restrict__ in, uint64_t ld_in, uint32_t rows,
-                            uint32_t cols, T* __restrict__ out, uint64_t ld_out) {
+                            uint32_t cols, T* __restrict__ out, uint64_t ld_out,
+                            const uint32_t* __restrict__ in_rows,
+                            const uint32_t* __restrict__ out_rows) {
   __shared__ T tile[32][33];
   const uint32_t c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
   for (uint32_t dy = threadIdx.y; dy < 32; dy += blockDim.y) {
     const uint32_t r = r0 + dy, c = c0 + threadIdx.x;
-    if (r < rows && c < cols) tile[dy][threadIdx.x] = in[(uint64_t)r * ld_in + c];
+    if (r < rows && c < cols) {
+      const uint64_t ir = in_rows ? in_rows[r] : r;
+      tile[dy][threadIdx.x] = in[ir * ld_in + c];
+    }
   }
   __syncthreads();
   for (uint32_t dy = threadIdx.y; dy < 32; dy += blockDim.y) {
     const uint32_t c = c0 + dy, r = r0 + threadIdx.x;
-    if (r < rows && c < cols) out[(uint64_t)c * ld_out + r] = tile[threadIdx.x][dy];
+    if (r < rows && c < cols) {
+      const uint64_t oc = out_rows ? out_rows[c] : c;
+      out[oc * ld_out + r] = tile[threadIdx.x][dy];
+    }
   }
 }
 
@@ -450,9 +467,9 @@ template <class T>
 void launch_rows(const T* x, uint64_t ld, uint32_t n, int which_case, const uint32_t* nnz,
                  const unsigned long long* rsum, uint32_t r0, uint32_t r1, int2* lists,
                  uint64_t cap, uint32_t* counts, unsigned long long* work, DevStatus* st,
-                 cudaStream_t s) {
+                 cudaStream_t s, uint32_t* nnz_row) {
   k_rows<T><<<grid_for_warps(n, 8), 256, 0, s>>>(x, ld, n, which_case, vec_ok(x, ld), nnz, rsum,
-                                                  r0, r1, lists, cap, counts, work, st);
+                                                  r0, r1, lists, cap, counts, work, st, nnz_row);
   note_launch();
 }
 
@@ -466,11 +483,11 @@ void launch_counts_f16(const T* y, uint64_t ld, uint32_t n, uint32_t tile_cols, 
 }
 
 template <class T>
-void launch_acompact(const T* x, uint64_t ld, uint32_t n, uint32_t r0, uint32_t r1,
-                     typename AEntry<T>::type* lists, uint64_t cap, uint32_t* counts,
-                     cudaStream_t s) {
-  k_acompact<T><<<grid_for_warps(r1 - r0, 8), 256, 0, s>>>(x, ld, n, vec_ok(x, ld), r0, r1, lists,
-                                                          cap, counts);
+void launch_acompact(const T* x, uint64_t ld, uint32_t n, uint32_t r0, uint32_t ntask,
+                     const uint32_t* rows_idx, typename AEntry<T>::type* lists, uint64_t cap,
+                     uint32_t* counts, cudaStream_t s) {
+  k_acompact<T><<<grid_for_warps(ntask, 8), 256, 0, s>>>(x, ld, n, vec_ok(x, ld), r0, ntask,
+                                                         rows_idx, lists, cap, counts);
   note_launch();
 }
 
@@ -483,9 +500,11 @@ void launch_transpose_compact(const T* y, uint64_t ld, uint32_t n, int2* lists, 
 
 template <class T>
 void launch_transpose(const T* in, uint64_t ld_in, uint32_t rows, uint32_t cols, T* out,
-                      uint64_t ld_out, cudaStream_t s) {
+                      uint64_t ld_out, cudaStream_t s, const uint32_t* in_rows,
+                      const uint32_t* out_rows) {
   dim3 grid((cols + 31) / 32, (rows + 31) / 32);
-  k_transpose<T><<<grid, dim3(32, 8), 0, s>>>(in, ld_in, rows, cols, out, ld_out);
+  k_transpose<T><<<grid, dim3(32, 8), 0, s>>>(in, ld_in, rows, cols, out, ld_out, in_rows,
+                                               out_rows);
   note_launch();
 }
 
@@ -513,15 +532,17 @@ void launch_reduce_slices(const T* part, uint64_t stride, uint64_t ld_part, uint
                                      uint32_t*, unsigned long long*, cudaStream_t);            \
   template void launch_rows<T>(const T*, uint64_t, uint32_t, int, const uint32_t*,             \
                                const unsigned long long*, uint32_t, uint32_t, int2*, uint64_t, \
-                               uint32_t*, unsigned long long*, DevStatus*, cudaStream_t);      \
+                               uint32_t*, unsigned long long*, DevStatus*, cudaStream_t,       \
+                               uint32_t*);                                                     \
   template void launch_counts_f16<T>(const T*, uint64_t, uint32_t, uint32_t, __half*, uint64_t, \
                                      uint16_t*, unsigned long long*, cudaStream_t);            \
   template void launch_acompact<T>(const T*, uint64_t, uint32_t, uint32_t, uint32_t,           \
-                                   typename AEntry<T>::type*, uint64_t, uint32_t*, cudaStream_t); \
+                                   const uint32_t*, typename AEntry<T>::type*, uint64_t,      \
+                                   uint32_t*, cudaStream_t);                                   \
   template void launch_transpose_compact<T>(const T*, uint64_t, uint32_t, int2*, uint64_t,     \
                                             uint32_t*, cudaStream_t);                          \
   template void launch_transpose<T>(const T*, uint64_t, uint32_t, uint32_t, T*, uint64_t,      \
-                                    cudaStream_t);                                             \
+                                    cudaStream_t, const uint32_t*, const uint32_t*);           \
   template void launch_reps_dense<T>(const T*, uint64_t, uint32_t, uint32_t, int, int32_t*,    \
                                      uint64_t, cudaStream_t);                                  \
   template void launch_reduce_slices<T>(const T*, uint64_t, uint64_t, uint32_t, uint32_t,     \

@@ -16,6 +16,7 @@
 #include <cstring>
 #include <mutex>
 #include <new>
+#include <vector>
 
 #include "../../include/afmm_b200.h"
 #include "kernels.h"
@@ -37,6 +38,7 @@ constexpr int kVariantSmall = 4; // TMA smem ring, 1 KB-wide x 4-row CTA tiles (
 constexpr int kVariantMR = 5;    // 4 rows per warp over a dense rep tile (bform.cu)
 constexpr int kVariantTmem = 7;  // bases served from tensor memory (bform.cu)
 constexpr int kVariantAForm = 8; // Case A with the base uniform per warp (k_aform, bform.cu)
+constexpr int kVariantHybrid = 9; // Case A rows split between A-form and B-form (tests)
 
 // AFMM_BFORM=wide|ring|small|mr forces one repeated-addition kernel (all are
 // bit-identical; tests/test_gpu_parity.py runs each). Default: auto.
@@ -48,6 +50,7 @@ int variant_from_env() {
   if (v && std::strcmp(v, "mr") == 0) return kVariantMR;
   if (v && std::strcmp(v, "tmem") == 0) return kVariantTmem;
   if (v && std::strcmp(v, "aform") == 0) return kVariantAForm;
+  if (v && std::strcmp(v, "hybrid") == 0) return kVariantHybrid;
   return kVariantAuto;
 }
 
@@ -158,6 +161,7 @@ struct afmm_context {
   std::mutex mu;
   // workspace
   DevBuf status, vec_k, work, lists, counts, base_copy, xt, zt, part, reps, cnt16, rmax, fstats;
+  DevBuf alists, acounts, ridx;  // A-form lists / counts, Case A row split order
   // host-buffer API staging
   DevBuf hx, hy, hz;
   DevStatus* status_host = nullptr;  // pinned
@@ -170,7 +174,7 @@ struct afmm_context {
   bool pending = false;
   uint64_t list_cap = 0;
   int variant = 0;  // kVariant* (AFMM_BFORM)
-  int last_form = 0;  // repeated-addition kernel of the last Case A call: 0 B-form, 1 A-form
+  int last_form = 0;  // kernel(s) of the last Case A call: 0 B-form, 1 A-form, 2 split
   // optional phase timing: ev[0] start, ev[1] before compute, ev[2] after compute, ev[3] end
   bool timing = false;
   bool timed_last = false;
@@ -313,25 +317,86 @@ afmm_status decode_status(afmm_context* c, afmm_op_counts* counts, afmm_error* e
 // Case A kernel choice from the prepass statistics (cycles per SM
 // sub-partition, fitted on B200 to tools/exp_time.py / quick_time.py runs of
 // cfg3 and cfg4):
-//   A-form: ~75 cycles per (nonzero base, column tile) entry + ~54 (fp32) /
-//           ~45 (fp64) per predicated iteration; the trip count of an entry is
-//           the tile's max |rep| at its k, so the iterations are
-//           (nonzero bases per k) x (sum over k and tiles of the trip counts);
-//   B-form: 32 cycles per rep step per tile entry + ~56 per entry (~100 when
-//           the mean rep is below 3: the smem-bound regime, tools/sweep.py).
-// The B-form wins unless the zero bases it adds (1 - d1 of its lanes) cost
-// more than the A-form's divergent trip counts.
-bool prefer_aform(size_t elem, uint64_t n, uint64_t rows, uint64_t nnz_x, uint64_t nnz_y,
-                  uint64_t trip_sum, uint64_t rep_sum) {
-  if (rows == 0 || nnz_y == 0) return false;
-  const double tile_a = elem == 4 ? 1024.0 : 512.0, tile_b = elem == 4 ? 1024.0 : 512.0;
-  const double it_a = elem == 4 ? 54.0 : 45.0;
-  const double tiles_a = std::ceil((double)n / tile_a), tiles_b = std::ceil((double)rows / tile_b);
-  const double cyc_a = 75.0 * (double)nnz_x * tiles_a + it_a * ((double)nnz_x / (double)n) *
-                                                           (double)trip_sum;
+//   A-form: ~75 cycles per (nonzero base, 1024-column tile) entry + ~54 (fp32)
+//           / ~45 (fp64) per predicated iteration; an entry's trip count is
+//           its tile's max |rep| at its k (mean R = trip_sum / (n x tiles));
+//   B-form: per tile of 1024 (fp32) / 512 (fp64) Z rows, 32 cycles per rep
+//           step + ~56 per list entry (~100 when the mean rep is below 3: the
+//           smem-bound regime, tools/sweep.py) over all of Y's nonzero reps.
+// The A-form cost of a row is proportional to its nonzero bases, the B-form
+// cost to the number of row tiles. Sorting the slab's rows by nonzero count,
+// the cheapest split runs the sparsest m rows as A-form and the rest as
+// B-form, with the B part a whole number of tiles (or none); both parts are
+// charged their wave quantisation. A full switch must beat the pure B-form by
+// 15%, a split by 10% (model error margin). Returns m and the row order (A
+// rows first) when 0 < m < rows.
+uint64_t choose_aform_rows(size_t elem, uint64_t n, int variant, int sms,
+                           const std::vector<uint32_t>& nnz, uint64_t nnz_y, uint64_t trip_sum,
+                           uint64_t rep_sum, std::vector<uint32_t>* order) {
+  const uint64_t rows = nnz.size();
+  if (variant == kVariantAForm) return rows;
+  if (rows == 0 || nnz_y == 0) return 0;
+  const double tile = elem == 4 ? 1024.0 : 512.0, it_a = elem == 4 ? 54.0 : 45.0;
+  const double tiles_a = std::ceil((double)n / tile);
+  const double rmean = (double)trip_sum / ((double)n * tiles_a);
+  const double per_base = tiles_a * (75.0 + it_a * rmean);  // A-form cycles per nonzero base
   const double rbar = (double)rep_sum / (double)nnz_y;
-  const double cyc_b = tiles_b * (32.0 * (double)rep_sum + (rbar < 3.0 ? 100.0 : 56.0) * nnz_y);
-  return cyc_a < 0.85 * cyc_b;
+  const double per_tile = 32.0 * (double)rep_sum + (rbar < 3.0 ? 100.0 : 56.0) * (double)nnz_y;
+  // wave quantisation of a grid of `ctas` 8-row CTAs on 2 x sms slots
+  const double slots = 2.0 * (sms > 0 ? sms : 148);
+  auto wave_eff = [&](double ctas) {
+    return ctas <= 0 ? 1.0 : ctas / (std::ceil(ctas / slots) * slots);
+  };
+  auto cost_b = [&](uint64_t tiles_b) {  // B part of tiles_b whole row tiles
+    return tiles_b == 0 ? 0.0
+                        : (double)tiles_b * per_tile /
+                              wave_eff(std::ceil((double)n / 8.0) * (double)tiles_b);
+  };
+  // rows by ascending nonzero count (counting sort: counts are <= n)
+  std::vector<uint32_t> start(n + 2, 0), idx(rows);
+  for (uint64_t i = 0; i < rows; ++i) ++start[std::min<uint64_t>(nnz[i], n) + 1];
+  for (uint64_t v = 1; v < n + 2; ++v) start[v] += start[v - 1];
+  for (uint64_t i = 0; i < rows; ++i) idx[start[std::min<uint64_t>(nnz[i], n)]++] = (uint32_t)i;
+  std::vector<double> pre(rows + 1, 0.0);
+  for (uint64_t i = 0; i < rows; ++i) pre[i + 1] = pre[i] + (double)nnz[idx[i]];
+  auto cost_a = [&](uint64_t m) {  // A part of the m sparsest rows
+    return m == 0 ? 0.0 : per_base * pre[m] / wave_eff(std::ceil((double)m / 8.0) * tiles_a);
+  };
+  const uint64_t tb = (uint64_t)tile, tiles_all = (rows + tb - 1) / tb;
+  const double pure_b = cost_b(tiles_all);
+  const double pure_a = cost_a(rows);
+  // splits: B part = j whole tiles, A part = the rest (sparsest rows)
+  double best_split = 0.0;
+  uint64_t m_split = 0;
+  for (uint64_t j = 1; j * tb < rows; ++j) {
+    const uint64_t m = rows - j * tb;
+    const double c = cost_a(m) + cost_b(j);
+    if (m_split == 0 || c < best_split) {
+      best_split = c;
+      m_split = m;
+    }
+  }
+  uint64_t best_m = 0;
+  if (variant == kVariantHybrid) {
+    best_m = m_split;
+  } else {
+    // switching every row needs a 15% margin over the pure B-form, a split
+    // (its A part is the sparse rows, its B part whole tiles) 10%
+    double best = pure_b;
+    if (pure_a < 0.85 * pure_b) {
+      best = pure_a;
+      best_m = rows;
+    }
+    if (m_split && best_split < 0.90 * pure_b && best_split < best) best_m = m_split;
+  }
+  if (best_m > 0 && best_m < rows) {
+    // A rows (sparsest first), then B rows in ascending row order
+    order->assign(idx.begin(), idx.begin() + best_m);
+    std::vector<uint32_t> rest(idx.begin() + best_m, idx.end());
+    std::sort(rest.begin(), rest.end());
+    order->insert(order->end(), rest.begin(), rest.end());
+  }
+  return best_m;
 }
 
 // The repeated-addition kernel over B-form rows [0, nrows) (their rep lists
@@ -478,17 +543,23 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
     }
     c->mark(2);
   } else {
-    // A-form or B-form: forced (AFMM_BFORM=aform / any B-form variant), or for
-    // n >= 1024 chosen from the prepass statistics read back here (a short
-    // host wait for the validation pass; the compute stays asynchronous).
+    // Case A runs the B-form on transposed operands, the A-form (base uniform
+    // per warp), or splits the slab's rows between them: forced by AFMM_BFORM
+    // (aform / hybrid / any B-form variant), else for n >= 1024 chosen from
+    // the prepass statistics read back here (a short host wait for the
+    // validation pass; the compute stays asynchronous).
     using E = typename afmm_dev::AEntry<T>::type;
     const uint32_t tc = afmm_dev::aform_tile_cols<T>();
     const uint64_t ntiles = (n + tc - 1) / tc, ldc = round_up(n, 64);
-    bool aform = false;
     const bool consider = rows > 0 && (c->variant == kVariantAForm ||
+                                       c->variant == kVariantHybrid ||
                                        (c->variant == kVariantAuto && n >= 1024));
+    if (consider) CK(c->acounts.ensure(rows * 4), "workspace");
     afmm_dev::launch_rows<T>(lhs, ld, n32, 0, nullptr, rsum, (uint32_t)r0, (uint32_t)r1, nullptr, 0,
-                             nullptr, work, st, s);
+                             nullptr, work, st, s,
+                             consider ? c->acounts.as<uint32_t>() : nullptr);
+    uint64_t m_a = 0;                 // slab rows run by the A-form
+    std::vector<uint32_t> order;      // hybrid: A rows first, then B rows (slab-relative)
     if (consider) {
       CK(c->cnt16.ensure(n * ldc * sizeof(__half)), "workspace");
       CK(c->rmax.ensure(n * ntiles * sizeof(uint16_t)), "workspace");
@@ -508,61 +579,76 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
                            hs.rep_too_large_inv) != 0;
       const unsigned long long* f = c->fstats_host;
       if (!failed && f[2] == 0) {  // every |rep| <= 2048 (exact fp16 counts)
-        const uint64_t nnz_x = rows * n - hs.zero_skips;
-        aform = c->variant == kVariantAForm ||
-                prefer_aform(sizeof(T), n, rows, nnz_x, f[0], f[1], f[3]);
+        std::vector<uint32_t> nnz(rows);
+        CK(cudaMemcpy(nnz.data(), c->acounts.p, rows * 4, cudaMemcpyDeviceToHost),
+           "statistics readback");
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+        m_a = choose_aform_rows(sizeof(T), n, c->variant, sms, nnz, f[0], f[1], f[3], &order);
       }
     }
-    c->last_form = aform ? 1 : 0;
-    if (aform) {
+    const uint64_t m_b = rows - m_a;
+    const bool split = m_a > 0 && m_b > 0;
+    c->last_form = m_a == 0 ? 0 : (split ? 2 : 1);
+    const uint32_t* ridx = nullptr;
+    if (split) {
+      CK(c->ridx.ensure(rows * 4), "workspace");
+      CK(cudaMemcpyAsync(c->ridx.p, order.data(), rows * 4, cudaMemcpyHostToDevice, s), "H2D");
+      CK(cudaStreamSynchronize(s), "H2D");  // `order` is pageable and local
+      ridx = c->ridx.as<uint32_t>();
+    }
+    if (m_a > 0) {  // the A rows' compacted nonzero bases (k, X[i,k])
+      CK(c->alists.ensure(rows * n * sizeof(E)), "workspace");
+      afmm_dev::launch_acompact<T>(lhs, ld, n32, (uint32_t)r0, (uint32_t)m_a, ridx,
+                                   c->alists.as<E>(), n, c->acounts.as<uint32_t>(), s);
+    }
+    c->mark(1);
+    if (m_a > 0) {
       // A-form: the reference's own orientation, zero bases skipped per warp
-      CK(c->lists.ensure(rows * n * sizeof(E)), "workspace");
-      CK(c->counts.ensure(rows * 4), "workspace");
-      afmm_dev::launch_acompact<T>(lhs, ld, n32, (uint32_t)r0, (uint32_t)r1, c->lists.as<E>(), n,
-                                   c->counts.as<uint32_t>(), s);
       CUtensorMap cmap;
       if (!make_count_tmap(&cmap, c->cnt16.as<__half>(), n, n, ldc)) {
         set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: cuTensorMapEncodeTiled failed");
         return AFMM_ERR_CUDA;
       }
-      c->mark(1);
-      CK(afmm_dev::launch_aform<T>(&cmap, c->lists.as<E>(), n, c->counts.as<uint32_t>(),
-                                   (uint32_t)rows, n32, n32, c->rmax.as<uint16_t>(), out, ld_out,
-                                   st, s),
+      CK(afmm_dev::launch_aform<T>(&cmap, c->alists.as<E>(), n, c->acounts.as<uint32_t>(),
+                                   (uint32_t)m_a, n32, n32, c->rmax.as<uint16_t>(), out, ld_out,
+                                   ridx, st, s),
          "aform");
-      c->mark(2);
-    } else {
-    // Case A as Case B on transposed operands: Z^T = (Y^T) (x) (X^T).
-    // B-form rows = Z columns j (rep list = column j of Y), B-form columns =
-    // Z rows of the slab (bases X[i,k], i in [r0, r1)).
-    const uint64_t lds = round_up(std::max<uint64_t>(rows, 1), 32);
-    CK(c->xt.ensure(n * lds * sizeof(T)), "workspace");
-    CK(c->zt.ensure(n * lds * sizeof(T)), "workspace");
-    CK(c->lists.ensure(n * n * sizeof(int2)), "workspace");
-    CK(c->counts.ensure(n * 4), "workspace");
-    const bool use_mr = c->variant == kVariantMR && rows > 0;
-    const uint64_t ld_r = round_up(n, 4);
-    if (use_mr) {  // dense reps R'[k][j] = llround(Y[k][j]): Y itself, converted
-      CK(c->reps.ensure(n * ld_r * sizeof(int32_t)), "workspace");
-      afmm_dev::launch_reps_dense<T>(rhs, ld, n32, n32, 0, c->reps.as<int32_t>(), ld_r, s);
-    } else {
-      afmm_dev::launch_transpose_compact<T>(rhs, ld, n32, c->lists.as<int2>(), n,
-                                            c->counts.as<uint32_t>(), s);
     }
-    if (rows > 0) {
-      afmm_dev::launch_transpose<T>(lhs + r0 * ld, ld, (uint32_t)rows, n32, c->xt.as<T>(), lds,
-                                    s);
-      c->mark(1);
-      afmm_status cs = launch_compute<T>(c, mode, c->xt.as<T>(), n, rows, lds, n32, 0, (int32_t)rows,
-                                         c->zt.as<T>(), lds, st, err,
-                                         use_mr ? c->reps.as<int32_t>() : nullptr, ld_r);
-      if (cs != AFMM_OK) return cs;
-      c->mark(2);
-      afmm_dev::launch_transpose<T>(c->zt.as<T>(), lds, n32, (uint32_t)rows, out, ld_out, s);
+    if (m_b > 0 || rows == 0) {
+      // B-form: Case A as Case B on transposed operands, Z^T = (Y^T) (x) (X^T).
+      // B-form rows = Z columns j (rep list = column j of Y), B-form columns =
+      // the slab's B rows (bases X[i,k]; gathered through ridx when split).
+      const uint64_t lds = round_up(std::max<uint64_t>(m_b, 1), 32);
+      CK(c->xt.ensure(n * lds * sizeof(T)), "workspace");
+      CK(c->zt.ensure(n * lds * sizeof(T)), "workspace");
+      CK(c->lists.ensure(n * n * sizeof(int2)), "workspace");
+      CK(c->counts.ensure(n * 4), "workspace");
+      const bool use_mr = c->variant == kVariantMR && m_b > 0;
+      const uint64_t ld_r = round_up(n, 4);
+      if (use_mr) {  // dense reps R'[k][j] = llround(Y[k][j]): Y itself, converted
+        CK(c->reps.ensure(n * ld_r * sizeof(int32_t)), "workspace");
+        afmm_dev::launch_reps_dense<T>(rhs, ld, n32, n32, 0, c->reps.as<int32_t>(), ld_r, s);
+      } else {
+        afmm_dev::launch_transpose_compact<T>(rhs, ld, n32, c->lists.as<int2>(), n,
+                                              c->counts.as<uint32_t>(), s);
+      }
+      if (m_b > 0) {
+        const uint32_t* bidx = split ? ridx + m_a : nullptr;
+        afmm_dev::launch_transpose<T>(lhs + r0 * ld, ld, (uint32_t)m_b, n32, c->xt.as<T>(), lds, s,
+                                      bidx, nullptr);
+        afmm_status cs = launch_compute<T>(c, mode, c->xt.as<T>(), n, m_b, lds, n32, 0,
+                                           (int32_t)m_b, c->zt.as<T>(), lds, st, err,
+                                           use_mr ? c->reps.as<int32_t>() : nullptr, ld_r);
+        if (cs != AFMM_OK) return cs;
+        c->mark(2);
+        afmm_dev::launch_transpose<T>(c->zt.as<T>(), lds, n32, (uint32_t)m_b, out, ld_out, s,
+                                      nullptr, bidx);
+      } else {
+        c->mark(2);
+      }
     } else {
-      c->mark(1);
       c->mark(2);
-    }
     }
   }
   c->mark(3);
@@ -749,7 +835,7 @@ void afmm_context_destroy(afmm_context* c) {
     cudaStreamSynchronize(c->stream);
     for (DevBuf* b : {&c->status, &c->vec_k, &c->work, &c->lists, &c->counts, &c->base_copy,
                       &c->xt, &c->zt, &c->part, &c->reps, &c->cnt16, &c->rmax, &c->fstats,
-                      &c->hx, &c->hy, &c->hz})
+                      &c->alists, &c->acounts, &c->ridx, &c->hx, &c->hy, &c->hz})
       b->release();
     if (c->status_host) cudaFreeHost(c->status_host);
     if (c->fstats_host) cudaFreeHost(c->fstats_host);

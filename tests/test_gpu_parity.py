@@ -225,6 +225,36 @@ def test_case_a_kernel_choice_bit_exact(cuda, oracle, d1, mu, dt, form):
     ctx.close()
 
 
+@pytest.mark.parametrize("dt,n,auto", [(np.float32, 1300, False), (np.float64, 1300, False),
+                                        (np.float32, 2100, True)])
+def test_case_a_row_split_bit_exact(cuda, oracle, monkeypatch, dt, n, auto):
+    """Case A with per-row X densities drawn from Beta(0.5, 0.5) (cfg4's
+    distribution): the slab's rows split between the A-form (sparsest rows,
+    gathered through a row map) and the B-form (the rest, gathered and scattered
+    by the transposes). Forced split and the automatic choice; bit-exact with
+    the reference order and counts on every row."""
+    import torch
+
+    from paper_1308_2400_b200.gen import make_inputs
+
+    if not auto:
+        monkeypatch.setenv("AFMM_BFORM", "hybrid")
+    afmm = _api()
+    lhs, rhs = make_inputs("cfg4", seed=4, n=n)
+    lhs, rhs = lhs.astype(dt), rhs.astype(dt)
+    ctx = afmm.DeviceContext(0)
+    L = torch.from_numpy(lhs).cuda()
+    R = torch.from_numpy(rhs).cuda()
+    O = torch.empty_like(L)
+    counts = ctx.product("a", L, R, O)
+    if not auto:
+        assert ctx.last_form() == "split"
+    z, c = oracle.product_mt("a", lhs, rhs, 0, n, 16)
+    assert (counts.additions, 0, counts.zero_skips) == c
+    assert _bits_equal(O.cpu().numpy(), z), ctx.last_form()
+    ctx.close()
+
+
 @pytest.mark.parametrize("big", [False, True])
 def test_case_a_form_signed_and_large_reps(cuda, oracle, big):
     """Sparse X with signed reps: the A-form's negative-tile path (step = -base,
