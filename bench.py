@@ -118,65 +118,98 @@ class ClockSampler(threading.Thread):
 # CPU baseline: the oracle port on a row sample
 # ---------------------------------------------------------------------------
 
-def cpu_sample_rate(case, lhs, rhs, threads, target_s, blocks_hint=None):
-    """Time the multithreaded oracle port on row blocks spread over the matrix.
+class CpuBaseline:
+    """The reference's CPU path on the host cores, on a bounded row sample.
 
-    Returns (adds/s, description, total_adds, seconds)."""
-    from oracle.oracle import Oracle
+    kind "reference": the UNMODIFIED afmm_case_{a,b} (oracle/_ref/libafmm_ref.so,
+    built from /root/reference in the build container; fp32 inputs widened
+    exactly to the reference's fp64), one call per thread, each on the lhs with
+    only its block of rows kept (rows are independent, kernels.hpp:119,148).
+    The per-call overhead of the n x n call (allocation, validation, zero-row
+    scans) is measured by the same batch with empty blocks and subtracted.
+    kind "port": the oracle restatement (bit-identical, tests/test_oracle.py),
+    used only when the reference library is absent."""
 
-    oracle = Oracle()
-    n = lhs.shape[0]
-    # calibrate with one block of `threads` rows in the middle
-    r0 = n // 2
-    t0 = time.perf_counter()
-    _, c = oracle.product_mt(case, lhs, rhs, r0, min(n, r0 + threads), threads)
-    dt = time.perf_counter() - t0
-    blocks = blocks_hint or max(1, min(64, int(target_s / max(dt, 1e-3))))
-    starts = np.linspace(0, max(n - threads, 0), blocks).astype(int)
-    adds = 0
-    t0 = time.perf_counter()
-    for s in starts:
-        _, c = oracle.product_mt(case, lhs, rhs, int(s), min(n, int(s) + threads), threads)
-        adds += c[0]
-    secs = time.perf_counter() - t0
-    rows = blocks * min(threads, n)
-    desc = (f"{rows} of {n} rows ({blocks} blocks of {min(threads, n)} consecutive rows spread "
-            f"evenly), {adds:.4e} additions, {secs:.1f} s")
-    return adds / secs, desc, adds, secs, blocks
+    def __init__(self, case, lhs, rhs, threads):
+        from oracle.oracle import Oracle, Reference, reference_available
+
+        self.case = case
+        self.n = lhs.shape[0]
+        self.threads = max(1, min(threads, self.n))
+        self.kind = "reference" if reference_available() else "port"
+        if self.kind == "reference":
+            self.ref = Reference()
+            self.lhs = np.ascontiguousarray(lhs, dtype=np.float64)
+            self.rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+            self.overhead, _, _ = self.ref.rows_batch(case, self.lhs, self.rhs,
+                                                      [(0, 0)] * self.threads)
+        else:
+            self.oracle = Oracle()
+            self.lhs, self.rhs = lhs, rhs
+            self.overhead = 0.0
+
+    def _blocks(self, b):
+        starts = np.linspace(0, self.n - b, self.threads).astype(int)
+        return [(int(st), int(st) + b) for st in starts]
+
+    def batch(self, b):
+        """b rows per thread -> (work seconds, additions)."""
+        if self.kind == "reference":
+            wall, adds, _ = self.ref.rows_batch(self.case, self.lhs, self.rhs, self._blocks(b))
+            return max(wall - self.overhead, 1e-6), adds
+        t0 = time.perf_counter()
+        adds = 0
+        for r0, r1 in self._blocks(b):
+            _, c = self.oracle.product_mt(self.case, self.lhs, self.rhs, r0, r1, self.threads)
+            adds += c[0]
+        return time.perf_counter() - t0, adds
+
+    def rows_for(self, target_s):
+        """Rows per thread for about target_s seconds of work."""
+        secs, _ = self.batch(1)
+        return int(max(1, min(self.n // self.threads, round(target_s / max(secs, 1e-4)))))
+
+    def describe(self, b, adds, secs):
+        what = ("unmodified reference afmm_case_%s (oracle/_ref/libafmm_ref.so, fp64; fp32 "
+                "inputs widened exactly), one call per thread on its row block, per-call "
+                "overhead %.2f s (measured with empty blocks) subtracted"
+                % (self.case, self.overhead)) if self.kind == "reference" else \
+            "oracle/afmm_oracle.c restatement (bit-identical to the unmodified reference)"
+        return (f"{self.threads} threads x {b} rows ({self.threads * b} of {self.n} rows, blocks "
+                f"spread evenly), {adds:.4e} additions in {secs:.1f} s; {what}")
 
 
 def run_reference_arm(args, rank):
-    """--impl reference: the reference's CPU algorithm (oracle port, bit-identical to the
-    unmodified reference per tests/test_oracle.py), all host threads, rank 0 only."""
+    """--impl reference: the reference's own CPU implementation of the path (unmodified
+    afmm_case_{a,b} from oracle/_ref) on all host threads, rank 0 only."""
     if rank != 0:
         return
     from paper_1308_2400_b200.gen import CONFIGS, make_inputs
 
     cfg = CONFIGS[args.config]
     lhs, rhs = make_inputs(args.config, seed=args.seed, d1=args.d1, mu=args.mu)
-    threads = os.cpu_count() or 1
-    # size one step to ~target seconds
-    _, _, _, _, blocks = cpu_sample_rate(cfg.case, lhs, rhs, threads, args.cpu_seconds * 0.4)
+    cpu = CpuBaseline(cfg.case, lhs, rhs, os.cpu_count() or 1)
+    b = cpu.rows_for(args.cpu_seconds * 0.5)
     for _ in range(max(0, min(args.warmup, 1))):
-        cpu_sample_rate(cfg.case, lhs, rhs, threads, 0, blocks_hint=1)
+        cpu.batch(1)
     adds = 0
     secs = 0.0
-    desc = ""
     for _ in range(args.steps):
-        _, desc, a, s, _ = cpu_sample_rate(cfg.case, lhs, rhs, threads, 0, blocks_hint=blocks)
+        s_, a = cpu.batch(b)
         adds += a
-        secs += s
+        secs += s_
     value = adds / secs
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64 (reference is fp64-only; fp32 configs run the fp32 restatement)"
+        "dtype": "f64 (the reference is fp64-only; fp32 configs widened exactly)"
         if cfg.dtype == "float32" else "f64",
         "data": "synthetic (seeded numpy, BASELINE.json distributions)",
         "config": _config_dict(args, cfg),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": "per step: " + desc},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu.threads, "kind": cpu.kind,
+                         "sample": "per step: " + cpu.describe(b, adds // args.steps,
+                                                               secs / args.steps)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -316,12 +349,11 @@ def main():
     # ---- CPU baseline ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
-        rate, desc, _, _, _ = cpu_sample_rate(cfg.case, lhs, rhs, threads, args.cpu_seconds)
-        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": desc + "; oracle/afmm_oracle.c restatement (bit-identical to the "
-                                "unmodified reference, tests/test_oracle.py), -O2 "
-                                "-ffp-contract=off, pthreads over rows"}
+        base = CpuBaseline(cfg.case, lhs, rhs, os.cpu_count() or 1)
+        b = base.rows_for(args.cpu_seconds)
+        secs, adds = base.batch(b)
+        cpu = {"value": adds / secs, "unit": UNIT, "cores": base.threads, "kind": base.kind,
+               "sample": base.describe(b, adds, secs)}
 
     if rank == 0:
         line = {

@@ -152,6 +152,12 @@ class Reference:
                                              c_uint64, c_void_p, c_void_p]
         lib.ref_make_matrix.restype = c_int
         lib.ref_make_matrix.argtypes = [c_uint64, c_char_p, c_size_t]
+        lib.ref_hold_matrix.restype = c_void_p
+        lib.ref_hold_matrix.argtypes = [c_void_p, c_uint64, c_char_p, c_size_t]
+        lib.ref_release_matrix.argtypes = [c_void_p]
+        lib.ref_case_rows.restype = c_int
+        lib.ref_case_rows.argtypes = [c_int, c_void_p, c_uint64, c_uint64, c_uint64, c_void_p,
+                                      c_void_p, POINTER(Counts), c_char_p, c_size_t]
         self.lib = lib
 
     STATUS = {0: None, 1: "shape_error", 2: "domain_error", 3: "invalid_argument", 4: "other"}
@@ -170,6 +176,45 @@ class Reference:
         if rc != 0:
             return None, None, (self.STATUS[rc], msg.value.decode())
         return out, c.as_tuple(), None
+
+    def rows_batch(self, case: str, lhs: np.ndarray, rhs: np.ndarray, blocks):
+        """Run the unmodified afmm_case_{a,b} once per row block (r0, r1), all blocks
+        concurrently on their own threads (ctypes releases the GIL), each on lhs with
+        only its rows kept and the shared rhs. Returns (wall seconds, total additions,
+        {(r0, r1): product rows})."""
+        import threading
+        import time
+
+        lhs = np.ascontiguousarray(lhs, dtype=np.float64)
+        rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+        n = lhs.shape[0]
+        msg = ctypes.create_string_buffer(512)
+        h = self.lib.ref_hold_matrix(rhs.ctypes.data, n, msg, 512)
+        if not h:
+            raise ValueError(msg.value.decode())
+        out = {b: np.empty((b[1] - b[0], n), dtype=np.float64) for b in blocks}
+        counts = {b: Counts() for b in blocks}
+        errs = []
+
+        def work(b):
+            m = ctypes.create_string_buffer(512)
+            rc = self.lib.ref_case_rows(1 if case == "b" else 0, lhs.ctypes.data, n, b[0], b[1],
+                                        h, out[b].ctypes.data if b[1] > b[0] else None,
+                                        ctypes.byref(counts[b]), m, 512)
+            if rc != 0:
+                errs.append(m.value.decode())
+
+        threads = [threading.Thread(target=work, args=(b,)) for b in blocks]
+        t0 = time.perf_counter()
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        wall = time.perf_counter() - t0
+        self.lib.ref_release_matrix(h)
+        if errs:
+            raise ValueError(errs[0])
+        return wall, sum(counts[b].additions for b in blocks), out
 
     def multiply_ijk(self, lhs, rhs):
         lhs = np.ascontiguousarray(lhs, dtype=np.float64)

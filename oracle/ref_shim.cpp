@@ -153,6 +153,43 @@ void ref_make_factor_pair(int case_b, std::uint64_t n, double d1, double d2, dou
   std::memcpy(rhs, pair.second.data().data(), n * n * sizeof(double));
 }
 
+// ---- row-block entry for the CPU baseline (bench.py) ----
+// A DenseMatrix held across calls (the shared rhs of a timing batch).
+void* ref_hold_matrix(const double* p, std::uint64_t n, char* msg, std::size_t cap) {
+  afmm::DenseMatrix* m = nullptr;
+  const int rc = guarded([&] { m = new afmm::DenseMatrix(wrap(p, n)); }, msg, cap);
+  return rc == 0 ? m : nullptr;
+}
+
+void ref_release_matrix(void* h) { delete static_cast<afmm::DenseMatrix*>(h); }
+
+// The unmodified afmm_case_{a,b} on (lhs with only rows [r0, r1) kept, the
+// other rows zero) x rhs. Rows are independent (kernels.hpp:119,148), so rows
+// [r0, r1) of the product are the reference's result for those rows; the zero
+// rows cost only the per-call overhead (validation, Z allocation, zero-row
+// scans), which the caller measures with r0 == r1 and subtracts. Several
+// threads may call this concurrently with the same rhs handle.
+int ref_case_rows(int case_b, const double* lhs, std::uint64_t n, std::uint64_t r0,
+                  std::uint64_t r1, const void* rhs_h, double* out_rows, RefCounts* counts,
+                  char* msg, std::size_t cap) {
+  return guarded(
+      [&] {
+        afmm::DenseMatrix l(n);
+        const auto ld = l.data();
+        std::memcpy(ld.data() + r0 * n, lhs + r0 * n, (r1 - r0) * n * sizeof(double));
+        const auto& r = *static_cast<const afmm::DenseMatrix*>(rhs_h);
+        const afmm::MultiplyResult res = case_b ? afmm::afmm_case_b(l, r) : afmm::afmm_case_a(l, r);
+        const auto d = res.product.data();
+        if (out_rows) std::memcpy(out_rows, d.data() + r0 * n, (r1 - r0) * n * sizeof(double));
+        if (counts) {
+          counts->additions = res.counts.additions;
+          counts->multiplications = res.counts.multiplications;
+          counts->zero_skips = res.counts.zero_skips;
+        }
+      },
+      msg, cap);
+}
+
 // test_kernels.cpp:208-217: the 16-bit-magnitude operands (|entries| <= 2^15),
 // drawn from std::mt19937_64(0xB16) exactly as that test does.
 void ref_b16_pair(double* lhs, double* rhs) {
