@@ -152,6 +152,38 @@ def test_device_api_row_slabs_and_padded_ld(cuda, oracle):
     ctx.close()
 
 
+@pytest.mark.parametrize("variant", ["aform", "hybrid", None])
+def test_device_api_row_slabs_case_a_forms(cuda, oracle, monkeypatch, variant):
+    """The A-form and the row split through the device entry: row slabs
+    [r0, r1) (slab-relative lists, row maps and output rows) and a padded
+    leading dimension, bit-exact against the oracle rows."""
+    import torch
+
+    from paper_1308_2400_b200.gen import make_inputs
+
+    if variant:
+        monkeypatch.setenv("AFMM_BFORM", variant)
+    afmm = _api()
+    ctx = afmm.DeviceContext(0)
+    n = 1100
+    lhs0, rhs0 = make_inputs("cfg4", seed=9, n=n)
+    rhs0[::7] = -rhs0[::7]  # some negative reps
+    for dt, tdt in ((np.float64, torch.float64), (np.float32, torch.float32)):
+        lhs, rhs = lhs0.astype(dt), rhs0.astype(dt)
+        ld = n + 3
+        L = torch.zeros((n, ld), dtype=tdt, device="cuda")
+        R = torch.zeros((n, ld), dtype=tdt, device="cuda")
+        L[:, :n] = torch.from_numpy(lhs)
+        R[:, :n] = torch.from_numpy(rhs)
+        for r0, r1 in ((0, n), (17, 900), (1099, 1100)):
+            O = torch.full((r1 - r0, ld), 7.0, dtype=tdt, device="cuda")
+            counts = ctx.product("a", L[:, :n], R[:, :n], O[:, :n], r0, r1)
+            z, c = oracle.product_mt("a", lhs, rhs, r0, r1, 16)
+            assert (counts.additions, 0, counts.zero_skips) == c
+            assert _bits_equal(O[:, :n].cpu().numpy(), z), (variant, dt, r0, r1, ctx.last_form())
+    ctx.close()
+
+
 def test_row_work_and_partition(cuda):
     import torch
 
