@@ -381,3 +381,44 @@ def test_both_kernel_variants_bit_exact(cuda, oracle, variant, monkeypatch):
         assert (counts.additions, 0, counts.zero_skips) == c
         assert _bits_equal(O.cpu().numpy(), z), (variant, name)
     ctx.close()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_randomized_shapes_and_distributions(cuda, oracle, seed, monkeypatch):
+    """Seeded fuzz over sizes, densities, rep ranges and signs, both cases, both
+    dtypes and every kernel form: bit-exact products and exact counts."""
+    import torch
+
+    rng = np.random.default_rng(1000 + seed)
+    variants = [None, "wide", "ring", "small", "aform", "hybrid", "tmem"]
+    for trial in range(16):
+        variant = variants[rng.integers(len(variants))]
+        if variant:
+            monkeypatch.setenv("AFMM_BFORM", variant)
+        else:
+            monkeypatch.delenv("AFMM_BFORM", raising=False)
+        afmm = _api()
+        ctx = afmm.DeviceContext(0)
+        n = int(rng.choice([1, 2, 7, 33, 129, 250, 511, 640, 1031]))
+        dt = np.float32 if rng.random() < 0.5 else np.float64
+        case = "a" if rng.random() < 0.5 else "b"
+        d_base, d_rep = rng.uniform(0.02, 1.0), rng.uniform(0.05, 1.0)
+        rmax = int(rng.choice([1, 2, 5, 40, 300]))
+        signed = rng.random() < 0.4
+        bases = rng.standard_normal((n, n)) * (rng.random((n, n)) < d_base)
+        reps = rng.integers(-rmax if signed else 0, rmax + 1, (n, n)) * (rng.random((n, n)) < d_rep)
+        lhs, rhs = (bases, reps) if case == "a" else (reps, bases)
+        lhs = np.ascontiguousarray(lhs, dtype=dt)
+        rhs = np.ascontiguousarray(rhs, dtype=dt)
+        lhs[lhs == 0] = 0
+        rhs[rhs == 0] = 0
+        z, c = oracle.product_mt(case, lhs, rhs, 0, n, 16)
+        L = torch.from_numpy(lhs).cuda()
+        R = torch.from_numpy(rhs).cuda()
+        O = torch.empty_like(L)
+        counts = ctx.product(case, L, R, O)
+        what = (trial, variant, n, dt.__name__, case, round(d_base, 2), round(d_rep, 2), rmax,
+                signed, ctx.last_form())
+        assert (counts.additions, 0, counts.zero_skips) == c, what
+        assert _bits_equal(O.cpu().numpy(), z), what
+        ctx.close()
