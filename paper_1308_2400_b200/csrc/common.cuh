@@ -137,7 +137,11 @@ __device__ __forceinline__ void mbar_wait_at(uint32_t addr, uint32_t parity) {
 // after a short system time limit and the retry loop costs issue slots that
 // the FP-bound warps on the same SM sub-partition need (ncu source view: the
 // producer's empty-barrier loop was 11% of all issued instructions).
+#ifndef AFMM_EXP_SUSPEND_NS
 constexpr uint32_t SUSPEND_NS = 1000000;
+#else
+constexpr uint32_t SUSPEND_NS = AFMM_EXP_SUSPEND_NS;
+#endif
 
 __device__ __forceinline__ void mbar_sleep_wait_at(uint32_t addr, uint32_t parity) {
   uint32_t ok = 0;
