@@ -5,8 +5,8 @@
 <launches.csv> is the CSV of
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
       --clock-control none --csv --log-file <csv> python tools/profile_one.py ...
-The last k_bform / k_aform launch in the list is taken; its bytes per launch
-go to profiles/ncu_traffic.json[<config-key>] (bench.py reports them as
+The k_bform / k_aform launches of the (single) product in the list are summed
+(a Case A row split runs both); the bytes go to profiles/ncu_traffic.json[<config-key>] (bench.py reports them as
 roofline.traffic next to the algorithmic bytes 3 n^2 x elem: X and Y read
 once, Z written once).
 """
@@ -37,16 +37,20 @@ def main():
         d[r[mi]] = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
     if not launches:
         sys.exit(f"no k_bform/k_aform launch in {path}")
+    # one product per launch list (tools/profile_one.py --reps 1): a Case A row
+    # split launches k_aform and k_bform; both belong to the product
+    rd = sum(d["dram__bytes_read.sum"] for d in launches.values())
+    wr = sum(d["dram__bytes_write.sum"] for d in launches.values())
+    t = sum(d["gpu__time_duration.sum"] for d in launches.values())  # seconds
     last = launches[max(launches)]
-    rd, wr = last["dram__bytes_read.sum"], last["dram__bytes_write.sum"]
-    t = last["gpu__time_duration.sum"]  # seconds (units normalised above)
     src = path
     if copy_to:
         os.makedirs(os.path.join(ROOT, copy_to), exist_ok=True)
         dst = os.path.join(copy_to, os.path.basename(path))
         shutil.copy(path, os.path.join(ROOT, dst))
         src = dst
-    kernel = last["kernel"].split("(")[0].replace("void ", "").replace("afmm_dev::", "")
+    kernel = " + ".join(d["kernel"].split("(")[0].replace("void ", "").replace("afmm_dev::", "")
+                        .replace("unnamed>::", "") for _, d in sorted(launches.items()))
     entry = {
         "bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
         "kernel_time_s": t, "kernel": kernel, "source": src,
