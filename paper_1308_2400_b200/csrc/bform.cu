@@ -6,7 +6,12 @@
 // rep is uniform along an output row, which is Case B verbatim
 // (kernels.hpp:142-165: rep = X[i,k], bases Y[k,:]); Case A is run through the
 // same kernel on transposed operands (afmm_case_a(X,Y) = afmm_case_b(Y^T,X^T)^T,
-// same per-element add sequence).
+// same per-element add sequence). "A-form" (k_aform, below) is
+// Case A in its own orientation, base uniform per warp, for sparse X.
+//
+// Contents: k_bform (the product kernel, three tile shapes), k_bform_tm
+// (opt-in TMEM-fed variant), k_aform (A-form), k_bform_mr (opt-in dense-rep
+// multi-row variant), and their launchers.
 //
 // k_bform (one CTA = CW consumer warps, each owning one output row, + 1 TMA
 // producer warp):

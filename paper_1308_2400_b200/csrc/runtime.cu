@@ -1,10 +1,12 @@
 // runtime.cu -- host runtime behind the C ABI (include/afmm_b200.h).
 //
 // Owns contexts (device + stream + grow-only workspace), builds the TMA
-// tensor maps, sequences prepass -> repeated-addition kernel -> epilogue on
-// one stream, and maps device-side validation results to the reference's
-// error contract (kernels.hpp:15-43, matrix.hpp:25-36, 54-57). No compute
-// happens on the host and there is no CPU fallback.
+// tensor maps, sequences prepass -> repeated-addition kernel(s) -> epilogue on
+// one stream, chooses the Case A form (B-form / A-form / row split) from the
+// prepass statistics, and maps device-side validation results to the
+// reference's error contract (kernels.hpp:15-43, matrix.hpp:25-36, 54-57). No
+// compute happens on the host (the host only sorts per-row counts for the
+// Case A split) and there is no CPU fallback.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -40,8 +42,10 @@ constexpr int kVariantTmem = 7;  // bases served from tensor memory (bform.cu)
 constexpr int kVariantAForm = 8; // Case A with the base uniform per warp (k_aform, bform.cu)
 constexpr int kVariantHybrid = 9; // Case A rows split between A-form and B-form (tests)
 
-// AFMM_BFORM=wide|ring|small|mr forces one repeated-addition kernel (all are
-// bit-identical; tests/test_gpu_parity.py runs each). Default: auto.
+// AFMM_BFORM=wide|ring|small|mr|tmem|aform|hybrid forces one repeated-addition
+// kernel or Case A form (all are bit-identical; tests/test_gpu_parity.py runs
+// each). Default: auto (tile shape from the problem size, Case A form from the
+// prepass statistics).
 int variant_from_env() {
   const char* v = std::getenv("AFMM_BFORM");
   if (v && std::strcmp(v, "ring") == 0) return kVariantRing;
