@@ -102,6 +102,37 @@ def test_rep_too_large_is_reported(cuda):
         afmm.afmm_case_a(np.eye(2), y)
 
 
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_errors_on_the_case_a_statistics_path(cuda, dt):
+    """n >= 1024 Case A reads prepass statistics to choose its kernel; invalid
+    inputs still raise the reference's error for the first offender in
+    row-major order (kernels.hpp:25-43) and leave the output untouched."""
+    from paper_1308_2400_b200.gen import make_inputs
+
+    afmm = _api()
+    lhs, rhs = make_inputs("cfg3", seed=2, n=1100, d1=0.1, mu=4)
+    lhs, rhs = lhs.astype(dt), rhs.astype(dt)
+    bad = rhs.copy()
+    bad[700, 3] = 2.5
+    bad[900, 1] = 0.25
+    out = np.full_like(lhs, 7.0)
+    with pytest.raises(afmm.DomainError, match=r"afmm_case_a: rhs\[700\]\[3\] = 2.500000 is not "
+                                               r"integer-valued"):
+        afmm.afmm_case_a(lhs, bad, out=out)
+    assert np.all(out == 7.0)
+    nf = lhs.copy()
+    nf[5, 6] = np.nan
+    with pytest.raises(afmm.DomainError, match="non-finite"):
+        afmm.afmm_case_a(nf, rhs)
+    big = rhs.copy()
+    big[10, 10] = 3.0e9
+    with pytest.raises(afmm.UnsupportedError, match=r"rhs\[10\]\[10\]"):
+        afmm.afmm_case_a(lhs, big)
+    # and a valid call on the same context afterwards is exact
+    res = afmm.afmm_case_a(lhs, rhs)
+    assert res.counts.multiplications == 0
+
+
 @pytest.mark.parametrize("name,n,kw", [
     ("cfg1", 256, {}),
     ("cfg2", 1024, {}),
