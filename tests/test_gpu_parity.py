@@ -1,3 +1,4 @@
+import os
 """Parity of the sm_100a product (through the C ABI) with the reference.
 
 Order-preserving mode must be bit-identical to the reference / its oracle:
@@ -259,6 +260,30 @@ def test_full_size_row_sample_bit_exact(cuda, oracle, name, kw):
         zr, _ = oracle.product_mt(cfg.case, lhs, rhs, r, r + 1, 1)
         assert _bits_equal(z[r:r + 1], zr), (name, r)
     ctx.close()
+
+
+@pytest.mark.parametrize("d1,mu", [(0.1, 1), (0.1, 4), (0.5, 1)])
+def test_full_size_cfg3_every_row(cuda, oracle, d1, mu):
+    """BASELINE cfg3 at its full n = 4096 (fp32), every row bit-exact against the
+    multithreaded oracle: the A-form at d1 = 0.1, the B-form at d1 = 0.5."""
+    import torch
+
+    from paper_1308_2400_b200.gen import make_inputs
+
+    afmm = _api()
+    lhs, rhs = make_inputs("cfg3", seed=0, d1=d1, mu=mu)
+    n = lhs.shape[0]
+    ctx = afmm.DeviceContext(0)
+    L = torch.from_numpy(lhs).cuda()
+    R = torch.from_numpy(rhs).cuda()
+    O = torch.empty_like(L)
+    counts = ctx.product("a", L, R, O)
+    form = ctx.last_form()
+    ctx.close()
+    z, c = oracle.product_mt("a", lhs, rhs, 0, n, os.cpu_count() or 1)
+    assert (counts.additions, 0, counts.zero_skips) == c
+    assert _bits_equal(O.cpu().numpy(), z), (d1, mu, form)
+    assert form == ("aform" if d1 < 0.2 else "bform")
 
 
 @pytest.mark.parametrize("d1,mu,dt,form", [(0.1, 1, np.float32, "aform"),
