@@ -1,4 +1,3 @@
-import os
 """Parity of the sm_100a product (through the C ABI) with the reference.
 
 Order-preserving mode must be bit-identical to the reference / its oracle:
@@ -8,6 +7,8 @@ Order-preserving mode must be bit-identical to the reference / its oracle:
   * BASELINE.json's five input distributions at reduced n against the oracle,
     and at full size through row samples + closed-form counts.
 """
+import os
+
 import numpy as np
 import pytest
 
