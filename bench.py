@@ -135,8 +135,18 @@ class CpuBaseline:
 
         self.case = case
         self.n = lhs.shape[0]
-        self.threads = max(1, min(threads, self.n))
         self.kind = "reference" if reference_available() else "port"
+        if self.kind == "reference":
+            # each concurrent reference call holds two n x n fp64 matrices (its
+            # masked lhs and the product); stay within half the available RAM
+            try:
+                avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+            except (ValueError, OSError):
+                avail = 0
+            per_call = 2 * 8 * self.n * self.n
+            if avail > 0:
+                threads = min(threads, max(1, int(0.5 * avail // per_call)))
+        self.threads = max(1, min(threads, self.n))
         if self.kind == "reference":
             self.ref = Reference()
             self.lhs = np.ascontiguousarray(lhs, dtype=np.float64)
