@@ -4,7 +4,7 @@ Dense Y (no zero bases) and a constant rep r isolate the repeated-addition
 kernel's instruction efficiency from the structural zero-base waste:
 effective adds/s / peak should approach 1 for large r.
 
-  AFMM_BFORM=dyn|ring|l1 python tools/sweep.py [n]
+  [AFMM_BFORM=wide|ring|small|tmem|mr] [AFMM_LIB=...] python tools/sweep.py [n]
 """
 import os
 import sys
@@ -24,7 +24,7 @@ rng = np.random.default_rng(0)
 Y = torch.from_numpy(rng.standard_normal((n, n), dtype=np.float32)).cuda()
 Y[Y == 0] = 1.0
 O = torch.empty_like(Y)
-print(f"variant={os.environ.get('AFMM_BFORM', 'dyn')} n={n} peak={peak:.4e} @ {mhz:.0f} MHz")
+print(f"variant={os.environ.get('AFMM_BFORM', 'auto')} n={n} peak={peak:.4e} @ {mhz:.0f} MHz")
 for r in (1, 2, 4, 8, 16, 32):
     X = torch.full((n, n), float(r), dtype=torch.float32, device="cuda")
     for _ in range(2):
