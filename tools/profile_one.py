@@ -19,6 +19,7 @@ p.add_argument("--d1", type=float, default=1.0)
 p.add_argument("--mu", type=int, default=16)
 p.add_argument("--n", type=int, default=None)
 p.add_argument("--reps", type=int, default=1)
+p.add_argument("--mode", default="order-preserving", choices=["order-preserving", "fast"])
 a = p.parse_args()
 cfg = CONFIGS[a.config]
 lhs, rhs = make_inputs(a.config, seed=0, n=a.n, d1=a.d1, mu=a.mu)
@@ -28,7 +29,7 @@ O = torch.empty_like(L)
 ctx = afmm.DeviceContext(0)
 ctx.enable_timing(True)
 for _ in range(a.reps):
-    c = ctx.product(cfg.case, L, R, O)
+    c = ctx.product(cfg.case, L, R, O, mode=a.mode)
     print(a.config, c, "kernel", ctx.last_form(), "phases ms (prepass, kernel, epilogue):",
           ctx.last_timing(), flush=True)
 ctx.close()
