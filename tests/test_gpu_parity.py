@@ -479,3 +479,36 @@ def test_randomized_shapes_and_distributions(cuda, oracle, seed, monkeypatch):
         assert (counts.additions, 0, counts.zero_skips) == c, what
         assert _bits_equal(O.cpu().numpy(), z), what
         ctx.close()
+
+
+def test_concurrent_host_calls_are_serialised_and_exact(cuda, oracle):
+    """SURVEY §8b threading: the C ABI is safe to call concurrently on distinct
+    inputs (the default context serialises per device); every call returns its
+    own bit-exact product and counts."""
+    import threading
+
+    from paper_1308_2400_b200.gen import make_inputs
+
+    afmm = _api()
+    jobs = [("cfg2", "b", 200 + 13 * i, i) for i in range(4)] + \
+           [("cfg1", "a", 150 + 7 * i, i) for i in range(4)]
+    results = {}
+
+    def work(j):
+        name, case, n, seed = j
+        lhs, rhs = make_inputs(name, seed=seed, n=n)
+        fn = afmm.afmm_case_a if case == "a" else afmm.afmm_case_b
+        for _ in range(3):
+            res = fn(lhs, rhs)
+        results[j] = (lhs, rhs, res)
+
+    threads = [threading.Thread(target=work, args=(j,)) for j in jobs]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert len(results) == len(jobs)
+    for (name, case, n, seed), (lhs, rhs, res) in results.items():
+        z, c, _ = oracle.product(case, lhs, rhs)
+        assert (res.counts.additions, 0, res.counts.zero_skips) == c
+        assert _bits_equal(res.product, z), (name, n)
