@@ -725,9 +725,24 @@ afmm_status host_product(int which, const T* lhs, uint64_t n_lhs, const T* rhs, 
   CK(cudaSetDevice(c->device), "afmm: cudaSetDevice");
   const uint64_t n = n_lhs, ld = round_up(n, 32);
   const size_t mat = n * ld * sizeof(T);
+  const int mode = opt ? opt->mode : AFMM_MODE_ORDER_PRESERVING;
+  // Zero-copy result: when `out` is page-locked host memory (mapped into the
+  // device address space) and the only kernel writing Z is k_bform (Case B,
+  // order-preserving), the kernel stores Z rows straight into `out` over PCIe
+  // as its CTAs finish, so the 1 GiB D2H of cfg5 overlaps the compute instead
+  // of following it. k_bform returns before writing when validation failed,
+  // so `out` stays untouched on error, as with the staged copy.
+  T* zdev = nullptr;
+  if (which == AFMM_CASE_B && mode == AFMM_MODE_ORDER_PRESERVING) {
+    cudaPointerAttributes attr{};
+    if (cudaPointerGetAttributes(&attr, out) == cudaSuccess && attr.type == cudaMemoryTypeHost &&
+        attr.devicePointer)
+      zdev = static_cast<T*>(attr.devicePointer);
+    cudaGetLastError();  // a pageable pointer is not an error here
+  }
   CK(c->hx.ensure(mat), "afmm: device allocation");
   CK(c->hy.ensure(mat), "afmm: device allocation");
-  CK(c->hz.ensure(mat), "afmm: device allocation");
+  if (!zdev) CK(c->hz.ensure(mat), "afmm: device allocation");
   cudaStream_t s = c->stream;
   CK(cudaMemcpy2DAsync(c->hx.p, ld * sizeof(T), lhs, n * sizeof(T), n * sizeof(T), n,
                        cudaMemcpyHostToDevice, s),
@@ -735,11 +750,12 @@ afmm_status host_product(int which, const T* lhs, uint64_t n_lhs, const T* rhs, 
   CK(cudaMemcpy2DAsync(c->hy.p, ld * sizeof(T), rhs, n * sizeof(T), n * sizeof(T), n,
                        cudaMemcpyHostToDevice, s),
      "afmm: H2D");
-  st = enqueue_product<T>(c, which, c->hx.as<T>(), c->hy.as<T>(), n, ld, c->hz.as<T>(), ld, 0, n,
-                          opt ? opt->mode : AFMM_MODE_ORDER_PRESERVING, err);
+  st = enqueue_product<T>(c, which, c->hx.as<T>(), c->hy.as<T>(), n, ld,
+                          zdev ? zdev : c->hz.as<T>(), zdev ? n : ld, 0, n, mode, err);
   if (st != AFMM_OK) return st;
   st = finish_locked(c, counts, err);
   if (st != AFMM_OK) return st;
+  if (zdev) return AFMM_OK;
   CK(cudaMemcpy2DAsync(out, n * sizeof(T), c->hz.p, ld * sizeof(T), n * sizeof(T), n,
                        cudaMemcpyDeviceToHost, s),
      "afmm: D2H");

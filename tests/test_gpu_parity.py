@@ -512,3 +512,30 @@ def test_concurrent_host_calls_are_serialised_and_exact(cuda, oracle):
         z, c, _ = oracle.product(case, lhs, rhs)
         assert (res.counts.additions, 0, res.counts.zero_skips) == c
         assert _bits_equal(res.product, z), (name, n)
+
+
+@pytest.mark.parametrize("dt,n", [(np.float32, 1024), (np.float32, 1030), (np.float64, 515)])
+def test_host_api_pinned_output_zero_copy(cuda, oracle, dt, n):
+    """Case B through the C ABI into page-locked host memory: k_bform writes Z
+    straight into `out` (no staging copy). Bit-exact, and `out` untouched when
+    validation fails."""
+    import torch
+
+    from paper_1308_2400_b200.gen import make_inputs
+
+    afmm = _api()
+    lhs, rhs = make_inputs("cfg5", seed=3, n=n)
+    lhs, rhs = lhs.astype(dt), rhs.astype(dt)
+    pinned = torch.full((n, n), 7.0, dtype=torch.float32 if dt == np.float32 else torch.float64)
+    pinned = pinned.pin_memory()
+    out = pinned.numpy()
+    res = afmm.afmm_case_b(lhs, rhs, out=out)
+    z, c, _ = oracle.product("b", lhs, rhs)
+    assert (res.counts.additions, 0, res.counts.zero_skips) == c
+    assert _bits_equal(out, z)
+    out[:] = 7.0
+    bad = lhs.copy()
+    bad[n // 2, 3] = 1.5
+    with pytest.raises(afmm.DomainError, match="is not integer-valued"):
+        afmm.afmm_case_b(bad, rhs, out=out)
+    assert np.all(out == 7.0)
