@@ -50,6 +50,8 @@ def parse_args():
     p.add_argument("--d1", type=float, default=1.0, help="cfg3 sweep point")
     p.add_argument("--mu", type=int, default=16, help="cfg3 sweep point")
     p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--size", dest="n", type=int, default=None,
+                   help="reduced problem size (tests only; the config's n by default)")
     p.add_argument("--mode", default="order-preserving", choices=["order-preserving", "fast"],
                    help="order-preserving = bit-exact with the reference (default); fast = "
                         "reassociated split-k within 1e-12/1e-5")
@@ -197,7 +199,7 @@ def run_reference_arm(args, rank):
     from paper_1308_2400_b200.gen import CONFIGS, make_inputs
 
     cfg = CONFIGS[args.config]
-    lhs, rhs = make_inputs(args.config, seed=args.seed, d1=args.d1, mu=args.mu)
+    lhs, rhs = make_inputs(args.config, seed=args.seed, n=args.n, d1=args.d1, mu=args.mu)
     cpu = CpuBaseline(cfg.case, lhs, rhs, os.cpu_count() or 1)
     b = cpu.rows_for(args.cpu_seconds * 0.5)
     for _ in range(max(0, min(args.warmup, 1))):
@@ -226,11 +228,14 @@ def run_reference_arm(args, rank):
 
 
 def _config_dict(args, cfg):
-    d = {"workload": f"{cfg.name}: {cfg.description}", "case": cfg.case, "n": cfg.n,
+    n = args.n or cfg.n
+    d = {"workload": f"{cfg.name}: {cfg.description}"
+                     + ("" if n == cfg.n else f" [REDUCED to n={n}: test run, not the config]"),
+         "case": cfg.case, "n": n,
          "mode": "order-preserving (bit-exact)" if args.mode == "order-preserving"
          else "fast (reassociated split-k, tolerance 1e-12 f64 / 1e-5 f32)",
          "parallelism": f"row-partition x{args.gpus}",
-         "l2": "operands larger than L2" if cfg.n >= 4096 else "L2 flushed between steps"}
+         "l2": "operands larger than L2" if n >= 4096 else "L2 flushed between steps"}
     if cfg.name == "cfg3":
         d["d1"] = args.d1
         d["mu"] = args.mu
@@ -257,16 +262,26 @@ def main():
     from paper_1308_2400_b200.distributed import ShardedProduct, gather_rows
     from paper_1308_2400_b200.gen import CONFIGS, make_inputs
 
+    # AFMM_DIST_BACKEND=gloo + AFMM_SINGLE_DEVICE=1: functional test of the N > 1
+    # path with every rank on cuda:0 (tests/test_multirank_gpu.py); never a
+    # measurement. The bench proper is one process per GPU over NCCL.
+    backend = os.environ.get("AFMM_DIST_BACKEND", "nccl")
+    if os.environ.get("AFMM_SINGLE_DEVICE"):
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
         dist.barrier()
+    red_dev = "cpu" if backend != "nccl" else None
     cfg = CONFIGS[args.config]
     tdt = torch.float32 if cfg.dtype == "float32" else torch.float64
     es = 4 if cfg.dtype == "float32" else 8
 
-    lhs, rhs = make_inputs(args.config, seed=args.seed, d1=args.d1, mu=args.mu)
-    n = cfg.n
+    lhs, rhs = make_inputs(args.config, seed=args.seed, n=args.n, d1=args.d1, mu=args.mu)
+    n = lhs.shape[0]
     dev = torch.device("cuda", local)
     L = torch.from_numpy(lhs).to(dev)
     R = torch.from_numpy(rhs).to(dev)
@@ -315,7 +330,7 @@ def main():
     launches = afmm.kernel_launch_count() - launches0
     clocks = sampler.stop()
 
-    t = torch.tensor([total_ms, float(rank_adds)], dtype=torch.float64, device=dev)
+    t = torch.tensor([total_ms, float(rank_adds)], dtype=torch.float64, device=red_dev or dev)
     if world > 1:
         tmax = t.clone()
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
@@ -387,7 +402,7 @@ def main():
 def _e2e(args, afmm, dist, torch, world, rank, local, cfg, lhs, rhs, es, job_adds, sharded, L,
          R, Z):
     """Same metric with pinned host operands copied in and Z copied out every step."""
-    n = cfg.n
+    n = lhs.shape[0]
     hl = torch.from_numpy(lhs).pin_memory()
     hr = torch.from_numpy(rhs).pin_memory()
     hz = torch.empty((n, n), dtype=hl.dtype).pin_memory()
@@ -418,7 +433,8 @@ def _e2e(args, afmm, dist, torch, world, rank, local, cfg, lhs, rhs, es, job_add
     torch.cuda.synchronize()
     secs = (time.perf_counter() - t0) / reps
     if world > 1:
-        t = torch.tensor([secs], dtype=torch.float64, device="cuda")
+        on_cpu = os.environ.get("AFMM_DIST_BACKEND", "nccl") != "nccl"
+        t = torch.tensor([secs], dtype=torch.float64, device="cpu" if on_cpu else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         secs = float(t[0])
     return {"value": job_adds / secs, "unit": UNIT,

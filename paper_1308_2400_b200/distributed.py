@@ -19,6 +19,7 @@ from __future__ import annotations
 from typing import Optional
 
 import numpy as np
+import torch
 
 from .afmm import DeviceContext, OpCounts, partition_rows
 
@@ -28,18 +29,28 @@ def gather_rows(dist, z_full, slab, cuts, rank: int, world: int) -> None:
 
     `slab` is this rank's (cuts[rank+1]-cuts[rank]) x n block; `z_full` is the
     n x n result on rank 0 (ignored elsewhere)."""
-    ops = []
+    # gloo has no CUDA point-to-point: stage device slabs through host memory
+    # (the functional multi-rank test on one GPU; the bench uses NCCL)
+    staged = dist.get_backend() == "gloo" and getattr(z_full, "is_cuda", False)
+    ops, landing = [], []
     if rank == 0:
         for r in range(1, world):
             r0, r1 = int(cuts[r]), int(cuts[r + 1])
             if r1 > r0:
-                ops.append(dist.P2POp(dist.irecv, z_full[r0:r1], r))
+                dst = z_full[r0:r1]
+                if staged:
+                    buf = torch.empty(dst.shape, dtype=dst.dtype)
+                    landing.append((dst, buf))
+                    dst = buf
+                ops.append(dist.P2POp(dist.irecv, dst, r))
     else:
         if int(cuts[rank + 1]) > int(cuts[rank]):
-            ops.append(dist.P2POp(dist.isend, slab, 0))
+            ops.append(dist.P2POp(dist.isend, slab.cpu() if staged else slab, 0))
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
+    for dst, buf in landing:
+        dst.copy_(buf)
 
 
 class ShardedProduct:

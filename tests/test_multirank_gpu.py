@@ -1,0 +1,101 @@
+"""The N > 1 row-sharded path with the real GPU product, as a functional test.
+
+The pool gives one GPU per call, so both ranks run on cuda:0 and exchange
+through gloo (host-staged point-to-point); the bench proper is one process per
+GPU over NCCL. Nothing here is a measurement: it checks that the sharded GPU
+path (row work on the device -> equal-work cuts -> per-rank slab product ->
+gather into rank 0) is bit-identical to the single-process product, and that
+bench.py's multi-rank code path (torchrun launch, max-over-ranks timing, e2e,
+JSON line) runs end to end.
+"""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, name, n, out_path):
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1308_2400_b200 as afmm
+    from paper_1308_2400_b200.distributed import ShardedProduct
+    from paper_1308_2400_b200.gen import CONFIGS, make_inputs
+
+    torch.cuda.set_device(0)
+    lhs, rhs = make_inputs(name, seed=6, n=n)
+    L = torch.from_numpy(lhs).cuda()
+    R = torch.from_numpy(rhs).cuda()
+    Z = torch.full((n, n), float("nan"), dtype=L.dtype, device="cuda")
+    ctx = afmm.DeviceContext(0)
+    sp = ShardedProduct(ctx, dist, rank, world)
+    counts = sp.run(CONFIGS[name].case, L, R, Z, torch.empty_like(Z))
+    adds = torch.tensor([counts.additions], dtype=torch.float64)
+    dist.all_reduce(adds)
+    if rank == 0:
+        np.save(out_path, Z.cpu().numpy())
+        np.save(out_path + ".meta.npy", np.array([adds.item(), *sp.cuts], dtype=np.float64))
+    dist.barrier()
+    ctx.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,n", [("cfg5", 900), ("cfg4", 1100)])
+def test_two_ranks_on_one_gpu_match_single_process(cuda, tmp_path, name, n):
+    import torch
+    import torch.multiprocessing as mp
+
+    import paper_1308_2400_b200 as afmm
+    from paper_1308_2400_b200.gen import CONFIGS, expected_additions, make_inputs
+
+    out = str(tmp_path / "z.npy")
+    mp.start_processes(_worker, args=(2, _free_port(), name, n, out), nprocs=2, join=True,
+                       start_method="spawn")
+    z = np.load(out)
+    meta = np.load(out + ".meta.npy")
+    lhs, rhs = make_inputs(name, seed=6, n=n)
+    case = CONFIGS[name].case
+    ctx = afmm.DeviceContext(0)
+    L = torch.from_numpy(lhs).cuda()
+    R = torch.from_numpy(rhs).cuda()
+    O = torch.empty_like(L)
+    counts = ctx.product(case, L, R, O)
+    ctx.close()
+    assert np.array_equal(z.view(np.uint8), O.cpu().numpy().view(np.uint8))
+    assert int(meta[0]) == counts.additions == expected_additions(case, lhs, rhs)
+    cuts = meta[1:].astype(int)
+    assert cuts[0] == 0 and cuts[-1] == n and 0 < cuts[1] < n
+
+
+def test_bench_multi_rank_path_runs(cuda):
+    env = dict(os.environ, AFMM_DIST_BACKEND="gloo", AFMM_SINGLE_DEVICE="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "2", "--warmup", "3",
+           "--size", "1024", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert "REDUCED" in d["config"]["workload"]
+    assert d["gpu_launches"] > 0
