@@ -77,6 +77,15 @@ class ClockSampler(threading.Thread):
     def __init__(self, device: int, period: float = 0.1):
         super().__init__(daemon=True)
         self.device = device
+        # NVML enumerates by PCI bus, CUDA may not (CUDA_VISIBLE_DEVICES,
+        # CUDA_DEVICE_ORDER): identify the device by its PCI address
+        try:
+            import torch
+
+            pr = torch.cuda.get_device_properties(device)
+            self.pci = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        except Exception:
+            self.pci = None
         self.period = period
         self.samples = []
         self.reasons = set()
@@ -89,7 +98,14 @@ class ClockSampler(threading.Thread):
             import pynvml
 
             pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            h = None
+            if self.pci:
+                try:
+                    h = pynvml.nvmlDeviceGetHandleByPciBusId(self.pci.encode())
+                except Exception:
+                    h = None
+            if h is None:
+                h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
             self.ok = True
             while not self._halt.is_set():
@@ -117,7 +133,7 @@ class ClockSampler(threading.Thread):
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the oracle port on a row sample
+# CPU baseline: the reference's CPU path (unmodified kernels) on a row sample
 # ---------------------------------------------------------------------------
 
 class CpuBaseline:
