@@ -379,6 +379,7 @@ def main():
         "kernel_ms": kms,
         "step_share": kms / ms_per_step if world == 1 else None,
         "traffic": traffic,
+        "hbm_check": _hbm_check(traffic),
     }
 
     # ---- end to end through the reference-facing API ----
@@ -458,6 +459,21 @@ def _e2e(args, afmm, dist, torch, world, rank, local, cfg, lhs, rhs, es, job_add
             "ms_per_step": secs * 1e3, "steps": reps,
             "api": "afmm_case_%s_%s (C ABI, host buffers)" % (cfg.case, "f32" if es == 4 else "f64")
             if world == 1 else "per-rank H2D + row-sharded product + NCCL gather + D2H on rank 0"}
+
+
+def _hbm_check(traffic):
+    """The kernel's DRAM bandwidth (ncu bytes per launch / launch time) against the
+    driver-measured HBM copy bandwidth: shows the HBM roofline is not the bound."""
+    if not traffic:
+        return None
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peak = float(json.load(f)["hbm_gbs"])
+        src = "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, ValueError, KeyError):
+        peak, src = 7700.0, "B200 nominal (MEASURED_PEAKS.json absent)"
+    gbs = traffic["bytes_per_launch"] / traffic["kernel_time_s"] / 1e9
+    return {"dram_GBps": gbs, "hbm_peak_GBps": peak, "frac": gbs / peak, "peak_source": src}
 
 
 def _ncu_traffic(config):
