@@ -64,6 +64,9 @@ constexpr int REP_UNROLL = AFMM_EXP_REP_UNROLL;
 #ifndef AFMM_EXP_WIDE_MINB
 #define AFMM_EXP_WIDE_MINB 2
 #endif
+#ifndef AFMM_EXP_WIDE_G
+#define AFMM_EXP_WIDE_G 8
+#endif
 #ifndef AFMM_EXP_WIDE_CW
 #define AFMM_EXP_WIDE_CW kWideRows
 #endif
@@ -1228,7 +1231,7 @@ cudaError_t launch_bform(int shape, const CUtensorMap* tmap, const int2* lists, 
     // rep 16), but 2x finer CTAs, so far less wave-quantisation tail (cfg3
     // n=4096: 87% vs 82%). 16 consumers + producer (17 warps) would cap the
     // registers at 96 and spill.
-    return launch_ring<T, 8, AFMM_EXP_WIDE_CW, AFMM_EXP_WIDE_STAGES, AFMM_EXP_WIDE_MINB>(tmap, lists, cap, counts, nrows, col0, ncols, nk,
+    return launch_ring<T, AFMM_EXP_WIDE_G, AFMM_EXP_WIDE_CW, AFMM_EXP_WIDE_STAGES, AFMM_EXP_WIDE_MINB>(tmap, lists, cap, counts, nrows, col0, ncols, nk,
                                               splits, slice_stride, out, ld_out, st, s);
   if (shape == kShapeTmem)
     // 1024 fp32 / 512 fp64 columns x 16 rows, bases from tensor memory, 1 CTA per SM
