@@ -371,7 +371,9 @@ def main():
                         "A-form): no tensor cores (they would multiply), far right of the HBM "
                         "ridge",
         "kernel": {"aform": "k_aform", "split": "k_aform+k_bform"}.get(form, "k_bform"),
-        "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tadd/s",
+        "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
+        "unit_note": "FLOP = one FP add (fp32 FADD2 lanes / fp64 DADD); the kernel does no "
+                     "multiplications, so FP-add/s is its FLOP/s",
         "frac": achieved / peak,
         "peak_source": f"measured in-process by afmm_fp_add_peak ({'FADD2' if es == 4 else 'DADD'}"
                        f" chains) at {peak_mhz:.0f} MHz",
