@@ -539,3 +539,26 @@ def test_host_api_pinned_output_zero_copy(cuda, oracle, dt, n):
     with pytest.raises(afmm.DomainError, match="is not integer-valued"):
         afmm.afmm_case_b(bad, rhs, out=out)
     assert np.all(out == 7.0)
+
+
+@pytest.mark.parametrize("name,n", [("cfg2", 3000), ("cfg1", 2049)])
+def test_fp64_configs_at_larger_n_every_row(cuda, oracle, name, n):
+    """The fp64 configurations (cfg1 Case A, cfg2 Case B) at several times
+    their BASELINE size, every row bit-exact against the multithreaded oracle
+    (wide fp64 tiles, the Case A statistics path)."""
+    import torch
+
+    from paper_1308_2400_b200.gen import CONFIGS, make_inputs
+
+    afmm = _api()
+    lhs, rhs = make_inputs(name, seed=12, n=n)
+    case = CONFIGS[name].case
+    ctx = afmm.DeviceContext(0)
+    L = torch.from_numpy(lhs).cuda()
+    R = torch.from_numpy(rhs).cuda()
+    O = torch.empty_like(L)
+    counts = ctx.product(case, L, R, O)
+    ctx.close()
+    z, c = oracle.product_mt(case, lhs, rhs, 0, n, os.cpu_count() or 1)
+    assert (counts.additions, 0, counts.zero_skips) == c
+    assert _bits_equal(O.cpu().numpy(), z)
