@@ -30,11 +30,12 @@ void launch_rows(const T* x, uint64_t ld, uint32_t n, int which_case, const uint
 template <class T>
 void launch_transpose_compact(const T* y, uint64_t ld, uint32_t n, int2* lists, uint64_t cap,
                               uint32_t* counts, cudaStream_t s);
-// out[oc][r] = in[ir][c] with optional row maps ir = in_rows[r], oc = out_rows[c].
+// out[oc][r] = in[ir][c] with optional row maps ir = in_rows[r], oc = out_rows[c];
+// with a status, nothing is written after a failed validation.
 template <class T>
 void launch_transpose(const T* in, uint64_t ld_in, uint32_t rows, uint32_t cols, T* out,
                       uint64_t ld_out, cudaStream_t s, const uint32_t* in_rows = nullptr,
-                      const uint32_t* out_rows = nullptr);
+                      const uint32_t* out_rows = nullptr, const DevStatus* st = nullptr);
 
 // ---- A-form (Case A, base uniform per warp; aform in bform.cu) ----
 // fp16 rep counts of Y (|rep| <= 2048) + per (k, tile) max |rep| | neg flag.
@@ -88,7 +89,8 @@ cudaError_t launch_bform(int shape, const CUtensorMap* tmap, const int2* lists, 
 // out[r*ld_out + c] = sum over z (ascending) of part[z*stride + r*ld_part + c]
 template <class T>
 void launch_reduce_slices(const T* part, uint64_t stride, uint64_t ld_part, uint32_t splits,
-                          uint32_t rows, uint32_t cols, T* out, uint64_t ld_out, cudaStream_t s);
+                          uint32_t rows, uint32_t cols, T* out, uint64_t ld_out,
+                          const DevStatus* st, cudaStream_t s);
 
 // Multi-row dense-rep kernel: rmap = int32 reps R'[k][row] (row inner),
 // box bform_mr_rows() x bform_kb().

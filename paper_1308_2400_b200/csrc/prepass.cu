@@ -400,7 +400,10 @@ template <class T>
 __global__ void k_transpose(const T* __restrict__ in, uint64_t ld_in, uint32_t rows,
                             uint32_t cols, T* __restrict__ out, uint64_t ld_out,
                             const uint32_t* __restrict__ in_rows,
-                            const uint32_t* __restrict__ out_rows) {
+                            const uint32_t* __restrict__ out_rows, const DevStatus* st) {
+  // the result transpose writes Z only for a valid product (out untouched on
+  // a validation error, like the kernels that write Z directly)
+  if (st && status_failed(st)) return;
   __shared__ T tile[32][33];
   const uint32_t c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
   for (uint32_t dy = threadIdx.y; dy < 32; dy += blockDim.y) {
@@ -426,7 +429,8 @@ __global__ void k_transpose(const T* __restrict__ in, uint64_t ld_in, uint32_t r
 template <class T>
 __global__ void k_reduce_slices(const T* __restrict__ part, uint64_t stride, uint64_t ld_part,
                                 uint32_t splits, uint32_t rows, uint32_t cols,
-                                T* __restrict__ out, uint64_t ld_out) {
+                                T* __restrict__ out, uint64_t ld_out, const DevStatus* st) {
+  if (status_failed(st)) return;
   const uint64_t total = (uint64_t)rows * cols;
   for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (uint64_t)gridDim.x * blockDim.x) {
@@ -501,10 +505,10 @@ void launch_transpose_compact(const T* y, uint64_t ld, uint32_t n, int2* lists, 
 template <class T>
 void launch_transpose(const T* in, uint64_t ld_in, uint32_t rows, uint32_t cols, T* out,
                       uint64_t ld_out, cudaStream_t s, const uint32_t* in_rows,
-                      const uint32_t* out_rows) {
+                      const uint32_t* out_rows, const DevStatus* st) {
   dim3 grid((cols + 31) / 32, (rows + 31) / 32);
   k_transpose<T><<<grid, dim3(32, 8), 0, s>>>(in, ld_in, rows, cols, out, ld_out, in_rows,
-                                               out_rows);
+                                               out_rows, st);
   note_launch();
 }
 
@@ -518,12 +522,13 @@ void launch_reps_dense(const T* src, uint64_t ld_src, uint32_t rows, uint32_t co
 
 template <class T>
 void launch_reduce_slices(const T* part, uint64_t stride, uint64_t ld_part, uint32_t splits,
-                          uint32_t rows, uint32_t cols, T* out, uint64_t ld_out, cudaStream_t s) {
+                          uint32_t rows, uint32_t cols, T* out, uint64_t ld_out,
+                          const DevStatus* st, cudaStream_t s) {
   uint64_t blocks = ((uint64_t)rows * cols + 255) / 256;
   if (blocks > 148ull * 16) blocks = 148ull * 16;
   if (blocks < 1) blocks = 1;
   k_reduce_slices<T><<<(unsigned)blocks, 256, 0, s>>>(part, stride, ld_part, splits, rows, cols,
-                                                      out, ld_out);
+                                                      out, ld_out, st);
   note_launch();
 }
 
@@ -542,11 +547,13 @@ void launch_reduce_slices(const T* part, uint64_t stride, uint64_t ld_part, uint
   template void launch_transpose_compact<T>(const T*, uint64_t, uint32_t, int2*, uint64_t,     \
                                             uint32_t*, cudaStream_t);                          \
   template void launch_transpose<T>(const T*, uint64_t, uint32_t, uint32_t, T*, uint64_t,      \
-                                    cudaStream_t, const uint32_t*, const uint32_t*);           \
+                                    cudaStream_t, const uint32_t*, const uint32_t*,            \
+                                    const DevStatus*);                                         \
   template void launch_reps_dense<T>(const T*, uint64_t, uint32_t, uint32_t, int, int32_t*,    \
                                      uint64_t, cudaStream_t);                                  \
   template void launch_reduce_slices<T>(const T*, uint64_t, uint64_t, uint32_t, uint32_t,     \
-                                        uint32_t, T*, uint64_t, cudaStream_t);
+                                        uint32_t, T*, uint64_t, const DevStatus*,             \
+                                        cudaStream_t);
 
 INSTANTIATE(float)
 INSTANTIATE(double)

@@ -63,9 +63,11 @@ inline uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  uint64_t* gen = nullptr;  // the owning context's buffer generation (bumped on reallocation)
   // grow-only; contents are not preserved
   cudaError_t ensure(size_t want) {
     if (want <= bytes) return cudaSuccess;
+    if (gen) ++*gen;  // captured graphs hold the old addresses
     if (p) {
       cudaFree(p);  // implicit device sync
       p = nullptr;
@@ -186,9 +188,41 @@ struct afmm_context {
   void mark(int i) {
     if (timing) cudaEventRecord(ev[i], stream);
   }
+  // CUDA-graph replay of repeated identical device-API calls (graph_call)
+  struct GraphKey {
+    int which = -1, dtype = 0, mode = 0, variant = 0, timing = 0;
+    const void* lhs = nullptr;
+    const void* rhs = nullptr;
+    void* out = nullptr;
+    uint64_t n = 0, ld = 0, ld_out = 0, r0 = 0, r1 = 0;
+    cudaStream_t user = nullptr;
+    bool operator==(const GraphKey& o) const {
+      return which == o.which && dtype == o.dtype && mode == o.mode && variant == o.variant &&
+             timing == o.timing && lhs == o.lhs && rhs == o.rhs && out == o.out && n == o.n &&
+             ld == o.ld && ld_out == o.ld_out && r0 == o.r0 && r1 == o.r1 && user == o.user;
+    }
+  };
+  struct GraphEntry {
+    GraphKey key;
+    cudaGraphExec_t exec = nullptr;
+    uint64_t gen = 0, launches = 0;
+    int last_form = 0;
+  };
+  uint64_t buf_gen = 0;
+  bool graphs = true;  // AFMM_GRAPHS=0 disables
+  GraphKey seen;       // the previous call: the second identical call is captured
+  std::vector<GraphEntry> graph_cache;
+  cudaStream_t gstream = nullptr;  // capturable stream (the legacy default stream is not)
+  cudaEvent_t join_in = nullptr, join_out = nullptr;
 };
 
 namespace {
+
+std::vector<DevBuf*> all_bufs(afmm_context* c) {
+  return {&c->status, &c->vec_k, &c->work,  &c->lists,  &c->counts, &c->base_copy, &c->xt,
+          &c->zt,     &c->part,  &c->reps,  &c->cnt16,  &c->rmax,   &c->fstats,    &c->alists,
+          &c->acounts, &c->ridx, &c->hx,    &c->hy,     &c->hz};
+}
 
 void set_error(afmm_error* err, int kind, int operand, uint64_t row, uint64_t col, double value,
                const char* msg) {
@@ -477,7 +511,7 @@ afmm_status launch_compute(afmm_context* c, int mode, const T* base, uint64_t kb
                                  &splits, stride, c->part.as<T>(), ldp, st, c->stream),
        "bform");
     afmm_dev::launch_reduce_slices<T>(c->part.as<T>(), stride, ldp, splits, nrows,
-                                      (uint32_t)ncols, out, ld_out, c->stream);
+                                      (uint32_t)ncols, out, ld_out, st, c->stream);
     return AFMM_OK;
   }
   uint32_t one = 1;
@@ -647,7 +681,7 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
         if (cs != AFMM_OK) return cs;
         c->mark(2);
         afmm_dev::launch_transpose<T>(c->zt.as<T>(), lds, n32, (uint32_t)m_b, out, ld_out, s,
-                                      nullptr, bidx);
+                                      nullptr, bidx, st);
       } else {
         c->mark(2);
       }
@@ -678,6 +712,130 @@ afmm_status finish_locked(afmm_context* c, afmm_op_counts* counts, afmm_error* e
   cudaError_t e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return cuda_fail(err, e, "afmm: device execution");
   return decode_status(c, counts, err);
+}
+
+// Device-API calls that repeat with the same pointers, sizes and options (a
+// serving loop, a benchmark step) replay a CUDA graph of the whole pipeline:
+// the first call runs normally, the second identical call is captured (on the
+// context's own capturable stream, joined to the caller's stream by events --
+// the legacy default stream cannot be captured), later ones replay it, which
+// removes the host enqueue of ~10 launches per call and the GPU gaps between
+// them (small problems are launch bound). Calls with a host wait in the
+// pipeline (the Case A statistics for n >= 1024) are never captured; a
+// workspace reallocation invalidates the cache; a failed capture falls back to
+// the direct path for good (AFMM_GRAPHS=0 disables the mechanism).
+template <class T>
+afmm_status graph_call(afmm_context* c, int which, const T* lhs, const T* rhs, uint64_t n,
+                       uint64_t ld, T* out, uint64_t ld_out, uint64_t r0, uint64_t r1, int mode,
+                       afmm_error* err) {
+  auto direct = [&]() {
+    return enqueue_product<T>(c, which, lhs, rhs, n, ld, out, ld_out, r0, r1, mode, err);
+  };
+  const bool host_wait = which == AFMM_CASE_A && r1 > r0 &&
+                         (c->variant == kVariantAForm || c->variant == kVariantHybrid ||
+                          (c->variant == kVariantAuto && n >= 1024));
+  if (!c->graphs || host_wait) return direct();
+  afmm_context::GraphKey key;
+  key.which = which;
+  key.dtype = sizeof(T) == 8 ? AFMM_F64 : AFMM_F32;
+  key.mode = mode;
+  key.variant = c->variant;
+  key.timing = c->timing ? 1 : 0;
+  key.lhs = lhs;
+  key.rhs = rhs;
+  key.out = out;
+  key.n = n;
+  key.ld = ld;
+  key.ld_out = ld_out;
+  key.r0 = r0;
+  key.r1 = r1;
+  key.user = c->stream;
+  auto& cache = c->graph_cache;
+  for (size_t i = 0; i < cache.size();) {  // entries captured before a reallocation
+    if (cache[i].gen != c->buf_gen) {
+      cudaGraphExecDestroy(cache[i].exec);
+      cache.erase(cache.begin() + i);
+    } else {
+      ++i;
+    }
+  }
+  afmm_context::GraphEntry* hit = nullptr;
+  for (auto& ge : cache)
+    if (ge.key == key) hit = &ge;
+  const cudaStream_t user = c->stream;
+  auto join_and_launch = [&](const afmm_context::GraphEntry& ge) -> cudaError_t {
+    cudaError_t e = cudaEventRecord(c->join_in, user);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->gstream, c->join_in, 0);
+    if (e == cudaSuccess) e = cudaGraphLaunch(ge.exec, c->gstream);
+    if (e == cudaSuccess) e = cudaEventRecord(c->join_out, c->gstream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(user, c->join_out, 0);
+    return e;
+  };
+  if (hit) {
+    CK(join_and_launch(*hit), "afmm: graph launch");
+    for (uint64_t i = 0; i < hit->launches; ++i) afmm_dev::note_launch();
+    c->timed_last = c->timing;
+    c->last_case = which;
+    c->last_dtype = key.dtype;
+    c->last_lhs = lhs;
+    c->last_rhs = rhs;
+    c->last_n = n;
+    c->last_ld = ld;
+    c->last_form = hit->last_form;
+    c->pending = true;
+    return AFMM_OK;
+  }
+  if (!(key == c->seen)) {
+    c->seen = key;
+    return direct();
+  }
+  // second identical call: capture it
+  if (!c->gstream) {
+    if (cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->join_in, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->join_out, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      c->graphs = false;
+      return direct();
+    }
+  }
+  const uint64_t launches0 = afmm_dev::g_launches.load();
+  c->stream = c->gstream;
+  if (cudaStreamBeginCapture(c->gstream, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+    cudaGetLastError();
+    c->stream = user;
+    c->graphs = false;
+    return direct();
+  }
+  const afmm_status st = direct();
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(c->gstream, &graph);
+  c->stream = user;
+  cudaGraphExec_t exec = nullptr;
+  const bool ok = st == AFMM_OK && ec == cudaSuccess && graph &&
+                  cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+  if (graph) cudaGraphDestroy(graph);
+  if (!ok) {  // fall back to direct calls for the life of the context
+    cudaGetLastError();
+    if (exec) cudaGraphExecDestroy(exec);
+    c->graphs = false;
+    c->pending = false;
+    if (st != AFMM_OK) return st;
+    return direct();
+  }
+  afmm_context::GraphEntry ge;
+  ge.key = key;
+  ge.exec = exec;
+  ge.gen = c->buf_gen;
+  ge.launches = afmm_dev::g_launches.load() - launches0;
+  ge.last_form = c->last_form;
+  if (cache.size() >= 8) {
+    cudaGraphExecDestroy(cache.front().exec);
+    cache.erase(cache.begin());
+  }
+  cache.push_back(ge);
+  CK(join_and_launch(cache.back()), "afmm: graph launch");
+  return AFMM_OK;  // the captured call left the host state of this product
 }
 
 std::mutex g_default_mu;
@@ -830,6 +988,11 @@ afmm_status afmm_context_create(int32_t device, afmm_context** ctx) {
   if (!c) return AFMM_ERR_OUT_OF_MEMORY;
   c->device = device;
   c->variant = variant_from_env();
+  {
+    const char* gv = std::getenv("AFMM_GRAPHS");
+    c->graphs = !(gv && std::strcmp(gv, "0") == 0);
+  }
+  for (DevBuf* b : all_bufs(c)) b->gen = &c->buf_gen;
   int prev = 0;
   cudaGetDevice(&prev);
   if (cudaSetDevice(device) != cudaSuccess ||
@@ -853,10 +1016,13 @@ void afmm_context_destroy(afmm_context* c) {
     std::lock_guard<std::mutex> g(c->mu);
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    for (DevBuf* b : {&c->status, &c->vec_k, &c->work, &c->lists, &c->counts, &c->base_copy,
-                      &c->xt, &c->zt, &c->part, &c->reps, &c->cnt16, &c->rmax, &c->fstats,
-                      &c->alists, &c->acounts, &c->ridx, &c->hx, &c->hy, &c->hz})
-      b->release();
+    if (c->gstream) cudaStreamSynchronize(c->gstream);
+    for (auto& ge : c->graph_cache) cudaGraphExecDestroy(ge.exec);
+    c->graph_cache.clear();
+    if (c->gstream) cudaStreamDestroy(c->gstream);
+    if (c->join_in) cudaEventDestroy(c->join_in);
+    if (c->join_out) cudaEventDestroy(c->join_out);
+    for (DevBuf* b : all_bufs(c)) b->release();
     if (c->status_host) cudaFreeHost(c->status_host);
     if (c->fstats_host) cudaFreeHost(c->fstats_host);
     for (cudaEvent_t& e : c->ev)
@@ -899,14 +1065,13 @@ afmm_status afmm_product_device(afmm_context* c, int32_t which_case, int32_t dty
       (void)st;
     }
     if (dtype == AFMM_F64)
-      st = enqueue_product<double>(c, which_case, static_cast<const double*>(lhs),
-                                   static_cast<const double*>(rhs), n, ld,
-                                   static_cast<double*>(out), ld_out, row_begin, row_end, mode,
-                                   err);
+      st = graph_call<double>(c, which_case, static_cast<const double*>(lhs),
+                              static_cast<const double*>(rhs), n, ld, static_cast<double*>(out),
+                              ld_out, row_begin, row_end, mode, err);
     else
-      st = enqueue_product<float>(c, which_case, static_cast<const float*>(lhs),
-                                  static_cast<const float*>(rhs), n, ld, static_cast<float*>(out),
-                                  ld_out, row_begin, row_end, mode, err);
+      st = graph_call<float>(c, which_case, static_cast<const float*>(lhs),
+                             static_cast<const float*>(rhs), n, ld, static_cast<float*>(out),
+                             ld_out, row_begin, row_end, mode, err);
     if (st != AFMM_OK) return st;
     if (sync) return finish_locked(c, counts, err);
     return AFMM_OK;
