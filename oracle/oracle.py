@@ -155,6 +155,10 @@ class Reference:
         lib.ref_hold_matrix.restype = c_void_p
         lib.ref_hold_matrix.argtypes = [c_void_p, c_uint64, c_char_p, c_size_t]
         lib.ref_release_matrix.argtypes = [c_void_p]
+        lib.ref_run_plan_csv.restype = c_int
+        lib.ref_run_plan_csv.argtypes = [c_int, c_void_p, c_size_t, c_double, c_double, c_double,
+                                         c_uint64, c_uint64, c_uint64, c_char_p, c_size_t,
+                                         POINTER(c_size_t), c_char_p, c_size_t]
         lib.ref_case_rows.restype = c_int
         lib.ref_case_rows.argtypes = [c_int, c_void_p, c_uint64, c_uint64, c_uint64, c_void_p,
                                       c_void_p, POINTER(Counts), c_char_p, c_size_t]
@@ -176,6 +180,25 @@ class Reference:
         if rc != 0:
             return None, None, (self.STATUS[rc], msg.value.decode())
         return out, c.as_tuple(), None
+
+    def run_plan_csv(self, case: str, sizes, d1: float, d2: float, mu: float, reps: int,
+                     warmups: int, seed: int) -> str:
+        """The reference's run_plan + emit_csv (bench.hpp:120-154, report.hpp:27-39)."""
+        sz = np.ascontiguousarray(sizes, dtype=np.uint64)
+        cap = 1 << 16
+        while True:
+            buf = ctypes.create_string_buffer(cap)
+            need = c_size_t()
+            msg = ctypes.create_string_buffer(512)
+            rc = self.lib.ref_run_plan_csv(1 if case == "b" else 0, sz.ctypes.data, len(sz), d1,
+                                           d2, mu, reps, warmups, seed, buf, cap,
+                                           ctypes.byref(need), msg, 512)
+            if rc == -1:
+                cap = need.value
+                continue
+            if rc != 0:
+                raise RuntimeError(msg.value.decode())
+            return buf.value.decode()
 
     def rows_batch(self, case: str, lhs: np.ndarray, rhs: np.ndarray, blocks):
         """Run the unmodified afmm_case_{a,b} once per row block (r0, r1), all blocks

@@ -13,6 +13,7 @@
 #include <cstring>
 #include <exception>
 #include <random>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -22,6 +23,7 @@
 #include "afmm/kernels.hpp"
 #include "afmm/matrix.hpp"
 #include "afmm/random.hpp"
+#include "afmm/report.hpp"
 
 namespace {
 
@@ -151,6 +153,39 @@ void ref_make_factor_pair(int case_b, std::uint64_t n, double d1, double d2, dou
                                            n, d1, d2, mu_prime, seed);
   std::memcpy(lhs, pair.first.data().data(), n * n * sizeof(double));
   std::memcpy(rhs, pair.second.data().data(), n * n * sizeof(double));
+}
+
+// The reference's own benchmark flow: run_plan (bench.hpp:120-154) for an
+// afmm kernel id, rendered by emit_csv (report.hpp:27-39) into `out`. Returns
+// 0, or -1 when `out` is too small (the needed size in *needed).
+int ref_run_plan_csv(int case_b, const std::uint64_t* sizes, std::size_t nsizes, double d1,
+                     double d2, double mu_prime, std::uint64_t reps, std::uint64_t warmups,
+                     std::uint64_t seed, char* out, std::size_t cap, std::size_t* needed,
+                     char* msg, std::size_t msg_cap) {
+  int fit = 0;
+  const int rc = guarded(
+      [&] {
+        afmm::ExperimentPlan plan;
+        plan.kernel = case_b ? afmm::KernelId::AFMM_B : afmm::KernelId::AFMM_A;
+        plan.sizes.assign(sizes, sizes + nsizes);
+        plan.d1 = d1;
+        plan.d2 = d2;
+        plan.mu_prime = mu_prime;
+        plan.replications = reps;
+        plan.warmups = warmups;
+        plan.base_seed = afmm::Seed{seed};
+        std::ostringstream csv;
+        afmm::emit_csv(afmm::run_plan(plan, nullptr), csv);
+        const std::string s = csv.str();
+        *needed = s.size() + 1;
+        if (s.size() + 1 > cap) {
+          fit = -1;
+          return;
+        }
+        std::memcpy(out, s.c_str(), s.size() + 1);
+      },
+      msg, msg_cap);
+  return rc != 0 ? rc : fit;
 }
 
 // ---- row-block entry for the CPU baseline (bench.py) ----

@@ -66,3 +66,53 @@ def test_cli_gpu_kernels_byte_identical(cuda, tmp_path):
     # non-integer rep -> the reference's domain_error text, exit code 2
     r = _run("mul", "y.mat", "x.mat", "--kernel", "afmm-a-gpu", cwd=tmp_path)
     assert r.returncode == 2 and "is not integer-valued" in r.stderr
+
+
+def _rows(csv_text):
+    lines = csv_text.strip().splitlines()
+    return lines[0], [ln.split(",") for ln in lines[1:]]
+
+
+_PLANS = [("a", ["--sizes", "16,24,40", "--d1", "0.6", "--d2", "0.9", "--mu", "4"]),
+          ("b", ["--sizes", "16,33", "--d1", "0.8", "--d2", "0.5", "--mu", "7"])]
+
+
+@pytest.mark.parametrize("case,plan", _PLANS)
+def test_cli_bench_restates_run_plan(reference, tmp_path, case, plan):
+    """`afmm_gpu bench` with a CPU kernel id reproduces the reference's own
+    run_plan + emit_csv (bench.hpp:120-154, report.hpp:27-39): same header,
+    cell seeds, replication indices and counts, every column but the time."""
+    _need_cli()
+    r = _run("bench", "--kernel", f"afmm-{case}", *plan, "--reps", "3", "--warmups", "1",
+             "--seed", "11", "--out", "rec.csv", cwd=tmp_path)
+    assert r.returncode == 0, r.stderr
+    hdr, ours = _rows((tmp_path / "rec.csv").read_text())
+    sizes = [int(x) for x in plan[1].split(",")]
+    kw = dict(zip(("d1", "d2", "mu"), (float(plan[3]), float(plan[5]), float(plan[7]))))
+    ref_hdr, ref = _rows(reference.run_plan_csv(case, sizes, kw["d1"], kw["d2"], kw["mu"], 3, 1,
+                                                11))
+    assert hdr == ref_hdr == ("kernel,n,d1,d2,mu_prime,seed,rep,elapsed_seconds,additions,"
+                              "multiplications,zero_skips")
+    assert len(ours) == len(ref) == 3 * len(sizes)
+    for a, b in zip(ours, ref):
+        assert a[:7] == b[:7] and a[8:] == b[8:]
+        assert len(a[7].split(".")[1]) == 9  # elapsed to 9 decimals
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case,plan", _PLANS)
+def test_cli_bench_gpu_kernel_ids(cuda, tmp_path, case, plan):
+    """The *-gpu kernel ids in the benchmark flow: the same cells (seeds,
+    factor pairs) as the CPU id, identical counts, positive times."""
+    _need_cli()
+    out = {}
+    for k in (f"afmm-{case}", f"afmm-{case}-gpu"):
+        r = _run("bench", "--kernel", k, *plan, "--reps", "2", "--warmups", "2", "--seed", "5",
+                 cwd=tmp_path)
+        assert r.returncode == 0, r.stderr
+        out[k] = _rows(r.stdout)
+    cpu, gpu = out[f"afmm-{case}"][1], out[f"afmm-{case}-gpu"][1]
+    assert len(cpu) == len(gpu) > 0
+    for a, b in zip(cpu, gpu):
+        assert b[0] == f"afmm-{case}-gpu" and a[1:7] == b[1:7] and a[8:] == b[8:]
+        assert float(b[7]) > 0
