@@ -6,8 +6,8 @@
 A step is one AFMM product over the workload's synthetic operands (BASELINE.json
 config; default cfg5 = Case-B n=16384 fp32, ~4.3e13 additions, the config the
 metric's 1/2/4/8-GPU scaling is specified on). Under torchrun each rank owns one
-GPU; the rows are partitioned by work and Z is gathered to rank 0 over NCCL
-inside the step.
+GPU; the rows are partitioned by work and every rank's kernels store its Z rows
+straight into rank 0's result (CUDA IPC peer mapping over NVLink) inside the step.
 
   value  adds/s with operands resident in HBM (CUDA events, max over ranks)
   e2e    the same metric through the reference-facing C-ABI call with pinned HOST
@@ -411,7 +411,12 @@ def main():
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks,
         }
+        if world > 1:
+            line["config"]["gather"] = (
+                "in-kernel peer stores into rank 0's Z (CUDA IPC mapping, NVLink), one barrier"
+                if sharded.used_p2p else "NCCL send/recv of the Z slabs after the compute")
         print(json.dumps(line), flush=True)
+    sharded.close()
     ctx.close()
     if world > 1:
         dist.barrier()
@@ -460,7 +465,8 @@ def _e2e(args, afmm, dist, torch, world, rank, local, cfg, lhs, rhs, es, job_add
             "h2d_bytes_per_step": 2 * n * n * es * world, "d2h_bytes_per_step": n * n * es,
             "ms_per_step": secs * 1e3, "steps": reps,
             "api": "afmm_case_%s_%s (C ABI, host buffers)" % (cfg.case, "f32" if es == 4 else "f64")
-            if world == 1 else "per-rank H2D + row-sharded product + NCCL gather + D2H on rank 0"}
+            if world == 1 else "per-rank H2D + row-sharded product (Z slabs into rank 0) + D2H "
+                               "on rank 0"}
 
 
 def _hbm_check(traffic):

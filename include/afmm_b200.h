@@ -161,6 +161,28 @@ afmm_status afmm_row_work_device(afmm_context* ctx, int32_t which_case, int32_t 
  * Pure host function (no device needed). */
 afmm_status afmm_partition_rows(const uint64_t* work, uint64_t n, uint32_t parts, uint64_t* cuts);
 
+/* ---- peer-memory output (multi-GPU row sharding) -----------
+ * A row-sharded product can write its Z slab straight into rank 0's result
+ * over NVLink instead of gathering the slabs afterwards: rank 0 exports the
+ * device buffer holding Z, every other rank opens the handle (CUDA IPC; peer
+ * access is enabled on open) and passes the opened pointer, advanced to its
+ * first row, as `out` of afmm_product_device. The repeated-addition kernels
+ * then store their Z tiles to the peer GPU as they finish, overlapping the
+ * transfer with the compute. Completion: each rank finishes its own product
+ * (sync = 1 or afmm_context_finish), then the ranks meet at a host barrier.
+ * `offset` is the byte offset of dev_ptr inside its allocation. */
+typedef struct afmm_ipc_handle {
+  uint8_t bytes[64];
+  uint64_t offset;
+} afmm_ipc_handle;
+
+afmm_status afmm_ipc_export(const void* dev_ptr, afmm_ipc_handle* handle, afmm_error* error);
+/* Opens a handle exported by another process on `device`; *dev_ptr is the
+ * exported pointer as seen from this process. */
+afmm_status afmm_ipc_open(int32_t device, const afmm_ipc_handle* handle, void** dev_ptr,
+                          afmm_error* error);
+afmm_status afmm_ipc_close(void* dev_ptr);
+
 /* ---- roofline ---------------------------------------------------------------
  * Measure the CUDA-core FP-add peak of `device` with a register-resident
  * add-chain microbenchmark (the same instruction mix as the product's inner

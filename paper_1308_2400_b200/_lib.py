@@ -61,6 +61,10 @@ class Error(ctypes.Structure):
     ]
 
 
+class IpcHandle(ctypes.Structure):
+    _fields_ = [("bytes", ctypes.c_uint8 * 64), ("offset", c_uint64)]
+
+
 class Options(ctypes.Structure):
     _fields_ = [("mode", c_int32), ("device", c_int32), ("split_k", c_int32), ("reserved", c_int32)]
 
@@ -91,6 +95,9 @@ _SIGNATURES = {
                                        c_uint64, POINTER(c_uint64), POINTER(Error)]),
     "afmm_partition_rows": (c_int32, [POINTER(c_uint64), c_uint64, c_uint32, POINTER(c_uint64)]),
     "afmm_fp_add_peak": (c_int32, [c_int32, c_int32, POINTER(c_double), POINTER(c_double)]),
+    "afmm_ipc_export": (c_int32, [c_void_p, POINTER(IpcHandle), POINTER(Error)]),
+    "afmm_ipc_open": (c_int32, [c_int32, POINTER(IpcHandle), POINTER(c_void_p), POINTER(Error)]),
+    "afmm_ipc_close": (c_int32, [c_void_p]),
     "afmm_kernel_launch_count": (c_uint64, []),
     "afmm_status_string": (ctypes.c_char_p, [c_int32]),
     "afmm_abi_version": (c_int32, []),

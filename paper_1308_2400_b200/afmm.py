@@ -156,8 +156,23 @@ def afmm_case_b(lhs, rhs, *, mode: str = ORDER_PRESERVING, device: Optional[int]
 _DT_CODE = {"float64": _lib.F64, "float32": _lib.F32}
 
 
+class RawRows:
+    """Row-major device rows addressed by a raw pointer (e.g. another GPU's
+    buffer opened with ipc_open): usable as `out` of DeviceContext.product."""
+
+    def __init__(self, ptr: int, ld: int, dtype: str, ncols: int):
+        self.ptr, self.ld, self.dtype, self.ncols = int(ptr), int(ld), dtype, int(ncols)
+
+    def rows(self, r0: int) -> "RawRows":
+        """The view starting at row r0."""
+        es = 4 if self.dtype == "float32" else 8
+        return RawRows(self.ptr + r0 * self.ld * es, self.ld, self.dtype, self.ncols)
+
+
 def _tensor_info(t) -> Tuple[int, int, str, int]:
     """(data_ptr, leading dimension, dtype name, n) of a 2D row-major CUDA tensor."""
+    if isinstance(t, RawRows):
+        return t.ptr, t.ld, t.dtype, t.ncols
     if t.dim() != 2 or t.stride(1) != 1:
         raise InvalidArgument("afmm: device operands must be 2D with unit column stride")
     name = str(t.dtype).replace("torch.", "")
@@ -272,6 +287,33 @@ def fp_add_peak(device: int = 0, dtype: str = "float32") -> Tuple[float, float]:
     if status != _lib.OK:
         raise DeviceError("afmm_fp_add_peak failed")
     return rate.value, mhz.value
+
+
+def ipc_export(tensor) -> Tuple[bytes, int]:
+    """CUDA IPC handle (64 bytes) and byte offset of a device tensor's storage
+    (afmm_ipc_export): another process opens it with ipc_open."""
+    h = _lib.IpcHandle()
+    err = _lib.Error()
+    _raise_for(_lib.load().afmm_ipc_export(ctypes.c_void_p(tensor.data_ptr()), ctypes.byref(h),
+                                           ctypes.byref(err)), err)
+    return bytes(h.bytes), int(h.offset)
+
+
+def ipc_open(device: int, handle: bytes, offset: int) -> int:
+    """Map a buffer exported by another process (afmm_ipc_open); returns the
+    device pointer (peer access over NVLink when the buffer is on another GPU)."""
+    h = _lib.IpcHandle()
+    ctypes.memmove(h.bytes, handle, 64)
+    h.offset = offset
+    p = ctypes.c_void_p()
+    err = _lib.Error()
+    _raise_for(_lib.load().afmm_ipc_open(int(device), ctypes.byref(h), ctypes.byref(p),
+                                         ctypes.byref(err)), err)
+    return int(p.value)
+
+
+def ipc_close(ptr: int) -> None:
+    _lib.load().afmm_ipc_close(ctypes.c_void_p(ptr))
 
 
 def kernel_launch_count() -> int:

@@ -1197,6 +1197,78 @@ afmm_status afmm_fp_add_peak(int32_t device, int32_t dtype, double* adds_per_sec
   return e == cudaSuccess ? AFMM_OK : AFMM_ERR_CUDA;
 }
 
+// ---- peer-memory output -----------------------------------------------------
+
+namespace {
+std::mutex g_ipc_mu;
+std::vector<std::pair<void*, void*>> g_ipc_open;  // (pointer handed out, mapped base)
+}  // namespace
+
+afmm_status afmm_ipc_export(const void* dev_ptr, afmm_ipc_handle* handle, afmm_error* err) {
+  clear_error(err);
+  if (!dev_ptr || !handle) return AFMM_ERR_INVALID_ARGUMENT;
+  static PFN_cuMemGetAddressRange_v3020 range_fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      range_fn = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(p);
+  });
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (!range_fn || range_fn(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS) {
+    set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0,
+              "afmm: cuMemGetAddressRange failed (not a device allocation)");
+    return AFMM_ERR_INVALID_ARGUMENT;
+  }
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return cuda_fail(err, e, "afmm: cudaIpcGetMemHandle");
+  static_assert(sizeof(h) <= sizeof(handle->bytes), "IPC handle size");
+  std::memset(handle->bytes, 0, sizeof(handle->bytes));
+  std::memcpy(handle->bytes, &h, sizeof(h));
+  handle->offset = reinterpret_cast<CUdeviceptr>(dev_ptr) - base;
+  return AFMM_OK;
+}
+
+afmm_status afmm_ipc_open(int32_t device, const afmm_ipc_handle* handle, void** dev_ptr,
+                          afmm_error* err) {
+  clear_error(err);
+  if (!handle || !dev_ptr) return AFMM_ERR_INVALID_ARGUMENT;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(err, e, "afmm: cudaSetDevice");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle->bytes, sizeof(h));
+  void* base = nullptr;
+  e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return cuda_fail(err, e, "afmm: cudaIpcOpenMemHandle");
+  *dev_ptr = static_cast<char*>(base) + handle->offset;
+  std::lock_guard<std::mutex> g(g_ipc_mu);
+  g_ipc_open.emplace_back(*dev_ptr, base);
+  return AFMM_OK;
+}
+
+afmm_status afmm_ipc_close(void* dev_ptr) {
+  void* base = nullptr;
+  {
+    std::lock_guard<std::mutex> g(g_ipc_mu);
+    for (size_t i = 0; i < g_ipc_open.size(); ++i)
+      if (g_ipc_open[i].first == dev_ptr) {
+        base = g_ipc_open[i].second;
+        g_ipc_open.erase(g_ipc_open.begin() + i);
+        break;
+      }
+  }
+  if (!base) return AFMM_ERR_INVALID_ARGUMENT;
+  return cudaIpcCloseMemHandle(base) == cudaSuccess ? AFMM_OK : AFMM_ERR_CUDA;
+}
+
 uint64_t afmm_kernel_launch_count(void) {
   return afmm_dev::g_launches.load(std::memory_order_relaxed);
 }

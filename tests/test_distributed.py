@@ -48,7 +48,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, case, n, result_path):
+def _worker(rank, world, port, case, n, result_path, gather=None):
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -64,8 +64,9 @@ def _worker(rank, world, port, case, n, result_path):
     lhs, rhs = make_inputs(name, seed=5, n=n)
     L, R = torch.from_numpy(lhs), torch.from_numpy(rhs)
     Z = torch.full((n, n), float("nan"), dtype=L.dtype)
-    sp = ShardedProduct(OracleContext(), dist, rank, world)
+    sp = ShardedProduct(OracleContext(), dist, rank, world, gather=gather)
     counts = sp.run(case, L, R, Z, torch.empty_like(Z))
+    assert not sp.used_p2p  # host tensors: the p2p path declines, send/recv runs
     adds = torch.tensor([counts.additions], dtype=torch.float64)
     dist.all_reduce(adds)
     if rank == 0:
@@ -75,12 +76,13 @@ def _worker(rank, world, port, case, n, result_path):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case,n", [("a", 96), ("b", 130)])
-def test_two_rank_gloo_sharded_product_matches_single_process(tmp_path, case, n, oracle):
+@pytest.mark.parametrize("case,n,gather", [("a", 96, None), ("b", 130, None),
+                                           ("b", 77, "sendrecv")])
+def test_two_rank_gloo_sharded_product_matches_single_process(tmp_path, case, n, gather, oracle):
     from paper_1308_2400_b200.gen import expected_additions, make_inputs
 
     out = str(tmp_path / "z.npy")
-    mp.spawn(_worker, args=(2, _free_port(), case, n, out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), case, n, out, gather), nprocs=2, join=True)
     z = np.load(out)
     meta = np.load(out + ".meta.npy")
     name = "cfg4" if case == "a" else "cfg5"

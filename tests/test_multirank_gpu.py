@@ -28,7 +28,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, name, n, out_path):
+def _worker(rank, world, port, name, n, out_path, gather):
     sys.path.insert(0, ROOT)
     import torch
     import torch.distributed as dist
@@ -46,20 +46,28 @@ def _worker(rank, world, port, name, n, out_path):
     R = torch.from_numpy(rhs).cuda()
     Z = torch.full((n, n), float("nan"), dtype=L.dtype, device="cuda")
     ctx = afmm.DeviceContext(0)
-    sp = ShardedProduct(ctx, dist, rank, world)
-    counts = sp.run(CONFIGS[name].case, L, R, Z, torch.empty_like(Z))
+    sp = ShardedProduct(ctx, dist, rank, world, gather=gather)
+    for _ in range(3):  # repeated steps (graph replay, IPC mapping reused)
+        Z.fill_(float("nan"))
+        counts = sp.run(CONFIGS[name].case, L, R, Z, torch.empty_like(Z))
+    assert sp.used_p2p == (gather == "p2p")
     adds = torch.tensor([counts.additions], dtype=torch.float64)
     dist.all_reduce(adds)
     if rank == 0:
         np.save(out_path, Z.cpu().numpy())
         np.save(out_path + ".meta.npy", np.array([adds.item(), *sp.cuts], dtype=np.float64))
     dist.barrier()
+    sp.close()
     ctx.close()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,n", [("cfg5", 900), ("cfg4", 1100)])
-def test_two_ranks_on_one_gpu_match_single_process(cuda, tmp_path, name, n):
+@pytest.mark.parametrize("name,n,gather", [("cfg5", 900, "p2p"), ("cfg4", 1100, "p2p"),
+                                           ("cfg5", 700, "sendrecv")])
+def test_two_ranks_on_one_gpu_match_single_process(cuda, tmp_path, name, n, gather):
+    """gather = "p2p": rank 1 maps rank 0's Z over CUDA IPC and its kernels
+    store its slab straight into it (on one GPU the mapping is the same
+    device; on a multi-GPU box it is peer memory over NVLink)."""
     import torch
     import torch.multiprocessing as mp
 
@@ -67,7 +75,8 @@ def test_two_ranks_on_one_gpu_match_single_process(cuda, tmp_path, name, n):
     from paper_1308_2400_b200.gen import CONFIGS, expected_additions, make_inputs
 
     out = str(tmp_path / "z.npy")
-    mp.start_processes(_worker, args=(2, _free_port(), name, n, out), nprocs=2, join=True,
+    mp.start_processes(_worker, args=(2, _free_port(), name, n, out, gather), nprocs=2,
+                       join=True,
                        start_method="spawn")
     z = np.load(out)
     meta = np.load(out + ".meta.npy")
@@ -99,3 +108,4 @@ def test_bench_multi_rank_path_runs(cuda):
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
     assert "REDUCED" in d["config"]["workload"]
     assert d["gpu_launches"] > 0
+    assert d["config"]["gather"].startswith("in-kernel peer stores")
