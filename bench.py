@@ -361,6 +361,8 @@ def main():
 
     # ---- roofline of the repeated-addition kernel (this rank's launch) ----
     kms = statistics.median(kernel_ms)
+    if not kms > 0.0:
+        raise RuntimeError(f"no device timing of the repeated-addition kernel: {kernel_ms}")
     achieved = rank_adds / (kms * 1e-3)
     traffic = _ncu_traffic(args.config if args.config != "cfg3"
                            else f"cfg3_d{args.d1:g}_mu{args.mu}")

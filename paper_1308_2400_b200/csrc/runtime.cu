@@ -184,9 +184,19 @@ struct afmm_context {
   // optional phase timing: ev[0] start, ev[1] before compute, ev[2] after compute, ev[3] end
   bool timing = false;
   bool timed_last = false;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // direct calls
+  cudaEvent_t* rec_ev = ev;  // where mark() records: ev, or a graph's own events while capturing
+  cudaEvent_t last_ev[4] = {nullptr, nullptr, nullptr, nullptr};  // the last product's events
+  // Under stream capture (graph_call) a plain record only orders the capture
+  // and is never replayed; an external record becomes an event-record node, so
+  // replays are timed like direct calls. Outside a capture the external flag
+  // is rejected (cudaErrorIllegalState, measured), and the captured graph gets
+  // its own events.
+  bool capturing = false;
   void mark(int i) {
-    if (timing) cudaEventRecord(ev[i], stream);
+    if (!timing) return;
+    if (capturing) cudaEventRecordWithFlags(rec_ev[i], stream, cudaEventRecordExternal);
+    else cudaEventRecord(rec_ev[i], stream);
   }
   // CUDA-graph replay of repeated identical device-API calls (graph_call)
   struct GraphKey {
@@ -207,6 +217,13 @@ struct afmm_context {
     cudaGraphExec_t exec = nullptr;
     uint64_t gen = 0, launches = 0;
     int last_form = 0;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // timing graphs only
+    void release() {
+      if (exec) cudaGraphExecDestroy(exec);
+      exec = nullptr;
+      for (cudaEvent_t& e : ev)
+        if (e) cudaEventDestroy(e);
+    }
   };
   uint64_t buf_gen = 0;
   bool graphs = true;  // AFMM_GRAPHS=0 disables
@@ -537,6 +554,7 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
   DevStatus* st = c->status.as<DevStatus>();
   c->list_cap = n;
   c->timed_last = c->timing;
+  for (int i = 0; i < 4; ++i) c->last_ev[i] = c->rec_ev[i];
   c->mark(0);
   CK(cudaMemsetAsync(st, 0, sizeof(DevStatus), s), "memset");
 
@@ -753,7 +771,7 @@ afmm_status graph_call(afmm_context* c, int which, const T* lhs, const T* rhs, u
   auto& cache = c->graph_cache;
   for (size_t i = 0; i < cache.size();) {  // entries captured before a reallocation
     if (cache[i].gen != c->buf_gen) {
-      cudaGraphExecDestroy(cache[i].exec);
+      cache[i].release();
       cache.erase(cache.begin() + i);
     } else {
       ++i;
@@ -775,6 +793,7 @@ afmm_status graph_call(afmm_context* c, int which, const T* lhs, const T* rhs, u
     CK(join_and_launch(*hit), "afmm: graph launch");
     for (uint64_t i = 0; i < hit->launches; ++i) afmm_dev::note_launch();
     c->timed_last = c->timing;
+    for (int i = 0; i < 4; ++i) c->last_ev[i] = hit->ev[i];
     c->last_case = which;
     c->last_dtype = key.dtype;
     c->last_lhs = lhs;
@@ -799,38 +818,47 @@ afmm_status graph_call(afmm_context* c, int which, const T* lhs, const T* rhs, u
       return direct();
     }
   }
+  afmm_context::GraphEntry ge;
+  for (int i = 0; key.timing && i < 4; ++i)
+    if (cudaEventCreate(&ge.ev[i]) != cudaSuccess) {
+      cudaGetLastError();
+      ge.release();
+      return direct();
+    }
   const uint64_t launches0 = afmm_dev::g_launches.load();
   c->stream = c->gstream;
   if (cudaStreamBeginCapture(c->gstream, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
     cudaGetLastError();
     c->stream = user;
     c->graphs = false;
+    ge.release();
     return direct();
   }
+  if (key.timing) c->rec_ev = ge.ev;
+  c->capturing = true;
   const afmm_status st = direct();
+  c->capturing = false;
+  c->rec_ev = c->ev;
   cudaGraph_t graph = nullptr;
   const cudaError_t ec = cudaStreamEndCapture(c->gstream, &graph);
   c->stream = user;
-  cudaGraphExec_t exec = nullptr;
   const bool ok = st == AFMM_OK && ec == cudaSuccess && graph &&
-                  cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+                  cudaGraphInstantiate(&ge.exec, graph, 0) == cudaSuccess;
   if (graph) cudaGraphDestroy(graph);
   if (!ok) {  // fall back to direct calls for the life of the context
     cudaGetLastError();
-    if (exec) cudaGraphExecDestroy(exec);
+    ge.release();
     c->graphs = false;
     c->pending = false;
     if (st != AFMM_OK) return st;
     return direct();
   }
-  afmm_context::GraphEntry ge;
   ge.key = key;
-  ge.exec = exec;
   ge.gen = c->buf_gen;
   ge.launches = afmm_dev::g_launches.load() - launches0;
   ge.last_form = c->last_form;
   if (cache.size() >= 8) {
-    cudaGraphExecDestroy(cache.front().exec);
+    cache.front().release();
     cache.erase(cache.begin());
   }
   cache.push_back(ge);
@@ -1017,7 +1045,7 @@ void afmm_context_destroy(afmm_context* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     if (c->gstream) cudaStreamSynchronize(c->gstream);
-    for (auto& ge : c->graph_cache) cudaGraphExecDestroy(ge.exec);
+    for (auto& ge : c->graph_cache) ge.release();
     c->graph_cache.clear();
     if (c->gstream) cudaStreamDestroy(c->gstream);
     if (c->join_in) cudaEventDestroy(c->join_in);
@@ -1112,7 +1140,8 @@ afmm_status afmm_context_last_timing(afmm_context* c, float* prepass_ms, float* 
   float v[3] = {-1.f, -1.f, -1.f};
   if (c->timed_last && !c->pending) {
     for (int i = 0; i < 3; ++i)
-      if (cudaEventElapsedTime(&v[i], c->ev[i], c->ev[i + 1]) != cudaSuccess) v[i] = -1.f;
+      if (cudaEventElapsedTime(&v[i], c->last_ev[i], c->last_ev[i + 1]) != cudaSuccess)
+        v[i] = -1.f;
   }
   if (prepass_ms) *prepass_ms = v[0];
   if (compute_ms) *compute_ms = v[1];

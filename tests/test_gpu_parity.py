@@ -644,3 +644,33 @@ def test_repeated_device_calls_replay_graphs_exactly(cuda, oracle, dt):
             ctx.product(case, lhs, rhs, Ob, mode=afmm.FAST)
         assert bool(torch.all(Ob == 7.0)), case
     ctx.close()
+
+
+def test_phase_timing_on_graph_replays(cuda):
+    """afmm_context_last_timing reports every phase of direct calls AND of
+    graph replays (the timing events are recorded as event-record nodes in the
+    captured graph); bench.py's roofline reads the compute phase."""
+    import torch
+
+    from paper_1308_2400_b200.gen import make_inputs
+
+    afmm = _api()
+    ctx = afmm.DeviceContext(0)
+    ctx.enable_timing(True)
+    lhs, rhs = make_inputs("cfg2", seed=3, n=512)
+    L = torch.from_numpy(lhs).cuda()
+    R = torch.from_numpy(rhs).cuda()
+    Z = torch.empty_like(L)
+    launches = []
+    for _ in range(5):  # direct, direct (captured), replays
+        k0 = afmm.kernel_launch_count()
+        ctx.product("b", L, R, Z)
+        launches.append(afmm.kernel_launch_count() - k0)
+        torch.cuda.synchronize()
+        pre, comp, epi = ctx.last_timing()
+        assert pre >= 0.0 and comp > 0.0 and epi >= 0.0, (pre, comp, epi)
+    assert len(set(launches)) == 1
+    ctx.enable_timing(False)
+    ctx.product("b", L, R, Z)
+    assert ctx.last_timing() == (-1.0, -1.0, -1.0)
+    ctx.close()
