@@ -70,6 +70,19 @@ constexpr int REP_UNROLL = AFMM_EXP_REP_UNROLL;
 #ifndef AFMM_EXP_WIDE_CW
 #define AFMM_EXP_WIDE_CW kWideRows
 #endif
+// Producer-less ring (experiment): no TMA warp; the consumer warp that
+// releases a stage last refills it (smem counter per slot), so 16 consumer
+// warps per SM get the 128-register budget of 16 warps.
+#ifndef AFMM_EXP_NOPROD
+#define AFMM_EXP_NOPROD 0
+#endif
+constexpr bool kNoProd = AFMM_EXP_NOPROD != 0;
+constexpr int kProdWarps = kNoProd ? 0 : 1;
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // A TMA box is at most 256 elements wide, so a stage is G/2 boxes of
 // KB x BOX_BYTES laid out box-major: [box][k row][BOX_BYTES].
 constexpr int BOX_BYTES = 1024;
@@ -464,7 +477,7 @@ __device__ __forceinline__ uint32_t lower_bound_k(const int2* lst, uint32_t cnt,
 // of the nkb_total k blocks and writes to out + z * slice_stride (fast-mode
 // split-k; one slice = the whole k range in order-preserving mode).
 template <class T, int G, int CW, int STAGES, int MINB, bool SPLIT>
-__global__ void __launch_bounds__((CW + 1) * 32, MINB)
+__global__ void __launch_bounds__((CW + kProdWarps) * 32, MINB)
     k_bform(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ lists,
             uint64_t cap, const uint32_t* __restrict__ counts, uint32_t nrows, uint32_t rpc,
             int32_t col0, int32_t ncols, uint32_t nkb_total, uint32_t slice_blocks, uint64_t slice_stride,
@@ -493,16 +506,29 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
   const uint32_t nkb = kb_hi - kb_lo;
   if (SPLIT) out += blockIdx.z * slice_stride;
 
+  // refill of ring slot `sl` with block `blk` of the slice (one thread)
+  auto refill = [&](uint32_t sl, uint32_t blk) {
+    mbar_arrive_expect_tx(&full[sl], (uint32_t)Gm::STAGE_BYTES);
+    const int32_t krow = (int32_t)((kb_lo + blk) * KB);
+#pragma unroll
+    for (int h = 0; h < Gm::NBOX; ++h)
+      tma_load_2d(base + sl * Gm::STAGE_BYTES + h * KB * BOX_BYTES, &tmap, &full[sl],
+                  col0 + tile_c + h * Gm::BOX_N, krow);
+  };
+  uint32_t* released = reinterpret_cast<uint32_t*>(empty);  // kNoProd: arrivals per slot
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CW);
+      if (kNoProd) released[s] = 0;
+      else mbar_init(&empty[s], CW);
     }
     fence_barrier_init();
+    if (kNoProd)
+      for (uint32_t s = 0; s < (uint32_t)STAGES && s < nkb; ++s) refill(s, s);
   }
   __syncthreads();
 
-  if (warp == CW) {
+  if (!kNoProd && warp == CW) {
     // ---- dedicated TMA producer warp ----
     // (Unlike k_bform_mr, the list-walking warps progress unevenly; an
     // in-warp pump makes warp 0 the ring's bottleneck: measured 2-3x slower.)
@@ -545,7 +571,18 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
   uint32_t stage_addr = ring + lane * 16;
   auto advance = [&]() {
     __syncwarp();
-    if (lane == 0) mbar_arrive_at(empty0 + slot * 8);
+    if (lane == 0) {
+      if (kNoProd) {
+        // the last of the CW warps to release this use of the slot refills it
+        const uint32_t old = atomicAdd(&released[slot], 1u);
+        if (old % CW == CW - 1 && kb_cur + STAGES < nkb) {
+          fence_proxy_async_smem();  // order the warps' smem reads before the TMA write
+          refill(slot, kb_cur + STAGES);
+        }
+      } else {
+        mbar_arrive_at(empty0 + slot * 8);
+      }
+    }
     ++kb_cur;
     stage_addr += Gm::STAGE_BYTES;
     if (++slot == STAGES) {
@@ -1207,7 +1244,7 @@ cudaError_t launch_ring(const CUtensorMap* tmap, const int2* lists, uint64_t cap
   const uint32_t tiles = (ncols + Geo<T, G>::TILE_N - 1) / Geo<T, G>::TILE_N;
   const uint32_t rpc = balanced_rows(nrows, tiles * *splits, CW, MINB);
   dim3 grid((nrows + rpc - 1) / rpc, tiles, *splits);
-  kern<<<grid, (CW + 1) * 32, smem, s>>>(*tmap, lists, cap, counts, nrows, rpc, col0, ncols, nkb,
+  kern<<<grid, (CW + kProdWarps) * 32, smem, s>>>(*tmap, lists, cap, counts, nrows, rpc, col0, ncols, nkb,
                                          slice_blocks, slice_stride, out, ld_out,
                                          vec_ok ? 1 : 0, st);
   note_launch();
