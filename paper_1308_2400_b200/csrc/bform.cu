@@ -54,9 +54,27 @@ constexpr int KB = 8;  // k rows per stage
 constexpr int KB = AFMM_EXP_KB;  // timing experiments (Makefile exp-%)
 #endif
 #ifndef AFMM_EXP_REP_UNROLL
-constexpr int REP_UNROLL = 4;  // rep-loop unroll (adds per column per trip)
+// rep loop: trips of 8 steps, then the remainder (< 8) by its binary digits
+// (4, 2, 1 steps) with no loop. Measured against 4-step trips + a 1-step
+// remainder loop: cfg5 1845 -> 1809 ms, rep 16 0.901 -> 0.912 of peak, and 88
+// registers instead of 96 + an 8-byte spill (ptxas); the loop counter and
+// back-edge instructions it removes issue on the FMA pipe (VIADD) or stall on
+// branch resolution.
+constexpr int REP_UNROLL = 8;  // rep-loop unroll (adds per column per trip)
 #else
 constexpr int REP_UNROLL = AFMM_EXP_REP_UNROLL;
+#endif
+#ifndef AFMM_EXP_REP_BIN
+constexpr bool REP_BIN = true;  // remainder by binary digits instead of a loop
+#else
+constexpr bool REP_BIN = AFMM_EXP_REP_BIN != 0;
+#endif
+static_assert(!REP_BIN || (REP_UNROLL & (REP_UNROLL - 1)) == 0,
+              "a binary remainder needs a power-of-two unroll");
+#ifndef AFMM_EXP_REP_MID
+constexpr int REP_MID = 0;  // optional mid-size chunk between the unrolled loop and single steps
+#else
+constexpr int REP_MID = AFMM_EXP_REP_MID;
 #endif
 #ifndef AFMM_EXP_WIDE_STAGES
 #define AFMM_EXP_WIDE_STAGES 3
@@ -232,6 +250,28 @@ struct Acc<float, G> {
                                       : b[c - 2 * G0]);
       t -= REP_UNROLL;
     }
+    if (REP_BIN) {  // remainder t < REP_UNROLL by its binary digits, no loop
+#pragma unroll
+      for (int bit = REP_UNROLL / 2; bit >= 1; bit >>= 1)
+        if (t & (uint32_t)bit) {
+#pragma unroll
+          for (int u = 0; u < bit; ++u)
+#pragma unroll
+            for (int c = 2 * G0; c < 2 * G1; ++c)
+              a[c] = __fadd2_rn(a[c], NEG ? make_float2(-b[c - 2 * G0].x, -b[c - 2 * G0].y)
+                                          : b[c - 2 * G0]);
+        }
+      return;
+    }
+    if (REP_MID > 0 && t >= (uint32_t)REP_MID) {
+#pragma unroll
+      for (int u = 0; u < REP_MID; ++u)
+#pragma unroll
+        for (int c = 2 * G0; c < 2 * G1; ++c)
+          a[c] = __fadd2_rn(a[c], NEG ? make_float2(-b[c - 2 * G0].x, -b[c - 2 * G0].y)
+                                      : b[c - 2 * G0]);
+      t -= REP_MID;
+    }
 #pragma unroll 1
     while (t != 0) {
 #pragma unroll
@@ -337,6 +377,26 @@ struct Acc<double, G> {
         for (int c = 2 * G0; c < 2 * G1; ++c)
           a[c] = __dadd_rn(a[c], NEG ? -b[c - 2 * G0] : b[c - 2 * G0]);
       t -= REP_UNROLL;
+    }
+    if (REP_BIN) {
+#pragma unroll
+      for (int bit = REP_UNROLL / 2; bit >= 1; bit >>= 1)
+        if (t & (uint32_t)bit) {
+#pragma unroll
+          for (int u = 0; u < bit; ++u)
+#pragma unroll
+            for (int c = 2 * G0; c < 2 * G1; ++c)
+              a[c] = __dadd_rn(a[c], NEG ? -b[c - 2 * G0] : b[c - 2 * G0]);
+        }
+      return;
+    }
+    if (REP_MID > 0 && t >= (uint32_t)REP_MID) {
+#pragma unroll
+      for (int u = 0; u < REP_MID; ++u)
+#pragma unroll
+        for (int c = 2 * G0; c < 2 * G1; ++c)
+          a[c] = __dadd_rn(a[c], NEG ? -b[c - 2 * G0] : b[c - 2 * G0]);
+      t -= REP_MID;
     }
 #pragma unroll 1
     while (t != 0) {
@@ -597,6 +657,10 @@ __global__ void __launch_bounds__((CW + kProdWarps) * 32, MINB)
   // entry e = (k, rep) broadcast one entry ahead of its use
   uint32_t k = (uint32_t)__shfl_sync(FULL, cur.x, 0);
   int rep = __shfl_sync(FULL, cur.y, 0);
+#ifdef AFMM_EXP_ENTRY_UNROLL
+  constexpr int kEntryUnroll = AFMM_EXP_ENTRY_UNROLL;
+#pragma unroll (kEntryUnroll)
+#endif
   for (uint32_t e = 0; e < cnt; ++e) {
     const uint32_t f = e + 1;
     if ((f & 31u) == 0) {  // next entry starts a new chunk of 32
