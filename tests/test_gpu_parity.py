@@ -371,6 +371,34 @@ def test_case_a_form_signed_and_large_reps(cuda, oracle, big):
     ctx.close()
 
 
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_every_rep_magnitude_and_remainder(cuda, oracle, dt):
+    """The B-form rep loop runs trips of 8 steps and then the remainder's binary
+    digits (4, 2, 1): every |rep| in 1..40 (all remainders, 0-5 full trips) with
+    both signs, each on its own output rows, plus rows mixing all of them;
+    bit-exact against the oracle (kernels.hpp:95-104)."""
+    n = 1200
+    rng = np.random.default_rng(40)
+    mags = np.arange(1, 41)
+    reps = np.empty((n, n))
+    for i in range(n):
+        if i < 160:  # row i: one magnitude, sign alternating along the row
+            m = mags[i % 40] * (1 if i < 80 else -1)
+            reps[i] = np.where(np.arange(n) % 2 == 0, m, -m)
+        else:
+            reps[i] = rng.choice(np.concatenate([mags, -mags, [0]]), n)
+    bases = rng.standard_normal((n, n)) * (rng.random((n, n)) < 0.7)
+    lhs, rhs = reps.astype(dt), bases.astype(dt)
+    res = _call("b", lhs, rhs)
+    rows = list(range(0, 160, 7)) + [160, 600, n - 1]
+    for r in rows:
+        zr, _ = oracle.product_mt("b", lhs, rhs, r, r + 1, 1)
+        assert _bits_equal(res.product[r:r + 1], zr), (dt, r)
+    from paper_1308_2400_b200.gen import expected_additions
+
+    assert res.counts.additions == expected_additions("b", lhs, rhs)
+
+
 @pytest.mark.parametrize("case,n,dt", [("a", 3001, np.float32), ("b", 5003, np.float32),
                                         ("a", 1537, np.float64), ("b", 2049, np.float64)])
 def test_ragged_sizes_every_tile_shape(cuda, oracle, case, n, dt):
