@@ -4,7 +4,7 @@
 
 Prints the repeated-addition kernel's fraction of the measured FP-add peak on
 constant-rep dense inputs (rep 1, 2, 4, 16) and the whole-product time of
-cfg2, cfg3 (d1=1, mu=1/4/16) and cfg4 (and cfg5 with --big).
+cfg2, cfg3 (d1=1, mu=1/4/16) and cfg4 (and cfg5 with --big, cfg3 d1 = 0.1 with --aform).
 """
 import os
 import sys
@@ -40,6 +40,8 @@ del X, Y, O
 
 points = [("cfg2", {}), ("cfg3", {"d1": 1.0, "mu": 1}), ("cfg3", {"d1": 1.0, "mu": 4}),
           ("cfg3", {"d1": 1.0, "mu": 16}), ("cfg4", {})]
+if "--aform" in sys.argv:  # sparse-X points that run the A-form kernel
+    points += [("cfg3", {"d1": 0.1, "mu": m}) for m in (1, 4, 16)]
 if "--big" in sys.argv:
     points.append(("cfg5", {}))
 for name, kw in points:
