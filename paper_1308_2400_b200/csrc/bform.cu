@@ -95,6 +95,7 @@ constexpr int REP_MID = AFMM_EXP_REP_MID;
 #define AFMM_EXP_NOPROD 0
 #endif
 constexpr bool kNoProd = AFMM_EXP_NOPROD != 0;
+constexpr uint32_t kListPrefetch = 64;  // list entries ahead prefetched into L1
 constexpr int kProdWarps = kNoProd ? 0 : 1;
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
@@ -652,32 +653,28 @@ __global__ void __launch_bounds__((CW + kProdWarps) * 32, MINB)
     }
   };
   mbar_sleep_wait_at(full0, 0);
-  int2 cur = lane < cnt ? lst[lane] : make_int2(0, 0);
-  int2 nxt = 32 + lane < cnt ? lst[32 + lane] : make_int2(0, 0);
-  // entry e = (k, rep) broadcast one entry ahead of its use
-  uint32_t k = (uint32_t)__shfl_sync(FULL, cur.x, 0);
-  int rep = __shfl_sync(FULL, cur.y, 0);
-#ifdef AFMM_EXP_ENTRY_UNROLL
-  constexpr int kEntryUnroll = AFMM_EXP_ENTRY_UNROLL;
-#pragma unroll (kEntryUnroll)
-#endif
+  // Entry e + 1 = (k, rep) is read by a warp-uniform load (L1 broadcast)
+  // while entry e runs, and the list line 64 entries ahead is prefetched into
+  // L1. (Measured against one coalesced 32-entry load per chunk + SHFL
+  // broadcasts: equal at cfg5, cfg3 mu = 4 +2.6%, cfg4 +1%, rep 1 -2%; fewer
+  // instructions and branches per entry.)
+  const int2* __restrict__ lp = lst;
+  const int2 e0 = cnt ? __ldg(lp) : make_int2(0, 0);
+  uint32_t k = (uint32_t)e0.x;
+  int rep = e0.y;
   for (uint32_t e = 0; e < cnt; ++e) {
     const uint32_t f = e + 1;
-    if ((f & 31u) == 0) {  // next entry starts a new chunk of 32
-      cur = nxt;
-      const uint32_t pn = f + 32 + lane;
-      nxt = pn < cnt ? lst[pn] : make_int2(0, 0);
-    }
-    const uint32_t k_n = (uint32_t)__shfl_sync(FULL, cur.x, f & 31u);
-    const int rep_n = __shfl_sync(FULL, cur.y, f & 31u);
+    const int2 ne = f < cnt ? __ldg(lp + f) : make_int2(0, 0);
+    if (f + kListPrefetch < cnt)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(lp + f + kListPrefetch));
     const uint32_t kb = (k - k_lo) / KB;  // block index within the slice
     while (kb_cur < kb) {
       advance();
       mbar_sleep_wait_at(full0 + slot * 8, phase);
     }
     acc.run(stage_addr + (k % KB) * BOX_BYTES, rep);
-    k = k_n;
-    rep = rep_n;
+    k = (uint32_t)ne.x;
+    rep = ne.y;
   }
   // release the remaining stages in order
   while (true) {
