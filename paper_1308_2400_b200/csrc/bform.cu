@@ -33,10 +33,10 @@
 //
 // Issue-slot budget: FADD2 and DADD occupy their pipe for 2 cycles per warp
 // instruction, so one non-FP instruction per FP instruction issues for free.
-// The entry path uses ALU/LSU instructions (SHF/LOP3, LDS, SHFL) and the rep
-// loop has no predicated FP tail (a predicated-off FADD2 still occupies the
-// pipe). The next entry's (k, rep) broadcast is issued before the current rep
-// loop so its shuffle latency is hidden. Wider tiles (G = 8: 1024 fp32
+// The entry path uses ALU/LSU instructions (SHF/LOP3, LDS, a uniform LDG) and
+// the rep loop has no predicated FP tail (a predicated-off FADD2 still
+// occupies the pipe). The next entry's (k, rep) load is issued before the
+// current rep loop so its latency is hidden. Wider tiles (G = 8: 1024 fp32
 // columns, 32 accumulators per lane) amortise the per-entry overhead over
 // twice the adds, which matters for small reps (tools/sweep.py).
 #include "common.cuh"
