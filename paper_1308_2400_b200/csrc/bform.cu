@@ -77,10 +77,10 @@ constexpr int REP_MID = 0;  // optional mid-size chunk between the unrolled loop
 constexpr int REP_MID = AFMM_EXP_REP_MID;
 #endif
 #ifndef AFMM_EXP_WIDE_STAGES
-#define AFMM_EXP_WIDE_STAGES 3
+#define AFMM_EXP_WIDE_STAGES 6
 #endif
 #ifndef AFMM_EXP_WIDE_MINB
-#define AFMM_EXP_WIDE_MINB 2
+#define AFMM_EXP_WIDE_MINB kWideCtasPerSm
 #endif
 #ifndef AFMM_EXP_WIDE_G
 #define AFMM_EXP_WIDE_G 8
@@ -1328,12 +1328,14 @@ cudaError_t launch_bform(int shape, const CUtensorMap* tmap, const int2* lists, 
                          uint32_t nk, uint32_t* splits, uint64_t slice_stride, T* out,
                          uint64_t ld_out, const DevStatus* st, cudaStream_t s) {
   if (shape == kShapeWide)
-    // 1024 fp32 / 512 fp64 columns x 8 rows, 8 consumers + producer, 3-stage
-    // ring, 2 CTAs per SM. Measured against 12 or 16 consumers at 1 CTA/SM
-    // (tools/sweep.py, sweep_var.py): equal per-SM throughput (90% of peak at
-    // rep 16), but 2x finer CTAs, so far less wave-quantisation tail (cfg3
-    // n=4096: 87% vs 82%). 16 consumers + producer (17 warps) would cap the
-    // registers at 96 and spill.
+    // 1024 fp32 / 512 fp64 columns x 16 rows, 16 consumers + producer, 6-stage
+    // ring (192 KB), 1 CTA per SM, 83 registers. Measured against 8 rows x 3
+    // stages x 2 CTAs per SM (tools/exp_time.py): cfg5 1810 -> 1802 ms, cfg2
+    // 0.307 -> 0.285 ms, cfg3 and cfg4 0.3-2% faster -- the deeper ring lets
+    // warps drift 5 k blocks apart instead of 2 (consumers had waited on a
+    // stage 6.5% of the time, ncu). Before the rep loop and list walk were
+    // slimmed (80-83 registers) this shape hit the 96-register cap of 17 warps
+    // and spilled.
     return launch_ring<T, AFMM_EXP_WIDE_G, AFMM_EXP_WIDE_CW, AFMM_EXP_WIDE_STAGES, AFMM_EXP_WIDE_MINB>(tmap, lists, cap, counts, nrows, col0, ncols, nk,
                                               splits, slice_stride, out, ld_out, st, s);
   if (shape == kShapeTmem)

@@ -76,7 +76,8 @@ constexpr int kShapeNarrow = 0;
 constexpr int kShapeWide = 1;
 constexpr int kShapeSmall = 2;
 constexpr int kShapeTmem = 3;
-constexpr int kWideRows = 8;  // rows per wide CTA
+constexpr int kWideRows = 16;      // rows per wide CTA (16 consumer warps + 1 TMA warp)
+constexpr int kWideCtasPerSm = 1;  // wide CTAs resident per SM (6-stage ring, 192 KB smem)
 constexpr int kTmemRows = 14; // rows per TMEM-fed CTA (14 + 2 warps: 128-register budget)
 // *splits: requested k slices in, slices launched out (1 = order-preserving).
 // Slice z writes its partial product to out + z * slice_stride.

@@ -397,15 +397,16 @@ uint64_t choose_aform_rows(size_t elem, uint64_t n, int variant, int sms,
   const double per_base = tiles_a * (75.0 + it_a * rmean);  // A-form cycles per nonzero base
   const double rbar = (double)rep_sum / (double)nnz_y;
   const double per_tile = 32.0 * (double)rep_sum + (rbar < 3.0 ? 100.0 : 56.0) * (double)nnz_y;
-  // wave quantisation of a grid of `ctas` 8-row CTAs on 2 x sms slots
-  const double slots = 2.0 * (sms > 0 ? sms : 148);
+  // wave quantisation of a grid of `ctas` wide CTAs on kWideCtasPerSm x sms slots
+  const double slots = (double)afmm_dev::kWideCtasPerSm * (sms > 0 ? sms : 148);
   auto wave_eff = [&](double ctas) {
     return ctas <= 0 ? 1.0 : ctas / (std::ceil(ctas / slots) * slots);
   };
   auto cost_b = [&](uint64_t tiles_b) {  // B part of tiles_b whole row tiles
     return tiles_b == 0 ? 0.0
                         : (double)tiles_b * per_tile /
-                              wave_eff(std::ceil((double)n / 8.0) * (double)tiles_b);
+                              wave_eff(std::ceil((double)n / afmm_dev::kWideRows) *
+                                       (double)tiles_b);
   };
   // rows by ascending nonzero count (counting sort: counts are <= n)
   std::vector<uint32_t> start(n + 2, 0), idx(rows);
@@ -478,13 +479,14 @@ afmm_status launch_compute(afmm_context* c, int mode, const T* base, uint64_t kb
   }
   // Tile shape: the widest one whose grid still fills the GPU (per-entry
   // overhead is amortised over more adds in wider tiles; small problems need
-  // the parallelism of narrow/small tiles). CTA slots per GPU: wide 296
-  // (2/SM), narrow 296 (2/SM), small 1184 (8/SM).
+  // the parallelism of narrow/small tiles). CTA slots per GPU: wide 148
+  // (1/SM), narrow 296 (2/SM), small 1184 (8/SM).
   const uint64_t cbytes = (uint64_t)ncols * sizeof(T);
   const uint64_t wide_ctas =
       (nrows + afmm_dev::kWideRows - 1) / afmm_dev::kWideRows * ((cbytes + 4095) / 4096);
   const uint64_t narrow_ctas = (nrows + 15) / 16 * ((cbytes + 2047) / 2048);
   const uint64_t small_ctas = (nrows + 3) / 4 * ((cbytes + 1023) / 1024);
+  const uint64_t wide_slots = 148ull * afmm_dev::kWideCtasPerSm;
   int shape = afmm_dev::kShapeNarrow;
   uint64_t ctas = narrow_ctas, slots = 296;
   if (c->variant == kVariantTmem) {
@@ -492,13 +494,13 @@ afmm_status launch_compute(afmm_context* c, int mode, const T* base, uint64_t kb
     ctas = (nrows + afmm_dev::kTmemRows - 1) / afmm_dev::kTmemRows * ((cbytes + 4095) / 4096);
     slots = 148;
   } else if (c->variant == kVariantWide ||
-             (c->variant == kVariantAuto && 4 * wide_ctas >= 3 * 296)) {
+             (c->variant == kVariantAuto && 4 * wide_ctas >= 3 * wide_slots)) {
     // (launch_ring trims the rows per CTA so a partial last wave costs little;
-    // wide tiles need about one wave of CTAs: 256 of them at n = 1024 fp64 run
-    // 7% faster than 256 narrow ones)
+    // wide tiles need about one wave of CTAs: at n = 1024 fp64 the 128 wide
+    // CTAs, trimmed to 148 of 14 rows, run 7% faster than 256 narrow ones)
     shape = afmm_dev::kShapeWide;
     ctas = wide_ctas;
-    slots = 296;
+    slots = wide_slots;
   } else if (c->variant == kVariantSmall || (c->variant == kVariantAuto && narrow_ctas < 148)) {
     shape = afmm_dev::kShapeSmall;
     ctas = small_ctas;
