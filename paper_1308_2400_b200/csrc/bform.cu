@@ -1365,15 +1365,17 @@ cudaError_t launch_aform(const CUtensorMap* cmap, const typename AEntry<T>::type
                          const uint32_t* row_idx, const DevStatus* st, cudaStream_t s) {
   using Ag = AformGeo<T>;
   static_assert(Ag::TILE == (int)aform_tile_cols<T>(), "A-form tile width");
-  constexpr int CW = kAformRows, STAGES = 6;
-  auto kern = k_aform<T, CW, STAGES, 2>;
+  // 16 rows x 12 stages x 1 CTA/SM: 4-5% faster than 8 rows x 6 stages x 2
+  // CTAs/SM on cfg3 d1 = 0.1 (tools/exp_time.py --aform)
+  constexpr int CW = kAformRows, STAGES = 12, MINB = kAformCtasPerSm;
+  auto kern = k_aform<T, CW, STAGES, MINB>;
   const size_t smem = 128 + (size_t)STAGES * Ag::STAGE_BYTES + 2 * STAGES * sizeof(uint64_t);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
   const uint32_t nkb = (nk + KB - 1) / KB;
   const uint32_t tiles = (ncols + Ag::TILE - 1) / Ag::TILE;
-  const uint32_t rpc = balanced_rows(nrows, tiles, CW, 2);
+  const uint32_t rpc = balanced_rows(nrows, tiles, CW, MINB);
   dim3 grid((nrows + rpc - 1) / rpc, tiles);
   kern<<<grid, (CW + 1) * 32, smem, s>>>(*cmap, lists, cap, counts, nrows, rpc, ncols, nkb, rmax,
                                          tiles, out, ld_out, row_idx, st);

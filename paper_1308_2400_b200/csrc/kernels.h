@@ -53,7 +53,8 @@ void launch_acompact(const T* x, uint64_t ld, uint32_t n, uint32_t r0, uint32_t 
 // Columns per A-form CTA tile (also the rmax tile width).
 template <class T>
 constexpr uint32_t aform_tile_cols() { return sizeof(T) == 4 ? 1024u : 512u; }
-constexpr int kAformRows = 8;  // rows (warps) per A-form CTA
+constexpr int kAformRows = 16;      // A-form CTA: 16 consumer warps + 1 TMA warp,
+constexpr int kAformCtasPerSm = 1;  // 12-stage fp16 count ring (192 KB), 1 CTA per SM  // rows (warps) per A-form CTA
 constexpr uint32_t kAformMaxRep = 2048;  // fp16 counts are exact up to here
 // Warp b computes Z row q = row_idx ? row_idx[b] : b (its list is lists row q,
 // its output out row q), b < nrows; cmap = fp16 count tensor map (box 256 x KB).

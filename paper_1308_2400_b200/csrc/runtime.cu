@@ -415,8 +415,11 @@ uint64_t choose_aform_rows(size_t elem, uint64_t n, int variant, int sms,
   for (uint64_t i = 0; i < rows; ++i) idx[start[std::min<uint64_t>(nnz[i], n)]++] = (uint32_t)i;
   std::vector<double> pre(rows + 1, 0.0);
   for (uint64_t i = 0; i < rows; ++i) pre[i + 1] = pre[i] + (double)nnz[idx[i]];
+  const double slots_a = (double)afmm_dev::kAformCtasPerSm * (sms > 0 ? sms : 148);
   auto cost_a = [&](uint64_t m) {  // A part of the m sparsest rows
-    return m == 0 ? 0.0 : per_base * pre[m] / wave_eff(std::ceil((double)m / 8.0) * tiles_a);
+    if (m == 0) return 0.0;
+    const double ctas = std::ceil((double)m / afmm_dev::kAformRows) * tiles_a;
+    return per_base * pre[m] / (ctas / (std::ceil(ctas / slots_a) * slots_a));
   };
   const uint64_t tb = (uint64_t)tile, tiles_all = (rows + tb - 1) / tb;
   const double pure_b = cost_b(tiles_all);
