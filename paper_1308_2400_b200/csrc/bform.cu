@@ -71,11 +71,6 @@ constexpr bool REP_BIN = AFMM_EXP_REP_BIN != 0;
 #endif
 static_assert(!REP_BIN || (REP_UNROLL & (REP_UNROLL - 1)) == 0,
               "a binary remainder needs a power-of-two unroll");
-#ifndef AFMM_EXP_REP_MID
-constexpr int REP_MID = 0;  // optional mid-size chunk between the unrolled loop and single steps
-#else
-constexpr int REP_MID = AFMM_EXP_REP_MID;
-#endif
 #ifndef AFMM_EXP_WIDE_STAGES
 #define AFMM_EXP_WIDE_STAGES 6
 #endif
@@ -264,15 +259,6 @@ struct Acc<float, G> {
         }
       return;
     }
-    if (REP_MID > 0 && t >= (uint32_t)REP_MID) {
-#pragma unroll
-      for (int u = 0; u < REP_MID; ++u)
-#pragma unroll
-        for (int c = 2 * G0; c < 2 * G1; ++c)
-          a[c] = __fadd2_rn(a[c], NEG ? make_float2(-b[c - 2 * G0].x, -b[c - 2 * G0].y)
-                                      : b[c - 2 * G0]);
-      t -= REP_MID;
-    }
 #pragma unroll 1
     while (t != 0) {
 #pragma unroll
@@ -390,14 +376,6 @@ struct Acc<double, G> {
               a[c] = __dadd_rn(a[c], NEG ? -b[c - 2 * G0] : b[c - 2 * G0]);
         }
       return;
-    }
-    if (REP_MID > 0 && t >= (uint32_t)REP_MID) {
-#pragma unroll
-      for (int u = 0; u < REP_MID; ++u)
-#pragma unroll
-        for (int c = 2 * G0; c < 2 * G1; ++c)
-          a[c] = __dadd_rn(a[c], NEG ? -b[c - 2 * G0] : b[c - 2 * G0]);
-      t -= REP_MID;
     }
 #pragma unroll 1
     while (t != 0) {
