@@ -430,12 +430,12 @@ struct Acc<double, G> {
 // column tiles: 256 CTAs on 296 slots; 14-row CTAs fill exactly one wave).
 // Keeps cw unless trimming gains more than 3%.
 inline uint32_t balanced_rows(uint32_t nrows, uint32_t tiles, uint32_t cw, uint32_t per_sm) {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);  // per call: contexts may drive GPUs of different sizes
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      sms <= 0) {
+    cudaGetLastError();
+    sms = 148;
   }
   const uint64_t slots = (uint64_t)sms * per_sm;
   auto cost = [&](uint32_t r) {
