@@ -399,6 +399,42 @@ def test_every_rep_magnitude_and_remainder(cuda, oracle, dt):
     assert res.counts.additions == expected_additions("b", lhs, rhs)
 
 
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("case", ["a", "b"])
+def test_subnormal_bases_are_not_flushed(cuda, oracle, dt, case, monkeypatch):
+    """Bases in the subnormal range, and sums that cross into and out of it:
+    every kernel form adds them without flush-to-zero (-ftz=false; FADD2/DADD
+    and the A-form's predicated adds), bit-exact against the oracle."""
+    tiny = np.finfo(dt).tiny  # smallest normal
+    n = 1100
+    rng = np.random.default_rng(77)
+    bases = (rng.integers(-40, 41, (n, n)) * (tiny / 64)).astype(dt)  # mostly subnormal
+    big = rng.random((n, n)) < 0.05
+    bases[big] = (rng.standard_normal(int(big.sum())) * tiny * 8).astype(dt)
+    reps = rng.integers(-9, 10, (n, n)).astype(dt)
+    lhs, rhs = (bases, reps) if case == "a" else (reps, bases)
+    assert np.count_nonzero((bases != 0) & (np.abs(bases) < tiny)) > n * n // 2
+    import torch
+
+    afmm = _api()
+    L = torch.from_numpy(lhs).cuda()
+    R = torch.from_numpy(rhs).cuda()
+    O = torch.empty_like(L)
+    rows = (0, 1, n // 3, n - 1)
+    want = {r: oracle.product_mt(case, lhs, rhs, r, r + 1, 1)[0] for r in rows}
+    forms = ["aform", "wide"] if case == "a" else ["wide", "small"]
+    for form in forms:
+        monkeypatch.setenv("AFMM_BFORM", form)
+        ctx = afmm.DeviceContext(0)  # reads AFMM_BFORM at creation
+        ctx.product(case, L, R, O)
+        z = O.cpu().numpy()
+        ctx.close()
+        for r in rows:
+            assert _bits_equal(z[r:r + 1], want[r]), (case, dt, form, r)
+        sub = z[(z != 0) & (np.abs(z) < tiny)]
+        assert sub.size > 0, "no subnormal results: the test lost its point"
+
+
 @pytest.mark.parametrize("case,n,dt", [("a", 3001, np.float32), ("b", 5003, np.float32),
                                         ("a", 1537, np.float64), ("b", 2049, np.float64)])
 def test_ragged_sizes_every_tile_shape(cuda, oracle, case, n, dt):
