@@ -401,6 +401,26 @@ def test_every_rep_magnitude_and_remainder(cuda, oracle, dt):
 
 @pytest.mark.parametrize("dt", [np.float32, np.float64])
 @pytest.mark.parametrize("case", ["a", "b"])
+def test_overflow_to_infinity_matches(cuda, oracle, dt, case):
+    """Bases near the top of the range: partial sums overflow to +inf / -inf and
+    stay there (a finite step never turns an infinity into NaN), exactly as the
+    reference's sequential adds do; bit-exact, counts unaffected."""
+    big = np.finfo(dt).max / 4
+    n = 700
+    rng = np.random.default_rng(5)
+    bases = (rng.choice([-1.0, 1.0], (n, n)) * rng.uniform(0.5, 1.0, (n, n)) * big).astype(dt)
+    bases[rng.random((n, n)) < 0.3] = 0
+    reps = rng.integers(-9, 10, (n, n)).astype(dt)
+    lhs, rhs = (bases, reps) if case == "a" else (reps, bases)
+    z, c, _ = oracle.product(case, lhs, rhs)
+    res = _call(case, lhs, rhs)
+    assert np.isinf(z).any() and not np.isnan(z).any()
+    assert (res.counts.additions, 0, res.counts.zero_skips) == c
+    assert _bits_equal(res.product, z)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("case", ["a", "b"])
 def test_subnormal_bases_are_not_flushed(cuda, oracle, dt, case, monkeypatch):
     """Bases in the subnormal range, and sums that cross into and out of it:
     every kernel form adds them without flush-to-zero (-ftz=false; FADD2/DADD
