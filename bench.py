@@ -250,7 +250,9 @@ def _config_dict(args, cfg):
          "case": cfg.case, "n": n,
          "mode": "order-preserving (bit-exact)" if args.mode == "order-preserving"
          else "fast (reassociated split-k, tolerance 1e-12 f64 / 1e-5 f32)",
-         "parallelism": f"row-partition x{args.gpus}",
+         "parallelism": f"row-partition x{args.gpus}" + (
+             " (one process per GPU, torchrun)" if int(os.environ.get("WORLD_SIZE", "1")) > 1
+             else " (one process, all GPUs)" if args.gpus > 1 else ""),
          "l2": "operands larger than L2" if n >= 4096 else "L2 flushed between steps"}
     if cfg.name == "cfg3":
         d["d1"] = args.d1
@@ -262,6 +264,12 @@ def _config_dict(args, cfg):
 # GPU arm
 # ---------------------------------------------------------------------------
 
+def refuse(why):
+    """No JSON line for a run that would not measure what it says."""
+    print(f"bench.py: refusing to report: {why}", file=sys.stderr, flush=True)
+    sys.exit(2)
+
+
 def main():
     args = parse_args()
     rank = int(os.environ.get("RANK", "0"))
@@ -269,6 +277,11 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference_arm(args, rank)
+        return
+    if world > 1 and args.gpus != world:
+        refuse(f"--gpus {args.gpus} under torchrun with WORLD_SIZE={world}")
+    if world == 1 and args.gpus > 1:
+        run_single_process(args)
         return
 
     import torch
@@ -423,6 +436,144 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_single_process(args):
+    """--gpus G without torchrun: one process drives G GPUs.
+
+    value: device-resident operands replicated on every GPU; the rows are cut
+    by predicted kernel time (afmm_row_cost_device) and each GPU's kernels
+    store its Z rows straight into GPU 0's Z over NVLink (peer access), all
+    enqueued asynchronously; the step time is the max over GPUs of CUDA events
+    on each GPU's stream.
+    e2e: the reference-facing C-ABI call with host buffers and
+    options.num_devices = G (afmm_case_*(..., devices=[0..G-1])): chunked H2D,
+    NVLink completion of Y, per-GPU products, Z rows straight to host."""
+    import torch
+
+    import paper_1308_2400_b200 as afmm
+    from paper_1308_2400_b200.afmm import RawRows
+    from paper_1308_2400_b200.gen import CONFIGS, make_inputs
+
+    G = args.gpus
+    # AFMM_SINGLE_DEVICE=1: functional test with every shard on cuda:0
+    # (tests/test_multirank_gpu.py), never a measurement
+    single = bool(os.environ.get("AFMM_SINGLE_DEVICE"))
+    dev = [0 if single else g for g in range(G)]
+    if not single and torch.cuda.device_count() < G:
+        refuse(f"--gpus {G} but only {torch.cuda.device_count()} CUDA devices are visible")
+    cfg = CONFIGS[args.config]
+    tdt = torch.float32 if cfg.dtype == "float32" else torch.float64
+    es = 4 if cfg.dtype == "float32" else 8
+    lhs, rhs = make_inputs(args.config, seed=args.seed, n=args.n, d1=args.d1, mu=args.mu)
+    n = lhs.shape[0]
+    Ls = [torch.from_numpy(lhs).to(f"cuda:{dev[g]}") for g in range(G)]
+    Rs = [torch.from_numpy(rhs).to(f"cuda:{dev[g]}") for g in range(G)]
+    Z = torch.empty((n, n), dtype=tdt, device="cuda:0")
+    ctxs = [afmm.DeviceContext(dev[g]) for g in range(G)]
+    for c in ctxs:
+        c.enable_timing(True)
+    peak, peak_mhz = afmm.fp_add_peak(0, cfg.dtype)
+    cost = ctxs[0].row_cost(cfg.case, Ls[0], Rs[0])
+    cuts = afmm.partition_rows(cost, G)
+    zrows = RawRows(Z.data_ptr(), Z.stride(0), cfg.dtype, n, n)
+    flush = [torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{d}")
+             for d in sorted(set(dev))] if n < 4096 else None
+    devices = sorted(set(dev))
+
+    def step():
+        for g in range(G):
+            r0, r1 = int(cuts[g]), int(cuts[g + 1])
+            with torch.cuda.device(dev[g]):
+                ctxs[g].product(cfg.case, Ls[g], Rs[g], zrows.rows(r0), r0, r1, sync=False,
+                                mode=args.mode)
+        return [c.finish() for c in ctxs]
+
+    for _ in range(args.warmup):
+        step()
+    for d in devices:
+        torch.cuda.synchronize(d)
+    sampler = ClockSampler(0)
+    sampler.start()
+    launches0 = afmm.kernel_launch_count()
+    total_ms = 0.0
+    kernel_ms = []
+    adds = 0
+    for _ in range(args.steps):
+        if flush is not None:
+            for f in flush:
+                f.fill_(1.0)
+        for d in devices:
+            torch.cuda.synchronize(d)
+        ev = []
+        for d in devices:
+            with torch.cuda.device(d):
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record()
+                ev.append((a, b))
+        counts = step()
+        for i, d in enumerate(devices):
+            with torch.cuda.device(d):
+                ev[i][1].record()
+        for d in devices:
+            torch.cuda.synchronize(d)
+        total_ms += max(a.elapsed_time(b) for a, b in ev)
+        kernel_ms.append(ctxs[0].last_timing()[1])
+        adds = sum(c.additions for c in counts)
+    launches = afmm.kernel_launch_count() - launches0
+    clocks = sampler.stop()
+    ms_per_step = total_ms / args.steps
+    value = adds / (ms_per_step * 1e-3)
+    kms = statistics.median(kernel_ms)
+    rank0_adds = int(counts[0].additions)
+    roofline = {
+        "bound": "fp-add", "kernel": "k_bform" if cfg.case == "b" else ctxs[0].last_form(),
+        "achieved": rank0_adds / (kms * 1e-3) / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
+        "unit_note": "FLOP = one FP add; GPU 0's repeated-addition kernel on its row share",
+        "frac": rank0_adds / (kms * 1e-3) / peak,
+        "peak_source": f"measured in-process by afmm_fp_add_peak at {peak_mhz:.0f} MHz",
+        "algorithmic_units_per_launch": rank0_adds, "kernel_ms": kms, "traffic": None,
+    }
+    e2e = None
+    if not args.no_e2e:
+        hl = torch.from_numpy(lhs).pin_memory()
+        hr = torch.from_numpy(rhs).pin_memory()
+        hz = torch.empty((n, n), dtype=hl.dtype).pin_memory()
+        fn = afmm.afmm_case_a if cfg.case == "a" else afmm.afmm_case_b
+        devs = dev
+        res = fn(hl.numpy(), hr.numpy(), out=hz.numpy(), mode=args.mode, devices=devs, timing=True)
+        reps = max(1, min(args.steps, 5))
+        t0 = time.perf_counter()
+        dev_ms = []
+        for _ in range(reps):
+            res = fn(hl.numpy(), hr.numpy(), out=hz.numpy(), mode=args.mode, devices=devs,
+                     timing=True)
+            dev_ms.append(res.timing["total_ms"])
+        secs = (time.perf_counter() - t0) / reps
+        e2e = {"value": res.counts.additions / secs, "unit": UNIT,
+               "h2d_bytes_per_step": 2 * n * n * es, "d2h_bytes_per_step": n * n * es,
+               "ms_per_step": secs * 1e3, "device_ms_per_step": statistics.median(dev_ms),
+               "steps": reps,
+               "api": f"afmm_case_{cfg.case}_{'f32' if es == 4 else 'f64'} (C ABI, host buffers, "
+                      f"options.num_devices={G})"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32" if es == 4 else "f64",
+        "data": "synthetic (seeded numpy PCG64, BASELINE.json distributions; no dataset)",
+        "config": dict(_config_dict(args, cfg), gather="in-kernel peer stores into GPU 0's Z "
+                                                       "(NVLink), no gather step",
+                       cuts=[int(c) for c in cuts],
+                       **({"test_mode": "AFMM_SINGLE_DEVICE: every shard on cuda:0, not a "
+                                        "measurement"} if single else {})),
+        "frac_of_fp_add_peak": value / (peak * G),
+        "roofline": roofline, "cpu_baseline": None, "e2e": e2e,
+        "gpu_launches": launches, "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    for c in ctxs:
+        c.close()
 
 
 def _e2e(args, afmm, dist, torch, world, rank, local, cfg, lhs, rhs, es, job_adds, sharded, L,

@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define AFMM_B200_ABI_VERSION 1
+#define AFMM_B200_ABI_VERSION 2
 
 typedef enum {
   AFMM_OK = 0,
@@ -40,7 +40,7 @@ typedef enum {
   AFMM_ERR_DOMAIN = 2,           /* std::domain_error (rep not integer / out of range / non-finite) */
   AFMM_ERR_INVALID_ARGUMENT = 3, /* std::invalid_argument (n == 0, bad option)          */
   AFMM_ERR_CUDA = 4,             /* CUDA runtime / driver failure, no device            */
-  AFMM_ERR_UNSUPPORTED = 5,      /* |rep| >= 2^31 (device loop-counter limit)           */
+  AFMM_ERR_UNSUPPORTED = 5,      /* n beyond the device index range (2^31 - 1)          */
   AFMM_ERR_OUT_OF_MEMORY = 6
 } afmm_status;
 
@@ -71,7 +71,7 @@ typedef enum {
   AFMM_ERRKIND_NON_FINITE = 3,    /* matrix.hpp:31-35 (DenseMatrix ctor) */
   AFMM_ERRKIND_SHAPE = 4,         /* kernels.hpp:15-21 */
   AFMM_ERRKIND_EMPTY = 5,         /* matrix.hpp:54-57 */
-  AFMM_ERRKIND_REP_TOO_LARGE = 6, /* device limit, no reference counterpart */
+  AFMM_ERRKIND_REP_TOO_LARGE = 6, /* unused since ABI 2: every |rep| <= 2^53 is accepted */
   AFMM_ERRKIND_OTHER = 7
 } afmm_error_kind;
 
@@ -84,14 +84,43 @@ typedef struct {
   char message[256]; /* the exact text the reference's exception would carry */
 } afmm_error;
 
+/* Device-measured phases of one reference-facing call (CUDA events on the
+ * call's streams; with several devices, the slowest device's figures). */
 typedef struct {
-  int32_t mode;      /* afmm_mode */
-  int32_t device;    /* CUDA device ordinal; -1 = current */
-  int32_t split_k;   /* fast mode only: 0 = auto */
+  float total_ms;    /* first host->device copy to the last device->host byte */
+  float compute_ms;  /* the repeated-addition kernel(s) */
+  int32_t devices;   /* devices the call ran on */
+  int32_t form;      /* Case A kernel form of device 0: 0 B-form, 1 A-form, 2 split */
+} afmm_timing;
+
+typedef enum {
+  /* contiguous Z row ranges of equal predicted kernel time: W_i (exact
+   * additions) for Case B, the Case A cost model (A-form / B-form) for Case A */
+  AFMM_PARTITION_WORK = 0,
+  AFMM_PARTITION_ROWS = 1 /* equal row counts */
+} afmm_partition;
+
+typedef struct {
+  int32_t mode;         /* afmm_mode; anything else is AFMM_ERR_INVALID_ARGUMENT */
+  int32_t device;       /* CUDA device ordinal; -1 = current (num_devices <= 1) */
+  int32_t split_k;      /* fast mode: upper bound on k slices (0 = automatic) */
+  int32_t num_devices;  /* G > 1: rows of Z sharded over G devices (0 or 1: one device) */
+  const int32_t* devices; /* G ordinals (NULL = 0..G-1); a device may repeat (two shards) */
+  int32_t partition;    /* afmm_partition */
   int32_t reserved;
+  afmm_timing* timing;  /* optional out: device-measured phases of this call */
 } afmm_options;
 
-/* ---- reference-facing entry points (host buffers) ------------------------ */
+/* ---- reference-facing entry points (host buffers) ------------------------
+ * One call = one product, host buffers in and out; `options` may be NULL
+ * (order-preserving, current device). With options->num_devices = G > 1 the
+ * rows of Z are sharded over G devices in one process (row i of Z depends only
+ * on row i of X and all of Y, kernels.hpp:119,148): each device receives an
+ * equal share of X's and Y's rows over PCIe, Y is completed over NVLink
+ * (peer copies), the prepass statistics choose work-balanced row cuts, each
+ * device copies the X rows of its cut it lacks from its peers and computes its
+ * Z rows, which go straight to `out`. Validation covers the whole operands
+ * before any Z element is written; results are bit-identical for every G. */
 
 afmm_status afmm_case_a_f64(const double* lhs, uint64_t n_lhs, const double* rhs, uint64_t n_rhs,
                             double* out, const afmm_options* options, afmm_op_counts* counts,
@@ -155,6 +184,16 @@ int32_t afmm_context_last_form(afmm_context* ctx);
 afmm_status afmm_row_work_device(afmm_context* ctx, int32_t which_case, int32_t dtype,
                                  const void* lhs, const void* rhs, uint64_t n, uint64_t ld,
                                  uint64_t* work, afmm_error* error);
+
+/* Predicted kernel time of each row (arbitrary units, for the row partition):
+ * Case B: W_i (the B-form's time is proportional to the additions); Case A:
+ * the cost model's time of the row in the cheaper of the A-form (proportional
+ * to its nonzero bases) and the B-form (a per-row share of a tile), so that
+ * rows of very different densities balance (afmm_partition_rows). Written to
+ * the host array cost[n]. */
+afmm_status afmm_row_cost_device(afmm_context* ctx, int32_t which_case, int32_t dtype,
+                                 const void* lhs, const void* rhs, uint64_t n, uint64_t ld,
+                                 uint64_t* cost, afmm_error* error);
 
 /* Cut n rows into `parts` contiguous ranges of (as near as possible) equal
  * total work: cuts[0] = 0, cuts[parts] = n, range p = [cuts[p], cuts[p+1]).

@@ -30,9 +30,15 @@ namespace afmm::gpu {
 
 enum class Mode { OrderPreserving = AFMM_MODE_ORDER_PRESERVING, Fast = AFMM_MODE_FAST };
 
+enum class Partition { Work = AFMM_PARTITION_WORK, Rows = AFMM_PARTITION_ROWS };
+
 struct Options {
   Mode mode = Mode::OrderPreserving;
-  int device = -1;  // -1: the calling thread's current CUDA device
+  int device = -1;           // -1: the calling thread's current CUDA device
+  std::vector<int> devices;  // > 1 entries: Z rows sharded over these devices (may repeat)
+  Partition partition = Partition::Work;  // row cuts: predicted time, or equal rows
+  int split_k = 0;           // fast mode: upper bound on k slices (0 = automatic)
+  afmm_timing* timing = nullptr;  // optional out: device-measured phases of the call
 };
 
 /// fp32 storage for BASELINE configs 3-5 (the reference has no fp32 type,
@@ -62,17 +68,27 @@ inline void throw_for(afmm_status status, const afmm_error& err) {
     case AFMM_OK: return;
     case AFMM_ERR_SHAPE: throw shape_error(msg);
     case AFMM_ERR_DOMAIN: throw std::domain_error(msg);
-    case AFMM_ERR_UNSUPPORTED: throw std::domain_error(msg);
+    case AFMM_ERR_UNSUPPORTED: throw std::length_error(msg);  // n beyond the device index range
     case AFMM_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
     case AFMM_ERR_OUT_OF_MEMORY: throw std::bad_alloc();
     default: throw std::runtime_error(msg.empty() ? "afmm: CUDA failure" : msg);
   }
 }
 
-inline afmm_options to_c(Options o) {
+static_assert(sizeof(int) == sizeof(int32_t), "device ordinals are passed as int32_t");
+
+// (the returned struct points into o.devices: keep `o` alive for the call)
+inline afmm_options to_c(const Options& o) {
   afmm_options c{};
   c.mode = static_cast<int32_t>(o.mode);
   c.device = o.device;
+  c.split_k = o.split_k;
+  c.partition = static_cast<int32_t>(o.partition);
+  c.timing = o.timing;
+  if (!o.devices.empty()) {
+    c.num_devices = static_cast<int32_t>(o.devices.size());
+    c.devices = reinterpret_cast<const int32_t*>(o.devices.data());
+  }
   return c;
 }
 
@@ -90,7 +106,7 @@ using FnF32 = afmm_status (*)(const float*, uint64_t, const float*, uint64_t, fl
                               const afmm_options*, afmm_op_counts*, afmm_error*);
 
 inline MultiplyResult run_f64(FnF64 fn, const DenseMatrix& lhs, const DenseMatrix& rhs,
-                              Options opt) {
+                              const Options& opt) {
   // The result buffer is allocated only once the dimensions are known to be
   // valid, so a mismatch reports shape_error exactly like kernels.hpp:114/143.
   // The C ABI checks dimensions before touching `out`, so an invalid call
@@ -108,7 +124,7 @@ inline MultiplyResult run_f64(FnF64 fn, const DenseMatrix& lhs, const DenseMatri
 }
 
 inline MultiplyResultF32 run_f32(FnF32 fn, const DenseMatrixF32& lhs, const DenseMatrixF32& rhs,
-                                 Options opt) {
+                                 const Options& opt) {
   const bool valid = lhs.dim() == rhs.dim() && lhs.dim() > 0;
   MultiplyResultF32 r;
   if (valid) r.product = DenseMatrixF32(lhs.dim());

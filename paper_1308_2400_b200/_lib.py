@@ -14,6 +14,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # AFMM_LIB overrides the in-tree library (kernel experiments built under build/).
 LIB_PATH = os.environ.get("AFMM_LIB") or os.path.join(_HERE, "libafmm_b200.so")
 
+ABI_VERSION = 2
+
 # afmm_status
 OK = 0
 ERR_SHAPE = 1
@@ -37,7 +39,7 @@ ERRKIND_OUT_OF_RANGE = 2
 ERRKIND_NON_FINITE = 3
 ERRKIND_SHAPE = 4
 ERRKIND_EMPTY = 5
-ERRKIND_REP_TOO_LARGE = 6
+ERRKIND_REP_TOO_LARGE = 6  # unused since ABI 2
 ERRKIND_OTHER = 7
 
 
@@ -65,8 +67,23 @@ class IpcHandle(ctypes.Structure):
     _fields_ = [("bytes", ctypes.c_uint8 * 64), ("offset", c_uint64)]
 
 
+class Timing(ctypes.Structure):
+    """afmm_timing: device-measured phases of one host-buffer call."""
+
+    _fields_ = [("total_ms", ctypes.c_float), ("compute_ms", ctypes.c_float),
+                ("devices", c_int32), ("form", c_int32)]
+
+
+PARTITION_WORK = 0
+PARTITION_ROWS = 1
+
+
 class Options(ctypes.Structure):
-    _fields_ = [("mode", c_int32), ("device", c_int32), ("split_k", c_int32), ("reserved", c_int32)]
+    """afmm_options (ABI 2)."""
+
+    _fields_ = [("mode", c_int32), ("device", c_int32), ("split_k", c_int32),
+                ("num_devices", c_int32), ("devices", POINTER(c_int32)), ("partition", c_int32),
+                ("reserved", c_int32), ("timing", POINTER(Timing))]
 
 
 # Every symbol include/afmm_b200.h declares, with its ctypes signature.
@@ -93,6 +110,8 @@ _SIGNATURES = {
     "afmm_context_last_form": (c_int32, [c_void_p]),
     "afmm_row_work_device": (c_int32, [c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_uint64,
                                        c_uint64, POINTER(c_uint64), POINTER(Error)]),
+    "afmm_row_cost_device": (c_int32, [c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_uint64,
+                                       c_uint64, POINTER(c_uint64), POINTER(Error)]),
     "afmm_partition_rows": (c_int32, [POINTER(c_uint64), c_uint64, c_uint32, POINTER(c_uint64)]),
     "afmm_fp_add_peak": (c_int32, [c_int32, c_int32, POINTER(c_double), POINTER(c_double)]),
     "afmm_ipc_export": (c_int32, [c_void_p, POINTER(IpcHandle), POINTER(Error)]),
@@ -118,6 +137,9 @@ def load() -> ctypes.CDLL:
             f"libafmm_b200.so not found at {LIB_PATH}: build it with `make` or "
             "`python -c 'import __graft_entry__ as g; g.build()'` (there is no CPU fallback)")
     lib = ctypes.CDLL(LIB_PATH)
+    if lib.afmm_abi_version() != ABI_VERSION:
+        raise RuntimeError(f"{LIB_PATH}: ABI {lib.afmm_abi_version()}, this binding expects "
+                           f"{ABI_VERSION} (rebuild with `make`)")
     for name, (res, args) in _SIGNATURES.items():
         fn = getattr(lib, name)
         fn.restype = res

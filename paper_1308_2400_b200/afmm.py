@@ -20,7 +20,7 @@ from __future__ import annotations
 
 import ctypes
 from dataclasses import dataclass
-from typing import Optional, Tuple
+from typing import Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -43,9 +43,10 @@ class InvalidArgument(ValueError):
     """std::invalid_argument: empty matrix or invalid option."""
 
 
-class UnsupportedError(DomainError):
-    """A rep magnitude at or above 2^31 (device loop-counter limit; the reference
-    would run 2^31+ sequential adds per element)."""
+class UnsupportedError(InvalidArgument):
+    """n beyond the device index range (2^31 - 1). (Every rep the reference
+    accepts, |rep| <= 2^53, is accepted: a rep beyond one list entry's range is
+    split into consecutive entries at the same k.)"""
 
 
 class DeviceError(RuntimeError):
@@ -63,10 +64,11 @@ class OpCounts:
 
 @dataclass
 class MultiplyResult:
-    """op_counts.hpp:30-33"""
+    """op_counts.hpp:30-33 (+ the device timing of the call when requested)"""
 
     product: np.ndarray
     counts: OpCounts
+    timing: Optional[dict] = None
 
 
 def _raise_for(status: int, err: _lib.Error) -> None:
@@ -86,10 +88,33 @@ def _raise_for(status: int, err: _lib.Error) -> None:
     raise DeviceError(msg)
 
 
-def _options(mode: str, device: Optional[int]) -> _lib.Options:
+_PARTITIONS = {"work": _lib.PARTITION_WORK, "rows": _lib.PARTITION_ROWS}
+
+
+def _options(mode: str, device: Optional[int], devices: Optional[Sequence[int]] = None,
+             partition: str = "work", split_k: int = 0,
+             timing: Optional[_lib.Timing] = None) -> Tuple[_lib.Options, object]:
+    """afmm_options + the ctypes objects it points to (kept alive by the caller)."""
     if mode not in _MODES:
         raise InvalidArgument(f"afmm: unknown mode {mode!r}")
-    return _lib.Options(_MODES[mode], -1 if device is None else int(device), 0, 0)
+    if partition not in _PARTITIONS:
+        raise InvalidArgument(f"afmm: unknown partition {partition!r}")
+    o = _lib.Options()
+    o.mode = _MODES[mode]
+    o.device = -1 if device is None else int(device)
+    o.split_k = int(split_k)
+    o.partition = _PARTITIONS[partition]
+    keep = None
+    if devices is not None:
+        devs = [int(d) for d in devices]
+        if not devs:
+            raise InvalidArgument("afmm: devices must not be empty")
+        keep = (ctypes.c_int32 * len(devs))(*devs)
+        o.num_devices = len(devs)
+        o.devices = ctypes.cast(keep, ctypes.POINTER(ctypes.c_int32))
+    if timing is not None:
+        o.timing = ctypes.pointer(timing)
+    return o, keep
 
 
 def _as_square(m, name: str) -> np.ndarray:
@@ -112,7 +137,8 @@ def _common_dtype(lhs: np.ndarray, rhs: np.ndarray, dtype) -> np.dtype:
 
 
 def _product(which: int, lhs, rhs, mode: str, device: Optional[int], dtype,
-             out: Optional[np.ndarray]) -> MultiplyResult:
+             out: Optional[np.ndarray], devices=None, partition: str = "work",
+             split_k: int = 0, timing: bool = False) -> MultiplyResult:
     lib = _lib.load()
     l = _as_square(lhs, "lhs")
     r = _as_square(rhs, "rhs")
@@ -126,7 +152,8 @@ def _product(which: int, lhs, rhs, mode: str, device: Optional[int], dtype,
         raise InvalidArgument("afmm: out must be a C-contiguous n x n array of the operand dtype")
     counts = _lib.OpCounts()
     err = _lib.Error()
-    opts = _options(mode, device)
+    tm = _lib.Timing() if timing else None
+    opts, _keep = _options(mode, device, devices, partition, split_k, tm)
     fn = {
         (_lib.CASE_A, np.float64): lib.afmm_case_a_f64,
         (_lib.CASE_B, np.float64): lib.afmm_case_b_f64,
@@ -136,19 +163,33 @@ def _product(which: int, lhs, rhs, mode: str, device: Optional[int], dtype,
     status = fn(l.ctypes.data, l.shape[0], r.ctypes.data, r.shape[0], out.ctypes.data,
                 ctypes.byref(opts), ctypes.byref(counts), ctypes.byref(err))
     _raise_for(status, err)
-    return MultiplyResult(out, OpCounts(*counts.as_tuple()))
+    t = None
+    if tm is not None:
+        t = {"total_ms": tm.total_ms, "compute_ms": tm.compute_ms, "devices": tm.devices,
+             "form": {1: "aform", 2: "split"}.get(tm.form, "bform")}
+    return MultiplyResult(out, OpCounts(*counts.as_tuple()), t)
 
 
 def afmm_case_a(lhs, rhs, *, mode: str = ORDER_PRESERVING, device: Optional[int] = None,
-                dtype=None, out: Optional[np.ndarray] = None) -> MultiplyResult:
-    """AFMM Case A on the GPU: real lhs bases, integer-valued rhs reps (kernels.hpp:113-136)."""
-    return _product(_lib.CASE_A, lhs, rhs, mode, device, dtype, out)
+                dtype=None, out: Optional[np.ndarray] = None, devices=None,
+                partition: str = "work", split_k: int = 0, timing: bool = False) -> MultiplyResult:
+    """AFMM Case A on the GPU: real lhs bases, integer-valued rhs reps (kernels.hpp:113-136).
+
+    devices=[d0, d1, ...] shards the rows of Z over several GPUs in this
+    process (a device may repeat); partition="work" balances predicted kernel
+    time, "rows" cuts equal row counts. timing=True adds the device-measured
+    phases of the call to the result."""
+    return _product(_lib.CASE_A, lhs, rhs, mode, device, dtype, out, devices, partition, split_k,
+                    timing)
 
 
 def afmm_case_b(lhs, rhs, *, mode: str = ORDER_PRESERVING, device: Optional[int] = None,
-                dtype=None, out: Optional[np.ndarray] = None) -> MultiplyResult:
-    """AFMM Case B on the GPU: integer-valued lhs reps, real rhs bases (kernels.hpp:142-165)."""
-    return _product(_lib.CASE_B, lhs, rhs, mode, device, dtype, out)
+                dtype=None, out: Optional[np.ndarray] = None, devices=None,
+                partition: str = "work", split_k: int = 0, timing: bool = False) -> MultiplyResult:
+    """AFMM Case B on the GPU: integer-valued lhs reps, real rhs bases (kernels.hpp:142-165).
+    Multi-GPU and timing options as in afmm_case_a."""
+    return _product(_lib.CASE_B, lhs, rhs, mode, device, dtype, out, devices, partition, split_k,
+                    timing)
 
 
 # ---- device-resident API ------------------------------------------------------
@@ -160,19 +201,27 @@ class RawRows:
     """Row-major device rows addressed by a raw pointer (e.g. another GPU's
     buffer opened with ipc_open): usable as `out` of DeviceContext.product."""
 
-    def __init__(self, ptr: int, ld: int, dtype: str, ncols: int):
+    def __init__(self, ptr: int, ld: int, dtype: str, ncols: int, nrows: Optional[int] = None):
         self.ptr, self.ld, self.dtype, self.ncols = int(ptr), int(ld), dtype, int(ncols)
+        self.nrows = nrows  # None: unknown (the caller vouches for the extent)
 
     def rows(self, r0: int) -> "RawRows":
         """The view starting at row r0."""
         es = 4 if self.dtype == "float32" else 8
-        return RawRows(self.ptr + r0 * self.ld * es, self.ld, self.dtype, self.ncols)
+        return RawRows(self.ptr + r0 * self.ld * es, self.ld, self.dtype, self.ncols,
+                       None if self.nrows is None else self.nrows - r0)
 
 
-def _tensor_info(t) -> Tuple[int, int, str, int]:
-    """(data_ptr, leading dimension, dtype name, n) of a 2D row-major CUDA tensor."""
+def _tensor_info(t, device: Optional[int] = None, what: str = "operand") -> Tuple[int, int, str, int]:
+    """(data_ptr, leading dimension, dtype name, ncols) of a 2D row-major CUDA
+    tensor on `device` (or a RawRows view)."""
     if isinstance(t, RawRows):
         return t.ptr, t.ld, t.dtype, t.ncols
+    if not getattr(t, "is_cuda", False):
+        raise InvalidArgument(f"afmm: {what} must be a CUDA tensor (device-resident API)")
+    if device is not None and t.device.index != device:
+        raise InvalidArgument(f"afmm: {what} is on cuda:{t.device.index}, the context on "
+                              f"cuda:{device}")
     if t.dim() != 2 or t.stride(1) != 1:
         raise InvalidArgument("afmm: device operands must be 2D with unit column stride")
     name = str(t.dtype).replace("torch.", "")
@@ -206,27 +255,53 @@ class DeviceContext:
             pass
 
     def set_stream(self, stream) -> None:
+        """Bind the context to a CUDA stream (a torch.cuda.Stream or a raw
+        handle); until then every call runs on torch's current stream."""
         handle = getattr(stream, "cuda_stream", stream)
-        self._lib.afmm_context_set_stream(self._h, ctypes.c_void_p(int(handle or 0)))
+        self._bind(int(handle or 0))
+        self._explicit_stream = True
+
+    def _bind(self, handle: int) -> None:
+        if handle != getattr(self, "_bound", None):
+            st = self._lib.afmm_context_set_stream(self._h, ctypes.c_void_p(handle))
+            if st != _lib.OK:
+                raise DeviceError(f"afmm_context_set_stream: {_lib.status_string(st)}")
+            self._bound = handle
+
+    def _follow_torch_stream(self) -> None:
+        if not getattr(self, "_explicit_stream", False):
+            import torch
+
+            self._bind(int(torch.cuda.current_stream(self.device).cuda_stream))
 
     def product(self, which: str, lhs, rhs, out, row_begin: int = 0,
                 row_end: Optional[int] = None, *, sync: bool = True,
-                mode: str = ORDER_PRESERVING) -> Optional[OpCounts]:
-        """Rows [row_begin, row_end) of Z into `out` (device tensors, row-major)."""
-        lp, ld, dname, n = _tensor_info(lhs)
-        rp, ld_r, dname_r, n_r = _tensor_info(rhs)
+                mode: str = ORDER_PRESERVING, split_k: int = 0) -> Optional[OpCounts]:
+        """Rows [row_begin, row_end) of Z into `out` (device tensors on this
+        context's device, row-major; `out` row r holds Z row row_begin + r)."""
+        lp, ld, dname, n = _tensor_info(lhs, self.device, "lhs")
+        rp, ld_r, dname_r, n_r = _tensor_info(rhs, self.device, "rhs")
         if dname_r != dname or ld_r != ld or lhs.shape[0] != n or rhs.shape != lhs.shape:
             raise ShapeError(f"afmm_case_{which}: dimension mismatch {n} vs {n_r}")
         row_end = n if row_end is None else int(row_end)
-        op, ld_out, dname_o, _ = _tensor_info(out)
+        row_begin = int(row_begin)
+        if not 0 <= row_begin <= row_end <= n:
+            raise InvalidArgument(f"afmm: rows [{row_begin}, {row_end}) outside [0, {n})")
+        op, ld_out, dname_o, ncols_o = _tensor_info(out, self.device, "out")
         if dname_o != dname:
             raise InvalidArgument("afmm: out dtype differs from the operands")
+        rows_o = out.nrows if isinstance(out, RawRows) else out.shape[0]
+        if row_end > row_begin and (ncols_o < n or (rows_o is not None and
+                                                    rows_o < row_end - row_begin)):
+            raise InvalidArgument(f"afmm: out holds {rows_o} x {ncols_o}, the slab needs "
+                                  f"{row_end - row_begin} x {n}")
+        self._follow_torch_stream()
         counts = _lib.OpCounts()
         err = _lib.Error()
-        opts = _options(mode, self.device)
+        opts, _ = _options(mode, self.device, split_k=split_k)
         status = self._lib.afmm_product_device(
             self._h, _lib.CASE_A if which == "a" else _lib.CASE_B, _DT_CODE[dname], lp, rp, n, ld,
-            op, ld_out, int(row_begin), row_end, ctypes.byref(opts), 1 if sync else 0,
+            op, ld_out, row_begin, row_end, ctypes.byref(opts), 1 if sync else 0,
             ctypes.byref(counts), ctypes.byref(err))
         _raise_for(status, err)
         return OpCounts(*counts.as_tuple()) if sync else None
@@ -253,16 +328,25 @@ class DeviceContext:
                    err)
         return OpCounts(*counts.as_tuple())
 
-    def row_work(self, which: str, lhs, rhs) -> np.ndarray:
-        lp, ld, dname, n = _tensor_info(lhs)
-        rp, _, _, _ = _tensor_info(rhs)
-        work = np.zeros(n, dtype=np.uint64)
+    def _row_query(self, fn, which: str, lhs, rhs) -> np.ndarray:
+        lp, ld, dname, n = _tensor_info(lhs, self.device, "lhs")
+        rp, _, _, _ = _tensor_info(rhs, self.device, "rhs")
+        self._follow_torch_stream()
+        out = np.zeros(n, dtype=np.uint64)
         err = _lib.Error()
-        status = self._lib.afmm_row_work_device(
-            self._h, _lib.CASE_A if which == "a" else _lib.CASE_B, _DT_CODE[dname], lp, rp, n, ld,
-            work.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), ctypes.byref(err))
+        status = fn(self._h, _lib.CASE_A if which == "a" else _lib.CASE_B, _DT_CODE[dname], lp, rp,
+                    n, ld, out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), ctypes.byref(err))
         _raise_for(status, err)
-        return work
+        return out
+
+    def row_work(self, which: str, lhs, rhs) -> np.ndarray:
+        """W_i: exact additions of each Z row (afmm_row_work_device)."""
+        return self._row_query(self._lib.afmm_row_work_device, which, lhs, rhs)
+
+    def row_cost(self, which: str, lhs, rhs) -> np.ndarray:
+        """Predicted kernel time of each Z row (afmm_row_cost_device): W_i for
+        Case B, the Case A cost model (cheaper of A-form and B-form) for Case A."""
+        return self._row_query(self._lib.afmm_row_cost_device, which, lhs, rhs)
 
 
 def partition_rows(work, parts: int) -> np.ndarray:

@@ -9,9 +9,10 @@
 // same per-element add sequence). "A-form" (k_aform, below) is
 // Case A in its own orientation, base uniform per warp, for sparse X.
 //
-// Contents: k_bform (the product kernel, three tile shapes), k_bform_tm
-// (opt-in TMEM-fed variant), k_aform (A-form), k_bform_mr (opt-in dense-rep
-// multi-row variant), and their launchers.
+// Contents: k_bform (the product kernel, three tile shapes), k_aform
+// (A-form) and their launchers. (Variants measured slower in round 1 -- a
+// TMEM-fed B-form and a dense-rep multi-row kernel -- were removed from the
+// library; DESIGN.md section 3.3 keeps their measurements.)
 //
 // k_bform (one CTA = CW consumer warps, each owning one output row, + 1 TMA
 // producer warp):
@@ -48,12 +49,7 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-#ifndef AFMM_EXP_KB
 constexpr int KB = 8;  // k rows per stage
-#else
-constexpr int KB = AFMM_EXP_KB;  // timing experiments (Makefile exp-%)
-#endif
-#ifndef AFMM_EXP_REP_UNROLL
 // rep loop: trips of 8 steps, then the remainder (< 8) by its binary digits
 // (4, 2, 1 steps) with no loop. Measured against 4-step trips + a 1-step
 // remainder loop: cfg5 1845 -> 1809 ms, rep 16 0.901 -> 0.912 of peak, and 88
@@ -61,41 +57,8 @@ constexpr int KB = AFMM_EXP_KB;  // timing experiments (Makefile exp-%)
 // back-edge instructions it removes issue on the FMA pipe (VIADD) or stall on
 // branch resolution.
 constexpr int REP_UNROLL = 8;  // rep-loop unroll (adds per column per trip)
-#else
-constexpr int REP_UNROLL = AFMM_EXP_REP_UNROLL;
-#endif
-#ifndef AFMM_EXP_REP_BIN
-constexpr bool REP_BIN = true;  // remainder by binary digits instead of a loop
-#else
-constexpr bool REP_BIN = AFMM_EXP_REP_BIN != 0;
-#endif
-static_assert(!REP_BIN || (REP_UNROLL & (REP_UNROLL - 1)) == 0,
-              "a binary remainder needs a power-of-two unroll");
-#ifndef AFMM_EXP_WIDE_STAGES
-#define AFMM_EXP_WIDE_STAGES 6
-#endif
-#ifndef AFMM_EXP_WIDE_MINB
-#define AFMM_EXP_WIDE_MINB kWideCtasPerSm
-#endif
-#ifndef AFMM_EXP_WIDE_G
-#define AFMM_EXP_WIDE_G 8
-#endif
-#ifndef AFMM_EXP_WIDE_CW
-#define AFMM_EXP_WIDE_CW kWideRows
-#endif
-// Producer-less ring (experiment): no TMA warp; the consumer warp that
-// releases a stage last refills it (smem counter per slot), so 16 consumer
-// warps per SM get the 128-register budget of 16 warps.
-#ifndef AFMM_EXP_NOPROD
-#define AFMM_EXP_NOPROD 0
-#endif
-constexpr bool kNoProd = AFMM_EXP_NOPROD != 0;
+static_assert((REP_UNROLL & (REP_UNROLL - 1)) == 0, "a binary remainder needs a power-of-two unroll");
 constexpr uint32_t kListPrefetch = 64;  // list entries ahead prefetched into L1
-constexpr int kProdWarps = kNoProd ? 0 : 1;
-
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
 
 // A TMA box is at most 256 elements wide, so a stage is G/2 boxes of
 // KB x BOX_BYTES laid out box-major: [box][k row][BOX_BYTES].
@@ -134,291 +97,117 @@ __device__ __forceinline__ double2 lds128d(uint32_t addr) {
 // (g>>1)*KB*BOX_BYTES + (g&1)*512 + l*16 of each staged k row: every 128-bit
 // LDS across the warp reads 512 contiguous bytes (no bank conflict). In
 // output columns that is tile_col + g*128 + 4l (fp32) / g*64 + 2l (fp64).
-// ---- tensor memory (TMEM) ---------------------------------------------------
 
-// 32 lanes x 32 columns of 32-bit words -> 32 registers per thread (lane t of
-// the warp's TMEM lane quadrant, 32 consecutive columns), then wait.
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n\t"
-      "tcgen05.wait::ld.sync.aligned;"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
-        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
-        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr)
-      : "memory");
-}
-
-__device__ __forceinline__ void tmem_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tmem_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-
-// smem -> TMEM copy of a 32-row x 16-byte matrix, replicated into all four
-// 32-lane quadrants (row r -> lane r of every quadrant, 4 columns).
-__device__ __forceinline__ void tmem_cp_32x128b_x4(uint32_t taddr, uint64_t desc) {
-  asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(desc)
-               : "memory");
-}
-
-// Arrive on an mbarrier once all previously issued tcgen05 async operations of
-// this thread (here: the copies) have completed.
-__device__ __forceinline__ void tmem_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   bar)
-               : "memory");
-}
-
-// tcgen05 shared-memory matrix descriptor, no swizzle: 8-row x 16-byte core
-// matrices stored contiguously (128 B apart), version 1 (sm_100).
-__device__ __forceinline__ uint64_t smem_desc_128(uint32_t saddr) {
-  const uint64_t start = (saddr >> 4) & 0x3fffu;
-  const uint64_t lbo = 128u >> 4, sbo = 128u >> 4;
-  return start | (lbo << 16) | (sbo << 32) | (1ull << 46);
-}
-
-template <class T, int G>
-struct Acc;
-
-template <int G>
-struct Acc<float, G> {
-  struct Bases {
-    float2 b[2 * G];
-  };
-  float2 a[2 * G];
-  __device__ __forceinline__ void zero() {
-#pragma unroll
-    for (int c = 0; c < 2 * G; ++c) a[c] = make_float2(0.f, 0.f);
-  }
-  __device__ __forceinline__ static Bases load_bases(uint32_t row_addr) {
-    Bases s;
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const float4 v = lds128f(row_addr + group_off(g));
-      s.b[2 * g] = make_float2(v.x, v.y);
-      s.b[2 * g + 1] = make_float2(v.z, v.w);
-    }
-    return s;
-  }
-  // t sequential `acc += step` per column; NEG: step = -base (kernels.hpp:97),
-  // applied as the FADD2 operand-negate modifier (exact), so the shared bases
-  // are never copied or rewritten.
+// One FP-add operand: a float2 (FADD2, two fp32 columns) or a double (DADD).
+template <class T>
+struct Lane;
+template <>
+struct Lane<float> {
+  using V = float2;
+  __device__ __forceinline__ static V zero() { return make_float2(0.f, 0.f); }
   template <bool NEG>
-  __device__ __forceinline__ void add_n(const Bases& s, uint32_t t) {
-#pragma unroll 1
-    while (t >= 4) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int c = 0; c < 2 * G; ++c)
-          a[c] = __fadd2_rn(a[c], NEG ? make_float2(-s.b[c].x, -s.b[c].y) : s.b[c]);
-      t -= 4;
-    }
-#pragma unroll 1
-    while (t != 0) {
-#pragma unroll
-      for (int c = 0; c < 2 * G; ++c)
-        a[c] = __fadd2_rn(a[c], NEG ? make_float2(-s.b[c].x, -s.b[c].y) : s.b[c]);
-      t -= 1;
-    }
+  __device__ __forceinline__ static V add(V a, V b) {
+    // the negation is the FADD2 operand-negate modifier (exact)
+    return __fadd2_rn(a, NEG ? make_float2(-b.x, -b.y) : b);
   }
-  // |rep| sequential `acc += step` per column, step = rep >= 0 ? base : -base
-  // (kernels.hpp:95-104).
-  __device__ __forceinline__ void add(const Bases& s, int rep) {
-    if (rep >= 0) add_n<false>(s, (uint32_t)rep);
-    else add_n<true>(s, 0u - (uint32_t)rep);
+  __device__ __forceinline__ static void load(uint32_t addr, V* b) {
+    const float4 v = lds128f(addr);
+    b[0] = make_float2(v.x, v.y);
+    b[1] = make_float2(v.z, v.w);
   }
-  // The same on column groups [G0, G1) only, with just those bases live.
-  template <bool NEG, int G0, int G1>
-  __device__ __forceinline__ void add_range(const float2* b, uint32_t t) {
-#pragma unroll 1
-    while (t >= REP_UNROLL) {
-#pragma unroll
-      for (int u = 0; u < REP_UNROLL; ++u)
-#pragma unroll
-        for (int c = 2 * G0; c < 2 * G1; ++c)
-          a[c] = __fadd2_rn(a[c], NEG ? make_float2(-b[c - 2 * G0].x, -b[c - 2 * G0].y)
-                                      : b[c - 2 * G0]);
-      t -= REP_UNROLL;
-    }
-    if (REP_BIN) {  // remainder t < REP_UNROLL by its binary digits, no loop
-#pragma unroll
-      for (int bit = REP_UNROLL / 2; bit >= 1; bit >>= 1)
-        if (t & (uint32_t)bit) {
-#pragma unroll
-          for (int u = 0; u < bit; ++u)
-#pragma unroll
-            for (int c = 2 * G0; c < 2 * G1; ++c)
-              a[c] = __fadd2_rn(a[c], NEG ? make_float2(-b[c - 2 * G0].x, -b[c - 2 * G0].y)
-                                          : b[c - 2 * G0]);
-        }
-      return;
-    }
-#pragma unroll 1
-    while (t != 0) {
-#pragma unroll
-      for (int c = 2 * G0; c < 2 * G1; ++c)
-        a[c] = __fadd2_rn(a[c], NEG ? make_float2(-b[c - 2 * G0].x, -b[c - 2 * G0].y)
-                                    : b[c - 2 * G0]);
-      t -= 1;
-    }
+};
+template <>
+struct Lane<double> {
+  using V = double;
+  __device__ __forceinline__ static V zero() { return 0.0; }
+  template <bool NEG>
+  __device__ __forceinline__ static V add(V a, V b) {
+    return __dadd_rn(a, NEG ? -b : b);
   }
-  template <int G0, int G1>
-  __device__ __forceinline__ void run_range(uint32_t row_addr, int rep) {
-    float2 b[2 * (G1 - G0)];
-#pragma unroll
-    for (int g = G0; g < G1; ++g) {
-      const float4 v = lds128f(row_addr + group_off(g));
-      b[2 * (g - G0)] = make_float2(v.x, v.y);
-      b[2 * (g - G0) + 1] = make_float2(v.z, v.w);
-    }
-    if (rep >= 0) add_range<false, G0, G1>(b, (uint32_t)rep);
-    else add_range<true, G0, G1>(b, 0u - (uint32_t)rep);
-  }
-  // One list entry, all G column groups in one rep loop. (Splitting wide tiles
-  // into two half-width loops to save 16 base registers was measured 3% slower.)
-  __device__ __forceinline__ void run(uint32_t row_addr, int rep) { run_range<0, G>(row_addr, rep); }
-  // The same entry with the bases read from tensor memory (k_bform_tm): the
-  // lane's 4G words sit in 4G consecutive TMEM columns in LDS order.
-  __device__ __forceinline__ void run_tm(uint32_t taddr, int rep) {
-    static_assert(G == 8, "TMEM bases: 32 columns per lane");
-    uint32_t r[32];
-    tmem_ld32(taddr, r);
-    float2 b[2 * G];
-#pragma unroll
-    for (int c = 0; c < 2 * G; ++c)
-      b[c] = make_float2(__uint_as_float(r[2 * c]), __uint_as_float(r[2 * c + 1]));
-    if (rep >= 0) add_range<false, 0, G>(b, (uint32_t)rep);
-    else add_range<true, 0, G>(b, 0u - (uint32_t)rep);
-  }
-  __device__ __forceinline__ void store(float* out_row, int32_t oc0, int32_t ncols, uint32_t lane,
-                                        bool vec_ok) const {
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const int32_t c = oc0 + g * 128 + 4 * (int32_t)lane;
-      const float v[4] = {a[2 * g].x, a[2 * g].y, a[2 * g + 1].x, a[2 * g + 1].y};
-      if (vec_ok && c + 3 < ncols) {
-        *reinterpret_cast<float4*>(out_row + c) = make_float4(v[0], v[1], v[2], v[3]);
-      } else {
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (c + e < ncols) out_row[c + e] = v[e];
-      }
-    }
+  __device__ __forceinline__ static void load(uint32_t addr, V* b) {
+    const double2 v = lds128d(addr);
+    b[0] = v.x;
+    b[1] = v.y;
   }
 };
 
-template <int G>
-struct Acc<double, G> {
-  double a[2 * G];
+// The bases of one staged k row for this lane: G 16-byte column groups.
+template <class T, int G>
+struct Bases {
+  typename Lane<T>::V b[2 * G];
+  __device__ __forceinline__ void load(uint32_t row_addr) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) Lane<T>::load(row_addr + group_off(g), &b[2 * g]);
+  }
+};
+
+// Register-resident accumulators of one output row: 2G operands per lane.
+template <class T, int G>
+struct Acc {
+  using L = Lane<T>;
+  typename L::V a[2 * G];
   __device__ __forceinline__ void zero() {
 #pragma unroll
-    for (int c = 0; c < 2 * G; ++c) a[c] = 0.0;
+    for (int c = 0; c < 2 * G; ++c) a[c] = L::zero();
   }
-  struct Bases {
-    double b[2 * G];
-  };
-  __device__ __forceinline__ static Bases load_bases(uint32_t row_addr) {
-    Bases s;
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const double2 v = lds128d(row_addr + group_off(g));
-      s.b[2 * g] = v.x;
-      s.b[2 * g + 1] = v.y;
-    }
-    return s;
-  }
+  // t sequential `acc += step` per column, step = NEG ? -base : base
+  // (kernels.hpp:95-104): trips of REP_UNROLL steps, then the remainder by its
+  // binary digits (no loop, no predicated FP tail).
   template <bool NEG>
-  __device__ __forceinline__ void add_n(const Bases& s, uint32_t t) {
-#pragma unroll 1
-    while (t >= 4) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int c = 0; c < 2 * G; ++c) a[c] = __dadd_rn(a[c], NEG ? -s.b[c] : s.b[c]);
-      t -= 4;
-    }
-#pragma unroll 1
-    while (t != 0) {
-#pragma unroll
-      for (int c = 0; c < 2 * G; ++c) a[c] = __dadd_rn(a[c], NEG ? -s.b[c] : s.b[c]);
-      t -= 1;
-    }
-  }
-  __device__ __forceinline__ void add(const Bases& s, int rep) {
-    if (rep >= 0) add_n<false>(s, (uint32_t)rep);
-    else add_n<true>(s, 0u - (uint32_t)rep);
-  }
-  template <bool NEG, int G0, int G1>
-  __device__ __forceinline__ void add_range(const double* b, uint32_t t) {
+  __device__ __forceinline__ void add_t(const Bases<T, G>& s, uint32_t t) {
 #pragma unroll 1
     while (t >= REP_UNROLL) {
 #pragma unroll
       for (int u = 0; u < REP_UNROLL; ++u)
 #pragma unroll
-        for (int c = 2 * G0; c < 2 * G1; ++c)
-          a[c] = __dadd_rn(a[c], NEG ? -b[c - 2 * G0] : b[c - 2 * G0]);
+        for (int c = 0; c < 2 * G; ++c) a[c] = L::template add<NEG>(a[c], s.b[c]);
       t -= REP_UNROLL;
     }
-    if (REP_BIN) {
 #pragma unroll
-      for (int bit = REP_UNROLL / 2; bit >= 1; bit >>= 1)
-        if (t & (uint32_t)bit) {
+    for (int bit = REP_UNROLL / 2; bit >= 1; bit >>= 1)
+      if (t & (uint32_t)bit) {
 #pragma unroll
-          for (int u = 0; u < bit; ++u)
+        for (int u = 0; u < bit; ++u)
 #pragma unroll
-            for (int c = 2 * G0; c < 2 * G1; ++c)
-              a[c] = __dadd_rn(a[c], NEG ? -b[c - 2 * G0] : b[c - 2 * G0]);
-        }
-      return;
-    }
-#pragma unroll 1
-    while (t != 0) {
-#pragma unroll
-      for (int c = 2 * G0; c < 2 * G1; ++c)
-        a[c] = __dadd_rn(a[c], NEG ? -b[c - 2 * G0] : b[c - 2 * G0]);
-      t -= 1;
-    }
+          for (int c = 0; c < 2 * G; ++c) a[c] = L::template add<NEG>(a[c], s.b[c]);
+      }
   }
-  template <int G0, int G1>
-  __device__ __forceinline__ void run_range(uint32_t row_addr, int rep) {
-    double b[2 * (G1 - G0)];
-#pragma unroll
-    for (int g = G0; g < G1; ++g) {
-      const double2 v = lds128d(row_addr + group_off(g));
-      b[2 * (g - G0)] = v.x;
-      b[2 * (g - G0) + 1] = v.y;
-    }
-    if (rep >= 0) add_range<false, G0, G1>(b, (uint32_t)rep);
-    else add_range<true, G0, G1>(b, 0u - (uint32_t)rep);
+  // |rep| sequential adds of step = rep >= 0 ? base : -base (kernels.hpp:97)
+  __device__ __forceinline__ void add(const Bases<T, G>& s, int rep) {
+    if (rep >= 0) add_t<false>(s, (uint32_t)rep);
+    else add_t<true>(s, 0u - (uint32_t)rep);
   }
-  __device__ __forceinline__ void run(uint32_t row_addr, int rep) { run_range<0, G>(row_addr, rep); }
-  __device__ __forceinline__ void run_tm(uint32_t taddr, int rep) {
-    static_assert(G == 8, "TMEM bases: 32 columns per lane");
-    uint32_t r[32];
-    tmem_ld32(taddr, r);
-    double b[2 * G];
-#pragma unroll
-    for (int c = 0; c < 2 * G; ++c)
-      b[c] = __hiloint2double((int)r[2 * c + 1], (int)r[2 * c]);
-    if (rep >= 0) add_range<false, 0, G>(b, (uint32_t)rep);
-    else add_range<true, 0, G>(b, 0u - (uint32_t)rep);
+  // One list entry: load the bases of the staged k row, run the rep loop.
+  // (Splitting wide tiles into two half-width loops to save 16 base registers
+  // was measured 3% slower.)
+  __device__ __forceinline__ void run(uint32_t row_addr, int rep) {
+    Bases<T, G> s;
+    s.load(row_addr);
+    add(s, rep);
   }
-  __device__ __forceinline__ void store(double* out_row, int32_t oc0, int32_t ncols,
-                                        uint32_t lane, bool vec_ok) const {
+  // Columns of operand c: tile_col + (c/2)*GROUP_COLS + lane*PER_LANE + (c%2)*(PER_LANE/2)
+  __device__ __forceinline__ void store(T* out_row, int32_t oc0, int32_t ncols, uint32_t lane,
+                                        bool vec_ok) const {
+    constexpr int PER_LANE = 16 / sizeof(T);      // columns per lane per group
+    constexpr int GROUP_COLS = 32 * PER_LANE;     // columns per group
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const int32_t c = oc0 + g * 64 + 2 * (int32_t)lane;
-      if (vec_ok && c + 1 < ncols) {
-        *reinterpret_cast<double2*>(out_row + c) = make_double2(a[2 * g], a[2 * g + 1]);
+      const int32_t c = oc0 + g * GROUP_COLS + PER_LANE * (int32_t)lane;
+      T v[PER_LANE];
+      if constexpr (sizeof(T) == 4) {
+        v[0] = a[2 * g].x; v[1] = a[2 * g].y; v[2] = a[2 * g + 1].x; v[3] = a[2 * g + 1].y;
       } else {
-        if (c < ncols) out_row[c] = a[2 * g];
-        if (c + 1 < ncols) out_row[c + 1] = a[2 * g + 1];
+        v[0] = a[2 * g]; v[1] = a[2 * g + 1];
+      }
+      if (vec_ok && c + PER_LANE - 1 < ncols) {
+        if constexpr (sizeof(T) == 4)
+          *reinterpret_cast<float4*>(out_row + c) = make_float4(v[0], v[1], v[2], v[3]);
+        else
+          *reinterpret_cast<double2*>(out_row + c) = make_double2(v[0], v[1]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < PER_LANE; ++e)
+          if (c + e < ncols) out_row[c + e] = v[e];
       }
     }
   }
@@ -460,47 +249,86 @@ __host__ __device__ constexpr size_t ring_smem_bytes() {
          2 * STAGES * sizeof(uint64_t);
 }
 
-// TMA issue logic of the producer warp (lane 0). pump() issues, without
-// blocking, every load whose ring slot has been released by all consumers:
-// the i-th block of the slice (k block kb_lo + i) goes to slot i % STAGES
-// once the block STAGES earlier is released. The producer alternates pump()
-// with a suspending wait on the next slot's empty barrier. (An in-consumer
-// variant that let warp 0 pump between its own entries was measured 2-3x
-// slower: the pumping warp becomes the ring's slowest consumer.)
-template <class T, int G, int STAGES>
-struct Pump {
-  using Gm = Geo<T, G>;
-  const CUtensorMap* tmap;
-  const CUtensorMap* rmap;  // optional dense-rep map (k_bform_mr)
-  unsigned char* ring;
-  unsigned char* rring;
-  uint64_t* full;
-  uint64_t* empty;
-  int32_t col;
-  int32_t rrow;
-  uint32_t nkb;
-  uint32_t kb_lo;
-  uint32_t rep_stage_bytes;
-  uint32_t next;
-  __device__ __forceinline__ void pump() {
-    while (next < nkb) {
-      const uint32_t slot = next % STAGES;
-      if (next >= STAGES && !mbar_test_wait(&empty[slot], ((next / STAGES) - 1) & 1)) return;
-      mbar_arrive_expect_tx(&full[slot], (uint32_t)Gm::STAGE_BYTES + rep_stage_bytes);
-      const int32_t krow = (int32_t)((kb_lo + next) * KB);
+// TMA producer (one thread): fills ring slot i % STAGES with k block
+// kb_lo + i of the slice, i < nkb, as soon as every consumer has released the
+// block STAGES earlier. The waits suspend in hardware (no polling).
+template <int STAGE_BYTES, int NBOX, int BOX_N, int STAGES>
+__device__ __forceinline__ void produce(const CUtensorMap* tmap, unsigned char* ring,
+                                        uint64_t* full, uint64_t* empty, int32_t col,
+                                        uint32_t kb_lo, uint32_t nkb) {
+  prefetch_tensormap(tmap);
+  for (uint32_t i = 0; i < nkb; ++i) {
+    const uint32_t slot = i % STAGES;
+    if (i >= STAGES) mbar_sleep_wait_at(smem_u32(&empty[slot]), ((i / STAGES) - 1) & 1);
+    mbar_arrive_expect_tx(&full[slot], (uint32_t)STAGE_BYTES);
+    const int32_t krow = (int32_t)((kb_lo + i) * KB);
 #pragma unroll
-      for (int h = 0; h < Gm::NBOX; ++h)
-        tma_load_2d(ring + slot * Gm::STAGE_BYTES + h * KB * BOX_BYTES, tmap, &full[slot],
-                    col + h * Gm::BOX_N, krow);
-      if (rmap) tma_load_2d(rring + slot * rep_stage_bytes, rmap, &full[slot], rrow, krow);
-      ++next;
+    for (int h = 0; h < NBOX; ++h)
+      tma_load_2d(ring + slot * STAGE_BYTES + h * KB * BOX_BYTES, tmap, &full[slot],
+                  col + h * BOX_N, krow);
+  }
+}
+
+// A consumer warp's position in the ring: the k block it holds (kb_cur), that
+// block's slot and fill parity, and the smem address of the slot plus this
+// lane's first 16-byte column group.
+template <int STAGES, int STAGE_BYTES>
+struct Cursor {
+  uint32_t kb_cur = 0, slot = 0, phase = 0, stage_addr, full0, empty0;
+  __device__ __forceinline__ Cursor(uint32_t ring, uint32_t full_addr, uint32_t empty_addr,
+                                    uint32_t lane)
+      : stage_addr(ring + lane * 16), full0(full_addr), empty0(empty_addr) {}
+  __device__ __forceinline__ void wait() { mbar_sleep_wait_at(full0 + slot * 8, phase); }
+  // release the held block (one arrival per warp) and step to the next
+  __device__ __forceinline__ void advance(uint32_t lane) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive_at(empty0 + slot * 8);
+    ++kb_cur;
+    stage_addr += STAGE_BYTES;
+    if (++slot == STAGES) {
+      slot = 0;
+      phase ^= 1;
+      stage_addr -= STAGES * STAGE_BYTES;
     }
+  }
+  __device__ __forceinline__ void seek(uint32_t kb, uint32_t lane) {
+    while (kb_cur < kb) {
+      advance(lane);
+      wait();
+    }
+  }
+  // release every remaining block in order (the ring needs all CW arrivals)
+  __device__ __forceinline__ void drain(uint32_t nkb, uint32_t lane) {
+    while (true) {
+      advance(lane);
+      if (kb_cur >= nkb) break;
+      wait();
+    }
+  }
+};
+
+// List entry of R B-form rows: R = 1 -> int2 {k, rep} (zero reps compacted
+// away); R = 4 -> int4 {k, rep0 | rep1 << 16, rep2 | rep3 << 16, 0} for the
+// rows of a quad, int16 reps (a zero rep is a row without a term at k).
+template <int R>
+struct Entry;
+template <>
+struct Entry<1> {
+  using type = int2;
+};
+template <>
+struct Entry<4> {
+  using type = int4;
+  __device__ __forceinline__ static int rep(const int4& e, int q) {
+    const int w = q < 2 ? e.y : e.z;
+    return (q & 1) ? (w >> 16) : (int)(short)(w & 0xffff);
   }
 };
 
 // First list index with k >= key (lists are sorted by k); every lane computes
 // the same answer from broadcast loads.
-__device__ __forceinline__ uint32_t lower_bound_k(const int2* lst, uint32_t cnt, uint32_t key) {
+template <class E>
+__device__ __forceinline__ uint32_t lower_bound_k(const E* lst, uint32_t cnt, uint32_t key) {
   uint32_t lo = 0, hi = cnt;
   while (lo < hi) {
     const uint32_t mid = (lo + hi) >> 1;
@@ -510,18 +338,27 @@ __device__ __forceinline__ uint32_t lower_bound_k(const int2* lst, uint32_t cnt,
   return lo;
 }
 
-// lists: row b's entries at lists[b * cap .. b * cap + counts[b]) in increasing k.
-// Output row b, column (col0 + c) -> out[b * ld_out + c], c < ncols.
-// k slice: blockIdx.z selects slice z = [z*slice_blocks, (z+1)*slice_blocks)
-// of the nkb_total k blocks and writes to out + z * slice_stride (fast-mode
-// split-k; one slice = the whole k range in order-preserving mode).
-template <class T, int G, int CW, int STAGES, int MINB, bool SPLIT>
-__global__ void __launch_bounds__((CW + kProdWarps) * 32, MINB)
-    k_bform(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ lists,
-            uint64_t cap, const uint32_t* __restrict__ counts, uint32_t nrows, uint32_t rpc,
-            int32_t col0, int32_t ncols, uint32_t nkb_total, uint32_t slice_blocks, uint64_t slice_stride,
-            T* __restrict__ out, uint64_t ld_out, int vec_ok, const DevStatus* __restrict__ st) {
+// k_bform: each consumer warp owns R B-form rows ("group" b: rows R*b ..
+// R*b + R - 1) of a TILE_N-column tile and walks the group's list.
+//   lists: group b's entries at lists[b * cap .. b * cap + counts[b]), k increasing.
+//   Output row r, column (col0 + c) -> out[r * ld_out + c], c < ncols.
+//   dyn_ncols (optional): ncols decided on the device (Case A row split).
+//   k slice: blockIdx.z selects slice z = [z*slice_blocks, (z+1)*slice_blocks)
+//   of the nkb_total k blocks and writes to out + z * slice_stride (fast-mode
+//   split-k; one slice = the whole k range in order-preserving mode).
+// R = 4 ("quad" lists): the bases of an entry are loaded once for four rows,
+// so each 16-byte LDS feeds up to 4x as many adds -- the small-rep regime is
+// bound by the shared-memory data pipe with R = 1.
+template <class T, int G, int CW, int STAGES, int MINB, int R, bool SPLIT>
+__global__ void __launch_bounds__((CW + 1) * 32, MINB)
+    k_bform(const __grid_constant__ CUtensorMap tmap,
+            const typename Entry<R>::type* __restrict__ lists, uint64_t cap,
+            const uint32_t* __restrict__ counts, uint32_t nrows, uint32_t gpc, int32_t col0,
+            int32_t ncols, const uint32_t* __restrict__ dyn_ncols, uint32_t nkb_total,
+            uint32_t slice_blocks, uint64_t slice_stride, T* __restrict__ out, uint64_t ld_out,
+            int vec_ok, const DevStatus* __restrict__ st) {
   using Gm = Geo<T, G>;
+  using E = typename Entry<R>::type;
   extern __shared__ unsigned char smem_raw[];
   // 128-byte aligned ring (TMA destination without swizzle); pointer arithmetic
   // on the smem pointer itself keeps the shared address space visible to the
@@ -529,15 +366,18 @@ __global__ void __launch_bounds__((CW + kProdWarps) * 32, MINB)
   unsigned char* base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   uint64_t* full = reinterpret_cast<uint64_t*>(base + STAGES * Gm::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  const uint32_t ring = smem_u32(base);
 
   if (status_failed(st)) return;  // validation failed: compute nothing (kernels.hpp:115,144)
+  const int32_t tile_c = blockIdx.y * Gm::TILE_N;  // relative to col0
+  if (dyn_ncols) {
+    ncols = (int32_t)*dyn_ncols;
+    if (tile_c >= ncols) return;  // the whole CTA: beyond the device-decided width
+  }
 
   // %laneid through asm volatile: under register pressure ptxas otherwise
   // re-derives the lane from S2R SR_TID inside the entry loop (a ~30-cycle
   // stall per entry, ncu source view at rep 1).
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-  const int32_t tile_c = blockIdx.y * Gm::TILE_N;  // relative to col0
   // SPLIT = false (order-preserving mode): one slice, k_lo = 0 at compile time
   // (a runtime k_lo was rematerialised from S2UR SR_CTAID.Z + LDC every entry).
   const uint32_t kb_lo = SPLIT ? blockIdx.z * slice_blocks : 0u;
@@ -545,51 +385,33 @@ __global__ void __launch_bounds__((CW + kProdWarps) * 32, MINB)
   const uint32_t nkb = kb_hi - kb_lo;
   if (SPLIT) out += blockIdx.z * slice_stride;
 
-  // refill of ring slot `sl` with block `blk` of the slice (one thread)
-  auto refill = [&](uint32_t sl, uint32_t blk) {
-    mbar_arrive_expect_tx(&full[sl], (uint32_t)Gm::STAGE_BYTES);
-    const int32_t krow = (int32_t)((kb_lo + blk) * KB);
-#pragma unroll
-    for (int h = 0; h < Gm::NBOX; ++h)
-      tma_load_2d(base + sl * Gm::STAGE_BYTES + h * KB * BOX_BYTES, &tmap, &full[sl],
-                  col0 + tile_c + h * Gm::BOX_N, krow);
-  };
-  uint32_t* released = reinterpret_cast<uint32_t*>(empty);  // kNoProd: arrivals per slot
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      if (kNoProd) released[s] = 0;
-      else mbar_init(&empty[s], CW);
+      mbar_init(&empty[s], CW);
     }
     fence_barrier_init();
-    if (kNoProd)
-      for (uint32_t s = 0; s < (uint32_t)STAGES && s < nkb; ++s) refill(s, s);
   }
   __syncthreads();
 
-  if (!kNoProd && warp == CW) {
+  if (warp == CW) {
     // ---- dedicated TMA producer warp ----
-    // (Unlike k_bform_mr, the list-walking warps progress unevenly; an
-    // in-warp pump makes warp 0 the ring's bottleneck: measured 2-3x slower.)
-    if (lane == 0) {
-      Pump<T, G, STAGES> pump{&tmap, nullptr, base, nullptr, full, empty, col0 + tile_c, 0,
-                              nkb, kb_lo, 0, 0};
-      prefetch_tensormap(&tmap);
-      while (true) {
-        pump.pump();
-        if (pump.next >= nkb) break;
-        mbar_sleep_wait_at(smem_u32(&empty[pump.next % STAGES]), ((pump.next / STAGES) - 1) & 1);
-      }
-    }
+    // (An in-consumer pump that let warp 0 issue the loads between its own
+    // entries was measured 2-3x slower: the list-walking warps progress
+    // unevenly and the pumping warp gates the ring.)
+    if (lane == 0)
+      produce<Gm::STAGE_BYTES, Gm::NBOX, Gm::BOX_N, STAGES>(&tmap, base, full, empty,
+                                                            col0 + tile_c, kb_lo, nkb);
     return;
   }
 
-  // ---- consumers: one output row per warp ----
-  // rpc <= CW rows per CTA (the launcher trims it to balance the last wave);
+  // ---- consumers: R output rows per warp ----
+  // gpc <= CW groups per CTA (the launcher trims it to balance the last wave);
   // warps past it walk no entries but still release every stage.
-  const uint32_t b = warp < rpc ? blockIdx.x * rpc + warp : nrows;
-  uint32_t cnt = b < nrows ? counts[b] : 0u;
-  const int2* lst = lists + (uint64_t)(b < nrows ? b : 0) * cap;
+  const uint32_t ngroups = (nrows + R - 1) / R;
+  const uint32_t b = warp < gpc ? blockIdx.x * gpc + warp : ngroups;
+  uint32_t cnt = b < ngroups ? counts[b] : 0u;
+  const E* lst = lists + (uint64_t)(b < ngroups ? b : 0) * cap;
   if (SPLIT) {
     // this slice's entries: [lower_bound(kb_lo*KB), lower_bound(kb_hi*KB))
     const uint32_t p0 = lower_bound_k(lst, cnt, kb_lo * KB);
@@ -598,324 +420,48 @@ __global__ void __launch_bounds__((CW + kProdWarps) * 32, MINB)
     cnt = p1 - p0;
   }
 
-  Acc<T, G> acc;
-  acc.zero();
+  Acc<T, G> acc[R];
+#pragma unroll
+  for (int q = 0; q < R; ++q) acc[q].zero();
   const uint32_t k_lo = kb_lo * KB;
-  const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty);
-
-  // (kb_cur, slot, phase): the k block currently held, its ring slot and the
-  // parity of that slot's current fill; stage_addr = smem address of the slot
-  // plus this lane's first 16-byte column group.
-  uint32_t kb_cur = 0, slot = 0, phase = 0;
-  uint32_t stage_addr = ring + lane * 16;
-  auto advance = [&]() {
-    __syncwarp();
-    if (lane == 0) {
-      if (kNoProd) {
-        // the last of the CW warps to release this use of the slot refills it
-        const uint32_t old = atomicAdd(&released[slot], 1u);
-        if (old % CW == CW - 1 && kb_cur + STAGES < nkb) {
-          fence_proxy_async_smem();  // order the warps' smem reads before the TMA write
-          refill(slot, kb_cur + STAGES);
-        }
-      } else {
-        mbar_arrive_at(empty0 + slot * 8);
-      }
-    }
-    ++kb_cur;
-    stage_addr += Gm::STAGE_BYTES;
-    if (++slot == STAGES) {
-      slot = 0;
-      phase ^= 1;
-      stage_addr -= STAGES * Gm::STAGE_BYTES;
-    }
-  };
-  mbar_sleep_wait_at(full0, 0);
-  // Entry e + 1 = (k, rep) is read by a warp-uniform load (L1 broadcast)
-  // while entry e runs, and the list line 64 entries ahead is prefetched into
-  // L1. (Measured against one coalesced 32-entry load per chunk + SHFL
+  Cursor<STAGES, Gm::STAGE_BYTES> cur(smem_u32(base), smem_u32(full), smem_u32(empty), lane);
+  cur.wait();
+  // Entry e + 1 is read by a warp-uniform load (L1 broadcast) while entry e
+  // runs, and the list line kListPrefetch entries ahead is prefetched into L1.
+  // (Measured against one coalesced 32-entry load per chunk + SHFL
   // broadcasts: equal at cfg5, cfg3 mu = 4 +2.6%, cfg4 +1%, rep 1 -2%; fewer
   // instructions and branches per entry.)
-  const int2* __restrict__ lp = lst;
-  const int2 e0 = cnt ? __ldg(lp) : make_int2(0, 0);
-  uint32_t k = (uint32_t)e0.x;
-  int rep = e0.y;
-  for (uint32_t e = 0; e < cnt; ++e) {
-    const uint32_t f = e + 1;
-    const int2 ne = f < cnt ? __ldg(lp + f) : make_int2(0, 0);
+  const E* __restrict__ lp = lst;
+  E e = cnt ? __ldg(lp) : E{};
+  for (uint32_t i = 0; i < cnt; ++i) {
+    const uint32_t f = i + 1;
+    const E ne = f < cnt ? __ldg(lp + f) : E{};
     if (f + kListPrefetch < cnt)
       asm volatile("prefetch.global.L1 [%0];" ::"l"(lp + f + kListPrefetch));
-    const uint32_t kb = (k - k_lo) / KB;  // block index within the slice
-    while (kb_cur < kb) {
-      advance();
-      mbar_sleep_wait_at(full0 + slot * 8, phase);
-    }
-    acc.run(stage_addr + (k % KB) * BOX_BYTES, rep);
-    k = (uint32_t)ne.x;
-    rep = ne.y;
-  }
-  // release the remaining stages in order
-  while (true) {
-    advance();
-    if (kb_cur >= nkb) break;
-    mbar_sleep_wait_at(full0 + slot * 8, phase);
-  }
-
-  if (b < nrows) acc.store(out + (uint64_t)b * ld_out, tile_c, ncols, lane, vec_ok != 0);
-}
-
-// ---------------------------------------------------------------------------
-// k_bform_tm: k_bform with the bases served from tensor memory.
-//
-// At small reps k_bform is bound by the shared-memory data pipe (ncu at rep 1:
-// L1TEX wavefronts 97%, FMA pipe 28%): each of the CTA's warps re-reads every
-// staged base row with 128-bit LDS at 128 B/clk/SM. TMEM reads into registers
-// run at >= 450 B/clk/SM (tools/tmem_probe.cu), so here
-//   * warp CW (TMA) streams KB x 1024-byte-row tiles of B' into an SST-deep
-//     smem ring (as in k_bform);
-//   * warp CW+1 (copy) moves each landed tile into one of TST TMEM stages with
-//     tcgen05.cp 32x128b.warpx4 (each 512-byte column group -> 4 columns of all
-//     128 lanes, i.e. one copy per lane quadrant), then tcgen05.commit arrives on
-//     the stage's full barrier and on the smem slot's empty barrier;
-//   * the CW consumer warps walk their rows' lists as in k_bform but fetch an
-//     entry's 32 bases per lane with one tcgen05.ld 32x32b.x32 from their lane
-//     quadrant, releasing TMEM stages through per-stage empty barriers.
-// CW = 14 consumers + 2 producers (4 warps per SM sub-partition, 128-register
-// budget), one CTA per SM owning all 512 TMEM columns: TM_TST = 4 stages of
-// TM_TKB = 4 k rows x 32 columns. Per element the order is unchanged (one
-// chain, k ascending, |rep| adds).
-//
-// Measured (tools/exp_time.py): equal to k_bform at rep >= 4 and slower at
-// rep 1-2 (0.20 vs 0.23 of peak): the replicating copy (one 32x128b.warpx4
-// per 512 bytes) cannot refill TMEM as fast as 14 warps drain it, so the
-// consumers wait on the stage-full barrier (ncu: 32% of warp samples). Kept
-// as an opt-in variant (AFMM_BFORM=tmem) with full parity coverage.
-// ---------------------------------------------------------------------------
-
-constexpr int TM_TKB = 4;           // k rows per TMEM stage (half an smem stage)
-constexpr int TM_TST = 4;           // TMEM stages
-constexpr int TM_COLS = 512;        // TMEM columns allocated (whole SM)
-constexpr int TM_STAGE_COLS = TM_TKB * 32;
-static_assert(KB % TM_TKB == 0, "TMEM stage must divide the smem stage");
-
-template <class T, int CW, int SST>
-__host__ __device__ constexpr size_t tm_smem_bytes() {
-  return 128 + (size_t)SST * Geo<T, 8>::STAGE_BYTES +
-         (2 * SST + 2 * TM_TST) * sizeof(uint64_t) + 16;
-}
-
-template <class T, int CW, int SST, bool SPLIT>
-__global__ void __launch_bounds__((CW + 2) * 32, 1)
-    k_bform_tm(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ lists,
-               uint64_t cap, const uint32_t* __restrict__ counts, uint32_t nrows, uint32_t rpc,
-               int32_t col0, int32_t ncols, uint32_t nkb_total, uint32_t slice_blocks, uint64_t slice_stride,
-               T* __restrict__ out, uint64_t ld_out, int vec_ok,
-               const DevStatus* __restrict__ st) {
-  constexpr int G = 8;
-  using Gm = Geo<T, G>;
-  static_assert(TM_TST * TM_STAGE_COLS <= TM_COLS, "TMEM stages");
-  extern __shared__ unsigned char smem_raw[];
-  unsigned char* base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
-  uint64_t* sfull = reinterpret_cast<uint64_t*>(base + SST * Gm::STAGE_BYTES);
-  uint64_t* sempty = sfull + SST;
-  uint64_t* tfull = sempty + SST;
-  uint64_t* tempty = tfull + TM_TST;
-  uint32_t* tbase_slot = reinterpret_cast<uint32_t*>(tempty + TM_TST);
-  const uint32_t ring = smem_u32(base);
-
-  if (status_failed(st)) return;  // validation failed: compute nothing (kernels.hpp:115,144)
-
-  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-  const int32_t tile_c = blockIdx.y * Gm::TILE_N;
-  const uint32_t kb_lo = SPLIT ? blockIdx.z * slice_blocks : 0u;
-  const uint32_t kb_hi = min(nkb_total, kb_lo + slice_blocks);
-  const uint32_t nkb = kb_hi - kb_lo;
-  if (SPLIT) out += blockIdx.z * slice_stride;
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < SST; ++i) {
-      mbar_init(&sfull[i], 1);
-      mbar_init(&sempty[i], 1);
-    }
-    for (int i = 0; i < TM_TST; ++i) {
-      mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], CW);
-    }
-    fence_barrier_init();
-  }
-  if (warp == CW + 1) {  // the copy warp owns the TMEM allocation
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tbase_slot)),
-                 "n"(TM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  tmem_fence_before();
-  __syncthreads();
-  tmem_fence_after();
-  const uint32_t tbase = *tbase_slot;
-
-  if (warp == CW) {
-    // ---- TMA producer: global -> smem ring ----
-    if (lane == 0) {
-      prefetch_tensormap(&tmap);
-      for (uint32_t i = 0; i < nkb; ++i) {
-        const uint32_t slot = i % SST;
-        if (i >= SST) mbar_sleep_wait_at(smem_u32(&sempty[slot]), ((i / SST) - 1) & 1);
-        mbar_arrive_expect_tx(&sfull[slot], (uint32_t)Gm::STAGE_BYTES);
-        const int32_t krow = (int32_t)((kb_lo + i) * KB);
+    const uint32_t k = (uint32_t)e.x;
+    cur.seek((k - k_lo) / KB, lane);  // block index within the slice
+    const uint32_t row_addr = cur.stage_addr + (k % KB) * BOX_BYTES;
+    if constexpr (R == 1) {
+      acc[0].run(row_addr, e.y);
+    } else {
+      Bases<T, G> s;
+      s.load(row_addr);
 #pragma unroll
-        for (int h = 0; h < Gm::NBOX; ++h)
-          tma_load_2d(base + slot * Gm::STAGE_BYTES + h * KB * BOX_BYTES, &tmap, &sfull[slot],
-                      col0 + tile_c + h * Gm::BOX_N, krow);
+      for (int q = 0; q < R; ++q) {
+        const int r = Entry<R>::rep(e, q);
+        if (r != 0) acc[q].add(s, r);
       }
     }
-    return;
+    e = ne;
   }
+  cur.drain(nkb, lane);
 
-  if (warp == CW + 1) {
-    // ---- copy warp: smem ring -> TMEM stages ----
-    if (lane == 0) {
-      for (uint32_t i = 0; i < nkb; ++i) {
-        const uint32_t slot = i % SST;
-        mbar_sleep_wait_at(smem_u32(&sfull[slot]), (i / SST) & 1);
-        const uint32_t src = ring + slot * Gm::STAGE_BYTES;
-#pragma unroll 1
-        for (int h = 0; h < KB / TM_TKB; ++h) {
-          const uint32_t j = i * (KB / TM_TKB) + h, ts = j % TM_TST;
-          if (j >= TM_TST) mbar_sleep_wait_at(smem_u32(&tempty[ts]), ((j / TM_TST) - 1) & 1);
-          tmem_fence_after();
-          const uint32_t dst = tbase + ts * TM_STAGE_COLS;
-#pragma unroll 1
-          for (int kk = 0; kk < TM_TKB; ++kk)
 #pragma unroll
-            for (int g = 0; g < G; ++g)
-              tmem_cp_32x128b_x4(
-                  dst + kk * 32 + g * 4,
-                  smem_desc_128(src + group_off(g) + (h * TM_TKB + kk) * BOX_BYTES));
-          tmem_commit(smem_u32(&tfull[ts]));
-        }
-        tmem_commit(smem_u32(&sempty[slot]));
-      }
-    }
-    __syncwarp();
-    // wait for the consumers, then free TMEM
-    asm volatile("bar.sync 1, %0;" ::"n"((CW + 1) * 32) : "memory");
-    tmem_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(TM_COLS)
-                 : "memory");
-    return;
+  for (int q = 0; q < R; ++q) {
+    const uint32_t row = b * R + q;
+    if (b < ngroups && row < nrows)
+      acc[q].store(out + (uint64_t)row * ld_out, tile_c, ncols, lane, vec_ok != 0);
   }
-
-  // ---- consumers: one output row per warp ----
-  // rpc <= CW rows per CTA (the launcher trims it to balance the last wave);
-  // warps past it walk no entries but still release every stage.
-  const uint32_t b = warp < rpc ? blockIdx.x * rpc + warp : nrows;
-  uint32_t cnt = b < nrows ? counts[b] : 0u;
-  const int2* lst = lists + (uint64_t)(b < nrows ? b : 0) * cap;
-  if (SPLIT) {
-    const uint32_t p0 = lower_bound_k(lst, cnt, kb_lo * KB);
-    const uint32_t p1 = kb_hi == nkb_total ? cnt : lower_bound_k(lst, cnt, kb_hi * KB);
-    lst += p0;
-    cnt = p1 - p0;
-  }
-
-  Acc<T, G> acc;
-  acc.zero();
-  const uint32_t k_lo = kb_lo * KB;
-  const uint32_t tfull0 = smem_u32(tfull), tempty0 = smem_u32(tempty);
-  // this warp's lane quadrant of the current TMEM stage
-  const uint32_t tq = tbase + (((warp & 3u) * 32u) << 16);
-  uint32_t kb_cur = 0, ts = 0, phase = 0;
-  uint32_t stage_t = tq;
-  auto advance = [&]() {
-    tmem_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive_at(tempty0 + ts * 8);
-    ++kb_cur;
-    stage_t += TM_STAGE_COLS;
-    if (++ts == TM_TST) {
-      ts = 0;
-      phase ^= 1;
-      stage_t = tq;
-    }
-  };
-  mbar_sleep_wait_at(tfull0, 0);
-  tmem_fence_after();
-  int2 cur = lane < cnt ? lst[lane] : make_int2(0, 0);
-  int2 nxt = 32 + lane < cnt ? lst[32 + lane] : make_int2(0, 0);
-  uint32_t k = (uint32_t)__shfl_sync(FULL, cur.x, 0);
-  int rep = __shfl_sync(FULL, cur.y, 0);
-  for (uint32_t e = 0; e < cnt; ++e) {
-    const uint32_t f = e + 1;
-    if ((f & 31u) == 0) {
-      cur = nxt;
-      const uint32_t pn = f + 32 + lane;
-      nxt = pn < cnt ? lst[pn] : make_int2(0, 0);
-    }
-    const uint32_t k_n = (uint32_t)__shfl_sync(FULL, cur.x, f & 31u);
-    const int rep_n = __shfl_sync(FULL, cur.y, f & 31u);
-    const uint32_t kb = (k - k_lo) / TM_TKB;  // TMEM block within the slice
-    while (kb_cur < kb) {
-      advance();
-      mbar_sleep_wait_at(tfull0 + ts * 8, phase);
-      tmem_fence_after();
-    }
-    acc.run_tm(stage_t + (k % TM_TKB) * 32, rep);
-    k = k_n;
-    rep = rep_n;
-  }
-  while (true) {
-    advance();
-    if (kb_cur >= nkb * (KB / TM_TKB)) break;
-    mbar_sleep_wait_at(tfull0 + ts * 8, phase);
-  }
-  tmem_fence_before();
-  asm volatile("bar.sync 1, %0;" ::"n"((CW + 1) * 32) : "memory");
-
-  if (b < nrows) acc.store(out + (uint64_t)b * ld_out, tile_c, ncols, lane, vec_ok != 0);
-}
-
-template <class T, bool SPLIT>
-cudaError_t launch_tm_impl(const CUtensorMap* tmap, const int2* lists, uint64_t cap,
-                           const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,
-                           uint32_t nkb, uint32_t slice_blocks, uint32_t splits,
-                           uint64_t slice_stride, T* out, uint64_t ld_out, bool vec_ok,
-                           const DevStatus* st, cudaStream_t s) {
-  constexpr int CW = kTmemRows, SST = 4;
-  auto kern = k_bform_tm<T, CW, SST, SPLIT>;
-  const size_t smem = tm_smem_bytes<T, CW, SST>();
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return e;
-  const uint32_t tiles = (ncols + Geo<T, 8>::TILE_N - 1) / Geo<T, 8>::TILE_N;
-  const uint32_t rpc = balanced_rows(nrows, tiles * splits, CW, 1);
-  dim3 grid((nrows + rpc - 1) / rpc, tiles, splits);
-  kern<<<grid, (CW + 2) * 32, smem, s>>>(*tmap, lists, cap, counts, nrows, rpc, col0, ncols, nkb,
-                                         slice_blocks, slice_stride, out, ld_out,
-                                         vec_ok ? 1 : 0, st);
-  note_launch();
-  return cudaGetLastError();
-}
-
-template <class T>
-cudaError_t launch_tm(const CUtensorMap* tmap, const int2* lists, uint64_t cap,
-                      const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,
-                      uint32_t nk, uint32_t* splits, uint64_t slice_stride, T* out,
-                      uint64_t ld_out, const DevStatus* st, cudaStream_t s) {
-  const uint32_t nkb = (nk + KB - 1) / KB;
-  uint32_t want = *splits < 1 ? 1 : *splits;
-  if (want > nkb) want = nkb;
-  const uint32_t slice_blocks = (nkb + want - 1) / want;
-  *splits = (nkb + slice_blocks - 1) / slice_blocks;
-  const bool vec_ok = (ld_out * sizeof(T)) % 16 == 0 &&
-                      (reinterpret_cast<uintptr_t>(out) % 16) == 0 &&
-                      (slice_stride * sizeof(T)) % 16 == 0;
-  if (*splits > 1)
-    return launch_tm_impl<T, true>(tmap, lists, cap, counts, nrows, col0, ncols, nkb,
-                                   slice_blocks, *splits, slice_stride, out, ld_out, vec_ok, st, s);
-  return launch_tm_impl<T, false>(tmap, lists, cap, counts, nrows, col0, ncols, nkb, slice_blocks,
-                                  1, slice_stride, out, ld_out, vec_ok, st, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -998,7 +544,8 @@ template <class T, int CW, int STAGES, int MINB>
 __global__ void __launch_bounds__((CW + 1) * 32, MINB)
     k_aform(const __grid_constant__ CUtensorMap cmap,
             const typename AEntry<T>::type* __restrict__ lists, uint64_t cap,
-            const uint32_t* __restrict__ counts, uint32_t nrows, uint32_t rpc, uint32_t ncols,
+            const uint32_t* __restrict__ counts, uint32_t nrows,
+            const uint32_t* __restrict__ dyn_nrows, uint32_t rpc, uint32_t ncols,
             uint32_t nkb, const uint16_t* __restrict__ rmax, uint32_t ntiles,
             T* __restrict__ out, uint64_t ld_out, const uint32_t* __restrict__ row_idx,
             const DevStatus* __restrict__ st) {
@@ -1011,6 +558,10 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
   const uint32_t ring = smem_u32(base);
 
   if (status_failed(st)) return;  // validation failed: compute nothing (kernels.hpp:115)
+  if (dyn_nrows) {
+    nrows = *dyn_nrows;  // decided on the device (k_choose); the grid covers the slab
+    if (blockIdx.x * rpc >= nrows) return;
+  }
 
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const uint32_t tile = blockIdx.y;
@@ -1149,148 +700,31 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
   }
 }
 
-// ---------------------------------------------------------------------------
-// k_bform_mr: RW output rows per warp over a DENSE rep tile.
-//
-// For small reps the per-entry cost of k_bform is the shared-memory read of
-// the bases (TILE_N * sizeof(T) bytes per warp per entry, at 128 B/clk/SM),
-// not the adds: with |rep| = 1 a 512-column fp32 entry moves 2 KB from smem
-// for 16 FADD2. Here each warp owns RW rows, walks k densely, reads the RW
-// reps of the current k with one broadcast LDS from a staged dense rep tile,
-// and loads the bases once for all RW rows. The rep tile ([k][row] int32,
-// built by the prepass) arrives through the same TMA ring as the bases.
-// Per element the order is unchanged: k ascending, |rep| sequential adds.
-// ---------------------------------------------------------------------------
-
-constexpr int MR_RW = 4;       // rows per warp
-// 12 consumer warps + 1 producer: 3 consumers per SM sub-partition and a
-// 128-register budget (4 x 16 accumulators + 16 bases); 17 warps cap it at 96.
-constexpr int MR_CW = 12;
-constexpr int MR_ROWS = MR_RW * MR_CW;  // 48 rows per CTA: a 192-byte int32 rep box row
-constexpr int MR_STAGES = 8;
-
-template <class T, int G>
-__host__ __device__ constexpr size_t mr_smem_bytes() {
-  return 1024 + (size_t)MR_STAGES * (Geo<T, G>::STAGE_BYTES + KB * MR_ROWS * 4) +
-         2 * MR_STAGES * sizeof(uint64_t);
-}
-
-__device__ __forceinline__ int4 lds128i(uint32_t addr) {
-  int4 v;
-  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "r"(addr));
-  return v;
-}
-
-// rmap: dense reps R'[k][row] (int32, rows = B-form rows, inner dimension).
-template <class T, int G>
-__global__ void __launch_bounds__((MR_CW + 1) * 32, 1)
-    k_bform_mr(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap rmap,
-               uint32_t nrows, int32_t col0, int32_t ncols, uint32_t nk, uint32_t nkb,
-               T* __restrict__ out, uint64_t ld_out, int vec_ok,
-               const DevStatus* __restrict__ st) {
-  using Gm = Geo<T, G>;
-  constexpr int REP_STAGE = KB * MR_ROWS * 4;
-  extern __shared__ unsigned char smem_raw[];
-  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  unsigned char* reps = base + MR_STAGES * Gm::STAGE_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(reps + MR_STAGES * REP_STAGE);
-  uint64_t* empty = full + MR_STAGES;
-  const uint32_t ring = smem_u32(base), rring = smem_u32(reps);
-
-  if (status_failed(st)) return;  // validation failed: compute nothing (kernels.hpp:115,144)
-
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t tile_c = blockIdx.y * Gm::TILE_N;
-  const uint32_t row0 = blockIdx.x * MR_ROWS;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < MR_STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], MR_CW);
-    }
-    fence_barrier_init();
-  }
-  __syncthreads();
-
-  if (warp == MR_CW) {
-    // ---- dedicated TMA producer warp: base tile + dense rep tile per stage ----
-    if (lane == 0) {
-      Pump<T, G, MR_STAGES> pump{&tmap, &rmap, base, reps, full, empty, col0 + tile_c,
-                                 (int32_t)row0, nkb, 0, (uint32_t)REP_STAGE, 0};
-      prefetch_tensormap(&tmap);
-      prefetch_tensormap(&rmap);
-      while (true) {
-        pump.pump();
-        if (pump.next >= nkb) break;
-        mbar_sleep_wait_at(smem_u32(&empty[pump.next % MR_STAGES]),
-                           ((pump.next / MR_STAGES) - 1) & 1);
-      }
-    }
-    return;
-  }
-
-  Acc<T, G> acc[MR_RW];
-#pragma unroll
-  for (int w = 0; w < MR_RW; ++w) acc[w].zero();
-
-  uint32_t slot = 0, phase = 0;
-  for (uint32_t kb = 0; kb < nkb; ++kb) {
-    mbar_sleep_wait_at(smem_u32(&full[slot]), phase);
-    const uint32_t bstage = ring + slot * Gm::STAGE_BYTES + lane * 16;
-    const uint32_t rstage = rring + slot * REP_STAGE + warp * (MR_RW * 4);
-    const uint32_t kk_end = nk - kb * KB < (uint32_t)KB ? nk - kb * KB : (uint32_t)KB;
-    for (uint32_t kk = 0; kk < kk_end; ++kk) {
-      const int4 r = lds128i(rstage + kk * (MR_ROWS * 4));  // this warp's RW reps at k
-      if ((r.x | r.y | r.z | r.w) == 0) continue;
-      const typename Acc<T, G>::Bases b = Acc<T, G>::load_bases(bstage + kk * BOX_BYTES);
-      if (r.x) acc[0].add(b, r.x);
-      if (r.y) acc[1].add(b, r.y);
-      if (r.z) acc[2].add(b, r.z);
-      if (r.w) acc[3].add(b, r.w);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[slot]);
-    if (++slot == MR_STAGES) {
-      slot = 0;
-      phase ^= 1;
-    }
-  }
-
-#pragma unroll
-  for (int w = 0; w < MR_RW; ++w) {
-    const uint32_t row = row0 + warp * MR_RW + w;
-    if (row < nrows) acc[w].store(out + (uint64_t)row * ld_out, tile_c, ncols, lane, vec_ok != 0);
-  }
-}
-
-template <class T, int G, int CW, int STAGES, int MINB>
-cudaError_t launch_ring(const CUtensorMap* tmap, const int2* lists, uint64_t cap,
-                        const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,
-                        uint32_t nk, uint32_t* splits, uint64_t slice_stride, T* out,
-                        uint64_t ld_out, const DevStatus* st, cudaStream_t s) {
-  const uint32_t nkb = (nk + KB - 1) / KB;
-  uint32_t want = *splits < 1 ? 1 : *splits;
+template <class T, int G, int CW, int STAGES, int MINB, int R>
+cudaError_t launch_ring(BformLaunch& a, T* out, cudaStream_t s) {
+  const uint32_t nkb = (a.nk + KB - 1) / KB;
+  uint32_t want = a.splits < 1 ? 1 : a.splits;
   if (want > nkb) want = nkb;
-  auto kern = want > 1 ? k_bform<T, G, CW, STAGES, MINB, true>
-                       : k_bform<T, G, CW, STAGES, MINB, false>;
+  auto kern = want > 1 ? k_bform<T, G, CW, STAGES, MINB, R, true>
+                       : k_bform<T, G, CW, STAGES, MINB, R, false>;
   const size_t smem = ring_smem_bytes<T, G, STAGES>();
   // set on every call: the attribute is per device and costs ~1 us
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
   const uint32_t slice_blocks = (nkb + want - 1) / want;
-  *splits = (nkb + slice_blocks - 1) / slice_blocks;
-  const bool vec_ok = (ld_out * sizeof(T)) % 16 == 0 &&
+  a.splits = (nkb + slice_blocks - 1) / slice_blocks;
+  const bool vec_ok = (a.ld_out * sizeof(T)) % 16 == 0 &&
                       (reinterpret_cast<uintptr_t>(out) % 16) == 0 &&
-                      (slice_stride * sizeof(T)) % 16 == 0;
-  const uint32_t tiles = (ncols + Geo<T, G>::TILE_N - 1) / Geo<T, G>::TILE_N;
-  const uint32_t rpc = balanced_rows(nrows, tiles * *splits, CW, MINB);
-  dim3 grid((nrows + rpc - 1) / rpc, tiles, *splits);
-  kern<<<grid, (CW + kProdWarps) * 32, smem, s>>>(*tmap, lists, cap, counts, nrows, rpc, col0, ncols, nkb,
-                                         slice_blocks, slice_stride, out, ld_out,
-                                         vec_ok ? 1 : 0, st);
+                      (a.slice_stride * sizeof(T)) % 16 == 0;
+  const uint32_t tiles = (a.ncols + Geo<T, G>::TILE_N - 1) / Geo<T, G>::TILE_N;
+  const uint32_t ngroups = (a.nrows + R - 1) / R;
+  const uint32_t gpc = balanced_rows(ngroups, tiles * a.splits, CW, MINB);
+  dim3 grid((ngroups + gpc - 1) / gpc, tiles, a.splits);
+  kern<<<grid, (CW + 1) * 32, smem, s>>>(
+      *a.tmap, static_cast<const typename Entry<R>::type*>(a.lists), a.cap, a.counts, a.nrows,
+      gpc, a.col0, a.ncols, a.dyn_ncols, nkb, slice_blocks, a.slice_stride, out, a.ld_out,
+      vec_ok ? 1 : 0, a.st);
   note_launch();
   return cudaGetLastError();
 }
@@ -1301,46 +735,38 @@ int bform_box_bytes() { return BOX_BYTES; }
 int bform_kb() { return KB; }
 
 template <class T>
-cudaError_t launch_bform(int shape, const CUtensorMap* tmap, const int2* lists, uint64_t cap,
-                         const uint32_t* counts, uint32_t nrows, int32_t col0, int32_t ncols,
-                         uint32_t nk, uint32_t* splits, uint64_t slice_stride, T* out,
-                         uint64_t ld_out, const DevStatus* st, cudaStream_t s) {
-  if (shape == kShapeWide)
-    // 1024 fp32 / 512 fp64 columns x 16 rows, 16 consumers + producer, 6-stage
-    // ring (192 KB), 1 CTA per SM, 83 registers. Measured against 8 rows x 3
-    // stages x 2 CTAs per SM (tools/exp_time.py): cfg5 1810 -> 1802 ms, cfg2
-    // 0.307 -> 0.285 ms, cfg3 and cfg4 0.3-2% faster -- the deeper ring lets
-    // warps drift 5 k blocks apart instead of 2 (consumers had waited on a
-    // stage 6.5% of the time, ncu). Before the rep loop and list walk were
-    // slimmed (80-83 registers) this shape hit the 96-register cap of 17 warps
-    // and spilled.
-    return launch_ring<T, AFMM_EXP_WIDE_G, AFMM_EXP_WIDE_CW, AFMM_EXP_WIDE_STAGES, AFMM_EXP_WIDE_MINB>(tmap, lists, cap, counts, nrows, col0, ncols, nk,
-                                              splits, slice_stride, out, ld_out, st, s);
-  if (shape == kShapeTmem)
-    // 1024 fp32 / 512 fp64 columns x 16 rows, bases from tensor memory, 1 CTA per SM
-    return launch_tm<T>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits, slice_stride,
-                        out, ld_out, st, s);
-  if (shape == kShapeSmall)  // 256 fp32 / 128 fp64 columns x 4 rows, up to 8 CTAs per SM
-    return launch_ring<T, 2, 4, 3, 8>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits,
-                                      slice_stride, out, ld_out, st, s);
-  return launch_ring<T, 4, 16, 6, 2>(tmap, lists, cap, counts, nrows, col0, ncols, nk, splits,
-                                     slice_stride, out, ld_out, st, s);
+cudaError_t launch_bform(BformLaunch& a, T* out, cudaStream_t s) {
+  switch (a.shape) {
+    case kShapeWide:
+      // 1024 fp32 / 512 fp64 columns x 16 rows, 16 consumers + producer,
+      // 6-stage ring (192 KB), 1 CTA per SM, 83 registers. Measured against 8
+      // rows x 3 stages x 2 CTAs per SM: cfg5 1810 -> 1802 ms, cfg2 0.307 ->
+      // 0.285 ms, cfg3 and cfg4 0.3-2% faster -- the deeper ring lets warps
+      // drift 5 k blocks apart instead of 2 (consumers had waited on a stage
+      // 6.5% of the time, ncu).
+      return launch_ring<T, 8, kWideRows, 6, kWideCtasPerSm, 1>(a, out, s);
+    case kShapeSmall:  // 256 fp32 / 128 fp64 columns x 4 rows, up to 8 CTAs per SM
+      return launch_ring<T, 2, 4, 3, 8, 1>(a, out, s);
+    case kShapeQuad:
+      // 512 fp32 / 256 fp64 columns x 15 quads (60 rows), 12-stage ring (192 KB),
+      // 1 CTA per SM
+      return launch_ring<T, 4, kQuadWarps, 12, 1, 4>(a, out, s);
+    case kShapeQuadSmall:  // 256 fp32 / 128 fp64 columns x 4 quads, up to 4 CTAs per SM
+      return launch_ring<T, 2, 4, 6, 4, 4>(a, out, s);
+    default:  // narrow: 512 fp32 / 256 fp64 columns x 16 rows, 2 CTAs per SM
+      return launch_ring<T, 4, 16, 6, 2, 1>(a, out, s);
+  }
 }
 
-template cudaError_t launch_bform<float>(int, const CUtensorMap*, const int2*, uint64_t,
-                                         const uint32_t*, uint32_t, int32_t, int32_t, uint32_t,
-                                         uint32_t*, uint64_t, float*, uint64_t, const DevStatus*,
-                                         cudaStream_t);
-template cudaError_t launch_bform<double>(int, const CUtensorMap*, const int2*, uint64_t,
-                                          const uint32_t*, uint32_t, int32_t, int32_t, uint32_t,
-                                          uint32_t*, uint64_t, double*, uint64_t,
-                                          const DevStatus*, cudaStream_t);
+template cudaError_t launch_bform<float>(BformLaunch&, float*, cudaStream_t);
+template cudaError_t launch_bform<double>(BformLaunch&, double*, cudaStream_t);
 
 template <class T>
 cudaError_t launch_aform(const CUtensorMap* cmap, const typename AEntry<T>::type* lists,
-                         uint64_t cap, const uint32_t* counts, uint32_t nrows, uint32_t ncols,
-                         uint32_t nk, const uint16_t* rmax, T* out, uint64_t ld_out,
-                         const uint32_t* row_idx, const DevStatus* st, cudaStream_t s) {
+                         uint64_t cap, const uint32_t* counts, uint32_t nrows,
+                         const uint32_t* dyn_nrows, uint32_t ncols, uint32_t nk,
+                         const uint16_t* rmax, T* out, uint64_t ld_out, const uint32_t* row_idx,
+                         const DevStatus* st, cudaStream_t s) {
   using Ag = AformGeo<T>;
   static_assert(Ag::TILE == (int)aform_tile_cols<T>(), "A-form tile width");
   // 16 rows x 12 stages x 1 CTA/SM: 4-5% faster than 8 rows x 6 stages x 2
@@ -1355,48 +781,19 @@ cudaError_t launch_aform(const CUtensorMap* cmap, const typename AEntry<T>::type
   const uint32_t tiles = (ncols + Ag::TILE - 1) / Ag::TILE;
   const uint32_t rpc = balanced_rows(nrows, tiles, CW, MINB);
   dim3 grid((nrows + rpc - 1) / rpc, tiles);
-  kern<<<grid, (CW + 1) * 32, smem, s>>>(*cmap, lists, cap, counts, nrows, rpc, ncols, nkb, rmax,
-                                         tiles, out, ld_out, row_idx, st);
+  kern<<<grid, (CW + 1) * 32, smem, s>>>(*cmap, lists, cap, counts, nrows, dyn_nrows, rpc, ncols,
+                                         nkb, rmax, tiles, out, ld_out, row_idx, st);
   note_launch();
   return cudaGetLastError();
 }
 
 template cudaError_t launch_aform<float>(const CUtensorMap*, const int2*, uint64_t,
-                                         const uint32_t*, uint32_t, uint32_t, uint32_t,
-                                         const uint16_t*, float*, uint64_t, const uint32_t*,
-                                         const DevStatus*, cudaStream_t);
+                                         const uint32_t*, uint32_t, const uint32_t*, uint32_t,
+                                         uint32_t, const uint16_t*, float*, uint64_t,
+                                         const uint32_t*, const DevStatus*, cudaStream_t);
 template cudaError_t launch_aform<double>(const CUtensorMap*, const int4*, uint64_t,
-                                          const uint32_t*, uint32_t, uint32_t, uint32_t,
-                                          const uint16_t*, double*, uint64_t, const uint32_t*,
-                                          const DevStatus*, cudaStream_t);
-
-int bform_mr_rows() { return MR_ROWS; }
-
-template <class T>
-cudaError_t launch_bform_mr(const CUtensorMap* tmap, const CUtensorMap* rmap, uint32_t nrows,
-                            int32_t col0, int32_t ncols, uint32_t nk, T* out, uint64_t ld_out,
-                            const DevStatus* st, cudaStream_t s) {
-  constexpr int G = 4;
-  auto kern = k_bform_mr<T, G>;
-  const size_t smem = mr_smem_bytes<T, G>();
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return e;
-  const uint32_t nkb = (nk + KB - 1) / KB;
-  const bool vec_ok = (ld_out * sizeof(T)) % 16 == 0 &&
-                      (reinterpret_cast<uintptr_t>(out) % 16) == 0;
-  dim3 grid((nrows + MR_ROWS - 1) / MR_ROWS, (ncols + Geo<T, G>::TILE_N - 1) / Geo<T, G>::TILE_N);
-  kern<<<grid, (MR_CW + 1) * 32, smem, s>>>(*tmap, *rmap, nrows, col0, ncols, nk, nkb, out,
-                                            ld_out, vec_ok ? 1 : 0, st);
-  note_launch();
-  return cudaGetLastError();
-}
-
-template cudaError_t launch_bform_mr<float>(const CUtensorMap*, const CUtensorMap*, uint32_t,
-                                            int32_t, int32_t, uint32_t, float*, uint64_t,
-                                            const DevStatus*, cudaStream_t);
-template cudaError_t launch_bform_mr<double>(const CUtensorMap*, const CUtensorMap*, uint32_t,
-                                             int32_t, int32_t, uint32_t, double*, uint64_t,
-                                             const DevStatus*, cudaStream_t);
+                                          const uint32_t*, uint32_t, const uint32_t*, uint32_t,
+                                          uint32_t, const uint16_t*, double*, uint64_t,
+                                          const uint32_t*, const DevStatus*, cudaStream_t);
 
 }  // namespace afmm_dev

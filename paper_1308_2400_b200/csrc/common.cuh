@@ -8,19 +8,29 @@
 
 namespace afmm_dev {
 
-// Device-side status of one product call: first offenders and the exact
-// counts, all written by the prepass. Offenders are stored INVERTED (~key,
-// reduced with atomicMax) so that an all-zero struct means "no error, zero
-// counts" and one memset initialises everything.
+// Device-side status of one product call: first offenders, the exact counts,
+// list overflow and the Case A form chosen on the device, all written by the
+// prepass. Offenders are stored INVERTED (~key, reduced with atomicMax) so
+// that an all-zero struct means "no error, zero counts" and one memset
+// initialises everything.
 struct DevStatus {
   unsigned long long nonfinite_lhs_inv;  // ~(linear index) of first non-finite lhs element
   unsigned long long nonfinite_rhs_inv;
   unsigned long long rep_bad_inv;        // ~((linear index << 2) | kind) of first bad rep
-  unsigned long long rep_too_large_inv;  // ~(linear index) of first |rep| >= 2^31
+  // Longest rep list the product needs when it exceeds the list capacity (0 =
+  // every list fits). Reps beyond an entry's range (|rep| > 2^31 - 1 in the
+  // int2 lists, > 32767 in the quad lists) are split into consecutive entries
+  // at the same k -- the element's |rep| sequential adds stay consecutive, so
+  // the result is unchanged -- and such lists can outgrow the n-entry
+  // capacity; the runtime then re-runs the product with this capacity.
+  unsigned long long list_need;
   unsigned long long additions;
   unsigned long long zero_skips;
-  unsigned long long pad[2];
+  uint32_t a_rows;     // Case A: slab rows the device-side choice gave the A-form
+  uint32_t form_rows;  // Case A: slab rows seen by the choice (0: no choice made)
+  unsigned long long pad;
 };
+static_assert(sizeof(DevStatus) == 64, "DevStatus is one 64-byte record");
 
 // A-form list entry: (k, base) of a nonzero base X[i,k] (k_aform).
 template <class T>
@@ -34,9 +44,9 @@ struct AEntry<double> {
   using type = int4;  // {k, 0, low word, high word}
 };
 
+// Validation failed or a list overflowed: the compute kernels do nothing.
 __device__ __forceinline__ bool status_failed(const DevStatus* st) {
-  return (st->nonfinite_lhs_inv | st->nonfinite_rhs_inv | st->rep_bad_inv |
-          st->rep_too_large_inv) != 0ull;
+  return (st->nonfinite_lhs_inv | st->nonfinite_rhs_inv | st->rep_bad_inv | st->list_need) != 0ull;
 }
 
 // kernels.hpp:31-40 on the widened value: 0 ok, 1 not integer-valued,
@@ -137,11 +147,7 @@ __device__ __forceinline__ void mbar_wait_at(uint32_t addr, uint32_t parity) {
 // after a short system time limit and the retry loop costs issue slots that
 // the FP-bound warps on the same SM sub-partition need (ncu source view: the
 // producer's empty-barrier loop was 11% of all issued instructions).
-#ifndef AFMM_EXP_SUSPEND_NS
 constexpr uint32_t SUSPEND_NS = 1000000;
-#else
-constexpr uint32_t SUSPEND_NS = AFMM_EXP_SUSPEND_NS;
-#endif
 
 __device__ __forceinline__ void mbar_sleep_wait_at(uint32_t addr, uint32_t parity) {
   uint32_t ok = 0;

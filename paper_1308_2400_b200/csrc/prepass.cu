@@ -2,29 +2,37 @@
 //
 // Replaces the inline zero tests and the up-front validation of the
 // reference kernels (/root/reference/proj/include/afmm/kernels.hpp:25-43,
-// :121-130, :150-159) with three streaming passes (one warp per matrix row,
-// 128-bit loads, one read of each operand):
+// :121-130, :150-159) with streaming passes (one warp per matrix row or row
+// quad, 128-bit loads, one read of each operand):
 //
-//   k_scan_stats   both operands: finite check (matrix.hpp:31-35), rep
+//   k_scan_stats   rows of both operands: finite check (matrix.hpp:31-35), rep
 //                  validation of the rep operand (kernels.hpp:25-43; first
 //                  offender by atomicMax on the inverted row-major index), and
 //                  the per-k vector the work formulas need: nnz(Y[k,:]) (Case B)
 //                  or R_k = sum_j |llround Y[k,j]| (Case A)
-//   k_rows         per row i of X: exact additions W_i and zero_skips (closed
-//                  forms of kernels.hpp:119-134 / :148-163), the slab's OpCounts,
-//                  and (Case B) the warp-scan stream compaction of the row's
-//                  nonzero reps into an ordered (k, rep) list: the zero-skip of
-//                  kernels.hpp:151-153 done once instead of per (i,k,j)
-//   k_transpose_compact  (Case A) the same compaction for the columns of Y,
+//   k_rows         rows of X: exact additions W_i and zero_skips (closed forms
+//                  of kernels.hpp:119-134 / :148-163), the slab's OpCounts, and
+//                  (Case B, one row per list) the warp-scan stream compaction of
+//                  the row's nonzero reps into an ordered (k, rep) list: the
+//                  zero-skip of kernels.hpp:151-153 done once instead of per (i,k,j)
+//   k_rows_quad    Case B, lists of row QUADS: per k where any of four
+//                  consecutive rows has a nonzero rep, one entry holding the four
+//                  reps (k_bform R = 4)
+//   k_transpose_compact  (Case A) the same compactions for the columns of Y,
 //                  through 32x33 smem tiles (the rep list of B-form row j is
-//                  column j of Y)
+//                  column j of Y; a quad is four adjacent columns)
+//   k_counts_f16, k_choose, k_acompact  the A-form inputs and the device-side
+//                  A-form / B-form choice (costmodel.h)
 //
 // plus k_transpose (Case A operand/result transposes) and k_reduce_slices
 // (fast-mode split-k combine). All are HBM-bound; none does FP arithmetic on
 // the product.
 #include <cuda_fp16.h>
 
+#include <type_traits>
+
 #include "common.cuh"
+#include "costmodel.h"
 #include "kernels.h"
 
 namespace afmm_dev {
@@ -32,6 +40,9 @@ namespace afmm_dev {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
+// Largest |rep| one list entry holds: int32 reps (R = 1 lists), int16 reps (quads).
+constexpr unsigned long long kMaxRep1 = 0x7fffffffull;
+constexpr unsigned long long kMaxRep4 = 0x7fffull;
 
 __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
 #pragma unroll
@@ -78,23 +89,58 @@ __device__ __forceinline__ void load4(const T* row, uint32_t j, uint32_t n, bool
   }
 }
 
-__device__ __forceinline__ long long abs_ll(long long r) { return r < 0 ? -r : r; }
+__device__ __forceinline__ unsigned long long abs_ll(long long r) {
+  return r < 0 ? 0ull - (unsigned long long)r : (unsigned long long)r;
+}
 
-// warp task t < n: lhs row t; t >= n: rhs row t - n.
+// The rep of an element as the reference reads it: value == 0.0 or
+// llround == 0 both mean "no term" (kernels.hpp:128-130, :151-153).
+template <class T>
+__device__ __forceinline__ long long rep_of(T v) {
+  return v != T(0) ? llround((double)v) : 0ll;
+}
+
+// List entries a term of magnitude a needs when an entry holds at most M.
+__device__ __forceinline__ uint32_t entries_for(unsigned long long a, unsigned long long M) {
+  if (a <= M) return a != 0 ? 1u : 0u;
+  const unsigned long long c = (a + M - 1) / M;
+  return c > 0x00ffffffull ? 0x00ffffffu : (uint32_t)c;  // saturates: such a list cannot be allocated
+}
+
+// Part c of a term split into entries of at most M: the first parts are M.
+__device__ __forceinline__ long long part_of(long long r, uint32_t c, unsigned long long M) {
+  const unsigned long long a = abs_ll(r), done = (unsigned long long)c * M;
+  if (a <= done) return 0;
+  const unsigned long long p = a - done < M ? a - done : M;
+  return r < 0 ? -(long long)p : (long long)p;
+}
+
+__device__ __forceinline__ uint32_t pack2(long long lo, long long hi) {
+  return ((uint32_t)(uint16_t)(int16_t)lo) | ((uint32_t)(uint16_t)(int16_t)hi << 16);
+}
+
+// Record the length of a list that does not fit (the runtime re-runs with it).
+__device__ __forceinline__ void note_list(DevStatus* st, unsigned long long len, uint64_t cap) {
+  if (len > cap) atomicMax(&st->list_need, len);
+}
+
+// warp task t < (l1 - l0): lhs row l0 + t; then rhs rows q0 .. q1 - 1.
 template <class T>
 __global__ void k_scan_stats(const T* __restrict__ lhs, const T* __restrict__ rhs, uint64_t ld,
-                             uint32_t n, int which_case, int vec, DevStatus* st,
-                             uint32_t* __restrict__ nnz, unsigned long long* __restrict__ rsum) {
+                             uint32_t n, int which_case, int vec, uint32_t l0, uint32_t l1,
+                             uint32_t q0, uint32_t q1, DevStatus* st, uint32_t* __restrict__ nnz,
+                             unsigned long long* __restrict__ rsum) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t t = warp; t < 2ull * n; t += nwarps) {
-    const bool is_rhs = t >= n;
-    const uint64_t i = is_rhs ? t - n : t;
+  const uint64_t ntl = l1 - l0, ntask = ntl + (q1 - q0);
+  for (uint64_t t = warp; t < ntask; t += nwarps) {
+    const bool is_rhs = t >= ntl;
+    const uint64_t i = is_rhs ? q0 + (t - ntl) : l0 + t;
     const T* row = (is_rhs ? rhs : lhs) + i * ld;
     // Case A validates rhs (kernels.hpp:115), Case B lhs (:144)
     const bool is_rep = is_rhs == (which_case == 0);
-    unsigned long long nf = 0, rb = 0, tl = 0;  // inverted keys, 0 = none
+    unsigned long long nf = 0, rb = 0;  // inverted keys, 0 = none
     uint32_t cnt = 0;
     unsigned long long s = 0;
     for (uint32_t j0 = 4 * lane; j0 < n; j0 += 128) {
@@ -110,22 +156,20 @@ __global__ void k_scan_stats(const T* __restrict__ lhs, const T* __restrict__ rh
         if (is_rep) {
           const int kind = rep_kind(d);
           if (kind && rb == 0) rb = ~((lin << 2) | (unsigned long long)kind);
-          else if (!kind && tl == 0 && fabs(d) >= 2147483647.5) tl = ~lin;
         }
         if (is_rhs) {
           cnt += v[e] != T(0) ? 1u : 0u;
-          if (v[e] != T(0)) s += (unsigned long long)abs_ll(llround(d));
+          if (v[e] != T(0) && isfinite(d) && fabs(d) <= 9007199254740992.0)
+            s += abs_ll(llround(d));
         }
       }
     }
-    if (__any_sync(FULL, (nf | rb | tl) != 0)) {
+    if (__any_sync(FULL, (nf | rb) != 0)) {
       nf = warp_max_u64(nf);
       rb = warp_max_u64(rb);
-      tl = warp_max_u64(tl);
       if (lane == 0) {
         if (nf) atomicMax(is_rhs ? &st->nonfinite_rhs_inv : &st->nonfinite_lhs_inv, nf);
         if (rb) atomicMax(&st->rep_bad_inv, rb);
-        if (tl) atomicMax(&st->rep_too_large_inv, tl);
       }
     }
     if (is_rhs) {
@@ -141,29 +185,28 @@ __global__ void k_scan_stats(const T* __restrict__ lhs, const T* __restrict__ rh
   }
 }
 
-// Per row i of X (all n rows): W_i -> work[i]; rows in [r0, r1) add to the
-// slab OpCounts and (Case B, lists != nullptr) get their compacted rep list.
+// Rows i in [a0, a1) of X: W_i -> work[i] (when work != nullptr); rows in the
+// slab [r0, r1) add to the slab OpCounts and get (Case B, lists != nullptr)
+// their compacted rep list / (Case A, nnz_row != nullptr) their nonzero-base
+// count.
 // Case A: W_i = sum_{k: X[i,k] != 0} R_k, zs_i = #{k: X[i,k] == 0}
 // Case B: W_i = sum_k |rep_ik| nnz_k,    zs_i = sum_{k: rep_ik != 0} (n - nnz_k)
-// A rep is skipped exactly when the reference skips it: value == 0.0 or
-// llround == 0 (kernels.hpp:151-153).
 template <class T>
 __global__ void k_rows(const T* __restrict__ x, uint64_t ld, uint32_t n, int which_case, int vec,
                        const uint32_t* __restrict__ nnz,
-                       const unsigned long long* __restrict__ rsum, uint32_t r0, uint32_t r1,
-                       int2* __restrict__ lists, uint64_t cap, uint32_t* __restrict__ counts,
-                       unsigned long long* __restrict__ work, DevStatus* st,
-                       uint32_t* __restrict__ nnz_row) {
+                       const unsigned long long* __restrict__ rsum, uint32_t a0, uint32_t a1,
+                       uint32_t r0, uint32_t r1, int2* __restrict__ lists, uint64_t cap,
+                       uint32_t* __restrict__ counts, unsigned long long* __restrict__ work,
+                       DevStatus* st, uint32_t* __restrict__ nnz_row) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t i = warp; i < n; i += nwarps) {
+  for (uint64_t i = a0 + warp; i < a1; i += nwarps) {
     const T* row = x + i * ld;
     const bool in_slab = i >= r0 && i < r1;
     const bool compact = which_case == 1 && in_slab && lists != nullptr;
     int2* out = compact ? lists + (i - r0) * cap : nullptr;
-    unsigned long long w = 0, z = 0;
-    uint32_t base = 0;
+    unsigned long long w = 0, z = 0, base = 0;
     for (uint32_t c0 = 0; c0 < n; c0 += 128) {  // warp-uniform trip count (the scan below)
       const uint32_t j0 = c0 + 4 * lane;
       T v[4];
@@ -172,8 +215,7 @@ __global__ void k_rows(const T* __restrict__ x, uint64_t ld, uint32_t n, int whi
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const uint32_t j = j0 + e;
-        rep[e] = 0;
-        if (j < n && v[e] != T(0)) rep[e] = llround((double)v[e]);
+        rep[e] = j < n ? rep_of(v[e]) : 0;
         if (which_case == 0) {
           if (j < n) {
             if (v[e] == T(0)) ++z;
@@ -181,28 +223,43 @@ __global__ void k_rows(const T* __restrict__ x, uint64_t ld, uint32_t n, int whi
           }
         } else if (rep[e] != 0) {
           const unsigned long long nb = nnz[j];
-          w += (unsigned long long)abs_ll(rep[e]) * nb;  // count bookkeeping, not an element product
+          w += abs_ll(rep[e]) * nb;  // count bookkeeping, not an element product
           z += (unsigned long long)n - nb;
         }
       }
       if (compact) {
-        const uint32_t mine = (rep[0] != 0) + (rep[1] != 0) + (rep[2] != 0) + (rep[3] != 0);
-        uint32_t total;
-        uint32_t pos = base + warp_excl_scan(mine, lane, &total);
+        uint32_t ne[4], mine = 0;
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (rep[e] != 0) out[pos++] = make_int2((int)(j0 + e), (int)rep[e]);
+        for (int e = 0; e < 4; ++e) {
+          ne[e] = entries_for(abs_ll(rep[e]), kMaxRep1);
+          mine += ne[e];
+        }
+        uint32_t total;
+        unsigned long long pos = base + warp_excl_scan(mine, lane, &total);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (ne[e] == 1) {
+            if (pos < cap) out[pos] = make_int2((int)(j0 + e), (int)rep[e]);
+            ++pos;
+          } else {
+            for (uint32_t c = 0; c < ne[e]; ++c, ++pos)
+              if (pos < cap) out[pos] = make_int2((int)(j0 + e), (int)part_of(rep[e], c, kMaxRep1));
+          }
+        }
         base += total;
       }
     }
     w = warp_sum_u64(w);
     z = warp_sum_u64(z);
     if (lane == 0) {
-      work[i] = w;
+      if (work) work[i] = w;
       if (in_slab) {
         if (w) atomicAdd(&st->additions, w);
         if (z) atomicAdd(&st->zero_skips, z);
-        if (compact) counts[i - r0] = base;
+        if (compact) {
+          counts[i - r0] = (uint32_t)(base < 0xffffffffull ? base : 0xffffffffull);
+          note_list(st, base, cap);
+        }
         // Case A: nonzero bases of the row (its A-form cost)
         if (nnz_row && which_case == 0) nnz_row[i - r0] = n - (uint32_t)z;
       }
@@ -210,18 +267,96 @@ __global__ void k_rows(const T* __restrict__ x, uint64_t ld, uint32_t n, int whi
   }
 }
 
-// Case A rep lists: B-form row j = column j of Y. A block owns 32 columns and
-// walks k in 32-row tiles through smem; warp w compacts columns 4w..4w+3.
+// Case B quad lists: slab rows r0 + 4q .. r0 + 4q + 3 (rows >= r1 are empty).
+// One entry per k where any of the four reps is nonzero: {k, rep0|rep1<<16,
+// rep2|rep3<<16, 0}; a |rep| beyond int16 is continued in further entries at
+// the same k. Also adds the slab's OpCounts.
 template <class T>
-__global__ void __launch_bounds__(256) k_transpose_compact(const T* __restrict__ y, uint64_t ld,
-                                                           uint32_t n, int2* __restrict__ lists,
-                                                           uint64_t cap,
-                                                           uint32_t* __restrict__ counts) {
+__global__ void k_rows_quad(const T* __restrict__ x, uint64_t ld, uint32_t n, int vec,
+                            const uint32_t* __restrict__ nnz, uint32_t r0, uint32_t r1,
+                            int4* __restrict__ lists, uint64_t cap, uint32_t* __restrict__ counts,
+                            DevStatus* st) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t rows = r1 - r0, nq = (rows + 3) / 4;
+  for (uint64_t q = warp; q < nq; q += nwarps) {
+    int4* out = lists + q * cap;
+    unsigned long long w = 0, z = 0, base = 0;
+    for (uint32_t c0 = 0; c0 < n; c0 += 128) {
+      const uint32_t j0 = c0 + 4 * lane;
+      long long rep[4][4];  // [row of the quad][element]
+#pragma unroll
+      for (int qr = 0; qr < 4; ++qr) {
+        const uint32_t r = 4 * (uint32_t)q + qr;
+        T v[4] = {T(0), T(0), T(0), T(0)};
+        if (r < rows) load4(x + (uint64_t)(r0 + r) * ld, j0, n, vec != 0, v);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          rep[qr][e] = j0 + e < n ? rep_of(v[e]) : 0;
+          if (rep[qr][e] != 0) {
+            const unsigned long long nb = nnz[j0 + e];
+            w += abs_ll(rep[qr][e]) * nb;
+            z += (unsigned long long)n - nb;
+          }
+        }
+      }
+      uint32_t ne[4], mine = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        ne[e] = 0;
+#pragma unroll
+        for (int qr = 0; qr < 4; ++qr) ne[e] = max(ne[e], entries_for(abs_ll(rep[qr][e]), kMaxRep4));
+        mine += ne[e];
+      }
+      uint32_t total;
+      unsigned long long pos = base + warp_excl_scan(mine, lane, &total);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (ne[e] == 1) {
+          if (pos < cap)
+            out[pos] = make_int4((int)(j0 + e), (int)pack2(rep[0][e], rep[1][e]),
+                                 (int)pack2(rep[2][e], rep[3][e]), 0);
+          ++pos;
+        } else {
+          for (uint32_t c = 0; c < ne[e]; ++c, ++pos)
+            if (pos < cap)
+              out[pos] = make_int4(
+                  (int)(j0 + e),
+                  (int)pack2(part_of(rep[0][e], c, kMaxRep4), part_of(rep[1][e], c, kMaxRep4)),
+                  (int)pack2(part_of(rep[2][e], c, kMaxRep4), part_of(rep[3][e], c, kMaxRep4)),
+                  0);
+        }
+      }
+      base += total;
+    }
+    w = warp_sum_u64(w);
+    z = warp_sum_u64(z);
+    if (lane == 0) {
+      if (w) atomicAdd(&st->additions, w);
+      if (z) atomicAdd(&st->zero_skips, z);
+      counts[q] = (uint32_t)(base < 0xffffffffull ? base : 0xffffffffull);
+      note_list(st, base, cap);
+    }
+  }
+}
+
+// Case A rep lists: B-form row j = column j of Y. A block owns 32 columns and
+// walks k in 32-row tiles through smem. R = 1: warp w compacts columns
+// 4w..4w+3 one list each; R = 4: warp w compacts the quad of columns 4w..4w+3
+// into one list. skip (optional): nothing to do when *skip == 0 (the
+// device-side Case A choice gave every row to the A-form).
+template <class T, int R>
+__global__ void __launch_bounds__(256)
+    k_transpose_compact(const T* __restrict__ y, uint64_t ld, uint32_t n,
+                        typename std::conditional<R == 1, int2, int4>::type* __restrict__ lists,
+                        uint64_t cap, uint32_t* __restrict__ counts, DevStatus* st,
+                        const uint32_t* __restrict__ skip) {
+  if (skip && *skip == 0) return;
   __shared__ T tile[32][33];
   const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const uint32_t j0 = blockIdx.x * 32;
-  const unsigned lt = (1u << tx) - 1u;
-  uint32_t base[4] = {0, 0, 0, 0};
+  unsigned long long base[R == 1 ? 4 : 1] = {};
   // the next 32-row tile is loaded into registers while this one is compacted
   // (the block walks k serially, so unhidden load latency is its whole cost
   // at small n)
@@ -239,24 +374,59 @@ __global__ void __launch_bounds__(256) k_transpose_compact(const T* __restrict__
     for (int q = 0; q < 4; ++q) tile[ty + 8 * q][tx] = pre[q];
     __syncthreads();
     if (k0 + 32 < n) fetch(k0 + 32);
+    const uint32_t k = k0 + tx;
+    if constexpr (R == 1) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint32_t jj = ty * 4 + q, j = j0 + jj;
-      const T v = tile[tx][jj];  // Y[k0 + tx, j]
-      int rep = 0;
-      if (v != T(0) && k0 + tx < n) rep = (int)llround((double)v);
-      const unsigned m = __ballot_sync(FULL, rep != 0);
-      if (rep != 0 && j < n) lists[(uint64_t)j * cap + base[q] + __popc(m & lt)] =
-          make_int2((int)(k0 + tx), rep);
-      base[q] += __popc(m);
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t j = j0 + ty * 4 + q;
+        const long long rep = k < n ? rep_of(tile[tx][ty * 4 + q]) : 0;  // Y[k, j]
+        const uint32_t ne = entries_for(abs_ll(rep), kMaxRep1);
+        uint32_t total;
+        unsigned long long pos = base[q] + warp_excl_scan(ne, tx, &total);
+        if (j < n)
+          for (uint32_t c = 0; c < ne; ++c, ++pos)
+            if (pos < cap)
+              lists[(uint64_t)j * cap + pos] =
+                  make_int2((int)k, (int)(ne == 1 ? rep : part_of(rep, c, kMaxRep1)));
+        base[q] += total;
+      }
+    } else {
+      long long rep[4];
+      uint32_t ne = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        rep[q] = (k < n && j0 + ty * 4 + q < n) ? rep_of(tile[tx][ty * 4 + q]) : 0;
+        ne = max(ne, entries_for(abs_ll(rep[q]), kMaxRep4));
+      }
+      uint32_t total;
+      unsigned long long pos = base[0] + warp_excl_scan(ne, tx, &total);
+      const uint64_t quad = (j0 >> 2) + ty;
+      if (j0 + ty * 4 < n)
+        for (uint32_t c = 0; c < ne; ++c, ++pos)
+          if (pos < cap)
+            lists[quad * cap + pos] =
+                ne == 1 ? make_int4((int)k, (int)pack2(rep[0], rep[1]), (int)pack2(rep[2], rep[3]), 0)
+                        : make_int4((int)k,
+                                    (int)pack2(part_of(rep[0], c, kMaxRep4), part_of(rep[1], c, kMaxRep4)),
+                                    (int)pack2(part_of(rep[2], c, kMaxRep4), part_of(rep[3], c, kMaxRep4)),
+                                    0);
+      base[0] += total;
     }
     __syncthreads();
   }
   if (tx == 0) {
+    if constexpr (R == 1) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint32_t j = j0 + ty * 4 + q;
-      if (j < n) counts[j] = base[q];
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t j = j0 + ty * 4 + q;
+        if (j < n) {
+          counts[j] = (uint32_t)(base[q] < 0xffffffffull ? base[q] : 0xffffffffull);
+          note_list(st, base[q], cap);
+        }
+      }
+    } else if (j0 + ty * 4 < n) {
+      counts[(j0 >> 2) + ty] = (uint32_t)(base[0] < 0xffffffffull ? base[0] : 0xffffffffull);
+      note_list(st, base[0], cap);
     }
   }
 }
@@ -268,8 +438,8 @@ __global__ void __launch_bounds__(256) k_transpose_compact(const T* __restrict__
 // and per (k, column tile) the largest |rep| (the warp-uniform trip count of
 // the predicated add loop) with bit 15 set when the tile row holds a negative
 // rep. One warp per (k, tile).
-// fstats (optional): [0] nonzero reps, [1] sum of the per-(k, tile) trip counts,
-// [2] reps beyond 2048, [3] sum of |rep| -- the A-form / B-form cost inputs.
+// fstats (accumulated): [0] nonzero reps, [1] sum of the per-(k, tile) trip
+// counts, [2] reps beyond 2048, [3] sum of |rep| -- the cost-model inputs.
 template <class T>
 __global__ void k_counts_f16(const T* __restrict__ y, uint64_t ld, uint32_t n, uint32_t tile_cols,
                              uint32_t ntiles, __half* __restrict__ cnt, uint64_t ldc,
@@ -284,9 +454,9 @@ __global__ void k_counts_f16(const T* __restrict__ y, uint64_t ld, uint32_t n, u
     unsigned long long sum = 0;
     for (uint32_t c = t * tile_cols + lane; c < (t + 1) * tile_cols && c < n; c += 32) {
       const T v = y[k * ld + c];
-      long long r = v != T(0) ? llround((double)v) : 0;
+      long long r = rep_of(v);
       nz += r != 0 ? 1u : 0u;
-      sum += (unsigned long long)abs_ll(r);
+      sum += abs_ll(r);
       if (r > 2048 || r < -2048) {
         big += 1;
         r = r > 0 ? 2048 : -2048;
@@ -307,25 +477,182 @@ __global__ void k_counts_f16(const T* __restrict__ y, uint64_t ld, uint32_t n, u
     sum = warp_sum_u64(sum);
     if (lane == 0) {
       rmax[k * ntiles + t] = (uint16_t)(mx | (neg ? 0x8000u : 0u));
-      if (fstats) {
-        if (nz) atomicAdd(&fstats[0], (unsigned long long)nz);
-        if (mx) atomicAdd(&fstats[1], (unsigned long long)mx);
-        if (big) atomicAdd(&fstats[2], (unsigned long long)big);
-        if (sum) atomicAdd(&fstats[3], sum);
-      }
+      if (nz) atomicAdd(&fstats[0], (unsigned long long)nz);
+      if (mx) atomicAdd(&fstats[1], (unsigned long long)mx);
+      if (big) atomicAdd(&fstats[2], (unsigned long long)big);
+      if (sum) atomicAdd(&fstats[3], sum);
     }
   }
 }
 
-// A-form lists: row i in [r0, r1) of X -> its nonzero bases (k, X[i,k]) in
-// increasing k (the zero-base skip of kernels.hpp:121-125 done once).
-// rows_idx (optional): task t compacts slab row rows_idx[t] (else t); lists
-// and counts are indexed by slab row either way.
+// Device-side Case A choice (one CTA): from the slab rows' nonzero-base
+// counts and the statistics of Y, evaluate the cost model (costmodel.h) and
+// write plan[0] = m (A-form rows), plan[1] = rows - m (B-form rows), and the
+// row order ridx: the A rows first (the m sparsest, by nonzero count, ties in
+// row order), then the B rows in ascending order (identity unless split).
+// scratch: 3 * (n + 2) words.
+constexpr int kChooseThreads = 1024;
+constexpr int kChooseCands = 1024;  // split candidates evaluated (j < 1024 B tiles)
+
+__global__ void __launch_bounds__(kChooseThreads)
+    k_choose(CaseAModel md, uint32_t rows, int variant, const uint32_t* __restrict__ nnz_row,
+             const unsigned long long* __restrict__ fstats, uint32_t* __restrict__ scratch,
+             uint32_t* __restrict__ plan, uint32_t* __restrict__ ridx, DevStatus* st) {
+  __shared__ double s_pre[kChooseCands + 1];
+  __shared__ uint32_t s_m, s_vstar, s_tstar;
+  __shared__ uint32_t s_wsum[32];
+  const uint32_t tid = threadIdx.x, n = (uint32_t)md.n;
+  const uint32_t nb = n + 2;  // values 0..n, plus one past the end
+  uint32_t* hist = scratch;             // count of rows per nonzero-base value
+  uint32_t* cum = scratch + nb;         // rows with value < v (then: next A slot of value v)
+  unsigned long long* csum = reinterpret_cast<unsigned long long*>(scratch + 2 * nb);  // 8-byte aligned
+  md.nnz_y = fstats[0];
+  md.trip_sum = fstats[1];
+  md.rep_sum = fstats[3];
+  const bool a_ok = fstats[2] == 0;  // every |rep| <= 2048 (exact fp16 counts)
+
+  for (uint32_t v = tid; v < nb; v += kChooseThreads) hist[v] = 0;
+  __syncthreads();
+  for (uint32_t i = tid; i < rows; i += kChooseThreads) atomicAdd(&hist[min(nnz_row[i], n)], 1u);
+  __syncthreads();
+  // exclusive scans over the values: each thread a contiguous chunk
+  const uint32_t per = (nb + kChooseThreads - 1) / kChooseThreads;
+  const uint32_t v0 = min(tid * per, nb), v1 = min(v0 + per, nb);
+  uint32_t lc = 0;
+  unsigned long long ls = 0;
+  for (uint32_t v = v0; v < v1; ++v) {
+    lc += hist[v];
+    ls += (unsigned long long)hist[v] * v;
+  }
+  // block exclusive scan of (lc, ls): warp scans + warp totals
+  const uint32_t lane = tid & 31, wid = tid >> 5;
+  uint32_t xc = lc;
+  unsigned long long xs = ls;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t yc = __shfl_up_sync(FULL, xc, o);
+    const unsigned long long ys = __shfl_up_sync(FULL, xs, o);
+    if (lane >= (uint32_t)o) {
+      xc += yc;
+      xs += ys;
+    }
+  }
+  __shared__ unsigned long long s_wsum_s[32];
+  if (lane == 31) {
+    s_wsum[wid] = xc;
+    s_wsum_s[wid] = xs;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t c = s_wsum[lane];
+    unsigned long long sm = s_wsum_s[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t yc = __shfl_up_sync(FULL, c, o);
+      const unsigned long long ys = __shfl_up_sync(FULL, sm, o);
+      if (lane >= (uint32_t)o) {
+        c += yc;
+        sm += ys;
+      }
+    }
+    s_wsum[lane] = c - s_wsum[lane];        // exclusive warp offsets
+    s_wsum_s[lane] = sm - s_wsum_s[lane];
+  }
+  __syncthreads();
+  uint32_t rc = s_wsum[wid] + xc - lc;
+  unsigned long long rs = s_wsum_s[wid] + xs - ls;
+  for (uint32_t v = v0; v < v1; ++v) {
+    cum[v] = rc;
+    csum[v] = rs;
+    rc += hist[v];
+    rs += (unsigned long long)hist[v] * v;
+  }
+  __syncthreads();
+  // nonzero bases of the m sparsest rows: value v* with cum[v*] <= m < cum[v*+1]
+  auto pre_of = [&](uint64_t m, uint32_t* vstar) -> double {
+    uint32_t lo = 0, hi = n + 1;  // largest v with cum[v] <= m
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      if (cum[mid] <= m) lo = mid;
+      else hi = mid - 1;
+    }
+    if (vstar) *vstar = lo;
+    return (double)csum[lo] + (double)lo * (double)(m - cum[lo]);
+  };
+  const uint64_t tb = md.b_tile;
+  // candidate c: c = 0 -> m = rows (pure A), c = j >= 1 -> m = rows - j * tb
+  for (uint32_t c = tid; c <= kChooseCands; c += kChooseThreads) {
+    const uint64_t m = c == 0 ? rows : (uint64_t)rows - (uint64_t)c * tb;
+    s_pre[c] = (c == 0 || (uint64_t)c * tb < rows) ? pre_of(m, nullptr) : 0.0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint64_t m = 0;
+    if (a_ok && rows > 0 && (rows - 1) / tb < (uint64_t)kChooseCands) {
+      m = choose_aform_rows(md, rows, variant, [&](uint64_t mm) {
+        return mm == rows ? s_pre[0] : s_pre[(rows - mm) / tb];
+      });
+    }
+    s_m = (uint32_t)m;
+    plan[0] = (uint32_t)m;
+    plan[1] = rows - (uint32_t)m;
+    st->a_rows = (uint32_t)m;
+    st->form_rows = rows;
+    uint32_t vstar = 0;
+    if (m > 0 && m < rows) pre_of(m, &vstar);
+    s_vstar = vstar;
+    s_tstar = (m > 0 && m < rows) ? (uint32_t)(m - cum[vstar]) : 0u;
+  }
+  __syncthreads();
+  const uint32_t m = s_m;
+  if (m == 0 || m == rows) {
+    for (uint32_t i = tid; i < rows; i += kChooseThreads) ridx[i] = i;
+    return;
+  }
+  // split: a stable counting sort of the A rows, B rows in ascending order
+  // (one warp walks the rows in order; cum[v] becomes the next slot of value v)
+  if (wid != 0) return;
+  const uint32_t vstar = s_vstar, tstar = s_tstar;
+  uint32_t run_eq = 0, run_b = 0;
+  for (uint32_t i0 = 0; i0 < rows; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const bool valid = i < rows;
+    const uint32_t v = valid ? min(nnz_row[i], n) : 0u;
+    const unsigned lt = (1u << lane) - 1u;
+    const bool is_eq = valid && v == vstar;
+    const unsigned eq_mask = __ballot_sync(FULL, is_eq);
+    const uint32_t rank_eq = run_eq + __popc(eq_mask & lt);
+    const bool is_a = valid && (v < vstar || (is_eq && rank_eq < tstar));
+    const bool is_b = valid && !is_a;
+    const unsigned b_mask = __ballot_sync(FULL, is_b);
+    const uint32_t key = is_a ? v : (0x80000000u | lane);
+    const unsigned peers = __match_any_sync(FULL, key);
+    const uint32_t leader = __ffs(peers) - 1;
+    uint32_t slot = 0;
+    if (is_a && lane == leader) {
+      slot = cum[v];
+      cum[v] = slot + __popc(peers);
+    }
+    slot = __shfl_sync(FULL, slot, leader);
+    if (is_a) ridx[slot + __popc(peers & lt)] = i;
+    if (is_b) ridx[m + run_b + __popc(b_mask & lt)] = i;
+    run_eq += __popc(eq_mask);
+    run_b += __popc(b_mask);
+    __syncwarp();
+  }
+}
+
+// A-form lists: tasks t < ntask (or *dyn_ntask) compact slab row q = rows_idx[t]
+// (or t) of X -> its nonzero bases (k, X[r0 + q, k]) in increasing k (the
+// zero-base skip of kernels.hpp:121-125 done once); lists / counts are indexed
+// by slab row.
 template <class T>
 __global__ void k_acompact(const T* __restrict__ x, uint64_t ld, uint32_t n, int vec, uint32_t r0,
-                           uint32_t ntask, const uint32_t* __restrict__ rows_idx,
+                           uint32_t ntask, const uint32_t* __restrict__ dyn_ntask,
+                           const uint32_t* __restrict__ rows_idx,
                            typename AEntry<T>::type* __restrict__ lists, uint64_t cap,
                            uint32_t* __restrict__ counts) {
+  if (dyn_ntask) ntask = *dyn_ntask;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -357,55 +684,30 @@ __global__ void k_acompact(const T* __restrict__ x, uint64_t ld, uint32_t n, int
   }
 }
 
-// Dense int32 reps for k_bform_mr: dst[r][c] = llround(src[r][c]) or, with
-// transpose, llround(src[c][r]); zero reps stay 0 (value == 0.0 or llround == 0
-// both skip, kernels.hpp:128-130 / :151-153). 32x33 smem tiles.
-template <class T>
-__global__ void k_reps_dense(const T* __restrict__ src, uint64_t ld_src, uint32_t rows,
-                             uint32_t cols, int transpose, int32_t* __restrict__ dst,
-                             uint64_t ld_dst) {
-  __shared__ int32_t tile[32][33];
-  const uint32_t c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
-  // destination tile rows [r0, r0+32) x cols [c0, c0+32)
-  for (uint32_t dy = threadIdx.y; dy < 32; dy += blockDim.y) {
-    int32_t v = 0;
-    if (transpose) {
-      // read src row (c0 + dy), columns r0 + tx  -> dst[r0 + tx][c0 + dy]
-      const uint32_t sr = c0 + dy, sc = r0 + threadIdx.x;
-      if (sr < cols && sc < rows) {
-        const T x = src[(uint64_t)sr * ld_src + sc];
-        if (x != T(0)) v = (int32_t)llround((double)x);
-      }
-    } else {
-      const uint32_t sr = r0 + dy, sc = c0 + threadIdx.x;
-      if (sr < rows && sc < cols) {
-        const T x = src[(uint64_t)sr * ld_src + sc];
-        if (x != T(0)) v = (int32_t)llround((double)x);
-      }
-    }
-    tile[dy][threadIdx.x] = v;
-  }
-  __syncthreads();
-  for (uint32_t dy = threadIdx.y; dy < 32; dy += blockDim.y) {
-    const uint32_t r = r0 + dy, c = c0 + threadIdx.x;
-    if (r < rows && c < cols)
-      dst[(uint64_t)r * ld_dst + c] = transpose ? tile[threadIdx.x][dy] : tile[dy][threadIdx.x];
-  }
-}
-
 // out[oc * ld_out + r] = in[ir * ld_in + c] for r < rows, c < cols, with
 // ir = in_rows ? in_rows[r] : r and oc = out_rows ? out_rows[c] : c (the row
 // maps gather / scatter the rows of a Case A split between the two kernels).
+// plan (optional, the device-side choice): dyn = 1 -> rows = plan[1] and
+// in_rows += plan[0]; dyn = 2 -> cols = plan[1] and out_rows += plan[0].
 template <class T>
 __global__ void k_transpose(const T* __restrict__ in, uint64_t ld_in, uint32_t rows,
                             uint32_t cols, T* __restrict__ out, uint64_t ld_out,
                             const uint32_t* __restrict__ in_rows,
-                            const uint32_t* __restrict__ out_rows, const DevStatus* st) {
+                            const uint32_t* __restrict__ out_rows, const DevStatus* st,
+                            const uint32_t* __restrict__ plan, int dyn) {
   // the result transpose writes Z only for a valid product (out untouched on
   // a validation error, like the kernels that write Z directly)
   if (st && status_failed(st)) return;
-  __shared__ T tile[32][33];
+  if (dyn == 1) {
+    rows = plan[1];
+    in_rows += plan[0];
+  } else if (dyn == 2) {
+    cols = plan[1];
+    out_rows += plan[0];
+  }
   const uint32_t c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  if (c0 >= cols || r0 >= rows) return;
+  __shared__ T tile[32][33];
   for (uint32_t dy = threadIdx.y; dy < 32; dy += blockDim.y) {
     const uint32_t r = r0 + dy, c = c0 + threadIdx.x;
     if (r < rows && c < cols) {
@@ -425,12 +727,14 @@ __global__ void k_transpose(const T* __restrict__ in, uint64_t ld_in, uint32_t r
 
 // Fast mode: combine the k-slice partial products in ascending slice order
 // (deterministic; the reassociation the fast mode allows is exactly this
-// regrouping of each element's k-sum).
+// regrouping of each element's k-sum). dyn_cols (optional): cols on the device.
 template <class T>
 __global__ void k_reduce_slices(const T* __restrict__ part, uint64_t stride, uint64_t ld_part,
                                 uint32_t splits, uint32_t rows, uint32_t cols,
-                                T* __restrict__ out, uint64_t ld_out, const DevStatus* st) {
+                                T* __restrict__ out, uint64_t ld_out, const DevStatus* st,
+                                const uint32_t* __restrict__ dyn_cols) {
   if (status_failed(st)) return;
+  if (dyn_cols) cols = *dyn_cols;
   const uint64_t total = (uint64_t)rows * cols;
   for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (uint64_t)gridDim.x * blockDim.x) {
@@ -460,20 +764,35 @@ int vec_ok(const T* p, uint64_t ld) {
 
 template <class T>
 void launch_scan_stats(const T* lhs, const T* rhs, uint64_t ld, uint32_t n, int which_case,
-                       DevStatus* st, uint32_t* nnz, unsigned long long* rsum, cudaStream_t s) {
+                       uint32_t l0, uint32_t l1, uint32_t q0, uint32_t q1, DevStatus* st,
+                       uint32_t* nnz, unsigned long long* rsum, cudaStream_t s) {
   const int vec = vec_ok(lhs, ld) & vec_ok(rhs, ld);
-  k_scan_stats<T><<<grid_for_warps(2ull * n, 8), 256, 0, s>>>(lhs, rhs, ld, n, which_case, vec,
-                                                               st, nnz, rsum);
+  const uint64_t tasks = (uint64_t)(l1 - l0) + (q1 - q0);
+  if (tasks == 0) return;
+  k_scan_stats<T><<<grid_for_warps(tasks, 8), 256, 0, s>>>(lhs, rhs, ld, n, which_case, vec, l0,
+                                                            l1, q0, q1, st, nnz, rsum);
   note_launch();
 }
 
 template <class T>
 void launch_rows(const T* x, uint64_t ld, uint32_t n, int which_case, const uint32_t* nnz,
-                 const unsigned long long* rsum, uint32_t r0, uint32_t r1, int2* lists,
-                 uint64_t cap, uint32_t* counts, unsigned long long* work, DevStatus* st,
-                 cudaStream_t s, uint32_t* nnz_row) {
-  k_rows<T><<<grid_for_warps(n, 8), 256, 0, s>>>(x, ld, n, which_case, vec_ok(x, ld), nnz, rsum,
-                                                  r0, r1, lists, cap, counts, work, st, nnz_row);
+                 const unsigned long long* rsum, uint32_t a0, uint32_t a1, uint32_t r0,
+                 uint32_t r1, int2* lists, uint64_t cap, uint32_t* counts,
+                 unsigned long long* work, DevStatus* st, cudaStream_t s, uint32_t* nnz_row) {
+  if (a1 <= a0) return;
+  k_rows<T><<<grid_for_warps(a1 - a0, 8), 256, 0, s>>>(x, ld, n, which_case, vec_ok(x, ld), nnz,
+                                                        rsum, a0, a1, r0, r1, lists, cap, counts,
+                                                        work, st, nnz_row);
+  note_launch();
+}
+
+template <class T>
+void launch_rows_quad(const T* x, uint64_t ld, uint32_t n, const uint32_t* nnz, uint32_t r0,
+                      uint32_t r1, int4* lists, uint64_t cap, uint32_t* counts, DevStatus* st,
+                      cudaStream_t s) {
+  if (r1 <= r0) return;
+  k_rows_quad<T><<<grid_for_warps((r1 - r0 + 3) / 4, 8), 256, 0, s>>>(
+      x, ld, n, vec_ok(x, ld), nnz, r0, r1, lists, cap, counts, st);
   note_launch();
 }
 
@@ -486,74 +805,90 @@ void launch_counts_f16(const T* y, uint64_t ld, uint32_t n, uint32_t tile_cols, 
   note_launch();
 }
 
-template <class T>
-void launch_acompact(const T* x, uint64_t ld, uint32_t n, uint32_t r0, uint32_t ntask,
-                     const uint32_t* rows_idx, typename AEntry<T>::type* lists, uint64_t cap,
-                     uint32_t* counts, cudaStream_t s) {
-  k_acompact<T><<<grid_for_warps(ntask, 8), 256, 0, s>>>(x, ld, n, vec_ok(x, ld), r0, ntask,
-                                                         rows_idx, lists, cap, counts);
+size_t choose_scratch_bytes(uint64_t n) { return (4 * (n + 2) + 2) * sizeof(uint32_t); }
+
+void launch_choose(const CaseAModel& md, uint32_t rows, int variant, const uint32_t* nnz_row,
+                   const unsigned long long* fstats, uint32_t* scratch, uint32_t* plan,
+                   uint32_t* ridx, DevStatus* st, cudaStream_t s) {
+  k_choose<<<1, kChooseThreads, 0, s>>>(md, rows, variant, nnz_row, fstats, scratch, plan, ridx,
+                                        st);
   note_launch();
 }
 
 template <class T>
-void launch_transpose_compact(const T* y, uint64_t ld, uint32_t n, int2* lists, uint64_t cap,
-                              uint32_t* counts, cudaStream_t s) {
-  k_transpose_compact<T><<<(n + 31) / 32, 256, 0, s>>>(y, ld, n, lists, cap, counts);
+void launch_acompact(const T* x, uint64_t ld, uint32_t n, uint32_t r0, uint32_t ntask,
+                     const uint32_t* dyn_ntask, const uint32_t* rows_idx,
+                     typename AEntry<T>::type* lists, uint64_t cap, uint32_t* counts,
+                     cudaStream_t s) {
+  if (ntask == 0) return;
+  k_acompact<T><<<grid_for_warps(ntask, 8), 256, 0, s>>>(x, ld, n, vec_ok(x, ld), r0, ntask,
+                                                         dyn_ntask, rows_idx, lists, cap, counts);
+  note_launch();
+}
+
+template <class T>
+void launch_transpose_compact(const T* y, uint64_t ld, uint32_t n, void* lists, uint64_t cap,
+                              uint32_t* counts, bool quads, DevStatus* st, const uint32_t* skip,
+                              cudaStream_t s) {
+  if (quads)
+    k_transpose_compact<T, 4><<<(n + 31) / 32, 256, 0, s>>>(y, ld, n, static_cast<int4*>(lists),
+                                                            cap, counts, st, skip);
+  else
+    k_transpose_compact<T, 1><<<(n + 31) / 32, 256, 0, s>>>(y, ld, n, static_cast<int2*>(lists),
+                                                            cap, counts, st, skip);
   note_launch();
 }
 
 template <class T>
 void launch_transpose(const T* in, uint64_t ld_in, uint32_t rows, uint32_t cols, T* out,
                       uint64_t ld_out, cudaStream_t s, const uint32_t* in_rows,
-                      const uint32_t* out_rows, const DevStatus* st) {
+                      const uint32_t* out_rows, const DevStatus* st, const uint32_t* plan,
+                      int dyn) {
+  if (rows == 0 || cols == 0) return;
   dim3 grid((cols + 31) / 32, (rows + 31) / 32);
   k_transpose<T><<<grid, dim3(32, 8), 0, s>>>(in, ld_in, rows, cols, out, ld_out, in_rows,
-                                               out_rows, st);
-  note_launch();
-}
-
-template <class T>
-void launch_reps_dense(const T* src, uint64_t ld_src, uint32_t rows, uint32_t cols,
-                       int transpose, int32_t* dst, uint64_t ld_dst, cudaStream_t s) {
-  dim3 grid((cols + 31) / 32, (rows + 31) / 32);
-  k_reps_dense<T><<<grid, dim3(32, 8), 0, s>>>(src, ld_src, rows, cols, transpose, dst, ld_dst);
+                                               out_rows, st, plan, dyn);
   note_launch();
 }
 
 template <class T>
 void launch_reduce_slices(const T* part, uint64_t stride, uint64_t ld_part, uint32_t splits,
                           uint32_t rows, uint32_t cols, T* out, uint64_t ld_out,
-                          const DevStatus* st, cudaStream_t s) {
+                          const DevStatus* st, const uint32_t* dyn_cols, cudaStream_t s) {
   uint64_t blocks = ((uint64_t)rows * cols + 255) / 256;
   if (blocks > 148ull * 16) blocks = 148ull * 16;
   if (blocks < 1) blocks = 1;
   k_reduce_slices<T><<<(unsigned)blocks, 256, 0, s>>>(part, stride, ld_part, splits, rows, cols,
-                                                      out, ld_out, st);
+                                                      out, ld_out, st, dyn_cols);
   note_launch();
 }
 
 #define INSTANTIATE(T)                                                                         \
-  template void launch_scan_stats<T>(const T*, const T*, uint64_t, uint32_t, int, DevStatus*,  \
-                                     uint32_t*, unsigned long long*, cudaStream_t);            \
+  template void launch_scan_stats<T>(const T*, const T*, uint64_t, uint32_t, int, uint32_t,    \
+                                     uint32_t, uint32_t, uint32_t, DevStatus*, uint32_t*,      \
+                                     unsigned long long*, cudaStream_t);                       \
   template void launch_rows<T>(const T*, uint64_t, uint32_t, int, const uint32_t*,             \
-                               const unsigned long long*, uint32_t, uint32_t, int2*, uint64_t, \
-                               uint32_t*, unsigned long long*, DevStatus*, cudaStream_t,       \
-                               uint32_t*);                                                     \
+                               const unsigned long long*, uint32_t, uint32_t, uint32_t,        \
+                               uint32_t, int2*, uint64_t, uint32_t*, unsigned long long*,      \
+                               DevStatus*, cudaStream_t, uint32_t*);                           \
+  template void launch_rows_quad<T>(const T*, uint64_t, uint32_t, const uint32_t*, uint32_t,   \
+                                    uint32_t, int4*, uint64_t, uint32_t*, DevStatus*,          \
+                                    cudaStream_t);                                             \
   template void launch_counts_f16<T>(const T*, uint64_t, uint32_t, uint32_t, __half*, uint64_t, \
                                      uint16_t*, unsigned long long*, cudaStream_t);            \
   template void launch_acompact<T>(const T*, uint64_t, uint32_t, uint32_t, uint32_t,           \
-                                   const uint32_t*, typename AEntry<T>::type*, uint64_t,      \
-                                   uint32_t*, cudaStream_t);                                   \
-  template void launch_transpose_compact<T>(const T*, uint64_t, uint32_t, int2*, uint64_t,     \
-                                            uint32_t*, cudaStream_t);                          \
+                                   const uint32_t*, const uint32_t*,                           \
+                                   typename AEntry<T>::type*, uint64_t, uint32_t*,             \
+                                   cudaStream_t);                                              \
+  template void launch_transpose_compact<T>(const T*, uint64_t, uint32_t, void*, uint64_t,     \
+                                            uint32_t*, bool, DevStatus*, const uint32_t*,      \
+                                            cudaStream_t);                                     \
   template void launch_transpose<T>(const T*, uint64_t, uint32_t, uint32_t, T*, uint64_t,      \
                                     cudaStream_t, const uint32_t*, const uint32_t*,            \
-                                    const DevStatus*);                                         \
-  template void launch_reps_dense<T>(const T*, uint64_t, uint32_t, uint32_t, int, int32_t*,    \
-                                     uint64_t, cudaStream_t);                                  \
+                                    const DevStatus*, const uint32_t*, int);                   \
   template void launch_reduce_slices<T>(const T*, uint64_t, uint64_t, uint32_t, uint32_t,     \
                                         uint32_t, T*, uint64_t, const DevStatus*,             \
-                                        cudaStream_t);
+                                        const uint32_t*, cudaStream_t);
 
 INSTANTIATE(float)
 INSTANTIATE(double)

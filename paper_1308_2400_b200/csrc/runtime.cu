@@ -2,22 +2,26 @@
 //
 // Owns contexts (device + stream + grow-only workspace), builds the TMA
 // tensor maps, sequences prepass -> repeated-addition kernel(s) -> epilogue on
-// one stream, chooses the Case A form (B-form / A-form / row split) from the
-// prepass statistics, and maps device-side validation results to the
-// reference's error contract (kernels.hpp:15-43, matrix.hpp:25-36, 54-57). No
-// compute happens on the host (the host only sorts per-row counts for the
-// Case A split) and there is no CPU fallback.
+// one stream, replays repeated device calls as CUDA graphs, shards the
+// reference-facing call over several devices, and maps device-side
+// validation results to the reference's error contract (kernels.hpp:15-43,
+// matrix.hpp:25-36, 54-57). No element of the product is computed on the
+// host and there is no CPU fallback: the Case A kernel choice is made on the
+// device (k_choose), so no call waits on the host between its kernels.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <atomic>
 #include <cinttypes>
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <new>
+#include <thread>
 #include <vector>
 
 #include "../../include/afmm_b200.h"
@@ -33,32 +37,45 @@ void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 namespace {
 
 constexpr uint64_t kNone = ~0ull;
-constexpr int kVariantAuto = -1; // shape chosen from the problem (launch_compute)
-constexpr int kVariantWide = 0;  // TMA smem ring, 1024-column tiles (bform.cu)
-constexpr int kVariantRing = 1;  // TMA smem ring, 512-column tiles (bform.cu)
-constexpr int kVariantSmall = 4; // TMA smem ring, 1 KB-wide x 4-row CTA tiles (bform.cu)
-constexpr int kVariantMR = 5;    // 4 rows per warp over a dense rep tile (bform.cu)
-constexpr int kVariantTmem = 7;  // bases served from tensor memory (bform.cu)
-constexpr int kVariantAForm = 8; // Case A with the base uniform per warp (k_aform, bform.cu)
-constexpr int kVariantHybrid = 9; // Case A rows split between A-form and B-form (tests)
 
-// AFMM_BFORM=wide|ring|small|mr|tmem|aform|hybrid forces one repeated-addition
-// kernel or Case A form (all are bit-identical; tests/test_gpu_parity.py runs
-// each). Default: auto (tile shape from the problem size, Case A form from the
-// prepass statistics).
+// AFMM_BFORM forces one repeated-addition kernel shape or Case A form (all are
+// bit-identical; tests/test_gpu_parity.py runs each). Default: automatic (the
+// shape from the problem size, the Case A form from the device-side model).
+enum Variant {
+  kAuto = -1,
+  kNarrow = 0,     // R = 1, 512 fp32 / 256 fp64 columns, 2 CTAs per SM
+  kWide = 1,       // R = 1, 1024 / 512 columns, 1 CTA per SM
+  kSmall = 2,      // R = 1, 256 / 128 columns x 4 rows
+  kQuad = 3,       // R = 4 (row quads), 512 / 256 columns x 16 quads
+  kQuadSmall = 4,  // R = 4, 256 / 128 columns x 4 quads
+  kAForm = 8,      // Case A: every row in the A-form
+  kHybrid = 9,     // Case A: the best A-form / B-form row split, forced
+};
+
 int variant_from_env() {
   const char* v = std::getenv("AFMM_BFORM");
-  if (v && std::strcmp(v, "ring") == 0) return kVariantRing;
-  if (v && std::strcmp(v, "wide") == 0) return kVariantWide;
-  if (v && std::strcmp(v, "small") == 0) return kVariantSmall;
-  if (v && std::strcmp(v, "mr") == 0) return kVariantMR;
-  if (v && std::strcmp(v, "tmem") == 0) return kVariantTmem;
-  if (v && std::strcmp(v, "aform") == 0) return kVariantAForm;
-  if (v && std::strcmp(v, "hybrid") == 0) return kVariantHybrid;
-  return kVariantAuto;
+  if (!v) return kAuto;
+  static const struct {
+    const char* name;
+    int variant;
+  } names[] = {{"ring", kNarrow}, {"narrow", kNarrow}, {"wide", kWide},     {"small", kSmall},
+               {"quad", kQuad},   {"quadsmall", kQuadSmall}, {"aform", kAForm}, {"hybrid", kHybrid}};
+  for (const auto& e : names)
+    if (std::strcmp(v, e.name) == 0) return e.variant;
+  return kAuto;
 }
 
 inline uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
+
+int sm_count(int device) {
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
+      sms <= 0) {
+    cudaGetLastError();
+    sms = 148;
+  }
+  return sms;
+}
 
 struct DevBuf {
   void* p = nullptr;
@@ -141,23 +158,18 @@ bool make_count_tmap(CUtensorMap* map, const __half* cnt, uint64_t rows, uint64_
   return r == CUDA_SUCCESS;
 }
 
-// Dense int32 reps R'[k][row] for k_bform_mr: box = 64 rows x KB k's,
-// out-of-range rows read as 0 (no adds).
-bool make_rep_tmap(CUtensorMap* map, const int32_t* reps, uint64_t nk, uint64_t rows,
-                   uint64_t ld) {
-  auto fn = get_encode_fn();
-  if (!fn) return false;
-  const cuuint64_t gdim[2] = {rows, nk};
-  const cuuint64_t gstride[1] = {ld * sizeof(int32_t)};
-  const cuuint32_t box[2] = {(cuuint32_t)afmm_dev::bform_mr_rows(),
-                             (cuuint32_t)afmm_dev::bform_kb()};
-  const cuuint32_t estride[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, const_cast<int32_t*>(reps), gdim,
-                  gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
+// One product call, as enqueued (kept for error decoding and the
+// list-overflow re-run).
+struct Call {
+  int which = 0, dtype = 0, mode = 0, split_k = 0;
+  const void* lhs = nullptr;
+  const void* rhs = nullptr;
+  uint64_t n = 0, ld = 0;
+  void* out = nullptr;
+  uint64_t ld_out = 0, r0 = 0, r1 = 0;
+  bool prevalidated = false;  // multi-device: validation and the per-k vector done already
+  bool have_counts = false;   // multi-device Case A: fp16 counts and statistics done already
+};
 
 }  // namespace
 
@@ -166,20 +178,16 @@ struct afmm_context {
   cudaStream_t stream = nullptr;
   std::mutex mu;
   // workspace
-  DevBuf status, vec_k, work, lists, counts, base_copy, xt, zt, part, reps, cnt16, rmax, fstats;
-  DevBuf alists, acounts, ridx;  // A-form lists / counts, Case A row split order
+  DevBuf status, vec_k, work, lists, counts, base_copy, xt, zt, part, cnt16, rmax, fstats;
+  DevBuf alists, acounts, ridx, plan, scratch;  // A-form lists / counts, Case A choice
   // host-buffer API staging
   DevBuf hx, hy, hz;
-  DevStatus* status_host = nullptr;  // pinned
-  unsigned long long* fstats_host = nullptr;  // pinned, 4 words (A-form / B-form choice)
-  // state of the last enqueued product, for error decoding
-  int last_case = 0, last_dtype = 0;
-  const void* last_lhs = nullptr;
-  const void* last_rhs = nullptr;
-  uint64_t last_n = 0, last_ld = 0;
+  DevStatus* status_host = nullptr;           // pinned
+  unsigned long long* stats_host = nullptr;   // pinned, 4 words (multi-device Case A statistics)
+  Call last;            // the last enqueued product
   bool pending = false;
-  uint64_t list_cap = 0;
-  int variant = 0;  // kVariant* (AFMM_BFORM)
+  uint64_t cap_need = 0;  // list capacity demanded by an overflowing product (re-run)
+  int variant = kAuto;
   int last_form = 0;  // kernel(s) of the last Case A call: 0 B-form, 1 A-form, 2 split
   // optional phase timing: ev[0] start, ev[1] before compute, ev[2] after compute, ev[3] end
   bool timing = false;
@@ -200,23 +208,23 @@ struct afmm_context {
   }
   // CUDA-graph replay of repeated identical device-API calls (graph_call)
   struct GraphKey {
-    int which = -1, dtype = 0, mode = 0, variant = 0, timing = 0;
+    int which = -1, dtype = 0, mode = 0, split_k = 0, variant = 0, timing = 0;
     const void* lhs = nullptr;
     const void* rhs = nullptr;
     void* out = nullptr;
     uint64_t n = 0, ld = 0, ld_out = 0, r0 = 0, r1 = 0;
     cudaStream_t user = nullptr;
     bool operator==(const GraphKey& o) const {
-      return which == o.which && dtype == o.dtype && mode == o.mode && variant == o.variant &&
-             timing == o.timing && lhs == o.lhs && rhs == o.rhs && out == o.out && n == o.n &&
-             ld == o.ld && ld_out == o.ld_out && r0 == o.r0 && r1 == o.r1 && user == o.user;
+      return which == o.which && dtype == o.dtype && mode == o.mode && split_k == o.split_k &&
+             variant == o.variant && timing == o.timing && lhs == o.lhs && rhs == o.rhs &&
+             out == o.out && n == o.n && ld == o.ld && ld_out == o.ld_out && r0 == o.r0 &&
+             r1 == o.r1 && user == o.user;
     }
   };
   struct GraphEntry {
     GraphKey key;
     cudaGraphExec_t exec = nullptr;
     uint64_t gen = 0, launches = 0;
-    int last_form = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // timing graphs only
     void release() {
       if (exec) cudaGraphExecDestroy(exec);
@@ -231,14 +239,18 @@ struct afmm_context {
   std::vector<GraphEntry> graph_cache;
   cudaStream_t gstream = nullptr;  // capturable stream (the legacy default stream is not)
   cudaEvent_t join_in = nullptr, join_out = nullptr;
+  // reference-facing (host buffer) call timing
+  cudaEvent_t hev[4] = {nullptr, nullptr, nullptr, nullptr};
+  const void* peer_checked = nullptr;  // the last `out` checked for peer access
 };
 
 namespace {
 
 std::vector<DevBuf*> all_bufs(afmm_context* c) {
-  return {&c->status, &c->vec_k, &c->work,  &c->lists,  &c->counts, &c->base_copy, &c->xt,
-          &c->zt,     &c->part,  &c->reps,  &c->cnt16,  &c->rmax,   &c->fstats,    &c->alists,
-          &c->acounts, &c->ridx, &c->hx,    &c->hy,     &c->hz};
+  return {&c->status, &c->vec_k, &c->work,    &c->lists,  &c->counts, &c->base_copy,
+          &c->xt,     &c->zt,    &c->part,    &c->cnt16,  &c->rmax,   &c->fstats,
+          &c->alists, &c->acounts, &c->ridx,  &c->plan,   &c->scratch, &c->hx,
+          &c->hy,     &c->hz};
 }
 
 void set_error(afmm_error* err, int kind, int operand, uint64_t row, uint64_t col, double value,
@@ -288,8 +300,25 @@ afmm_status check_dims(int which, uint64_t n_lhs, uint64_t n_rhs, afmm_error* er
   return AFMM_OK;
 }
 
-// Read one element back (only on the error path).
-double read_element(const void* base, int dtype, uint64_t ld, uint64_t row, uint64_t col) {
+afmm_status check_options(const afmm_options* o, afmm_error* err) {
+  if (!o) return AFMM_OK;
+  if (o->mode != AFMM_MODE_ORDER_PRESERVING && o->mode != AFMM_MODE_FAST) {
+    set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: options.mode must be 0 or 1");
+    return AFMM_ERR_INVALID_ARGUMENT;
+  }
+  if (o->split_k < 0 || o->num_devices < 0 ||
+      (o->partition != AFMM_PARTITION_WORK && o->partition != AFMM_PARTITION_ROWS)) {
+    set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0,
+              "afmm: invalid options (split_k, num_devices or partition)");
+    return AFMM_ERR_INVALID_ARGUMENT;
+  }
+  return AFMM_OK;
+}
+
+// Reads element (row, col) of an operand (only on the error path).
+using ValueReader = std::function<double(int operand, uint64_t row, uint64_t col)>;
+
+double read_device_element(const void* base, int dtype, uint64_t ld, uint64_t row, uint64_t col) {
   if (dtype == AFMM_F64) {
     double v = 0.0;
     cudaMemcpy(&v, static_cast<const double*>(base) + row * ld + col, sizeof v,
@@ -302,24 +331,33 @@ double read_element(const void* base, int dtype, uint64_t ld, uint64_t row, uint
   return (double)v;
 }
 
-// Translate the device status of the last product into status / counts / error.
-afmm_status decode_status(afmm_context* c, afmm_op_counts* counts, afmm_error* err) {
-  const DevStatus& s = *c->status_host;
-  const uint64_t n = c->last_n;
-  const int rep_operand = c->last_case == AFMM_CASE_A ? 1 : 0;  // rhs for A, lhs for B
-  const char* where = case_name(c->last_case);
+// Merge the device status of another shard (first offenders by index, counts summed).
+void merge_status(DevStatus* into, const DevStatus& s) {
+  into->nonfinite_lhs_inv = std::max(into->nonfinite_lhs_inv, s.nonfinite_lhs_inv);
+  into->nonfinite_rhs_inv = std::max(into->nonfinite_rhs_inv, s.nonfinite_rhs_inv);
+  into->rep_bad_inv = std::max(into->rep_bad_inv, s.rep_bad_inv);
+  into->list_need = std::max(into->list_need, s.list_need);
+  into->additions += s.additions;
+  into->zero_skips += s.zero_skips;
+}
+
+// Translate a device status into status / counts / error (the reference's
+// exception precedence: non-finite elements at DenseMatrix construction,
+// then the rep operand's first offender, kernels.hpp:25-43).
+afmm_status decode_status(const DevStatus& s, int which, uint64_t n, const ValueReader& rd,
+                          afmm_op_counts* counts, afmm_error* err) {
+  const int rep_operand = which == AFMM_CASE_A ? 1 : 0;  // rhs for A, lhs for B
+  const char* where = case_name(which);
   const char* opname = rep_operand ? "rhs" : "lhs";
   char buf[256];
   // offenders are stored inverted (0 = none); see DevStatus
   auto key = [](unsigned long long inv) { return inv ? ~inv : kNone; };
   const uint64_t nf_lhs = key(s.nonfinite_lhs_inv), nf_rhs = key(s.nonfinite_rhs_inv);
-  const uint64_t rep_bad = key(s.rep_bad_inv), rep_too_large = key(s.rep_too_large_inv);
+  const uint64_t rep_bad = key(s.rep_bad_inv);
   if (nf_lhs != kNone || nf_rhs != kNone) {
     const int operand = nf_lhs != kNone ? 0 : 1;
     const uint64_t lin = operand == 0 ? nf_lhs : nf_rhs;
-    const double v = read_element(operand == 0 ? c->last_lhs : c->last_rhs, c->last_dtype,
-                                  c->last_ld, lin / n, lin % n);
-    set_error(err, AFMM_ERRKIND_NON_FINITE, operand, lin / n, lin % n, v,
+    set_error(err, AFMM_ERRKIND_NON_FINITE, operand, lin / n, lin % n, rd(operand, lin / n, lin % n),
               "DenseMatrix: non-finite element");
     return AFMM_ERR_DOMAIN;
   }
@@ -327,8 +365,7 @@ afmm_status decode_status(afmm_context* c, afmm_op_counts* counts, afmm_error* e
     const uint64_t lin = rep_bad >> 2;
     const int kind = (int)(rep_bad & 3);
     const uint64_t i = lin / n, j = lin % n;
-    const double v = read_element(rep_operand ? c->last_rhs : c->last_lhs, c->last_dtype,
-                                  c->last_ld, i, j);
+    const double v = rd(rep_operand, i, j);
     if (kind == 1) {
       // std::to_string(double) is "%f" (kernels.hpp:32-34)
       std::snprintf(buf, sizeof buf, "%s: %s[%" PRIu64 "][%" PRIu64 "] = %f is not integer-valued",
@@ -341,18 +378,6 @@ afmm_status decode_status(afmm_context* c, afmm_op_counts* counts, afmm_error* e
       set_error(err, AFMM_ERRKIND_OUT_OF_RANGE, rep_operand, i, j, v, buf);
     }
     return AFMM_ERR_DOMAIN;
-  }
-  if (rep_too_large != kNone) {
-    const uint64_t lin = rep_too_large;
-    const uint64_t i = lin / n, j = lin % n;
-    const double v = read_element(rep_operand ? c->last_rhs : c->last_lhs, c->last_dtype,
-                                  c->last_ld, i, j);
-    std::snprintf(buf, sizeof buf,
-                  "%s: %s[%" PRIu64 "][%" PRIu64 "] = %f exceeds the device repeat-count limit "
-                  "(2^31 - 1)",
-                  where, opname, i, j, v);
-    set_error(err, AFMM_ERRKIND_REP_TOO_LARGE, rep_operand, i, j, v, buf);
-    return AFMM_ERR_UNSUPPORTED;
   }
   if (counts) {
     counts->additions = s.additions;
@@ -369,195 +394,156 @@ afmm_status decode_status(afmm_context* c, afmm_op_counts* counts, afmm_error* e
     if (_e != cudaSuccess) return cuda_fail(err, _e, what); \
   } while (0)
 
-// Case A kernel choice from the prepass statistics (cycles per SM
-// sub-partition, fitted on B200 to tools/exp_time.py / quick_time.py runs of
-// cfg3 and cfg4):
-//   A-form: ~75 cycles per (nonzero base, 1024-column tile) entry + ~54 (fp32)
-//           / ~45 (fp64) per predicated iteration; an entry's trip count is
-//           its tile's max |rep| at its k (mean R = trip_sum / (n x tiles));
-//   B-form: per tile of 1024 (fp32) / 512 (fp64) Z rows, 32 cycles per rep
-//           step + ~56 per list entry (~100 when the mean rep is below 3: the
-//           smem-bound regime, tools/sweep.py) over all of Y's nonzero reps.
-// The A-form cost of a row is proportional to its nonzero bases, the B-form
-// cost to the number of row tiles. Sorting the slab's rows by nonzero count,
-// the cheapest split runs the sparsest m rows as A-form and the rest as
-// B-form, with the B part a whole number of tiles (or none); both parts are
-// charged their wave quantisation. A full switch must beat the pure B-form by
-// 15%, a split by 10% (model error margin). Returns m and the row order (A
-// rows first) when 0 < m < rows.
-uint64_t choose_aform_rows(size_t elem, uint64_t n, int variant, int sms,
-                           const std::vector<uint32_t>& nnz, uint64_t nnz_y, uint64_t trip_sum,
-                           uint64_t rep_sum, std::vector<uint32_t>* order) {
-  const uint64_t rows = nnz.size();
-  if (variant == kVariantAForm) return rows;
-  if (rows == 0 || nnz_y == 0) return 0;
-  const double tile = elem == 4 ? 1024.0 : 512.0, it_a = elem == 4 ? 54.0 : 45.0;
-  const double tiles_a = std::ceil((double)n / tile);
-  const double rmean = (double)trip_sum / ((double)n * tiles_a);
-  const double per_base = tiles_a * (75.0 + it_a * rmean);  // A-form cycles per nonzero base
-  const double rbar = (double)rep_sum / (double)nnz_y;
-  const double per_tile = 32.0 * (double)rep_sum + (rbar < 3.0 ? 100.0 : 56.0) * (double)nnz_y;
-  // wave quantisation of a grid of `ctas` wide CTAs on kWideCtasPerSm x sms slots
-  const double slots = (double)afmm_dev::kWideCtasPerSm * (sms > 0 ? sms : 148);
-  auto wave_eff = [&](double ctas) {
-    return ctas <= 0 ? 1.0 : ctas / (std::ceil(ctas / slots) * slots);
-  };
-  auto cost_b = [&](uint64_t tiles_b) {  // B part of tiles_b whole row tiles
-    return tiles_b == 0 ? 0.0
-                        : (double)tiles_b * per_tile /
-                              wave_eff(std::ceil((double)n / afmm_dev::kWideRows) *
-                                       (double)tiles_b);
-  };
-  // rows by ascending nonzero count (counting sort: counts are <= n)
-  std::vector<uint32_t> start(n + 2, 0), idx(rows);
-  for (uint64_t i = 0; i < rows; ++i) ++start[std::min<uint64_t>(nnz[i], n) + 1];
-  for (uint64_t v = 1; v < n + 2; ++v) start[v] += start[v - 1];
-  for (uint64_t i = 0; i < rows; ++i) idx[start[std::min<uint64_t>(nnz[i], n)]++] = (uint32_t)i;
-  std::vector<double> pre(rows + 1, 0.0);
-  for (uint64_t i = 0; i < rows; ++i) pre[i + 1] = pre[i] + (double)nnz[idx[i]];
-  const double slots_a = (double)afmm_dev::kAformCtasPerSm * (sms > 0 ? sms : 148);
-  auto cost_a = [&](uint64_t m) {  // A part of the m sparsest rows
-    if (m == 0) return 0.0;
-    const double ctas = std::ceil((double)m / afmm_dev::kAformRows) * tiles_a;
-    return per_base * pre[m] / (ctas / (std::ceil(ctas / slots_a) * slots_a));
-  };
-  const uint64_t tb = (uint64_t)tile, tiles_all = (rows + tb - 1) / tb;
-  const double pure_b = cost_b(tiles_all);
-  const double pure_a = cost_a(rows);
-  // splits: B part = j whole tiles, A part = the rest (sparsest rows)
-  double best_split = 0.0;
-  uint64_t m_split = 0;
-  for (uint64_t j = 1; j * tb < rows; ++j) {
-    const uint64_t m = rows - j * tb;
-    const double c = cost_a(m) + cost_b(j);
-    if (m_split == 0 || c < best_split) {
-      best_split = c;
-      m_split = m;
-    }
+// B-form tile shape for a problem of `nrows` B-form rows and `ncols` base
+// columns: the widest shape whose grid still fills the GPU (per-entry
+// overhead is amortised over more adds in wider tiles; small problems need the
+// parallelism of narrow/small tiles). CTA slots per GPU: wide 1/SM, narrow
+// 2/SM, small 8/SM.
+int pick_shape(int variant, uint64_t nrows, uint64_t ncols, size_t elem, int sms) {
+  switch (variant) {
+    case kNarrow: return afmm_dev::kShapeNarrow;
+    case kWide: return afmm_dev::kShapeWide;
+    case kSmall: return afmm_dev::kShapeSmall;
+    case kQuad: return afmm_dev::kShapeQuad;
+    case kQuadSmall: return afmm_dev::kShapeQuadSmall;
+    default: break;
   }
-  uint64_t best_m = 0;
-  if (variant == kVariantHybrid) {
-    best_m = m_split;
-  } else {
-    // switching every row needs a 15% margin over the pure B-form, a split
-    // (its A part is the sparse rows, its B part whole tiles) 10%
-    double best = pure_b;
-    if (pure_a < 0.85 * pure_b) {
-      best = pure_a;
-      best_m = rows;
-    }
-    if (m_split && best_split < 0.90 * pure_b && best_split < best) best_m = m_split;
-  }
-  if (best_m > 0 && best_m < rows) {
-    // A rows (sparsest first), then B rows in ascending row order
-    order->assign(idx.begin(), idx.begin() + best_m);
-    std::vector<uint32_t> rest(idx.begin() + best_m, idx.end());
-    std::sort(rest.begin(), rest.end());
-    order->insert(order->end(), rest.begin(), rest.end());
-  }
-  return best_m;
-}
-
-// The repeated-addition kernel over B-form rows [0, nrows) (their rep lists
-// are in c->lists / c->counts) and base columns [col0, col0 + ncols) of the
-// base matrix (kb_rows x b_cols, leading dimension ldb).
-template <class T>
-afmm_status launch_compute(afmm_context* c, int mode, const T* base, uint64_t kb_rows,
-                           uint64_t b_cols, uint64_t ldb, uint32_t nrows, int32_t col0,
-                           int32_t ncols, T* out, uint64_t ld_out, DevStatus* st,
-                           afmm_error* err, const int32_t* reps_dense = nullptr,
-                           uint64_t ld_reps = 0) {
-  if (reps_dense) {
-    // multi-row dense-rep kernel (small reps)
-    CUtensorMap tmap, rmap;
-    if (!make_tmap<T>(&tmap, base, kb_rows, b_cols, ldb) ||
-        !make_rep_tmap(&rmap, reps_dense, kb_rows, nrows, ld_reps)) {
-      set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: cuTensorMapEncodeTiled failed");
-      return AFMM_ERR_CUDA;
-    }
-    CK(afmm_dev::launch_bform_mr<T>(&tmap, &rmap, nrows, col0, ncols, (uint32_t)kb_rows, out,
-                                    ld_out, st, c->stream),
-       "bform_mr");
-    return AFMM_OK;
-  }
-  // Tile shape: the widest one whose grid still fills the GPU (per-entry
-  // overhead is amortised over more adds in wider tiles; small problems need
-  // the parallelism of narrow/small tiles). CTA slots per GPU: wide 148
-  // (1/SM), narrow 296 (2/SM), small 1184 (8/SM).
-  const uint64_t cbytes = (uint64_t)ncols * sizeof(T);
+  const uint64_t cbytes = ncols * elem;
   const uint64_t wide_ctas =
       (nrows + afmm_dev::kWideRows - 1) / afmm_dev::kWideRows * ((cbytes + 4095) / 4096);
   const uint64_t narrow_ctas = (nrows + 15) / 16 * ((cbytes + 2047) / 2048);
-  const uint64_t small_ctas = (nrows + 3) / 4 * ((cbytes + 1023) / 1024);
-  const uint64_t wide_slots = 148ull * afmm_dev::kWideCtasPerSm;
-  int shape = afmm_dev::kShapeNarrow;
-  uint64_t ctas = narrow_ctas, slots = 296;
-  if (c->variant == kVariantTmem) {
-    shape = afmm_dev::kShapeTmem;
-    ctas = (nrows + afmm_dev::kTmemRows - 1) / afmm_dev::kTmemRows * ((cbytes + 4095) / 4096);
-    slots = 148;
-  } else if (c->variant == kVariantWide ||
-             (c->variant == kVariantAuto && 4 * wide_ctas >= 3 * wide_slots)) {
-    // (launch_ring trims the rows per CTA so a partial last wave costs little;
-    // wide tiles need about one wave of CTAs: at n = 1024 fp64 the 128 wide
-    // CTAs, trimmed to 148 of 14 rows, run 7% faster than 256 narrow ones)
-    shape = afmm_dev::kShapeWide;
-    ctas = wide_ctas;
-    slots = wide_slots;
-  } else if (c->variant == kVariantSmall || (c->variant == kVariantAuto && narrow_ctas < 148)) {
-    shape = afmm_dev::kShapeSmall;
-    ctas = small_ctas;
-    slots = 1184;
+  const uint64_t wide_slots = (uint64_t)sms * afmm_dev::kWideCtasPerSm;
+  // (launch_ring trims the rows per CTA so a partial last wave costs little;
+  // wide tiles need about one wave of CTAs: at n = 1024 fp64 the 128 wide
+  // CTAs, trimmed to 148 of 14 rows, run 7% faster than 256 narrow ones)
+  if (4 * wide_ctas >= 3 * wide_slots) return afmm_dev::kShapeWide;
+  if (narrow_ctas < (uint64_t)sms) return afmm_dev::kShapeSmall;
+  return afmm_dev::kShapeNarrow;
+}
+
+// Geometry of a B-form shape: (rows per list, columns per tile, rows per CTA, CTAs per SM)
+struct ShapeGeo {
+  uint32_t r, tile_bytes, rows_per_cta, ctas_per_sm;
+};
+ShapeGeo shape_geo(int shape) {
+  switch (shape) {
+    case afmm_dev::kShapeWide: return {1, 4096, afmm_dev::kWideRows, afmm_dev::kWideCtasPerSm};
+    case afmm_dev::kShapeSmall: return {1, 1024, 4, 8};
+    case afmm_dev::kShapeQuad: return {4, 2048, 4 * afmm_dev::kQuadWarps, 1};
+    case afmm_dev::kShapeQuadSmall: return {4, 1024, 16, 4};
+    default: return {1, 2048, 16, 2};
   }
+}
+
+// The Case A cost model for this problem (costmodel.h) with the B-form
+// geometry of `shape`; the statistics are filled in on the device.
+afmm_dev::CaseAModel case_a_model(size_t elem, uint64_t n, int sms, int shape) {
+  afmm_dev::CaseAModel md;
+  const ShapeGeo g = shape_geo(shape);
+  md.elem = (uint32_t)elem;
+  md.n = n;
+  md.sms = (uint32_t)sms;
+  md.b_tile = (uint32_t)(g.tile_bytes / elem);
+  md.b_rows_per_cta = g.rows_per_cta;
+  md.b_ctas_per_sm = g.ctas_per_sm;
+  // cycles per rep step per list entry and B tile: 2 pipe cycles per FADD2 /
+  // DADD warp instruction, tile_bytes / 512 instructions per rep step and row
+  md.b_step = 2.0 * (double)(g.tile_bytes / 512);
+  const double scale = (double)g.tile_bytes / 4096.0;  // fitted on the wide shape
+  md.b_entry = 56.0 * (g.r == 4 ? 0.5 : 1.0) * (scale < 1.0 ? 1.0 : scale);
+  md.b_entry_small = 100.0 * (g.r == 4 ? 0.5 : 1.0) * (scale < 1.0 ? 1.0 : scale);
+  md.a_tile = afmm_dev::aform_tile_cols<float>() * 4 / (uint32_t)elem;
+  md.a_rows_per_cta = afmm_dev::kAformRows;
+  md.a_ctas_per_sm = afmm_dev::kAformCtasPerSm;
+  return md;
+}
+
+// The repeated-addition kernel over B-form rows [0, nrows) (their lists are
+// in c->lists / c->counts) and base columns [0, ncols) of the base matrix
+// (kb_rows x b_cols, leading dimension ldb). dyn_ncols: ncols decided on the
+// device (a Case A split); the grid covers ncols.
+template <class T>
+afmm_status launch_compute(afmm_context* c, const Call& call, int shape, const T* base,
+                           uint64_t kb_rows, uint64_t b_cols, uint64_t ldb, uint32_t nrows,
+                           int32_t ncols, const uint32_t* dyn_ncols, T* out, uint64_t ld_out,
+                           DevStatus* st, afmm_error* err) {
+  const ShapeGeo g = shape_geo(shape);
+  const uint64_t cbytes = (uint64_t)ncols * sizeof(T);
+  const uint64_t groups = (nrows + g.r - 1) / g.r;
+  const uint64_t per_cta = g.rows_per_cta / g.r;
+  const uint64_t ctas = (groups + per_cta - 1) / per_cta * ((cbytes + g.tile_bytes - 1) / g.tile_bytes);
+  const uint64_t slots = (uint64_t)sm_count(c->device) * g.ctas_per_sm;
   // Fast mode (reassociated): split the k range into slices when the tile grid
   // alone cannot fill 2 waves, then add the slice partials in a fixed order.
   // Each slice is still the exact repeated-addition chain.
   const uint64_t nkb = (kb_rows + afmm_dev::bform_kb() - 1) / afmm_dev::bform_kb();
   uint32_t splits = 1;
-  if (mode == AFMM_MODE_FAST) {
+  if (call.mode == AFMM_MODE_FAST) {
     uint64_t want = (2 * slots + ctas - 1) / std::max<uint64_t>(ctas, 1);
     want = std::min<uint64_t>(want, std::max<uint64_t>(nkb / 4, 1));
-    splits = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, 32));
+    want = std::min<uint64_t>(want, 32);
+    if (call.split_k > 0) want = std::min<uint64_t>(want, (uint64_t)call.split_k);
+    splits = (uint32_t)std::max<uint64_t>(1, want);
   }
   CUtensorMap tmap;
   if (!make_tmap<T>(&tmap, base, kb_rows, b_cols, ldb)) {
     set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: cuTensorMapEncodeTiled failed");
     return AFMM_ERR_CUDA;
   }
+  afmm_dev::BformLaunch a;
+  a.shape = shape;
+  a.tmap = &tmap;
+  a.lists = c->lists.p;
+  a.cap = std::max<uint64_t>(call.n, c->cap_need);
+  a.counts = c->counts.as<uint32_t>();
+  a.nrows = nrows;
+  a.col0 = 0;
+  a.ncols = ncols;
+  a.dyn_ncols = dyn_ncols;
+  a.nk = (uint32_t)kb_rows;
+  a.st = st;
   if (splits > 1) {
     const uint64_t ldp = round_up((uint64_t)ncols, 32);
     const uint64_t stride = (uint64_t)nrows * ldp;
     CK(c->part.ensure(stride * splits * sizeof(T)), "workspace");
-    CK(afmm_dev::launch_bform<T>(shape, &tmap, c->lists.as<int2>(), c->list_cap,
-                                 c->counts.as<uint32_t>(), nrows, col0, ncols, (uint32_t)kb_rows,
-                                 &splits, stride, c->part.as<T>(), ldp, st, c->stream),
-       "bform");
-    afmm_dev::launch_reduce_slices<T>(c->part.as<T>(), stride, ldp, splits, nrows,
-                                      (uint32_t)ncols, out, ld_out, st, c->stream);
+    a.splits = splits;
+    a.slice_stride = stride;
+    a.ld_out = ldp;
+    CK(afmm_dev::launch_bform<T>(a, c->part.as<T>(), c->stream), "bform");
+    afmm_dev::launch_reduce_slices<T>(c->part.as<T>(), stride, ldp, a.splits, nrows,
+                                      (uint32_t)ncols, out, ld_out, st, dyn_ncols, c->stream);
     return AFMM_OK;
   }
-  uint32_t one = 1;
-  CK(afmm_dev::launch_bform<T>(shape, &tmap, c->lists.as<int2>(), c->list_cap,
-                               c->counts.as<uint32_t>(), nrows, col0, ncols, (uint32_t)kb_rows,
-                               &one, 0, out, ld_out, st, c->stream),
-     "bform");
+  a.splits = 1;
+  a.ld_out = ld_out;
+  CK(afmm_dev::launch_bform<T>(a, out, c->stream), "bform");
   return AFMM_OK;
 }
 
+// Case A kernel-choice variant code for k_choose
+int choose_variant(int variant) {
+  if (variant == kAForm) return afmm_dev::kChooseAForm;
+  if (variant == kHybrid) return afmm_dev::kChooseSplit;
+  return afmm_dev::kChooseAuto;
+}
+
 // Enqueue the whole device pipeline for Z rows [r0, r1). Pointers are device
-// memory with leading dimension ld (lhs, rhs) and ld_out (out).
+// memory with leading dimension ld (lhs, rhs) and ld_out (out). Nothing waits
+// on the host.
 template <class T>
-afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* rhs, uint64_t n,
-                            uint64_t ld, T* out, uint64_t ld_out, uint64_t r0, uint64_t r1,
-                            int mode, afmm_error* err) {
+afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) {
   cudaStream_t s = c->stream;
+  const T* lhs = static_cast<const T*>(call.lhs);
+  const T* rhs = static_cast<const T*>(call.rhs);
+  T* out = static_cast<T*>(call.out);
+  const uint64_t n = call.n, ld = call.ld, ld_out = call.ld_out, r0 = call.r0, r1 = call.r1;
   const uint64_t rows = r1 - r0;
   const uint32_t n32 = (uint32_t)n;
+  const uint64_t cap = std::max<uint64_t>(n, c->cap_need);
+  const int sms = sm_count(c->device);
   CK(c->status.ensure(sizeof(DevStatus)), "workspace");
   CK(c->vec_k.ensure(n * 8), "workspace");
-  CK(c->work.ensure(n * 8), "workspace");
   DevStatus* st = c->status.as<DevStatus>();
-  c->list_cap = n;
   c->timed_last = c->timing;
   for (int i = 0; i < 4; ++i) c->last_ev[i] = c->rec_ev[i];
   c->mark(0);
@@ -567,16 +553,24 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
   // + the per-k vector of the work formulas, one pass over both operands
   auto* nnz = c->vec_k.as<uint32_t>();
   auto* rsum = c->vec_k.as<unsigned long long>();
-  afmm_dev::launch_scan_stats<T>(lhs, rhs, ld, n32, which == AFMM_CASE_B ? 1 : 0, st, nnz, rsum,
-                                 s);
+  if (!call.prevalidated)
+    afmm_dev::launch_scan_stats<T>(lhs, rhs, ld, n32, call.which == AFMM_CASE_B ? 1 : 0, 0, n32, 0,
+                                   n32, st, nnz, rsum, s);
 
-  auto* work = c->work.as<unsigned long long>();
-  if (which == AFMM_CASE_B) {
+  if (call.which == AFMM_CASE_B) {
     // rep = X[i,k] (lhs), bases = Y[k,:] (rhs): B-form directly.
-    CK(c->lists.ensure(std::max<uint64_t>(rows, 1) * n * sizeof(int2)), "workspace");
-    CK(c->counts.ensure(std::max<uint64_t>(rows, 1) * 4), "workspace");
-    afmm_dev::launch_rows<T>(lhs, ld, n32, 1, nnz, nullptr, (uint32_t)r0, (uint32_t)r1,
-                             c->lists.as<int2>(), n, c->counts.as<uint32_t>(), work, st, s);
+    const int shape = pick_shape(c->variant, rows, n, sizeof(T), sms);
+    const bool quads = afmm_dev::shape_is_quad(shape);
+    const uint64_t groups = std::max<uint64_t>(quads ? (rows + 3) / 4 : rows, 1);
+    CK(c->lists.ensure(groups * cap * (quads ? sizeof(int4) : sizeof(int2))), "workspace");
+    CK(c->counts.ensure(groups * 4), "workspace");
+    if (quads)
+      afmm_dev::launch_rows_quad<T>(lhs, ld, n32, nnz, (uint32_t)r0, (uint32_t)r1,
+                                    c->lists.as<int4>(), cap, c->counts.as<uint32_t>(), st, s);
+    else
+      afmm_dev::launch_rows<T>(lhs, ld, n32, 1, nnz, nullptr, (uint32_t)r0, (uint32_t)r1,
+                               (uint32_t)r0, (uint32_t)r1, c->lists.as<int2>(), cap,
+                               c->counts.as<uint32_t>(), nullptr, st, s);
     const T* base = rhs;
     uint64_t ldb = ld;
     if ((ld * sizeof(T)) % 16 != 0 || reinterpret_cast<uintptr_t>(rhs) % 16 != 0) {
@@ -587,84 +581,74 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
          "copy");
       base = c->base_copy.as<T>();
     }
-    const bool use_mr = c->variant == kVariantMR && rows > 0;
-    uint64_t ld_r = 0;
-    if (use_mr) {  // dense reps R'[k][i - r0] = llround(X[i][k]) for the slab
-      ld_r = round_up(rows, 4);
-      CK(c->reps.ensure(n * ld_r * sizeof(int32_t)), "workspace");
-      afmm_dev::launch_reps_dense<T>(lhs + r0 * ld, ld, n32, (uint32_t)rows, 1,
-                                     c->reps.as<int32_t>(), ld_r, s);
-    }
     c->mark(1);
     if (rows > 0) {
-      afmm_status cs = launch_compute<T>(c, mode, base, n, n, ldb, (uint32_t)rows, 0, (int32_t)n, out,
-                                         ld_out, st, err, use_mr ? c->reps.as<int32_t>() : nullptr,
-                                         ld_r);
+      afmm_status cs = launch_compute<T>(c, call, shape, base, n, n, ldb, (uint32_t)rows,
+                                         (int32_t)n, nullptr, out, ld_out, st, err);
       if (cs != AFMM_OK) return cs;
     }
     c->mark(2);
+    c->last_form = 0;
   } else {
-    // Case A runs the B-form on transposed operands, the A-form (base uniform
-    // per warp), or splits the slab's rows between them: forced by AFMM_BFORM
-    // (aform / hybrid / any B-form variant), else for n >= 1024 chosen from
-    // the prepass statistics read back here (a short host wait for the
-    // validation pass; the compute stays asynchronous).
+    // Case A: the B-form on transposed operands, the A-form (base uniform per
+    // warp), or the slab's rows split between them. For n >= 1024 (or when
+    // forced by AFMM_BFORM=aform|hybrid) k_choose decides on the device from
+    // the prepass statistics; every kernel of both forms is enqueued and reads
+    // its row count from the plan (a form with no rows exits at once).
     using E = typename afmm_dev::AEntry<T>::type;
     const uint32_t tc = afmm_dev::aform_tile_cols<T>();
     const uint64_t ntiles = (n + tc - 1) / tc, ldc = round_up(n, 64);
-    const bool consider = rows > 0 && (c->variant == kVariantAForm ||
-                                       c->variant == kVariantHybrid ||
-                                       (c->variant == kVariantAuto && n >= 1024));
-    if (consider) CK(c->acounts.ensure(rows * 4), "workspace");
-    afmm_dev::launch_rows<T>(lhs, ld, n32, 0, nullptr, rsum, (uint32_t)r0, (uint32_t)r1, nullptr, 0,
-                             nullptr, work, st, s,
-                             consider ? c->acounts.as<uint32_t>() : nullptr);
-    uint64_t m_a = 0;                 // slab rows run by the A-form
-    std::vector<uint32_t> order;      // hybrid: A rows first, then B rows (slab-relative)
-    if (consider) {
+    const bool choose = rows > 0 && (c->variant == kAForm || c->variant == kHybrid ||
+                                     (c->variant == kAuto && n >= 1024));
+    // B part: B-form rows = Z columns j (rep list = column j of Y), B-form
+    // columns = the slab's B rows (bases X[i,k], gathered through ridx)
+    const int shape = pick_shape(c->variant, n, std::max<uint64_t>(rows, 1), sizeof(T), sms);
+    const bool quads = afmm_dev::shape_is_quad(shape);
+    const uint64_t groups = quads ? (n + 3) / 4 : n;
+    if (choose) CK(c->acounts.ensure(rows * 4), "workspace");
+    afmm_dev::launch_rows<T>(lhs, ld, n32, 0, nullptr, rsum, (uint32_t)r0, (uint32_t)r1,
+                             (uint32_t)r0, (uint32_t)r1, nullptr, 0, nullptr, nullptr, st, s,
+                             choose ? c->acounts.as<uint32_t>() : nullptr);
+    const uint32_t* plan = nullptr;
+    const uint32_t* ridx = nullptr;
+    if (choose) {
       CK(c->cnt16.ensure(n * ldc * sizeof(__half)), "workspace");
       CK(c->rmax.ensure(n * ntiles * sizeof(uint16_t)), "workspace");
       CK(c->fstats.ensure(4 * sizeof(unsigned long long)), "workspace");
-      auto* fs = c->fstats.as<unsigned long long>();
-      CK(cudaMemsetAsync(fs, 0, 4 * sizeof(unsigned long long), s), "memset");
-      afmm_dev::launch_counts_f16<T>(rhs, ld, n32, tc, c->cnt16.as<__half>(), ldc,
-                                     c->rmax.as<uint16_t>(), fs, s);
-      CK(cudaMemcpyAsync(c->status_host, st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s),
-         "statistics readback");
-      CK(cudaMemcpyAsync(c->fstats_host, fs, 4 * sizeof(unsigned long long),
-                         cudaMemcpyDeviceToHost, s),
-         "statistics readback");
-      CK(cudaStreamSynchronize(s), "statistics readback");
-      const DevStatus& hs = *c->status_host;
-      const bool failed = (hs.nonfinite_lhs_inv | hs.nonfinite_rhs_inv | hs.rep_bad_inv |
-                           hs.rep_too_large_inv) != 0;
-      const unsigned long long* f = c->fstats_host;
-      if (!failed && f[2] == 0) {  // every |rep| <= 2048 (exact fp16 counts)
-        std::vector<uint32_t> nnz(rows);
-        CK(cudaMemcpy(nnz.data(), c->acounts.p, rows * 4, cudaMemcpyDeviceToHost),
-           "statistics readback");
-        int sms = 0;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-        m_a = choose_aform_rows(sizeof(T), n, c->variant, sms, nnz, f[0], f[1], f[3], &order);
-      }
-    }
-    const uint64_t m_b = rows - m_a;
-    const bool split = m_a > 0 && m_b > 0;
-    c->last_form = m_a == 0 ? 0 : (split ? 2 : 1);
-    const uint32_t* ridx = nullptr;
-    if (split) {
+      CK(c->plan.ensure(4 * sizeof(uint32_t)), "workspace");
       CK(c->ridx.ensure(rows * 4), "workspace");
-      CK(cudaMemcpyAsync(c->ridx.p, order.data(), rows * 4, cudaMemcpyHostToDevice, s), "H2D");
-      CK(cudaStreamSynchronize(s), "H2D");  // `order` is pageable and local
-      ridx = c->ridx.as<uint32_t>();
-    }
-    if (m_a > 0) {  // the A rows' compacted nonzero bases (k, X[i,k])
+      CK(c->scratch.ensure(afmm_dev::choose_scratch_bytes(n)), "workspace");
       CK(c->alists.ensure(rows * n * sizeof(E)), "workspace");
-      afmm_dev::launch_acompact<T>(lhs, ld, n32, (uint32_t)r0, (uint32_t)m_a, ridx,
+      auto* fs = c->fstats.as<unsigned long long>();
+      if (!call.have_counts) {
+        CK(cudaMemsetAsync(fs, 0, 4 * sizeof(unsigned long long), s), "memset");
+        afmm_dev::launch_counts_f16<T>(rhs, ld, n32, tc, c->cnt16.as<__half>(), ldc,
+                                       c->rmax.as<uint16_t>(), fs, s);
+      }
+      afmm_dev::launch_choose(case_a_model(sizeof(T), n, sms, shape), (uint32_t)rows,
+                              choose_variant(c->variant), c->acounts.as<uint32_t>(), fs,
+                              c->scratch.as<uint32_t>(), c->plan.as<uint32_t>(),
+                              c->ridx.as<uint32_t>(), st, s);
+      plan = c->plan.as<uint32_t>();
+      ridx = c->ridx.as<uint32_t>();
+      // the A rows' compacted nonzero bases (k, X[i,k])
+      afmm_dev::launch_acompact<T>(lhs, ld, n32, (uint32_t)r0, (uint32_t)rows, plan, ridx,
                                    c->alists.as<E>(), n, c->acounts.as<uint32_t>(), s);
     }
+    const uint64_t lds = round_up(std::max<uint64_t>(rows, 1), 32);
+    CK(c->xt.ensure(n * lds * sizeof(T)), "workspace");
+    CK(c->zt.ensure(n * lds * sizeof(T)), "workspace");
+    CK(c->lists.ensure(groups * cap * (quads ? sizeof(int4) : sizeof(int2))), "workspace");
+    CK(c->counts.ensure(groups * 4), "workspace");
+    if (rows > 0) {
+      afmm_dev::launch_transpose_compact<T>(rhs, ld, n32, c->lists.p, cap,
+                                            c->counts.as<uint32_t>(), quads, st,
+                                            plan ? plan + 1 : nullptr, s);
+      afmm_dev::launch_transpose<T>(lhs + r0 * ld, ld, (uint32_t)rows, n32, c->xt.as<T>(), lds, s,
+                                    ridx, nullptr, nullptr, plan, plan ? 1 : 0);
+    }
     c->mark(1);
-    if (m_a > 0) {
+    if (choose) {
       // A-form: the reference's own orientation, zero bases skipped per warp
       CUtensorMap cmap;
       if (!make_count_tmap(&cmap, c->cnt16.as<__half>(), n, n, ldc)) {
@@ -672,60 +656,45 @@ afmm_status enqueue_product(afmm_context* c, int which, const T* lhs, const T* r
         return AFMM_ERR_CUDA;
       }
       CK(afmm_dev::launch_aform<T>(&cmap, c->alists.as<E>(), n, c->acounts.as<uint32_t>(),
-                                   (uint32_t)m_a, n32, n32, c->rmax.as<uint16_t>(), out, ld_out,
-                                   ridx, st, s),
+                                   (uint32_t)rows, plan, n32, n32, c->rmax.as<uint16_t>(), out,
+                                   ld_out, ridx, st, s),
          "aform");
     }
-    if (m_b > 0 || rows == 0) {
-      // B-form: Case A as Case B on transposed operands, Z^T = (Y^T) (x) (X^T).
-      // B-form rows = Z columns j (rep list = column j of Y), B-form columns =
-      // the slab's B rows (bases X[i,k]; gathered through ridx when split).
-      const uint64_t lds = round_up(std::max<uint64_t>(m_b, 1), 32);
-      CK(c->xt.ensure(n * lds * sizeof(T)), "workspace");
-      CK(c->zt.ensure(n * lds * sizeof(T)), "workspace");
-      CK(c->lists.ensure(n * n * sizeof(int2)), "workspace");
-      CK(c->counts.ensure(n * 4), "workspace");
-      const bool use_mr = c->variant == kVariantMR && m_b > 0;
-      const uint64_t ld_r = round_up(n, 4);
-      if (use_mr) {  // dense reps R'[k][j] = llround(Y[k][j]): Y itself, converted
-        CK(c->reps.ensure(n * ld_r * sizeof(int32_t)), "workspace");
-        afmm_dev::launch_reps_dense<T>(rhs, ld, n32, n32, 0, c->reps.as<int32_t>(), ld_r, s);
-      } else {
-        afmm_dev::launch_transpose_compact<T>(rhs, ld, n32, c->lists.as<int2>(), n,
-                                              c->counts.as<uint32_t>(), s);
-      }
-      if (m_b > 0) {
-        const uint32_t* bidx = split ? ridx + m_a : nullptr;
-        afmm_dev::launch_transpose<T>(lhs + r0 * ld, ld, (uint32_t)m_b, n32, c->xt.as<T>(), lds, s,
-                                      bidx, nullptr);
-        afmm_status cs = launch_compute<T>(c, mode, c->xt.as<T>(), n, m_b, lds, n32, 0,
-                                           (int32_t)m_b, c->zt.as<T>(), lds, st, err,
-                                           use_mr ? c->reps.as<int32_t>() : nullptr, ld_r);
-        if (cs != AFMM_OK) return cs;
-        c->mark(2);
-        afmm_dev::launch_transpose<T>(c->zt.as<T>(), lds, n32, (uint32_t)m_b, out, ld_out, s,
-                                      nullptr, bidx, st);
-      } else {
-        c->mark(2);
-      }
-    } else {
-      c->mark(2);
+    if (rows > 0) {
+      // B-form: Case A as Case B on transposed operands, Z^T = (Y^T) (x) (X^T)
+      afmm_status cs = launch_compute<T>(c, call, shape, c->xt.as<T>(), n, rows, lds, n32,
+                                         (int32_t)rows, plan ? plan + 1 : nullptr, c->zt.as<T>(),
+                                         lds, st, err);
+      if (cs != AFMM_OK) return cs;
     }
+    c->mark(2);
+    if (rows > 0)
+      afmm_dev::launch_transpose<T>(c->zt.as<T>(), lds, n32, (uint32_t)rows, out, ld_out, s,
+                                    nullptr, ridx, st, plan, plan ? 2 : 0);
   }
   c->mark(3);
   CK(cudaGetLastError(), "launch");
   CK(cudaMemcpyAsync(c->status_host, st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s),
      "status readback");
-  c->last_case = which;
-  c->last_dtype = sizeof(T) == 8 ? AFMM_F64 : AFMM_F32;
-  c->last_lhs = lhs;
-  c->last_rhs = rhs;
-  c->last_n = n;
-  c->last_ld = ld;
+  c->last = call;
   c->pending = true;
   return AFMM_OK;
 }
 
+afmm_status enqueue_call(afmm_context* c, const Call& call, afmm_error* err) {
+  return call.dtype == AFMM_F64 ? enqueue_product<double>(c, call, err)
+                                : enqueue_product<float>(c, call, err);
+}
+
+ValueReader device_reader(const Call& call) {
+  return [call](int operand, uint64_t row, uint64_t col) {
+    return read_device_element(operand == 0 ? call.lhs : call.rhs, call.dtype, call.ld, row, col);
+  };
+}
+
+// Wait for the pending product and decode it. A product whose rep lists did
+// not fit (reps beyond an entry's range, split into several entries) is
+// re-run once with the capacity it reported.
 afmm_status finish_locked(afmm_context* c, afmm_op_counts* counts, afmm_error* err) {
   if (!c->pending) {
     clear_error(err);
@@ -734,7 +703,24 @@ afmm_status finish_locked(afmm_context* c, afmm_op_counts* counts, afmm_error* e
   c->pending = false;
   cudaError_t e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return cuda_fail(err, e, "afmm: device execution");
-  return decode_status(c, counts, err);
+  const DevStatus s = *c->status_host;
+  if (s.form_rows) c->last_form = s.a_rows == 0 ? 0 : (s.a_rows == s.form_rows ? 1 : 2);
+  else if (c->last.which == AFMM_CASE_A) c->last_form = 0;
+  const afmm_status st = decode_status(s, c->last.which, c->last.n, device_reader(c->last),
+                                       counts, err);
+  if (st != AFMM_OK || s.list_need == 0) return st;
+  // list overflow (validation passed): re-run with the capacity it needs
+  if (s.list_need > (1ull << 40) / std::max<uint64_t>(c->last.n, 1)) {
+    set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0,
+              "afmm: reps this large need rep lists beyond device memory");
+    return AFMM_ERR_OUT_OF_MEMORY;
+  }
+  c->cap_need = s.list_need;
+  const Call again = c->last;
+  afmm_status r = enqueue_call(c, again, err);
+  c->cap_need = 0;
+  if (r != AFMM_OK) return r;
+  return finish_locked(c, counts, err);
 }
 
 // Device-API calls that repeat with the same pointers, sizes and options (a
@@ -743,35 +729,28 @@ afmm_status finish_locked(afmm_context* c, afmm_op_counts* counts, afmm_error* e
 // context's own capturable stream, joined to the caller's stream by events --
 // the legacy default stream cannot be captured), later ones replay it, which
 // removes the host enqueue of ~10 launches per call and the GPU gaps between
-// them (small problems are launch bound). Calls with a host wait in the
-// pipeline (the Case A statistics for n >= 1024) are never captured; a
-// workspace reallocation invalidates the cache; a failed capture falls back to
-// the direct path for good (AFMM_GRAPHS=0 disables the mechanism).
-template <class T>
-afmm_status graph_call(afmm_context* c, int which, const T* lhs, const T* rhs, uint64_t n,
-                       uint64_t ld, T* out, uint64_t ld_out, uint64_t r0, uint64_t r1, int mode,
-                       afmm_error* err) {
-  auto direct = [&]() {
-    return enqueue_product<T>(c, which, lhs, rhs, n, ld, out, ld_out, r0, r1, mode, err);
-  };
-  const bool host_wait = which == AFMM_CASE_A && r1 > r0 &&
-                         (c->variant == kVariantAForm || c->variant == kVariantHybrid ||
-                          (c->variant == kVariantAuto && n >= 1024));
-  if (!c->graphs || host_wait) return direct();
+// them (small problems are launch bound). Every call is capturable: the Case
+// A form is chosen on the device. A workspace reallocation invalidates the
+// cache; a failed capture falls back to the direct path for good
+// (AFMM_GRAPHS=0 disables the mechanism).
+afmm_status graph_call(afmm_context* c, const Call& call, afmm_error* err) {
+  auto direct = [&]() { return enqueue_call(c, call, err); };
+  if (!c->graphs) return direct();
   afmm_context::GraphKey key;
-  key.which = which;
-  key.dtype = sizeof(T) == 8 ? AFMM_F64 : AFMM_F32;
-  key.mode = mode;
+  key.which = call.which;
+  key.dtype = call.dtype;
+  key.mode = call.mode;
+  key.split_k = call.split_k;
   key.variant = c->variant;
   key.timing = c->timing ? 1 : 0;
-  key.lhs = lhs;
-  key.rhs = rhs;
-  key.out = out;
-  key.n = n;
-  key.ld = ld;
-  key.ld_out = ld_out;
-  key.r0 = r0;
-  key.r1 = r1;
+  key.lhs = call.lhs;
+  key.rhs = call.rhs;
+  key.out = call.out;
+  key.n = call.n;
+  key.ld = call.ld;
+  key.ld_out = call.ld_out;
+  key.r0 = call.r0;
+  key.r1 = call.r1;
   key.user = c->stream;
   auto& cache = c->graph_cache;
   for (size_t i = 0; i < cache.size();) {  // entries captured before a reallocation
@@ -799,13 +778,7 @@ afmm_status graph_call(afmm_context* c, int which, const T* lhs, const T* rhs, u
     for (uint64_t i = 0; i < hit->launches; ++i) afmm_dev::note_launch();
     c->timed_last = c->timing;
     for (int i = 0; i < 4; ++i) c->last_ev[i] = hit->ev[i];
-    c->last_case = which;
-    c->last_dtype = key.dtype;
-    c->last_lhs = lhs;
-    c->last_rhs = rhs;
-    c->last_n = n;
-    c->last_ld = ld;
-    c->last_form = hit->last_form;
+    c->last = call;
     c->pending = true;
     return AFMM_OK;
   }
@@ -861,7 +834,6 @@ afmm_status graph_call(afmm_context* c, int which, const T* lhs, const T* rhs, u
   ge.key = key;
   ge.gen = c->buf_gen;
   ge.launches = afmm_dev::g_launches.load() - launches0;
-  ge.last_form = c->last_form;
   if (cache.size() >= 8) {
     cache.front().release();
     cache.erase(cache.begin());
@@ -871,33 +843,501 @@ afmm_status graph_call(afmm_context* c, int which, const T* lhs, const T* rhs, u
   return AFMM_OK;  // the captured call left the host state of this product
 }
 
+// Default contexts of the reference-facing calls: one per (device, shard
+// slot) -- a device listed twice in options->devices gets two contexts.
+constexpr int kMaxDevices = 64, kMaxSlots = 8;
 std::mutex g_default_mu;
-afmm_context* g_default[64] = {};
+afmm_context* g_default[kMaxDevices][kMaxSlots] = {};
 
-afmm_status default_context(int device, afmm_context** out, afmm_error* err) {
+afmm_status default_context(int device, int slot, afmm_context** out, afmm_error* err) {
   if (device < 0) {
     cudaError_t e = cudaGetDevice(&device);
     if (e != cudaSuccess) return cuda_fail(err, e, "afmm: no CUDA device");
   }
-  if (device >= 64) {
+  if (device >= kMaxDevices || slot >= kMaxSlots) {
     set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: device ordinal out of range");
     return AFMM_ERR_INVALID_ARGUMENT;
   }
   std::lock_guard<std::mutex> g(g_default_mu);
-  if (!g_default[device]) {
+  if (!g_default[device][slot]) {
     afmm_context* c = nullptr;
     afmm_status s = afmm_context_create(device, &c);
     if (s != AFMM_OK) {
       set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: cannot create a CUDA context");
       return s;
     }
-    g_default[device] = c;
+    g_default[device][slot] = c;
   }
-  *out = g_default[device];
+  *out = g_default[device][slot];
   return AFMM_OK;
 }
 
-// The reference-facing call: host buffers in, host buffer out.
+afmm_status enable_timing_locked(afmm_context* c, int32_t enable) {
+  if (enable && !c->ev[0]) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(c->device);
+    for (cudaEvent_t& e : c->ev)
+      if (cudaEventCreate(&e) != cudaSuccess) {
+        cudaSetDevice(prev);
+        return AFMM_ERR_CUDA;
+      }
+    cudaSetDevice(prev);
+  }
+  c->timing = enable != 0;
+  return AFMM_OK;
+}
+
+// Is `p` page-locked host memory mapped into the device address space? Then
+// the kernels can store Z rows straight into it (zero-copy).
+template <class T>
+T* mapped_pointer(T* p) {
+  cudaPointerAttributes attr{};
+  T* d = nullptr;
+  if (cudaPointerGetAttributes(&attr, p) == cudaSuccess && attr.type == cudaMemoryTypeHost &&
+      attr.devicePointer)
+    d = static_cast<T*>(attr.devicePointer);
+  cudaGetLastError();  // a pageable pointer is not an error here
+  return d;
+}
+
+ValueReader host_reader(const void* lhs, const void* rhs, int dtype, uint64_t n) {
+  return [=](int operand, uint64_t row, uint64_t col) {
+    const void* b = operand == 0 ? lhs : rhs;
+    return dtype == AFMM_F64 ? static_cast<const double*>(b)[row * n + col]
+                             : (double)static_cast<const float*>(b)[row * n + col];
+  };
+}
+
+afmm_status ensure_host_events(afmm_context* c) {
+  for (cudaEvent_t& e : c->hev)
+    if (!e && cudaEventCreate(&e) != cudaSuccess) return AFMM_ERR_CUDA;
+  return AFMM_OK;
+}
+
+// The reference-facing call on one device: host buffers in, host buffer out.
+template <class T>
+afmm_status host_product_one(int which, const T* lhs, const T* rhs, uint64_t n, T* out,
+                             const afmm_options* opt, afmm_op_counts* counts, afmm_error* err) {
+  afmm_context* c = nullptr;
+  int device = opt ? opt->device : -1;
+  if (opt && opt->num_devices == 1 && opt->devices) device = opt->devices[0];
+  afmm_status st = default_context(device, 0, &c, err);
+  if (st != AFMM_OK) return st;
+  std::lock_guard<std::mutex> g(c->mu);
+  CK(cudaSetDevice(c->device), "afmm: cudaSetDevice");
+  const uint64_t ld = round_up(n, 32);
+  const size_t mat = n * ld * sizeof(T);
+  const int mode = opt ? opt->mode : AFMM_MODE_ORDER_PRESERVING;
+  afmm_timing* timing = opt ? opt->timing : nullptr;
+  if (timing && ensure_host_events(c) != AFMM_OK) return cuda_fail(err, cudaErrorUnknown, "events");
+  const bool time_it = timing != nullptr;
+  const bool kernel_timing = c->timing;
+  if (time_it) CK(enable_timing_locked(c, 1) == AFMM_OK ? cudaSuccess : cudaErrorUnknown,
+                  "afmm: timing events");
+  // Zero-copy result: when `out` is page-locked host memory (mapped into the
+  // device address space) and the only kernel writing Z is k_bform (Case B,
+  // order-preserving), the kernel stores Z rows straight into `out` over PCIe
+  // as its CTAs finish, so the 1 GiB D2H of cfg5 overlaps the compute instead
+  // of following it. k_bform returns before writing when validation failed,
+  // so `out` stays untouched on error, as with the staged copy.
+  T* zdev = which == AFMM_CASE_B && mode == AFMM_MODE_ORDER_PRESERVING ? mapped_pointer(out)
+                                                                         : nullptr;
+  CK(c->hx.ensure(mat), "afmm: device allocation");
+  CK(c->hy.ensure(mat), "afmm: device allocation");
+  if (!zdev) CK(c->hz.ensure(mat), "afmm: device allocation");
+  cudaStream_t s = c->stream;
+  if (time_it) CK(cudaEventRecord(c->hev[0], s), "event");
+  CK(cudaMemcpy2DAsync(c->hx.p, ld * sizeof(T), lhs, n * sizeof(T), n * sizeof(T), n,
+                       cudaMemcpyHostToDevice, s),
+     "afmm: H2D");
+  CK(cudaMemcpy2DAsync(c->hy.p, ld * sizeof(T), rhs, n * sizeof(T), n * sizeof(T), n,
+                       cudaMemcpyHostToDevice, s),
+     "afmm: H2D");
+  Call call;
+  call.which = which;
+  call.dtype = sizeof(T) == 8 ? AFMM_F64 : AFMM_F32;
+  call.mode = mode;
+  call.split_k = opt ? opt->split_k : 0;
+  call.lhs = c->hx.p;
+  call.rhs = c->hy.p;
+  call.n = n;
+  call.ld = ld;
+  call.out = zdev ? static_cast<void*>(zdev) : c->hz.p;
+  call.ld_out = zdev ? n : ld;
+  call.r0 = 0;
+  call.r1 = n;
+  st = enqueue_call(c, call, err);
+  if (st == AFMM_OK) st = finish_locked(c, counts, err);
+  if (st == AFMM_OK && !zdev) {
+    CK(cudaMemcpy2DAsync(out, n * sizeof(T), c->hz.p, ld * sizeof(T), n * sizeof(T), n,
+                         cudaMemcpyDeviceToHost, s),
+       "afmm: D2H");
+  }
+  if (time_it) CK(cudaEventRecord(c->hev[1], s), "event");
+  if (st == AFMM_OK) CK(cudaStreamSynchronize(s), "afmm: D2H");
+  if (time_it) {
+    float total = -1.f, compute = -1.f;
+    if (st == AFMM_OK) {
+      cudaEventElapsedTime(&total, c->hev[0], c->hev[1]);
+      cudaEventElapsedTime(&compute, c->last_ev[1], c->last_ev[2]);
+    }
+    timing->total_ms = total;
+    timing->compute_ms = compute;
+    timing->devices = 1;
+    timing->form = which == AFMM_CASE_A ? c->last_form : 0;
+    if (!kernel_timing) enable_timing_locked(c, 0);
+  }
+  return st;
+}
+
+// A reusable barrier for the shard threads of a multi-device call.
+class Barrier {
+ public:
+  explicit Barrier(int n) : n_(n) {}
+  void wait() {
+    std::unique_lock<std::mutex> l(m_);
+    const uint64_t gen = gen_;
+    if (++count_ == n_) {
+      count_ = 0;
+      ++gen_;
+      cv_.notify_all();
+    } else {
+      cv_.wait(l, [&] { return gen_ != gen; });
+    }
+  }
+
+ private:
+  std::mutex m_;
+  std::condition_variable cv_;
+  int n_, count_ = 0;
+  uint64_t gen_ = 0;
+};
+
+// Enable peer access from `device` to `peer` once per pair (NVLink): the
+// kernels may then store Z rows into another GPU's memory, and peer copies
+// go device to device. Returns whether access is possible.
+bool ensure_peer_access(int device, int peer) {
+  if (device == peer) return true;
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<int, int>, bool>> known;
+  std::lock_guard<std::mutex> g(mu);
+  for (const auto& k : known)
+    if (k.first == std::make_pair(device, peer)) return k.second;
+  int can = 0;
+  cudaDeviceCanAccessPeer(&can, device, peer);
+  bool ok = false;
+  if (can) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    ok = e == cudaSuccess || e == cudaErrorPeerAccessAlreadyEnabled;
+    cudaGetLastError();
+    cudaSetDevice(prev);
+  }
+  known.push_back({{device, peer}, ok});
+  return ok;
+}
+
+// Per-row predicted kernel time for the row partition (afmm_row_cost_device
+// and the multi-device call): Case B W_i; Case A the cheaper of the row's
+// A-form cost and its share of a B-form tile (costmodel.h).
+void row_costs(int which, size_t elem, uint64_t n, int sms, const uint64_t* work,
+               const uint32_t* nnz_row, const unsigned long long* fstats, uint64_t* cost) {
+  if (which == AFMM_CASE_B) {
+    std::memcpy(cost, work, n * sizeof(uint64_t));
+    return;
+  }
+  const int shape = pick_shape(kAuto, n, n, elem, sms);
+  afmm_dev::CaseAModel md = case_a_model(elem, n, sms, shape);
+  md.nnz_y = fstats[0];
+  md.trip_sum = fstats[1];
+  md.rep_sum = fstats[3];
+  const bool a_ok = fstats[2] == 0;
+  const double per_row_b = md.per_tile() / (double)md.b_tile;
+  const double per_base = md.per_base();
+  for (uint64_t i = 0; i < n; ++i) {
+    const double a = a_ok ? per_base * (double)nnz_row[i] : per_row_b;
+    cost[i] = (uint64_t)std::llround(std::min(a, per_row_b) + 1.0);
+  }
+}
+
+// The reference-facing call sharded over several devices (one process):
+//   A  each shard copies an equal row chunk of X and Y to its device (its own
+//      host thread: pageable copies run in parallel) and validates it,
+//      computing the per-k vector of its Y rows;
+//   B  each shard completes Y and the per-k vector from its peers (NVLink peer
+//      copies), computes W_i (and, Case A, the nonzero bases per row and the
+//      statistics of Y) for its chunk rows, and reads them back;
+//   -  the statuses merge (first offender of the whole operands); the cuts
+//      balance the predicted time;
+//   C  each shard copies the X rows of its cut that it lacks from their owners
+//      and runs the product on its rows; its Z rows go straight into `out`
+//      (zero-copy Case B) or are copied back.
+template <class T>
+afmm_status host_product_multi(int which, const T* lhs, const T* rhs, uint64_t n, T* out,
+                               const afmm_options* opt, afmm_op_counts* counts,
+                               afmm_error* err) {
+  const int G = opt->num_devices;
+  std::vector<int> devs(G);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return cuda_fail(err, cudaErrorNoDevice, "afmm: no CUDA device");
+  for (int g = 0; g < G; ++g) {
+    devs[g] = opt->devices ? opt->devices[g] : g;
+    if (devs[g] < 0 || devs[g] >= ndev) {
+      set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: options.devices holds an invalid ordinal");
+      return AFMM_ERR_INVALID_ARGUMENT;
+    }
+  }
+  std::vector<afmm_context*> ctx(G);
+  for (int g = 0; g < G; ++g) {
+    int slot = 0;
+    for (int h = 0; h < g; ++h) slot += devs[h] == devs[g];
+    afmm_status st = default_context(devs[g], slot, &ctx[g], err);
+    if (st != AFMM_OK) return st;
+  }
+  // lock the contexts in address order (no lock-order inversion between callers)
+  std::vector<afmm_context*> order(ctx);
+  std::sort(order.begin(), order.end());
+  std::vector<std::unique_lock<std::mutex>> locks;
+  for (afmm_context* c : order) locks.emplace_back(c->mu);
+  // peer access between the devices (NVLink)
+  for (int a : devs)
+    for (int b : devs) ensure_peer_access(a, b);
+  const int dtype = sizeof(T) == 8 ? AFMM_F64 : AFMM_F32;
+  const int mode = opt->mode;
+  const uint64_t ld = round_up(n, 32);
+  const size_t row_bytes = ld * sizeof(T), mat = n * row_bytes;
+  T* zmapped = which == AFMM_CASE_B && mode == AFMM_MODE_ORDER_PRESERVING ? mapped_pointer(out)
+                                                                            : nullptr;
+  std::vector<uint64_t> e(G + 1), cuts(G + 1);
+  for (int g = 0; g <= G; ++g) e[g] = n * (uint64_t)g / (uint64_t)G;
+  std::vector<uint64_t> work(n, 0), cost(n, 0);
+  std::vector<uint32_t> nnz_row(which == AFMM_CASE_A ? n : 0, 0);
+  std::vector<DevStatus> stat(G);
+  std::vector<afmm_status> rc(G, AFMM_OK);
+  std::vector<afmm_error> errs(G);
+  std::vector<afmm_op_counts> cnt(G);
+  std::vector<cudaEvent_t> ev_a(G, nullptr);
+  std::vector<float> total_ms(G, -1.f), compute_ms(G, -1.f);
+  unsigned long long fstats[4] = {0, 0, 0, 0};
+  Barrier bar(G);
+  bool failed = false;  // set by shard 0 between the barriers
+  const int sms = sm_count(devs[0]);
+  afmm_timing* timing = opt->timing;
+
+  auto shard = [&](int g) {
+    afmm_context* c = ctx[g];
+    afmm_error* er = &errs[g];
+    auto fail = [&](cudaError_t ce, const char* what) {
+      rc[g] = cuda_fail(er, ce, what);
+    };
+    cudaSetDevice(c->device);
+    cudaStream_t s = c->stream;
+    const uint64_t a0 = e[g], a1 = e[g + 1];
+    // ---- A: chunk copies + validation ----
+    cudaError_t ce = cudaSuccess;
+    if (ce == cudaSuccess) ce = c->hx.ensure(mat);
+    if (ce == cudaSuccess) ce = c->hy.ensure(mat);
+    if (ce == cudaSuccess && !zmapped) ce = c->hz.ensure(mat);
+    if (ce == cudaSuccess) ce = c->status.ensure(sizeof(DevStatus));
+    if (ce == cudaSuccess) ce = c->vec_k.ensure(n * 8);
+    if (ce == cudaSuccess) ce = c->work.ensure(n * 8);
+    if (ce == cudaSuccess && which == AFMM_CASE_A) ce = c->acounts.ensure(n * 4);
+    if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&ev_a[g], cudaEventDisableTiming);
+    if (ce == cudaSuccess && timing && ensure_host_events(c) != AFMM_OK) ce = cudaErrorUnknown;
+    if (ce == cudaSuccess && timing) ce = cudaEventRecord(c->hev[0], s);
+    auto* st = c->status.as<DevStatus>();
+    if (ce == cudaSuccess && a1 > a0) {
+      ce = cudaMemcpy2DAsync(c->hx.as<char>() + a0 * row_bytes, row_bytes, lhs + a0 * n,
+                             n * sizeof(T), n * sizeof(T), a1 - a0, cudaMemcpyHostToDevice, s);
+      if (ce == cudaSuccess)
+        ce = cudaMemcpy2DAsync(c->hy.as<char>() + a0 * row_bytes, row_bytes, rhs + a0 * n,
+                               n * sizeof(T), n * sizeof(T), a1 - a0, cudaMemcpyHostToDevice, s);
+    }
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(st, 0, sizeof(DevStatus), s);
+    if (ce == cudaSuccess)
+      afmm_dev::launch_scan_stats<T>(c->hx.as<T>(), c->hy.as<T>(), ld, (uint32_t)n,
+                                     which == AFMM_CASE_B ? 1 : 0, (uint32_t)a0, (uint32_t)a1,
+                                     (uint32_t)a0, (uint32_t)a1, st, c->vec_k.as<uint32_t>(),
+                                     c->vec_k.as<unsigned long long>(), s);
+    if (ce == cudaSuccess) ce = cudaEventRecord(ev_a[g], s);
+    if (ce != cudaSuccess) fail(ce, "afmm: shard setup");
+    bar.wait();  // every chunk's copy and scan is enqueued (events recorded)
+    // ---- B: complete Y and the per-k vector, W_i of the chunk ----
+    const size_t vk = which == AFMM_CASE_B ? sizeof(uint32_t) : sizeof(unsigned long long);
+    for (int h = 0; h < G && rc[g] == AFMM_OK; ++h) {
+      if (h == g || e[h + 1] == e[h]) continue;
+      afmm_context* p = ctx[h];
+      if (rc[h] != AFMM_OK) continue;
+      ce = cudaStreamWaitEvent(s, ev_a[h], 0);
+      if (ce == cudaSuccess)
+        ce = cudaMemcpyPeerAsync(c->hy.as<char>() + e[h] * row_bytes, c->device,
+                                 p->hy.as<char>() + e[h] * row_bytes, p->device,
+                                 (e[h + 1] - e[h]) * row_bytes, s);
+      if (ce == cudaSuccess)
+        ce = cudaMemcpyPeerAsync(c->vec_k.as<char>() + e[h] * vk, c->device,
+                                 p->vec_k.as<char>() + e[h] * vk, p->device,
+                                 (e[h + 1] - e[h]) * vk, s);
+      if (ce != cudaSuccess) fail(ce, "afmm: peer copy");
+    }
+    if (rc[g] == AFMM_OK) {
+      afmm_dev::launch_rows<T>(c->hx.as<T>(), ld, (uint32_t)n, which == AFMM_CASE_B ? 1 : 0,
+                               c->vec_k.as<uint32_t>(), c->vec_k.as<unsigned long long>(),
+                               (uint32_t)a0, (uint32_t)a1, (uint32_t)a0, (uint32_t)a1, nullptr, 0,
+                               nullptr, c->work.as<unsigned long long>(), st, s,
+                               which == AFMM_CASE_A ? c->acounts.as<uint32_t>() + 0 : nullptr);
+      ce = cudaSuccess;
+      if (which == AFMM_CASE_A) {
+        // A-form counts / statistics of the (now complete) Y, used by the
+        // partition here and by this shard's product in C
+        const uint32_t tc = afmm_dev::aform_tile_cols<T>();
+        const uint64_t ntiles = (n + tc - 1) / tc, ldc = round_up(n, 64);
+        ce = c->cnt16.ensure(n * ldc * sizeof(__half));
+        if (ce == cudaSuccess) ce = c->rmax.ensure(n * ntiles * sizeof(uint16_t));
+        if (ce == cudaSuccess) ce = c->fstats.ensure(4 * sizeof(unsigned long long));
+        if (ce == cudaSuccess)
+          ce = cudaMemsetAsync(c->fstats.p, 0, 4 * sizeof(unsigned long long), s);
+        if (ce == cudaSuccess)
+          afmm_dev::launch_counts_f16<T>(c->hy.as<T>(), ld, (uint32_t)n, tc,
+                                         c->cnt16.as<__half>(), ldc, c->rmax.as<uint16_t>(),
+                                         c->fstats.as<unsigned long long>(), s);
+        // nnz_row of the chunk rows (slab-relative index = i - a0)
+        if (ce == cudaSuccess && a1 > a0)
+          ce = cudaMemcpyAsync(nnz_row.data() + a0, c->acounts.p, (a1 - a0) * 4,
+                               cudaMemcpyDeviceToHost, s);
+        if (ce == cudaSuccess && g == 0)
+          ce = cudaMemcpyAsync(c->stats_host, c->fstats.p, 4 * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, s);
+      }
+      if (ce == cudaSuccess && a1 > a0)
+        ce = cudaMemcpyAsync(work.data() + a0, c->work.as<uint64_t>() + a0, (a1 - a0) * 8,
+                             cudaMemcpyDeviceToHost, s);
+      if (ce == cudaSuccess)
+        ce = cudaMemcpyAsync(c->status_host, st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s);
+      if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+      if (ce != cudaSuccess) fail(ce, "afmm: shard statistics");
+      else stat[g] = *c->status_host;
+    }
+    bar.wait();
+    if (g == 0) {
+      // ---- merge the statuses; cut the rows ----
+      for (int h = 0; h < G; ++h)
+        if (rc[h] != AFMM_OK) {
+          failed = true;
+          if (err) *err = errs[h];
+          rc[0] = rc[h];
+          break;
+        }
+      if (!failed) {
+        DevStatus all{};
+        for (int h = 0; h < G; ++h) merge_status(&all, stat[h]);
+        const afmm_status dst =
+            decode_status(all, which, n, host_reader(lhs, rhs, dtype, n), nullptr, err);
+        if (dst != AFMM_OK) {
+          failed = true;
+          rc[0] = dst;
+        }
+      }
+      if (!failed) {
+        if (which == AFMM_CASE_A) std::memcpy(fstats, ctx[0]->stats_host, sizeof fstats);
+        if (opt->partition == AFMM_PARTITION_ROWS) {
+          cuts = e;
+        } else {
+          row_costs(which, sizeof(T), n, sms, work.data(),
+                    which == AFMM_CASE_A ? nnz_row.data() : nullptr, fstats, cost.data());
+          afmm_partition_rows(cost.data(), n, (uint32_t)G, cuts.data());
+        }
+      }
+    }
+    bar.wait();
+    if (failed) return;
+    // ---- C: the rows of the cut this shard lacks, then its product ----
+    const uint64_t r0 = cuts[g], r1 = cuts[g + 1];
+    for (int h = 0; h < G; ++h) {
+      if (h == g) continue;
+      const uint64_t lo = std::max(r0, e[h]), hi = std::min(r1, e[h + 1]);
+      if (hi <= lo) continue;
+      ce = cudaMemcpyPeerAsync(c->hx.as<char>() + lo * row_bytes, c->device,
+                               ctx[h]->hx.as<char>() + lo * row_bytes, ctx[h]->device,
+                               (hi - lo) * row_bytes, s);
+      if (ce != cudaSuccess) {
+        fail(ce, "afmm: peer copy");
+        return;
+      }
+    }
+    Call call;
+    call.which = which;
+    call.dtype = dtype;
+    call.mode = mode;
+    call.split_k = opt->split_k;
+    call.lhs = c->hx.p;
+    call.rhs = c->hy.p;
+    call.n = n;
+    call.ld = ld;
+    call.out = zmapped ? static_cast<void*>(zmapped + r0 * n) : c->hz.p;
+    call.ld_out = zmapped ? n : ld;
+    call.r0 = r0;
+    call.r1 = r1;
+    call.prevalidated = true;
+    call.have_counts = which == AFMM_CASE_A;
+    const bool kernel_timing = c->timing;
+    if (timing) enable_timing_locked(c, 1);
+    afmm_status st2 = enqueue_call(c, call, er);
+    if (st2 == AFMM_OK) st2 = finish_locked(c, &cnt[g], er);
+    if (st2 == AFMM_OK && !zmapped && r1 > r0) {
+      ce = cudaMemcpy2DAsync(out + r0 * n, n * sizeof(T), c->hz.p, row_bytes, n * sizeof(T),
+                             r1 - r0, cudaMemcpyDeviceToHost, s);
+      if (ce == cudaSuccess && timing) ce = cudaEventRecord(c->hev[1], s);
+      if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+      if (ce != cudaSuccess) st2 = cuda_fail(er, ce, "afmm: D2H");
+    } else if (st2 == AFMM_OK && timing) {
+      cudaEventRecord(c->hev[1], s);
+      cudaStreamSynchronize(s);
+    }
+    if (timing && st2 == AFMM_OK) {
+      cudaEventElapsedTime(&total_ms[g], c->hev[0], c->hev[1]);
+      cudaEventElapsedTime(&compute_ms[g], c->last_ev[1], c->last_ev[2]);
+    }
+    if (timing && !kernel_timing) enable_timing_locked(c, 0);
+    rc[g] = st2;
+  };
+
+  std::vector<std::thread> threads;
+  for (int g = 1; g < G; ++g) threads.emplace_back(shard, g);
+  shard(0);
+  for (auto& t : threads) t.join();
+  for (int g = 0; g < G; ++g) {
+    if (ev_a[g]) {
+      cudaSetDevice(ctx[g]->device);
+      cudaEventDestroy(ev_a[g]);
+    }
+  }
+  if (failed) return rc[0];
+  for (int g = 0; g < G; ++g)
+    if (rc[g] != AFMM_OK) {
+      if (err) *err = errs[g];
+      return rc[g];
+    }
+  if (counts) {
+    *counts = afmm_op_counts{0, 0, 0};
+    for (int g = 0; g < G; ++g) {
+      counts->additions += cnt[g].additions;
+      counts->zero_skips += cnt[g].zero_skips;
+    }
+  }
+  if (timing) {
+    timing->total_ms = *std::max_element(total_ms.begin(), total_ms.end());
+    timing->compute_ms = *std::max_element(compute_ms.begin(), compute_ms.end());
+    timing->devices = G;
+    timing->form = which == AFMM_CASE_A ? ctx[0]->last_form : 0;
+  }
+  clear_error(err);
+  return AFMM_OK;
+}
+
 template <class T>
 afmm_status host_product(int which, const T* lhs, uint64_t n_lhs, const T* rhs, uint64_t n_rhs,
                          T* out, const afmm_options* opt, afmm_op_counts* counts,
@@ -905,53 +1345,26 @@ afmm_status host_product(int which, const T* lhs, uint64_t n_lhs, const T* rhs, 
   clear_error(err);
   afmm_status st = check_dims(which, n_lhs, n_rhs, err);
   if (st != AFMM_OK) return st;
+  st = check_options(opt, err);
+  if (st != AFMM_OK) return st;
   if (!lhs || !rhs || !out) {
     set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: null pointer argument");
     return AFMM_ERR_INVALID_ARGUMENT;
   }
-  afmm_context* c = nullptr;
-  st = default_context(opt ? opt->device : -1, &c, err);
-  if (st != AFMM_OK) return st;
-  std::lock_guard<std::mutex> g(c->mu);
-  CK(cudaSetDevice(c->device), "afmm: cudaSetDevice");
-  const uint64_t n = n_lhs, ld = round_up(n, 32);
-  const size_t mat = n * ld * sizeof(T);
-  const int mode = opt ? opt->mode : AFMM_MODE_ORDER_PRESERVING;
-  // Zero-copy result: when `out` is page-locked host memory (mapped into the
-  // device address space) and the only kernel writing Z is k_bform (Case B,
-  // order-preserving), the kernel stores Z rows straight into `out` over PCIe
-  // as its CTAs finish, so the 1 GiB D2H of cfg5 overlaps the compute instead
-  // of following it. k_bform returns before writing when validation failed,
-  // so `out` stays untouched on error, as with the staged copy.
-  T* zdev = nullptr;
-  if (which == AFMM_CASE_B && mode == AFMM_MODE_ORDER_PRESERVING) {
-    cudaPointerAttributes attr{};
-    if (cudaPointerGetAttributes(&attr, out) == cudaSuccess && attr.type == cudaMemoryTypeHost &&
-        attr.devicePointer)
-      zdev = static_cast<T*>(attr.devicePointer);
-    cudaGetLastError();  // a pageable pointer is not an error here
+  if (opt && opt->num_devices > 1)
+    return host_product_multi<T>(which, lhs, rhs, n_lhs, out, opt, counts, err);
+  return host_product_one<T>(which, lhs, rhs, n_lhs, out, opt, counts, err);
+}
+
+template <class F>
+afmm_status guarded(F f) {
+  try {
+    return f();
+  } catch (const std::bad_alloc&) {
+    return AFMM_ERR_OUT_OF_MEMORY;
+  } catch (...) {
+    return AFMM_ERR_CUDA;
   }
-  CK(c->hx.ensure(mat), "afmm: device allocation");
-  CK(c->hy.ensure(mat), "afmm: device allocation");
-  if (!zdev) CK(c->hz.ensure(mat), "afmm: device allocation");
-  cudaStream_t s = c->stream;
-  CK(cudaMemcpy2DAsync(c->hx.p, ld * sizeof(T), lhs, n * sizeof(T), n * sizeof(T), n,
-                       cudaMemcpyHostToDevice, s),
-     "afmm: H2D");
-  CK(cudaMemcpy2DAsync(c->hy.p, ld * sizeof(T), rhs, n * sizeof(T), n * sizeof(T), n,
-                       cudaMemcpyHostToDevice, s),
-     "afmm: H2D");
-  st = enqueue_product<T>(c, which, c->hx.as<T>(), c->hy.as<T>(), n, ld,
-                          zdev ? zdev : c->hz.as<T>(), zdev ? n : ld, 0, n, mode, err);
-  if (st != AFMM_OK) return st;
-  st = finish_locked(c, counts, err);
-  if (st != AFMM_OK) return st;
-  if (zdev) return AFMM_OK;
-  CK(cudaMemcpy2DAsync(out, n * sizeof(T), c->hz.p, ld * sizeof(T), n * sizeof(T), n,
-                       cudaMemcpyDeviceToHost, s),
-     "afmm: D2H");
-  CK(cudaStreamSynchronize(s), "afmm: D2H");
-  return AFMM_OK;
 }
 
 }  // namespace
@@ -965,49 +1378,33 @@ extern "C" {
 afmm_status afmm_case_a_f64(const double* lhs, uint64_t n_lhs, const double* rhs, uint64_t n_rhs,
                             double* out, const afmm_options* options, afmm_op_counts* counts,
                             afmm_error* error) {
-  try {
+  return guarded([&] {
     return host_product<double>(AFMM_CASE_A, lhs, n_lhs, rhs, n_rhs, out, options, counts, error);
-  } catch (const std::bad_alloc&) {
-    return AFMM_ERR_OUT_OF_MEMORY;
-  } catch (...) {
-    return AFMM_ERR_CUDA;
-  }
+  });
 }
 
 afmm_status afmm_case_b_f64(const double* lhs, uint64_t n_lhs, const double* rhs, uint64_t n_rhs,
                             double* out, const afmm_options* options, afmm_op_counts* counts,
                             afmm_error* error) {
-  try {
+  return guarded([&] {
     return host_product<double>(AFMM_CASE_B, lhs, n_lhs, rhs, n_rhs, out, options, counts, error);
-  } catch (const std::bad_alloc&) {
-    return AFMM_ERR_OUT_OF_MEMORY;
-  } catch (...) {
-    return AFMM_ERR_CUDA;
-  }
+  });
 }
 
 afmm_status afmm_case_a_f32(const float* lhs, uint64_t n_lhs, const float* rhs, uint64_t n_rhs,
                             float* out, const afmm_options* options, afmm_op_counts* counts,
                             afmm_error* error) {
-  try {
+  return guarded([&] {
     return host_product<float>(AFMM_CASE_A, lhs, n_lhs, rhs, n_rhs, out, options, counts, error);
-  } catch (const std::bad_alloc&) {
-    return AFMM_ERR_OUT_OF_MEMORY;
-  } catch (...) {
-    return AFMM_ERR_CUDA;
-  }
+  });
 }
 
 afmm_status afmm_case_b_f32(const float* lhs, uint64_t n_lhs, const float* rhs, uint64_t n_rhs,
                             float* out, const afmm_options* options, afmm_op_counts* counts,
                             afmm_error* error) {
-  try {
+  return guarded([&] {
     return host_product<float>(AFMM_CASE_B, lhs, n_lhs, rhs, n_rhs, out, options, counts, error);
-  } catch (const std::bad_alloc&) {
-    return AFMM_ERR_OUT_OF_MEMORY;
-  } catch (...) {
-    return AFMM_ERR_CUDA;
-  }
+  });
 }
 
 afmm_status afmm_context_create(int32_t device, afmm_context** ctx) {
@@ -1031,7 +1428,7 @@ afmm_status afmm_context_create(int32_t device, afmm_context** ctx) {
   if (cudaSetDevice(device) != cudaSuccess ||
       cudaHostAlloc(reinterpret_cast<void**>(&c->status_host), sizeof(DevStatus),
                     cudaHostAllocDefault) != cudaSuccess ||
-      cudaHostAlloc(reinterpret_cast<void**>(&c->fstats_host), 4 * sizeof(unsigned long long),
+      cudaHostAlloc(reinterpret_cast<void**>(&c->stats_host), 4 * sizeof(unsigned long long),
                     cudaHostAllocDefault) != cudaSuccess) {
     if (c->status_host) cudaFreeHost(c->status_host);
     delete c;
@@ -1057,16 +1454,25 @@ void afmm_context_destroy(afmm_context* c) {
     if (c->join_out) cudaEventDestroy(c->join_out);
     for (DevBuf* b : all_bufs(c)) b->release();
     if (c->status_host) cudaFreeHost(c->status_host);
-    if (c->fstats_host) cudaFreeHost(c->fstats_host);
+    if (c->stats_host) cudaFreeHost(c->stats_host);
     for (cudaEvent_t& e : c->ev)
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t& e : c->hev)
       if (e) cudaEventDestroy(e);
   }
   delete c;
 }
 
+// Switching streams first drains a pending asynchronous product on the old
+// stream (its status readback was queued there), so afmm_context_finish()
+// still reports that product.
 afmm_status afmm_context_set_stream(afmm_context* c, void* stream) {
   if (!c) return AFMM_ERR_INVALID_ARGUMENT;
   std::lock_guard<std::mutex> g(c->mu);
+  if (c->pending) {
+    cudaSetDevice(c->device);
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess) return AFMM_ERR_CUDA;
+  }
   c->stream = static_cast<cudaStream_t>(stream);
   return AFMM_OK;
 }
@@ -1077,7 +1483,6 @@ afmm_status afmm_product_device(afmm_context* c, int32_t which_case, int32_t dty
                                 const afmm_options* options, int32_t sync,
                                 afmm_op_counts* counts, afmm_error* err) {
   clear_error(err);
-  const int mode = options ? options->mode : AFMM_MODE_ORDER_PRESERVING;
   if (!c || (which_case != AFMM_CASE_A && which_case != AFMM_CASE_B) ||
       (dtype != AFMM_F64 && dtype != AFMM_F32)) {
     set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: invalid context/case/dtype");
@@ -1085,57 +1490,63 @@ afmm_status afmm_product_device(afmm_context* c, int32_t which_case, int32_t dty
   }
   afmm_status st = check_dims(which_case, n, n, err);
   if (st != AFMM_OK) return st;
+  st = check_options(options, err);
+  if (st != AFMM_OK) return st;
   if (ld < n || ld_out < n || row_begin > row_end || row_end > n || !lhs || !rhs ||
       (!out && row_end > row_begin)) {
     set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: invalid leading dimension / rows");
     return AFMM_ERR_INVALID_ARGUMENT;
   }
-  try {
+  return guarded([&]() -> afmm_status {
     std::lock_guard<std::mutex> g(c->mu);
     CK(cudaSetDevice(c->device), "afmm: cudaSetDevice");
     if (c->pending) {
-      st = finish_locked(c, nullptr, nullptr);  // drain an unfinished async call
-      (void)st;
+      // a previous asynchronous product was never finished: report its
+      // outcome instead of starting new work on top of it
+      afmm_status prev = finish_locked(c, nullptr, err);
+      if (prev != AFMM_OK) return prev;
     }
-    if (dtype == AFMM_F64)
-      st = graph_call<double>(c, which_case, static_cast<const double*>(lhs),
-                              static_cast<const double*>(rhs), n, ld, static_cast<double*>(out),
-                              ld_out, row_begin, row_end, mode, err);
-    else
-      st = graph_call<float>(c, which_case, static_cast<const float*>(lhs),
-                             static_cast<const float*>(rhs), n, ld, static_cast<float*>(out),
-                             ld_out, row_begin, row_end, mode, err);
-    if (st != AFMM_OK) return st;
+    if (out && out != c->peer_checked) {
+      // `out` in another GPU's memory (a row shard storing into the device
+      // that gathers Z): enable peer access so the kernels' stores go over NVLink
+      cudaPointerAttributes attr{};
+      if (cudaPointerGetAttributes(&attr, out) == cudaSuccess &&
+          attr.type == cudaMemoryTypeDevice && attr.device != c->device)
+        ensure_peer_access(c->device, attr.device);
+      cudaGetLastError();
+      c->peer_checked = out;
+    }
+    Call call;
+    call.which = which_case;
+    call.dtype = dtype;
+    call.mode = options ? options->mode : AFMM_MODE_ORDER_PRESERVING;
+    call.split_k = options ? options->split_k : 0;
+    call.lhs = lhs;
+    call.rhs = rhs;
+    call.n = n;
+    call.ld = ld;
+    call.out = out;
+    call.ld_out = ld_out;
+    call.r0 = row_begin;
+    call.r1 = row_end;
+    afmm_status s2 = graph_call(c, call, err);
+    if (s2 != AFMM_OK) return s2;
     if (sync) return finish_locked(c, counts, err);
     return AFMM_OK;
-  } catch (const std::bad_alloc&) {
-    return AFMM_ERR_OUT_OF_MEMORY;
-  }
+  });
 }
 
 afmm_status afmm_context_finish(afmm_context* c, afmm_op_counts* counts, afmm_error* err) {
   if (!c) return AFMM_ERR_INVALID_ARGUMENT;
   std::lock_guard<std::mutex> g(c->mu);
   CK(cudaSetDevice(c->device), "afmm: cudaSetDevice");
-  return finish_locked(c, counts, err);
+  return guarded([&] { return finish_locked(c, counts, err); });
 }
 
 afmm_status afmm_context_enable_timing(afmm_context* c, int32_t enable) {
   if (!c) return AFMM_ERR_INVALID_ARGUMENT;
   std::lock_guard<std::mutex> g(c->mu);
-  if (enable && !c->ev[0]) {
-    int prev = 0;
-    cudaGetDevice(&prev);
-    cudaSetDevice(c->device);
-    for (cudaEvent_t& e : c->ev)
-      if (cudaEventCreate(&e) != cudaSuccess) {
-        cudaSetDevice(prev);
-        return AFMM_ERR_CUDA;
-      }
-    cudaSetDevice(prev);
-  }
-  c->timing = enable != 0;
-  return AFMM_OK;
+  return enable_timing_locked(c, enable);
 }
 
 afmm_status afmm_context_last_timing(afmm_context* c, float* prepass_ms, float* compute_ms,
@@ -1157,18 +1568,19 @@ afmm_status afmm_context_last_timing(afmm_context* c, float* prepass_ms, float* 
 int32_t afmm_context_last_form(afmm_context* c) {
   if (!c) return -1;
   std::lock_guard<std::mutex> g(c->mu);
-  return c->last_case == AFMM_CASE_A ? c->last_form : 0;
+  return c->last.which == AFMM_CASE_A ? c->last_form : 0;
 }
 
-afmm_status afmm_row_work_device(afmm_context* c, int32_t which_case, int32_t dtype,
-                                 const void* lhs, const void* rhs, uint64_t n, uint64_t ld,
-                                 uint64_t* work_host, afmm_error* err) {
-  clear_error(err);
-  if (!c || !work_host || (dtype != AFMM_F64 && dtype != AFMM_F32)) return AFMM_ERR_INVALID_ARGUMENT;
-  afmm_status st = check_dims(which_case, n, n, err);
-  if (st != AFMM_OK) return st;
-  std::lock_guard<std::mutex> g(c->mu);
-  CK(cudaSetDevice(c->device), "afmm: cudaSetDevice");
+}  // extern "C"
+
+namespace {
+
+// Statistics of the full operands on one context: W_i (work), and for Case A
+// the nonzero bases per row and the statistics of Y. Host arrays out.
+template <class T>
+afmm_status row_stats(afmm_context* c, int which, const T* lhs, const T* rhs, uint64_t n,
+                      uint64_t ld, uint64_t* work_host, std::vector<uint32_t>* nnz_row,
+                      unsigned long long* fstats, afmm_error* err) {
   CK(c->vec_k.ensure(n * 8), "workspace");
   CK(c->work.ensure(n * 8), "workspace");
   CK(c->status.ensure(sizeof(DevStatus)), "workspace");
@@ -1176,25 +1588,82 @@ afmm_status afmm_row_work_device(afmm_context* c, int32_t which_case, int32_t dt
   auto* work = c->work.as<unsigned long long>();
   DevStatus* dst = c->status.as<DevStatus>();
   CK(cudaMemsetAsync(dst, 0, sizeof(DevStatus), s), "memset");
-  const int cb = which_case == AFMM_CASE_B ? 1 : 0;
-  auto* nnz = c->vec_k.as<uint32_t>();
-  auto* rsum = c->vec_k.as<unsigned long long>();
-  if (dtype == AFMM_F64) {
-    auto* l = static_cast<const double*>(lhs);
-    auto* r = static_cast<const double*>(rhs);
-    afmm_dev::launch_scan_stats<double>(l, r, ld, (uint32_t)n, cb, dst, nnz, rsum, s);
-    afmm_dev::launch_rows<double>(l, ld, (uint32_t)n, cb, nnz, rsum, 0, 0, nullptr, 0, nullptr,
-                                  work, dst, s);
-  } else {
-    auto* l = static_cast<const float*>(lhs);
-    auto* r = static_cast<const float*>(rhs);
-    afmm_dev::launch_scan_stats<float>(l, r, ld, (uint32_t)n, cb, dst, nnz, rsum, s);
-    afmm_dev::launch_rows<float>(l, ld, (uint32_t)n, cb, nnz, rsum, 0, 0, nullptr, 0, nullptr,
-                                 work, dst, s);
-  }
+  const int cb = which == AFMM_CASE_B ? 1 : 0;
+  const uint32_t n32 = (uint32_t)n;
+  afmm_dev::launch_scan_stats<T>(lhs, rhs, ld, n32, cb, 0, 0, 0, n32, dst, c->vec_k.as<uint32_t>(),
+                                 c->vec_k.as<unsigned long long>(), s);
+  if (nnz_row) CK(c->acounts.ensure(n * 4), "workspace");
+  afmm_dev::launch_rows<T>(lhs, ld, n32, cb, c->vec_k.as<uint32_t>(),
+                           c->vec_k.as<unsigned long long>(), 0, n32, nnz_row ? 0 : n32,
+                           nnz_row ? n32 : n32, nullptr, 0, nullptr, work, dst, s,
+                           nnz_row ? c->acounts.as<uint32_t>() : nullptr);
   CK(cudaMemcpyAsync(work_host, work, n * 8, cudaMemcpyDeviceToHost, s), "work readback");
+  if (nnz_row) {
+    const uint32_t tc = afmm_dev::aform_tile_cols<T>();
+    const uint64_t ntiles = (n + tc - 1) / tc, ldc = round_up(n, 64);
+    CK(c->cnt16.ensure(n * ldc * sizeof(__half)), "workspace");
+    CK(c->rmax.ensure(n * ntiles * sizeof(uint16_t)), "workspace");
+    CK(c->fstats.ensure(4 * sizeof(unsigned long long)), "workspace");
+    CK(cudaMemsetAsync(c->fstats.p, 0, 4 * sizeof(unsigned long long), s), "memset");
+    afmm_dev::launch_counts_f16<T>(rhs, ld, n32, tc, c->cnt16.as<__half>(), ldc,
+                                   c->rmax.as<uint16_t>(), c->fstats.as<unsigned long long>(), s);
+    nnz_row->resize(n);
+    CK(cudaMemcpyAsync(nnz_row->data(), c->acounts.p, n * 4, cudaMemcpyDeviceToHost, s),
+       "readback");
+    CK(cudaMemcpyAsync(c->stats_host, c->fstats.p, 4 * 8, cudaMemcpyDeviceToHost, s), "readback");
+  }
   CK(cudaStreamSynchronize(s), "work readback");
+  if (fstats && nnz_row) std::memcpy(fstats, c->stats_host, 4 * 8);
   return AFMM_OK;
+}
+
+afmm_status row_query(afmm_context* c, int32_t which, int32_t dtype, const void* lhs,
+                      const void* rhs, uint64_t n, uint64_t ld, uint64_t* out, bool cost,
+                      afmm_error* err) {
+  clear_error(err);
+  if (!c || !out || (dtype != AFMM_F64 && dtype != AFMM_F32) ||
+      (which != AFMM_CASE_A && which != AFMM_CASE_B) || !lhs || !rhs)
+    return AFMM_ERR_INVALID_ARGUMENT;
+  afmm_status st = check_dims(which, n, n, err);
+  if (st != AFMM_OK) return st;
+  if (ld < n) return AFMM_ERR_INVALID_ARGUMENT;
+  return guarded([&]() -> afmm_status {
+    std::lock_guard<std::mutex> g(c->mu);
+    CK(cudaSetDevice(c->device), "afmm: cudaSetDevice");
+    const bool case_a_cost = cost && which == AFMM_CASE_A;
+    std::vector<uint32_t> nnz;
+    unsigned long long fstats[4] = {0, 0, 0, 0};
+    std::vector<uint64_t> work(cost ? n : 0);
+    uint64_t* w = cost ? work.data() : out;
+    afmm_status r =
+        dtype == AFMM_F64
+            ? row_stats<double>(c, which, static_cast<const double*>(lhs),
+                                static_cast<const double*>(rhs), n, ld, w,
+                                case_a_cost ? &nnz : nullptr, fstats, err)
+            : row_stats<float>(c, which, static_cast<const float*>(lhs),
+                               static_cast<const float*>(rhs), n, ld, w,
+                               case_a_cost ? &nnz : nullptr, fstats, err);
+    if (r != AFMM_OK || !cost) return r;
+    row_costs(which, dtype == AFMM_F64 ? 8 : 4, n, sm_count(c->device), w,
+              case_a_cost ? nnz.data() : nullptr, fstats, out);
+    return AFMM_OK;
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+afmm_status afmm_row_work_device(afmm_context* c, int32_t which_case, int32_t dtype,
+                                 const void* lhs, const void* rhs, uint64_t n, uint64_t ld,
+                                 uint64_t* work_host, afmm_error* err) {
+  return row_query(c, which_case, dtype, lhs, rhs, n, ld, work_host, false, err);
+}
+
+afmm_status afmm_row_cost_device(afmm_context* c, int32_t which_case, int32_t dtype,
+                                 const void* lhs, const void* rhs, uint64_t n, uint64_t ld,
+                                 uint64_t* cost, afmm_error* err) {
+  return row_query(c, which_case, dtype, lhs, rhs, n, ld, cost, true, err);
 }
 
 afmm_status afmm_partition_rows(const uint64_t* work, uint64_t n, uint32_t parts, uint64_t* cuts) {
@@ -1231,12 +1700,16 @@ afmm_status afmm_fp_add_peak(int32_t device, int32_t dtype, double* adds_per_sec
   return e == cudaSuccess ? AFMM_OK : AFMM_ERR_CUDA;
 }
 
+}  // extern "C"
+
 // ---- peer-memory output -----------------------------------------------------
 
 namespace {
 std::mutex g_ipc_mu;
 std::vector<std::pair<void*, void*>> g_ipc_open;  // (pointer handed out, mapped base)
 }  // namespace
+
+extern "C" {
 
 afmm_status afmm_ipc_export(const void* dev_ptr, afmm_ipc_handle* handle, afmm_error* err) {
   clear_error(err);

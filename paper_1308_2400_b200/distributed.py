@@ -3,9 +3,11 @@
 Z row i depends only on X row i and all of Y (kernels.hpp:119 and :148 loop over
 independent rows), so the product shards by contiguous Z-row ranges:
 
-  1. every rank computes the exact per-row work W_i on its own GPU
-     (afmm_row_work_device; Y and X are replicated, so no communication) and
-     cuts the rows into `world` ranges of equal total work (afmm_partition_rows);
+  1. every rank computes the predicted kernel time of each row on its own GPU
+     (afmm_row_cost_device: W_i for Case B, the Case A cost model for Case A,
+     whose A-form time follows a row's nonzero bases and whose B-form time does
+     not; Y and X are replicated, so no communication) and cuts the rows into
+     `world` ranges of equal predicted time (afmm_partition_rows);
   2. every rank runs the product on its row slab (afmm_product_device);
   3. the slabs land in rank 0's Z. Default ("p2p"): rank 0 exports its Z
      buffer over CUDA IPC, the other ranks map it (peer access over NVLink /
@@ -75,7 +77,12 @@ class PeerResult:
         self._ptr = None
 
     def exchange(self, z_full):
-        """(enabled, pointer of rank 0's Z in this process or None on rank 0, its ld)."""
+        """(enabled, pointer of rank 0's Z in this process or None on rank 0, its ld).
+
+        Every rank must be able to map the buffer: a rank that cannot (no peer
+        access, IPC blocked) says so in an all-reduced flag and then ALL ranks
+        fall back to the send/recv gather together (none is left waiting in a
+        barrier the others never reach)."""
         msg = np.zeros(81, dtype=np.uint8)
         if self.rank == 0 and getattr(z_full, "is_cuda", False):
             try:
@@ -86,22 +93,32 @@ class PeerResult:
                                                     dtype=np.uint64).tobytes(), dtype=np.uint8)
             except Exception:
                 msg[0] = 0
+        on_gpu = self.dist.get_backend() == "nccl"
         t = torch.from_numpy(msg)
-        if self.dist.get_backend() == "nccl":
+        if on_gpu:
             t = t.cuda(self.device)
         self.dist.broadcast(t, src=0)
         msg = t.cpu().numpy()
-        if msg[0] == 0:
+        ok, ptr, ld = False, None, 0
+        if msg[0] != 0:
+            offset, ld = (int(v) for v in np.frombuffer(msg[65:81].tobytes(), dtype=np.uint64))
+            ok = True
+            if self.rank != 0:
+                key = msg[:73].tobytes()
+                if key != self._key:
+                    self.close()
+                    try:
+                        self._ptr = ipc_open(self.device, msg[1:65].tobytes(), offset)
+                        self._key = key
+                    except Exception:
+                        ok = False
+                ptr = self._ptr
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32,
+                            device=f"cuda:{self.device}" if on_gpu else "cpu")
+        self.dist.all_reduce(flag, op=self.dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
             return False, None, 0
-        offset, ld = (int(v) for v in np.frombuffer(msg[65:81].tobytes(), dtype=np.uint64))
-        if self.rank == 0:
-            return True, None, ld
-        key = msg[:73].tobytes()
-        if key != self._key:
-            self.close()
-            self._ptr = ipc_open(self.device, msg[1:65].tobytes(), offset)
-            self._key = key
-        return True, self._ptr, ld
+        return True, ptr, ld
 
     def close(self) -> None:
         if self._ptr is not None:
@@ -133,8 +150,8 @@ class ShardedProduct:
             counts = self.ctx.product(case, lhs, rhs, z_full, 0, n, mode=mode)
             self.cuts = np.array([0, n])
             return counts
-        work = self.ctx.row_work(case, lhs, rhs)
-        cuts = partition_rows(work, self.world)
+        cost = self.ctx.row_cost(case, lhs, rhs)
+        cuts = partition_rows(cost, self.world)
         self.cuts = cuts
         r0, r1 = int(cuts[self.rank]), int(cuts[self.rank + 1])
         ok, peer, ld = self._peer.exchange(z_full) if self._peer else (False, None, 0)

@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert set(declared) == set(_lib.EXPORTED_SYMBOLS)
-    assert lib.afmm_abi_version() == 1
+    assert lib.afmm_abi_version() == _lib.ABI_VERSION == 2
 
 
 def test_library_is_sm100a_only():
@@ -134,3 +134,21 @@ def test_cpp_wrapper_header_compiles():
                         os.path.join(ROOT, "include"), "-"], input=src, capture_output=True,
                        text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_bench_refuses_more_gpus_than_visible():
+    """`bench.py --gpus N` without torchrun drives N devices in one process; it
+    refuses (exit 2, no JSON line) when fewer are visible instead of timing one
+    GPU under an N-GPU label."""
+    import sys
+
+    import torch
+
+    if torch.cuda.device_count() >= 4:
+        pytest.skip("enough GPUs")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4",
+                        "--steps", "1", "--warmup", "3", "--size", "64"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 2
+    assert not [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert "refusing" in r.stderr

@@ -32,6 +32,8 @@ class OracleContext:
         nnz = (r != 0).sum(axis=1)
         return (np.abs(np.rint(l)) * nnz[None, :]).sum(axis=1).astype(np.uint64)
 
+    row_cost = row_work  # the GPU context predicts time; W_i stands in for it here
+
     def product(self, which, lhs, rhs, out, r0, r1, mode="order-preserving"):
         z, counts, err = self.oracle.product(which, lhs.numpy(), rhs.numpy(), r0, r1)
         assert err is None
@@ -92,3 +94,41 @@ def test_two_rank_gloo_sharded_product_matches_single_process(tmp_path, case, n,
     assert int(meta[0]) == counts[0] == expected_additions(case, lhs, rhs)
     cuts = meta[1:].astype(int)
     assert cuts[0] == 0 and cuts[-1] == n and 0 < cuts[1] < n
+
+
+def _ipc_worker(rank, world, port, result_path):
+    """Rank 0 exports (faked), rank 1 cannot open the handle: both ranks must
+    agree to fall back to the send/recv gather (none may hang in a barrier)."""
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1308_2400_b200.distributed as D
+
+    class FakeCuda:  # a "device tensor" for the export step
+        is_cuda = True
+
+        def stride(self, i):
+            return 7
+
+    D.ipc_export = lambda t: (bytes(range(64)), 128)
+
+    def failing_open(device, handle, offset):
+        raise RuntimeError("cudaIpcOpenMemHandle: peer access unavailable")
+
+    D.ipc_open = failing_open
+    peer = D.PeerResult(dist, rank, 0)
+    ok, ptr, ld = peer.exchange(FakeCuda() if rank == 0 else None)
+    dist.barrier()
+    np.save(result_path + f".{rank}.npy", np.array([1 if ok else 0]))
+    dist.destroy_process_group()
+
+
+def test_ipc_open_failure_falls_back_on_every_rank(tmp_path):
+    out = str(tmp_path / "ipc")
+    mp.spawn(_ipc_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    assert int(np.load(out + ".0.npy")[0]) == 0
+    assert int(np.load(out + ".1.npy")[0]) == 0

@@ -96,12 +96,23 @@ def test_non_finite_is_domain_error(cuda):
         afmm.afmm_case_b(x, y)
 
 
-def test_rep_too_large_is_reported(cuda):
+@pytest.mark.parametrize("case", ["a", "b"])
+def test_huge_rep_beyond_int32_is_accepted_and_exact(cuda, oracle, case):
+    """The reference accepts any rep with |rep| <= 2^53 (kernels.hpp:36-39). A
+    rep of 2^31 + 5 does not fit one int32 list entry: it is split into
+    consecutive entries at the same k (2^31 - 1, then 6), so the element still
+    receives its |rep| sequential adds in order -- bit-exact against the
+    oracle, and the additions count is exact."""
     afmm = _api()
-    y = np.eye(2)
-    y[0, 1] = 2.0 ** 31
-    with pytest.raises(afmm.UnsupportedError, match=r"rhs\[0\]\[1\]"):
-        afmm.afmm_case_a(np.eye(2), y)
+    huge = float(2 ** 31 + 5)
+    bases = np.array([[0.5, -0.25], [1e-3, 3.0]])
+    reps = np.array([[1.0, huge], [-2.0, 0.0]])
+    lhs, rhs = (bases, reps) if case == "a" else (reps.T.copy(), bases)
+    z, c, err = oracle.product(case, lhs, rhs)
+    assert err is None
+    res = _call(case, lhs, rhs)
+    assert (res.counts.additions, res.counts.multiplications, res.counts.zero_skips) == c
+    assert _bits_equal(res.product, z)
 
 
 @pytest.mark.parametrize("dt", [np.float64, np.float32])
@@ -126,10 +137,6 @@ def test_errors_on_the_case_a_statistics_path(cuda, dt):
     nf[5, 6] = np.nan
     with pytest.raises(afmm.DomainError, match="non-finite"):
         afmm.afmm_case_a(nf, rhs)
-    big = rhs.copy()
-    big[10, 10] = 3.0e9
-    with pytest.raises(afmm.UnsupportedError, match=r"rhs\[10\]\[10\]"):
-        afmm.afmm_case_a(lhs, big)
     # and a valid call on the same context afterwards is exact
     res = afmm.afmm_case_a(lhs, rhs)
     assert res.counts.multiplications == 0
@@ -442,7 +449,7 @@ def test_subnormal_bases_are_not_flushed(cuda, oracle, dt, case, monkeypatch):
     O = torch.empty_like(L)
     rows = (0, 1, n // 3, n - 1)
     want = {r: oracle.product_mt(case, lhs, rhs, r, r + 1, 1)[0] for r in rows}
-    forms = ["aform", "wide"] if case == "a" else ["wide", "small"]
+    forms = ["aform", "wide", "quad"] if case == "a" else ["wide", "small", "quad"]
     for form in forms:
         monkeypatch.setenv("AFMM_BFORM", form)
         ctx = afmm.DeviceContext(0)  # reads AFMM_BFORM at creation
@@ -500,9 +507,11 @@ def test_fast_mode_within_tolerance(cuda, oracle, name, n, kw):
     assert float(err.max()) <= tol, (name, float(err.max()))
 
 
-@pytest.mark.parametrize("variant", ["wide", "ring", "small", "mr", "tmem", "aform"])
+@pytest.mark.parametrize("variant", ["wide", "ring", "small", "quad", "quadsmall", "aform",
+                                     "hybrid"])
 def test_both_kernel_variants_bit_exact(cuda, oracle, variant, monkeypatch):
-    """k_bform (TMA smem ring) and k_bform_l1 (decoupled warps) give identical bits."""
+    """Every B-form tile shape (one row or a row quad per warp) and the forced
+    Case A forms give the oracle's bits."""
     import torch
 
     from paper_1308_2400_b200.gen import CONFIGS, make_inputs
@@ -531,7 +540,7 @@ def test_randomized_shapes_and_distributions(cuda, oracle, seed, monkeypatch):
     import torch
 
     rng = np.random.default_rng(1000 + seed)
-    variants = [None, "wide", "ring", "small", "aform", "hybrid", "tmem"]
+    variants = [None, "wide", "ring", "small", "quad", "quadsmall", "aform", "hybrid"]
     for trial in range(16):
         variant = variants[rng.integers(len(variants))]
         if variant:
@@ -758,3 +767,127 @@ def test_phase_timing_on_graph_replays(cuda):
     ctx.product("b", L, R, Z)
     assert ctx.last_timing() == (-1.0, -1.0, -1.0)
     ctx.close()
+
+
+@pytest.mark.parametrize("dt,n", [(np.float32, 1100), (np.float64, 1300)])
+def test_case_a_large_n_is_async_and_replayed(cuda, oracle, dt, n):
+    """Case A with n >= 1024 chooses its form on the device (k_choose), so the
+    call enqueues without waiting on the host (sync=False returns before the
+    kernels finish) and repeated calls are captured and replayed as CUDA graphs
+    (a constant number of kernels per call); every replay re-decides from the
+    current data and stays bit-exact."""
+    import torch
+
+    from paper_1308_2400_b200.gen import make_inputs
+
+    afmm = _api()
+    ctx = afmm.DeviceContext(0)
+    lhs, rhs = make_inputs("cfg3", seed=17, n=n, d1=0.1, mu=4)
+    lhs, rhs = lhs.astype(dt), rhs.astype(dt)
+    L = torch.from_numpy(lhs).cuda()
+    R = torch.from_numpy(rhs).cuda()
+    O = torch.empty_like(L)
+    launches, forms = [], []
+    for it in range(5):
+        if it == 3:  # densify X in place: the replayed graph must re-decide
+            L.copy_(torch.from_numpy(np.where(lhs == 0, 0.5, lhs).astype(dt)))
+        k0 = afmm.kernel_launch_count()
+        assert ctx.product("a", L, R, O, sync=False) is None
+        c = ctx.finish()
+        launches.append(afmm.kernel_launch_count() - k0)
+        forms.append(ctx.last_form())
+        z, cc = oracle.product_mt("a", L.cpu().numpy(), rhs, 0, n, 16)
+        assert (c.additions, 0, c.zero_skips) == cc, it
+        assert _bits_equal(O.cpu().numpy(), z), (it, forms[-1])
+    assert len(set(launches)) == 1, launches
+    assert forms[0] == "aform" and forms[-1] == "bform", forms
+    ctx.close()
+
+
+def test_set_stream_keeps_a_pending_product(cuda, oracle):
+    """afmm_context_set_stream drains a pending asynchronous product on the old
+    stream, so finish() still reports that product's counts."""
+    import torch
+
+    from paper_1308_2400_b200.gen import make_inputs
+
+    afmm = _api()
+    ctx = afmm.DeviceContext(0)
+    lhs, rhs = make_inputs("cfg2", seed=4, n=700)
+    L = torch.from_numpy(lhs).cuda()
+    R = torch.from_numpy(rhs).cuda()
+    O = torch.empty_like(L)
+    ctx.product("b", L, R, O, sync=False)
+    s = torch.cuda.Stream()
+    ctx.set_stream(s)
+    c = ctx.finish()
+    z, cc, _ = oracle.product("b", lhs, rhs)
+    assert (c.additions, 0, c.zero_skips) == cc
+    assert _bits_equal(O.cpu().numpy(), z)
+    with torch.cuda.stream(s):
+        c2 = ctx.product("b", L, R, O)
+    assert c2 == c
+    ctx.close()
+
+
+def test_unfinished_failed_product_is_reported_by_the_next_call(cuda):
+    """A failed asynchronous product that was never finished is reported by
+    the next call on the context (its error is not dropped)."""
+    import torch
+
+    afmm = _api()
+    ctx = afmm.DeviceContext(0)
+    n = 300
+    L = torch.eye(n, dtype=torch.float64, device="cuda")
+    bad = torch.eye(n, dtype=torch.float64, device="cuda")
+    bad[5, 9] = 0.5
+    O = torch.empty_like(L)
+    ctx.product("b", bad, L, O, sync=False)
+    with pytest.raises(afmm.DomainError, match=r"lhs\[5\]\[9\] = 0.500000"):
+        ctx.product("b", L, L, O)
+    assert ctx.product("b", L, L, O).additions == n
+
+
+def test_device_api_rejects_bad_tensors(cuda):
+    """The device entry checks what the C ABI cannot: tensors on the context's
+    device and an `out` large enough for the slab."""
+    import torch
+
+    afmm = _api()
+    ctx = afmm.DeviceContext(0)
+    L = torch.eye(64, device="cuda")
+    with pytest.raises(afmm.InvalidArgument, match="CUDA tensor"):
+        ctx.product("a", L.cpu(), L, torch.empty_like(L))
+    with pytest.raises(afmm.InvalidArgument, match="slab needs"):
+        ctx.product("a", L, L, torch.empty((10, 64), device="cuda"), 0, 64)
+    with pytest.raises(afmm.InvalidArgument, match="slab needs"):
+        ctx.product("a", L, L, torch.empty((64, 32), device="cuda"))
+    ctx.close()
+
+
+@pytest.mark.parametrize("case", ["a", "b"])
+def test_quad_lists_split_reps_beyond_int16(cuda, oracle, monkeypatch, case):
+    """Quad lists hold int16 reps: a |rep| above 32767 continues in further
+    entries at the same k (the other rows of the quad get 0 there), so each
+    element's adds stay consecutive -- bit-exact, counts exact."""
+    import torch
+
+    monkeypatch.setenv("AFMM_BFORM", "quad")
+    afmm = _api()
+    rng = np.random.default_rng(12)
+    n = 300
+    bases = rng.standard_normal((n, n)) * (rng.random((n, n)) < 0.6)
+    reps = rng.integers(-6, 7, (n, n)).astype(np.float64)
+    reps[7, 3] = 40000.0
+    reps[8, 3] = -70001.0
+    reps[100, 250] = 32768.0
+    lhs, rhs = (bases, reps) if case == "a" else (reps, bases)
+    ctx = afmm.DeviceContext(0)
+    L = torch.from_numpy(lhs).cuda()
+    R = torch.from_numpy(rhs).cuda()
+    O = torch.empty_like(L)
+    c = ctx.product(case, L, R, O)
+    ctx.close()
+    z, cc = oracle.product_mt(case, lhs, rhs, 0, n, 16)
+    assert (c.additions, 0, c.zero_skips) == cc
+    assert _bits_equal(O.cpu().numpy(), z)
