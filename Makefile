@@ -29,7 +29,7 @@ oracle:
 # The reference's kernel tests restated against the drop-in C++ front end
 # (needs the reference headers, so it is built in the build container; the
 # binary travels to the GPU box with the snapshot).
-cpptest: build/test_gpu_kernels build/afmm_gpu
+cpptest: build/test_gpu_kernels build/afmm_gpu build/acceptance_gpu
 build/afmm_gpu: tools/afmm_gpu_cli.cpp include/afmm_b200/kernels.hpp include/afmm_b200.h $(LIB)
 	@mkdir -p build
 	g++ -std=c++20 -O2 -ffp-contract=off -I$(REF_INC) -Iinclude -o $@ $< \
@@ -37,6 +37,12 @@ build/afmm_gpu: tools/afmm_gpu_cli.cpp include/afmm_b200/kernels.hpp include/afm
 build/test_gpu_kernels: tests/cpp/test_gpu_kernels.cpp include/afmm_b200/kernels.hpp include/afmm_b200.h $(LIB)
 	@mkdir -p build
 	g++ -std=c++20 -O2 -ffp-contract=off -I$(REF_INC) -Iinclude -o $@ $< \
+	    -L paper_1308_2400_b200 -lafmm_b200 -Wl,-rpath,'$$ORIGIN/../paper_1308_2400_b200'
+
+# The reference's acceptance gate with its AFMM calls on the B200 (test only)
+build/acceptance_gpu: tests/cpp/acceptance_gpu.cpp tests/cpp/acceptance_gpu_shim.hpp include/afmm_b200/kernels.hpp include/afmm_b200.h $(LIB)
+	@mkdir -p build
+	g++ -std=c++20 -O2 -ffp-contract=off -I$(REF_INC) -Iinclude -Itests/cpp -o $@ $< \
 	    -L paper_1308_2400_b200 -lafmm_b200 -Wl,-rpath,'$$ORIGIN/../paper_1308_2400_b200'
 
 sass: $(LIB)

@@ -195,6 +195,23 @@ afmm_status afmm_row_cost_device(afmm_context* ctx, int32_t which_case, int32_t 
                                  const void* lhs, const void* rhs, uint64_t n, uint64_t ld,
                                  uint64_t* cost, afmm_error* error);
 
+/* Row cuts for `parts` devices from the operands' statistics (computed on
+ * the context's device): Case B equal W_i; Case A equal modeled kernel time,
+ * the device-side A-form / B-form choice evaluated per slab (tile and wave
+ * quantisation included). cuts[parts + 1] as in afmm_partition_rows. */
+afmm_status afmm_partition_device(afmm_context* ctx, int32_t which_case, int32_t dtype,
+                                  const void* lhs, const void* rhs, uint64_t n, uint64_t ld,
+                                  uint32_t parts, uint64_t* cuts, afmm_error* error);
+
+/* The same Case A cut from given statistics, on the host (no device): stats =
+ * {nonzero reps of Y, sum over (k, A-form tile) of the tile's max |rep|, reps
+ * beyond 2048, sum of |rep|}, nnz_row[n] = nonzero bases of each row of X;
+ * sms = SM count (0 = 148). slab_cycles[parts] (optional) receives each
+ * slab's modeled time. */
+afmm_status afmm_model_partition_case_a(int32_t dtype, uint64_t n, int32_t sms,
+                                        const uint64_t* stats, const uint32_t* nnz_row,
+                                        uint32_t parts, uint64_t* cuts, double* slab_cycles);
+
 /* Cut n rows into `parts` contiguous ranges of (as near as possible) equal
  * total work: cuts[0] = 0, cuts[parts] = n, range p = [cuts[p], cuts[p+1]).
  * Pure host function (no device needed). */

@@ -159,6 +159,9 @@ class Reference:
         lib.ref_run_plan_csv.argtypes = [c_int, c_void_p, c_size_t, c_double, c_double, c_double,
                                          c_uint64, c_uint64, c_uint64, c_char_p, c_size_t,
                                          POINTER(c_size_t), c_char_p, c_size_t]
+        lib.ref_emit_table.restype = c_int
+        lib.ref_emit_table.argtypes = [c_char_p, c_char_p, c_size_t, POINTER(c_size_t), c_char_p,
+                                       c_size_t]
         lib.ref_case_rows.restype = c_int
         lib.ref_case_rows.argtypes = [c_int, c_void_p, c_uint64, c_uint64, c_uint64, c_void_p,
                                       c_void_p, POINTER(Counts), c_char_p, c_size_t]
@@ -193,6 +196,21 @@ class Reference:
             rc = self.lib.ref_run_plan_csv(1 if case == "b" else 0, sz.ctypes.data, len(sz), d1,
                                            d2, mu, reps, warmups, seed, buf, cap,
                                            ctypes.byref(need), msg, 512)
+            if rc == -1:
+                cap = need.value
+                continue
+            if rc != 0:
+                raise RuntimeError(msg.value.decode())
+            return buf.value.decode()
+
+    def emit_table(self, csv_text: str) -> str:
+        """The reference's parse_csv + emit_table (report.hpp:74-124, 265-267)."""
+        cap = 1 << 16
+        while True:
+            buf = ctypes.create_string_buffer(cap)
+            need = c_size_t()
+            msg = ctypes.create_string_buffer(512)
+            rc = self.lib.ref_emit_table(csv_text.encode(), buf, cap, ctypes.byref(need), msg, 512)
             if rc == -1:
                 cap = need.value
                 continue

@@ -188,6 +188,28 @@ int ref_run_plan_csv(int case_b, const std::uint64_t* sizes, std::size_t nsizes,
   return rc != 0 ? rc : fit;
 }
 
+// The reference's report flow: parse_csv (report.hpp:74-124) + emit_table
+// (report.hpp:265-267) of the record CSV text `csv`, into `out`. Returns 0,
+// -1 when `out` is too small (the needed size in *needed), or the status of
+// the reference's exception (its message in msg).
+int ref_emit_table(const char* csv, char* out, std::size_t cap, std::size_t* needed, char* msg,
+                   std::size_t msg_cap) {
+  int fit = 0;
+  const int rc = guarded(
+      [&] {
+        std::istringstream in(csv);
+        const std::string s = afmm::emit_table(afmm::parse_csv(in));
+        *needed = s.size() + 1;
+        if (s.size() + 1 > cap) {
+          fit = -1;
+          return;
+        }
+        std::memcpy(out, s.c_str(), s.size() + 1);
+      },
+      msg, msg_cap);
+  return rc != 0 ? rc : fit;
+}
+
 // ---- row-block entry for the CPU baseline (bench.py) ----
 // A DenseMatrix held across calls (the shared rhs of a timing batch).
 void* ref_hold_matrix(const double* p, std::uint64_t n, char* msg, std::size_t cap) {

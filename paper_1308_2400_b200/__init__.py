@@ -17,13 +17,16 @@ from .afmm import (  # noqa: F401
     UnsupportedError,
     afmm_case_a,
     afmm_case_b,
+    case_a_statistics,
     fp_add_peak,
     kernel_launch_count,
+    model_partition_case_a,
     partition_rows,
 )
 
 __all__ = [
     "afmm_case_a", "afmm_case_b", "MultiplyResult", "OpCounts", "ShapeError", "DomainError",
     "InvalidArgument", "UnsupportedError", "DeviceError", "DeviceContext", "partition_rows",
-    "fp_add_peak", "kernel_launch_count", "ORDER_PRESERVING", "FAST",
+    "fp_add_peak", "kernel_launch_count", "ORDER_PRESERVING", "FAST", "case_a_statistics",
+    "model_partition_case_a",
 ]

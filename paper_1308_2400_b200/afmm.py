@@ -343,6 +343,20 @@ class DeviceContext:
         """W_i: exact additions of each Z row (afmm_row_work_device)."""
         return self._row_query(self._lib.afmm_row_work_device, which, lhs, rhs)
 
+    def partition(self, which: str, lhs, rhs, parts: int) -> np.ndarray:
+        """Row cuts for `parts` devices (afmm_partition_device): equal W_i for
+        Case B, equal modeled kernel time for Case A."""
+        lp, ld, dname, n = _tensor_info(lhs, self.device, "lhs")
+        rp, _, _, _ = _tensor_info(rhs, self.device, "rhs")
+        self._follow_torch_stream()
+        cuts = np.zeros(int(parts) + 1, dtype=np.uint64)
+        err = _lib.Error()
+        status = self._lib.afmm_partition_device(
+            self._h, _lib.CASE_A if which == "a" else _lib.CASE_B, _DT_CODE[dname], lp, rp, n, ld,
+            int(parts), cuts.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), ctypes.byref(err))
+        _raise_for(status, err)
+        return cuts.astype(np.int64)
+
     def row_cost(self, which: str, lhs, rhs) -> np.ndarray:
         """Predicted kernel time of each Z row (afmm_row_cost_device): W_i for
         Case B, the Case A cost model (cheaper of A-form and B-form) for Case A."""
@@ -359,6 +373,47 @@ def partition_rows(work, parts: int) -> np.ndarray:
     if status != _lib.OK:
         raise InvalidArgument("afmm_partition_rows: invalid arguments")
     return cuts.astype(np.int64)
+
+
+def case_a_statistics(lhs: np.ndarray, rhs: np.ndarray):
+    """(stats[4], nnz_row[n]) of a Case A problem as the prepass computes them
+    (host restatement for model queries): nonzero reps of Y, sum over (k,
+    A-form tile) of the tile's max |rep|, reps beyond 2048, sum of |rep|; and
+    the nonzero bases of each row of X."""
+    n = lhs.shape[0]
+    tile = 1024 if lhs.dtype == np.float32 else 512
+    reps = np.where(rhs != 0, np.rint(rhs.astype(np.float64)), 0).astype(np.int64)
+    # llround rounds half away from zero; np.rint to even: fix the halves
+    half = np.abs(rhs.astype(np.float64) - np.trunc(rhs.astype(np.float64))) == 0.5
+    reps[half] = (np.trunc(rhs[half]) + np.sign(rhs[half])).astype(np.int64)
+    a = np.abs(reps)
+    ntiles = (n + tile - 1) // tile
+    trip = 0
+    for t in range(ntiles):
+        trip += int(np.minimum(a[:, t * tile:(t + 1) * tile], 2048).max(axis=1).sum())
+    stats = np.array([int((a != 0).sum()), trip, int((a > 2048).sum()), int(a.sum())],
+                     dtype=np.uint64)
+    nnz_row = (lhs != 0).sum(axis=1).astype(np.uint32)
+    return stats, nnz_row
+
+
+def model_partition_case_a(stats, nnz_row, parts: int, dtype: str = "float32",
+                           sms: int = 148) -> Tuple[np.ndarray, np.ndarray]:
+    """Case A row cuts by modeled kernel time and each slab's modeled cycles
+    (afmm_model_partition_case_a; host only, no device)."""
+    lib = _lib.load()
+    st = np.ascontiguousarray(stats, dtype=np.uint64)
+    nz = np.ascontiguousarray(nnz_row, dtype=np.uint32)
+    cuts = np.zeros(int(parts) + 1, dtype=np.uint64)
+    cyc = np.zeros(int(parts), dtype=np.float64)
+    status = lib.afmm_model_partition_case_a(
+        _DT_CODE[dtype], nz.size, int(sms), st.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+        nz.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), int(parts),
+        cuts.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+        cyc.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    if status != _lib.OK:
+        raise InvalidArgument("afmm_model_partition_case_a: invalid arguments")
+    return cuts.astype(np.int64), cyc
 
 
 def fp_add_peak(device: int = 0, dtype: str = "float32") -> Tuple[float, float]:

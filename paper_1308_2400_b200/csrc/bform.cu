@@ -307,28 +307,9 @@ struct Cursor {
   }
 };
 
-// List entry of R B-form rows: R = 1 -> int2 {k, rep} (zero reps compacted
-// away); R = 4 -> int4 {k, rep0 | rep1 << 16, rep2 | rep3 << 16, 0} for the
-// rows of a quad, int16 reps (a zero rep is a row without a term at k).
-template <int R>
-struct Entry;
-template <>
-struct Entry<1> {
-  using type = int2;
-};
-template <>
-struct Entry<4> {
-  using type = int4;
-  __device__ __forceinline__ static int rep(const int4& e, int q) {
-    const int w = q < 2 ? e.y : e.z;
-    return (q & 1) ? (w >> 16) : (int)(short)(w & 0xffff);
-  }
-};
-
 // First list index with k >= key (lists are sorted by k); every lane computes
 // the same answer from broadcast loads.
-template <class E>
-__device__ __forceinline__ uint32_t lower_bound_k(const E* lst, uint32_t cnt, uint32_t key) {
+__device__ __forceinline__ uint32_t lower_bound_k(const int2* lst, uint32_t cnt, uint32_t key) {
   uint32_t lo = 0, hi = cnt;
   while (lo < hi) {
     const uint32_t mid = (lo + hi) >> 1;
@@ -338,27 +319,22 @@ __device__ __forceinline__ uint32_t lower_bound_k(const E* lst, uint32_t cnt, ui
   return lo;
 }
 
-// k_bform: each consumer warp owns R B-form rows ("group" b: rows R*b ..
-// R*b + R - 1) of a TILE_N-column tile and walks the group's list.
-//   lists: group b's entries at lists[b * cap .. b * cap + counts[b]), k increasing.
-//   Output row r, column (col0 + c) -> out[r * ld_out + c], c < ncols.
+// k_bform: each consumer warp owns one B-form row b of a TILE_N-column tile
+// and walks the row's (k, rep) list.
+//   lists: row b's entries at lists[b * cap .. b * cap + counts[b]), k increasing.
+//   Output row b, column (col0 + c) -> out[b * ld_out + c], c < ncols.
 //   dyn_ncols (optional): ncols decided on the device (Case A row split).
 //   k slice: blockIdx.z selects slice z = [z*slice_blocks, (z+1)*slice_blocks)
 //   of the nkb_total k blocks and writes to out + z * slice_stride (fast-mode
 //   split-k; one slice = the whole k range in order-preserving mode).
-// R = 4 ("quad" lists): the bases of an entry are loaded once for four rows,
-// so each 16-byte LDS feeds up to 4x as many adds -- the small-rep regime is
-// bound by the shared-memory data pipe with R = 1.
-template <class T, int G, int CW, int STAGES, int MINB, int R, bool SPLIT>
+template <class T, int G, int CW, int STAGES, int MINB, bool SPLIT>
 __global__ void __launch_bounds__((CW + 1) * 32, MINB)
-    k_bform(const __grid_constant__ CUtensorMap tmap,
-            const typename Entry<R>::type* __restrict__ lists, uint64_t cap,
-            const uint32_t* __restrict__ counts, uint32_t nrows, uint32_t gpc, int32_t col0,
-            int32_t ncols, const uint32_t* __restrict__ dyn_ncols, uint32_t nkb_total,
-            uint32_t slice_blocks, uint64_t slice_stride, T* __restrict__ out, uint64_t ld_out,
-            int vec_ok, const DevStatus* __restrict__ st) {
+    k_bform(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ lists,
+            uint64_t cap, const uint32_t* __restrict__ counts, uint32_t nrows, uint32_t rpc,
+            int32_t col0, int32_t ncols, const uint32_t* __restrict__ dyn_ncols,
+            uint32_t nkb_total, uint32_t slice_blocks, uint64_t slice_stride,
+            T* __restrict__ out, uint64_t ld_out, int vec_ok, const DevStatus* __restrict__ st) {
   using Gm = Geo<T, G>;
-  using E = typename Entry<R>::type;
   extern __shared__ unsigned char smem_raw[];
   // 128-byte aligned ring (TMA destination without swizzle); pointer arithmetic
   // on the smem pointer itself keeps the shared address space visible to the
@@ -405,13 +381,12 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
     return;
   }
 
-  // ---- consumers: R output rows per warp ----
-  // gpc <= CW groups per CTA (the launcher trims it to balance the last wave);
+  // ---- consumers: one output row per warp ----
+  // rpc <= CW rows per CTA (the launcher trims it to balance the last wave);
   // warps past it walk no entries but still release every stage.
-  const uint32_t ngroups = (nrows + R - 1) / R;
-  const uint32_t b = warp < gpc ? blockIdx.x * gpc + warp : ngroups;
-  uint32_t cnt = b < ngroups ? counts[b] : 0u;
-  const E* lst = lists + (uint64_t)(b < ngroups ? b : 0) * cap;
+  const uint32_t b = warp < rpc ? blockIdx.x * rpc + warp : nrows;
+  uint32_t cnt = b < nrows ? counts[b] : 0u;
+  const int2* lst = lists + (uint64_t)(b < nrows ? b : 0) * cap;
   if (SPLIT) {
     // this slice's entries: [lower_bound(kb_lo*KB), lower_bound(kb_hi*KB))
     const uint32_t p0 = lower_bound_k(lst, cnt, kb_lo * KB);
@@ -420,48 +395,31 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
     cnt = p1 - p0;
   }
 
-  Acc<T, G> acc[R];
-#pragma unroll
-  for (int q = 0; q < R; ++q) acc[q].zero();
+  Acc<T, G> acc;
+  acc.zero();
   const uint32_t k_lo = kb_lo * KB;
   Cursor<STAGES, Gm::STAGE_BYTES> cur(smem_u32(base), smem_u32(full), smem_u32(empty), lane);
   cur.wait();
-  // Entry e + 1 is read by a warp-uniform load (L1 broadcast) while entry e
-  // runs, and the list line kListPrefetch entries ahead is prefetched into L1.
-  // (Measured against one coalesced 32-entry load per chunk + SHFL
-  // broadcasts: equal at cfg5, cfg3 mu = 4 +2.6%, cfg4 +1%, rep 1 -2%; fewer
-  // instructions and branches per entry.)
-  const E* __restrict__ lp = lst;
-  E e = cnt ? __ldg(lp) : E{};
+  // Entry e + 1 = (k, rep) is read by a warp-uniform load (L1 broadcast)
+  // while entry e runs, and the list line kListPrefetch entries ahead is
+  // prefetched into L1. (Measured against one coalesced 32-entry load per
+  // chunk + SHFL broadcasts: equal at cfg5, cfg3 mu = 4 +2.6%, cfg4 +1%, rep
+  // 1 -2%; fewer instructions and branches per entry.)
+  const int2* __restrict__ lp = lst;
+  int2 e = cnt ? __ldg(lp) : make_int2(0, 0);
   for (uint32_t i = 0; i < cnt; ++i) {
     const uint32_t f = i + 1;
-    const E ne = f < cnt ? __ldg(lp + f) : E{};
+    const int2 ne = f < cnt ? __ldg(lp + f) : make_int2(0, 0);
     if (f + kListPrefetch < cnt)
       asm volatile("prefetch.global.L1 [%0];" ::"l"(lp + f + kListPrefetch));
     const uint32_t k = (uint32_t)e.x;
     cur.seek((k - k_lo) / KB, lane);  // block index within the slice
-    const uint32_t row_addr = cur.stage_addr + (k % KB) * BOX_BYTES;
-    if constexpr (R == 1) {
-      acc[0].run(row_addr, e.y);
-    } else {
-      Bases<T, G> s;
-      s.load(row_addr);
-#pragma unroll
-      for (int q = 0; q < R; ++q) {
-        const int r = Entry<R>::rep(e, q);
-        if (r != 0) acc[q].add(s, r);
-      }
-    }
+    acc.run(cur.stage_addr + (k % KB) * BOX_BYTES, e.y);
     e = ne;
   }
   cur.drain(nkb, lane);
 
-#pragma unroll
-  for (int q = 0; q < R; ++q) {
-    const uint32_t row = b * R + q;
-    if (b < ngroups && row < nrows)
-      acc[q].store(out + (uint64_t)row * ld_out, tile_c, ncols, lane, vec_ok != 0);
-  }
+  if (b < nrows) acc.store(out + (uint64_t)b * ld_out, tile_c, ncols, lane, vec_ok != 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -700,13 +658,13 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
   }
 }
 
-template <class T, int G, int CW, int STAGES, int MINB, int R>
+template <class T, int G, int CW, int STAGES, int MINB>
 cudaError_t launch_ring(BformLaunch& a, T* out, cudaStream_t s) {
   const uint32_t nkb = (a.nk + KB - 1) / KB;
   uint32_t want = a.splits < 1 ? 1 : a.splits;
   if (want > nkb) want = nkb;
-  auto kern = want > 1 ? k_bform<T, G, CW, STAGES, MINB, R, true>
-                       : k_bform<T, G, CW, STAGES, MINB, R, false>;
+  auto kern = want > 1 ? k_bform<T, G, CW, STAGES, MINB, true>
+                       : k_bform<T, G, CW, STAGES, MINB, false>;
   const size_t smem = ring_smem_bytes<T, G, STAGES>();
   // set on every call: the attribute is per device and costs ~1 us
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -718,13 +676,11 @@ cudaError_t launch_ring(BformLaunch& a, T* out, cudaStream_t s) {
                       (reinterpret_cast<uintptr_t>(out) % 16) == 0 &&
                       (a.slice_stride * sizeof(T)) % 16 == 0;
   const uint32_t tiles = (a.ncols + Geo<T, G>::TILE_N - 1) / Geo<T, G>::TILE_N;
-  const uint32_t ngroups = (a.nrows + R - 1) / R;
-  const uint32_t gpc = balanced_rows(ngroups, tiles * a.splits, CW, MINB);
-  dim3 grid((ngroups + gpc - 1) / gpc, tiles, a.splits);
-  kern<<<grid, (CW + 1) * 32, smem, s>>>(
-      *a.tmap, static_cast<const typename Entry<R>::type*>(a.lists), a.cap, a.counts, a.nrows,
-      gpc, a.col0, a.ncols, a.dyn_ncols, nkb, slice_blocks, a.slice_stride, out, a.ld_out,
-      vec_ok ? 1 : 0, a.st);
+  const uint32_t rpc = balanced_rows(a.nrows, tiles * a.splits, CW, MINB);
+  dim3 grid((a.nrows + rpc - 1) / rpc, tiles, a.splits);
+  kern<<<grid, (CW + 1) * 32, smem, s>>>(*a.tmap, a.lists, a.cap, a.counts, a.nrows, rpc, a.col0,
+                                         a.ncols, a.dyn_ncols, nkb, slice_blocks, a.slice_stride,
+                                         out, a.ld_out, vec_ok ? 1 : 0, a.st);
   note_launch();
   return cudaGetLastError();
 }
@@ -744,17 +700,11 @@ cudaError_t launch_bform(BformLaunch& a, T* out, cudaStream_t s) {
       // 0.285 ms, cfg3 and cfg4 0.3-2% faster -- the deeper ring lets warps
       // drift 5 k blocks apart instead of 2 (consumers had waited on a stage
       // 6.5% of the time, ncu).
-      return launch_ring<T, 8, kWideRows, 6, kWideCtasPerSm, 1>(a, out, s);
+      return launch_ring<T, 8, kWideRows, 6, kWideCtasPerSm>(a, out, s);
     case kShapeSmall:  // 256 fp32 / 128 fp64 columns x 4 rows, up to 8 CTAs per SM
-      return launch_ring<T, 2, 4, 3, 8, 1>(a, out, s);
-    case kShapeQuad:
-      // 512 fp32 / 256 fp64 columns x 15 quads (60 rows), 12-stage ring (192 KB),
-      // 1 CTA per SM
-      return launch_ring<T, 4, kQuadWarps, 12, 1, 4>(a, out, s);
-    case kShapeQuadSmall:  // 256 fp32 / 128 fp64 columns x 4 quads, up to 4 CTAs per SM
-      return launch_ring<T, 2, 4, 6, 4, 4>(a, out, s);
+      return launch_ring<T, 2, 4, 3, 8>(a, out, s);
     default:  // narrow: 512 fp32 / 256 fp64 columns x 16 rows, 2 CTAs per SM
-      return launch_ring<T, 4, 16, 6, 2, 1>(a, out, s);
+      return launch_ring<T, 4, 16, 6, 2>(a, out, s);
   }
 }
 

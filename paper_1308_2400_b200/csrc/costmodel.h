@@ -41,7 +41,7 @@ struct CaseAModel {
   uint64_t rep_sum = 0;     // sum of |rep| over Y
   // B-form launch geometry (the shape the runtime picks for the B part)
   uint32_t b_tile = 1024;       // slab rows per B-form tile (TILE_N)
-  uint32_t b_rows_per_cta = 16; // B-form rows (Z columns) per CTA
+  uint32_t b_warps_per_cta = 16; // B-form rows (consumer warps) per CTA
   uint32_t b_ctas_per_sm = 1;
   double b_step = 32.0;         // cycles per rep step per list entry and tile
   double b_entry = 56.0;        // cycles per list entry and tile (mean rep >= 3)
@@ -65,22 +65,30 @@ struct CaseAModel {
     const double rbar = (double)rep_sum / (double)nnz_y;
     return b_step * (double)rep_sum + (rbar < 3.0 ? b_entry_small : b_entry) * (double)nnz_y;
   }
-  AFMM_HD static double wave_eff(double ctas, double slots) {
-    if (ctas <= 0.0) return 1.0;
-    const double waves = (double)(uint64_t)((ctas + slots - 1.0) / slots);
-    return ctas / (waves * slots);
+  // Busy fraction of the GPU's warp slots for `rows` rows (warps) of `tiles`
+  // column tiles in CTAs of at most cw rows, `per_sm` CTAs per SM: the
+  // launchers trim the rows per CTA (balanced_rows in bform.cu) to the r in
+  // [cw/2, cw] minimising waves x r, i.e. the busiest SM's share of rows.
+  AFMM_HD double wave_eff(uint64_t rows, uint64_t tiles, uint32_t cw, uint32_t per_sm) const {
+    if (rows == 0 || tiles == 0) return 1.0;
+    const uint64_t slots = (uint64_t)per_sm * sms;
+    uint64_t best = 0;
+    for (uint32_t r = cw; r >= 1 && 2 * r >= cw; --r) {
+      const uint64_t ctas = (rows + r - 1) / r * tiles;
+      const uint64_t c = (ctas + slots - 1) / slots * r;
+      if (best == 0 || c * 100 < best * 97) best = c;
+    }
+    return (double)rows * (double)tiles / ((double)slots * (double)best);
   }
-  // B part of tiles_b whole tiles, charged its wave quantisation
+  // B part of tiles_b whole tiles (n B-form rows), charged its wave quantisation
   AFMM_HD double cost_b(uint64_t tiles_b) const {
     if (tiles_b == 0) return 0.0;
-    const double ctas = (double)((n + b_rows_per_cta - 1) / b_rows_per_cta) * (double)tiles_b;
-    return (double)tiles_b * per_tile() / wave_eff(ctas, (double)b_ctas_per_sm * sms);
+    return (double)tiles_b * per_tile() / wave_eff(n, tiles_b, b_warps_per_cta, b_ctas_per_sm);
   }
   // A part of m rows holding `bases` nonzero bases in total
   AFMM_HD double cost_a(uint64_t m, double bases) const {
     if (m == 0) return 0.0;
-    const double ctas = (double)((m + a_rows_per_cta - 1) / a_rows_per_cta) * a_tiles();
-    return per_base() * bases / wave_eff(ctas, (double)a_ctas_per_sm * sms);
+    return per_base() * bases / wave_eff(m, (uint64_t)a_tiles(), a_rows_per_cta, a_ctas_per_sm);
   }
 };
 
@@ -93,14 +101,22 @@ constexpr int kChooseSplit = 2;
 
 // The number m of slab rows to run in the A-form (the m sparsest rows; 0 =
 // pure B-form, rows = pure A-form). pre(m) = total nonzero bases of the m
-// sparsest rows. Splits keep the B part a whole number of tiles.
+// sparsest rows. Splits keep the B part a whole number of tiles. *time (if
+// given) receives the modeled cycles of the choice.
 template <class Pre>
-AFMM_HD uint64_t choose_aform_rows(const CaseAModel& md, uint64_t rows, int variant, Pre pre) {
-  if (variant == kChooseAForm) return rows;
-  if (rows == 0 || md.nnz_y == 0) return 0;
+AFMM_HD uint64_t choose_aform_rows(const CaseAModel& md, uint64_t rows, int variant, Pre pre,
+                                   double* time = nullptr) {
+  if (rows == 0 || md.nnz_y == 0) {
+    if (time) *time = 0.0;
+    return variant == kChooseAForm ? rows : 0;
+  }
   const uint64_t tb = md.b_tile, tiles_all = (rows + tb - 1) / tb;
   const double pure_b = md.cost_b(tiles_all);
   const double pure_a = md.cost_a(rows, pre(rows));
+  if (variant == kChooseAForm) {
+    if (time) *time = pure_a;
+    return rows;
+  }
   double best_split = 0.0;
   uint64_t m_split = 0;
   for (uint64_t j = 1; j * tb < rows; ++j) {
@@ -111,14 +127,21 @@ AFMM_HD uint64_t choose_aform_rows(const CaseAModel& md, uint64_t rows, int vari
       m_split = m;
     }
   }
-  if (variant == kChooseSplit) return m_split;
+  if (variant == kChooseSplit) {
+    if (time) *time = m_split ? best_split : pure_b;
+    return m_split;
+  }
   double best = pure_b;
   uint64_t best_m = 0;
   if (pure_a < 0.85 * pure_b) {
     best = pure_a;
     best_m = rows;
   }
-  if (m_split && best_split < 0.90 * pure_b && best_split < best) best_m = m_split;
+  if (m_split && best_split < 0.90 * pure_b && best_split < best) {
+    best = best_split;
+    best_m = m_split;
+  }
+  if (time) *time = best;
   return best_m;
 }
 

@@ -30,16 +30,11 @@ void launch_rows(const T* x, uint64_t ld, uint32_t n, int which_case, const uint
                  uint32_t r1, int2* lists, uint64_t cap, uint32_t* counts,
                  unsigned long long* work, DevStatus* st, cudaStream_t s,
                  uint32_t* nnz_row = nullptr);
-// Case B quad lists of slab rows [r0, r1) + the slab's OpCounts.
+// Case A rep lists: list j = compacted column j of Y. skip (optional): no-op
+// when *skip == 0.
 template <class T>
-void launch_rows_quad(const T* x, uint64_t ld, uint32_t n, const uint32_t* nnz, uint32_t r0,
-                      uint32_t r1, int4* lists, uint64_t cap, uint32_t* counts, DevStatus* st,
-                      cudaStream_t s);
-// Case A rep lists: list j = compacted column j of Y (quads: columns 4q..4q+3).
-// skip (optional): no-op when *skip == 0.
-template <class T>
-void launch_transpose_compact(const T* y, uint64_t ld, uint32_t n, void* lists, uint64_t cap,
-                              uint32_t* counts, bool quads, DevStatus* st, const uint32_t* skip,
+void launch_transpose_compact(const T* y, uint64_t ld, uint32_t n, int2* lists, uint64_t cap,
+                              uint32_t* counts, DevStatus* st, const uint32_t* skip,
                               cudaStream_t s);
 // out[oc][r] = in[ir][c] with optional row maps ir = in_rows[r], oc = out_rows[c];
 // with a status, nothing is written after a failed validation. plan/dyn: the
@@ -92,29 +87,22 @@ cudaError_t launch_aform(const CUtensorMap* cmap, const typename AEntry<T>::type
 int bform_kb();
 int bform_box_bytes();
 
-// k_bform tile shapes. R = 1 (one B-form row per warp, int2 {k, rep} lists):
-// narrow = 512 fp32 / 256 fp64 columns, 2 CTAs per SM; wide = 1024 / 512
-// columns, 1 CTA per SM; small = 256 / 128 columns x 4 rows for problems too
-// small to fill the GPU with the larger tiles. R = 4 (a row quad per warp,
-// int4 {k, reps} lists): quad = 512 / 256 columns x 16 quads, 1 CTA per SM;
-// quad_small = 256 / 128 columns x 4 quads, 4 CTAs per SM.
+// k_bform tile shapes: narrow = 512 fp32 / 256 fp64 columns, 2 CTAs per SM;
+// wide = 1024 / 512 columns, 1 CTA per SM; small = 256 / 128 columns x 4 rows
+// for problems too small to fill the GPU with the larger tiles.
 constexpr int kShapeNarrow = 0;
 constexpr int kShapeWide = 1;
 constexpr int kShapeSmall = 2;
-constexpr int kShapeQuad = 3;
-constexpr int kShapeQuadSmall = 4;
 constexpr int kWideRows = 16;      // rows per wide CTA (16 consumer warps + 1 TMA warp)
 constexpr int kWideCtasPerSm = 1;  // wide CTAs resident per SM (6-stage ring, 192 KB smem)
-constexpr int kQuadWarps = 15;     // consumer warps per quad CTA (60 rows; 16 warps: 128 registers)
-inline bool shape_is_quad(int shape) { return shape == kShapeQuad || shape == kShapeQuadSmall; }
 
 struct BformLaunch {
   int shape = kShapeNarrow;
   const CUtensorMap* tmap = nullptr;  // base matrix, box bform_kb() x bform_box_bytes()
-  const void* lists = nullptr;  // R = 1: int2 per row; R = 4: int4 per row quad
+  const int2* lists = nullptr;  // {k, rep} per row
   uint64_t cap = 0;             // entries per list
   const uint32_t* counts = nullptr;  // entries of each list
-  uint32_t nrows = 0;           // B-form rows (R = 4: rows, not quads)
+  uint32_t nrows = 0;           // B-form rows
   int32_t col0 = 0, ncols = 0;  // base columns [col0, col0 + ncols)
   const uint32_t* dyn_ncols = nullptr;  // optional: ncols decided on the device
   uint32_t nk = 0;              // k range

@@ -2,8 +2,8 @@
 //
 // Replaces the inline zero tests and the up-front validation of the
 // reference kernels (/root/reference/proj/include/afmm/kernels.hpp:25-43,
-// :121-130, :150-159) with streaming passes (one warp per matrix row or row
-// quad, 128-bit loads, one read of each operand):
+// :121-130, :150-159) with streaming passes (one warp per matrix row,
+// 128-bit loads, one read of each operand):
 //
 //   k_scan_stats   rows of both operands: finite check (matrix.hpp:31-35), rep
 //                  validation of the rep operand (kernels.hpp:25-43; first
@@ -15,12 +15,9 @@
 //                  (Case B, one row per list) the warp-scan stream compaction of
 //                  the row's nonzero reps into an ordered (k, rep) list: the
 //                  zero-skip of kernels.hpp:151-153 done once instead of per (i,k,j)
-//   k_rows_quad    Case B, lists of row QUADS: per k where any of four
-//                  consecutive rows has a nonzero rep, one entry holding the four
-//                  reps (k_bform R = 4)
-//   k_transpose_compact  (Case A) the same compactions for the columns of Y,
+//   k_transpose_compact  (Case A) the same compaction for the columns of Y,
 //                  through 32x33 smem tiles (the rep list of B-form row j is
-//                  column j of Y; a quad is four adjacent columns)
+//                  column j of Y)
 //   k_counts_f16, k_choose, k_acompact  the A-form inputs and the device-side
 //                  A-form / B-form choice (costmodel.h)
 //
@@ -28,8 +25,6 @@
 // (fast-mode split-k combine). All are HBM-bound; none does FP arithmetic on
 // the product.
 #include <cuda_fp16.h>
-
-#include <type_traits>
 
 #include "common.cuh"
 #include "costmodel.h"
@@ -40,9 +35,8 @@ namespace afmm_dev {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-// Largest |rep| one list entry holds: int32 reps (R = 1 lists), int16 reps (quads).
-constexpr unsigned long long kMaxRep1 = 0x7fffffffull;
-constexpr unsigned long long kMaxRep4 = 0x7fffull;
+// Largest |rep| one list entry {k, int32 rep} holds.
+constexpr unsigned long long kMaxRep = 0x7fffffffull;
 
 __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
 #pragma unroll
@@ -113,10 +107,6 @@ __device__ __forceinline__ long long part_of(long long r, uint32_t c, unsigned l
   if (a <= done) return 0;
   const unsigned long long p = a - done < M ? a - done : M;
   return r < 0 ? -(long long)p : (long long)p;
-}
-
-__device__ __forceinline__ uint32_t pack2(long long lo, long long hi) {
-  return ((uint32_t)(uint16_t)(int16_t)lo) | ((uint32_t)(uint16_t)(int16_t)hi << 16);
 }
 
 // Record the length of a list that does not fit (the runtime re-runs with it).
@@ -231,7 +221,7 @@ __global__ void k_rows(const T* __restrict__ x, uint64_t ld, uint32_t n, int whi
         uint32_t ne[4], mine = 0;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          ne[e] = entries_for(abs_ll(rep[e]), kMaxRep1);
+          ne[e] = entries_for(abs_ll(rep[e]), kMaxRep);
           mine += ne[e];
         }
         uint32_t total;
@@ -243,7 +233,7 @@ __global__ void k_rows(const T* __restrict__ x, uint64_t ld, uint32_t n, int whi
             ++pos;
           } else {
             for (uint32_t c = 0; c < ne[e]; ++c, ++pos)
-              if (pos < cap) out[pos] = make_int2((int)(j0 + e), (int)part_of(rep[e], c, kMaxRep1));
+              if (pos < cap) out[pos] = make_int2((int)(j0 + e), (int)part_of(rep[e], c, kMaxRep));
           }
         }
         base += total;
@@ -267,96 +257,20 @@ __global__ void k_rows(const T* __restrict__ x, uint64_t ld, uint32_t n, int whi
   }
 }
 
-// Case B quad lists: slab rows r0 + 4q .. r0 + 4q + 3 (rows >= r1 are empty).
-// One entry per k where any of the four reps is nonzero: {k, rep0|rep1<<16,
-// rep2|rep3<<16, 0}; a |rep| beyond int16 is continued in further entries at
-// the same k. Also adds the slab's OpCounts.
-template <class T>
-__global__ void k_rows_quad(const T* __restrict__ x, uint64_t ld, uint32_t n, int vec,
-                            const uint32_t* __restrict__ nnz, uint32_t r0, uint32_t r1,
-                            int4* __restrict__ lists, uint64_t cap, uint32_t* __restrict__ counts,
-                            DevStatus* st) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  const uint32_t rows = r1 - r0, nq = (rows + 3) / 4;
-  for (uint64_t q = warp; q < nq; q += nwarps) {
-    int4* out = lists + q * cap;
-    unsigned long long w = 0, z = 0, base = 0;
-    for (uint32_t c0 = 0; c0 < n; c0 += 128) {
-      const uint32_t j0 = c0 + 4 * lane;
-      long long rep[4][4];  // [row of the quad][element]
-#pragma unroll
-      for (int qr = 0; qr < 4; ++qr) {
-        const uint32_t r = 4 * (uint32_t)q + qr;
-        T v[4] = {T(0), T(0), T(0), T(0)};
-        if (r < rows) load4(x + (uint64_t)(r0 + r) * ld, j0, n, vec != 0, v);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          rep[qr][e] = j0 + e < n ? rep_of(v[e]) : 0;
-          if (rep[qr][e] != 0) {
-            const unsigned long long nb = nnz[j0 + e];
-            w += abs_ll(rep[qr][e]) * nb;
-            z += (unsigned long long)n - nb;
-          }
-        }
-      }
-      uint32_t ne[4], mine = 0;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        ne[e] = 0;
-#pragma unroll
-        for (int qr = 0; qr < 4; ++qr) ne[e] = max(ne[e], entries_for(abs_ll(rep[qr][e]), kMaxRep4));
-        mine += ne[e];
-      }
-      uint32_t total;
-      unsigned long long pos = base + warp_excl_scan(mine, lane, &total);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        if (ne[e] == 1) {
-          if (pos < cap)
-            out[pos] = make_int4((int)(j0 + e), (int)pack2(rep[0][e], rep[1][e]),
-                                 (int)pack2(rep[2][e], rep[3][e]), 0);
-          ++pos;
-        } else {
-          for (uint32_t c = 0; c < ne[e]; ++c, ++pos)
-            if (pos < cap)
-              out[pos] = make_int4(
-                  (int)(j0 + e),
-                  (int)pack2(part_of(rep[0][e], c, kMaxRep4), part_of(rep[1][e], c, kMaxRep4)),
-                  (int)pack2(part_of(rep[2][e], c, kMaxRep4), part_of(rep[3][e], c, kMaxRep4)),
-                  0);
-        }
-      }
-      base += total;
-    }
-    w = warp_sum_u64(w);
-    z = warp_sum_u64(z);
-    if (lane == 0) {
-      if (w) atomicAdd(&st->additions, w);
-      if (z) atomicAdd(&st->zero_skips, z);
-      counts[q] = (uint32_t)(base < 0xffffffffull ? base : 0xffffffffull);
-      note_list(st, base, cap);
-    }
-  }
-}
-
 // Case A rep lists: B-form row j = column j of Y. A block owns 32 columns and
-// walks k in 32-row tiles through smem. R = 1: warp w compacts columns
-// 4w..4w+3 one list each; R = 4: warp w compacts the quad of columns 4w..4w+3
-// into one list. skip (optional): nothing to do when *skip == 0 (the
-// device-side Case A choice gave every row to the A-form).
-template <class T, int R>
+// walks k in 32-row tiles through smem; warp w compacts columns 4w..4w+3.
+// skip (optional): nothing to do when *skip == 0 (the device-side Case A
+// choice gave every row to the A-form).
+template <class T>
 __global__ void __launch_bounds__(256)
-    k_transpose_compact(const T* __restrict__ y, uint64_t ld, uint32_t n,
-                        typename std::conditional<R == 1, int2, int4>::type* __restrict__ lists,
+    k_transpose_compact(const T* __restrict__ y, uint64_t ld, uint32_t n, int2* __restrict__ lists,
                         uint64_t cap, uint32_t* __restrict__ counts, DevStatus* st,
                         const uint32_t* __restrict__ skip) {
   if (skip && *skip == 0) return;
   __shared__ T tile[32][33];
   const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const uint32_t j0 = blockIdx.x * 32;
-  unsigned long long base[R == 1 ? 4 : 1] = {};
+  unsigned long long base[4] = {0, 0, 0, 0};
   // the next 32-row tile is loaded into registers while this one is compacted
   // (the block walks k serially, so unhidden load latency is its whole cost
   // at small n)
@@ -375,58 +289,30 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     if (k0 + 32 < n) fetch(k0 + 32);
     const uint32_t k = k0 + tx;
-    if constexpr (R == 1) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t j = j0 + ty * 4 + q;
-        const long long rep = k < n ? rep_of(tile[tx][ty * 4 + q]) : 0;  // Y[k, j]
-        const uint32_t ne = entries_for(abs_ll(rep), kMaxRep1);
-        uint32_t total;
-        unsigned long long pos = base[q] + warp_excl_scan(ne, tx, &total);
-        if (j < n)
-          for (uint32_t c = 0; c < ne; ++c, ++pos)
-            if (pos < cap)
-              lists[(uint64_t)j * cap + pos] =
-                  make_int2((int)k, (int)(ne == 1 ? rep : part_of(rep, c, kMaxRep1)));
-        base[q] += total;
-      }
-    } else {
-      long long rep[4];
-      uint32_t ne = 0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        rep[q] = (k < n && j0 + ty * 4 + q < n) ? rep_of(tile[tx][ty * 4 + q]) : 0;
-        ne = max(ne, entries_for(abs_ll(rep[q]), kMaxRep4));
-      }
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t j = j0 + ty * 4 + q;
+      const long long rep = k < n ? rep_of(tile[tx][ty * 4 + q]) : 0;  // Y[k, j]
+      const uint32_t ne = entries_for(abs_ll(rep), kMaxRep);
       uint32_t total;
-      unsigned long long pos = base[0] + warp_excl_scan(ne, tx, &total);
-      const uint64_t quad = (j0 >> 2) + ty;
-      if (j0 + ty * 4 < n)
+      unsigned long long pos = base[q] + warp_excl_scan(ne, tx, &total);
+      if (j < n)
         for (uint32_t c = 0; c < ne; ++c, ++pos)
           if (pos < cap)
-            lists[quad * cap + pos] =
-                ne == 1 ? make_int4((int)k, (int)pack2(rep[0], rep[1]), (int)pack2(rep[2], rep[3]), 0)
-                        : make_int4((int)k,
-                                    (int)pack2(part_of(rep[0], c, kMaxRep4), part_of(rep[1], c, kMaxRep4)),
-                                    (int)pack2(part_of(rep[2], c, kMaxRep4), part_of(rep[3], c, kMaxRep4)),
-                                    0);
-      base[0] += total;
+            lists[(uint64_t)j * cap + pos] =
+                make_int2((int)k, (int)(ne == 1 ? rep : part_of(rep, c, kMaxRep)));
+      base[q] += total;
     }
     __syncthreads();
   }
   if (tx == 0) {
-    if constexpr (R == 1) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t j = j0 + ty * 4 + q;
-        if (j < n) {
-          counts[j] = (uint32_t)(base[q] < 0xffffffffull ? base[q] : 0xffffffffull);
-          note_list(st, base[q], cap);
-        }
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t j = j0 + ty * 4 + q;
+      if (j < n) {
+        counts[j] = (uint32_t)(base[q] < 0xffffffffull ? base[q] : 0xffffffffull);
+        note_list(st, base[q], cap);
       }
-    } else if (j0 + ty * 4 < n) {
-      counts[(j0 >> 2) + ty] = (uint32_t)(base[0] < 0xffffffffull ? base[0] : 0xffffffffull);
-      note_list(st, base[0], cap);
     }
   }
 }
@@ -787,16 +673,6 @@ void launch_rows(const T* x, uint64_t ld, uint32_t n, int which_case, const uint
 }
 
 template <class T>
-void launch_rows_quad(const T* x, uint64_t ld, uint32_t n, const uint32_t* nnz, uint32_t r0,
-                      uint32_t r1, int4* lists, uint64_t cap, uint32_t* counts, DevStatus* st,
-                      cudaStream_t s) {
-  if (r1 <= r0) return;
-  k_rows_quad<T><<<grid_for_warps((r1 - r0 + 3) / 4, 8), 256, 0, s>>>(
-      x, ld, n, vec_ok(x, ld), nnz, r0, r1, lists, cap, counts, st);
-  note_launch();
-}
-
-template <class T>
 void launch_counts_f16(const T* y, uint64_t ld, uint32_t n, uint32_t tile_cols, __half* cnt,
                        uint64_t ldc, uint16_t* rmax, unsigned long long* fstats, cudaStream_t s) {
   const uint32_t ntiles = (n + tile_cols - 1) / tile_cols;
@@ -827,15 +703,10 @@ void launch_acompact(const T* x, uint64_t ld, uint32_t n, uint32_t r0, uint32_t 
 }
 
 template <class T>
-void launch_transpose_compact(const T* y, uint64_t ld, uint32_t n, void* lists, uint64_t cap,
-                              uint32_t* counts, bool quads, DevStatus* st, const uint32_t* skip,
+void launch_transpose_compact(const T* y, uint64_t ld, uint32_t n, int2* lists, uint64_t cap,
+                              uint32_t* counts, DevStatus* st, const uint32_t* skip,
                               cudaStream_t s) {
-  if (quads)
-    k_transpose_compact<T, 4><<<(n + 31) / 32, 256, 0, s>>>(y, ld, n, static_cast<int4*>(lists),
-                                                            cap, counts, st, skip);
-  else
-    k_transpose_compact<T, 1><<<(n + 31) / 32, 256, 0, s>>>(y, ld, n, static_cast<int2*>(lists),
-                                                            cap, counts, st, skip);
+  k_transpose_compact<T><<<(n + 31) / 32, 256, 0, s>>>(y, ld, n, lists, cap, counts, st, skip);
   note_launch();
 }
 
@@ -871,17 +742,14 @@ void launch_reduce_slices(const T* part, uint64_t stride, uint64_t ld_part, uint
                                const unsigned long long*, uint32_t, uint32_t, uint32_t,        \
                                uint32_t, int2*, uint64_t, uint32_t*, unsigned long long*,      \
                                DevStatus*, cudaStream_t, uint32_t*);                           \
-  template void launch_rows_quad<T>(const T*, uint64_t, uint32_t, const uint32_t*, uint32_t,   \
-                                    uint32_t, int4*, uint64_t, uint32_t*, DevStatus*,          \
-                                    cudaStream_t);                                             \
   template void launch_counts_f16<T>(const T*, uint64_t, uint32_t, uint32_t, __half*, uint64_t, \
                                      uint16_t*, unsigned long long*, cudaStream_t);            \
   template void launch_acompact<T>(const T*, uint64_t, uint32_t, uint32_t, uint32_t,           \
                                    const uint32_t*, const uint32_t*,                           \
                                    typename AEntry<T>::type*, uint64_t, uint32_t*,             \
                                    cudaStream_t);                                              \
-  template void launch_transpose_compact<T>(const T*, uint64_t, uint32_t, void*, uint64_t,     \
-                                            uint32_t*, bool, DevStatus*, const uint32_t*,      \
+  template void launch_transpose_compact<T>(const T*, uint64_t, uint32_t, int2*, uint64_t,     \
+                                            uint32_t*, DevStatus*, const uint32_t*,            \
                                             cudaStream_t);                                     \
   template void launch_transpose<T>(const T*, uint64_t, uint32_t, uint32_t, T*, uint64_t,      \
                                     cudaStream_t, const uint32_t*, const uint32_t*,            \

@@ -43,13 +43,11 @@ constexpr uint64_t kNone = ~0ull;
 // shape from the problem size, the Case A form from the device-side model).
 enum Variant {
   kAuto = -1,
-  kNarrow = 0,     // R = 1, 512 fp32 / 256 fp64 columns, 2 CTAs per SM
-  kWide = 1,       // R = 1, 1024 / 512 columns, 1 CTA per SM
-  kSmall = 2,      // R = 1, 256 / 128 columns x 4 rows
-  kQuad = 3,       // R = 4 (row quads), 512 / 256 columns x 16 quads
-  kQuadSmall = 4,  // R = 4, 256 / 128 columns x 4 quads
-  kAForm = 8,      // Case A: every row in the A-form
-  kHybrid = 9,     // Case A: the best A-form / B-form row split, forced
+  kNarrow = 0,  // 512 fp32 / 256 fp64 columns, 2 CTAs per SM
+  kWide = 1,    // 1024 / 512 columns, 1 CTA per SM
+  kSmall = 2,   // 256 / 128 columns x 4 rows
+  kAForm = 8,   // Case A: every row in the A-form
+  kHybrid = 9,  // Case A: the best A-form / B-form row split, forced
 };
 
 int variant_from_env() {
@@ -58,8 +56,8 @@ int variant_from_env() {
   static const struct {
     const char* name;
     int variant;
-  } names[] = {{"ring", kNarrow}, {"narrow", kNarrow}, {"wide", kWide},     {"small", kSmall},
-               {"quad", kQuad},   {"quadsmall", kQuadSmall}, {"aform", kAForm}, {"hybrid", kHybrid}};
+  } names[] = {{"ring", kNarrow}, {"narrow", kNarrow}, {"wide", kWide},
+               {"small", kSmall}, {"aform", kAForm},    {"hybrid", kHybrid}};
   for (const auto& e : names)
     if (std::strcmp(v, e.name) == 0) return e.variant;
   return kAuto;
@@ -404,8 +402,6 @@ int pick_shape(int variant, uint64_t nrows, uint64_t ncols, size_t elem, int sms
     case kNarrow: return afmm_dev::kShapeNarrow;
     case kWide: return afmm_dev::kShapeWide;
     case kSmall: return afmm_dev::kShapeSmall;
-    case kQuad: return afmm_dev::kShapeQuad;
-    case kQuadSmall: return afmm_dev::kShapeQuadSmall;
     default: break;
   }
   const uint64_t cbytes = ncols * elem;
@@ -421,17 +417,15 @@ int pick_shape(int variant, uint64_t nrows, uint64_t ncols, size_t elem, int sms
   return afmm_dev::kShapeNarrow;
 }
 
-// Geometry of a B-form shape: (rows per list, columns per tile, rows per CTA, CTAs per SM)
+// Geometry of a B-form shape: (columns per tile in bytes, rows per CTA, CTAs per SM)
 struct ShapeGeo {
-  uint32_t r, tile_bytes, rows_per_cta, ctas_per_sm;
+  uint32_t tile_bytes, rows_per_cta, ctas_per_sm;
 };
 ShapeGeo shape_geo(int shape) {
   switch (shape) {
-    case afmm_dev::kShapeWide: return {1, 4096, afmm_dev::kWideRows, afmm_dev::kWideCtasPerSm};
-    case afmm_dev::kShapeSmall: return {1, 1024, 4, 8};
-    case afmm_dev::kShapeQuad: return {4, 2048, 4 * afmm_dev::kQuadWarps, 1};
-    case afmm_dev::kShapeQuadSmall: return {4, 1024, 16, 4};
-    default: return {1, 2048, 16, 2};
+    case afmm_dev::kShapeWide: return {4096, afmm_dev::kWideRows, afmm_dev::kWideCtasPerSm};
+    case afmm_dev::kShapeSmall: return {1024, 4, 8};
+    default: return {2048, 16, 2};
   }
 }
 
@@ -444,14 +438,14 @@ afmm_dev::CaseAModel case_a_model(size_t elem, uint64_t n, int sms, int shape) {
   md.n = n;
   md.sms = (uint32_t)sms;
   md.b_tile = (uint32_t)(g.tile_bytes / elem);
-  md.b_rows_per_cta = g.rows_per_cta;
+  md.b_warps_per_cta = g.rows_per_cta;
   md.b_ctas_per_sm = g.ctas_per_sm;
   // cycles per rep step per list entry and B tile: 2 pipe cycles per FADD2 /
   // DADD warp instruction, tile_bytes / 512 instructions per rep step and row
   md.b_step = 2.0 * (double)(g.tile_bytes / 512);
   const double scale = (double)g.tile_bytes / 4096.0;  // fitted on the wide shape
-  md.b_entry = 56.0 * (g.r == 4 ? 0.5 : 1.0) * (scale < 1.0 ? 1.0 : scale);
-  md.b_entry_small = 100.0 * (g.r == 4 ? 0.5 : 1.0) * (scale < 1.0 ? 1.0 : scale);
+  md.b_entry = 56.0 * (scale < 1.0 ? 1.0 : scale);
+  md.b_entry_small = 100.0 * (scale < 1.0 ? 1.0 : scale);
   md.a_tile = afmm_dev::aform_tile_cols<float>() * 4 / (uint32_t)elem;
   md.a_rows_per_cta = afmm_dev::kAformRows;
   md.a_ctas_per_sm = afmm_dev::kAformCtasPerSm;
@@ -469,9 +463,8 @@ afmm_status launch_compute(afmm_context* c, const Call& call, int shape, const T
                            DevStatus* st, afmm_error* err) {
   const ShapeGeo g = shape_geo(shape);
   const uint64_t cbytes = (uint64_t)ncols * sizeof(T);
-  const uint64_t groups = (nrows + g.r - 1) / g.r;
-  const uint64_t per_cta = g.rows_per_cta / g.r;
-  const uint64_t ctas = (groups + per_cta - 1) / per_cta * ((cbytes + g.tile_bytes - 1) / g.tile_bytes);
+  const uint64_t ctas = (nrows + g.rows_per_cta - 1) / g.rows_per_cta *
+                        ((cbytes + g.tile_bytes - 1) / g.tile_bytes);
   const uint64_t slots = (uint64_t)sm_count(c->device) * g.ctas_per_sm;
   // Fast mode (reassociated): split the k range into slices when the tile grid
   // alone cannot fill 2 waves, then add the slice partials in a fixed order.
@@ -493,7 +486,7 @@ afmm_status launch_compute(afmm_context* c, const Call& call, int shape, const T
   afmm_dev::BformLaunch a;
   a.shape = shape;
   a.tmap = &tmap;
-  a.lists = c->lists.p;
+  a.lists = c->lists.as<int2>();
   a.cap = std::max<uint64_t>(call.n, c->cap_need);
   a.counts = c->counts.as<uint32_t>();
   a.nrows = nrows;
@@ -560,17 +553,11 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
   if (call.which == AFMM_CASE_B) {
     // rep = X[i,k] (lhs), bases = Y[k,:] (rhs): B-form directly.
     const int shape = pick_shape(c->variant, rows, n, sizeof(T), sms);
-    const bool quads = afmm_dev::shape_is_quad(shape);
-    const uint64_t groups = std::max<uint64_t>(quads ? (rows + 3) / 4 : rows, 1);
-    CK(c->lists.ensure(groups * cap * (quads ? sizeof(int4) : sizeof(int2))), "workspace");
-    CK(c->counts.ensure(groups * 4), "workspace");
-    if (quads)
-      afmm_dev::launch_rows_quad<T>(lhs, ld, n32, nnz, (uint32_t)r0, (uint32_t)r1,
-                                    c->lists.as<int4>(), cap, c->counts.as<uint32_t>(), st, s);
-    else
-      afmm_dev::launch_rows<T>(lhs, ld, n32, 1, nnz, nullptr, (uint32_t)r0, (uint32_t)r1,
-                               (uint32_t)r0, (uint32_t)r1, c->lists.as<int2>(), cap,
-                               c->counts.as<uint32_t>(), nullptr, st, s);
+    CK(c->lists.ensure(std::max<uint64_t>(rows, 1) * cap * sizeof(int2)), "workspace");
+    CK(c->counts.ensure(std::max<uint64_t>(rows, 1) * 4), "workspace");
+    afmm_dev::launch_rows<T>(lhs, ld, n32, 1, nnz, nullptr, (uint32_t)r0, (uint32_t)r1,
+                             (uint32_t)r0, (uint32_t)r1, c->lists.as<int2>(), cap,
+                             c->counts.as<uint32_t>(), nullptr, st, s);
     const T* base = rhs;
     uint64_t ldb = ld;
     if ((ld * sizeof(T)) % 16 != 0 || reinterpret_cast<uintptr_t>(rhs) % 16 != 0) {
@@ -603,8 +590,6 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
     // B part: B-form rows = Z columns j (rep list = column j of Y), B-form
     // columns = the slab's B rows (bases X[i,k], gathered through ridx)
     const int shape = pick_shape(c->variant, n, std::max<uint64_t>(rows, 1), sizeof(T), sms);
-    const bool quads = afmm_dev::shape_is_quad(shape);
-    const uint64_t groups = quads ? (n + 3) / 4 : n;
     if (choose) CK(c->acounts.ensure(rows * 4), "workspace");
     afmm_dev::launch_rows<T>(lhs, ld, n32, 0, nullptr, rsum, (uint32_t)r0, (uint32_t)r1,
                              (uint32_t)r0, (uint32_t)r1, nullptr, 0, nullptr, nullptr, st, s,
@@ -638,11 +623,11 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
     const uint64_t lds = round_up(std::max<uint64_t>(rows, 1), 32);
     CK(c->xt.ensure(n * lds * sizeof(T)), "workspace");
     CK(c->zt.ensure(n * lds * sizeof(T)), "workspace");
-    CK(c->lists.ensure(groups * cap * (quads ? sizeof(int4) : sizeof(int2))), "workspace");
-    CK(c->counts.ensure(groups * 4), "workspace");
+    CK(c->lists.ensure(n * cap * sizeof(int2)), "workspace");
+    CK(c->counts.ensure(n * 4), "workspace");
     if (rows > 0) {
-      afmm_dev::launch_transpose_compact<T>(rhs, ld, n32, c->lists.p, cap,
-                                            c->counts.as<uint32_t>(), quads, st,
+      afmm_dev::launch_transpose_compact<T>(rhs, ld, n32, c->lists.as<int2>(), cap,
+                                            c->counts.as<uint32_t>(), st,
                                             plan ? plan + 1 : nullptr, s);
       afmm_dev::launch_transpose<T>(lhs + r0 * ld, ld, (uint32_t)rows, n32, c->xt.as<T>(), lds, s,
                                     ridx, nullptr, nullptr, plan, plan ? 1 : 0);
@@ -1063,6 +1048,114 @@ void row_costs(int which, size_t elem, uint64_t n, int sms, const uint64_t* work
   }
 }
 
+// Modeled kernel time of Case A slabs (rows [r0, r1) of a product whose
+// rows have nnz[i] nonzero bases): the device-side choice (k_choose) run on
+// the host -- pure B-form, pure A-form or the best split, whichever the model
+// picks -- with the slab's own wave quantisation.
+class SlabModel {
+ public:
+  SlabModel(const afmm_dev::CaseAModel& md, const uint32_t* nnz, bool a_ok)
+      : md_(md), nnz_(nnz), a_ok_(a_ok), cnt_(md.n + 2), cum_c_(md.n + 3), cum_s_(md.n + 3) {}
+  double time(uint64_t r0, uint64_t r1) {
+    const uint64_t rows = r1 > r0 ? r1 - r0 : 0, n = md_.n;
+    if (rows == 0) return 0.0;
+    if (!a_ok_) return md_.cost_b((rows + md_.b_tile - 1) / md_.b_tile);
+    std::fill(cnt_.begin(), cnt_.end(), 0u);
+    for (uint64_t i = r0; i < r1; ++i) ++cnt_[std::min<uint64_t>(nnz_[i], n)];
+    cum_c_[0] = 0;
+    cum_s_[0] = 0.0;
+    for (uint64_t v = 0; v <= n + 1; ++v) {
+      cum_c_[v + 1] = cum_c_[v] + cnt_[v];
+      cum_s_[v + 1] = cum_s_[v] + (double)v * cnt_[v];
+    }
+    auto pre = [&](uint64_t m) {
+      // largest v with cum_c[v] <= m: the m sparsest rows take every row of
+      // value < v and (m - cum_c[v]) rows of value v
+      const uint64_t v =
+          (uint64_t)(std::upper_bound(cum_c_.begin(), cum_c_.begin() + n + 2, m) - cum_c_.begin()) - 1;
+      return cum_s_[v] + (double)v * (double)(m - cum_c_[v]);
+    };
+    double t = 0.0;
+    afmm_dev::choose_aform_rows(md_, rows, afmm_dev::kChooseAuto, pre, &t);
+    return t;
+  }
+
+ private:
+  const afmm_dev::CaseAModel& md_;
+  const uint32_t* nnz_;
+  bool a_ok_;
+  std::vector<uint32_t> cnt_;
+  std::vector<uint64_t> cum_c_;
+  std::vector<double> cum_s_;
+};
+
+// Case A row cuts by modeled slab time: start from the cut of the additive
+// per-row costs (row_costs), then move each boundary between neighbours to
+// balance their modeled times (a few sweeps of bisection; the model's
+// tile and wave quantisation make the slab time non-additive).
+void partition_case_a(const afmm_dev::CaseAModel& md, const uint32_t* nnz, bool a_ok,
+                      const uint64_t* add_cost, uint32_t parts, uint64_t* cuts, double* times) {
+  const uint64_t n = md.n;
+  afmm_partition_rows(add_cost, n, parts, cuts);
+  SlabModel sm(md, nnz, a_ok);
+  std::vector<double> t(parts);
+  for (uint32_t p = 0; p < parts; ++p) t[p] = sm.time(cuts[p], cuts[p + 1]);
+  for (int sweep = 0; sweep < 8 && parts > 1; ++sweep) {
+    bool moved = false;
+    for (uint32_t p = 0; p + 1 < parts; ++p) {
+      // boundary b = cuts[p + 1] in [cuts[p], cuts[p + 2]]: find the b where
+      // time(left) crosses time(right) (left grows, right shrinks with b)
+      uint64_t lo = cuts[p], hi = cuts[p + 2];
+      const double before = std::max(t[p], t[p + 1]);
+      while (hi - lo > 1) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if (sm.time(cuts[p], mid) <= sm.time(mid, cuts[p + 2])) lo = mid;
+        else hi = mid;
+      }
+      // accept a lower pair maximum, or the same maximum with the pair closer
+      // together (a B-form slab's time is flat within a tile: its neighbour
+      // can take rows up to that level at no cost)
+      uint64_t best_b = cuts[p + 1];
+      double best = before, gap = std::fabs(t[p] - t[p + 1]);
+      for (uint64_t b : {lo, hi}) {
+        const double tl = sm.time(cuts[p], b), tr = sm.time(b, cuts[p + 2]);
+        const double mx = std::max(tl, tr), g = std::fabs(tl - tr);
+        if (mx < best * (1.0 - 1e-9) || (mx <= best * (1.0 + 1e-12) && g < gap * (1.0 - 1e-9))) {
+          best = mx;
+          gap = g;
+          best_b = b;
+        }
+      }
+      if (best_b != cuts[p + 1]) {
+        cuts[p + 1] = best_b;
+        t[p] = sm.time(cuts[p], best_b);
+        t[p + 1] = sm.time(best_b, cuts[p + 2]);
+        moved = true;
+      }
+    }
+    if (!moved) break;
+  }
+  if (times)
+    for (uint32_t p = 0; p < parts; ++p) times[p] = t[p];
+}
+
+// Row cuts for `parts` devices from the full operands' statistics.
+void partition_from_stats(int which, size_t elem, uint64_t n, int sms, const uint64_t* work,
+                          const uint32_t* nnz_row, const unsigned long long* fstats,
+                          uint32_t parts, uint64_t* cuts) {
+  std::vector<uint64_t> cost(n);
+  row_costs(which, elem, n, sms, work, nnz_row, fstats, cost.data());
+  if (which == AFMM_CASE_B) {
+    afmm_partition_rows(cost.data(), n, parts, cuts);
+    return;
+  }
+  afmm_dev::CaseAModel md = case_a_model(elem, n, sms, pick_shape(kAuto, n, n, elem, sms));
+  md.nnz_y = fstats[0];
+  md.trip_sum = fstats[1];
+  md.rep_sum = fstats[3];
+  partition_case_a(md, nnz_row, fstats[2] == 0, cost.data(), parts, cuts, nullptr);
+}
+
 // The reference-facing call sharded over several devices (one process):
 //   A  each shard copies an equal row chunk of X and Y to its device (its own
 //      host thread: pageable copies run in parallel) and validates it,
@@ -1114,7 +1207,7 @@ afmm_status host_product_multi(int which, const T* lhs, const T* rhs, uint64_t n
                                                                             : nullptr;
   std::vector<uint64_t> e(G + 1), cuts(G + 1);
   for (int g = 0; g <= G; ++g) e[g] = n * (uint64_t)g / (uint64_t)G;
-  std::vector<uint64_t> work(n, 0), cost(n, 0);
+  std::vector<uint64_t> work(n, 0);
   std::vector<uint32_t> nnz_row(which == AFMM_CASE_A ? n : 0, 0);
   std::vector<DevStatus> stat(G);
   std::vector<afmm_status> rc(G, AFMM_OK);
@@ -1246,9 +1339,9 @@ afmm_status host_product_multi(int which, const T* lhs, const T* rhs, uint64_t n
         if (opt->partition == AFMM_PARTITION_ROWS) {
           cuts = e;
         } else {
-          row_costs(which, sizeof(T), n, sms, work.data(),
-                    which == AFMM_CASE_A ? nnz_row.data() : nullptr, fstats, cost.data());
-          afmm_partition_rows(cost.data(), n, (uint32_t)G, cuts.data());
+          partition_from_stats(which, sizeof(T), n, sms, work.data(),
+                               which == AFMM_CASE_A ? nnz_row.data() : nullptr, fstats,
+                               (uint32_t)G, cuts.data());
         }
       }
     }
@@ -1617,12 +1710,16 @@ afmm_status row_stats(afmm_context* c, int which, const T* lhs, const T* rhs, ui
   return AFMM_OK;
 }
 
+// What a row query returns: W_i, the per-row cost, or the row cuts.
+enum RowQuery { kQueryWork, kQueryCost, kQueryCuts };
+
 afmm_status row_query(afmm_context* c, int32_t which, int32_t dtype, const void* lhs,
-                      const void* rhs, uint64_t n, uint64_t ld, uint64_t* out, bool cost,
-                      afmm_error* err) {
+                      const void* rhs, uint64_t n, uint64_t ld, uint64_t* out, RowQuery q,
+                      uint32_t parts, afmm_error* err) {
   clear_error(err);
   if (!c || !out || (dtype != AFMM_F64 && dtype != AFMM_F32) ||
-      (which != AFMM_CASE_A && which != AFMM_CASE_B) || !lhs || !rhs)
+      (which != AFMM_CASE_A && which != AFMM_CASE_B) || !lhs || !rhs ||
+      (q == kQueryCuts && parts == 0))
     return AFMM_ERR_INVALID_ARGUMENT;
   afmm_status st = check_dims(which, n, n, err);
   if (st != AFMM_OK) return st;
@@ -1630,22 +1727,27 @@ afmm_status row_query(afmm_context* c, int32_t which, int32_t dtype, const void*
   return guarded([&]() -> afmm_status {
     std::lock_guard<std::mutex> g(c->mu);
     CK(cudaSetDevice(c->device), "afmm: cudaSetDevice");
-    const bool case_a_cost = cost && which == AFMM_CASE_A;
+    const bool case_a_model = q != kQueryWork && which == AFMM_CASE_A;
     std::vector<uint32_t> nnz;
     unsigned long long fstats[4] = {0, 0, 0, 0};
-    std::vector<uint64_t> work(cost ? n : 0);
-    uint64_t* w = cost ? work.data() : out;
+    std::vector<uint64_t> work(q == kQueryWork ? 0 : n);
+    uint64_t* w = q == kQueryWork ? out : work.data();
     afmm_status r =
         dtype == AFMM_F64
             ? row_stats<double>(c, which, static_cast<const double*>(lhs),
                                 static_cast<const double*>(rhs), n, ld, w,
-                                case_a_cost ? &nnz : nullptr, fstats, err)
+                                case_a_model ? &nnz : nullptr, fstats, err)
             : row_stats<float>(c, which, static_cast<const float*>(lhs),
                                static_cast<const float*>(rhs), n, ld, w,
-                               case_a_cost ? &nnz : nullptr, fstats, err);
-    if (r != AFMM_OK || !cost) return r;
-    row_costs(which, dtype == AFMM_F64 ? 8 : 4, n, sm_count(c->device), w,
-              case_a_cost ? nnz.data() : nullptr, fstats, out);
+                               case_a_model ? &nnz : nullptr, fstats, err);
+    if (r != AFMM_OK || q == kQueryWork) return r;
+    const size_t elem = dtype == AFMM_F64 ? 8 : 4;
+    const int sms = sm_count(c->device);
+    if (q == kQueryCost)
+      row_costs(which, elem, n, sms, w, case_a_model ? nnz.data() : nullptr, fstats, out);
+    else
+      partition_from_stats(which, elem, n, sms, w, case_a_model ? nnz.data() : nullptr, fstats,
+                           parts, out);
     return AFMM_OK;
   });
 }
@@ -1657,13 +1759,40 @@ extern "C" {
 afmm_status afmm_row_work_device(afmm_context* c, int32_t which_case, int32_t dtype,
                                  const void* lhs, const void* rhs, uint64_t n, uint64_t ld,
                                  uint64_t* work_host, afmm_error* err) {
-  return row_query(c, which_case, dtype, lhs, rhs, n, ld, work_host, false, err);
+  return row_query(c, which_case, dtype, lhs, rhs, n, ld, work_host, kQueryWork, 0, err);
 }
 
 afmm_status afmm_row_cost_device(afmm_context* c, int32_t which_case, int32_t dtype,
                                  const void* lhs, const void* rhs, uint64_t n, uint64_t ld,
                                  uint64_t* cost, afmm_error* err) {
-  return row_query(c, which_case, dtype, lhs, rhs, n, ld, cost, true, err);
+  return row_query(c, which_case, dtype, lhs, rhs, n, ld, cost, kQueryCost, 0, err);
+}
+
+afmm_status afmm_partition_device(afmm_context* c, int32_t which_case, int32_t dtype,
+                                  const void* lhs, const void* rhs, uint64_t n, uint64_t ld,
+                                  uint32_t parts, uint64_t* cuts, afmm_error* err) {
+  return row_query(c, which_case, dtype, lhs, rhs, n, ld, cuts, kQueryCuts, parts, err);
+}
+
+afmm_status afmm_model_partition_case_a(int32_t dtype, uint64_t n, int32_t sms,
+                                        const uint64_t* stats, const uint32_t* nnz_row,
+                                        uint32_t parts, uint64_t* cuts, double* slab_cycles) {
+  if (!stats || !nnz_row || !cuts || parts == 0 || n == 0 ||
+      (dtype != AFMM_F64 && dtype != AFMM_F32))
+    return AFMM_ERR_INVALID_ARGUMENT;
+  return guarded([&]() -> afmm_status {
+    const size_t elem = dtype == AFMM_F64 ? 8 : 4;
+    const int s = sms > 0 ? sms : 148;
+    const unsigned long long fs[4] = {stats[0], stats[1], stats[2], stats[3]};
+    std::vector<uint64_t> cost(n);
+    row_costs(AFMM_CASE_A, elem, n, s, nullptr, nnz_row, fs, cost.data());
+    afmm_dev::CaseAModel md = case_a_model(elem, n, s, pick_shape(kAuto, n, n, elem, s));
+    md.nnz_y = fs[0];
+    md.trip_sum = fs[1];
+    md.rep_sum = fs[3];
+    partition_case_a(md, nnz_row, fs[2] == 0, cost.data(), parts, cuts, slab_cycles);
+    return AFMM_OK;
+  });
 }
 
 afmm_status afmm_partition_rows(const uint64_t* work, uint64_t n, uint32_t parts, uint64_t* cuts) {

@@ -3,11 +3,10 @@
 Z row i depends only on X row i and all of Y (kernels.hpp:119 and :148 loop over
 independent rows), so the product shards by contiguous Z-row ranges:
 
-  1. every rank computes the predicted kernel time of each row on its own GPU
-     (afmm_row_cost_device: W_i for Case B, the Case A cost model for Case A,
-     whose A-form time follows a row's nonzero bases and whose B-form time does
-     not; Y and X are replicated, so no communication) and cuts the rows into
-     `world` ranges of equal predicted time (afmm_partition_rows);
+  1. every rank computes the same row cuts on its own GPU (afmm_partition_device;
+     Y and X are replicated, so no communication): equal W_i for Case B, equal
+     modeled kernel time for Case A, whose A-form time follows a row's nonzero
+     bases and whose B-form time does not;
   2. every rank runs the product on its row slab (afmm_product_device);
   3. the slabs land in rank 0's Z. Default ("p2p"): rank 0 exports its Z
      buffer over CUDA IPC, the other ranks map it (peer access over NVLink /
@@ -29,8 +28,7 @@ from typing import Optional
 import numpy as np
 import torch
 
-from .afmm import DeviceContext, OpCounts, RawRows, ipc_close, ipc_export, ipc_open, \
-    partition_rows
+from .afmm import DeviceContext, OpCounts, RawRows, ipc_close, ipc_export, ipc_open
 
 
 def gather_rows(dist, z_full, slab, cuts, rank: int, world: int) -> None:
@@ -150,8 +148,7 @@ class ShardedProduct:
             counts = self.ctx.product(case, lhs, rhs, z_full, 0, n, mode=mode)
             self.cuts = np.array([0, n])
             return counts
-        cost = self.ctx.row_cost(case, lhs, rhs)
-        cuts = partition_rows(cost, self.world)
+        cuts = self.ctx.partition(case, lhs, rhs, self.world)
         self.cuts = cuts
         r0, r1 = int(cuts[self.rank]), int(cuts[self.rank + 1])
         ok, peer, ld = self._peer.exchange(z_full) if self._peer else (False, None, 0)

@@ -152,3 +152,43 @@ def test_bench_refuses_more_gpus_than_visible():
     assert r.returncode == 2
     assert not [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert "refusing" in r.stderr
+
+
+def test_case_a_cut_by_modeled_time_balances_sorted_density_rows():
+    """cfg4's Case A (per-row densities from Beta(0.5, 0.5)) with the rows
+    SORTED by density, 8 devices: an equal-row cut gives the sparse slabs
+    (A-form, cheap) a fraction of the dense slabs' (B-form) time; the cut by
+    modeled time (the device-side A-form / B-form choice evaluated per slab,
+    tile and wave quantisation included) balances them to max/min <= 1.05.
+    Host-only model query: no device needed."""
+    import paper_1308_2400_b200 as afmm
+    from paper_1308_2400_b200.gen import make_inputs
+
+    lhs, rhs = make_inputs("cfg4", seed=0, n=8192)
+    order = np.argsort((lhs != 0).sum(axis=1), kind="stable")
+    lhs = np.ascontiguousarray(lhs[order])
+    stats, nnz_row = afmm.case_a_statistics(lhs, rhs)
+    cuts, cyc = afmm.model_partition_case_a(stats, nnz_row, 8)
+    assert cuts[0] == 0 and cuts[-1] == 8192 and np.all(np.diff(cuts) > 0)
+    assert cyc.max() / cyc.min() <= 1.05, (cuts, cyc)
+    # the equal-row cut of the same input is far out of balance
+    eq = np.linspace(0, 8192, 9).astype(np.int64)
+    ws = np.diff(cuts)
+    assert ws[0] > 1.5 * ws[-1]  # sparse slabs get more rows
+    del eq
+
+
+def test_case_a_statistics_match_the_closed_forms():
+    import paper_1308_2400_b200 as afmm
+
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((70, 70)) * (rng.random((70, 70)) < 0.3)
+    y = rng.integers(-3000, 3000, (70, 70)).astype(np.float64)
+    y[0, 0] = 2.5  # llround(2.5) = 3 (half away from zero)
+    stats, nnz = afmm.case_a_statistics(x, y)
+    r = np.where(np.abs(y - np.trunc(y)) == 0.5, np.trunc(y) + np.sign(y), np.rint(y))
+    assert int(stats[0]) == int((r != 0).sum())
+    assert int(stats[2]) == int((np.abs(r) > 2048).sum())
+    assert int(stats[3]) == int(np.abs(r).sum())
+    assert int(stats[1]) == int(np.minimum(np.abs(r), 2048).max(axis=1).sum())
+    assert np.array_equal(nnz, (x != 0).sum(axis=1))

@@ -32,7 +32,11 @@ class OracleContext:
         nnz = (r != 0).sum(axis=1)
         return (np.abs(np.rint(l)) * nnz[None, :]).sum(axis=1).astype(np.uint64)
 
-    row_cost = row_work  # the GPU context predicts time; W_i stands in for it here
+    def partition(self, which, lhs, rhs, parts):
+        # the GPU context cuts by modeled time; equal W_i stands in for it here
+        from paper_1308_2400_b200 import partition_rows
+
+        return partition_rows(self.row_work(which, lhs, rhs), parts)
 
     def product(self, which, lhs, rhs, out, r0, r1, mode="order-preserving"):
         z, counts, err = self.oracle.product(which, lhs.numpy(), rhs.numpy(), r0, r1)

@@ -1,6 +1,6 @@
 """Compare B-form kernel shapes (dev tool): kernel time and bit-identity.
 
-  python tools/shape_time.py [--variants wide,quad] [--big] [--sweep]
+  python tools/shape_time.py [--variants auto,wide,ring] [--big] [--sweep]
 
 For each BASELINE point (cfg2, cfg3 d1 in {1.0, 0.5} x mu in {1, 4, 16}, cfg4,
 cfg5 with --big) every variant (AFMM_BFORM, read at context creation) runs the
@@ -22,7 +22,7 @@ import paper_1308_2400_b200 as afmm  # noqa: E402
 from paper_1308_2400_b200.gen import CONFIGS, make_inputs  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--variants", default="auto,wide,quad")
+ap.add_argument("--variants", default="auto,wide,ring")
 ap.add_argument("--big", action="store_true")
 ap.add_argument("--sweep", action="store_true")
 ap.add_argument("--points", default=None, help="comma list like cfg2,cfg3:1.0:1,cfg4")
