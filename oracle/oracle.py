@@ -5,6 +5,9 @@ reference legs import this module; the product path (paper_1308_2400_b200/)
 never does.
 
   Oracle     -> oracle/liboracle.so, the C restatement (afmm_oracle.c)
+  FastCheck  -> oracle/libfastcheck.so, the vectorised full-size checker
+                (fast_check.c; same per-element add order, pinned to the
+                oracle and the reference by tests/test_oracle.py)
   Reference  -> oracle/_ref/libafmm_ref.so, the UNMODIFIED reference headers
                 behind a C shim (ref_shim.cpp); built only where
                 /root/reference exists, so it may be absent on a GPU box.
@@ -20,6 +23,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "liboracle.so")
+FAST_SO = os.path.join(HERE, "libfastcheck.so")
 REF_SO = os.path.join(HERE, "_ref", "libafmm_ref.so")
 
 
@@ -295,6 +299,48 @@ class Reference:
         self.lib.ref_make_factor_pair(1 if case_b else 0, n, d1, d2, mu, seed, lhs.ctypes.data,
                                       rhs.ctypes.data)
         return lhs, rhs
+
+
+class FastCheck:
+    """Full-size products for parity checks (fast_check.c): Case B rows
+    vectorised across columns; Case A through afmm_case_a(X, Y) ==
+    afmm_case_b(Y^T, X^T)^T. Inputs must be valid (the checker does not
+    validate); returns Z only (counts come from the closed forms)."""
+
+    def __init__(self):
+        if not os.path.exists(FAST_SO):
+            build()
+        self.lib = ctypes.CDLL(FAST_SO)
+        self.lib.fast_case_b_rows.restype = c_int
+        self.lib.fast_case_b_rows.argtypes = [c_int, c_void_p, c_void_p, c_uint64, c_void_p,
+                                              c_uint64, c_void_p, c_int]
+
+    def case_b_rows(self, lhs: np.ndarray, rhs: np.ndarray, rows, threads: int = 0) -> np.ndarray:
+        """Rows `rows` (any row indices, or a (r0, r1) range) of afmm_case_b(lhs, rhs)."""
+        dt = lhs.dtype
+        assert rhs.dtype == dt and dt in (np.float32, np.float64)
+        lhs = np.ascontiguousarray(lhs)
+        rhs = np.ascontiguousarray(rhs)
+        n = lhs.shape[0]
+        if isinstance(rows, tuple):
+            rows = np.arange(rows[0], rows[1])
+        idx = np.ascontiguousarray(rows, dtype=np.uint64)
+        z = np.empty((idx.size, n), dtype=dt)
+        rc = self.lib.fast_case_b_rows(0 if dt == np.float64 else 1, lhs.ctypes.data,
+                                       rhs.ctypes.data, n, idx.ctypes.data, idx.size,
+                                       z.ctypes.data, threads or os.cpu_count() or 1)
+        if rc != 0:
+            raise RuntimeError("fast_case_b_rows failed")
+        return z
+
+    def product(self, case: str, lhs: np.ndarray, rhs: np.ndarray, threads: int = 0) -> np.ndarray:
+        """The whole n x n product."""
+        n = lhs.shape[0]
+        if case == "b":
+            return self.case_b_rows(lhs, rhs, (0, n), threads)
+        zt = self.case_b_rows(np.ascontiguousarray(rhs.T), np.ascontiguousarray(lhs.T), (0, n),
+                              threads)
+        return np.ascontiguousarray(zt.T)
 
 
 def reference_available() -> bool:

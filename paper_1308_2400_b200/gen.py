@@ -99,3 +99,17 @@ def expected_additions(case: str, lhs: np.ndarray, rhs: np.ndarray) -> int:
     reps = np.abs(np.rint(lhs.astype(np.float64))).astype(np.int64)
     nnz = (rhs != 0).sum(axis=1).astype(np.int64)
     return int((reps.sum(axis=0) * nnz).sum())
+
+
+def expected_counts(case: str, lhs: np.ndarray, rhs: np.ndarray) -> tuple[int, int, int]:
+    """Closed-form OpCounts (additions, multiplications, zero_skips) of valid
+    integer-rep operands (SURVEY.md 8.0, test_kernels.cpp:45-57, :160-173):
+    Case A zero_skips = #{(i,k): X[i,k] == 0}; Case B zero_skips =
+    sum over (i,k) with a nonzero rep of (n - nnz(Y[k,:]))."""
+    n = lhs.shape[0]
+    adds = expected_additions(case, lhs, rhs)
+    if case == "a":
+        return adds, 0, int((lhs == 0).sum())
+    rep_nz = (np.rint(lhs.astype(np.float64)) != 0).astype(np.int64)
+    nnz = (rhs != 0).sum(axis=1).astype(np.int64)
+    return adds, 0, int((rep_nz.sum(axis=0) * (n - nnz)).sum())

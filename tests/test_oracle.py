@@ -140,3 +140,47 @@ def test_row_slab_and_threads_are_bit_identical(oracle):
         assert np.array_equal(zs, z[5:23])
         zm, cm = oracle.product_mt(case, lhs, rhs, 0, 37, 4)
         assert np.array_equal(zm.view(np.uint64), z.view(np.uint64)) and cm == c
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_fast_checker_is_bit_identical_to_the_oracle(oracle, seed):
+    """oracle/fast_check.c (the vectorised full-size checker) against the
+    scalar restatement: both cases, fp32/fp64, ragged n (chunk tails), signed
+    reps, zero / -0.0 / subnormal bases, overflow to +/-inf, any row list."""
+    from oracle.oracle import FastCheck
+
+    fc = FastCheck()
+    rng = np.random.default_rng(600 + seed)
+    for n in (1, 3, 31, 65, 257, 300):
+        for dt in (np.float32, np.float64):
+            bases = rng.standard_normal((n, n)) * (rng.random((n, n)) < 0.6)
+            u = rng.random((n, n))
+            bases[u < 0.05] = -0.0
+            bases[(u > 0.05) & (u < 0.08)] = np.finfo(dt).tiny / 7
+            if seed == 3:
+                bases *= np.finfo(dt).max / 8
+            reps = rng.integers(-9, 10, (n, n)) * (rng.random((n, n)) < 0.7)
+            bases, reps = bases.astype(dt), reps.astype(dt)
+            for case, lhs, rhs in (("a", bases, reps), ("b", reps, bases)):
+                z, c, _ = oracle.product(case, lhs, rhs)
+                zf = fc.product(case, lhs, rhs, threads=3)
+                assert np.array_equal(z.view(np.uint8), zf.view(np.uint8)), (n, dt, case)
+                if case == "b":
+                    rows = rng.integers(0, n, min(n, 37))
+                    zr = fc.case_b_rows(lhs, rhs, rows, threads=2)
+                    assert np.array_equal(zr.view(np.uint8), z[rows].view(np.uint8))
+
+
+def test_fast_checker_matches_live_reference(reference):
+    """The checker against the unmodified reference (fp64) on a BASELINE-like
+    Case B and Case A input."""
+    from oracle.oracle import FastCheck
+    from paper_1308_2400_b200.gen import expected_counts, make_inputs
+
+    fc = FastCheck()
+    for name, case in (("cfg2", "b"), ("cfg1", "a")):
+        lhs, rhs = make_inputs(name, seed=5, n=160)
+        z, c, err = reference.product(case, lhs, rhs)
+        assert err is None
+        assert np.array_equal(z.view(np.uint8), fc.product(case, lhs, rhs).view(np.uint8))
+        assert c == expected_counts(case, lhs, rhs)
