@@ -213,6 +213,45 @@ struct Acc {
   }
 };
 
+// Fast (reassociated) mode: each element's chain runs in the T accumulators
+// for a block of kFlushBlocks k blocks, then the block's partial is added into
+// an fp64 total ("blocked summation"): every term keeps its |rep| adds, plus
+// one add per element and block. An fp32 chain of ~32K adds (cfg4, full size)
+// drifts to 7e-5 of sum |terms|; chains of one block stay within ~1e-6.
+constexpr uint32_t kFlushBlocks = 4;
+
+template <class T, int G>
+struct Total {
+  static constexpr int NE = 2 * G * (int)(sizeof(float2) / sizeof(T));  // elements per lane
+  double t[NE];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int e = 0; e < NE; ++e) t[e] = 0.0;
+  }
+  __device__ __forceinline__ void flush(Acc<T, G>& acc) {
+#pragma unroll
+    for (int c = 0; c < 2 * G; ++c) {
+      if constexpr (sizeof(T) == 4) {
+        t[2 * c] = __dadd_rn(t[2 * c], (double)acc.a[c].x);
+        t[2 * c + 1] = __dadd_rn(t[2 * c + 1], (double)acc.a[c].y);
+      } else {
+        t[c] = __dadd_rn(t[c], acc.a[c]);
+      }
+    }
+    acc.zero();
+  }
+  // the totals, rounded once to T, back into the accumulators (for store())
+  __device__ __forceinline__ void to(Acc<T, G>& acc) const {
+#pragma unroll
+    for (int c = 0; c < 2 * G; ++c) {
+      if constexpr (sizeof(T) == 4)
+        acc.a[c] = make_float2(__double2float_rn(t[2 * c]), __double2float_rn(t[2 * c + 1]));
+      else
+        acc.a[c] = t[c];
+    }
+  }
+};
+
 // Rows per CTA (<= cw) that minimise (waves x rows per CTA), i.e. the busiest
 // SM's share of rows when every SM holds `per_sm` CTAs: a last wave that is
 // mostly empty costs as much as a full one (n = 1024 fp64, 16-row CTAs, 4
@@ -327,7 +366,7 @@ __device__ __forceinline__ uint32_t lower_bound_k(const int2* lst, uint32_t cnt,
 //   k slice: blockIdx.z selects slice z = [z*slice_blocks, (z+1)*slice_blocks)
 //   of the nkb_total k blocks and writes to out + z * slice_stride (fast-mode
 //   split-k; one slice = the whole k range in order-preserving mode).
-template <class T, int G, int CW, int STAGES, int MINB, bool SPLIT>
+template <class T, int G, int CW, int STAGES, int MINB, bool SPLIT, bool BLOCKED>
 __global__ void __launch_bounds__((CW + 1) * 32, MINB)
     k_bform(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ lists,
             uint64_t cap, const uint32_t* __restrict__ counts, uint32_t nrows, uint32_t rpc,
@@ -397,6 +436,9 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
 
   Acc<T, G> acc;
   acc.zero();
+  Total<T, BLOCKED ? G : 1> tot;  // fast mode only
+  if constexpr (BLOCKED) tot.zero();
+  uint32_t flush_kb = kFlushBlocks;
   const uint32_t k_lo = kb_lo * KB;
   Cursor<STAGES, Gm::STAGE_BYTES> cur(smem_u32(base), smem_u32(full), smem_u32(empty), lane);
   cur.wait();
@@ -413,11 +455,22 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
     if (f + kListPrefetch < cnt)
       asm volatile("prefetch.global.L1 [%0];" ::"l"(lp + f + kListPrefetch));
     const uint32_t k = (uint32_t)e.x;
-    cur.seek((k - k_lo) / KB, lane);  // block index within the slice
+    const uint32_t kb = (k - k_lo) / KB;  // block index within the slice
+    if constexpr (BLOCKED) {
+      if (kb >= flush_kb) {  // the entry starts a new block of the blocked sum
+        tot.flush(acc);
+        flush_kb = (kb / kFlushBlocks + 1) * kFlushBlocks;
+      }
+    }
+    cur.seek(kb, lane);
     acc.run(cur.stage_addr + (k % KB) * BOX_BYTES, e.y);
     e = ne;
   }
   cur.drain(nkb, lane);
+  if constexpr (BLOCKED) {
+    tot.flush(acc);
+    tot.to(acc);
+  }
 
   if (b < nrows) acc.store(out + (uint64_t)b * ld_out, tile_c, ncols, lane, vec_ok != 0);
 }
@@ -658,13 +711,13 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
   }
 }
 
-template <class T, int G, int CW, int STAGES, int MINB>
+template <class T, int G, int CW, int STAGES, int MINB, bool BLOCKED = false>
 cudaError_t launch_ring(BformLaunch& a, T* out, cudaStream_t s) {
   const uint32_t nkb = (a.nk + KB - 1) / KB;
   uint32_t want = a.splits < 1 ? 1 : a.splits;
   if (want > nkb) want = nkb;
-  auto kern = want > 1 ? k_bform<T, G, CW, STAGES, MINB, true>
-                       : k_bform<T, G, CW, STAGES, MINB, false>;
+  auto kern = want > 1 ? k_bform<T, G, CW, STAGES, MINB, true, BLOCKED>
+                       : k_bform<T, G, CW, STAGES, MINB, false, BLOCKED>;
   const size_t smem = ring_smem_bytes<T, G, STAGES>();
   // set on every call: the attribute is per device and costs ~1 us
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -703,6 +756,10 @@ cudaError_t launch_bform(BformLaunch& a, T* out, cudaStream_t s) {
       return launch_ring<T, 8, kWideRows, 6, kWideCtasPerSm>(a, out, s);
     case kShapeSmall:  // 256 fp32 / 128 fp64 columns x 4 rows, up to 8 CTAs per SM
       return launch_ring<T, 2, 4, 3, 8>(a, out, s);
+    case kShapeTiny:  // the small tile, 16-stage ring (128 KB), 1 CTA per SM
+      return launch_ring<T, 2, 4, 16, 1>(a, out, s);
+    case kShapeFast:  // fast mode: 512 fp32 / 256 fp64 columns x 16 rows, fp64 blocked totals
+      return launch_ring<T, 4, 16, 12, 1, true>(a, out, s);
     default:  // narrow: 512 fp32 / 256 fp64 columns x 16 rows, 2 CTAs per SM
       return launch_ring<T, 4, 16, 6, 2>(a, out, s);
   }

@@ -89,10 +89,14 @@ int bform_box_bytes();
 
 // k_bform tile shapes: narrow = 512 fp32 / 256 fp64 columns, 2 CTAs per SM;
 // wide = 1024 / 512 columns, 1 CTA per SM; small = 256 / 128 columns x 4 rows
-// for problems too small to fill the GPU with the larger tiles.
+// for problems too small to fill the GPU with the larger tiles; tiny = the
+// small tile with a 16-stage ring (128 KB: half of the k range at n = 256)
+// when a single wave of small CTAs covers the problem.
 constexpr int kShapeNarrow = 0;
 constexpr int kShapeWide = 1;
 constexpr int kShapeSmall = 2;
+constexpr int kShapeTiny = 3;
+constexpr int kShapeFast = 4;  // reassociated mode: narrow tile, 1 CTA/SM, blocked fp64 totals
 constexpr int kWideRows = 16;      // rows per wide CTA (16 consumer warps + 1 TMA warp)
 constexpr int kWideCtasPerSm = 1;  // wide CTAs resident per SM (6-stage ring, 192 KB smem)
 

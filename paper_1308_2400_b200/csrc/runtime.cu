@@ -46,6 +46,7 @@ enum Variant {
   kNarrow = 0,  // 512 fp32 / 256 fp64 columns, 2 CTAs per SM
   kWide = 1,    // 1024 / 512 columns, 1 CTA per SM
   kSmall = 2,   // 256 / 128 columns x 4 rows
+  kTiny = 3,    // the small tile with a 16-stage ring
   kAForm = 8,   // Case A: every row in the A-form
   kHybrid = 9,  // Case A: the best A-form / B-form row split, forced
 };
@@ -57,7 +58,8 @@ int variant_from_env() {
     const char* name;
     int variant;
   } names[] = {{"ring", kNarrow}, {"narrow", kNarrow}, {"wide", kWide},
-               {"small", kSmall}, {"aform", kAForm},    {"hybrid", kHybrid}};
+               {"small", kSmall}, {"tiny", kTiny},      {"aform", kAForm},
+               {"hybrid", kHybrid}};
   for (const auto& e : names)
     if (std::strcmp(v, e.name) == 0) return e.variant;
   return kAuto;
@@ -402,6 +404,7 @@ int pick_shape(int variant, uint64_t nrows, uint64_t ncols, size_t elem, int sms
     case kNarrow: return afmm_dev::kShapeNarrow;
     case kWide: return afmm_dev::kShapeWide;
     case kSmall: return afmm_dev::kShapeSmall;
+    case kTiny: return afmm_dev::kShapeTiny;
     default: break;
   }
   const uint64_t cbytes = ncols * elem;
@@ -413,6 +416,8 @@ int pick_shape(int variant, uint64_t nrows, uint64_t ncols, size_t elem, int sms
   // wide tiles need about one wave of CTAs: at n = 1024 fp64 the 128 wide
   // CTAs, trimmed to 148 of 14 rows, run 7% faster than 256 narrow ones)
   if (4 * wide_ctas >= 3 * wide_slots) return afmm_dev::kShapeWide;
+  const uint64_t small_ctas = (nrows + 3) / 4 * ((cbytes + 1023) / 1024);
+  if (small_ctas <= (uint64_t)sms) return afmm_dev::kShapeTiny;
   if (narrow_ctas < (uint64_t)sms) return afmm_dev::kShapeSmall;
   return afmm_dev::kShapeNarrow;
 }
@@ -425,6 +430,8 @@ ShapeGeo shape_geo(int shape) {
   switch (shape) {
     case afmm_dev::kShapeWide: return {4096, afmm_dev::kWideRows, afmm_dev::kWideCtasPerSm};
     case afmm_dev::kShapeSmall: return {1024, 4, 8};
+    case afmm_dev::kShapeTiny: return {1024, 4, 1};
+    case afmm_dev::kShapeFast: return {2048, 16, 1};
     default: return {2048, 16, 2};
   }
 }
@@ -461,6 +468,9 @@ afmm_status launch_compute(afmm_context* c, const Call& call, int shape, const T
                            uint64_t kb_rows, uint64_t b_cols, uint64_t ldb, uint32_t nrows,
                            int32_t ncols, const uint32_t* dyn_ncols, T* out, uint64_t ld_out,
                            DevStatus* st, afmm_error* err) {
+  // reassociated mode: the blocked-sum kernel (bform.cu kShapeFast), k slices
+  // on top when the tile grid is small
+  if (call.mode == AFMM_MODE_FAST) shape = afmm_dev::kShapeFast;
   const ShapeGeo g = shape_geo(shape);
   const uint64_t cbytes = (uint64_t)ncols * sizeof(T);
   const uint64_t ctas = (nrows + g.rows_per_cta - 1) / g.rows_per_cta *

@@ -553,7 +553,7 @@ def test_fast_mode_within_tolerance(cuda, oracle, name, n, kw):
     assert float(err.max()) <= tol, (name, float(err.max()))
 
 
-@pytest.mark.parametrize("variant", ["wide", "ring", "small", "aform", "hybrid"])
+@pytest.mark.parametrize("variant", ["wide", "ring", "small", "tiny", "aform", "hybrid"])
 def test_both_kernel_variants_bit_exact(cuda, oracle, variant, monkeypatch):
     """Every B-form tile shape and the forced Case A forms give the oracle's bits."""
     import torch
@@ -584,7 +584,7 @@ def test_randomized_shapes_and_distributions(cuda, oracle, seed, monkeypatch):
     import torch
 
     rng = np.random.default_rng(1000 + seed)
-    variants = [None, "wide", "ring", "small", "aform", "hybrid"]
+    variants = [None, "wide", "ring", "small", "tiny", "aform", "hybrid"]
     for trial in range(16):
         variant = variants[rng.integers(len(variants))]
         if variant:
