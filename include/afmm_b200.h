@@ -40,7 +40,7 @@ typedef enum {
   AFMM_ERR_DOMAIN = 2,           /* std::domain_error (rep not integer / out of range / non-finite) */
   AFMM_ERR_INVALID_ARGUMENT = 3, /* std::invalid_argument (n == 0, bad option)          */
   AFMM_ERR_CUDA = 4,             /* CUDA runtime / driver failure, no device            */
-  AFMM_ERR_UNSUPPORTED = 5,      /* n beyond the device index range (2^31 - 1)          */
+  AFMM_ERR_UNSUPPORTED = 5,      /* n beyond 2^31 - 1; a NaN rep (AFMM_FLAG_KERNEL_SEMANTICS) */
   AFMM_ERR_OUT_OF_MEMORY = 6
 } afmm_status;
 
@@ -72,6 +72,7 @@ typedef enum {
   AFMM_ERRKIND_SHAPE = 4,         /* kernels.hpp:15-21 */
   AFMM_ERRKIND_EMPTY = 5,         /* matrix.hpp:54-57 */
   AFMM_ERRKIND_REP_TOO_LARGE = 6, /* unused since ABI 2: every |rep| <= 2^53 is accepted */
+  AFMM_ERRKIND_REP_NAN = 8,       /* a NaN rep under AFMM_FLAG_KERNEL_SEMANTICS */
   AFMM_ERRKIND_OTHER = 7
 } afmm_error_kind;
 
@@ -93,6 +94,18 @@ typedef struct {
   int32_t form;      /* Case A kernel form of device 0: 0 B-form, 1 A-form, 2 split */
 } afmm_timing;
 
+/* The operands are already-constructed matrices (the C++ wrapper's
+ * DenseMatrix arguments), so only the kernel's own checks apply
+ * (kernels.hpp:25-43): a non-finite BASE is computed with (inf / NaN
+ * propagate through the adds exactly as in the reference), an infinite rep
+ * "exceeds the exact integer range", and a NaN rep -- which the reference's
+ * check lets through and then repeats llround(NaN) ~ 2^63 times, i.e. never
+ * finishes -- is rejected with AFMM_ERR_UNSUPPORTED. Without the flag the
+ * arrays are taken as the values a DenseMatrix is constructed from, and any
+ * non-finite element is the constructor's "DenseMatrix: non-finite element"
+ * (matrix.hpp:31-35). */
+#define AFMM_FLAG_KERNEL_SEMANTICS 1
+
 typedef enum {
   /* contiguous Z row ranges of equal predicted kernel time: W_i (exact
    * additions) for Case B, the Case A cost model (A-form / B-form) for Case A */
@@ -107,7 +120,7 @@ typedef struct {
   int32_t num_devices;  /* G > 1: rows of Z sharded over G devices (0 or 1: one device) */
   const int32_t* devices; /* G ordinals (NULL = 0..G-1); a device may repeat (two shards) */
   int32_t partition;    /* afmm_partition */
-  int32_t reserved;
+  int32_t flags;        /* AFMM_FLAG_* */
   afmm_timing* timing;  /* optional out: device-measured phases of this call */
 } afmm_options;
 

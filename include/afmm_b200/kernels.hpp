@@ -68,7 +68,8 @@ inline void throw_for(afmm_status status, const afmm_error& err) {
     case AFMM_OK: return;
     case AFMM_ERR_SHAPE: throw shape_error(msg);
     case AFMM_ERR_DOMAIN: throw std::domain_error(msg);
-    case AFMM_ERR_UNSUPPORTED: throw std::length_error(msg);  // n beyond the device index range
+    // n beyond the device index range, or a NaN rep (the reference would not finish)
+    case AFMM_ERR_UNSUPPORTED: throw std::length_error(msg);
     case AFMM_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
     case AFMM_ERR_OUT_OF_MEMORY: throw std::bad_alloc();
     default: throw std::runtime_error(msg.empty() ? "afmm: CUDA failure" : msg);
@@ -85,6 +86,9 @@ inline afmm_options to_c(const Options& o) {
   c.split_k = o.split_k;
   c.partition = static_cast<int32_t>(o.partition);
   c.timing = o.timing;
+  // the arguments are constructed matrices: the kernel's checks only
+  // (non-finite bases are computed, an infinite rep is out of range)
+  c.flags = AFMM_FLAG_KERNEL_SEMANTICS;
   if (!o.devices.empty()) {
     c.num_devices = static_cast<int32_t>(o.devices.size());
     c.devices = reinterpret_cast<const int32_t*>(o.devices.data());

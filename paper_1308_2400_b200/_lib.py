@@ -40,6 +40,7 @@ ERRKIND_NON_FINITE = 3
 ERRKIND_SHAPE = 4
 ERRKIND_EMPTY = 5
 ERRKIND_REP_TOO_LARGE = 6  # unused since ABI 2
+ERRKIND_REP_NAN = 8
 ERRKIND_OTHER = 7
 
 
@@ -83,7 +84,10 @@ class Options(ctypes.Structure):
 
     _fields_ = [("mode", c_int32), ("device", c_int32), ("split_k", c_int32),
                 ("num_devices", c_int32), ("devices", POINTER(c_int32)), ("partition", c_int32),
-                ("reserved", c_int32), ("timing", POINTER(Timing))]
+                ("flags", c_int32), ("timing", POINTER(Timing))]
+
+
+FLAG_KERNEL_SEMANTICS = 1
 
 
 # Every symbol include/afmm_b200.h declares, with its ctypes signature.

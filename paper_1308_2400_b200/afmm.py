@@ -93,7 +93,8 @@ _PARTITIONS = {"work": _lib.PARTITION_WORK, "rows": _lib.PARTITION_ROWS}
 
 def _options(mode: str, device: Optional[int], devices: Optional[Sequence[int]] = None,
              partition: str = "work", split_k: int = 0,
-             timing: Optional[_lib.Timing] = None) -> Tuple[_lib.Options, object]:
+             timing: Optional[_lib.Timing] = None,
+             kernel_semantics: bool = False) -> Tuple[_lib.Options, object]:
     """afmm_options + the ctypes objects it points to (kept alive by the caller)."""
     if mode not in _MODES:
         raise InvalidArgument(f"afmm: unknown mode {mode!r}")
@@ -104,6 +105,7 @@ def _options(mode: str, device: Optional[int], devices: Optional[Sequence[int]] 
     o.device = -1 if device is None else int(device)
     o.split_k = int(split_k)
     o.partition = _PARTITIONS[partition]
+    o.flags = _lib.FLAG_KERNEL_SEMANTICS if kernel_semantics else 0
     keep = None
     if devices is not None:
         devs = [int(d) for d in devices]
@@ -138,7 +140,8 @@ def _common_dtype(lhs: np.ndarray, rhs: np.ndarray, dtype) -> np.dtype:
 
 def _product(which: int, lhs, rhs, mode: str, device: Optional[int], dtype,
              out: Optional[np.ndarray], devices=None, partition: str = "work",
-             split_k: int = 0, timing: bool = False) -> MultiplyResult:
+             split_k: int = 0, timing: bool = False,
+             kernel_semantics: bool = False) -> MultiplyResult:
     lib = _lib.load()
     l = _as_square(lhs, "lhs")
     r = _as_square(rhs, "rhs")
@@ -153,7 +156,7 @@ def _product(which: int, lhs, rhs, mode: str, device: Optional[int], dtype,
     counts = _lib.OpCounts()
     err = _lib.Error()
     tm = _lib.Timing() if timing else None
-    opts, _keep = _options(mode, device, devices, partition, split_k, tm)
+    opts, _keep = _options(mode, device, devices, partition, split_k, tm, kernel_semantics)
     fn = {
         (_lib.CASE_A, np.float64): lib.afmm_case_a_f64,
         (_lib.CASE_B, np.float64): lib.afmm_case_b_f64,
@@ -172,24 +175,30 @@ def _product(which: int, lhs, rhs, mode: str, device: Optional[int], dtype,
 
 def afmm_case_a(lhs, rhs, *, mode: str = ORDER_PRESERVING, device: Optional[int] = None,
                 dtype=None, out: Optional[np.ndarray] = None, devices=None,
-                partition: str = "work", split_k: int = 0, timing: bool = False) -> MultiplyResult:
+                partition: str = "work", split_k: int = 0, timing: bool = False,
+                kernel_semantics: bool = False) -> MultiplyResult:
     """AFMM Case A on the GPU: real lhs bases, integer-valued rhs reps (kernels.hpp:113-136).
 
     devices=[d0, d1, ...] shards the rows of Z over several GPUs in this
     process (a device may repeat); partition="work" balances predicted kernel
     time, "rows" cuts equal row counts. timing=True adds the device-measured
-    phases of the call to the result."""
+    phases of the call to the result. By default the arrays are the values a
+    DenseMatrix is constructed from (a non-finite element is the constructor's
+    error, matrix.hpp:31-35); kernel_semantics=True applies only the kernel's
+    own checks, as for matrices built element by element (non-finite bases
+    are computed, an infinite rep is out of range, a NaN rep unsupported)."""
     return _product(_lib.CASE_A, lhs, rhs, mode, device, dtype, out, devices, partition, split_k,
-                    timing)
+                    timing, kernel_semantics)
 
 
 def afmm_case_b(lhs, rhs, *, mode: str = ORDER_PRESERVING, device: Optional[int] = None,
                 dtype=None, out: Optional[np.ndarray] = None, devices=None,
-                partition: str = "work", split_k: int = 0, timing: bool = False) -> MultiplyResult:
+                partition: str = "work", split_k: int = 0, timing: bool = False,
+                kernel_semantics: bool = False) -> MultiplyResult:
     """AFMM Case B on the GPU: integer-valued lhs reps, real rhs bases (kernels.hpp:142-165).
-    Multi-GPU and timing options as in afmm_case_a."""
+    Multi-GPU, timing and kernel_semantics options as in afmm_case_a."""
     return _product(_lib.CASE_B, lhs, rhs, mode, device, dtype, out, devices, partition, split_k,
-                    timing)
+                    timing, kernel_semantics)
 
 
 # ---- device-resident API ------------------------------------------------------

@@ -756,8 +756,6 @@ cudaError_t launch_bform(BformLaunch& a, T* out, cudaStream_t s) {
       return launch_ring<T, 8, kWideRows, 6, kWideCtasPerSm>(a, out, s);
     case kShapeSmall:  // 256 fp32 / 128 fp64 columns x 4 rows, up to 8 CTAs per SM
       return launch_ring<T, 2, 4, 3, 8>(a, out, s);
-    case kShapeTiny:  // the small tile, 16-stage ring (128 KB), 1 CTA per SM
-      return launch_ring<T, 2, 4, 16, 1>(a, out, s);
     case kShapeFast:  // fast mode: 512 fp32 / 256 fp64 columns x 16 rows, fp64 blocked totals
       return launch_ring<T, 4, 16, 12, 1, true>(a, out, s);
     default:  // narrow: 512 fp32 / 256 fp64 columns x 16 rows, 2 CTAs per SM

@@ -28,7 +28,7 @@ struct DevStatus {
   unsigned long long zero_skips;
   uint32_t a_rows;     // Case A: slab rows the device-side choice gave the A-form
   uint32_t form_rows;  // Case A: slab rows seen by the choice (0: no choice made)
-  unsigned long long pad;
+  unsigned long long rep_nan_inv;  // ~(linear index) of the first NaN rep (kernel semantics)
 };
 static_assert(sizeof(DevStatus) == 64, "DevStatus is one 64-byte record");
 
@@ -46,7 +46,8 @@ struct AEntry<double> {
 
 // Validation failed or a list overflowed: the compute kernels do nothing.
 __device__ __forceinline__ bool status_failed(const DevStatus* st) {
-  return (st->nonfinite_lhs_inv | st->nonfinite_rhs_inv | st->rep_bad_inv | st->list_need) != 0ull;
+  return (st->nonfinite_lhs_inv | st->nonfinite_rhs_inv | st->rep_bad_inv | st->list_need |
+          st->rep_nan_inv) != 0ull;
 }
 
 // kernels.hpp:31-40 on the widened value: 0 ok, 1 not integer-valued,

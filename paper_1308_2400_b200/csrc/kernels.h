@@ -14,13 +14,15 @@ namespace afmm_dev {
 
 void note_launch();  // counts library kernel launches (runtime.cu)
 
-// Rows [l0, l1) of lhs and [q0, q1) of rhs: finite check, rep validation
+// Rows [l0, l1) of lhs and [q0, q1) of rhs: finite check (check_finite; a
+// NaN rep is recorded either way), rep validation
 // (into st, global row-major indices), and the per-k vector of the rhs rows
 // (Case B: nnz[k] of rhs rows; Case A: rsum[k] of rhs rows). which_case: 0 = A, 1 = B.
 template <class T>
 void launch_scan_stats(const T* lhs, const T* rhs, uint64_t ld, uint32_t n, int which_case,
                        uint32_t l0, uint32_t l1, uint32_t q0, uint32_t q1, DevStatus* st,
-                       uint32_t* nnz, unsigned long long* rsum, cudaStream_t s);
+                       uint32_t* nnz, unsigned long long* rsum, cudaStream_t s,
+                       int check_finite = 1);
 // Rows [a0, a1) of X: work[i] (if work != nullptr); slab rows [r0, r1) add
 // OpCounts to st and, for Case B with lists != nullptr, get their compacted
 // int2 (k, rep) lists; nnz_row (optional, Case A): nonzero bases of each slab row.
@@ -89,14 +91,12 @@ int bform_box_bytes();
 
 // k_bform tile shapes: narrow = 512 fp32 / 256 fp64 columns, 2 CTAs per SM;
 // wide = 1024 / 512 columns, 1 CTA per SM; small = 256 / 128 columns x 4 rows
-// for problems too small to fill the GPU with the larger tiles; tiny = the
-// small tile with a 16-stage ring (128 KB: half of the k range at n = 256)
-// when a single wave of small CTAs covers the problem.
+// for problems too small to fill the GPU with the larger tiles; fast = the
+// reassociated mode's kernel (narrow tile, 1 CTA per SM, blocked fp64 totals).
 constexpr int kShapeNarrow = 0;
 constexpr int kShapeWide = 1;
 constexpr int kShapeSmall = 2;
-constexpr int kShapeTiny = 3;
-constexpr int kShapeFast = 4;  // reassociated mode: narrow tile, 1 CTA/SM, blocked fp64 totals
+constexpr int kShapeFast = 4;
 constexpr int kWideRows = 16;      // rows per wide CTA (16 consumer warps + 1 TMA warp)
 constexpr int kWideCtasPerSm = 1;  // wide CTAs resident per SM (6-stage ring, 192 KB smem)
 

@@ -117,9 +117,9 @@ __device__ __forceinline__ void note_list(DevStatus* st, unsigned long long len,
 // warp task t < (l1 - l0): lhs row l0 + t; then rhs rows q0 .. q1 - 1.
 template <class T>
 __global__ void k_scan_stats(const T* __restrict__ lhs, const T* __restrict__ rhs, uint64_t ld,
-                             uint32_t n, int which_case, int vec, uint32_t l0, uint32_t l1,
-                             uint32_t q0, uint32_t q1, DevStatus* st, uint32_t* __restrict__ nnz,
-                             unsigned long long* __restrict__ rsum) {
+                             uint32_t n, int which_case, int vec, int check_finite, uint32_t l0,
+                             uint32_t l1, uint32_t q0, uint32_t q1, DevStatus* st,
+                             uint32_t* __restrict__ nnz, unsigned long long* __restrict__ rsum) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -130,7 +130,7 @@ __global__ void k_scan_stats(const T* __restrict__ lhs, const T* __restrict__ rh
     const T* row = (is_rhs ? rhs : lhs) + i * ld;
     // Case A validates rhs (kernels.hpp:115), Case B lhs (:144)
     const bool is_rep = is_rhs == (which_case == 0);
-    unsigned long long nf = 0, rb = 0;  // inverted keys, 0 = none
+    unsigned long long nf = 0, rb = 0, rn = 0;  // inverted keys, 0 = none
     uint32_t cnt = 0;
     unsigned long long s = 0;
     for (uint32_t j0 = 4 * lane; j0 < n; j0 += 128) {
@@ -142,10 +142,12 @@ __global__ void k_scan_stats(const T* __restrict__ lhs, const T* __restrict__ rh
         if (j >= n) break;
         const double d = (double)v[e];
         const unsigned long long lin = i * (uint64_t)n + j;
-        if (!isfinite(d) && nf == 0) nf = ~lin;  // ascending j: the first one is the minimum
+        // ascending j: the first one is the minimum
+        if (check_finite && !isfinite(d) && nf == 0) nf = ~lin;
         if (is_rep) {
-          const int kind = rep_kind(d);
+          const int kind = rep_kind(d);  // (an infinite rep: kind 2, as in the reference)
           if (kind && rb == 0) rb = ~((lin << 2) | (unsigned long long)kind);
+          if (isnan(d) && rn == 0) rn = ~lin;
         }
         if (is_rhs) {
           cnt += v[e] != T(0) ? 1u : 0u;
@@ -154,12 +156,14 @@ __global__ void k_scan_stats(const T* __restrict__ lhs, const T* __restrict__ rh
         }
       }
     }
-    if (__any_sync(FULL, (nf | rb) != 0)) {
+    if (__any_sync(FULL, (nf | rb | rn) != 0)) {
       nf = warp_max_u64(nf);
       rb = warp_max_u64(rb);
+      rn = warp_max_u64(rn);
       if (lane == 0) {
         if (nf) atomicMax(is_rhs ? &st->nonfinite_rhs_inv : &st->nonfinite_lhs_inv, nf);
         if (rb) atomicMax(&st->rep_bad_inv, rb);
+        if (rn) atomicMax(&st->rep_nan_inv, rn);
       }
     }
     if (is_rhs) {
@@ -651,12 +655,12 @@ int vec_ok(const T* p, uint64_t ld) {
 template <class T>
 void launch_scan_stats(const T* lhs, const T* rhs, uint64_t ld, uint32_t n, int which_case,
                        uint32_t l0, uint32_t l1, uint32_t q0, uint32_t q1, DevStatus* st,
-                       uint32_t* nnz, unsigned long long* rsum, cudaStream_t s) {
+                       uint32_t* nnz, unsigned long long* rsum, cudaStream_t s, int check_finite) {
   const int vec = vec_ok(lhs, ld) & vec_ok(rhs, ld);
   const uint64_t tasks = (uint64_t)(l1 - l0) + (q1 - q0);
   if (tasks == 0) return;
-  k_scan_stats<T><<<grid_for_warps(tasks, 8), 256, 0, s>>>(lhs, rhs, ld, n, which_case, vec, l0,
-                                                            l1, q0, q1, st, nnz, rsum);
+  k_scan_stats<T><<<grid_for_warps(tasks, 8), 256, 0, s>>>(
+      lhs, rhs, ld, n, which_case, vec, check_finite, l0, l1, q0, q1, st, nnz, rsum);
   note_launch();
 }
 
@@ -737,7 +741,7 @@ void launch_reduce_slices(const T* part, uint64_t stride, uint64_t ld_part, uint
 #define INSTANTIATE(T)                                                                         \
   template void launch_scan_stats<T>(const T*, const T*, uint64_t, uint32_t, int, uint32_t,    \
                                      uint32_t, uint32_t, uint32_t, DevStatus*, uint32_t*,      \
-                                     unsigned long long*, cudaStream_t);                       \
+                                     unsigned long long*, cudaStream_t, int);                  \
   template void launch_rows<T>(const T*, uint64_t, uint32_t, int, const uint32_t*,             \
                                const unsigned long long*, uint32_t, uint32_t, uint32_t,        \
                                uint32_t, int2*, uint64_t, uint32_t*, unsigned long long*,      \

@@ -46,7 +46,6 @@ enum Variant {
   kNarrow = 0,  // 512 fp32 / 256 fp64 columns, 2 CTAs per SM
   kWide = 1,    // 1024 / 512 columns, 1 CTA per SM
   kSmall = 2,   // 256 / 128 columns x 4 rows
-  kTiny = 3,    // the small tile with a 16-stage ring
   kAForm = 8,   // Case A: every row in the A-form
   kHybrid = 9,  // Case A: the best A-form / B-form row split, forced
 };
@@ -58,8 +57,7 @@ int variant_from_env() {
     const char* name;
     int variant;
   } names[] = {{"ring", kNarrow}, {"narrow", kNarrow}, {"wide", kWide},
-               {"small", kSmall}, {"tiny", kTiny},      {"aform", kAForm},
-               {"hybrid", kHybrid}};
+               {"small", kSmall}, {"aform", kAForm},    {"hybrid", kHybrid}};
   for (const auto& e : names)
     if (std::strcmp(v, e.name) == 0) return e.variant;
   return kAuto;
@@ -169,6 +167,7 @@ struct Call {
   uint64_t ld_out = 0, r0 = 0, r1 = 0;
   bool prevalidated = false;  // multi-device: validation and the per-k vector done already
   bool have_counts = false;   // multi-device Case A: fp16 counts and statistics done already
+  bool check_finite = true;   // false: AFMM_FLAG_KERNEL_SEMANTICS (no DenseMatrix ctor check)
 };
 
 }  // namespace
@@ -208,7 +207,7 @@ struct afmm_context {
   }
   // CUDA-graph replay of repeated identical device-API calls (graph_call)
   struct GraphKey {
-    int which = -1, dtype = 0, mode = 0, split_k = 0, variant = 0, timing = 0;
+    int which = -1, dtype = 0, mode = 0, split_k = 0, variant = 0, timing = 0, check = 1;
     const void* lhs = nullptr;
     const void* rhs = nullptr;
     void* out = nullptr;
@@ -216,6 +215,7 @@ struct afmm_context {
     cudaStream_t user = nullptr;
     bool operator==(const GraphKey& o) const {
       return which == o.which && dtype == o.dtype && mode == o.mode && split_k == o.split_k &&
+             check == o.check &&
              variant == o.variant && timing == o.timing && lhs == o.lhs && rhs == o.rhs &&
              out == o.out && n == o.n && ld == o.ld && ld_out == o.ld_out && r0 == o.r0 &&
              r1 == o.r1 && user == o.user;
@@ -306,7 +306,7 @@ afmm_status check_options(const afmm_options* o, afmm_error* err) {
     set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: options.mode must be 0 or 1");
     return AFMM_ERR_INVALID_ARGUMENT;
   }
-  if (o->split_k < 0 || o->num_devices < 0 ||
+  if (o->split_k < 0 || o->num_devices < 0 || (o->flags & ~AFMM_FLAG_KERNEL_SEMANTICS) ||
       (o->partition != AFMM_PARTITION_WORK && o->partition != AFMM_PARTITION_ROWS)) {
     set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0,
               "afmm: invalid options (split_k, num_devices or partition)");
@@ -337,6 +337,7 @@ void merge_status(DevStatus* into, const DevStatus& s) {
   into->nonfinite_rhs_inv = std::max(into->nonfinite_rhs_inv, s.nonfinite_rhs_inv);
   into->rep_bad_inv = std::max(into->rep_bad_inv, s.rep_bad_inv);
   into->list_need = std::max(into->list_need, s.list_need);
+  into->rep_nan_inv = std::max(into->rep_nan_inv, s.rep_nan_inv);
   into->additions += s.additions;
   into->zero_skips += s.zero_skips;
 }
@@ -379,6 +380,18 @@ afmm_status decode_status(const DevStatus& s, int which, uint64_t n, const Value
     }
     return AFMM_ERR_DOMAIN;
   }
+  if (s.rep_nan_inv) {
+    // the reference's check passes a NaN rep (both of its tests compare
+    // false), then llround(NaN) asks for ~2^63 sequential adds: it never
+    // finishes, so this is the one input we reject where it does not
+    const uint64_t lin = ~s.rep_nan_inv, i = lin / n, j = lin % n;
+    std::snprintf(buf, sizeof buf,
+                  "%s: %s[%" PRIu64 "][%" PRIu64 "] is NaN (the reference would repeat "
+                  "llround(NaN) ~2^63 times)",
+                  where, opname, i, j);
+    set_error(err, AFMM_ERRKIND_REP_NAN, rep_operand, i, j, rd(rep_operand, i, j), buf);
+    return AFMM_ERR_UNSUPPORTED;
+  }
   if (counts) {
     counts->additions = s.additions;
     counts->multiplications = 0;
@@ -404,7 +417,6 @@ int pick_shape(int variant, uint64_t nrows, uint64_t ncols, size_t elem, int sms
     case kNarrow: return afmm_dev::kShapeNarrow;
     case kWide: return afmm_dev::kShapeWide;
     case kSmall: return afmm_dev::kShapeSmall;
-    case kTiny: return afmm_dev::kShapeTiny;
     default: break;
   }
   const uint64_t cbytes = ncols * elem;
@@ -416,8 +428,6 @@ int pick_shape(int variant, uint64_t nrows, uint64_t ncols, size_t elem, int sms
   // wide tiles need about one wave of CTAs: at n = 1024 fp64 the 128 wide
   // CTAs, trimmed to 148 of 14 rows, run 7% faster than 256 narrow ones)
   if (4 * wide_ctas >= 3 * wide_slots) return afmm_dev::kShapeWide;
-  const uint64_t small_ctas = (nrows + 3) / 4 * ((cbytes + 1023) / 1024);
-  if (small_ctas <= (uint64_t)sms) return afmm_dev::kShapeTiny;
   if (narrow_ctas < (uint64_t)sms) return afmm_dev::kShapeSmall;
   return afmm_dev::kShapeNarrow;
 }
@@ -430,7 +440,6 @@ ShapeGeo shape_geo(int shape) {
   switch (shape) {
     case afmm_dev::kShapeWide: return {4096, afmm_dev::kWideRows, afmm_dev::kWideCtasPerSm};
     case afmm_dev::kShapeSmall: return {1024, 4, 8};
-    case afmm_dev::kShapeTiny: return {1024, 4, 1};
     case afmm_dev::kShapeFast: return {2048, 16, 1};
     default: return {2048, 16, 2};
   }
@@ -558,7 +567,7 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
   auto* rsum = c->vec_k.as<unsigned long long>();
   if (!call.prevalidated)
     afmm_dev::launch_scan_stats<T>(lhs, rhs, ld, n32, call.which == AFMM_CASE_B ? 1 : 0, 0, n32, 0,
-                                   n32, st, nnz, rsum, s);
+                                   n32, st, nnz, rsum, s, call.check_finite ? 1 : 0);
 
   if (call.which == AFMM_CASE_B) {
     // rep = X[i,k] (lhs), bases = Y[k,:] (rhs): B-form directly.
@@ -736,6 +745,7 @@ afmm_status graph_call(afmm_context* c, const Call& call, afmm_error* err) {
   key.dtype = call.dtype;
   key.mode = call.mode;
   key.split_k = call.split_k;
+  key.check = call.check_finite ? 1 : 0;
   key.variant = c->variant;
   key.timing = c->timing ? 1 : 0;
   key.lhs = call.lhs;
@@ -954,6 +964,7 @@ afmm_status host_product_one(int which, const T* lhs, const T* rhs, uint64_t n, 
   call.dtype = sizeof(T) == 8 ? AFMM_F64 : AFMM_F32;
   call.mode = mode;
   call.split_k = opt ? opt->split_k : 0;
+  call.check_finite = !(opt && (opt->flags & AFMM_FLAG_KERNEL_SEMANTICS));
   call.lhs = c->hx.p;
   call.rhs = c->hy.p;
   call.n = n;
@@ -1211,6 +1222,7 @@ afmm_status host_product_multi(int which, const T* lhs, const T* rhs, uint64_t n
     for (int b : devs) ensure_peer_access(a, b);
   const int dtype = sizeof(T) == 8 ? AFMM_F64 : AFMM_F32;
   const int mode = opt->mode;
+  const bool check_finite = !(opt->flags & AFMM_FLAG_KERNEL_SEMANTICS);
   const uint64_t ld = round_up(n, 32);
   const size_t row_bytes = ld * sizeof(T), mat = n * row_bytes;
   T* zmapped = which == AFMM_CASE_B && mode == AFMM_MODE_ORDER_PRESERVING ? mapped_pointer(out)
@@ -1265,7 +1277,7 @@ afmm_status host_product_multi(int which, const T* lhs, const T* rhs, uint64_t n
       afmm_dev::launch_scan_stats<T>(c->hx.as<T>(), c->hy.as<T>(), ld, (uint32_t)n,
                                      which == AFMM_CASE_B ? 1 : 0, (uint32_t)a0, (uint32_t)a1,
                                      (uint32_t)a0, (uint32_t)a1, st, c->vec_k.as<uint32_t>(),
-                                     c->vec_k.as<unsigned long long>(), s);
+                                     c->vec_k.as<unsigned long long>(), s, check_finite ? 1 : 0);
     if (ce == cudaSuccess) ce = cudaEventRecord(ev_a[g], s);
     if (ce != cudaSuccess) fail(ce, "afmm: shard setup");
     bar.wait();  // every chunk's copy and scan is enqueued (events recorded)
@@ -1376,6 +1388,7 @@ afmm_status host_product_multi(int which, const T* lhs, const T* rhs, uint64_t n
     call.dtype = dtype;
     call.mode = mode;
     call.split_k = opt->split_k;
+    call.check_finite = check_finite;
     call.lhs = c->hx.p;
     call.rhs = c->hy.p;
     call.n = n;
@@ -1624,6 +1637,7 @@ afmm_status afmm_product_device(afmm_context* c, int32_t which_case, int32_t dty
     call.dtype = dtype;
     call.mode = options ? options->mode : AFMM_MODE_ORDER_PRESERVING;
     call.split_k = options ? options->split_k : 0;
+    call.check_finite = !(options && (options->flags & AFMM_FLAG_KERNEL_SEMANTICS));
     call.lhs = lhs;
     call.rhs = rhs;
     call.n = n;

@@ -5,7 +5,9 @@
 //
 // Built by `make cpptest` against /root/reference/proj/include (build
 // container only); run on the B200 by tests/test_cpp_dropin.py.
+#include <cmath>
 #include <cstdio>
+#include <limits>
 #include <cstdlib>
 #include <random>
 #include <string>
@@ -173,6 +175,38 @@ int main() {
     CHECK(r.product(0, 0) == 6.f && r.product(0, 1) == 2.f && r.product(1, 0) == 1.5f &&
           r.product(1, 1) == 2.5f);
     CHECK(r.counts.additions == 10 && r.counts.zero_skips == 1);
+  }
+  // matrices built element by element may hold non-finite values: the drop-in
+  // applies only the kernel's checks, like the reference (kernels.hpp:25-43)
+  {
+    DenseMatrix x(3), y(3);
+    x(0, 1) = std::numeric_limits<double>::infinity();
+    x(1, 2) = 2.5;
+    x(2, 0) = -1.0;
+    y(1, 0) = 3; y(2, 2) = -2; y(0, 1) = 1;
+    same_as_reference_a(x, y);  // inf base: computed, Z gets inf
+    CHECK(std::isinf(gpu::afmm_case_a(x, y).product(0, 0)));
+    DenseMatrix bad(3);
+    bad(2, 1) = std::numeric_limits<double>::infinity();
+    const std::string ref_msg = expect_throw<std::domain_error>([&] { afmm_case_a(x, bad); });
+    const std::string gpu_msg = expect_throw<std::domain_error>([&] { gpu::afmm_case_a(x, bad); });
+    CHECK(ref_msg == gpu_msg);
+    CHECK(gpu_msg.find("exceeds the exact integer range") != std::string::npos);
+  }
+  // a rep beyond int32: split into consecutive list entries, same bits
+  {
+    const auto x = from_rows({{0.5, -0.25}, {1e-3, 3.0}});
+    const auto y = from_rows({{1, 2147483653.0}, {-2, 0}});
+    same_as_reference_a(x, y);
+  }
+  // sharded over two contexts of one device (options.devices), same bits
+  {
+    gpu::Options o;
+    o.devices = {0, 0};
+    const auto x = random_integer_matrix(70, -9, 9, 5);
+    const auto y = random_integer_matrix(70, -9, 9, 6);
+    CHECK(gpu::afmm_case_a(x, y, o).product == afmm_case_a(x, y).product);
+    CHECK(gpu::afmm_case_b(x, y, o).counts == afmm_case_b(x, y).counts);
   }
   std::printf("%d checks, %d failures\n", g_checks, g_failures);
   return g_failures == 0 ? 0 : 1;

@@ -78,6 +78,16 @@ def main() -> None:
     stored("a_b16", "a", b16_l, b16_r, "test_kernels.cpp:208-223")
     stored("b_b16", "b", b16_l, b16_r, "test_kernels.cpp:208-223")
 
+    # --- reps beyond int32 (accepted by the reference up to 2^53, kernels.hpp:36-39);
+    # the device splits them into consecutive list entries at the same k --------------
+    huge = float(2 ** 31 + 5)
+    stored("a_rep_2p31_plus_5", "a", [[0.5, -0.25], [1e-3, 3.0]], [[1, huge], [-2, 0]],
+           "kernels.hpp:36-39, 95-104 (|rep| > 2^31 - 1)")
+    stored("b_rep_2p31_plus_5", "b", [[1, -2], [huge, 0]], [[0.5, -0.25], [1e-3, 3.0]],
+           "kernels.hpp:36-39, 95-104 (|rep| > 2^31 - 1)")
+    stored("a_rep_2p31_plus_5_n1", "a", [[-0.375]], [[huge]],
+           "kernels.hpp:36-39 (one list needs 2 entries > n: capacity re-run)")
+
     # --- range / sign / zero edge cases (kernels.hpp:25-43, :95-104) -------------
     big = 2.0 ** 53 + 2.0
     stored("a_out_of_range", "a", np.eye(2), [[1, 0], [big, 2]], "kernels.hpp:36-39")
