@@ -57,6 +57,8 @@ def parse_args():
                         "reassociated split-k within 1e-12/1e-5")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-secondary", action="store_true",
+                   help="skip the other BASELINE configurations' device-resident numbers")
     p.add_argument("--cpu-seconds", type=float, default=12.0,
                    help="target CPU time of one baseline sample")
     return p.parse_args()
@@ -405,6 +407,11 @@ def main():
         e2e = _e2e(args, afmm, dist, torch, world, rank, local, cfg, lhs, rhs, es, job_adds,
                    sharded, L, R, Z)
 
+    # ---- the other BASELINE configurations (device-resident, this GPU) ----
+    secondary = None
+    if rank == 0 and world == 1 and not args.no_secondary and args.n is None:
+        secondary = _secondary(args, afmm, torch, local, {"float32": peak} if es == 4 else {})
+
     # ---- CPU baseline ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -426,6 +433,8 @@ def main():
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks,
         }
+        if secondary is not None:
+            line["secondary_configs"] = secondary
         if world > 1:
             line["config"]["gather"] = (
                 "in-kernel peer stores into rank 0's Z (CUDA IPC mapping, NVLink), one barrier"
@@ -576,6 +585,63 @@ def run_single_process(args):
         c.close()
 
 
+def _secondary(args, afmm, torch, local, peaks):
+    """Every other BASELINE configuration at its full size on this GPU: the
+    same device-resident step (CUDA events, L2 flushed between steps below
+    n = 4096), the repeated-addition kernel's time and its fraction of the
+    measured FP-add peak of its dtype. Reported beside the headline so every
+    configuration has a driver-run number; not part of `value`."""
+    from paper_1308_2400_b200.gen import CONFIGS, make_inputs
+
+    points = [("cfg1", {}), ("cfg2", {})] + [("cfg3", {"d1": d, "mu": m}) for d in (0.1, 0.5, 1.0)
+                                              for m in (1, 4, 16)] + [("cfg4", {})]
+    points = [(name, kw) for name, kw in points
+              if not (name == args.config and (name != "cfg3" or
+                                               (kw["d1"], kw["mu"]) == (args.d1, args.mu)))]
+    dev = torch.device("cuda", local)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    out = {}
+    for name, kw in points:
+        cfg = CONFIGS[name]
+        if cfg.dtype not in peaks:
+            peaks[cfg.dtype] = afmm.fp_add_peak(local, cfg.dtype)[0]
+        lhs, rhs = make_inputs(name, seed=args.seed, **kw)
+        L = torch.from_numpy(lhs).to(dev)
+        R = torch.from_numpy(rhs).to(dev)
+        Z = torch.empty_like(L)
+        ctx = afmm.DeviceContext(local)
+        ctx.enable_timing(True)
+        steps = 10 if cfg.n <= 4096 else 3
+        for _ in range(3):
+            ctx.product(cfg.case, L, R, Z)
+        ms, kms = [], []
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        for _ in range(steps):
+            if cfg.n < 4096:
+                flush.fill_(1.0)
+            torch.cuda.synchronize()
+            e0.record()
+            c = ctx.product(cfg.case, L, R, Z)
+            e1.record()
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+            kms.append(ctx.last_timing()[1])
+        form = ctx.last_form() if cfg.case == "a" else "bform"
+        ctx.close()
+        step = statistics.median(ms)
+        k = statistics.median(kms)
+        key = name if name != "cfg3" else f"cfg3_d{kw['d1']:g}_mu{kw['mu']}"
+        out[key] = {"n": cfg.n, "dtype": "f32" if cfg.dtype == "float32" else "f64",
+                    "case": cfg.case, "additions": c.additions, "steps": steps,
+                    "ms_per_step": step, "value": c.additions / (step * 1e-3),
+                    "frac_of_fp_add_peak": c.additions / (step * 1e-3) / peaks[cfg.dtype],
+                    "kernel_ms": k, "kernel_frac": c.additions / (k * 1e-3) / peaks[cfg.dtype],
+                    "kernel": form}
+        del L, R, Z
+    return out
+
+
 def _e2e(args, afmm, dist, torch, world, rank, local, cfg, lhs, rhs, es, job_adds, sharded, L,
          R, Z):
     """Same metric with pinned host operands copied in and Z copied out every step."""
@@ -589,7 +655,8 @@ def _e2e(args, afmm, dist, torch, world, rank, local, cfg, lhs, rhs, es, job_add
     def step():
         if world == 1:
             # the reference-facing call: afmm_case_{a,b}_{f32,f64}(host ptrs) via the C ABI
-            fn(hl_np, hr_np, device=local, out=hz_np, mode=args.mode)
+            r = fn(hl_np, hr_np, device=local, out=hz_np, mode=args.mode, timing=True)
+            dev_ms.append(r.timing["total_ms"])
         else:
             L.copy_(hl, non_blocking=True)
             R.copy_(hr, non_blocking=True)
@@ -599,8 +666,10 @@ def _e2e(args, afmm, dist, torch, world, rank, local, cfg, lhs, rhs, es, job_add
             torch.cuda.synchronize()
 
     reps = max(1, min(args.steps, 5))
+    dev_ms = []
     for _ in range(1):
         step()
+    dev_ms.clear()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -617,6 +686,7 @@ def _e2e(args, afmm, dist, torch, world, rank, local, cfg, lhs, rhs, es, job_add
     return {"value": job_adds / secs, "unit": UNIT,
             "h2d_bytes_per_step": 2 * n * n * es * world, "d2h_bytes_per_step": n * n * es,
             "ms_per_step": secs * 1e3, "steps": reps,
+            "device_ms_per_step": statistics.median(dev_ms) if dev_ms else None,
             "api": "afmm_case_%s_%s (C ABI, host buffers)" % (cfg.case, "f32" if es == 4 else "f64")
             if world == 1 else "per-rank H2D + row-sharded product (Z slabs into rank 0) + D2H "
                                "on rank 0"}

@@ -225,6 +225,12 @@ afmm_status afmm_model_partition_case_a(int32_t dtype, uint64_t n, int32_t sms,
                                         const uint64_t* stats, const uint32_t* nnz_row,
                                         uint32_t parts, uint64_t* cuts, double* slab_cycles);
 
+/* The modeled kernel time (cycles) of the Case A slab [row_begin, row_end)
+ * under the same statistics: the device-side choice evaluated on the host. */
+afmm_status afmm_model_slab_time_case_a(int32_t dtype, uint64_t n, int32_t sms,
+                                        const uint64_t* stats, const uint32_t* nnz_row,
+                                        uint64_t row_begin, uint64_t row_end, double* cycles);
+
 /* Cut n rows into `parts` contiguous ranges of (as near as possible) equal
  * total work: cuts[0] = 0, cuts[parts] = n, range p = [cuts[p], cuts[p+1]).
  * Pure host function (no device needed). */

@@ -121,6 +121,9 @@ _SIGNATURES = {
     "afmm_model_partition_case_a": (c_int32, [c_int32, c_uint64, c_int32, POINTER(c_uint64),
                                               POINTER(c_uint32), c_uint32, POINTER(c_uint64),
                                               POINTER(c_double)]),
+    "afmm_model_slab_time_case_a": (c_int32, [c_int32, c_uint64, c_int32, POINTER(c_uint64),
+                                              POINTER(c_uint32), c_uint64, c_uint64,
+                                              POINTER(c_double)]),
     "afmm_partition_rows": (c_int32, [POINTER(c_uint64), c_uint64, c_uint32, POINTER(c_uint64)]),
     "afmm_fp_add_peak": (c_int32, [c_int32, c_int32, POINTER(c_double), POINTER(c_double)]),
     "afmm_ipc_export": (c_int32, [c_void_p, POINTER(IpcHandle), POINTER(Error)]),

@@ -425,6 +425,25 @@ def model_partition_case_a(stats, nnz_row, parts: int, dtype: str = "float32",
     return cuts.astype(np.int64), cyc
 
 
+def model_slab_times_case_a(stats, nnz_row, cuts, dtype: str = "float32",
+                            sms: int = 148) -> np.ndarray:
+    """Modeled cycles of each Case A slab [cuts[p], cuts[p+1]) (host only)."""
+    lib = _lib.load()
+    st = np.ascontiguousarray(stats, dtype=np.uint64)
+    nz = np.ascontiguousarray(nnz_row, dtype=np.uint32)
+    out = []
+    for p in range(len(cuts) - 1):
+        c = ctypes.c_double()
+        status = lib.afmm_model_slab_time_case_a(
+            _DT_CODE[dtype], nz.size, int(sms), st.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+            nz.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), int(cuts[p]), int(cuts[p + 1]),
+            ctypes.byref(c))
+        if status != _lib.OK:
+            raise InvalidArgument("afmm_model_slab_time_case_a: invalid arguments")
+        out.append(c.value)
+    return np.array(out)
+
+
 def fp_add_peak(device: int = 0, dtype: str = "float32") -> Tuple[float, float]:
     """Measured CUDA-core FP-add peak (adds/s) and the SM clock it ran at (MHz)."""
     lib = _lib.load()

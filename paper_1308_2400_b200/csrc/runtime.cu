@@ -457,8 +457,9 @@ afmm_dev::CaseAModel case_a_model(size_t elem, uint64_t n, int sms, int shape) {
   md.b_warps_per_cta = g.rows_per_cta;
   md.b_ctas_per_sm = g.ctas_per_sm;
   // cycles per rep step per list entry and B tile: 2 pipe cycles per FADD2 /
-  // DADD warp instruction, tile_bytes / 512 instructions per rep step and row
-  md.b_step = 2.0 * (double)(g.tile_bytes / 512);
+  // DADD warp instruction, 2 instructions per 16-byte column group (G =
+  // tile_bytes / 512 groups per lane): 32 cycles for the wide tile
+  md.b_step = 4.0 * (double)(g.tile_bytes / 512);
   const double scale = (double)g.tile_bytes / 4096.0;  // fitted on the wide shape
   md.b_entry = 56.0 * (scale < 1.0 ? 1.0 : scale);
   md.b_entry_small = 100.0 * (scale < 1.0 ? 1.0 : scale);
@@ -1815,6 +1816,25 @@ afmm_status afmm_model_partition_case_a(int32_t dtype, uint64_t n, int32_t sms,
     md.trip_sum = fs[1];
     md.rep_sum = fs[3];
     partition_case_a(md, nnz_row, fs[2] == 0, cost.data(), parts, cuts, slab_cycles);
+    return AFMM_OK;
+  });
+}
+
+afmm_status afmm_model_slab_time_case_a(int32_t dtype, uint64_t n, int32_t sms,
+                                        const uint64_t* stats, const uint32_t* nnz_row,
+                                        uint64_t row_begin, uint64_t row_end, double* cycles) {
+  if (!stats || !nnz_row || !cycles || n == 0 || row_begin > row_end || row_end > n ||
+      (dtype != AFMM_F64 && dtype != AFMM_F32))
+    return AFMM_ERR_INVALID_ARGUMENT;
+  return guarded([&]() -> afmm_status {
+    const size_t elem = dtype == AFMM_F64 ? 8 : 4;
+    const int s = sms > 0 ? sms : 148;
+    afmm_dev::CaseAModel md = case_a_model(elem, n, s, pick_shape(kAuto, n, n, elem, s));
+    md.nnz_y = stats[0];
+    md.trip_sum = stats[1];
+    md.rep_sum = stats[3];
+    SlabModel sm(md, nnz_row, stats[2] == 0);
+    *cycles = sm.time(row_begin, row_end);
     return AFMM_OK;
   });
 }

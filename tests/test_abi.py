@@ -156,11 +156,14 @@ def test_bench_refuses_more_gpus_than_visible():
 
 def test_case_a_cut_by_modeled_time_balances_sorted_density_rows():
     """cfg4's Case A (per-row densities from Beta(0.5, 0.5)) with the rows
-    SORTED by density, 8 devices: an equal-row cut gives the sparse slabs
-    (A-form, cheap) a fraction of the dense slabs' (B-form) time; the cut by
-    modeled time (the device-side A-form / B-form choice evaluated per slab,
-    tile and wave quantisation included) balances them to max/min <= 1.05.
-    Host-only model query: no device needed."""
+    SORTED by density. The cut by modeled time (the device-side A-form /
+    B-form choice evaluated per slab, tile and wave quantisation included)
+    balances what an equal-row cut leaves lopsided: at 8 devices the slabs'
+    modeled times are within 7% of each other (equal rows: the sparsest slab
+    takes 1/9 of the densest one's time) and at 2 devices the makespan drops.
+    The residual: each dense slab costs one whole B-form tile (1024 rows)
+    whatever its row count, and the sparse slab's A-form time jumps by a wave
+    exactly where it would catch up. Host-only model query."""
     import paper_1308_2400_b200 as afmm
     from paper_1308_2400_b200.gen import make_inputs
 
@@ -168,14 +171,18 @@ def test_case_a_cut_by_modeled_time_balances_sorted_density_rows():
     order = np.argsort((lhs != 0).sum(axis=1), kind="stable")
     lhs = np.ascontiguousarray(lhs[order])
     stats, nnz_row = afmm.case_a_statistics(lhs, rhs)
-    cuts, cyc = afmm.model_partition_case_a(stats, nnz_row, 8)
-    assert cuts[0] == 0 and cuts[-1] == 8192 and np.all(np.diff(cuts) > 0)
-    assert cyc.max() / cyc.min() <= 1.05, (cuts, cyc)
-    # the equal-row cut of the same input is far out of balance
-    eq = np.linspace(0, 8192, 9).astype(np.int64)
-    ws = np.diff(cuts)
-    assert ws[0] > 1.5 * ws[-1]  # sparse slabs get more rows
-    del eq
+    for parts in (8, 2):
+        cuts, cyc = afmm.model_partition_case_a(stats, nnz_row, parts)
+        assert cuts[0] == 0 and cuts[-1] == 8192 and np.all(np.diff(cuts) > 0)
+        assert np.allclose(cyc, afmm.model_slab_times_case_a(stats, nnz_row, cuts))
+        equal = np.linspace(0, 8192, parts + 1).astype(np.int64)
+        t_equal = afmm.model_slab_times_case_a(stats, nnz_row, equal)
+        assert cyc.max() <= t_equal.max() * 1.0001
+        if parts == 8:
+            assert cyc.max() / cyc.min() <= 1.07, (cuts, cyc)
+            assert t_equal.max() / t_equal.min() > 5
+        else:
+            assert cyc.max() < t_equal.max() * 0.99, (cyc, t_equal)
 
 
 def test_case_a_statistics_match_the_closed_forms():
