@@ -52,7 +52,15 @@ clean:
 	rm -rf build $(LIB)
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle clean sass cpptest
+.PHONY: all oracle clean sass cpptest checked
+
+# Checked build (never the product): device bound checks counted into the
+# call status + guard bands around every workspace buffer, verified after each
+# product (compute-sanitizer is closed on this pool). Used by
+# `AFMM_LIB=build/checked/libafmm_b200.so python tools/sanitize_cases.py`.
+checked:
+	@mkdir -p build/checked
+	$(NVCC) $(NVFLAGS) -DAFMM_CHECKED -shared -o build/checked/libafmm_b200.so $(SRCS)
 
 # Kernel timing experiments (never the product): build/exp/<name>/libafmm_b200.so
 # with extra defines, selected at run time through AFMM_LIB.

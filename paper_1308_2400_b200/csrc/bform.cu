@@ -456,6 +456,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
       asm volatile("prefetch.global.L1 [%0];" ::"l"(lp + f + kListPrefetch));
     const uint32_t k = (uint32_t)e.x;
     const uint32_t kb = (k - k_lo) / KB;  // block index within the slice
+    AFMM_CHECK(st, k >= k_lo && kb < nkb && e.y != 0 && (i == 0 || (uint32_t)lp[i - 1].x <= k));
     if constexpr (BLOCKED) {
       if (kb >= flush_kb) {  // the entry starts a new block of the blocked sum
         tot.flush(acc);
@@ -463,6 +464,9 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
       }
     }
     cur.seek(kb, lane);
+    AFMM_CHECK(st, cur.kb_cur == kb && cur.stage_addr >= smem_u32(base) &&
+                       cur.stage_addr + (uint32_t)Gm::STAGE_BYTES <=
+                           smem_u32(base) + (uint32_t)(STAGES * Gm::STAGE_BYTES) + 32u * 16u);
     acc.run(cur.stage_addr + (k % KB) * BOX_BYTES, e.y);
     e = ne;
   }
@@ -472,6 +476,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
     tot.to(acc);
   }
 
+  AFMM_CHECK(st, cur.kb_cur == nkb);
   if (b < nrows) acc.store(out + (uint64_t)b * ld_out, tile_c, ncols, lane, vec_ok != 0);
 }
 
@@ -607,6 +612,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
   // ---- consumers: one Z row per warp ----
   const uint32_t b = warp < rpc ? blockIdx.x * rpc + warp : nrows;
   const uint32_t q = b < nrows ? (row_idx ? row_idx[b] : b) : 0u;  // list / Z row
+  AFMM_CHECK(st, b >= nrows || !row_idx || q < gridDim.x * rpc);
   const uint32_t cnt = b < nrows ? counts[q] : 0u;
   const E* lst = lists + (uint64_t)q * cap;
   T acc[Ag::CPL];
@@ -644,6 +650,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
     const uint32_t rm_n = f < cnt ? __ldg(rm_col + (uint64_t)(uint32_t)ent_n.x * ntiles) : 0u;
     const uint32_t k = (uint32_t)ent.x;
     const uint32_t kb = k / KB;
+    AFMM_CHECK(st, k < nkb * KB && kb >= kb_cur && cnt <= cap);
     while (kb_cur < kb) {
       advance();
       mbar_sleep_wait_at(full0 + slot * 8, phase);

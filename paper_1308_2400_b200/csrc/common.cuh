@@ -29,8 +29,26 @@ struct DevStatus {
   uint32_t a_rows;     // Case A: slab rows the device-side choice gave the A-form
   uint32_t form_rows;  // Case A: slab rows seen by the choice (0: no choice made)
   unsigned long long rep_nan_inv;  // ~(linear index) of the first NaN rep (kernel semantics)
+  // checked build (-DAFMM_CHECKED, `make checked`): bound-check violations
+  // counted by the kernels (AFMM_CHECK); always 0 in the product build
+  unsigned long long check_violations;
+  unsigned long long pad[7];
 };
-static_assert(sizeof(DevStatus) == 64, "DevStatus is one 64-byte record");
+static_assert(sizeof(DevStatus) == 128, "DevStatus is a 128-byte record");
+
+// Bound checks of the checked build (compute-sanitizer is not available on
+// this pool): a violated condition is counted in the call's status (the
+// runtime reports it as an error) instead of faulting the context.
+#ifdef AFMM_CHECKED
+#define AFMM_CHECK(st, cond)                                                              \
+  do {                                                                                    \
+    if (!(cond)) atomicAdd(const_cast<unsigned long long*>(&(st)->check_violations), 1ull); \
+  } while (0)
+#else
+#define AFMM_CHECK(st, cond) \
+  do {                       \
+  } while (0)
+#endif
 
 // A-form list entry: (k, base) of a nonzero base X[i,k] (k_aform).
 template <class T>

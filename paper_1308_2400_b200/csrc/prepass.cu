@@ -610,6 +610,7 @@ __global__ void k_transpose(const T* __restrict__ in, uint64_t ld_in, uint32_t r
     const uint32_t c = c0 + dy, r = r0 + threadIdx.x;
     if (r < rows && c < cols) {
       const uint64_t oc = out_rows ? out_rows[c] : c;
+      if (st) AFMM_CHECK(st, !out_rows || oc < (uint64_t)gridDim.x * 32 + (dyn == 2 ? plan[0] : 0));
       out[oc * ld_out + r] = tile[threadIdx.x][dy];
     }
   }

@@ -75,6 +75,16 @@ int sm_count(int device) {
   return sms;
 }
 
+// Guard bands of the checked build: every workspace allocation is framed by
+// kGuard bytes of a known pattern, verified after each product (an
+// out-of-bounds write by a library kernel into a neighbouring allocation).
+#ifdef AFMM_CHECKED
+constexpr size_t kGuard = 4096;
+#else
+constexpr size_t kGuard = 0;
+#endif
+constexpr unsigned char kGuardByte = 0xA5;
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -83,24 +93,40 @@ struct DevBuf {
   cudaError_t ensure(size_t want) {
     if (want <= bytes) return cudaSuccess;
     if (gen) ++*gen;  // captured graphs hold the old addresses
-    if (p) {
-      cudaFree(p);  // implicit device sync
-      p = nullptr;
-      bytes = 0;
-    }
+    release();
     want = std::max<size_t>(want, 256);
-    cudaError_t e = cudaMalloc(&p, want);
-    if (e != cudaSuccess) {
-      p = nullptr;
-      return e;
+    void* raw = nullptr;
+    cudaError_t e = cudaMalloc(&raw, want + 2 * kGuard);
+    if (e != cudaSuccess) return e;
+    if (kGuard) {
+      e = cudaMemset(raw, kGuardByte, kGuard);
+      if (e == cudaSuccess) e = cudaMemset(static_cast<char*>(raw) + kGuard + want, kGuardByte, kGuard);
+      if (e != cudaSuccess) {
+        cudaFree(raw);
+        return e;
+      }
     }
+    p = static_cast<char*>(raw) + kGuard;
     bytes = want;
     return cudaSuccess;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) cudaFree(static_cast<char*>(p) - kGuard);  // implicit device sync
     p = nullptr;
     bytes = 0;
+  }
+  // checked build: are both guard bands intact?
+  bool guards_intact() const {
+    if (!kGuard || !p) return true;
+    std::vector<unsigned char> g(2 * kGuard);
+    if (cudaMemcpy(g.data(), static_cast<char*>(p) - kGuard, kGuard, cudaMemcpyDeviceToHost) !=
+            cudaSuccess ||
+        cudaMemcpy(g.data() + kGuard, static_cast<char*>(p) + bytes, kGuard,
+                   cudaMemcpyDeviceToHost) != cudaSuccess)
+      return false;
+    for (unsigned char b : g)
+      if (b != kGuardByte) return false;
+    return true;
   }
   template <class U>
   U* as() const {
@@ -338,6 +364,7 @@ void merge_status(DevStatus* into, const DevStatus& s) {
   into->rep_bad_inv = std::max(into->rep_bad_inv, s.rep_bad_inv);
   into->list_need = std::max(into->list_need, s.list_need);
   into->rep_nan_inv = std::max(into->rep_nan_inv, s.rep_nan_inv);
+  into->check_violations += s.check_violations;
   into->additions += s.additions;
   into->zero_skips += s.zero_skips;
 }
@@ -711,6 +738,21 @@ afmm_status finish_locked(afmm_context* c, afmm_op_counts* counts, afmm_error* e
   const DevStatus s = *c->status_host;
   if (s.form_rows) c->last_form = s.a_rows == 0 ? 0 : (s.a_rows == s.form_rows ? 1 : 2);
   else if (c->last.which == AFMM_CASE_A) c->last_form = 0;
+#ifdef AFMM_CHECKED
+  {
+    int bad_guards = 0;
+    for (DevBuf* b : all_bufs(c)) bad_guards += b->guards_intact() ? 0 : 1;
+    if (s.check_violations || bad_guards) {
+      char buf[256];
+      std::snprintf(buf, sizeof buf,
+                    "afmm (checked build): %llu device bound-check violations, %d workspace "
+                    "guard bands overwritten",
+                    (unsigned long long)s.check_violations, bad_guards);
+      set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, buf);
+      return AFMM_ERR_CUDA;
+    }
+  }
+#endif
   const afmm_status st = decode_status(s, c->last.which, c->last.n, device_reader(c->last),
                                        counts, err);
   if (st != AFMM_OK || s.list_need == 0) return st;

@@ -958,3 +958,52 @@ def test_kernel_semantics_non_finite_bases_and_reps(cuda, oracle, case, dt):
     args = (lhs, r) if case == "a" else (r, rhs)
     with pytest.raises(afmm.UnsupportedError, match=r"\[40\]\[9\] is NaN"):
         _call(case, *args, kernel_semantics=True)
+
+
+@pytest.mark.parametrize("variant", [None, "wide", "ring", "small", "aform", "hybrid"])
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_no_write_outside_the_output(cuda, oracle, monkeypatch, variant, dt):
+    """Every kernel path writes exactly its output slab: `out` is a view into a
+    larger buffer filled with a sentinel (offset rows and columns, padded
+    leading dimension) and every byte around it must survive, in both cases,
+    order-preserving and fast mode; and the page-locked zero-copy output of
+    the host call leaves the rows around it alone. (compute-sanitizer is
+    closed on this pool: this, the checked build's bound checks and guard
+    bands -- tools/sanitize_cases.py -- stand in for memcheck.)"""
+    import torch
+
+    if variant:
+        monkeypatch.setenv("AFMM_BFORM", variant)
+    else:
+        monkeypatch.delenv("AFMM_BFORM", raising=False)
+    afmm = _api()
+    tdt = torch.float32 if dt == np.float32 else torch.float64
+    rng = np.random.default_rng(33)
+    n = 1100 if variant in ("aform", "hybrid", None) else 333
+    bases = rng.standard_normal((n, n)) * (rng.random((n, n)) < 0.3)
+    reps = rng.integers(-5, 6, (n, n)).astype(np.float64)
+    bases, reps = bases.astype(dt), reps.astype(dt)
+    sentinel = -12345.5
+    ctx = afmm.DeviceContext(0)
+    for case, lhs, rhs in (("a", bases, reps), ("b", reps, bases)):
+        if variant in ("aform", "hybrid") and case == "b":
+            continue
+        L = torch.from_numpy(lhs).cuda()
+        R = torch.from_numpy(rhs).cuda()
+        for mode in ("order-preserving", "fast"):
+            r0, r1 = 17, n - 5
+            big = torch.full((r1 - r0 + 9, n + 40), sentinel, dtype=tdt, device="cuda")
+            view = big[4:4 + r1 - r0, 16:16 + n]
+            ctx.product(case, L, R, view, r0, r1, mode=mode)
+            b = big.cpu().numpy()
+            inside = np.zeros(b.shape, dtype=bool)
+            inside[4:4 + r1 - r0, 16:16 + n] = True
+            assert np.all(b[~inside] == sentinel), (case, mode, variant)
+            if mode == "order-preserving":
+                z, _ = oracle.product_mt(case, lhs, rhs, r0, r1, 16)
+                assert _bits_equal(b[4:4 + r1 - r0, 16:16 + n], z), (case, variant)
+    ctx.close()
+    if variant is None:
+        pinned = torch.full((n + 4, n), sentinel, dtype=tdt).pin_memory().numpy()
+        afmm.afmm_case_b(reps, bases, out=pinned[2:2 + n])
+        assert np.all(pinned[:2] == sentinel) and np.all(pinned[2 + n:] == sentinel)
