@@ -651,6 +651,16 @@ def _e2e(args, afmm, dist, torch, world, rank, local, cfg, lhs, rhs, es, job_add
     hz = torch.empty((n, n), dtype=hl.dtype).pin_memory()
     hl_np, hr_np, hz_np = hl.numpy(), hr.numpy(), hz.numpy()
     fn = afmm.afmm_case_a if cfg.case == "a" else afmm.afmm_case_b
+    if world > 1:
+        from paper_1308_2400_b200.distributed import ShardedProduct
+
+        nccl = os.environ.get("AFMM_DIST_BACKEND", "nccl") == "nccl"
+        chunk = (n + world - 1) // world
+        c0, c1 = min(n, rank * chunk), min(n, (rank + 1) * chunk)
+        Lp = torch.zeros((world * chunk, n), dtype=L.dtype, device=L.device)
+        Rp = torch.zeros((world * chunk, n), dtype=R.dtype, device=R.device)
+        S = torch.empty((n, n), dtype=L.dtype, device=L.device)
+        local = ShardedProduct(sharded.ctx, dist, rank, world, gather="none")
 
     def step():
         if world == 1:
@@ -658,11 +668,24 @@ def _e2e(args, afmm, dist, torch, world, rank, local, cfg, lhs, rhs, es, job_add
             r = fn(hl_np, hr_np, device=local, out=hz_np, mode=args.mode, timing=True)
             dev_ms.append(r.timing["total_ms"])
         else:
-            L.copy_(hl, non_blocking=True)
-            R.copy_(hr, non_blocking=True)
-            sharded.run(cfg.case, L, R, Z, Z, mode=args.mode)
-            if rank == 0:
-                hz.copy_(Z, non_blocking=True)
+            # each rank: H2D of its 1/world row chunk of X and Y, all-gather
+            # over NCCL (NVLink), its row slab, D2H of that slab
+            if nccl:
+                Lp[c0:c1].copy_(hl[c0:c1], non_blocking=True)
+                Rp[c0:c1].copy_(hr[c0:c1], non_blocking=True)
+                dist.all_gather_into_tensor(Lp, Lp[c0:c1].clone())
+                dist.all_gather_into_tensor(Rp, Rp[c0:c1].clone())
+            else:  # gloo (functional test): gather host chunks, then one copy
+                for src, dst in ((hl, Lp), (hr, Rp)):
+                    parts = [torch.empty_like(torch.zeros(chunk, n, dtype=src.dtype))
+                             for _ in range(world)]
+                    mine = torch.zeros(chunk, n, dtype=src.dtype)
+                    mine[: c1 - c0] = src[c0:c1]
+                    dist.all_gather(parts, mine)
+                    dst.copy_(torch.cat(parts))
+            local.run(cfg.case, Lp[:n], Rp[:n], None, S, mode=args.mode)
+            r0, r1 = int(local.cuts[rank]), int(local.cuts[rank + 1])
+            hz[r0:r1].copy_(S[: r1 - r0], non_blocking=True)
             torch.cuda.synchronize()
 
     reps = max(1, min(args.steps, 5))
@@ -684,12 +707,12 @@ def _e2e(args, afmm, dist, torch, world, rank, local, cfg, lhs, rhs, es, job_add
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         secs = float(t[0])
     return {"value": job_adds / secs, "unit": UNIT,
-            "h2d_bytes_per_step": 2 * n * n * es * world, "d2h_bytes_per_step": n * n * es,
+            "h2d_bytes_per_step": 2 * n * n * es, "d2h_bytes_per_step": n * n * es,
             "ms_per_step": secs * 1e3, "steps": reps,
             "device_ms_per_step": statistics.median(dev_ms) if dev_ms else None,
             "api": "afmm_case_%s_%s (C ABI, host buffers)" % (cfg.case, "f32" if es == 4 else "f64")
-            if world == 1 else "per-rank H2D + row-sharded product (Z slabs into rank 0) + D2H "
-                               "on rank 0"}
+            if world == 1 else "per rank: H2D of its 1/N row chunk of X and Y, NCCL all-gather, "
+                               "its row slab (cut by predicted time), D2H of the slab"}
 
 
 def _hbm_check(traffic):

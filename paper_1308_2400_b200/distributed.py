@@ -134,6 +134,9 @@ class ShardedProduct:
         self.rank = rank
         self.world = world
         self.cuts: Optional[np.ndarray] = None
+        # "p2p": kernels store into rank 0's Z over CUDA IPC; "sendrecv": NCCL
+        # gather after the compute; "none": each rank keeps its slab (rows
+        # cuts[rank]..cuts[rank+1] in slab_buf), e.g. to copy it to its host
         self.gather = gather or os.environ.get("AFMM_GATHER", "p2p")
         self.used_p2p = False
         self._peer = PeerResult(dist, rank, getattr(ctx, "device", 0)) if world > 1 and \
@@ -151,6 +154,9 @@ class ShardedProduct:
         cuts = self.ctx.partition(case, lhs, rhs, self.world)
         self.cuts = cuts
         r0, r1 = int(cuts[self.rank]), int(cuts[self.rank + 1])
+        if self.gather == "none":
+            return self.ctx.product(case, lhs, rhs, slab_buf[: max(r1 - r0, 1)], r0, r1,
+                                    mode=mode)
         ok, peer, ld = self._peer.exchange(z_full) if self._peer else (False, None, 0)
         self.used_p2p = ok
         if ok:
