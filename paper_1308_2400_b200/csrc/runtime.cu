@@ -632,8 +632,12 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
     using E = typename afmm_dev::AEntry<T>::type;
     const uint32_t tc = afmm_dev::aform_tile_cols<T>();
     const uint64_t ntiles = (n + tc - 1) / tc, ldc = round_up(n, 64);
-    const bool choose = rows > 0 && (c->variant == kAForm || c->variant == kHybrid ||
-                                     (c->variant == kAuto && n >= 1024));
+    // (fast mode keeps the B-form: its blocked fp64 totals bound the fp32 chain
+    // error, §3.2; the A-form's chains are the order-preserving ones, and on
+    // sparse rows of n = 8192 they drift to 2.6e-5 of sum |terms|)
+    const bool choose = rows > 0 && call.mode != AFMM_MODE_FAST &&
+                        (c->variant == kAForm || c->variant == kHybrid ||
+                         (c->variant == kAuto && n >= 1024));
     // B part: B-form rows = Z columns j (rep list = column j of Y), B-form
     // columns = the slab's B rows (bases X[i,k], gathered through ridx)
     const int shape = pick_shape(c->variant, n, std::max<uint64_t>(rows, 1), sizeof(T), sms);
