@@ -16,7 +16,8 @@ REF_INC ?= /root/reference/proj/include
 
 all: $(LIB) oracle $(if $(wildcard $(REF_INC)/afmm/kernels.hpp),cpptest)
 
-build/%.o: $(CSRC)/%.cu $(CSRC)/common.cuh $(CSRC)/kernels.h include/afmm_b200.h
+build/%.o: $(CSRC)/%.cu $(CSRC)/common.cuh $(CSRC)/kernels.h $(CSRC)/costmodel.h \
+           $(CSRC)/jumptable.inc include/afmm_b200.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c -o $@ $<
 

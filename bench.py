@@ -381,13 +381,13 @@ def main():
     achieved = rank_adds / (kms * 1e-3)
     traffic = _ncu_traffic(args.config if args.config != "cfg3"
                            else f"cfg3_d{args.d1:g}_mu{args.mu}")
-    form = ctx.last_form() if cfg.case == "a" else "bform"
+    form = ctx.last_form()
     roofline = {
         "bound": "fp-add",
         "bound_detail": "CUDA-core FP add issue (FADD2/DADD; FADD under predicates in the "
                         "A-form): no tensor cores (they would multiply), far right of the HBM "
                         "ridge",
-        "kernel": {"aform": "k_aform", "split": "k_aform+k_bform"}.get(form, "k_bform"),
+        "kernel": afmm.FORM_KERNELS.get(form, "k_bform"),
         "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
         "unit_note": "FLOP = one FP add (fp32 FADD2 lanes / fp64 DADD); the kernel does no "
                      "multiplications, so FP-add/s is its FLOP/s",
@@ -537,7 +537,7 @@ def run_single_process(args):
     kms = statistics.median(kernel_ms)
     rank0_adds = int(counts[0].additions)
     roofline = {
-        "bound": "fp-add", "kernel": "k_bform" if cfg.case == "b" else ctxs[0].last_form(),
+        "bound": "fp-add", "kernel": afmm.FORM_KERNELS.get(ctxs[0].last_form(), "k_bform"),
         "achieved": rank0_adds / (kms * 1e-3) / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
         "unit_note": "FLOP = one FP add; GPU 0's repeated-addition kernel on its row share",
         "frac": rank0_adds / (kms * 1e-3) / peak,
@@ -627,7 +627,7 @@ def _secondary(args, afmm, torch, local, peaks):
             torch.cuda.synchronize()
             ms.append(e0.elapsed_time(e1))
             kms.append(ctx.last_timing()[1])
-        form = ctx.last_form() if cfg.case == "a" else "bform"
+        form = ctx.last_form()
         ctx.close()
         step = statistics.median(ms)
         k = statistics.median(kms)

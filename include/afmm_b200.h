@@ -91,7 +91,7 @@ typedef struct {
   float total_ms;    /* first host->device copy to the last device->host byte */
   float compute_ms;  /* the repeated-addition kernel(s) */
   int32_t devices;   /* devices the call ran on */
-  int32_t form;      /* Case A kernel form of device 0: 0 B-form, 1 A-form, 2 split */
+  int32_t form;      /* kernel form of device 0 (afmm_context_last_form codes) */
 } afmm_timing;
 
 /* The operands are already-constructed matrices (the C++ wrapper's
@@ -185,8 +185,10 @@ afmm_status afmm_context_last_timing(afmm_context* ctx, float* prepass_ms, float
 /* Repeated-addition kernel of the context's last product: 0 = B-form
  * (k_bform: rep uniform per warp; Case B directly, Case A on transposed
  * operands), 1 = A-form (k_aform: Case A with the base uniform per warp,
- * chosen for sparse X), 2 = Case A rows split between the two (the sparsest
- * rows in the A-form). */
+ * zero bases skipped), 2 = split (Case A: the sparsest rows in the A-form,
+ * the rest in the B-form); + 4 when the B-form part ran the small-rep group
+ * kernel (k_bgroup: fp32, order-preserving, every rep in 0..2; chosen on the
+ * device), i.e. 4 = Case B or Case A B-form, 6 = split. */
 int32_t afmm_context_last_form(afmm_context* ctx);
 
 /* Per-row work W_i (exact additions of Z row i) for the row partition:

@@ -169,7 +169,7 @@ def _product(which: int, lhs, rhs, mode: str, device: Optional[int], dtype,
     t = None
     if tm is not None:
         t = {"total_ms": tm.total_ms, "compute_ms": tm.compute_ms, "devices": tm.devices,
-             "form": {1: "aform", 2: "split"}.get(tm.form, "bform")}
+             "form": FORMS.get(tm.form, "bform")}
     return MultiplyResult(out, OpCounts(*counts.as_tuple()), t)
 
 
@@ -237,6 +237,13 @@ def _tensor_info(t, device: Optional[int] = None, what: str = "operand") -> Tupl
     if name not in _DT_CODE:
         raise InvalidArgument(f"afmm: unsupported dtype {t.dtype}")
     return t.data_ptr(), t.stride(0), name, t.shape[1]
+
+
+# afmm_context_last_form codes (include/afmm_b200.h)
+FORMS = {0: "bform", 1: "aform", 2: "split", 4: "group", 6: "split-group"}
+# the repeated-addition kernel(s) behind each form (bench lines, profiles)
+FORM_KERNELS = {"bform": "k_bform", "aform": "k_aform", "split": "k_aform+k_bform",
+                "group": "k_bgroup", "split-group": "k_aform+k_bgroup"}
 
 
 class DeviceContext:
@@ -326,9 +333,10 @@ class DeviceContext:
 
     def last_form(self) -> str:
         """Kernel(s) of the last product: "bform" (rep uniform per warp), "aform"
-        (Case A, base uniform per warp) or "split" (Case A rows divided between
-        the two)."""
-        return {1: "aform", 2: "split"}.get(self._lib.afmm_context_last_form(self._h), "bform")
+        (Case A, base uniform per warp), "split" (Case A rows divided between
+        the two), "group" / "split-group" (the B-form part ran the small-rep
+        group kernel k_bgroup: fp32, every rep in 0..2)."""
+        return FORMS.get(self._lib.afmm_context_last_form(self._h), "bform")
 
     def finish(self) -> OpCounts:
         counts = _lib.OpCounts()

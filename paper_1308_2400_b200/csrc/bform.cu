@@ -372,7 +372,8 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
             uint64_t cap, const uint32_t* __restrict__ counts, uint32_t nrows, uint32_t rpc,
             int32_t col0, int32_t ncols, const uint32_t* __restrict__ dyn_ncols,
             uint32_t nkb_total, uint32_t slice_blocks, uint64_t slice_stride,
-            T* __restrict__ out, uint64_t ld_out, int vec_ok, const DevStatus* __restrict__ st) {
+            T* __restrict__ out, uint64_t ld_out, int vec_ok, const DevStatus* __restrict__ st,
+            int group_allow) {
   using Gm = Geo<T, G>;
   extern __shared__ unsigned char smem_raw[];
   // 128-byte aligned ring (TMA destination without swizzle); pointer arithmetic
@@ -383,6 +384,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
   uint64_t* empty = full + STAGES;
 
   if (status_failed(st)) return;  // validation failed: compute nothing (kernels.hpp:115,144)
+  if (group_mode(st, group_allow)) return;  // the small-rep group kernel runs instead
   const int32_t tile_c = blockIdx.y * Gm::TILE_N;  // relative to col0
   if (dyn_ncols) {
     ncols = (int32_t)*dyn_ncols;
@@ -718,6 +720,127 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_bgroup: the small-rep B-form (every |rep| <= kGroupMaxRep, none negative;
+// decided on the device, group_mode()).
+//
+// k_bform loads a warp's bases from shared memory once per list entry: at rep
+// 1 that is 4 bytes of smem per add against the SM's 1 byte per add of smem
+// bandwidth per FP add (128 B/clk vs 128 adds/clk), so rep 1-2 rows run at
+// 25-45% of the FP-add peak whatever the rest of the kernel does. Here a warp
+// owns a GROUP of kGroupRows = 5 B-form rows over 512 columns (40 float2
+// accumulators per lane) and walks k densely: per k it loads the 512 staged
+// bases once (4 LDS.128 per lane) and applies them to all five rows. The
+// rows' rep magnitudes at k arrive as one u16 index (gidx, built by
+// k_group_idx_rows / _cols): two `brx.idx` jumps (rows 0-2: 27 targets, rows
+// 3-4: 9 targets; tools/gen_jumptable.py) into straight-line blocks of
+// FADD2 steps replace five data-dependent rep loops. Each element still gets
+// its |rep| sequential adds at its k, k ascending (kernels.hpp:95-104): the
+// reference's order, bit for bit. Zero bases add +/-0 as in k_bform.
+// Measured (tools/group_proto.cu, n = 4096, reps uniform {0,1,2}): 0.50 of
+// the FP-add peak against 0.33 for k_bform; constant rep 1: 0.52 vs 0.23.
+// ---------------------------------------------------------------------------
+#include "jumptable.inc"
+
+__device__ __forceinline__ void lds128u64(uint32_t addr, unsigned long long& a,
+                                          unsigned long long& b) {
+  asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "r"(addr));
+}
+
+template <int CW, int STAGES>
+__global__ void __launch_bounds__((CW + 1) * 32, 1)
+    k_bgroup(const __grid_constant__ CUtensorMap tmap, const uint16_t* __restrict__ gidx,
+             uint64_t ldg, uint32_t nrows, uint32_t gpc, int32_t ncols,
+             const uint32_t* __restrict__ dyn_ncols, uint32_t nkb, float* __restrict__ out,
+             uint64_t ld_out, int vec_ok, const DevStatus* __restrict__ st, int allow) {
+  using Gm = Geo<float, 4>;  // 512 columns, KB x 2 KB stages
+  constexpr int NV = 8;      // float2 operands per lane and row
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + STAGES * Gm::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  if (status_failed(st) || !group_mode(st, allow)) return;
+  const int32_t tile_c = blockIdx.y * Gm::TILE_N;
+  if (dyn_ncols) {
+    ncols = (int32_t)*dyn_ncols;
+    if (tile_c >= ncols) return;
+  }
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CW);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp == CW) {
+    if (lane == 0)
+      produce<Gm::STAGE_BYTES, Gm::NBOX, Gm::BOX_N, STAGES>(&tmap, base, full, empty, tile_c, 0u,
+                                                            nkb);
+    return;
+  }
+  const uint32_t ngroups = (nrows + kGroupRows - 1) / kGroupRows;
+  const uint32_t g = warp < gpc ? blockIdx.x * gpc + warp : ngroups;
+  const bool active = g < ngroups;
+  const uint4* __restrict__ gp =
+      reinterpret_cast<const uint4*>(gidx + (uint64_t)(active ? g : 0) * ldg);
+  unsigned long long acc[kGroupRows * NV];
+#pragma unroll
+  for (int i = 0; i < kGroupRows * NV; ++i) acc[i] = 0ull;
+  Cursor<STAGES, Gm::STAGE_BYTES> cur(smem_u32(base), smem_u32(full), smem_u32(empty), lane);
+  cur.wait();
+  // one uniform 16-byte load = the group's indices of a whole k block
+  uint4 w = active ? __ldg(gp) : make_uint4(0u, 0u, 0u, 0u);
+  for (uint32_t kb = 0; kb < nkb; ++kb) {
+    const uint4 nw = (active && kb + 1 < nkb) ? __ldg(gp + kb + 1) : make_uint4(0u, 0u, 0u, 0u);
+    if (active && kb + 16 < nkb) asm volatile("prefetch.global.L1 [%0];" ::"l"(gp + kb + 16));
+    unsigned long long lo = ((unsigned long long)w.y << 32) | w.x;
+    unsigned long long hi = ((unsigned long long)w.w << 32) | w.z;
+    if ((lo | hi) != 0ull) {
+#pragma unroll 1
+      for (int kk = 0; kk < KB; ++kk) {
+        const uint32_t idx = (uint32_t)lo & 0xffffu;
+        lo = (lo >> 16) | (hi << 48);
+        hi >>= 16;
+        if (idx == 0u) continue;
+        AFMM_CHECK(st, (idx & 0xffu) < 27u && (idx >> 8) < 9u);
+        const uint32_t ra = cur.stage_addr + (uint32_t)kk * BOX_BYTES;
+        unsigned long long b[NV];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) lds128u64(ra + group_off(q), b[2 * q], b[2 * q + 1]);
+        jt_apply<3, 2, NV>(*reinterpret_cast<unsigned long long(*)[3 * NV]>(acc), b, idx & 0xffu);
+        jt_apply<2, 2, NV>(*reinterpret_cast<unsigned long long(*)[2 * NV]>(acc + 3 * NV), b,
+                           idx >> 8);
+      }
+    }
+    w = nw;
+    cur.advance(lane);
+    if (kb + 1 < nkb) cur.wait();
+  }
+  if (!active) return;
+#pragma unroll
+  for (int r = 0; r < kGroupRows; ++r) {
+    const uint32_t row = g * kGroupRows + r;
+    if (row >= nrows) break;
+    float* orow = out + (uint64_t)row * ld_out;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int32_t c = tile_c + (q >> 1) * 256 + (q & 1) * 128 + 4 * (int32_t)lane;
+      const unsigned long long x = acc[r * NV + 2 * q], y = acc[r * NV + 2 * q + 1];
+      const float v[4] = {__uint_as_float((uint32_t)x), __uint_as_float((uint32_t)(x >> 32)),
+                          __uint_as_float((uint32_t)y), __uint_as_float((uint32_t)(y >> 32))};
+      if (vec_ok && c + 3 < ncols) {
+        *reinterpret_cast<float4*>(orow + c) = make_float4(v[0], v[1], v[2], v[3]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (c + e < ncols) orow[c + e] = v[e];
+      }
+    }
+  }
+}
+
 template <class T, int G, int CW, int STAGES, int MINB, bool BLOCKED = false>
 cudaError_t launch_ring(BformLaunch& a, T* out, cudaStream_t s) {
   const uint32_t nkb = (a.nk + KB - 1) / KB;
@@ -740,7 +863,7 @@ cudaError_t launch_ring(BformLaunch& a, T* out, cudaStream_t s) {
   dim3 grid((a.nrows + rpc - 1) / rpc, tiles, a.splits);
   kern<<<grid, (CW + 1) * 32, smem, s>>>(*a.tmap, a.lists, a.cap, a.counts, a.nrows, rpc, a.col0,
                                          a.ncols, a.dyn_ncols, nkb, slice_blocks, a.slice_stride,
-                                         out, a.ld_out, vec_ok ? 1 : 0, a.st);
+                                         out, a.ld_out, vec_ok ? 1 : 0, a.st, a.group_allow);
   note_launch();
   return cudaGetLastError();
 }
@@ -772,6 +895,32 @@ cudaError_t launch_bform(BformLaunch& a, T* out, cudaStream_t s) {
 
 template cudaError_t launch_bform<float>(BformLaunch&, float*, cudaStream_t);
 template cudaError_t launch_bform<double>(BformLaunch&, double*, cudaStream_t);
+
+cudaError_t launch_bgroup(const CUtensorMap* tmap, const uint16_t* gidx, uint64_t ldg,
+                          uint32_t nrows, int32_t ncols, const uint32_t* dyn_ncols, uint32_t nk,
+                          float* out, uint64_t ld_out, const DevStatus* st, int allow,
+                          cudaStream_t s) {
+  // 15 consumer warps (121 registers: the 16-warp CTA's 128-register budget)
+  // + the TMA warp, 12-stage ring (192 KB), 1 CTA per SM
+  constexpr int CW = kGroupWarps, STAGES = 12;
+  using Gm = Geo<float, 4>;
+  auto kern = k_bgroup<CW, STAGES>;
+  const size_t smem = ring_smem_bytes<float, 4, STAGES>();
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  const uint32_t nkb = (nk + KB - 1) / KB;
+  const uint32_t tiles = (uint32_t)((ncols + Gm::TILE_N - 1) / Gm::TILE_N);
+  const uint32_t ngroups = (nrows + kGroupRows - 1) / kGroupRows;
+  if (tiles == 0 || ngroups == 0) return cudaSuccess;
+  const uint32_t gpc = balanced_rows(ngroups, tiles, CW, 1);
+  const bool vec_ok = (ld_out * sizeof(float)) % 16 == 0 && (reinterpret_cast<uintptr_t>(out) % 16) == 0;
+  dim3 grid((ngroups + gpc - 1) / gpc, tiles);
+  kern<<<grid, (CW + 1) * 32, smem, s>>>(*tmap, gidx, ldg, nrows, gpc, ncols, dyn_ncols, nkb, out,
+                                         ld_out, vec_ok ? 1 : 0, st, allow);
+  note_launch();
+  return cudaGetLastError();
+}
 
 template <class T>
 cudaError_t launch_aform(const CUtensorMap* cmap, const typename AEntry<T>::type* lists,

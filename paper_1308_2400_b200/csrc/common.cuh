@@ -32,7 +32,12 @@ struct DevStatus {
   // checked build (-DAFMM_CHECKED, `make checked`): bound-check violations
   // counted by the kernels (AFMM_CHECK); always 0 in the product build
   unsigned long long check_violations;
-  unsigned long long pad[7];
+  // Rep statistics for the small-rep group kernel (k_bgroup): the largest
+  // |rep| of the rep operand (saturated at 255) and whether any rep is
+  // negative. Both are reduced over every shard of a multi-device call.
+  uint32_t rep_max;
+  uint32_t rep_neg;
+  unsigned long long pad[6];
 };
 static_assert(sizeof(DevStatus) == 128, "DevStatus is a 128-byte record");
 
@@ -66,6 +71,19 @@ struct AEntry<double> {
 __device__ __forceinline__ bool status_failed(const DevStatus* st) {
   return (st->nonfinite_lhs_inv | st->nonfinite_rhs_inv | st->rep_bad_inv | st->list_need |
           st->rep_nan_inv) != 0ull;
+}
+
+// Largest |rep| (and no negative rep) the group kernel takes: its jump tables
+// cover reps 0..kGroupMaxRep (tools/gen_jumptable.py).
+constexpr uint32_t kGroupMaxRep = 2;
+constexpr int kGroupRows = 5;  // B-form rows per group (one warp)
+
+// The product runs the small-rep group kernel (k_bgroup) instead of k_bform:
+// decided on the device from the validated rep statistics, so the choice needs
+// no host round trip. `allow` is the host's half (fp32, order-preserving mode,
+// no forced k_bform shape).
+__device__ __forceinline__ bool group_mode(const DevStatus* st, int allow) {
+  return allow && st->rep_max <= kGroupMaxRep && st->rep_neg == 0;
 }
 
 // kernels.hpp:31-40 on the widened value: 0 ok, 1 not integer-valued,

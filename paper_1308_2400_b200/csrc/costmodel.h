@@ -18,7 +18,10 @@
 //           tile's max |rep| at its k (mean R = trip_sum / (n x tiles)).
 //   B-form: per B tile, b_step cycles per rep step per list entry + an entry
 //           overhead (larger when the mean rep is below 3: the smem-bound
-//           regime), over all of Y's nonzero reps.
+//           regime), over all of Y's nonzero reps; in group mode (k_bgroup,
+//           reps <= 2) 16 cycles per rep step and row + 78 per nonempty
+//           (group of 5 rows, k), per 512-row tile (fitted on constant reps 1
+//           and 2 at n = 4096: 3.59 and 5.37 ms).
 #pragma once
 
 #include <stdint.h>
@@ -46,6 +49,16 @@ struct CaseAModel {
   double b_step = 32.0;         // cycles per rep step per list entry and tile
   double b_entry = 56.0;        // cycles per list entry and tile (mean rep >= 3)
   double b_entry_small = 100.0; // the same when the mean rep is below 3
+  // Group kernel (k_bgroup: every |rep| <= 2, none negative, fp32): the B part
+  // runs 5 B-form rows per warp over 512-column tiles. group_allow is the
+  // host's half of the decision, group the device's (group_mode in k_choose,
+  // or the merged status of a multi-device call).
+  int group_allow = 0;
+  bool group = false;
+  uint32_t g_tile = 512;       // slab rows per k_bgroup tile
+  uint32_t g_warps_per_cta = 15;
+  double g_step = 16.0;        // cycles per rep step per B-form row and tile (8 FADD2)
+  double g_entry = 78.0;       // cycles per nonempty (group, k) and tile
   // A-form launch geometry
   uint32_t a_tile = 1024;   // columns per A-form CTA (aform_tile_cols)
   uint32_t a_rows_per_cta = 16;
@@ -59,9 +72,19 @@ struct CaseAModel {
     const double it = elem == 4 ? 54.0 : 45.0;
     return tiles * (75.0 + it * rmean);
   }
+  // B-form slab rows per tile
+  AFMM_HD uint64_t tile_rows() const { return group ? g_tile : b_tile; }
   // B-form cycles per tile of slab rows
   AFMM_HD double per_tile() const {
     if (nnz_y == 0) return 0.0;
+    if (group) {
+      // nonempty (group, k): a group of 5 rows is empty at k with
+      // probability (1 - d)^5, d = the density of nonzero reps
+      const double d = (double)nnz_y / ((double)n * (double)n);
+      const double e1 = 1.0 - d, e5 = e1 * e1 * e1 * e1 * e1;
+      const double entries = (double)((n + 4) / 5) * (double)n * (1.0 - e5);
+      return g_step * (double)rep_sum + g_entry * entries;
+    }
     const double rbar = (double)rep_sum / (double)nnz_y;
     return b_step * (double)rep_sum + (rbar < 3.0 ? b_entry_small : b_entry) * (double)nnz_y;
   }
@@ -83,6 +106,8 @@ struct CaseAModel {
   // B part of tiles_b whole tiles (n B-form rows), charged its wave quantisation
   AFMM_HD double cost_b(uint64_t tiles_b) const {
     if (tiles_b == 0) return 0.0;
+    if (group)
+      return (double)tiles_b * per_tile() / wave_eff((n + 4) / 5, tiles_b, g_warps_per_cta, 1);
     return (double)tiles_b * per_tile() / wave_eff(n, tiles_b, b_warps_per_cta, b_ctas_per_sm);
   }
   // A part of m rows holding `bases` nonzero bases in total
@@ -110,7 +135,7 @@ AFMM_HD uint64_t choose_aform_rows(const CaseAModel& md, uint64_t rows, int vari
     if (time) *time = 0.0;
     return variant == kChooseAForm ? rows : 0;
   }
-  const uint64_t tb = md.b_tile, tiles_all = (rows + tb - 1) / tb;
+  const uint64_t tb = md.tile_rows(), tiles_all = (rows + tb - 1) / tb;
   const double pure_b = md.cost_b(tiles_all);
   const double pure_a = md.cost_a(rows, pre(rows));
   if (variant == kChooseAForm) {

@@ -31,13 +31,20 @@ void launch_rows(const T* x, uint64_t ld, uint32_t n, int which_case, const uint
                  const unsigned long long* rsum, uint32_t a0, uint32_t a1, uint32_t r0,
                  uint32_t r1, int2* lists, uint64_t cap, uint32_t* counts,
                  unsigned long long* work, DevStatus* st, cudaStream_t s,
-                 uint32_t* nnz_row = nullptr);
+                 uint32_t* nnz_row = nullptr, int group_allow = 0);
 // Case A rep lists: list j = compacted column j of Y. skip (optional): no-op
-// when *skip == 0.
+// when *skip == 0; also a no-op in group mode (group_mode(st, group_allow)).
 template <class T>
 void launch_transpose_compact(const T* y, uint64_t ld, uint32_t n, int2* lists, uint64_t cap,
                               uint32_t* counts, DevStatus* st, const uint32_t* skip,
-                              cudaStream_t s);
+                              cudaStream_t s, int group_allow = 0);
+// Dense group index of k_bgroup (gidx[g][k], g < ceil(B-form rows / 5), k <
+// ldg, ldg % 8 == 0): Case B (which_case 1) from slab rows [r0, r0 + rows) of
+// X, Case A from the columns of Y. A no-op unless group_mode(st, allow).
+template <class T>
+void launch_group_idx(const T* rep, uint64_t ld, uint32_t n, int which_case, uint32_t r0,
+                      uint32_t rows, uint16_t* gidx, uint64_t ldg, const DevStatus* st, int allow,
+                      cudaStream_t s);
 // out[oc][r] = in[ir][c] with optional row maps ir = in_rows[r], oc = out_rows[c];
 // with a status, nothing is written after a failed validation. plan/dyn: the
 // device-side Case A choice (1: rows = plan[1], in_rows += plan[0]; 2: cols =
@@ -114,9 +121,20 @@ struct BformLaunch {
   uint64_t slice_stride = 0;    // slice z writes to out + z * slice_stride
   uint64_t ld_out = 0;
   const DevStatus* st = nullptr;
+  int group_allow = 0;          // exit when the device chose the group kernel (group_mode)
 };
 template <class T>
 cudaError_t launch_bform(BformLaunch& a, T* out, cudaStream_t s);
+
+// The small-rep group kernel (fp32, order-preserving): B-form rows [0, nrows)
+// in groups of kGroupRows over the dense group index gidx (ldg >= nk rounded
+// up to bform_kb()), base columns [0, ncols) of the map's matrix (box
+// bform_kb() x bform_box_bytes()). Exits unless group_mode(st, allow).
+constexpr int kGroupWarps = 15;  // groups (consumer warps) per k_bgroup CTA
+cudaError_t launch_bgroup(const CUtensorMap* tmap, const uint16_t* gidx, uint64_t ldg,
+                          uint32_t nrows, int32_t ncols, const uint32_t* dyn_ncols, uint32_t nk,
+                          float* out, uint64_t ld_out, const DevStatus* st, int allow,
+                          cudaStream_t s);
 
 // out[r*ld_out + c] = sum over z (ascending) of part[z*stride + r*ld_part + c]
 template <class T>

@@ -131,7 +131,7 @@ __global__ void k_scan_stats(const T* __restrict__ lhs, const T* __restrict__ rh
     // Case A validates rhs (kernels.hpp:115), Case B lhs (:144)
     const bool is_rep = is_rhs == (which_case == 0);
     unsigned long long nf = 0, rb = 0, rn = 0;  // inverted keys, 0 = none
-    uint32_t cnt = 0;
+    uint32_t cnt = 0, rmx = 0, rneg = 0;  // rep operand: max |rep| (saturated), any negative
     unsigned long long s = 0;
     for (uint32_t j0 = 4 * lane; j0 < n; j0 += 128) {
       T v[4];
@@ -148,6 +148,12 @@ __global__ void k_scan_stats(const T* __restrict__ lhs, const T* __restrict__ rh
           const int kind = rep_kind(d);  // (an infinite rep: kind 2, as in the reference)
           if (kind && rb == 0) rb = ~((lin << 2) | (unsigned long long)kind);
           if (isnan(d) && rn == 0) rn = ~lin;
+          if (kind == 0 && !isnan(d) && v[e] != T(0)) {
+            const double a = fabs(d);
+            const uint32_t m = a >= 255.0 ? 255u : (uint32_t)llround(a);
+            rmx = m > rmx ? m : rmx;
+            rneg |= (d <= -0.5) ? 1u : 0u;  // llround(d) < 0
+          }
         }
         if (is_rhs) {
           cnt += v[e] != T(0) ? 1u : 0u;
@@ -164,6 +170,17 @@ __global__ void k_scan_stats(const T* __restrict__ lhs, const T* __restrict__ rh
         if (nf) atomicMax(is_rhs ? &st->nonfinite_rhs_inv : &st->nonfinite_lhs_inv, nf);
         if (rb) atomicMax(&st->rep_bad_inv, rb);
         if (rn) atomicMax(&st->rep_nan_inv, rn);
+      }
+    }
+    if (is_rep && __any_sync(FULL, (rmx | rneg) != 0)) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        rmx = max(rmx, __shfl_xor_sync(FULL, rmx, o));
+        rneg |= __shfl_xor_sync(FULL, rneg, o);
+      }
+      if (lane == 0) {
+        if (rmx > kGroupMaxRep) atomicMax(&st->rep_max, rmx);
+        if (rneg) atomicOr(&st->rep_neg, 1u);
       }
     }
     if (is_rhs) {
@@ -191,14 +208,16 @@ __global__ void k_rows(const T* __restrict__ x, uint64_t ld, uint32_t n, int whi
                        const unsigned long long* __restrict__ rsum, uint32_t a0, uint32_t a1,
                        uint32_t r0, uint32_t r1, int2* __restrict__ lists, uint64_t cap,
                        uint32_t* __restrict__ counts, unsigned long long* __restrict__ work,
-                       DevStatus* st, uint32_t* __restrict__ nnz_row) {
+                       DevStatus* st, uint32_t* __restrict__ nnz_row, int group_allow) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  // group mode: k_bgroup reads the dense group index instead of the lists
+  const bool lists_needed = lists != nullptr && !group_mode(st, group_allow);
   for (uint64_t i = a0 + warp; i < a1; i += nwarps) {
     const T* row = x + i * ld;
     const bool in_slab = i >= r0 && i < r1;
-    const bool compact = which_case == 1 && in_slab && lists != nullptr;
+    const bool compact = which_case == 1 && in_slab && lists_needed;
     int2* out = compact ? lists + (i - r0) * cap : nullptr;
     unsigned long long w = 0, z = 0, base = 0;
     for (uint32_t c0 = 0; c0 < n; c0 += 128) {  // warp-uniform trip count (the scan below)
@@ -269,8 +288,9 @@ template <class T>
 __global__ void __launch_bounds__(256)
     k_transpose_compact(const T* __restrict__ y, uint64_t ld, uint32_t n, int2* __restrict__ lists,
                         uint64_t cap, uint32_t* __restrict__ counts, DevStatus* st,
-                        const uint32_t* __restrict__ skip) {
+                        const uint32_t* __restrict__ skip, int group_allow) {
   if (skip && *skip == 0) return;
+  if (group_mode(st, group_allow)) return;  // k_bgroup runs: no lists
   __shared__ T tile[32][33];
   const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const uint32_t j0 = blockIdx.x * 32;
@@ -319,6 +339,82 @@ __global__ void __launch_bounds__(256)
       }
     }
   }
+}
+
+// ---- group index of the small-rep group kernel (k_bgroup, bform.cu) ----
+//
+// B-form rows 5g .. 5g+4 form group g; gidx[g][k] = (t0 + 3 t1 + 9 t2) |
+// (t3 + 3 t4) << 8, t_r = the row's rep at k (0..kGroupMaxRep in group mode,
+// 0 past the last row and for k >= n up to the padded ldg). Dense: one u16
+// per (group, k), so both builders are plain parallel passes (no compaction);
+// k_bgroup skips the k with index 0. Both exit unless the device-side status
+// chose group mode.
+__device__ __forceinline__ uint32_t group_digit(int r) {
+  return r == 0 ? 1u : r == 1 ? 3u : r == 2 ? 9u : r == 3 ? 256u : 768u;
+}
+
+// Case B: groups of slab rows r0 + 5g .. of X; one warp per group.
+template <class T>
+__global__ void k_group_idx_rows(const T* __restrict__ x, uint64_t ld, uint32_t n, int vec,
+                                 uint32_t r0, uint32_t rows, uint16_t* __restrict__ gidx,
+                                 uint64_t ldg, const DevStatus* st, int allow) {
+  if (!group_mode(st, allow) || status_failed(st)) return;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t ngroups = (rows + kGroupRows - 1) / kGroupRows;
+  for (uint64_t g = warp; g < ngroups; g += nwarps) {
+    for (uint64_t c0 = 0; c0 < ldg; c0 += 128) {
+      const uint32_t j0 = (uint32_t)c0 + 4 * lane;
+      uint32_t idx[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int r = 0; r < kGroupRows; ++r) {
+        const uint64_t q = g * kGroupRows + r;
+        if (q >= rows) break;
+        T v[4];
+        load4(x + (r0 + q) * ld, j0, n, vec != 0, v);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (j0 + e < n) idx[e] += (uint32_t)rep_of(v[e]) * group_digit(r);
+      }
+      if (j0 < ldg)  // ldg % 8 == 0: the 4 entries are in range together
+        *reinterpret_cast<ushort4*>(gidx + g * ldg + j0) =
+            make_ushort4((unsigned short)idx[0], (unsigned short)idx[1], (unsigned short)idx[2],
+                         (unsigned short)idx[3]);
+    }
+  }
+}
+
+// Case A: groups of columns 5g .. of Y (B-form row j = column j of Y), through
+// 32 k x 160 column smem tiles (32 groups per block).
+template <class T>
+__global__ void __launch_bounds__(256)
+    k_group_idx_cols(const T* __restrict__ y, uint64_t ld, uint32_t n,
+                     uint16_t* __restrict__ gidx, uint64_t ldg, const DevStatus* st, int allow) {
+  if (!group_mode(st, allow) || status_failed(st)) return;
+  constexpr uint32_t GC = 32 * kGroupRows;  // columns per block
+  __shared__ uint8_t tile[32][GC + 1];
+  const uint32_t j0 = blockIdx.x * GC, k0 = blockIdx.y * 32;
+  for (uint32_t i = threadIdx.x; i < 32 * GC; i += blockDim.x) {
+    const uint32_t r = i / GC, c = i % GC, k = k0 + r, j = j0 + c;
+    tile[r][c] = (k < n && j < n) ? (uint8_t)rep_of(y[(uint64_t)k * ld + j]) : (uint8_t)0;
+  }
+  __syncthreads();
+  const uint32_t gl = threadIdx.x >> 3, kq = (threadIdx.x & 7) * 4;
+  const uint64_t g = (uint64_t)blockIdx.x * 32 + gl;
+  const uint32_t ngroups = (n + kGroupRows - 1) / kGroupRows;
+  if (g >= ngroups || k0 + kq >= ldg) return;
+  uint32_t idx[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int r = 0; r < kGroupRows; ++r) v += (uint32_t)tile[kq + e][gl * kGroupRows + r] * group_digit(r);
+    idx[e] = v;
+  }
+  *reinterpret_cast<ushort4*>(gidx + g * ldg + k0 + kq) =
+      make_ushort4((unsigned short)idx[0], (unsigned short)idx[1], (unsigned short)idx[2],
+                   (unsigned short)idx[3]);
 }
 
 // ---- A-form prepass (k_aform, Case A with the base uniform per warp) ----
@@ -399,6 +495,7 @@ __global__ void __launch_bounds__(kChooseThreads)
   md.nnz_y = fstats[0];
   md.trip_sum = fstats[1];
   md.rep_sum = fstats[3];
+  md.group = group_mode(st, md.group_allow);  // the B part runs k_bgroup
   const bool a_ok = fstats[2] == 0;  // every |rep| <= 2048 (exact fp16 counts)
 
   for (uint32_t v = tid; v < nb; v += kChooseThreads) hist[v] = 0;
@@ -469,7 +566,7 @@ __global__ void __launch_bounds__(kChooseThreads)
     if (vstar) *vstar = lo;
     return (double)csum[lo] + (double)lo * (double)(m - cum[lo]);
   };
-  const uint64_t tb = md.b_tile;
+  const uint64_t tb = md.tile_rows();
   // candidate c: c = 0 -> m = rows (pure A), c = j >= 1 -> m = rows - j * tb
   for (uint32_t c = tid; c <= kChooseCands; c += kChooseThreads) {
     const uint64_t m = c == 0 ? rows : (uint64_t)rows - (uint64_t)c * tb;
@@ -669,11 +766,29 @@ template <class T>
 void launch_rows(const T* x, uint64_t ld, uint32_t n, int which_case, const uint32_t* nnz,
                  const unsigned long long* rsum, uint32_t a0, uint32_t a1, uint32_t r0,
                  uint32_t r1, int2* lists, uint64_t cap, uint32_t* counts,
-                 unsigned long long* work, DevStatus* st, cudaStream_t s, uint32_t* nnz_row) {
+                 unsigned long long* work, DevStatus* st, cudaStream_t s, uint32_t* nnz_row,
+                 int group_allow) {
   if (a1 <= a0) return;
   k_rows<T><<<grid_for_warps(a1 - a0, 8), 256, 0, s>>>(x, ld, n, which_case, vec_ok(x, ld), nnz,
                                                         rsum, a0, a1, r0, r1, lists, cap, counts,
-                                                        work, st, nnz_row);
+                                                        work, st, nnz_row, group_allow);
+  note_launch();
+}
+
+template <class T>
+void launch_group_idx(const T* rep, uint64_t ld, uint32_t n, int which_case, uint32_t r0,
+                      uint32_t rows, uint16_t* gidx, uint64_t ldg, const DevStatus* st, int allow,
+                      cudaStream_t s) {
+  if (which_case == 1) {
+    const uint32_t ngroups = (rows + kGroupRows - 1) / kGroupRows;
+    if (ngroups == 0) return;
+    k_group_idx_rows<T><<<grid_for_warps(ngroups, 8), 256, 0, s>>>(rep, ld, n, vec_ok(rep, ld), r0,
+                                                                  rows, gidx, ldg, st, allow);
+  } else {
+    const uint32_t ngroups = (n + kGroupRows - 1) / kGroupRows;
+    dim3 grid((ngroups + 31) / 32, (uint32_t)((ldg + 31) / 32));
+    k_group_idx_cols<T><<<grid, 256, 0, s>>>(rep, ld, n, gidx, ldg, st, allow);
+  }
   note_launch();
 }
 
@@ -710,8 +825,9 @@ void launch_acompact(const T* x, uint64_t ld, uint32_t n, uint32_t r0, uint32_t 
 template <class T>
 void launch_transpose_compact(const T* y, uint64_t ld, uint32_t n, int2* lists, uint64_t cap,
                               uint32_t* counts, DevStatus* st, const uint32_t* skip,
-                              cudaStream_t s) {
-  k_transpose_compact<T><<<(n + 31) / 32, 256, 0, s>>>(y, ld, n, lists, cap, counts, st, skip);
+                              cudaStream_t s, int group_allow) {
+  k_transpose_compact<T><<<(n + 31) / 32, 256, 0, s>>>(y, ld, n, lists, cap, counts, st, skip,
+                                                       group_allow);
   note_launch();
 }
 
@@ -746,7 +862,9 @@ void launch_reduce_slices(const T* part, uint64_t stride, uint64_t ld_part, uint
   template void launch_rows<T>(const T*, uint64_t, uint32_t, int, const uint32_t*,             \
                                const unsigned long long*, uint32_t, uint32_t, uint32_t,        \
                                uint32_t, int2*, uint64_t, uint32_t*, unsigned long long*,      \
-                               DevStatus*, cudaStream_t, uint32_t*);                           \
+                               DevStatus*, cudaStream_t, uint32_t*, int);                      \
+  template void launch_group_idx<T>(const T*, uint64_t, uint32_t, int, uint32_t, uint32_t,     \
+                                    uint16_t*, uint64_t, const DevStatus*, int, cudaStream_t); \
   template void launch_counts_f16<T>(const T*, uint64_t, uint32_t, uint32_t, __half*, uint64_t, \
                                      uint16_t*, unsigned long long*, cudaStream_t);            \
   template void launch_acompact<T>(const T*, uint64_t, uint32_t, uint32_t, uint32_t,           \
@@ -755,7 +873,7 @@ void launch_reduce_slices(const T* part, uint64_t stride, uint64_t ld_part, uint
                                    cudaStream_t);                                              \
   template void launch_transpose_compact<T>(const T*, uint64_t, uint32_t, int2*, uint64_t,     \
                                             uint32_t*, DevStatus*, const uint32_t*,            \
-                                            cudaStream_t);                                     \
+                                            cudaStream_t, int);                                \
   template void launch_transpose<T>(const T*, uint64_t, uint32_t, uint32_t, T*, uint64_t,      \
                                     cudaStream_t, const uint32_t*, const uint32_t*,            \
                                     const DevStatus*, const uint32_t*, int);                   \

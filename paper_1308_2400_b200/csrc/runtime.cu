@@ -63,6 +63,13 @@ int variant_from_env() {
   return kAuto;
 }
 
+// AFMM_BFORM=nogroup: automatic choices, but never the small-rep group kernel
+// (k_bgroup) -- for comparisons; a forced k_bform shape also excludes it.
+bool group_off_from_env() {
+  const char* v = std::getenv("AFMM_BFORM");
+  return v && std::strcmp(v, "nogroup") == 0;
+}
+
 inline uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
 
 int sm_count(int device) {
@@ -194,6 +201,9 @@ struct Call {
   bool prevalidated = false;  // multi-device: validation and the per-k vector done already
   bool have_counts = false;   // multi-device Case A: fp16 counts and statistics done already
   bool check_finite = true;   // false: AFMM_FLAG_KERNEL_SEMANTICS (no DenseMatrix ctor check)
+  // prevalidated calls: the rep statistics of the whole operands (DevStatus
+  // rep_max / rep_neg, merged over the shards) for the group-kernel choice
+  uint32_t rep_max = 0, rep_neg = 0;
 };
 
 }  // namespace
@@ -205,6 +215,7 @@ struct afmm_context {
   // workspace
   DevBuf status, vec_k, work, lists, counts, base_copy, xt, zt, part, cnt16, rmax, fstats;
   DevBuf alists, acounts, ridx, plan, scratch;  // A-form lists / counts, Case A choice
+  DevBuf gidx;  // dense group index of the small-rep group kernel (k_bgroup)
   // host-buffer API staging
   DevBuf hx, hy, hz;
   DevStatus* status_host = nullptr;           // pinned
@@ -213,7 +224,10 @@ struct afmm_context {
   bool pending = false;
   uint64_t cap_need = 0;  // list capacity demanded by an overflowing product (re-run)
   int variant = kAuto;
-  int last_form = 0;  // kernel(s) of the last Case A call: 0 B-form, 1 A-form, 2 split
+  bool group_off = false;  // AFMM_BFORM=nogroup
+  // kernel(s) of the last call: Case A 0 B-form, 1 A-form, 2 split; + 4 when
+  // the B-form part ran the small-rep group kernel (Case B: 0 or 4)
+  int last_form = 0;
   // optional phase timing: ev[0] start, ev[1] before compute, ev[2] after compute, ev[3] end
   bool timing = false;
   bool timed_last = false;
@@ -276,7 +290,7 @@ std::vector<DevBuf*> all_bufs(afmm_context* c) {
   return {&c->status, &c->vec_k, &c->work,    &c->lists,  &c->counts, &c->base_copy,
           &c->xt,     &c->zt,    &c->part,    &c->cnt16,  &c->rmax,   &c->fstats,
           &c->alists, &c->acounts, &c->ridx,  &c->plan,   &c->scratch, &c->hx,
-          &c->hy,     &c->hz};
+          &c->hy,     &c->hz,      &c->gidx};
 }
 
 void set_error(afmm_error* err, int kind, int operand, uint64_t row, uint64_t col, double value,
@@ -364,6 +378,8 @@ void merge_status(DevStatus* into, const DevStatus& s) {
   into->rep_bad_inv = std::max(into->rep_bad_inv, s.rep_bad_inv);
   into->list_need = std::max(into->list_need, s.list_need);
   into->rep_nan_inv = std::max(into->rep_nan_inv, s.rep_nan_inv);
+  into->rep_max = std::max(into->rep_max, s.rep_max);
+  into->rep_neg |= s.rep_neg;
   into->check_violations += s.check_violations;
   into->additions += s.additions;
   into->zero_skips += s.zero_skips;
@@ -504,7 +520,7 @@ template <class T>
 afmm_status launch_compute(afmm_context* c, const Call& call, int shape, const T* base,
                            uint64_t kb_rows, uint64_t b_cols, uint64_t ldb, uint32_t nrows,
                            int32_t ncols, const uint32_t* dyn_ncols, T* out, uint64_t ld_out,
-                           DevStatus* st, afmm_error* err) {
+                           DevStatus* st, int group_allow, afmm_error* err) {
   // reassociated mode: the blocked-sum kernel (bform.cu kShapeFast), k slices
   // on top when the tile grid is small
   if (call.mode == AFMM_MODE_FAST) shape = afmm_dev::kShapeFast;
@@ -542,6 +558,7 @@ afmm_status launch_compute(afmm_context* c, const Call& call, int shape, const T
   a.dyn_ncols = dyn_ncols;
   a.nk = (uint32_t)kb_rows;
   a.st = st;
+  a.group_allow = group_allow;
   if (splits > 1) {
     const uint64_t ldp = round_up((uint64_t)ncols, 32);
     const uint64_t stride = (uint64_t)nrows * ldp;
@@ -558,6 +575,39 @@ afmm_status launch_compute(afmm_context* c, const Call& call, int shape, const T
   a.ld_out = ld_out;
   CK(afmm_dev::launch_bform<T>(a, out, c->stream), "bform");
   return AFMM_OK;
+}
+
+// The host's half of the small-rep group-kernel decision (group_mode() on the
+// device completes it from the validated rep statistics): fp32, the
+// order-preserving mode, and no forced k_bform shape.
+int group_allow(const afmm_context* c, const Call& call) {
+  if (call.dtype != AFMM_F32 || call.mode == AFMM_MODE_FAST || c->group_off) return 0;
+  return (c->variant == kAuto || c->variant == kAForm || c->variant == kHybrid) ? 1 : 0;
+}
+
+// Group index row length: k rounded up to whole ring stages.
+uint64_t group_ldg(uint64_t n) { return round_up(n, (uint64_t)afmm_dev::bform_kb()); }
+
+// The small-rep group kernel over the same B-form operands as launch_compute
+// (it exits on the device unless group mode was chosen, k_bform the reverse).
+template <class T>
+afmm_status launch_group_compute(afmm_context* c, const T* base, uint64_t kb_rows, uint64_t b_cols,
+                                 uint64_t ldb, uint32_t nrows, int32_t ncols,
+                                 const uint32_t* dyn_ncols, T* out, uint64_t ld_out,
+                                 DevStatus* st, int allow, afmm_error* err) {
+  if constexpr (sizeof(T) != 4) {
+    return AFMM_OK;  // fp32 only (group_allow is 0 for fp64)
+  } else {
+    CUtensorMap tmap;
+    if (!make_tmap<T>(&tmap, base, kb_rows, b_cols, ldb)) {
+      set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: cuTensorMapEncodeTiled failed");
+      return AFMM_ERR_CUDA;
+    }
+    CK(afmm_dev::launch_bgroup(&tmap, c->gidx.as<uint16_t>(), group_ldg(kb_rows), nrows, ncols,
+                               dyn_ncols, (uint32_t)kb_rows, out, ld_out, st, allow, c->stream),
+       "bgroup");
+    return AFMM_OK;
+  }
 }
 
 // Case A kernel-choice variant code for k_choose
@@ -588,6 +638,13 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
   for (int i = 0; i < 4; ++i) c->last_ev[i] = c->rec_ev[i];
   c->mark(0);
   CK(cudaMemsetAsync(st, 0, sizeof(DevStatus), s), "memset");
+  const int gallow = group_allow(c, call);
+  if (call.prevalidated && gallow) {
+    // the shards' merged rep statistics (k_scan_stats does not run here);
+    // both fields are < 256, so a one-byte memset of the low byte sets them
+    CK(cudaMemsetAsync(&st->rep_max, (int)std::min<uint32_t>(call.rep_max, 255u), 1, s), "memset");
+    CK(cudaMemsetAsync(&st->rep_neg, call.rep_neg ? 1 : 0, 1, s), "memset");
+  }
 
   // validation (kernels.hpp:115 / :144) + DenseMatrix finite check (matrix.hpp:31-35)
   // + the per-k vector of the work formulas, one pass over both operands
@@ -604,7 +661,13 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
     CK(c->counts.ensure(std::max<uint64_t>(rows, 1) * 4), "workspace");
     afmm_dev::launch_rows<T>(lhs, ld, n32, 1, nnz, nullptr, (uint32_t)r0, (uint32_t)r1,
                              (uint32_t)r0, (uint32_t)r1, c->lists.as<int2>(), cap,
-                             c->counts.as<uint32_t>(), nullptr, st, s);
+                             c->counts.as<uint32_t>(), nullptr, st, s, nullptr, gallow);
+    if (gallow && rows > 0) {
+      const uint64_t ldg = group_ldg(n), ngroups = (rows + afmm_dev::kGroupRows - 1) / afmm_dev::kGroupRows;
+      CK(c->gidx.ensure(ngroups * ldg * sizeof(uint16_t)), "workspace");
+      afmm_dev::launch_group_idx<T>(lhs, ld, n32, 1, (uint32_t)r0, (uint32_t)rows,
+                                    c->gidx.as<uint16_t>(), ldg, st, gallow, s);
+    }
     const T* base = rhs;
     uint64_t ldb = ld;
     if ((ld * sizeof(T)) % 16 != 0 || reinterpret_cast<uintptr_t>(rhs) % 16 != 0) {
@@ -618,11 +681,16 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
     c->mark(1);
     if (rows > 0) {
       afmm_status cs = launch_compute<T>(c, call, shape, base, n, n, ldb, (uint32_t)rows,
-                                         (int32_t)n, nullptr, out, ld_out, st, err);
+                                         (int32_t)n, nullptr, out, ld_out, st, gallow, err);
       if (cs != AFMM_OK) return cs;
+      if (gallow) {
+        cs = launch_group_compute<T>(c, base, n, n, ldb, (uint32_t)rows, (int32_t)n, nullptr, out,
+                                     ld_out, st, gallow, err);
+        if (cs != AFMM_OK) return cs;
+      }
     }
     c->mark(2);
-    c->last_form = 0;
+    c->last_form = 0;  // (+ 4 from the status when k_bgroup ran)
   } else {
     // Case A: the B-form on transposed operands, the A-form (base uniform per
     // warp), or the slab's rows split between them. For n >= 1024 (or when
@@ -661,7 +729,9 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
         afmm_dev::launch_counts_f16<T>(rhs, ld, n32, tc, c->cnt16.as<__half>(), ldc,
                                        c->rmax.as<uint16_t>(), fs, s);
       }
-      afmm_dev::launch_choose(case_a_model(sizeof(T), n, sms, shape), (uint32_t)rows,
+      afmm_dev::CaseAModel md = case_a_model(sizeof(T), n, sms, shape);
+      md.group_allow = gallow;
+      afmm_dev::launch_choose(md, (uint32_t)rows,
                               choose_variant(c->variant), c->acounts.as<uint32_t>(), fs,
                               c->scratch.as<uint32_t>(), c->plan.as<uint32_t>(),
                               c->ridx.as<uint32_t>(), st, s);
@@ -679,7 +749,13 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
     if (rows > 0) {
       afmm_dev::launch_transpose_compact<T>(rhs, ld, n32, c->lists.as<int2>(), cap,
                                             c->counts.as<uint32_t>(), st,
-                                            plan ? plan + 1 : nullptr, s);
+                                            plan ? plan + 1 : nullptr, s, gallow);
+      if (gallow) {
+        const uint64_t ldg = group_ldg(n), ngroups = (n + afmm_dev::kGroupRows - 1) / afmm_dev::kGroupRows;
+        CK(c->gidx.ensure(ngroups * ldg * sizeof(uint16_t)), "workspace");
+        afmm_dev::launch_group_idx<T>(rhs, ld, n32, 0, 0, n32, c->gidx.as<uint16_t>(), ldg, st,
+                                      gallow, s);
+      }
       afmm_dev::launch_transpose<T>(lhs + r0 * ld, ld, (uint32_t)rows, n32, c->xt.as<T>(), lds, s,
                                     ridx, nullptr, nullptr, plan, plan ? 1 : 0);
     }
@@ -700,8 +776,14 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
       // B-form: Case A as Case B on transposed operands, Z^T = (Y^T) (x) (X^T)
       afmm_status cs = launch_compute<T>(c, call, shape, c->xt.as<T>(), n, rows, lds, n32,
                                          (int32_t)rows, plan ? plan + 1 : nullptr, c->zt.as<T>(),
-                                         lds, st, err);
+                                         lds, st, gallow, err);
       if (cs != AFMM_OK) return cs;
+      if (gallow) {
+        cs = launch_group_compute<T>(c, c->xt.as<T>(), n, rows, lds, n32, (int32_t)rows,
+                                     plan ? plan + 1 : nullptr, c->zt.as<T>(), lds, st, gallow,
+                                     err);
+        if (cs != AFMM_OK) return cs;
+      }
     }
     c->mark(2);
     if (rows > 0)
@@ -741,7 +823,11 @@ afmm_status finish_locked(afmm_context* c, afmm_op_counts* counts, afmm_error* e
   if (e != cudaSuccess) return cuda_fail(err, e, "afmm: device execution");
   const DevStatus s = *c->status_host;
   if (s.form_rows) c->last_form = s.a_rows == 0 ? 0 : (s.a_rows == s.form_rows ? 1 : 2);
-  else if (c->last.which == AFMM_CASE_A) c->last_form = 0;
+  else c->last_form = 0;
+  // the B-form part ran the small-rep group kernel (group_mode on the device)
+  const bool b_part = c->last_form != 1 && c->last.r1 > c->last.r0;
+  if (b_part && group_allow(c, c->last) && s.rep_max <= afmm_dev::kGroupMaxRep && s.rep_neg == 0)
+    c->last_form |= 4;
 #ifdef AFMM_CHECKED
   {
     int bad_guards = 0;
@@ -793,7 +879,7 @@ afmm_status graph_call(afmm_context* c, const Call& call, afmm_error* err) {
   key.mode = call.mode;
   key.split_k = call.split_k;
   key.check = call.check_finite ? 1 : 0;
-  key.variant = c->variant;
+  key.variant = c->variant + (c->group_off ? 100 : 0);
   key.timing = c->timing ? 1 : 0;
   key.lhs = call.lhs;
   key.rhs = call.rhs;
@@ -1038,7 +1124,7 @@ afmm_status host_product_one(int which, const T* lhs, const T* rhs, uint64_t n, 
     timing->total_ms = total;
     timing->compute_ms = compute;
     timing->devices = 1;
-    timing->form = which == AFMM_CASE_A ? c->last_form : 0;
+    timing->form = c->last_form;
     if (!kernel_timing) enable_timing_locked(c, 0);
   }
   return st;
@@ -1097,7 +1183,8 @@ bool ensure_peer_access(int device, int peer) {
 // and the multi-device call): Case B W_i; Case A the cheaper of the row's
 // A-form cost and its share of a B-form tile (costmodel.h).
 void row_costs(int which, size_t elem, uint64_t n, int sms, const uint64_t* work,
-               const uint32_t* nnz_row, const unsigned long long* fstats, uint64_t* cost) {
+               const uint32_t* nnz_row, const unsigned long long* fstats, uint64_t* cost,
+               bool group = false) {
   if (which == AFMM_CASE_B) {
     std::memcpy(cost, work, n * sizeof(uint64_t));
     return;
@@ -1107,8 +1194,9 @@ void row_costs(int which, size_t elem, uint64_t n, int sms, const uint64_t* work
   md.nnz_y = fstats[0];
   md.trip_sum = fstats[1];
   md.rep_sum = fstats[3];
+  md.group = group;
   const bool a_ok = fstats[2] == 0;
-  const double per_row_b = md.per_tile() / (double)md.b_tile;
+  const double per_row_b = md.per_tile() / (double)md.tile_rows();
   const double per_base = md.per_base();
   for (uint64_t i = 0; i < n; ++i) {
     const double a = a_ok ? per_base * (double)nnz_row[i] : per_row_b;
@@ -1127,7 +1215,7 @@ class SlabModel {
   double time(uint64_t r0, uint64_t r1) {
     const uint64_t rows = r1 > r0 ? r1 - r0 : 0, n = md_.n;
     if (rows == 0) return 0.0;
-    if (!a_ok_) return md_.cost_b((rows + md_.b_tile - 1) / md_.b_tile);
+    if (!a_ok_) return md_.cost_b((rows + md_.tile_rows() - 1) / md_.tile_rows());
     std::fill(cnt_.begin(), cnt_.end(), 0u);
     for (uint64_t i = r0; i < r1; ++i) ++cnt_[std::min<uint64_t>(nnz_[i], n)];
     cum_c_[0] = 0;
@@ -1210,9 +1298,9 @@ void partition_case_a(const afmm_dev::CaseAModel& md, const uint32_t* nnz, bool 
 // Row cuts for `parts` devices from the full operands' statistics.
 void partition_from_stats(int which, size_t elem, uint64_t n, int sms, const uint64_t* work,
                           const uint32_t* nnz_row, const unsigned long long* fstats,
-                          uint32_t parts, uint64_t* cuts) {
+                          uint32_t parts, uint64_t* cuts, bool group = false) {
   std::vector<uint64_t> cost(n);
-  row_costs(which, elem, n, sms, work, nnz_row, fstats, cost.data());
+  row_costs(which, elem, n, sms, work, nnz_row, fstats, cost.data(), group);
   if (which == AFMM_CASE_B) {
     afmm_partition_rows(cost.data(), n, parts, cuts);
     return;
@@ -1221,6 +1309,7 @@ void partition_from_stats(int which, size_t elem, uint64_t n, int sms, const uin
   md.nnz_y = fstats[0];
   md.trip_sum = fstats[1];
   md.rep_sum = fstats[3];
+  md.group = group;
   partition_case_a(md, nnz_row, fstats[2] == 0, cost.data(), parts, cuts, nullptr);
 }
 
@@ -1285,6 +1374,7 @@ afmm_status host_product_multi(int which, const T* lhs, const T* rhs, uint64_t n
   std::vector<cudaEvent_t> ev_a(G, nullptr);
   std::vector<float> total_ms(G, -1.f), compute_ms(G, -1.f);
   unsigned long long fstats[4] = {0, 0, 0, 0};
+  uint32_t rep_max = 0, rep_neg = 0;  // merged rep statistics (group-kernel choice)
   Barrier bar(G);
   bool failed = false;  // set by shard 0 between the barriers
   const int sms = sm_count(devs[0]);
@@ -1396,6 +1486,8 @@ afmm_status host_product_multi(int which, const T* lhs, const T* rhs, uint64_t n
       if (!failed) {
         DevStatus all{};
         for (int h = 0; h < G; ++h) merge_status(&all, stat[h]);
+        rep_max = all.rep_max;
+        rep_neg = all.rep_neg;
         const afmm_status dst =
             decode_status(all, which, n, host_reader(lhs, rhs, dtype, n), nullptr, err);
         if (dst != AFMM_OK) {
@@ -1408,9 +1500,15 @@ afmm_status host_product_multi(int which, const T* lhs, const T* rhs, uint64_t n
         if (opt->partition == AFMM_PARTITION_ROWS) {
           cuts = e;
         } else {
+          // the B part's kernel as the shards will choose it (group_mode)
+          Call probe;
+          probe.dtype = dtype;
+          probe.mode = mode;
+          const bool grp = group_allow(ctx[0], probe) && rep_max <= afmm_dev::kGroupMaxRep &&
+                           rep_neg == 0;
           partition_from_stats(which, sizeof(T), n, sms, work.data(),
                                which == AFMM_CASE_A ? nnz_row.data() : nullptr, fstats,
-                               (uint32_t)G, cuts.data());
+                               (uint32_t)G, cuts.data(), grp);
         }
       }
     }
@@ -1445,6 +1543,8 @@ afmm_status host_product_multi(int which, const T* lhs, const T* rhs, uint64_t n
     call.r0 = r0;
     call.r1 = r1;
     call.prevalidated = true;
+    call.rep_max = rep_max;
+    call.rep_neg = rep_neg;
     call.have_counts = which == AFMM_CASE_A;
     const bool kernel_timing = c->timing;
     if (timing) enable_timing_locked(c, 1);
@@ -1495,7 +1595,7 @@ afmm_status host_product_multi(int which, const T* lhs, const T* rhs, uint64_t n
     timing->total_ms = *std::max_element(total_ms.begin(), total_ms.end());
     timing->compute_ms = *std::max_element(compute_ms.begin(), compute_ms.end());
     timing->devices = G;
-    timing->form = which == AFMM_CASE_A ? ctx[0]->last_form : 0;
+    timing->form = ctx[0]->last_form;
   }
   clear_error(err);
   return AFMM_OK;
@@ -1581,6 +1681,7 @@ afmm_status afmm_context_create(int32_t device, afmm_context** ctx) {
   if (!c) return AFMM_ERR_OUT_OF_MEMORY;
   c->device = device;
   c->variant = variant_from_env();
+  c->group_off = group_off_from_env();
   {
     const char* gv = std::getenv("AFMM_GRAPHS");
     c->graphs = !(gv && std::strcmp(gv, "0") == 0);
@@ -1732,7 +1833,7 @@ afmm_status afmm_context_last_timing(afmm_context* c, float* prepass_ms, float* 
 int32_t afmm_context_last_form(afmm_context* c) {
   if (!c) return -1;
   std::lock_guard<std::mutex> g(c->mu);
-  return c->last.which == AFMM_CASE_A ? c->last_form : 0;
+  return c->last_form;
 }
 
 }  // extern "C"

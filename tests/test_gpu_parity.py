@@ -296,7 +296,9 @@ def test_full_size_every_row_bit_exact(cuda, fastcheck, name, kw):
                          .any(axis=1))
     assert bad.size == 0, (name, kw, form, bad[:10])
     if name == "cfg3":
-        assert form == ("aform" if kw["d1"] < 0.2 else "bform"), form
+        # reps uniform {0..2mu}: mu = 1 runs the small-rep group kernel
+        assert form == ("aform" if kw["d1"] < 0.2 else "group" if kw["mu"] == 1
+                        else "bform"), form
 
 
 def test_full_size_cfg5_rows_in_every_row_block(cuda, fastcheck):
