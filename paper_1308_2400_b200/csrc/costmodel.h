@@ -127,10 +127,12 @@ constexpr int kChooseSplit = 2;
 // The number m of slab rows to run in the A-form (the m sparsest rows; 0 =
 // pure B-form, rows = pure A-form). pre(m) = total nonzero bases of the m
 // sparsest rows. Splits keep the B part a whole number of tiles. *time (if
-// given) receives the modeled cycles of the choice.
+// given) receives the modeled cycles of the choice. split_cost (optional):
+// split_cost[j] = the cost of the split with j B tiles, precomputed (k_choose
+// prices the candidates in parallel; the same expression).
 template <class Pre>
 AFMM_HD uint64_t choose_aform_rows(const CaseAModel& md, uint64_t rows, int variant, Pre pre,
-                                   double* time = nullptr) {
+                                   double* time = nullptr, const double* split_cost = nullptr) {
   if (rows == 0 || md.nnz_y == 0) {
     if (time) *time = 0.0;
     return variant == kChooseAForm ? rows : 0;
@@ -146,7 +148,7 @@ AFMM_HD uint64_t choose_aform_rows(const CaseAModel& md, uint64_t rows, int vari
   uint64_t m_split = 0;
   for (uint64_t j = 1; j * tb < rows; ++j) {
     const uint64_t m = rows - j * tb;
-    const double c = md.cost_a(m, pre(m)) + md.cost_b(j);
+    const double c = split_cost ? split_cost[j] : md.cost_a(m, pre(m)) + md.cost_b(j);
     if (m_split == 0 || c < best_split) {
       best_split = c;
       m_split = m;

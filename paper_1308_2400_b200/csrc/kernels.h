@@ -18,11 +18,13 @@ void note_launch();  // counts library kernel launches (runtime.cu)
 // NaN rep is recorded either way), rep validation
 // (into st, global row-major indices), and the per-k vector of the rhs rows
 // (Case B: nnz[k] of rhs rows; Case A: rsum[k] of rhs rows). which_case: 0 = A, 1 = B.
+// fstats (Case A, optional): the cost-model statistics of the rhs rows
+// (launch_counts_f16's four sums), accumulated.
 template <class T>
 void launch_scan_stats(const T* lhs, const T* rhs, uint64_t ld, uint32_t n, int which_case,
                        uint32_t l0, uint32_t l1, uint32_t q0, uint32_t q1, DevStatus* st,
                        uint32_t* nnz, unsigned long long* rsum, cudaStream_t s,
-                       int check_finite = 1);
+                       int check_finite = 1, unsigned long long* fstats = nullptr);
 // Rows [a0, a1) of X: work[i] (if work != nullptr); slab rows [r0, r1) add
 // OpCounts to st and, for Case B with lists != nullptr, get their compacted
 // int2 (k, rep) lists; nnz_row (optional, Case A): nonzero bases of each slab row.
@@ -40,11 +42,12 @@ void launch_transpose_compact(const T* y, uint64_t ld, uint32_t n, int2* lists, 
                               cudaStream_t s, int group_allow = 0);
 // Dense group index of k_bgroup (gidx[g][k], g < ceil(B-form rows / 5), k <
 // ldg, ldg % 8 == 0): Case B (which_case 1) from slab rows [r0, r0 + rows) of
-// X, Case A from the columns of Y. A no-op unless group_mode(st, allow).
+// X, Case A from the columns of Y. A no-op unless group_mode(st, allow), and
+// (Case A) when skip is given and *skip == 0 (no B-form rows).
 template <class T>
 void launch_group_idx(const T* rep, uint64_t ld, uint32_t n, int which_case, uint32_t r0,
                       uint32_t rows, uint16_t* gidx, uint64_t ldg, const DevStatus* st, int allow,
-                      cudaStream_t s);
+                      cudaStream_t s, const uint32_t* skip = nullptr);
 // out[oc][r] = in[ir][c] with optional row maps ir = in_rows[r], oc = out_rows[c];
 // with a status, nothing is written after a failed validation. plan/dyn: the
 // device-side Case A choice (1: rows = plan[1], in_rows += plan[0]; 2: cols =
@@ -57,11 +60,13 @@ void launch_transpose(const T* in, uint64_t ld_in, uint32_t rows, uint32_t cols,
 
 // ---- A-form (Case A, base uniform per warp; aform in bform.cu) ----
 // fp16 rep counts of Y (|rep| <= 2048) + per (k, tile) max |rep| | neg flag.
-// fstats (4 x u64, accumulated): nonzero reps, sum of trip counts, reps beyond
-// 2048, sum of |rep|.
+// fstats (4 x u64, accumulated; optional): nonzero reps, sum of trip counts,
+// reps beyond 2048, sum of |rep|. need (optional): a no-op when *need == 0
+// (run after k_choose with need = the A-form row count).
 template <class T>
 void launch_counts_f16(const T* y, uint64_t ld, uint32_t n, uint32_t tile_cols, __half* cnt,
-                       uint64_t ldc, uint16_t* rmax, unsigned long long* fstats, cudaStream_t s);
+                       uint64_t ldc, uint16_t* rmax, unsigned long long* fstats, cudaStream_t s,
+                       const uint32_t* need = nullptr);
 // Device-side Case A choice (costmodel.h): plan[0] = A-form rows, plan[1] =
 // B-form rows, ridx = the slab row order (A rows first), st->a_rows.
 size_t choose_scratch_bytes(uint64_t n);

@@ -94,6 +94,15 @@ __device__ __forceinline__ long long rep_of(T v) {
   return v != T(0) ? llround((double)v) : 0ll;
 }
 
+// rep_of for an operand that passed validation: an fp32 rep is then an exact
+// integer or rounds to 0 (|v| <= 1e-9; float spacing near integers >= 1 is
+// far wider than 1e-9), so truncation equals llround without FP64 work.
+template <class T>
+__device__ __forceinline__ long long rep_valid(T v) {
+  if constexpr (sizeof(T) == 4) return (long long)v;
+  else return rep_of(v);
+}
+
 // List entries a term of magnitude a needs when an entry holds at most M.
 __device__ __forceinline__ uint32_t entries_for(unsigned long long a, unsigned long long M) {
   if (a <= M) return a != 0 ? 1u : 0u;
@@ -114,12 +123,131 @@ __device__ __forceinline__ void note_list(DevStatus* st, unsigned long long len,
   if (len > cap) atomicMax(&st->list_need, len);
 }
 
+// One element as the validation sees it (kernels.hpp:25-43 on the widened
+// value; matrix.hpp:31-35 for the finite check): *kind = 0 ok, 1 not
+// integer-valued, 2 beyond the exact integer range; *rep = llround (0 for a
+// zero or a value that rounds to 0). NaN: kind 0, rep 0 (reported apart).
+__device__ __forceinline__ void classify(double d, int* kind, long long* rep) {
+  *kind = rep_kind(d);
+  *rep = (*kind == 0 && d == d && d != 0.0) ? llround(d) : 0ll;
+}
+// fp32 without double arithmetic: a float is integer-valued within 1e-9
+// exactly when it is integral (float spacing is >= 2^-24 at |v| >= 0.5) or
+// |v| <= 1e-9 (then it rounds to 0); integral floats convert exactly. (The
+// FP64 rounding of the generic path made k_scan_stats FP64-bound: 108 us at
+// n = 4096 for 128 MB.)
+__device__ __forceinline__ void classify(float v, int* kind, long long* rep) {
+  const float a = fabsf(v);
+  if (rintf(v) == v) {  // integral, +-0 and +-inf included
+    *kind = a > 9007199254740992.0f ? 2 : 0;
+    *rep = *kind == 0 ? (long long)v : 0ll;
+  } else {
+    *kind = (double)a > 1e-9 ? 1 : 0;  // NaN compares false: kind 0
+    *rep = 0;
+  }
+}
+
+// Per-lane state of one row scan (k_scan_stats). Offenders are kept as the
+// lane's first column (its columns ascend), turned into inverted row-major
+// keys once per row.
+struct ScanState {
+  uint32_t nf_j = ~0u;                // first non-finite element
+  uint32_t rb_j = ~0u, rb_kind = 0;   // first rep that fails kernels.hpp:31-40
+  uint32_t rn_j = ~0u;                // first NaN rep
+  uint32_t cnt = 0;                   // nonzero elements (Case B rhs: nnz_k)
+  uint32_t rmx = 0, rneg = 0;         // rep operand: max |rep| (saturated at 255), any < 0
+  uint32_t nzr = 0, big = 0, tmx = 0; // Case A statistics: nonzero reps, > 2048, tile max
+  unsigned long long s = 0;           // Case A: sum |rep| (R_k)
+};
+
+// One element, every check spelled out (fp64, and fp32 elements that leave
+// the fast path below).
+template <class T>
+__device__ __forceinline__ void scan_elem(T x, uint32_t j, bool check_finite, bool is_rep,
+                                          bool is_rhs, bool stats, ScanState& S) {
+  if (check_finite && !isfinite(x) && S.nf_j == ~0u) S.nf_j = j;
+  if (is_rhs) S.cnt += x != T(0) ? 1u : 0u;
+  if (!is_rep) return;
+  int kind;
+  long long r;
+  classify(x, &kind, &r);
+  // (an infinite rep: kind 2, as in the reference)
+  if (kind && S.rb_j == ~0u) {
+    S.rb_j = j;
+    S.rb_kind = (uint32_t)kind;
+  }
+  if (isnan(x) && S.rn_j == ~0u) S.rn_j = j;
+  const unsigned long long a = abs_ll(r);
+  S.rmx = max(S.rmx, a >= 255ull ? 255u : (uint32_t)a);
+  S.rneg |= r < 0 ? 1u : 0u;
+  if (is_rhs && isfinite(x)) {  // Case A (rhs = the reps): R_k; statistics
+    S.s += a;
+    if (stats) {
+      S.nzr += a != 0 ? 1u : 0u;
+      S.big += a > 2048ull ? 1u : 0u;
+      S.tmx = max(S.tmx, a > 2048ull ? 2048u : (uint32_t)a);
+    }
+  }
+}
+
+// Four consecutive elements j0..j0+3 (all < n). fp32 fast path: when the four
+// are finite (and, for the rep operand, integral with |rep| <= 2^24) every
+// check passes and the rep statistics are plain 32-bit arithmetic; anything
+// else takes scan_elem. (k_scan_stats was issue bound at ~60 instructions per
+// element with the generic checks, 86 us for 128 MB at n = 4096.)
+template <class T>
+__device__ __forceinline__ void scan4(const T (&v)[4], uint32_t j0, uint32_t n, bool check_finite,
+                                      bool is_rep, bool is_rhs, bool stats, ScanState& S) {
+  if constexpr (sizeof(T) == 4) {
+    if (j0 + 3 < n) {
+      bool good = true;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float x = v[e], a = fabsf(x);
+        good = good && (is_rep ? (x == rintf(x) && a <= 16777216.0f) : a <= 3.402823466e38f);
+      }
+      if (good) {
+        uint32_t sum = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float x = v[e];
+          if (is_rhs) S.cnt += x != 0.0f ? 1u : 0u;
+          if (is_rep) {
+            const uint32_t a = (uint32_t)fabsf(x);
+            S.rmx = max(S.rmx, min(a, 255u));
+            S.rneg |= x < 0.0f ? 1u : 0u;
+            sum += a;
+            if (stats) {
+              S.nzr += a != 0 ? 1u : 0u;
+              S.big += a > 2048u ? 1u : 0u;
+              S.tmx = max(S.tmx, min(a, 2048u));
+            }
+          }
+        }
+        if (is_rep && is_rhs) S.s += sum;
+        return;
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    if (j0 + e < n) scan_elem(v[e], j0 + e, check_finite, is_rep, is_rhs, stats, S);
+}
+
 // warp task t < (l1 - l0): lhs row l0 + t; then rhs rows q0 .. q1 - 1.
+// fstats (Case A, optional; accumulated): the cost-model statistics of the
+// rhs rows -- nonzero reps, sum over (row, atile-column tile) of the tile's
+// max |rep| (clamped to 2048), reps beyond 2048, sum of |rep| (as
+// k_counts_f16 computes them, so the A-form counts can be built after the
+// choice, only when some row takes the A-form).
 template <class T>
 __global__ void k_scan_stats(const T* __restrict__ lhs, const T* __restrict__ rhs, uint64_t ld,
                              uint32_t n, int which_case, int vec, int check_finite, uint32_t l0,
                              uint32_t l1, uint32_t q0, uint32_t q1, DevStatus* st,
-                             uint32_t* __restrict__ nnz, unsigned long long* __restrict__ rsum) {
+                             uint32_t* __restrict__ nnz, unsigned long long* __restrict__ rsum,
+                             unsigned long long* __restrict__ fstats, uint32_t atile) {
+  constexpr uint32_t U = 4;          // 16-byte loads in flight per lane
+  constexpr uint32_t W = 128 * U;    // columns per warp iteration
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -130,38 +258,29 @@ __global__ void k_scan_stats(const T* __restrict__ lhs, const T* __restrict__ rh
     const T* row = (is_rhs ? rhs : lhs) + i * ld;
     // Case A validates rhs (kernels.hpp:115), Case B lhs (:144)
     const bool is_rep = is_rhs == (which_case == 0);
-    unsigned long long nf = 0, rb = 0, rn = 0;  // inverted keys, 0 = none
-    uint32_t cnt = 0, rmx = 0, rneg = 0;  // rep operand: max |rep| (saturated), any negative
-    unsigned long long s = 0;
-    for (uint32_t j0 = 4 * lane; j0 < n; j0 += 128) {
-      T v[4];
-      load4(row, j0, n, vec != 0, v);
+    const bool stats = is_rhs && which_case == 0 && fstats != nullptr;
+    ScanState S;
+    unsigned long long trip = 0;
+    for (uint32_t c0 = 0; c0 < n; c0 += W) {  // warp-uniform trip count
+      T v[U][4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const uint32_t j = j0 + e;
-        if (j >= n) break;
-        const double d = (double)v[e];
-        const unsigned long long lin = i * (uint64_t)n + j;
-        // ascending j: the first one is the minimum
-        if (check_finite && !isfinite(d) && nf == 0) nf = ~lin;
-        if (is_rep) {
-          const int kind = rep_kind(d);  // (an infinite rep: kind 2, as in the reference)
-          if (kind && rb == 0) rb = ~((lin << 2) | (unsigned long long)kind);
-          if (isnan(d) && rn == 0) rn = ~lin;
-          if (kind == 0 && !isnan(d) && v[e] != T(0)) {
-            const double a = fabs(d);
-            const uint32_t m = a >= 255.0 ? 255u : (uint32_t)llround(a);
-            rmx = m > rmx ? m : rmx;
-            rneg |= (d <= -0.5) ? 1u : 0u;  // llround(d) < 0
-          }
-        }
-        if (is_rhs) {
-          cnt += v[e] != T(0) ? 1u : 0u;
-          if (v[e] != T(0) && isfinite(d) && fabs(d) <= 9007199254740992.0)
-            s += abs_ll(llround(d));
-        }
+      for (uint32_t u = 0; u < U; ++u) load4(row, c0 + u * 128 + 4 * lane, n, vec != 0, v[u]);
+#pragma unroll
+      for (uint32_t u = 0; u < U; ++u)
+        scan4(v[u], c0 + u * 128 + 4 * lane, n, check_finite != 0, is_rep, is_rhs, stats, S);
+      // per-tile max |rep| (A-form trip counts): tiles of atile columns
+      if (stats && ((c0 + W) % atile == 0 || c0 + W >= n)) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) S.tmx = max(S.tmx, __shfl_xor_sync(FULL, S.tmx, o));
+        trip += S.tmx;
+        S.tmx = 0;
       }
     }
+    const unsigned long long base = i * (uint64_t)n;
+    unsigned long long nf = S.nf_j != ~0u ? ~(base + S.nf_j) : 0ull;  // inverted keys, 0 = none
+    unsigned long long rb =
+        S.rb_j != ~0u ? ~(((base + S.rb_j) << 2) | (unsigned long long)S.rb_kind) : 0ull;
+    unsigned long long rn = S.rn_j != ~0u ? ~(base + S.rn_j) : 0ull;
     if (__any_sync(FULL, (nf | rb | rn) != 0)) {
       nf = warp_max_u64(nf);
       rb = warp_max_u64(rb);
@@ -172,7 +291,8 @@ __global__ void k_scan_stats(const T* __restrict__ lhs, const T* __restrict__ rh
         if (rn) atomicMax(&st->rep_nan_inv, rn);
       }
     }
-    if (is_rep && __any_sync(FULL, (rmx | rneg) != 0)) {
+    if (is_rep && __any_sync(FULL, (S.rmx > kGroupMaxRep) || S.rneg != 0)) {
+      uint32_t rmx = S.rmx, rneg = S.rneg;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         rmx = max(rmx, __shfl_xor_sync(FULL, rmx, o));
@@ -185,12 +305,27 @@ __global__ void k_scan_stats(const T* __restrict__ lhs, const T* __restrict__ rh
     }
     if (is_rhs) {
       if (which_case == 1) {
+        uint32_t cnt = S.cnt;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
         if (lane == 0) nnz[i] = cnt;
       } else {
-        s = warp_sum_u64(s);
-        if (lane == 0) rsum[i] = s;
+        const unsigned long long sum = warp_sum_u64(S.s);
+        if (lane == 0) rsum[i] = sum;
+        if (stats) {
+          uint32_t nzr = S.nzr, big = S.big;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            nzr += __shfl_xor_sync(FULL, nzr, o);
+            big += __shfl_xor_sync(FULL, big, o);
+          }
+          if (lane == 0) {
+            if (nzr) atomicAdd(&fstats[0], (unsigned long long)nzr);
+            if (trip) atomicAdd(&fstats[1], trip);
+            if (big) atomicAdd(&fstats[2], (unsigned long long)big);
+            if (sum) atomicAdd(&fstats[3], sum);
+          }
+        }
       }
     }
   }
@@ -220,46 +355,67 @@ __global__ void k_rows(const T* __restrict__ x, uint64_t ld, uint32_t n, int whi
     const bool compact = which_case == 1 && in_slab && lists_needed;
     int2* out = compact ? lists + (i - r0) * cap : nullptr;
     unsigned long long w = 0, z = 0, base = 0;
-    for (uint32_t c0 = 0; c0 < n; c0 += 128) {  // warp-uniform trip count (the scan below)
-      const uint32_t j0 = c0 + 4 * lane;
-      T v[4];
-      load4(row, j0, n, vec != 0, v);
-      long long rep[4];
+    // warp-uniform trip count (the scan below); 4 loads in flight per lane
+    for (uint32_t c1 = 0; c1 < n; c1 += 512) {
+      T vv[4][4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const uint32_t j = j0 + e;
-        rep[e] = j < n ? rep_of(v[e]) : 0;
+      for (uint32_t u = 0; u < 4; ++u) load4(row, c1 + u * 128 + 4 * lane, n, vec != 0, vv[u]);
+#pragma unroll
+      for (uint32_t u = 0; u < 4; ++u) {
+        const uint32_t c0 = c1 + u * 128;
+        const uint32_t j0 = c0 + 4 * lane;
+        const T* v = vv[u];
+        long long rep[4];
+        // Case A: R_k of the four columns as two 16-byte loads (a load per
+        // nonzero element kept k_rows on long-scoreboard stalls)
+        unsigned long long rs[4] = {0ull, 0ull, 0ull, 0ull};
         if (which_case == 0) {
-          if (j < n) {
-            if (v[e] == T(0)) ++z;
-            else w += rsum[j];
-          }
-        } else if (rep[e] != 0) {
-          const unsigned long long nb = nnz[j];
-          w += abs_ll(rep[e]) * nb;  // count bookkeeping, not an element product
-          z += (unsigned long long)n - nb;
-        }
-      }
-      if (compact) {
-        uint32_t ne[4], mine = 0;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          ne[e] = entries_for(abs_ll(rep[e]), kMaxRep);
-          mine += ne[e];
-        }
-        uint32_t total;
-        unsigned long long pos = base + warp_excl_scan(mine, lane, &total);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          if (ne[e] == 1) {
-            if (pos < cap) out[pos] = make_int2((int)(j0 + e), (int)rep[e]);
-            ++pos;
+          if (j0 + 3 < n) {
+            const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(rsum + j0));
+            const ulonglong2 b = __ldg(reinterpret_cast<const ulonglong2*>(rsum + j0 + 2));
+            rs[0] = a.x; rs[1] = a.y; rs[2] = b.x; rs[3] = b.y;
           } else {
-            for (uint32_t c = 0; c < ne[e]; ++c, ++pos)
-              if (pos < cap) out[pos] = make_int2((int)(j0 + e), (int)part_of(rep[e], c, kMaxRep));
+#pragma unroll
+            for (int e = 0; e < 4; ++e) rs[e] = j0 + e < n ? rsum[j0 + e] : 0ull;
           }
         }
-        base += total;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t j = j0 + e;
+          rep[e] = (which_case == 1 && j < n) ? rep_of(v[e]) : 0;
+          if (which_case == 0) {
+            if (j < n) {
+              if (v[e] == T(0)) ++z;
+              else w += rs[e];
+            }
+          } else if (rep[e] != 0) {
+            const unsigned long long nb = nnz[j];
+            w += abs_ll(rep[e]) * nb;  // count bookkeeping, not an element product
+            z += (unsigned long long)n - nb;
+          }
+        }
+        if (compact) {
+          uint32_t ne[4], mine = 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            ne[e] = entries_for(abs_ll(rep[e]), kMaxRep);
+            mine += ne[e];
+          }
+          uint32_t total;
+          unsigned long long pos = base + warp_excl_scan(mine, lane, &total);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (ne[e] == 1) {
+              if (pos < cap) out[pos] = make_int2((int)(j0 + e), (int)rep[e]);
+              ++pos;
+            } else {
+              for (uint32_t c = 0; c < ne[e]; ++c, ++pos)
+                if (pos < cap)
+                  out[pos] = make_int2((int)(j0 + e), (int)part_of(rep[e], c, kMaxRep));
+            }
+          }
+          base += total;
+        }
       }
     }
     w = warp_sum_u64(w);
@@ -349,6 +505,15 @@ __global__ void __launch_bounds__(256)
 // per (group, k), so both builders are plain parallel passes (no compaction);
 // k_bgroup skips the k with index 0. Both exit unless the device-side status
 // chose group mode.
+// A rep of a validated group-mode operand (fp32, 0..kGroupMaxRep): the float
+// is an exact small integer or rounds to 0 (|v| <= 1e-9), so truncation is
+// llround (kernels.hpp:128-130) without the FP64 conversion.
+template <class T>
+__device__ __forceinline__ uint32_t group_rep(T v) {
+  if constexpr (sizeof(T) == 4) return (uint32_t)(int)v;
+  else return (uint32_t)rep_of(v);
+}
+
 __device__ __forceinline__ uint32_t group_digit(int r) {
   return r == 0 ? 1u : r == 1 ? 3u : r == 2 ? 9u : r == 3 ? 256u : 768u;
 }
@@ -375,7 +540,7 @@ __global__ void k_group_idx_rows(const T* __restrict__ x, uint64_t ld, uint32_t 
         load4(x + (r0 + q) * ld, j0, n, vec != 0, v);
 #pragma unroll
         for (int e = 0; e < 4; ++e)
-          if (j0 + e < n) idx[e] += (uint32_t)rep_of(v[e]) * group_digit(r);
+          if (j0 + e < n) idx[e] += group_rep(v[e]) * group_digit(r);
       }
       if (j0 < ldg)  // ldg % 8 == 0: the 4 entries are in range together
         *reinterpret_cast<ushort4*>(gidx + g * ldg + j0) =
@@ -389,15 +554,34 @@ __global__ void k_group_idx_rows(const T* __restrict__ x, uint64_t ld, uint32_t 
 // 32 k x 160 column smem tiles (32 groups per block).
 template <class T>
 __global__ void __launch_bounds__(256)
-    k_group_idx_cols(const T* __restrict__ y, uint64_t ld, uint32_t n,
-                     uint16_t* __restrict__ gidx, uint64_t ldg, const DevStatus* st, int allow) {
+    k_group_idx_cols(const T* __restrict__ y, uint64_t ld, uint32_t n, int vec,
+                     uint16_t* __restrict__ gidx, uint64_t ldg, const DevStatus* st, int allow,
+                     const uint32_t* __restrict__ skip) {
   if (!group_mode(st, allow) || status_failed(st)) return;
+  if (skip && *skip == 0) return;  // the Case A choice left the B-form no rows
   constexpr uint32_t GC = 32 * kGroupRows;  // columns per block
   __shared__ uint8_t tile[32][GC + 1];
   const uint32_t j0 = blockIdx.x * GC, k0 = blockIdx.y * 32;
-  for (uint32_t i = threadIdx.x; i < 32 * GC; i += blockDim.x) {
-    const uint32_t r = i / GC, c = i % GC, k = k0 + r, j = j0 + c;
-    tile[r][c] = (k < n && j < n) ? (uint8_t)rep_of(y[(uint64_t)k * ld + j]) : (uint8_t)0;
+  if (vec && j0 + GC <= n && k0 + 32 <= n) {
+    // whole tile: 16-byte loads, all of a thread's issued before any is used
+    constexpr uint32_t Q = 32 * GC / 4 / 256;  // 16-byte quads per thread (5)
+    T q[Q][4];
+#pragma unroll
+    for (uint32_t u = 0; u < Q; ++u) {
+      const uint32_t idx = threadIdx.x + u * 256, r = idx / (GC / 4), c = (idx % (GC / 4)) * 4;
+      load4(y + (uint64_t)(k0 + r) * ld + j0, c, GC, true, q[u]);
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < Q; ++u) {
+      const uint32_t idx = threadIdx.x + u * 256, r = idx / (GC / 4), c = (idx % (GC / 4)) * 4;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) tile[r][c + e] = (uint8_t)group_rep(q[u][e]);
+    }
+  } else {
+    for (uint32_t i = threadIdx.x; i < 32 * GC; i += blockDim.x) {
+      const uint32_t r = i / GC, c = i % GC, k = k0 + r, j = j0 + c;
+      tile[r][c] = (k < n && j < n) ? (uint8_t)group_rep(y[(uint64_t)k * ld + j]) : (uint8_t)0;
+    }
   }
   __syncthreads();
   const uint32_t gl = threadIdx.x >> 3, kq = (threadIdx.x & 7) * 4;
@@ -427,9 +611,12 @@ __global__ void __launch_bounds__(256)
 // fstats (accumulated): [0] nonzero reps, [1] sum of the per-(k, tile) trip
 // counts, [2] reps beyond 2048, [3] sum of |rep| -- the cost-model inputs.
 template <class T>
-__global__ void k_counts_f16(const T* __restrict__ y, uint64_t ld, uint32_t n, uint32_t tile_cols,
-                             uint32_t ntiles, __half* __restrict__ cnt, uint64_t ldc,
-                             uint16_t* __restrict__ rmax, unsigned long long* __restrict__ fstats) {
+__global__ void k_counts_f16(const T* __restrict__ y, uint64_t ld, uint32_t n, int vec,
+                             uint32_t tile_cols, uint32_t ntiles, __half* __restrict__ cnt,
+                             uint64_t ldc,
+                             uint16_t* __restrict__ rmax, unsigned long long* __restrict__ fstats,
+                             const uint32_t* __restrict__ need) {
+  if (need && *need == 0) return;  // the device-side choice gave the A-form no rows
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -438,19 +625,43 @@ __global__ void k_counts_f16(const T* __restrict__ y, uint64_t ld, uint32_t n, u
     const uint32_t t = (uint32_t)(task % ntiles);
     uint32_t mx = 0, neg = 0, nz = 0, big = 0;
     unsigned long long sum = 0;
-    for (uint32_t c = t * tile_cols + lane; c < (t + 1) * tile_cols && c < n; c += 32) {
-      const T v = y[k * ld + c];
-      long long r = rep_of(v);
-      nz += r != 0 ? 1u : 0u;
-      sum += abs_ll(r);
-      if (r > 2048 || r < -2048) {
-        big += 1;
-        r = r > 0 ? 2048 : -2048;
+    // 4 columns per lane per 16-byte load, all of the tile's loads in flight
+    // (scalar loads left this pass at ~1.2 TB/s)
+    const uint32_t cb = t * tile_cols, ce = min(cb + tile_cols, n);
+    constexpr uint32_t U = 8;
+    for (uint32_t c1 = cb; c1 < ce; c1 += 128 * U) {
+      T v[U][4];
+#pragma unroll
+      for (uint32_t u = 0; u < U; ++u) load4(y + k * ld, c1 + u * 128 + 4 * lane, ce, vec != 0, v[u]);
+#pragma unroll
+      for (uint32_t u = 0; u < U; ++u) {
+        const uint32_t c = c1 + u * 128 + 4 * lane;
+        if (c >= ce) break;
+        __half h[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          long long r = c + e < ce ? rep_valid(v[u][e]) : 0ll;
+          nz += r != 0 ? 1u : 0u;
+          sum += abs_ll(r);
+          if (r > 2048 || r < -2048) {
+            big += 1;
+            r = r > 0 ? 2048 : -2048;
+          }
+          h[e] = __int2half_rn((int)r);
+          const uint32_t a = (uint32_t)(r < 0 ? -r : r);
+          mx = a > mx ? a : mx;
+          neg |= r < 0 ? 1u : 0u;
+        }
+        __half* dst = cnt + k * ldc + c;  // ldc % 64 == 0: 8-byte aligned
+        if (c + 3 < ce) {
+          const __half2 p[2] = {__halves2half2(h[0], h[1]), __halves2half2(h[2], h[3])};
+          *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(p);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (c + e < ce) dst[e] = h[e];
+        }
       }
-      cnt[k * ldc + c] = __int2half_rn((int)r);
-      const uint32_t a = (uint32_t)(r < 0 ? -r : r);
-      mx = a > mx ? a : mx;
-      neg |= r < 0 ? 1u : 0u;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -463,6 +674,7 @@ __global__ void k_counts_f16(const T* __restrict__ y, uint64_t ld, uint32_t n, u
     sum = warp_sum_u64(sum);
     if (lane == 0) {
       rmax[k * ntiles + t] = (uint16_t)(mx | (neg ? 0x8000u : 0u));
+      if (!fstats) continue;
       if (nz) atomicAdd(&fstats[0], (unsigned long long)nz);
       if (mx) atomicAdd(&fstats[1], (unsigned long long)mx);
       if (big) atomicAdd(&fstats[2], (unsigned long long)big);
@@ -478,6 +690,12 @@ __global__ void k_counts_f16(const T* __restrict__ y, uint64_t ld, uint32_t n, u
 // row order), then the B rows in ascending order (identity unless split).
 // scratch: 3 * (n + 2) words.
 constexpr int kChooseThreads = 1024;
+// Dynamic shared memory of k_choose: its scratch when that fits next to the
+// static arrays (n <= 12000: 192 KB), else 0 (global scratch).
+__host__ __device__ inline size_t choose_smem_bytes(uint64_t n) {
+  const size_t b = (4 * (n + 2) + 2) * sizeof(uint32_t);
+  return n <= 12000 ? b : 0;
+}
 constexpr int kChooseCands = 1024;  // split candidates evaluated (j < 1024 B tiles)
 
 __global__ void __launch_bounds__(kChooseThreads)
@@ -485,10 +703,17 @@ __global__ void __launch_bounds__(kChooseThreads)
              const unsigned long long* __restrict__ fstats, uint32_t* __restrict__ scratch,
              uint32_t* __restrict__ plan, uint32_t* __restrict__ ridx, DevStatus* st) {
   __shared__ double s_pre[kChooseCands + 1];
+  __shared__ double s_split[kChooseCands + 1];  // modeled cost of the split with c B tiles
   __shared__ uint32_t s_m, s_vstar, s_tstar;
   __shared__ uint32_t s_wsum[32];
   const uint32_t tid = threadIdx.x, n = (uint32_t)md.n;
   const uint32_t nb = n + 2;  // values 0..n, plus one past the end
+  // the histogram and its prefix sums live in shared memory when they fit
+  // (the launcher sizes the dynamic smem; global scratch otherwise): the
+  // binary searches over `cum` below are serial dependent loads, ~30 cycles
+  // each from smem against ~600 from L2 (k_choose took 54 us at n = 4096)
+  extern __shared__ __align__(8) uint32_t s_dyn[];
+  if (choose_smem_bytes(n)) scratch = s_dyn;
   uint32_t* hist = scratch;             // count of rows per nonzero-base value
   uint32_t* cum = scratch + nb;         // rows with value < v (then: next A slot of value v)
   unsigned long long* csum = reinterpret_cast<unsigned long long*>(scratch + 2 * nb);  // 8-byte aligned
@@ -500,7 +725,15 @@ __global__ void __launch_bounds__(kChooseThreads)
 
   for (uint32_t v = tid; v < nb; v += kChooseThreads) hist[v] = 0;
   __syncthreads();
-  for (uint32_t i = tid; i < rows; i += kChooseThreads) atomicAdd(&hist[min(nnz_row[i], n)], 1u);
+  // warp-aggregated: rows of equal density (all of them when X is dense) would
+  // otherwise serialise on one counter
+  for (uint32_t i0 = 0; i0 < rows; i0 += kChooseThreads) {
+    const uint32_t i = i0 + tid;
+    const uint32_t v = i < rows ? min(nnz_row[i], n) : 0xffffffffu;
+    const unsigned peers = __match_any_sync(FULL, v);
+    if (v != 0xffffffffu && (tid & 31) == (uint32_t)(__ffs(peers) - 1))
+      atomicAdd(&hist[v], (uint32_t)__popc(peers));
+  }
   __syncthreads();
   // exclusive scans over the values: each thread a contiguous chunk
   const uint32_t per = (nb + kChooseThreads - 1) / kChooseThreads;
@@ -567,18 +800,23 @@ __global__ void __launch_bounds__(kChooseThreads)
     return (double)csum[lo] + (double)lo * (double)(m - cum[lo]);
   };
   const uint64_t tb = md.tile_rows();
-  // candidate c: c = 0 -> m = rows (pure A), c = j >= 1 -> m = rows - j * tb
+  // candidate c: c = 0 -> m = rows (pure A), c = j >= 1 -> m = rows - j * tb;
+  // each thread prices its own split (thread 0 alone took ~20 us: 64-bit
+  // divisions in the wave quantisation of every candidate)
   for (uint32_t c = tid; c <= kChooseCands; c += kChooseThreads) {
     const uint64_t m = c == 0 ? rows : (uint64_t)rows - (uint64_t)c * tb;
-    s_pre[c] = (c == 0 || (uint64_t)c * tb < rows) ? pre_of(m, nullptr) : 0.0;
+    const bool ok = c == 0 || (uint64_t)c * tb < rows;
+    s_pre[c] = ok ? pre_of(m, nullptr) : 0.0;
+    s_split[c] = (ok && c > 0) ? md.cost_a(m, s_pre[c]) + md.cost_b(c) : 0.0;
   }
   __syncthreads();
   if (tid == 0) {
     uint64_t m = 0;
     if (a_ok && rows > 0 && (rows - 1) / tb < (uint64_t)kChooseCands) {
-      m = choose_aform_rows(md, rows, variant, [&](uint64_t mm) {
-        return mm == rows ? s_pre[0] : s_pre[(rows - mm) / tb];
-      });
+      m = choose_aform_rows(
+          md, rows, variant,
+          [&](uint64_t mm) { return mm == rows ? s_pre[0] : s_pre[(rows - mm) / tb]; }, nullptr,
+          s_split);
     }
     s_m = (uint32_t)m;
     plan[0] = (uint32_t)m;
@@ -648,24 +886,29 @@ __global__ void k_acompact(const T* __restrict__ x, uint64_t ld, uint32_t n, int
     const T* row = x + (r0 + q) * ld;
     auto* out = lists + q * cap;
     uint32_t base = 0;
-    for (uint32_t c0 = 0; c0 < n; c0 += 128) {
-      const uint32_t j0 = c0 + 4 * lane;
-      T v[4];
-      load4(row, j0, n, vec != 0, v);
-      const uint32_t mine = (v[0] != T(0)) + (v[1] != T(0)) + (v[2] != T(0)) + (v[3] != T(0));
-      uint32_t total;
-      uint32_t pos = base + warp_excl_scan(mine, lane, &total);
+    for (uint32_t c1 = 0; c1 < n; c1 += 512) {  // 4 loads in flight per lane
+      T vv[4][4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        if (v[e] == T(0)) continue;
-        if constexpr (sizeof(T) == 4) {
-          out[pos++] = make_int2((int)(j0 + e), __float_as_int((float)v[e]));
-        } else {
-          const double d = (double)v[e];
-          out[pos++] = make_int4((int)(j0 + e), 0, __double2loint(d), __double2hiint(d));
+      for (uint32_t u = 0; u < 4; ++u) load4(row, c1 + u * 128 + 4 * lane, n, vec != 0, vv[u]);
+#pragma unroll
+      for (uint32_t u = 0; u < 4; ++u) {
+        const uint32_t j0 = c1 + u * 128 + 4 * lane;
+        const T* v = vv[u];
+        const uint32_t mine = (v[0] != T(0)) + (v[1] != T(0)) + (v[2] != T(0)) + (v[3] != T(0));
+        uint32_t total;
+        uint32_t pos = base + warp_excl_scan(mine, lane, &total);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (v[e] == T(0)) continue;
+          if constexpr (sizeof(T) == 4) {
+            out[pos++] = make_int2((int)(j0 + e), __float_as_int((float)v[e]));
+          } else {
+            const double d = (double)v[e];
+            out[pos++] = make_int4((int)(j0 + e), 0, __double2loint(d), __double2hiint(d));
+          }
         }
+        base += total;
       }
-      base += total;
     }
     if (lane == 0) counts[q] = base;
   }
@@ -753,12 +996,14 @@ int vec_ok(const T* p, uint64_t ld) {
 template <class T>
 void launch_scan_stats(const T* lhs, const T* rhs, uint64_t ld, uint32_t n, int which_case,
                        uint32_t l0, uint32_t l1, uint32_t q0, uint32_t q1, DevStatus* st,
-                       uint32_t* nnz, unsigned long long* rsum, cudaStream_t s, int check_finite) {
+                       uint32_t* nnz, unsigned long long* rsum, cudaStream_t s, int check_finite,
+                       unsigned long long* fstats) {
   const int vec = vec_ok(lhs, ld) & vec_ok(rhs, ld);
   const uint64_t tasks = (uint64_t)(l1 - l0) + (q1 - q0);
   if (tasks == 0) return;
   k_scan_stats<T><<<grid_for_warps(tasks, 8), 256, 0, s>>>(
-      lhs, rhs, ld, n, which_case, vec, check_finite, l0, l1, q0, q1, st, nnz, rsum);
+      lhs, rhs, ld, n, which_case, vec, check_finite, l0, l1, q0, q1, st, nnz, rsum, fstats,
+      aform_tile_cols<T>());
   note_launch();
 }
 
@@ -778,7 +1023,7 @@ void launch_rows(const T* x, uint64_t ld, uint32_t n, int which_case, const uint
 template <class T>
 void launch_group_idx(const T* rep, uint64_t ld, uint32_t n, int which_case, uint32_t r0,
                       uint32_t rows, uint16_t* gidx, uint64_t ldg, const DevStatus* st, int allow,
-                      cudaStream_t s) {
+                      cudaStream_t s, const uint32_t* skip) {
   if (which_case == 1) {
     const uint32_t ngroups = (rows + kGroupRows - 1) / kGroupRows;
     if (ngroups == 0) return;
@@ -787,17 +1032,19 @@ void launch_group_idx(const T* rep, uint64_t ld, uint32_t n, int which_case, uin
   } else {
     const uint32_t ngroups = (n + kGroupRows - 1) / kGroupRows;
     dim3 grid((ngroups + 31) / 32, (uint32_t)((ldg + 31) / 32));
-    k_group_idx_cols<T><<<grid, 256, 0, s>>>(rep, ld, n, gidx, ldg, st, allow);
+    k_group_idx_cols<T><<<grid, 256, 0, s>>>(rep, ld, n, vec_ok(rep, ld), gidx, ldg, st, allow,
+                                             skip);
   }
   note_launch();
 }
 
 template <class T>
 void launch_counts_f16(const T* y, uint64_t ld, uint32_t n, uint32_t tile_cols, __half* cnt,
-                       uint64_t ldc, uint16_t* rmax, unsigned long long* fstats, cudaStream_t s) {
+                       uint64_t ldc, uint16_t* rmax, unsigned long long* fstats, cudaStream_t s,
+                       const uint32_t* need) {
   const uint32_t ntiles = (n + tile_cols - 1) / tile_cols;
   k_counts_f16<T><<<grid_for_warps((uint64_t)n * ntiles, 8), 256, 0, s>>>(
-      y, ld, n, tile_cols, ntiles, cnt, ldc, rmax, fstats);
+      y, ld, n, vec_ok(y, ld), tile_cols, ntiles, cnt, ldc, rmax, fstats, need);
   note_launch();
 }
 
@@ -806,8 +1053,11 @@ size_t choose_scratch_bytes(uint64_t n) { return (4 * (n + 2) + 2) * sizeof(uint
 void launch_choose(const CaseAModel& md, uint32_t rows, int variant, const uint32_t* nnz_row,
                    const unsigned long long* fstats, uint32_t* scratch, uint32_t* plan,
                    uint32_t* ridx, DevStatus* st, cudaStream_t s) {
-  k_choose<<<1, kChooseThreads, 0, s>>>(md, rows, variant, nnz_row, fstats, scratch, plan, ridx,
-                                        st);
+  const size_t smem = choose_smem_bytes(md.n);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_choose, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_choose<<<1, kChooseThreads, smem, s>>>(md, rows, variant, nnz_row, fstats, scratch, plan, ridx,
+                                           st);
   note_launch();
 }
 
@@ -858,15 +1108,18 @@ void launch_reduce_slices(const T* part, uint64_t stride, uint64_t ld_part, uint
 #define INSTANTIATE(T)                                                                         \
   template void launch_scan_stats<T>(const T*, const T*, uint64_t, uint32_t, int, uint32_t,    \
                                      uint32_t, uint32_t, uint32_t, DevStatus*, uint32_t*,      \
-                                     unsigned long long*, cudaStream_t, int);                  \
+                                     unsigned long long*, cudaStream_t, int,                   \
+                                     unsigned long long*);                                     \
   template void launch_rows<T>(const T*, uint64_t, uint32_t, int, const uint32_t*,             \
                                const unsigned long long*, uint32_t, uint32_t, uint32_t,        \
                                uint32_t, int2*, uint64_t, uint32_t*, unsigned long long*,      \
                                DevStatus*, cudaStream_t, uint32_t*, int);                      \
   template void launch_group_idx<T>(const T*, uint64_t, uint32_t, int, uint32_t, uint32_t,     \
-                                    uint16_t*, uint64_t, const DevStatus*, int, cudaStream_t); \
+                                    uint16_t*, uint64_t, const DevStatus*, int, cudaStream_t,  \
+                                    const uint32_t*);                                          \
   template void launch_counts_f16<T>(const T*, uint64_t, uint32_t, uint32_t, __half*, uint64_t, \
-                                     uint16_t*, unsigned long long*, cudaStream_t);            \
+                                     uint16_t*, unsigned long long*, cudaStream_t,             \
+                                     const uint32_t*);                                         \
   template void launch_acompact<T>(const T*, uint64_t, uint32_t, uint32_t, uint32_t,           \
                                    const uint32_t*, const uint32_t*,                           \
                                    typename AEntry<T>::type*, uint64_t, uint32_t*,             \

@@ -650,9 +650,24 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
   // + the per-k vector of the work formulas, one pass over both operands
   auto* nnz = c->vec_k.as<uint32_t>();
   auto* rsum = c->vec_k.as<unsigned long long>();
+  // Case A: the device-side A-form / B-form choice (k_choose) for n >= 1024 or
+  // when forced by AFMM_BFORM=aform|hybrid. (Fast mode keeps the B-form: its
+  // blocked fp64 totals bound the fp32 chain error, DESIGN 3.2; the A-form's
+  // chains are the order-preserving ones, and on sparse rows of n = 8192 they
+  // drift to 2.6e-5 of sum |terms|.)
+  const bool choose = call.which == AFMM_CASE_A && rows > 0 && call.mode != AFMM_MODE_FAST &&
+                      (c->variant == kAForm || c->variant == kHybrid ||
+                       (c->variant == kAuto && n >= 1024));
+  // its statistics come out of the validation pass; the A-form's fp16 counts
+  // are then built after the choice, only when some row takes the A-form
+  const bool stats_in_scan = choose && !call.have_counts && !call.prevalidated;
+  if (choose) CK(c->fstats.ensure(4 * sizeof(unsigned long long)), "workspace");
+  if (stats_in_scan)
+    CK(cudaMemsetAsync(c->fstats.p, 0, 4 * sizeof(unsigned long long), s), "memset");
   if (!call.prevalidated)
     afmm_dev::launch_scan_stats<T>(lhs, rhs, ld, n32, call.which == AFMM_CASE_B ? 1 : 0, 0, n32, 0,
-                                   n32, st, nnz, rsum, s, call.check_finite ? 1 : 0);
+                                   n32, st, nnz, rsum, s, call.check_finite ? 1 : 0,
+                                   stats_in_scan ? c->fstats.as<unsigned long long>() : nullptr);
 
   if (call.which == AFMM_CASE_B) {
     // rep = X[i,k] (lhs), bases = Y[k,:] (rhs): B-form directly.
@@ -700,12 +715,6 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
     using E = typename afmm_dev::AEntry<T>::type;
     const uint32_t tc = afmm_dev::aform_tile_cols<T>();
     const uint64_t ntiles = (n + tc - 1) / tc, ldc = round_up(n, 64);
-    // (fast mode keeps the B-form: its blocked fp64 totals bound the fp32 chain
-    // error, §3.2; the A-form's chains are the order-preserving ones, and on
-    // sparse rows of n = 8192 they drift to 2.6e-5 of sum |terms|)
-    const bool choose = rows > 0 && call.mode != AFMM_MODE_FAST &&
-                        (c->variant == kAForm || c->variant == kHybrid ||
-                         (c->variant == kAuto && n >= 1024));
     // B part: B-form rows = Z columns j (rep list = column j of Y), B-form
     // columns = the slab's B rows (bases X[i,k], gathered through ridx)
     const int shape = pick_shape(c->variant, n, std::max<uint64_t>(rows, 1), sizeof(T), sms);
@@ -718,13 +727,12 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
     if (choose) {
       CK(c->cnt16.ensure(n * ldc * sizeof(__half)), "workspace");
       CK(c->rmax.ensure(n * ntiles * sizeof(uint16_t)), "workspace");
-      CK(c->fstats.ensure(4 * sizeof(unsigned long long)), "workspace");
       CK(c->plan.ensure(4 * sizeof(uint32_t)), "workspace");
       CK(c->ridx.ensure(rows * 4), "workspace");
       CK(c->scratch.ensure(afmm_dev::choose_scratch_bytes(n)), "workspace");
       CK(c->alists.ensure(rows * n * sizeof(E)), "workspace");
       auto* fs = c->fstats.as<unsigned long long>();
-      if (!call.have_counts) {
+      if (!call.have_counts && !stats_in_scan) {
         CK(cudaMemsetAsync(fs, 0, 4 * sizeof(unsigned long long), s), "memset");
         afmm_dev::launch_counts_f16<T>(rhs, ld, n32, tc, c->cnt16.as<__half>(), ldc,
                                        c->rmax.as<uint16_t>(), fs, s);
@@ -737,6 +745,9 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
                               c->ridx.as<uint32_t>(), st, s);
       plan = c->plan.as<uint32_t>();
       ridx = c->ridx.as<uint32_t>();
+      if (stats_in_scan)  // the A-form's counts, only when it got rows (plan[0])
+        afmm_dev::launch_counts_f16<T>(rhs, ld, n32, tc, c->cnt16.as<__half>(), ldc,
+                                       c->rmax.as<uint16_t>(), nullptr, s, plan);
       // the A rows' compacted nonzero bases (k, X[i,k])
       afmm_dev::launch_acompact<T>(lhs, ld, n32, (uint32_t)r0, (uint32_t)rows, plan, ridx,
                                    c->alists.as<E>(), n, c->acounts.as<uint32_t>(), s);
@@ -754,7 +765,7 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
         const uint64_t ldg = group_ldg(n), ngroups = (n + afmm_dev::kGroupRows - 1) / afmm_dev::kGroupRows;
         CK(c->gidx.ensure(ngroups * ldg * sizeof(uint16_t)), "workspace");
         afmm_dev::launch_group_idx<T>(rhs, ld, n32, 0, 0, n32, c->gidx.as<uint16_t>(), ldg, st,
-                                      gallow, s);
+                                      gallow, s, plan ? plan + 1 : nullptr);
       }
       afmm_dev::launch_transpose<T>(lhs + r0 * ld, ld, (uint32_t)rows, n32, c->xt.as<T>(), lds, s,
                                     ridx, nullptr, nullptr, plan, plan ? 1 : 0);
