@@ -503,12 +503,24 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
 // waste of the B-form is larger (sparse X).
 // ---------------------------------------------------------------------------
 
+// k rows of fp16 counts per A-form ring stage (the ring keeps 96 k rows:
+// 192 KB). A row of cfg3 d1 = 0.1 has ~1 nonzero base per 8 k, so with
+// 8-row stages every entry paid a stage hand-off (arrive + wait); 32-row
+// stages (3 of them) measured cfg3 d1 = 0.1 mu = 1 / 4 / 16: 1.497 -> 1.341 /
+// 3.678 -> 3.569 / 12.66 -> 12.71 ms, cfg4 130.05 -> 130.31 ms (16-row: 1.378
+// / 3.577 / 12.62 / 130.03).
+#ifndef AFMM_AKB
+#define AFMM_AKB 32
+#endif
+constexpr int AKB = AFMM_AKB;
+constexpr int ASTAGES = 96 / AKB;
+
 template <class T>
 struct AformGeo {
   static constexpr int CPL = sizeof(T) == 4 ? 32 : 16;  // columns per lane
   static constexpr int TILE = 32 * CPL;                 // columns per CTA
   static constexpr int NBOX = TILE / 256;               // 256-half TMA boxes per k row
-  static constexpr int STAGE_BYTES = KB * TILE * 2;
+  static constexpr int STAGE_BYTES = AKB * TILE * 2;
   static constexpr int NPAIR = CPL / 2;                 // f16x2 count registers per lane
   static constexpr int NGRP = CPL / 8;                  // 128-bit count loads per entry
 };
@@ -604,8 +616,8 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
         mbar_arrive_expect_tx(&full[slot], (uint32_t)Ag::STAGE_BYTES);
 #pragma unroll
         for (int bx = 0; bx < Ag::NBOX; ++bx)
-          tma_load_2d(base + slot * Ag::STAGE_BYTES + bx * KB * 512, &cmap, &full[slot],
-                      tile_c + bx * 256, (int32_t)(i * KB));
+          tma_load_2d(base + slot * Ag::STAGE_BYTES + bx * AKB * 512, &cmap, &full[slot],
+                      tile_c + bx * 256, (int32_t)(i * AKB));
       }
     }
     return;
@@ -651,8 +663,8 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
     const E ent_n = shfl_entry(cur, f & 31u);
     const uint32_t rm_n = f < cnt ? __ldg(rm_col + (uint64_t)(uint32_t)ent_n.x * ntiles) : 0u;
     const uint32_t k = (uint32_t)ent.x;
-    const uint32_t kb = k / KB;
-    AFMM_CHECK(st, k < nkb * KB && kb >= kb_cur && cnt <= cap);
+    const uint32_t kb = k / AKB;
+    AFMM_CHECK(st, k < nkb * AKB && kb >= kb_cur && cnt <= cap);
     while (kb_cur < kb) {
       advance();
       mbar_sleep_wait_at(full0 + slot * 8, phase);
@@ -665,7 +677,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
         uint32_t v0, v1, v2, v3;
         asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                      : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
-                     : "r"(stage_addr + g * KB * 512 + (k % KB) * 512));
+                     : "r"(stage_addr + g * AKB * 512 + (k % AKB) * 512));
         c2[4 * g] = v0;
         c2[4 * g + 1] = v1;
         c2[4 * g + 2] = v2;
@@ -872,6 +884,7 @@ cudaError_t launch_ring(BformLaunch& a, T* out, cudaStream_t s) {
 
 int bform_box_bytes() { return BOX_BYTES; }
 int bform_kb() { return KB; }
+int aform_kb() { return AKB; }
 
 template <class T>
 cudaError_t launch_bform(BformLaunch& a, T* out, cudaStream_t s) {
@@ -932,13 +945,13 @@ cudaError_t launch_aform(const CUtensorMap* cmap, const typename AEntry<T>::type
   static_assert(Ag::TILE == (int)aform_tile_cols<T>(), "A-form tile width");
   // 16 rows x 12 stages x 1 CTA/SM: 4-5% faster than 8 rows x 6 stages x 2
   // CTAs/SM on cfg3 d1 = 0.1 (tools/exp_time.py --aform)
-  constexpr int CW = kAformRows, STAGES = 12, MINB = kAformCtasPerSm;
+  constexpr int CW = kAformRows, STAGES = ASTAGES, MINB = kAformCtasPerSm;
   auto kern = k_aform<T, CW, STAGES, MINB>;
   const size_t smem = 128 + (size_t)STAGES * Ag::STAGE_BYTES + 2 * STAGES * sizeof(uint64_t);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  const uint32_t nkb = (nk + KB - 1) / KB;
+  const uint32_t nkb = (nk + AKB - 1) / AKB;
   const uint32_t tiles = (ncols + Ag::TILE - 1) / Ag::TILE;
   const uint32_t rpc = balanced_rows(nrows, tiles, CW, MINB);
   dim3 grid((nrows + rpc - 1) / rpc, tiles);

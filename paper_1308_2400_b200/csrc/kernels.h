@@ -12,7 +12,8 @@
 
 namespace afmm_dev {
 
-void note_launch();  // counts library kernel launches (runtime.cu)
+void note_launch();  // counts library kernel launches, records launch errors (runtime.cu)
+cudaError_t take_launch_error();  // first launch error of this host thread since the last call
 
 // Rows [l0, l1) of lhs and [q0, q1) of rhs: finite check (check_finite; a
 // NaN rep is recorded either way), rep validation
@@ -70,7 +71,7 @@ void launch_counts_f16(const T* y, uint64_t ld, uint32_t n, uint32_t tile_cols, 
 // Device-side Case A choice (costmodel.h): plan[0] = A-form rows, plan[1] =
 // B-form rows, ridx = the slab row order (A rows first), st->a_rows.
 size_t choose_scratch_bytes(uint64_t n);
-void launch_choose(const CaseAModel& md, uint32_t rows, int variant, const uint32_t* nnz_row,
+cudaError_t launch_choose(const CaseAModel& md, uint32_t rows, int variant, const uint32_t* nnz_row,
                    const unsigned long long* fstats, uint32_t* scratch, uint32_t* plan,
                    uint32_t* ridx, DevStatus* st, cudaStream_t s);
 // Compacted nonzero bases (k, X[r0 + q, k]) of slab rows q = rows_idx[t]
@@ -100,6 +101,7 @@ cudaError_t launch_aform(const CUtensorMap* cmap, const typename AEntry<T>::type
 // bform_box_bytes() bytes.
 int bform_kb();
 int bform_box_bytes();
+int aform_kb();  // k rows per A-form stage (the fp16 count map's box height)
 
 // k_bform tile shapes: narrow = 512 fp32 / 256 fp64 columns, 2 CTAs per SM;
 // wide = 1024 / 512 columns, 1 CTA per SM; small = 256 / 128 columns x 4 rows

@@ -1050,15 +1050,22 @@ void launch_counts_f16(const T* y, uint64_t ld, uint32_t n, uint32_t tile_cols, 
 
 size_t choose_scratch_bytes(uint64_t n) { return (4 * (n + 2) + 2) * sizeof(uint32_t); }
 
-void launch_choose(const CaseAModel& md, uint32_t rows, int variant, const uint32_t* nnz_row,
+cudaError_t launch_choose(const CaseAModel& md, uint32_t rows, int variant, const uint32_t* nnz_row,
                    const unsigned long long* fstats, uint32_t* scratch, uint32_t* plan,
                    uint32_t* ridx, DevStatus* st, cudaStream_t s) {
+  // the static arrays (16.8 KB) count against the default 48 KB as well: set
+  // the opt-in size for every dynamic size (a first call at n = 2100 -- 33.6
+  // KB dynamic -- failed to launch before any call had raised the limit)
   const size_t smem = choose_smem_bytes(md.n);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_choose, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (smem > 0) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(k_choose, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
   k_choose<<<1, kChooseThreads, smem, s>>>(md, rows, variant, nnz_row, fstats, scratch, plan, ridx,
                                            st);
   note_launch();
+  return cudaGetLastError();
 }
 
 template <class T>

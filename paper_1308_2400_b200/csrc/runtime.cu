@@ -31,7 +31,25 @@ using afmm_dev::DevStatus;
 
 namespace afmm_dev {
 static std::atomic<uint64_t> g_launches{0};
-void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+// Launch errors (a bad configuration, too much shared memory) are recorded
+// right after each launch: the runtime's last-error state does not survive a
+// later successful call -- a cudaFuncSetAttribute resets it (measured: a
+// k_choose launch failure was wiped by the next kernel's attribute call and
+// the product returned untouched output) -- so checking once at the end of
+// the enqueue is not enough. Per host thread (the multi-device shards enqueue
+// from their own threads).
+static thread_local cudaError_t t_launch_err = cudaSuccess;
+void note_launch() {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  const cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess && t_launch_err == cudaSuccess) t_launch_err = e;
+}
+// The first launch error since the last call (and clear it).
+cudaError_t take_launch_error() {
+  const cudaError_t e = t_launch_err;
+  t_launch_err = cudaSuccess;
+  return e;
+}
 }  // namespace afmm_dev
 
 namespace {
@@ -180,7 +198,7 @@ bool make_count_tmap(CUtensorMap* map, const __half* cnt, uint64_t rows, uint64_
   if (!fn) return false;
   const cuuint64_t gdim[2] = {cols, rows};
   const cuuint64_t gstride[1] = {ldc * sizeof(__half)};
-  const cuuint32_t box[2] = {256, (cuuint32_t)afmm_dev::bform_kb()};
+  const cuuint32_t box[2] = {256, (cuuint32_t)afmm_dev::aform_kb()};
   const cuuint32_t estride[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(cnt), gdim,
                   gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -637,6 +655,7 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
   c->timed_last = c->timing;
   for (int i = 0; i < 4; ++i) c->last_ev[i] = c->rec_ev[i];
   c->mark(0);
+  afmm_dev::take_launch_error();  // (a stale one belongs to no product)
   CK(cudaMemsetAsync(st, 0, sizeof(DevStatus), s), "memset");
   const int gallow = group_allow(c, call);
   if (call.prevalidated && gallow) {
@@ -739,10 +758,10 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
       }
       afmm_dev::CaseAModel md = case_a_model(sizeof(T), n, sms, shape);
       md.group_allow = gallow;
-      afmm_dev::launch_choose(md, (uint32_t)rows,
-                              choose_variant(c->variant), c->acounts.as<uint32_t>(), fs,
-                              c->scratch.as<uint32_t>(), c->plan.as<uint32_t>(),
-                              c->ridx.as<uint32_t>(), st, s);
+      CK(afmm_dev::launch_choose(md, (uint32_t)rows, choose_variant(c->variant),
+                                 c->acounts.as<uint32_t>(), fs, c->scratch.as<uint32_t>(),
+                                 c->plan.as<uint32_t>(), c->ridx.as<uint32_t>(), st, s),
+         "choose");
       plan = c->plan.as<uint32_t>();
       ridx = c->ridx.as<uint32_t>();
       if (stats_in_scan)  // the A-form's counts, only when it got rows (plan[0])
@@ -803,6 +822,7 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
   }
   c->mark(3);
   CK(cudaGetLastError(), "launch");
+  CK(afmm_dev::take_launch_error(), "launch");
   CK(cudaMemcpyAsync(c->status_host, st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s),
      "status readback");
   c->last = call;
@@ -1426,6 +1446,7 @@ afmm_status host_product_multi(int which, const T* lhs, const T* rhs, uint64_t n
                                      which == AFMM_CASE_B ? 1 : 0, (uint32_t)a0, (uint32_t)a1,
                                      (uint32_t)a0, (uint32_t)a1, st, c->vec_k.as<uint32_t>(),
                                      c->vec_k.as<unsigned long long>(), s, check_finite ? 1 : 0);
+    if (ce == cudaSuccess) ce = afmm_dev::take_launch_error();
     if (ce == cudaSuccess) ce = cudaEventRecord(ev_a[g], s);
     if (ce != cudaSuccess) fail(ce, "afmm: shard setup");
     bar.wait();  // every chunk's copy and scan is enqueued (events recorded)
@@ -1475,6 +1496,7 @@ afmm_status host_product_multi(int which, const T* lhs, const T* rhs, uint64_t n
           ce = cudaMemcpyAsync(c->stats_host, c->fstats.p, 4 * sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, s);
       }
+      if (ce == cudaSuccess) ce = afmm_dev::take_launch_error();
       if (ce == cudaSuccess && a1 > a0)
         ce = cudaMemcpyAsync(work.data() + a0, c->work.as<uint64_t>() + a0, (a1 - a0) * 8,
                              cudaMemcpyDeviceToHost, s);
@@ -1857,6 +1879,7 @@ template <class T>
 afmm_status row_stats(afmm_context* c, int which, const T* lhs, const T* rhs, uint64_t n,
                       uint64_t ld, uint64_t* work_host, std::vector<uint32_t>* nnz_row,
                       unsigned long long* fstats, afmm_error* err) {
+  afmm_dev::take_launch_error();
   CK(c->vec_k.ensure(n * 8), "workspace");
   CK(c->work.ensure(n * 8), "workspace");
   CK(c->status.ensure(sizeof(DevStatus)), "workspace");
@@ -1888,6 +1911,7 @@ afmm_status row_stats(afmm_context* c, int which, const T* lhs, const T* rhs, ui
        "readback");
     CK(cudaMemcpyAsync(c->stats_host, c->fstats.p, 4 * 8, cudaMemcpyDeviceToHost, s), "readback");
   }
+  CK(afmm_dev::take_launch_error(), "launch");
   CK(cudaStreamSynchronize(s), "work readback");
   if (fstats && nnz_row) std::memcpy(fstats, c->stats_host, 4 * 8);
   return AFMM_OK;

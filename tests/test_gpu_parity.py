@@ -1009,3 +1009,37 @@ def test_no_write_outside_the_output(cuda, oracle, monkeypatch, variant, dt):
         pinned = torch.full((n + 4, n), sentinel, dtype=tdt).pin_memory().numpy()
         afmm.afmm_case_b(reps, bases, out=pinned[2:2 + n])
         assert np.all(pinned[:2] == sentinel) and np.all(pinned[2 + n:] == sentinel)
+
+
+@pytest.mark.parametrize("n", [2100, 1300])
+def test_first_product_in_a_fresh_process(cuda, n, tmp_path):
+    """The first Case A product of a process (no earlier call has raised any
+    kernel's shared-memory limit) with the device-side choice at sizes whose
+    k_choose scratch sits in shared memory: bit-exact, not silently empty. (A
+    k_choose launch that exceeded the default 48 KB failed, and the failure was
+    wiped from the runtime's error state by the next cudaFuncSetAttribute;
+    launch errors are now recorded right after every launch.)"""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "first.py"
+    script.write_text(f"""
+import sys
+sys.path.insert(0, {root!r})
+import numpy as np, torch
+import paper_1308_2400_b200 as afmm
+from oracle.oracle import Oracle
+from paper_1308_2400_b200.gen import make_inputs
+lhs, rhs = make_inputs("cfg4", seed=4, n={n})
+ctx = afmm.DeviceContext(0)
+L, R = torch.from_numpy(lhs).cuda(), torch.from_numpy(rhs).cuda()
+O = torch.zeros_like(L)
+c = ctx.product("a", L, R, O)
+z, cc = Oracle().product_mt("a", lhs, rhs, 0, {n}, 16)
+assert (c.additions, 0, c.zero_skips) == cc
+assert np.array_equal(O.cpu().numpy().view(np.uint8), z.view(np.uint8)), ctx.last_form()
+print("ok", ctx.last_form())
+""")
+    r = subprocess.run([sys.executable, str(script)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
