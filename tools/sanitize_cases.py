@@ -8,8 +8,9 @@ tool lets finish also proves the result), and covers one path of the library:
 the three B-form tile shapes (Case B and Case A on transposed operands), the
 A-form, the device-side row split, the reassociated fast mode (split-k +
 reduce), CUDA-graph replays, a validation error (kernels exit early), the
-zero-copy page-locked output, and the multi-device host path (several shards
-on one device: chunked copies, peer completion, cut, per-shard product).
+zero-copy page-locked output, the multi-device host path (several shards
+on one device: chunked copies, peer completion, cut, per-shard product), and
+the small-rep group kernel (both cases and a split).
 """
 import os
 import sys
@@ -72,6 +73,13 @@ device("case A fp32 fast mode", "a", l4, r4, mode="fast")
 device("case B fp64 fast mode", "b", l2, r2, mode="fast")
 device("case B graph replays", "b", l2, r2, reps=4)
 device("case A graph replays", "a", la, ra, reps=4)
+# the small-rep group kernel (every rep in 0..2): Case A (column groups, ragged
+# tiles), Case B (row groups), and the split with a group B part
+lg, rg = make_inputs("cfg3", seed=1, n=777, d1=1.0, mu=1)
+device("case A group kernel", "a", lg, rg)
+device("case B group kernel", "b", rg.T.copy(), lg)
+lh, rh = make_inputs("cfg3", seed=2, n=1100, d1=0.5, mu=1)
+device("case A split with group B part (forced)", "a", lh, rh, "hybrid")
 os.environ.pop("AFMM_BFORM", None)
 
 bad = l2.copy()
