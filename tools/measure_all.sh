@@ -23,7 +23,8 @@ for spec in "cfg1" "cfg2" "cfg4" "cfg5" "cfg3 --d1 0.1 --mu 1" "cfg3 --d1 0.1 --
     ncu --metrics $NCU_M --print-units base --clock-control none --csv --log-file $D/launches_$tag.csv python tools/profile_one.py $spec > /dev/null 2>&1
   fi
 done
-# full captures of the two repeated-addition kernels (already run above without ncu)
+# full captures of the three repeated-addition kernels (already run above without ncu)
 ncu --set full --clock-control none --import-source on -k regex:k_aform -c 1 -f -o $D/prof_aform_cfg3_d0.1_mu4 python tools/profile_one.py cfg3 --d1 0.1 --mu 4 > $D/ncu_aform.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_bform -c 1 -f -o $D/prof_bform_cfg5_n4096 python tools/profile_one.py cfg5 --n 4096 > $D/ncu_bform.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_bgroup -c 1 -f -o $D/prof_bgroup_cfg3_d1.0_mu1 python tools/profile_one.py cfg3 --d1 1.0 --mu 1 > $D/ncu_bgroup.log 2>&1
 echo done > $D/DONE

@@ -5,7 +5,8 @@
 <launches.csv> is the CSV of
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
       --clock-control none --csv --log-file <csv> python tools/profile_one.py ...
-The k_bform / k_aform launches of the (single) product in the list are summed
+The repeated-addition launches (k_bform, k_aform, k_bgroup) of the (single)
+product in the list are summed
 (a Case A row split runs both); the bytes go to profiles/ncu_traffic.json[<config-key>] (bench.py reports them as
 roofline.traffic next to the algorithmic bytes 3 n^2 x elem: X and Y read
 once, Z written once).
@@ -31,12 +32,12 @@ def main():
              "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
     launches = {}
     for r in rows[1:]:
-        if "k_bform" not in r[ki] and "k_aform" not in r[ki]:
+        if not any(x in r[ki] for x in ("k_bform", "k_aform", "k_bgroup")):
             continue
         d = launches.setdefault(int(r[ii]), {"kernel": r[ki]})
         d[r[mi]] = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
     if not launches:
-        sys.exit(f"no k_bform/k_aform launch in {path}")
+        sys.exit(f"no repeated-addition kernel launch in {path}")
     # one product per launch list (tools/profile_one.py --reps 1): a Case A row
     # split launches k_aform and k_bform; both belong to the product
     rd = sum(d["dram__bytes_read.sum"] for d in launches.values())
@@ -49,8 +50,11 @@ def main():
         dst = os.path.join(copy_to, os.path.basename(path))
         shutil.copy(path, os.path.join(ROOT, dst))
         src = dst
+    # the kernels that ran (the form not chosen on the device exits at once:
+    # named only when it took at least 1% of the product's kernel time)
     kernel = " + ".join(d["kernel"].split("(")[0].replace("void ", "").replace("afmm_dev::", "")
-                        .replace("unnamed>::", "") for _, d in sorted(launches.items()))
+                        .replace("unnamed>::", "") for _, d in sorted(launches.items())
+                        if d["gpu__time_duration.sum"] >= 0.01 * t)
     entry = {
         "bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
         "kernel_time_s": t, "kernel": kernel, "source": src,
