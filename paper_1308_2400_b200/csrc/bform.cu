@@ -588,10 +588,15 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
   const uint32_t ring = smem_u32(base);
 
   if (status_failed(st)) return;  // validation failed: compute nothing (kernels.hpp:115)
-  if (dyn_nrows) {
-    nrows = *dyn_nrows;  // decided on the device (k_choose); the grid covers the slab
-    if (blockIdx.x * rpc >= nrows) return;
-  }
+  // Rows decided on the device (k_choose; the grid covers the whole slab):
+  // only the CTA-level exit reads the device count. A per-warp test against
+  // it (live across the entry loop) changed the loop's register allocation
+  // and cost 13% (dispatch stalls on the predicated FADDs; cfg3 d1 = 0.1
+  // mu = 16: 12.7 vs 11.2 ms), so warps past the A rows in the last A-form
+  // CTA run with an empty list instead (k_acompact zeroes the B rows'
+  // counts) and store zeros that the B part's result overwrites later on
+  // the same stream.
+  if (dyn_nrows && blockIdx.x * rpc >= *dyn_nrows) return;
 
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const uint32_t tile = blockIdx.y;
@@ -625,9 +630,10 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
 
   // ---- consumers: one Z row per warp ----
   const uint32_t b = warp < rpc ? blockIdx.x * rpc + warp : nrows;
-  const uint32_t q = b < nrows ? (row_idx ? row_idx[b] : b) : 0u;  // list / Z row
-  AFMM_CHECK(st, b >= nrows || !row_idx || q < gridDim.x * rpc);
-  const uint32_t cnt = b < nrows ? counts[q] : 0u;
+  const bool active = b < nrows;
+  const uint32_t q = active ? (row_idx ? row_idx[b] : b) : 0u;  // list / Z row
+  AFMM_CHECK(st, !active || !row_idx || q < gridDim.x * rpc);
+  const uint32_t cnt = active ? counts[q] : 0u;
   const E* lst = lists + (uint64_t)q * cap;
   T acc[Ag::CPL];
 #pragma unroll
@@ -720,7 +726,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
     mbar_sleep_wait_at(full0 + slot * 8, phase);
   }
 
-  if (b < nrows) {
+  if (active) {
     T* orow = out + (uint64_t)q * ld_out;
 #pragma unroll
     for (int g = 0; g < Ag::NGRP; ++g) {

@@ -877,10 +877,15 @@ __global__ void k_acompact(const T* __restrict__ x, uint64_t ld, uint32_t n, int
                            const uint32_t* __restrict__ rows_idx,
                            typename AEntry<T>::type* __restrict__ lists, uint64_t cap,
                            uint32_t* __restrict__ counts) {
+  const uint32_t ntotal = ntask;
   if (dyn_ntask) ntask = *dyn_ntask;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  // the rows the choice left to the B-form: empty lists, so that the warps of
+  // the last A-form CTA that fall on them add nothing (k_aform)
+  if (rows_idx)
+    for (uint64_t t = ntask + warp * 32 + lane; t < ntotal; t += nwarps * 32) counts[rows_idx[t]] = 0;
   for (uint64_t t = warp; t < ntask; t += nwarps) {
     const uint64_t q = rows_idx ? rows_idx[t] : t;  // slab row
     const T* row = x + (r0 + q) * ld;
