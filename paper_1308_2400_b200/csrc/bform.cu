@@ -386,10 +386,9 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
   if (status_failed(st)) return;  // validation failed: compute nothing (kernels.hpp:115,144)
   if (group_mode(st, group_allow)) return;  // the small-rep group kernel runs instead
   const int32_t tile_c = blockIdx.y * Gm::TILE_N;  // relative to col0
-  if (dyn_ncols) {
-    ncols = (int32_t)*dyn_ncols;
-    if (tile_c >= ncols) return;  // the whole CTA: beyond the device-decided width
-  }
+  // the whole CTA beyond the device-decided width: exit (the width is read
+  // again at the store rather than kept live across the entry loop)
+  if (dyn_ncols && tile_c >= (int32_t)*dyn_ncols) return;
 
   // %laneid through asm volatile: under register pressure ptxas otherwise
   // re-derives the lane from S2R SR_TID inside the entry loop (a ~30-cycle
@@ -479,6 +478,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
   }
 
   AFMM_CHECK(st, cur.kb_cur == nkb);
+  if (dyn_ncols) ncols = (int32_t)*dyn_ncols;
   if (b < nrows) acc.store(out + (uint64_t)b * ld_out, tile_c, ncols, lane, vec_ok != 0);
 }
 
@@ -779,10 +779,9 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
   uint64_t* empty = full + STAGES;
   if (status_failed(st) || !group_mode(st, allow)) return;
   const int32_t tile_c = blockIdx.y * Gm::TILE_N;
-  if (dyn_ncols) {
-    ncols = (int32_t)*dyn_ncols;
-    if (tile_c >= ncols) return;
-  }
+  // (the device-decided width is read again at the store, not kept live
+  // across the k loop: see k_aform's row count)
+  if (dyn_ncols && tile_c >= (int32_t)*dyn_ncols) return;
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -837,6 +836,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
     if (kb + 1 < nkb) cur.wait();
   }
   if (!active) return;
+  if (dyn_ncols) ncols = (int32_t)*dyn_ncols;
 #pragma unroll
   for (int r = 0; r < kGroupRows; ++r) {
     const uint32_t row = g * kGroupRows + r;
