@@ -9,7 +9,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
 NVFLAGS += -fmad=false -ftz=false -prec-div=true -prec-sqrt=true
 
 CSRC := paper_1308_2400_b200/csrc
-SRCS := $(CSRC)/runtime.cu $(CSRC)/prepass.cu $(CSRC)/bform.cu $(CSRC)/peak.cu
+SRCS := $(CSRC)/runtime.cu $(CSRC)/prepass.cu $(CSRC)/bform.cu $(CSRC)/peak.cu $(CSRC)/generate.cu
 OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
 LIB := paper_1308_2400_b200/libafmm_b200.so
 REF_INC ?= /root/reference/proj/include

@@ -260,6 +260,35 @@ afmm_status afmm_ipc_open(int32_t device, const afmm_ipc_handle* handle, void** 
                           afmm_error* error);
 afmm_status afmm_ipc_close(void* dev_ptr);
 
+/* ---- seeded generation (random.hpp:111-129) ---------------------------------
+ * afmm::generate on the GPU: the same matrix, bit for bit, as the reference's
+ * single std::mt19937_64 stream over the n^2 entries in row-major order
+ * (Bernoulli(density) per entry, then a value draw for a nonzero entry), for
+ * the reference's GeneratorSpec (random.hpp:30-58). An invalid spec returns
+ * AFMM_ERR_INVALID_ARGUMENT with the text of random.hpp:60-79. */
+typedef enum { AFMM_ROLE_REAL = 0, AFMM_ROLE_INTEGER = 1 } afmm_value_role;
+typedef struct {
+  uint64_t n;
+  double density;     /* probability an entry is nonzero */
+  double mu_prime;    /* IntegerValued: values uniform over {1, ..., 2 mu' - 1} */
+  int32_t role;       /* afmm_value_role */
+  double value_low;   /* RealValued: values low + (high - low) * uniform01 */
+  double value_high;
+} afmm_generator_spec;
+
+/* Into a caller-owned n x n host array (row-major); the device is
+ * options->device (NULL options: the current device). f32 stores the
+ * reference's double values rounded to float. */
+afmm_status afmm_generate_f64(const afmm_generator_spec* spec, uint64_t seed, double* out,
+                              const afmm_options* options, afmm_error* error);
+afmm_status afmm_generate_f32(const afmm_generator_spec* spec, uint64_t seed, float* out,
+                              const afmm_options* options, afmm_error* error);
+/* Into device memory on the context's device and stream (n rows of leading
+ * dimension ld): operands for afmm_product_device without a host round trip. */
+afmm_status afmm_generate_device(afmm_context* ctx, const afmm_generator_spec* spec,
+                                 uint64_t seed, int32_t dtype, void* out, uint64_t ld,
+                                 afmm_error* error);
+
 /* ---- roofline ---------------------------------------------------------------
  * Measure the CUDA-core FP-add peak of `device` with a register-resident
  * add-chain microbenchmark (the same instruction mix as the product's inner

@@ -5,6 +5,7 @@
 //
 //   afmm::afmm_case_a(const DenseMatrix&, const DenseMatrix&) -> MultiplyResult  (:113)
 //   afmm::afmm_case_b(const DenseMatrix&, const DenseMatrix&) -> MultiplyResult  (:142)
+//   afmm::generate(const GeneratorSpec&, Seed) -> DenseMatrix       (random.hpp:111)
 //
 // Include it next to the reference headers (it uses their DenseMatrix,
 // MultiplyResult, OpCounts and shape_error) and link libafmm_b200.so. Errors
@@ -24,6 +25,7 @@
 #include "afmm/errors.hpp"
 #include "afmm/matrix.hpp"
 #include "afmm/op_counts.hpp"
+#include "afmm/random.hpp"
 #include "afmm_b200.h"
 
 namespace afmm::gpu {
@@ -178,6 +180,28 @@ inline std::optional<KernelId> parse_kernel(std::string_view name) {
   if (name == "afmm-a-gpu") return KernelId::AFMM_A_GPU;
   if (name == "afmm-b-gpu") return KernelId::AFMM_B_GPU;
   return std::nullopt;
+}
+
+/// afmm::generate(spec, seed) (random.hpp:111-129) on the GPU: the same
+/// matrix, bit for bit; an invalid spec throws std::invalid_argument with
+/// validate()'s text (random.hpp:60-79). opt.device selects the GPU.
+inline DenseMatrix generate(const GeneratorSpec& spec, Seed seed, Options opt = {}) {
+  afmm_generator_spec c{};
+  c.n = spec.n;
+  c.density = spec.density;
+  c.mu_prime = spec.mu_prime;
+  c.role = spec.role == ValueRole::IntegerValued ? AFMM_ROLE_INTEGER : AFMM_ROLE_REAL;
+  c.value_low = spec.value_low;
+  c.value_high = spec.value_high;
+  // the spec is validated before `out` is touched, so an invalid one reports
+  // the reference's error rather than DenseMatrix's
+  DenseMatrix m = spec.n > 0 ? DenseMatrix(spec.n) : DenseMatrix();
+  afmm_error err{};
+  const afmm_options o = detail::to_c(opt);
+  detail::throw_for(afmm_generate_f64(&c, seed.value, spec.n > 0 ? m.data().data() : nullptr, &o,
+                                      &err),
+                    err);
+  return m;
 }
 
 /// The GPU arm of afmm::run_kernel (bench.hpp:103-113).

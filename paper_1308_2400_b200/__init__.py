@@ -21,6 +21,7 @@ from .afmm import (  # noqa: F401
     afmm_case_b,
     case_a_statistics,
     fp_add_peak,
+    generate,
     kernel_launch_count,
     model_partition_case_a,
     model_slab_times_case_a,
@@ -31,5 +32,5 @@ __all__ = [
     "afmm_case_a", "afmm_case_b", "MultiplyResult", "OpCounts", "ShapeError", "DomainError",
     "InvalidArgument", "UnsupportedError", "DeviceError", "DeviceContext", "partition_rows",
     "fp_add_peak", "kernel_launch_count", "ORDER_PRESERVING", "FAST", "case_a_statistics",
-    "model_partition_case_a", "model_slab_times_case_a", "FORMS", "FORM_KERNELS",
+    "model_partition_case_a", "model_slab_times_case_a", "FORMS", "FORM_KERNELS", "generate",
 ]

@@ -89,6 +89,16 @@ class Options(ctypes.Structure):
 
 FLAG_KERNEL_SEMANTICS = 1
 
+ROLE_REAL = 0
+ROLE_INTEGER = 1
+
+
+class GeneratorSpec(ctypes.Structure):
+    """afmm_generator_spec: the reference's GeneratorSpec (random.hpp:30-58)."""
+
+    _fields_ = [("n", c_uint64), ("density", c_double), ("mu_prime", c_double),
+                ("role", c_int32), ("value_low", c_double), ("value_high", c_double)]
+
 
 # Every symbol include/afmm_b200.h declares, with its ctypes signature.
 _SIGNATURES = {
@@ -126,6 +136,12 @@ _SIGNATURES = {
                                               POINTER(c_double)]),
     "afmm_partition_rows": (c_int32, [POINTER(c_uint64), c_uint64, c_uint32, POINTER(c_uint64)]),
     "afmm_fp_add_peak": (c_int32, [c_int32, c_int32, POINTER(c_double), POINTER(c_double)]),
+    "afmm_generate_f64": (c_int32, [POINTER(GeneratorSpec), c_uint64, c_void_p, POINTER(Options),
+                                    POINTER(Error)]),
+    "afmm_generate_f32": (c_int32, [POINTER(GeneratorSpec), c_uint64, c_void_p, POINTER(Options),
+                                    POINTER(Error)]),
+    "afmm_generate_device": (c_int32, [c_void_p, POINTER(GeneratorSpec), c_uint64, c_int32,
+                                       c_void_p, c_uint64, POINTER(Error)]),
     "afmm_ipc_export": (c_int32, [c_void_p, POINTER(IpcHandle), POINTER(Error)]),
     "afmm_ipc_open": (c_int32, [c_int32, POINTER(IpcHandle), POINTER(c_void_p), POINTER(Error)]),
     "afmm_ipc_close": (c_int32, [c_void_p]),

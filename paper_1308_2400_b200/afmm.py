@@ -290,6 +290,21 @@ class DeviceContext:
 
             self._bind(int(torch.cuda.current_stream(self.device).cuda_stream))
 
+    def generate(self, out, density: float, mu_prime: float, integer: bool, seed: int,
+                 low: float = 0.5, high: float = 1.5) -> None:
+        """afmm::generate (random.hpp:111-129) on this context's device, into the
+        n x n device tensor `out` (float64, or float32 = the values rounded):
+        operands for `product` without a host round trip."""
+        p, ld, dname, n = _tensor_info(out, self.device, "out")
+        if out.shape[0] != n:
+            raise InvalidArgument("afmm: out must be n x n")
+        spec = _gen_spec(n, density, mu_prime, integer, low, high)
+        err = _lib.Error()
+        status = self._lib.afmm_generate_device(self._h, ctypes.byref(spec),
+                                                int(seed) & 0xFFFFFFFFFFFFFFFF, _DT_CODE[dname],
+                                                p, ld, ctypes.byref(err))
+        _raise_for(status, err)
+
     def product(self, which: str, lhs, rhs, out, row_begin: int = 0,
                 row_end: Optional[int] = None, *, sync: bool = True,
                 mode: str = ORDER_PRESERVING, split_k: int = 0) -> Optional[OpCounts]:
@@ -450,6 +465,41 @@ def model_slab_times_case_a(stats, nnz_row, cuts, dtype: str = "float32",
             raise InvalidArgument("afmm_model_slab_time_case_a: invalid arguments")
         out.append(c.value)
     return np.array(out)
+
+
+def _gen_spec(n, density, mu_prime, integer, low, high) -> _lib.GeneratorSpec:
+    spec = _lib.GeneratorSpec()
+    spec.n = int(n)
+    spec.density = float(density)
+    spec.mu_prime = float(mu_prime)
+    spec.role = _lib.ROLE_INTEGER if integer else _lib.ROLE_REAL
+    spec.value_low = float(low)
+    spec.value_high = float(high)
+    return spec
+
+
+def generate(n: int, density: float, mu_prime: float, integer: bool, seed: int,
+             low: float = 0.5, high: float = 1.5, *, dtype=np.float64,
+             device: Optional[int] = None) -> np.ndarray:
+    """afmm::generate(GeneratorSpec, Seed) (random.hpp:111-129) on the GPU:
+    the reference's matrix, bit for bit (one std::mt19937_64 stream over the
+    entries in row-major order). integer=True is ValueRole::IntegerValued
+    (values 1 .. 2 mu' - 1), else RealValued with bounds [low, high] (the
+    reference's real_valued() sets mu' = (low + high) / 2). An invalid spec
+    raises InvalidArgument with the reference's message (random.hpp:60-79)."""
+    lib = _lib.load()
+    dt = np.dtype(dtype)
+    if dt not in (np.dtype(np.float64), np.dtype(np.float32)):
+        raise InvalidArgument(f"afmm: dtype must be float32 or float64, got {dt}")
+    spec = _gen_spec(n, density, mu_prime, integer, low, high)
+    out = np.empty((max(int(n), 1), max(int(n), 1)), dtype=dt)
+    opts, _keep = _options(ORDER_PRESERVING, device)
+    err = _lib.Error()
+    fn = lib.afmm_generate_f64 if dt == np.float64 else lib.afmm_generate_f32
+    status = fn(ctypes.byref(spec), int(seed) & 0xFFFFFFFFFFFFFFFF, out.ctypes.data,
+                ctypes.byref(opts), ctypes.byref(err))
+    _raise_for(status, err)
+    return out
 
 
 def fp_add_peak(device: int = 0, dtype: str = "float32") -> Tuple[float, float]:

@@ -149,6 +149,25 @@ void launch_reduce_slices(const T* part, uint64_t stride, uint64_t ld_part, uint
                           uint32_t rows, uint32_t cols, T* out, uint64_t ld_out,
                           const DevStatus* st, const uint32_t* dyn_cols, cudaStream_t s);
 
+// ---- device-side seeded generation (generate.cu; random.hpp:111-129) ----
+struct GenSpecDev {
+  uint64_t n = 0;
+  double density = 0.0, low = 0.0, high = 0.0;
+  uint64_t range = 0, limit = 0;  // IntegerValued: 2 mu' - 1 and the rejection limit
+  int integer = 0;
+};
+size_t gen_block_count(uint64_t ndraws);
+size_t gen_scratch_bytes(uint64_t ndraws);  // per chunk of ndraws draws
+size_t gen_carry_bytes();                   // the device carry record
+// One chunk: twists x 312 draws of the MT19937-64 stream whose state is
+// mt_state (advanced in place), then the entries they complete written to out
+// (row-major, leading dimension ld; out zeroed beforehand). carry: device
+// record {state, entries started}, updated (zero = the start of a matrix).
+template <class T>
+cudaError_t launch_generate_chunk(const GenSpecDev& spec, uint64_t* mt_state, uint32_t twists,
+                                  uint64_t* draws, void* scratch, void* carry, T* out, uint64_t ld,
+                                  cudaStream_t s);
+
 // FP-add peak microbenchmark (peak.cu)
 cudaError_t run_peak(int dtype, double* adds_per_second, double* sm_mhz);
 

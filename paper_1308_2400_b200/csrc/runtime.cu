@@ -236,6 +236,7 @@ struct afmm_context {
   DevBuf gidx;  // dense group index of the small-rep group kernel (k_bgroup)
   // host-buffer API staging
   DevBuf hx, hy, hz;
+  DevBuf gen_state, gen_draws, gen_scratch, gen_carry;  // seeded generation (generate.cu)
   DevStatus* status_host = nullptr;           // pinned
   unsigned long long* stats_host = nullptr;   // pinned, 4 words (multi-device Case A statistics)
   Call last;            // the last enqueued product
@@ -308,7 +309,8 @@ std::vector<DevBuf*> all_bufs(afmm_context* c) {
   return {&c->status, &c->vec_k, &c->work,    &c->lists,  &c->counts, &c->base_copy,
           &c->xt,     &c->zt,    &c->part,    &c->cnt16,  &c->rmax,   &c->fstats,
           &c->alists, &c->acounts, &c->ridx,  &c->plan,   &c->scratch, &c->hx,
-          &c->hy,     &c->hz,      &c->gidx};
+          &c->hy,     &c->hz,      &c->gidx,   &c->gen_state, &c->gen_draws,
+          &c->gen_scratch, &c->gen_carry};
 }
 
 void set_error(afmm_error* err, int kind, int operand, uint64_t row, uint64_t col, double value,
@@ -1665,6 +1667,135 @@ afmm_status guarded(F f) {
 
 }  // namespace
 
+// ---- seeded generation (random.hpp:60-129) ----------------------------------
+
+// validate() of random.hpp:60-79: the same checks, order and messages
+// (std::invalid_argument).
+afmm_status check_gen_spec(const afmm_generator_spec* sp, afmm_error* err) {
+  auto bad = [&](const char* m) {
+    set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, m);
+    return AFMM_ERR_INVALID_ARGUMENT;
+  };
+  if (!sp) return bad("afmm: null generator spec");
+  if (sp->n == 0) return bad("GeneratorSpec: n must be >= 1");
+  if (!(sp->density >= 0.0 && sp->density <= 1.0))
+    return bad("GeneratorSpec: density must be in [0, 1]");
+  if (!(sp->mu_prime > 0.0)) return bad("GeneratorSpec: mu_prime must be positive");
+  if (sp->role == AFMM_ROLE_INTEGER) {
+    if (std::fabs(sp->mu_prime - std::round(sp->mu_prime)) > 1e-9 || sp->mu_prime < 1.0)
+      return bad("GeneratorSpec: IntegerValued role requires integer mu_prime >= 1");
+  } else if (sp->role == AFMM_ROLE_REAL) {
+    if (!(std::isfinite(sp->value_low) && std::isfinite(sp->value_high)) ||
+        sp->value_low > sp->value_high)
+      return bad("GeneratorSpec: invalid value bounds");
+  } else {
+    return bad("afmm: unknown generator role");
+  }
+  if (sp->n > 0x7fffffffull) {
+    set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: n beyond 2^31 - 1");
+    return AFMM_ERR_UNSUPPORTED;
+  }
+  return AFMM_OK;
+}
+
+// afmm::generate (random.hpp:111-129) into device memory on the context's
+// stream: chunks of the MT19937-64 stream until every entry is complete
+// (generate.cu). One host round trip per chunk (the carry decides whether
+// another chunk is needed); a product-sized matrix is one or two chunks.
+template <class T>
+afmm_status generate_locked(afmm_context* c, const afmm_generator_spec& sp, uint64_t seed, T* out,
+                            uint64_t ld, afmm_error* err) {
+  cudaStream_t s = c->stream;
+  const uint64_t n = sp.n, nn = n * n;
+  afmm_dev::take_launch_error();
+  CK(cudaMemset2DAsync(out, ld * sizeof(T), 0, n * sizeof(T), n, s), "memset");
+  if (sp.density == 0.0) {  // every Bernoulli draw says zero (uniform01 >= 0)
+    CK(cudaStreamSynchronize(s), "generate");
+    return AFMM_OK;
+  }
+  // std::mt19937_64(seed): the standard 64-bit initialisation
+  uint64_t st[312];
+  st[0] = seed;
+  for (uint64_t i = 1; i < 312; ++i)
+    st[i] = 6364136223846793005ull * (st[i - 1] ^ (st[i - 1] >> 62)) + i;
+  afmm_dev::GenSpecDev g;
+  g.n = n;
+  g.density = sp.density;
+  g.low = sp.value_low;
+  g.high = sp.value_high;
+  g.integer = sp.role == AFMM_ROLE_INTEGER ? 1 : 0;
+  if (g.integer) {
+    g.range = 2 * (uint64_t)std::llround(sp.mu_prime) - 1;
+    g.limit = UINT64_MAX - UINT64_MAX % g.range;  // random.hpp:97-99
+  }
+  // draws still needed: one per entry + one per nonzero entry (+ the
+  // astronomically rare rejections); 1% slack, at most 20.4M draws per chunk
+  constexpr uint64_t kMaxTwists = 1ull << 16;
+  auto twists_for = [&](uint64_t entries) {
+    const double rem = entries < nn ? (double)(nn - entries) : 0.0;
+    const uint64_t t = (uint64_t)std::ceil(rem * (1.0 + sp.density) * 1.01 / 312.0) + 1;
+    return std::min<uint64_t>(t, kMaxTwists);
+  };
+  const uint64_t cap = twists_for(0);
+  CK(c->gen_state.ensure(312 * 8), "workspace");
+  CK(c->gen_draws.ensure(cap * 312 * 8), "workspace");
+  CK(c->gen_scratch.ensure(afmm_dev::gen_scratch_bytes(cap * 312)), "workspace");
+  CK(c->gen_carry.ensure(afmm_dev::gen_carry_bytes()), "workspace");
+  CK(cudaMemcpyAsync(c->gen_state.p, st, sizeof st, cudaMemcpyHostToDevice, s), "copy");
+  CK(cudaMemsetAsync(c->gen_carry.p, 0, afmm_dev::gen_carry_bytes(), s), "memset");
+  uint64_t entries = 0;
+  uint32_t state = 0;
+  while (true) {
+    const uint32_t tw = (uint32_t)std::min(twists_for(entries), cap);
+    CK(afmm_dev::launch_generate_chunk<T>(g, c->gen_state.as<uint64_t>(), tw,
+                                          c->gen_draws.as<uint64_t>(), c->gen_scratch.p,
+                                          c->gen_carry.p, out, ld, s),
+       "generate");
+    CK(afmm_dev::take_launch_error(), "generate");
+    CK(cudaMemcpyAsync(c->stats_host, c->gen_carry.p, afmm_dev::gen_carry_bytes(),
+                       cudaMemcpyDeviceToHost, s),
+       "carry readback");
+    CK(cudaStreamSynchronize(s), "generate");
+    state = (uint32_t)(c->stats_host[0] & 0xffffffffull);
+    entries = c->stats_host[1];
+    // every entry started, and the last one's value drawn
+    if (entries > nn || (entries == nn && state == 0)) break;
+  }
+  return AFMM_OK;
+}
+
+template <class T>
+afmm_status generate_host(const afmm_generator_spec* spec, uint64_t seed, T* out,
+                          const afmm_options* opt, afmm_error* err) {
+  clear_error(err);
+  afmm_status st = check_gen_spec(spec, err);
+  if (st != AFMM_OK) return st;
+  if (!out) {
+    set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: null output");
+    return AFMM_ERR_INVALID_ARGUMENT;
+  }
+  return guarded([&]() -> afmm_status {
+    afmm_context* c = nullptr;
+    afmm_status s0 = default_context(opt ? opt->device : -1, 0, &c, err);
+    if (s0 != AFMM_OK) return s0;
+    std::lock_guard<std::mutex> g(c->mu);
+    CK(cudaSetDevice(c->device), "afmm: cudaSetDevice");
+    if (c->pending) {
+      afmm_status prev = finish_locked(c, nullptr, err);
+      if (prev != AFMM_OK) return prev;
+    }
+    const uint64_t n = spec->n;
+    CK(c->hz.ensure(n * n * sizeof(T)), "workspace");
+    afmm_status r = generate_locked<T>(c, *spec, seed, c->hz.as<T>(), n, err);
+    if (r != AFMM_OK) return r;
+    CK(cudaMemcpyAsync(out, c->hz.p, n * n * sizeof(T), cudaMemcpyDeviceToHost, c->stream),
+       "result copy");
+    CK(cudaStreamSynchronize(c->stream), "result copy");
+    clear_error(err);
+    return AFMM_OK;
+  });
+}
+
 // ---------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------
@@ -2043,6 +2174,38 @@ afmm_status afmm_partition_rows(const uint64_t* work, uint64_t n, uint32_t parts
   }
   cuts[parts] = n;
   return AFMM_OK;
+}
+
+afmm_status afmm_generate_f64(const afmm_generator_spec* spec, uint64_t seed, double* out,
+                              const afmm_options* options, afmm_error* err) {
+  return generate_host<double>(spec, seed, out, options, err);
+}
+
+afmm_status afmm_generate_f32(const afmm_generator_spec* spec, uint64_t seed, float* out,
+                              const afmm_options* options, afmm_error* err) {
+  return generate_host<float>(spec, seed, out, options, err);
+}
+
+afmm_status afmm_generate_device(afmm_context* c, const afmm_generator_spec* spec, uint64_t seed,
+                                 int32_t dtype, void* out, uint64_t ld, afmm_error* err) {
+  clear_error(err);
+  afmm_status st = check_gen_spec(spec, err);
+  if (st != AFMM_OK) return st;
+  if (!c || !out || ld < spec->n || (dtype != AFMM_F64 && dtype != AFMM_F32)) {
+    set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: invalid context/output/dtype");
+    return AFMM_ERR_INVALID_ARGUMENT;
+  }
+  return guarded([&]() -> afmm_status {
+    std::lock_guard<std::mutex> g(c->mu);
+    CK(cudaSetDevice(c->device), "afmm: cudaSetDevice");
+    if (c->pending) {
+      afmm_status prev = finish_locked(c, nullptr, err);
+      if (prev != AFMM_OK) return prev;
+    }
+    return dtype == AFMM_F64
+               ? generate_locked<double>(c, *spec, seed, static_cast<double*>(out), ld, err)
+               : generate_locked<float>(c, *spec, seed, static_cast<float*>(out), ld, err);
+  });
 }
 
 afmm_status afmm_fp_add_peak(int32_t device, int32_t dtype, double* adds_per_second,

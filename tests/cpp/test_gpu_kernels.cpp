@@ -208,6 +208,27 @@ int main() {
     CHECK(gpu::afmm_case_a(x, y, o).product == afmm_case_a(x, y).product);
     CHECK(gpu::afmm_case_b(x, y, o).counts == afmm_case_b(x, y).counts);
   }
+  // seeded generation on the GPU: the reference's generator, bit for bit
+  // (random.hpp:111-129), both roles, edge densities, and validate()'s errors
+  {
+    const GeneratorSpec specs[] = {
+        GeneratorSpec::integer_valued(1, 1.0, 1.0),   GeneratorSpec::integer_valued(33, 0.5, 21.0),
+        GeneratorSpec::integer_valued(64, 1.0, 4.0),  GeneratorSpec::integer_valued(100, 0.0, 3.0),
+        GeneratorSpec::real_valued(50, 0.9),          GeneratorSpec::real_valued(257, 0.3, -2.0, 5.0),
+        GeneratorSpec::real_valued(16, 1.0, 1.0, 1.0)};
+    for (const auto& sp : specs)
+      for (std::uint64_t seed : {0ull, 7ull, 0xFFFFFFFFFFFFFFFFull})
+        CHECK(gpu::generate(sp, Seed{seed}) == generate(sp, Seed{seed}));
+    GeneratorSpec bad = GeneratorSpec::integer_valued(4, 0.5, 2.5);
+    CHECK(expect_throw<std::invalid_argument>([&] { gpu::generate(bad, Seed{1}); }) ==
+          expect_throw<std::invalid_argument>([&] { generate(bad, Seed{1}); }));
+    bad = GeneratorSpec::real_valued(0, 0.5);
+    CHECK(expect_throw<std::invalid_argument>([&] { gpu::generate(bad, Seed{1}); }) ==
+          expect_throw<std::invalid_argument>([&] { generate(bad, Seed{1}); }));
+    bad = GeneratorSpec::real_valued(3, 1.5);
+    CHECK(expect_throw<std::invalid_argument>([&] { gpu::generate(bad, Seed{1}); }) ==
+          expect_throw<std::invalid_argument>([&] { generate(bad, Seed{1}); }));
+  }
   std::printf("%d checks, %d failures\n", g_checks, g_failures);
   return g_failures == 0 ? 0 : 1;
 }
