@@ -3,7 +3,7 @@
 #   oracle/liboracle.so, oracle/_ref/...    test infrastructure (see oracle/Makefile)
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall -Xcompiler -mpclmul \
            -Xptxas -warn-spills -Iinclude
 # Bit-exactness: keep IEEE adds (no fast-math, no FTZ), no FMA contraction.
 NVFLAGS += -fmad=false -ftz=false -prec-div=true -prec-sqrt=true
@@ -17,7 +17,7 @@ REF_INC ?= /root/reference/proj/include
 all: $(LIB) oracle $(if $(wildcard $(REF_INC)/afmm/kernels.hpp),cpptest)
 
 build/%.o: $(CSRC)/%.cu $(CSRC)/common.cuh $(CSRC)/kernels.h $(CSRC)/costmodel.h \
-           $(CSRC)/jumptable.inc include/afmm_b200.h
+           $(CSRC)/jumptable.inc $(CSRC)/mt64jump.h include/afmm_b200.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c -o $@ $<
 

@@ -130,6 +130,8 @@ constexpr int kChooseSplit = 2;
 // given) receives the modeled cycles of the choice. split_cost (optional):
 // split_cost[j] = the cost of the split with j B tiles, precomputed (k_choose
 // prices the candidates in parallel; the same expression).
+// (host instantiations pass host lambdas; the device one a device functor)
+#pragma nv_exec_check_disable
 template <class Pre>
 AFMM_HD uint64_t choose_aform_rows(const CaseAModel& md, uint64_t rows, int variant, Pre pre,
                                    double* time = nullptr, const double* split_cost = nullptr) {

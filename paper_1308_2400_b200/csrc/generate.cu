@@ -9,11 +9,16 @@
 // rejection loop; RealValued: low + (high - low) * uniform01). Which draw
 // belongs to which entry is data dependent, so the device pipeline is:
 //
-//   k_mt_gen        the raw 64-bit stream, one CTA: MT19937-64's recurrence
-//                   w[k + 312] = f(w[k], w[k + 1], w[k + 156]) makes 156
-//                   words computable at once, so a twist is two parallel
-//                   half-steps over a 624-word smem ring; tempered outputs
-//                   are stored in stream order.
+//   k_mt_jump       the stream's start offsets: CTA c of a chunk generates
+//                   the stretch [c L, (c+1) L) of the chunk, and its start
+//                   window comes from a radix-4 tree of jump-aheads (the
+//                   window at k + J is a GF(2) convolution of the words after
+//                   k with x^J mod phi, mt64jump.h) -- log4(CTAs) levels.
+//   k_mt_gen        the raw 64-bit stream, one CTA per stretch: MT19937-64's
+//                   recurrence w[k + 312] = f(w[k], w[k + 1], w[k + 156])
+//                   makes 156 words computable at once, so a twist is two
+//                   parallel half-steps over a 624-word smem ring; tempered
+//                   outputs are stored in stream order.
 //   k_gen_reduce    every draw is a transition of a two-state automaton
 //                   (B: the next draw is an entry's Bernoulli variate, V: a
 //                   value variate); per block of draws the composed
@@ -57,20 +62,28 @@ __device__ __forceinline__ uint64_t mt_temper(uint64_t y) {
   return y;
 }
 
-// `twists` x 312 outputs of the stream whose 312-word state is `state` (read
-// at entry, written back at exit). Ring slot of stream word k: k % 624; the
-// current generation sits at slots [0, 312), the next is built at [312, 624)
-// and then the roles swap.
-__global__ void __launch_bounds__(MT_M) k_mt_gen(uint64_t* __restrict__ state,
-                                                uint64_t* __restrict__ out, uint32_t twists) {
+// The raw stream, one CTA per stretch of `twists` x 312 outputs: CTA c starts
+// from windows[c] (the window at output offset c * twists * 312, placed there
+// by k_mt_jump) and stores its outputs in stream order; the last CTA leaves
+// the window that follows the chunk in *end_window. Ring slot of stream word
+// k: k % 624; the current generation sits at one half while the next one is
+// built in the other: w[k + 312] = f(w[k], w[k + 1], w[k + 156]) makes 156
+// words computable at once, so a twist is two parallel half-steps.
+__global__ void __launch_bounds__(MT_M) k_mt_gen(const uint64_t* __restrict__ windows,
+                                                uint64_t* __restrict__ out, uint32_t twists,
+                                                uint64_t* __restrict__ end_window) {
   __shared__ uint64_t ring[2 * MT_N];
   const uint32_t i = threadIdx.x;  // 0..155
-  ring[i] = state[i];
-  ring[i + MT_M] = state[i + MT_M];
+  const uint64_t* w0 = windows + (uint64_t)blockIdx.x * MT_N;
+  ring[i] = w0[i];
+  ring[i + MT_M] = w0[i + MT_M];
   __syncthreads();
+  uint64_t* o = out + (uint64_t)blockIdx.x * twists * MT_N;
   uint32_t cur = 0;  // ring offset of the current generation
-  for (uint32_t t = 0; t < twists; ++t) {
+  for (uint32_t t = 0; t < twists; ++t, o += MT_N) {
     const uint32_t nxt = cur ^ MT_N;
+    o[i] = mt_temper(ring[cur + i]);
+    o[i + MT_M] = mt_temper(ring[cur + i + MT_M]);
     // first half: w'[i] = f(w[i], w[i+1], w[i+156]) -- all old words
     ring[nxt + i] = mt_mix(ring[cur + i], ring[cur + i + 1], ring[cur + i + MT_M]);
     __syncthreads();
@@ -79,14 +92,75 @@ __global__ void __launch_bounds__(MT_M) k_mt_gen(uint64_t* __restrict__ state,
     const uint64_t b = j + 1 < MT_N ? ring[cur + j + 1] : ring[nxt];
     ring[nxt + j] = mt_mix(ring[cur + j], b, ring[nxt + i]);
     __syncthreads();
-    uint64_t* o = out + (uint64_t)t * MT_N;
-    o[i] = mt_temper(ring[nxt + i]);
-    o[j] = mt_temper(ring[nxt + j]);
     cur = nxt;
   }
+  if (end_window && blockIdx.x == gridDim.x - 1) {
+    end_window[i] = ring[cur + i];
+    end_window[i + MT_M] = ring[cur + i + MT_M];
+  }
+}
+
+// Jump-ahead (mt64jump.h): the window at offset k + J is the XOR of the
+// windows at offsets k + i over the set coefficients c_i of x^J mod phi. One
+// CTA per jump of the tree level with stride S (radix 4): block t moves
+// windows[t / 3] by (t % 3 + 1) * S stretches with polys[t % 3]. The CTA
+// generates the kD + 311 words after its source window into shared memory
+// (64 twists), then each warp takes every 32nd coefficient word and, for each
+// set bit i, XORs words i .. i + 311 into its lanes' accumulators (lane l
+// holds w = l + 32 r); the warps' partial windows are XOR-reduced at the end.
+constexpr int JUMP_THREADS = 1024;
+constexpr int JUMP_TWISTS = 64;  // 65 x 312 = 20280 >= kD + 311 words
+constexpr size_t kJumpSmem = (size_t)(JUMP_TWISTS + 1) * MT_N * sizeof(uint64_t);
+
+__global__ void __launch_bounds__(JUMP_THREADS, 1)
+    k_mt_jump(uint64_t* __restrict__ windows, const uint64_t* __restrict__ polys,
+              uint32_t stride, uint32_t count) {
+  extern __shared__ uint64_t v[];
+  const uint32_t src = blockIdx.x / 3, a = blockIdx.x % 3 + 1;
+  const uint32_t dst = src + a * stride;
+  if (dst >= count) return;  // the whole CTA: no barrier is skipped by part of it
+  const uint64_t* __restrict__ poly = polys + (a - 1) * MT_N;
+  const uint32_t tid = threadIdx.x;
+  if (tid < MT_N) v[tid] = windows[(uint64_t)src * MT_N + tid];
   __syncthreads();
-  state[i] = ring[cur + i];
-  state[i + MT_M] = ring[cur + i + MT_M];
+  for (int t = 0; t < JUMP_TWISTS; ++t) {
+    uint64_t* g = v + t * MT_N;
+    if (tid < MT_M) g[MT_N + tid] = mt_mix(g[tid], g[tid + 1], g[tid + MT_M]);
+    __syncthreads();
+    if (tid < MT_M) {
+      const uint32_t j = tid + MT_M;
+      g[MT_N + j] = mt_mix(g[j], g[j + 1], g[MT_N + tid]);
+    }
+    __syncthreads();
+  }
+  const uint32_t lane = tid & 31, warp = tid >> 5;
+  uint64_t acc[10];
+#pragma unroll
+  for (int r = 0; r < 10; ++r) acc[r] = 0;
+  for (uint32_t q = warp; q < MT_N; q += 32) {
+    uint64_t m = __ldg(poly + q);
+    while (m) {
+      const uint32_t b = __ffsll((long long)m) - 1;
+      m &= m - 1;
+      const uint64_t* p = v + q * 64 + b + lane;
+#pragma unroll
+      for (int r = 0; r < 9; ++r) acc[r] ^= p[32 * r];
+      if (lane < MT_N - 288) acc[9] ^= p[288];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t w = lane + 32 * r;
+    if (w < MT_N) v[warp * MT_N + w] = acc[r];
+  }
+  __syncthreads();
+  if (tid < MT_N) {
+    uint64_t x = 0;
+#pragma unroll 8
+    for (int wp = 0; wp < JUMP_THREADS / 32; ++wp) x ^= v[wp * MT_N + tid];
+    windows[(uint64_t)dst * MT_N + tid] = x;
+  }
 }
 
 // One draw as an automaton transition (random.hpp:92-104, 118-127).
@@ -267,15 +341,35 @@ size_t gen_scratch_bytes(uint64_t ndraws) {
 }
 size_t gen_carry_bytes() { return sizeof(GenCarry); }
 
-// One chunk: `twists` x 312 draws of the stream (state advanced in place),
-// then the entries they complete written to out. carry: device GenCarry,
-// updated. draws: twists * 312 words; scratch: gen_scratch_bytes.
+// One chunk: `ctas` stretches of `twists` x 312 draws of the stream, the
+// first starting at windows[0]; the jump tree fills windows[1 .. ctas) (levels
+// of stride 1, 4, 16, ...; polys: 3 x 312 words per level), the generators
+// write the draws and the window after the chunk to end_window; then the
+// entries the draws complete are written to out. carry: device GenCarry,
+// updated; scratch: gen_scratch_bytes(ctas * twists * 312).
 template <class T>
-cudaError_t launch_generate_chunk(const GenSpecDev& spec, uint64_t* mt_state, uint32_t twists,
-                                  uint64_t* draws, void* scratch, void* carry, T* out, uint64_t ld,
-                                  cudaStream_t s) {
-  const uint64_t ndraws = (uint64_t)twists * MT_N;
-  k_mt_gen<<<1, MT_M, 0, s>>>(mt_state, draws, twists);
+cudaError_t launch_generate_chunk(const GenSpecDev& spec, uint64_t* windows,
+                                  const uint64_t* polys, uint32_t ctas, uint32_t twists,
+                                  uint64_t* end_window, uint64_t* draws, void* scratch, void* carry,
+                                  T* out, uint64_t ld, cudaStream_t s) {
+  const uint64_t ndraws = (uint64_t)ctas * twists * MT_N;
+  if (ctas > 1) {
+    static bool attr = false;  // idempotent; a race only repeats the call
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(k_mt_jump, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)kJumpSmem);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    uint32_t level = 0;
+    for (uint64_t stride = 1; stride < ctas; stride *= 4, ++level) {
+      const uint32_t jumps = (uint32_t)std::min<uint64_t>(stride, ctas) * 3;
+      k_mt_jump<<<jumps, JUMP_THREADS, kJumpSmem, s>>>(windows, polys + (size_t)level * 3 * MT_N,
+                                                       (uint32_t)stride, ctas);
+      note_launch();
+    }
+  }
+  k_mt_gen<<<ctas, MT_M, 0, s>>>(windows, draws, twists, end_window);
   note_launch();
   GenParams p;
   p.density = spec.density;
@@ -298,11 +392,11 @@ cudaError_t launch_generate_chunk(const GenSpecDev& spec, uint64_t* mt_state, ui
   return cudaGetLastError();
 }
 
-template cudaError_t launch_generate_chunk<double>(const GenSpecDev&, uint64_t*, uint32_t,
-                                                   uint64_t*, void*, void*, double*, uint64_t,
-                                                   cudaStream_t);
-template cudaError_t launch_generate_chunk<float>(const GenSpecDev&, uint64_t*, uint32_t,
-                                                  uint64_t*, void*, void*, float*, uint64_t,
-                                                  cudaStream_t);
+template cudaError_t launch_generate_chunk<double>(const GenSpecDev&, uint64_t*, const uint64_t*,
+                                                   uint32_t, uint32_t, uint64_t*, uint64_t*, void*,
+                                                   void*, double*, uint64_t, cudaStream_t);
+template cudaError_t launch_generate_chunk<float>(const GenSpecDev&, uint64_t*, const uint64_t*,
+                                                  uint32_t, uint32_t, uint64_t*, uint64_t*, void*,
+                                                  void*, float*, uint64_t, cudaStream_t);
 
 }  // namespace afmm_dev

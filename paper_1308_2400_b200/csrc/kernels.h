@@ -159,14 +159,22 @@ struct GenSpecDev {
 size_t gen_block_count(uint64_t ndraws);
 size_t gen_scratch_bytes(uint64_t ndraws);  // per chunk of ndraws draws
 size_t gen_carry_bytes();                   // the device carry record
-// One chunk: twists x 312 draws of the MT19937-64 stream whose state is
-// mt_state (advanced in place), then the entries they complete written to out
-// (row-major, leading dimension ld; out zeroed beforehand). carry: device
-// record {state, entries started}, updated (zero = the start of a matrix).
+// One chunk: `ctas` stretches of twists x 312 draws of the MT19937-64
+// stream, the first starting at the window windows[0] (mt64jump.h's window
+// convention); windows[1 .. ctas) are filled by the jump tree (polys: per
+// level of stride 4^l, the 3 x 312-word polynomials x^(a 4^l twists 312) mod
+// phi, a = 1..3), the window after the chunk goes to end_window; then the
+// entries the draws complete are written to out (row-major, leading dimension
+// ld; out zeroed beforehand). carry: device record {state, entries started},
+// updated (zero = the start of a matrix). scratch: gen_scratch_bytes(draws).
+constexpr uint32_t kGenTwistsPerCta = 2048;  // the stretch L = 2048 x 312 draws
+constexpr uint32_t kGenMaxCtas = 512;        // 4.5 tree levels; 2.6 GB of draws
+constexpr uint32_t kGenLevels = 5;
 template <class T>
-cudaError_t launch_generate_chunk(const GenSpecDev& spec, uint64_t* mt_state, uint32_t twists,
-                                  uint64_t* draws, void* scratch, void* carry, T* out, uint64_t ld,
-                                  cudaStream_t s);
+cudaError_t launch_generate_chunk(const GenSpecDev& spec, uint64_t* windows,
+                                  const uint64_t* polys, uint32_t ctas, uint32_t twists,
+                                  uint64_t* end_window, uint64_t* draws, void* scratch, void* carry,
+                                  T* out, uint64_t ld, cudaStream_t s);
 
 // FP-add peak microbenchmark (peak.cu)
 cudaError_t run_peak(int dtype, double* adds_per_second, double* sm_mhz);

@@ -26,6 +26,7 @@
 
 #include "../../include/afmm_b200.h"
 #include "kernels.h"
+#include "mt64jump.h"
 
 using afmm_dev::DevStatus;
 
@@ -140,6 +141,7 @@ struct DevBuf {
     p = nullptr;
     bytes = 0;
   }
+#ifdef AFMM_CHECKED
   // checked build: are both guard bands intact?
   bool guards_intact() const {
     if (!kGuard || !p) return true;
@@ -153,6 +155,8 @@ struct DevBuf {
       if (b != kGuardByte) return false;
     return true;
   }
+#endif
+
   template <class U>
   U* as() const {
     return static_cast<U*>(p);
@@ -236,7 +240,7 @@ struct afmm_context {
   DevBuf gidx;  // dense group index of the small-rep group kernel (k_bgroup)
   // host-buffer API staging
   DevBuf hx, hy, hz;
-  DevBuf gen_state, gen_draws, gen_scratch, gen_carry;  // seeded generation (generate.cu)
+  DevBuf gen_state, gen_draws, gen_scratch, gen_carry, gen_polys;  // seeded generation (generate.cu)
   DevStatus* status_host = nullptr;           // pinned
   unsigned long long* stats_host = nullptr;   // pinned, 4 words (multi-device Case A statistics)
   Call last;            // the last enqueued product
@@ -310,7 +314,7 @@ std::vector<DevBuf*> all_bufs(afmm_context* c) {
           &c->xt,     &c->zt,    &c->part,    &c->cnt16,  &c->rmax,   &c->fstats,
           &c->alists, &c->acounts, &c->ridx,  &c->plan,   &c->scratch, &c->hx,
           &c->hy,     &c->hz,      &c->gidx,   &c->gen_state, &c->gen_draws,
-          &c->gen_scratch, &c->gen_carry};
+          &c->gen_scratch, &c->gen_carry, &c->gen_polys};
 }
 
 void set_error(afmm_error* err, int kind, int operand, uint64_t row, uint64_t col, double value,
@@ -1698,10 +1702,33 @@ afmm_status check_gen_spec(const afmm_generator_spec* sp, afmm_error* err) {
   return AFMM_OK;
 }
 
+// The jump polynomials of the generation tree: per level l (stride 4^l
+// stretches of L = kGenTwistsPerCta x 312 draws), x^(a 4^l L) mod phi for
+// a = 1, 2, 3 (mt64jump.h); computed once per process (~30 ms of host time).
+const std::vector<uint64_t>& gen_jump_polys() {
+  static const std::vector<uint64_t> table = [] {
+    const auto& f = mt64jump::field();
+    std::vector<uint64_t> t;
+    if (!f.ok) return t;  // cannot happen for MT19937-64; reported by the caller
+    mt64jump::Poly p = f.xpow((uint64_t)afmm_dev::kGenTwistsPerCta * mt64jump::kN);
+    for (uint32_t l = 0; l < afmm_dev::kGenLevels; ++l) {
+      const mt64jump::Poly p2 = f.mulmod(p, p), p3 = f.mulmod(p2, p);
+      t.insert(t.end(), p.begin(), p.end());
+      t.insert(t.end(), p2.begin(), p2.end());
+      t.insert(t.end(), p3.begin(), p3.end());
+      p = f.mulmod(p2, p2);
+    }
+    return t;
+  }();
+  return table;
+}
+
 // afmm::generate (random.hpp:111-129) into device memory on the context's
 // stream: chunks of the MT19937-64 stream until every entry is complete
-// (generate.cu). One host round trip per chunk (the carry decides whether
-// another chunk is needed); a product-sized matrix is one or two chunks.
+// (generate.cu). A chunk is up to kGenMaxCtas stretches of L draws generated
+// in parallel from jump-ahead start windows; one host round trip per chunk
+// (the carry decides whether another chunk is needed); a chunk holds up to
+// 3.3e8 draws, so a matrix up to n ~ 13000 is one chunk.
 template <class T>
 afmm_status generate_locked(afmm_context* c, const afmm_generator_spec& sp, uint64_t seed, T* out,
                             uint64_t ld, afmm_error* err) {
@@ -1713,11 +1740,13 @@ afmm_status generate_locked(afmm_context* c, const afmm_generator_spec& sp, uint
     CK(cudaStreamSynchronize(s), "generate");
     return AFMM_OK;
   }
-  // std::mt19937_64(seed): the standard 64-bit initialisation
-  uint64_t st[312];
-  st[0] = seed;
-  for (uint64_t i = 1; i < 312; ++i)
-    st[i] = 6364136223846793005ull * (st[i - 1] ^ (st[i - 1] >> 62)) + i;
+  const std::vector<uint64_t>& polys = gen_jump_polys();
+  if (polys.empty()) {
+    set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: MT19937-64 jump table unavailable");
+    return AFMM_ERR_CUDA;
+  }
+  uint64_t win[mt64jump::kN];  // std::mt19937_64(seed) after its first twist
+  mt64jump::seed_window(seed, win);
   afmm_dev::GenSpecDev g;
   g.n = n;
   g.density = sp.density;
@@ -1729,27 +1758,44 @@ afmm_status generate_locked(afmm_context* c, const afmm_generator_spec& sp, uint
     g.limit = UINT64_MAX - UINT64_MAX % g.range;  // random.hpp:97-99
   }
   // draws still needed: one per entry + one per nonzero entry (+ the
-  // astronomically rare rejections); 1% slack, at most 20.4M draws per chunk
-  constexpr uint64_t kMaxTwists = 1ull << 16;
-  auto twists_for = [&](uint64_t entries) {
+  // astronomically rare rejections), 1% slack; whole stretches, except that a
+  // one-stretch chunk stops at the twist that covers it
+  constexpr uint64_t kL = (uint64_t)afmm_dev::kGenTwistsPerCta * mt64jump::kN;
+  auto shape_for = [&](uint64_t entries, uint32_t* ctas, uint32_t* twists) {
     const double rem = entries < nn ? (double)(nn - entries) : 0.0;
-    const uint64_t t = (uint64_t)std::ceil(rem * (1.0 + sp.density) * 1.01 / 312.0) + 1;
-    return std::min<uint64_t>(t, kMaxTwists);
+    const uint64_t need = (uint64_t)std::ceil(rem * (1.0 + sp.density) * 1.01) + mt64jump::kN;
+    const uint64_t k = (need + kL - 1) / kL;
+    *ctas = (uint32_t)std::min<uint64_t>(k, afmm_dev::kGenMaxCtas);
+    *twists = *ctas > 1 ? afmm_dev::kGenTwistsPerCta
+                        : (uint32_t)std::min<uint64_t>((need + mt64jump::kN - 1) / mt64jump::kN,
+                                                       afmm_dev::kGenTwistsPerCta);
   };
-  const uint64_t cap = twists_for(0);
-  CK(c->gen_state.ensure(312 * 8), "workspace");
-  CK(c->gen_draws.ensure(cap * 312 * 8), "workspace");
-  CK(c->gen_scratch.ensure(afmm_dev::gen_scratch_bytes(cap * 312)), "workspace");
+  uint32_t ctas0, tw0;
+  shape_for(0, &ctas0, &tw0);
+  const uint64_t cap = (uint64_t)ctas0 * tw0 * mt64jump::kN;
+  const size_t wbytes = (size_t)mt64jump::kN * sizeof(uint64_t);
+  CK(c->gen_state.ensure(wbytes * (afmm_dev::kGenMaxCtas + 1)), "workspace");
+  CK(c->gen_polys.ensure(polys.size() * sizeof(uint64_t)), "workspace");
+  CK(c->gen_draws.ensure(cap * 8), "workspace");
+  CK(c->gen_scratch.ensure(afmm_dev::gen_scratch_bytes(cap)), "workspace");
   CK(c->gen_carry.ensure(afmm_dev::gen_carry_bytes()), "workspace");
-  CK(cudaMemcpyAsync(c->gen_state.p, st, sizeof st, cudaMemcpyHostToDevice, s), "copy");
+  uint64_t* windows = c->gen_state.as<uint64_t>();
+  uint64_t* end_window = windows + (size_t)afmm_dev::kGenMaxCtas * mt64jump::kN;
+  CK(cudaMemcpyAsync(c->gen_polys.p, polys.data(), polys.size() * sizeof(uint64_t),
+                     cudaMemcpyHostToDevice, s),
+     "copy");
+  CK(cudaMemcpyAsync(windows, win, wbytes, cudaMemcpyHostToDevice, s), "copy");
   CK(cudaMemsetAsync(c->gen_carry.p, 0, afmm_dev::gen_carry_bytes(), s), "memset");
   uint64_t entries = 0;
   uint32_t state = 0;
-  while (true) {
-    const uint32_t tw = (uint32_t)std::min(twists_for(entries), cap);
-    CK(afmm_dev::launch_generate_chunk<T>(g, c->gen_state.as<uint64_t>(), tw,
-                                          c->gen_draws.as<uint64_t>(), c->gen_scratch.p,
-                                          c->gen_carry.p, out, ld, s),
+  for (bool first = true;; first = false) {
+    uint32_t ctas, tw;
+    shape_for(entries, &ctas, &tw);
+    if (!first)  // the next chunk starts where the last one ended
+      CK(cudaMemcpyAsync(windows, end_window, wbytes, cudaMemcpyDeviceToDevice, s), "copy");
+    CK(afmm_dev::launch_generate_chunk<T>(g, windows, c->gen_polys.as<uint64_t>(), ctas, tw,
+                                          end_window, c->gen_draws.as<uint64_t>(),
+                                          c->gen_scratch.p, c->gen_carry.p, out, ld, s),
        "generate");
     CK(afmm_dev::take_launch_error(), "generate");
     CK(cudaMemcpyAsync(c->stats_host, c->gen_carry.p, afmm_dev::gen_carry_bytes(),

@@ -56,10 +56,18 @@ def test_generate_matches_reference_generator(cuda, oracle, case, seed):
     assert _bits_equal(z32, want.astype(np.float32))
 
 
-@pytest.mark.parametrize("n,d,mu,integer", [(4096, 0.9, 16.0, True), (3000, 0.6, 1.0, False)])
-def test_generate_several_chunks(cuda, oracle, n, d, mu, integer):
-    """~3e7 draws: more than one chunk of the stream (20.4M draws each), so
-    the carry (automaton state, entries started) crosses chunk boundaries."""
+@pytest.mark.parametrize("n,d,mu,integer", [
+    (800, 0.9, 16.0, True),     # 1.2M draws: 2 stretches (one tree level, a = 1)
+    (1500, 1.0, 2.0, True),     # 4.5M draws: 8 stretches (two levels, partial)
+    (4096, 0.9, 16.0, True),    # 3.2e7 draws: 51 stretches (three levels)
+    (3000, 0.6, 1.0, False),    # 1.4e7 draws: 23 stretches
+    (13000, 1.0, 4.0, True),    # 3.4e8 draws: a full chunk of 512 stretches (five levels) + a second chunk
+])
+def test_generate_several_stretches_and_chunks(cuda, oracle, n, d, mu, integer):
+    """Draws from many parallel stretches of the stream, each started from a
+    jump-ahead window (the radix-4 tree of k_mt_jump), and from more than one
+    chunk, so the carry (automaton state, entries started) and the chunk's end
+    window cross chunk boundaries."""
     afmm = _api()
     z = afmm.generate(n, d, mu, integer, 99)
     want = oracle.generate(n, d, mu, integer, 99)
