@@ -52,7 +52,7 @@ def parse_args():
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--size", dest="n", type=int, default=None,
                    help="reduced problem size (tests only; the config's n by default)")
-    p.add_argument("--mode", default="order-preserving", choices=["order-preserving", "fast"],
+    p.add_argument("--mode", default="order-preserving", choices=["order-preserving", "fast", "fast-ladder"],
                    help="order-preserving = bit-exact with the reference (default); fast = "
                         "reassociated split-k within 1e-12/1e-5")
     p.add_argument("--no-e2e", action="store_true")
@@ -251,7 +251,9 @@ def _config_dict(args, cfg):
                      + ("" if n == cfg.n else f" [REDUCED to n={n}: test run, not the config]"),
          "case": cfg.case, "n": n,
          "mode": "order-preserving (bit-exact)" if args.mode == "order-preserving"
-         else "fast (reassociated split-k, tolerance 1e-12 f64 / 1e-5 f32)",
+         else "fast (reassociated split-k, tolerance 1e-12 f64 / 1e-5 f32)" if args.mode == "fast"
+         else "fast-ladder (fast + each term's |rep| copies summed as a doubling ladder: "
+              "floor(log2 rep) + popcount(rep) adds per term; the metric still counts |rep|)",
          "parallelism": f"row-partition x{args.gpus}" + (
              " (one process per GPU, torchrun)" if int(os.environ.get("WORLD_SIZE", "1")) > 1
              else " (one process, all GPUs)" if args.gpus > 1 else ""),
@@ -433,6 +435,16 @@ def main():
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks,
         }
+        if args.mode == "fast-ladder":
+            # the metric counts the additions the product stands for (sum |rep|);
+            # the ladder performs fewer -- report those too, and the pipe
+            # fraction they amount to
+            from paper_1308_2400_b200.gen import ladder_additions
+            performed = ladder_additions(cfg.case, lhs, rhs)
+            line["performed_additions"] = performed
+            line["effective_over_performed"] = job_adds / max(performed, 1)
+            if world == 1:
+                line["performed_frac_of_fp_add_peak"] = performed / (kms * 1e-3) / peak
         if secondary is not None:
             line["secondary_configs"] = secondary
         if world > 1:

@@ -54,7 +54,16 @@ typedef enum {
   /* Same additions, reassociated (split-k partial sums combined in a fixed
    * order). Within 1e-12 (f64) / 1e-5 (f32) of the reference, normalised by
    * sum_k |X[i,k]|*|Y[k,j]|. */
-  AFMM_MODE_FAST = 1
+  AFMM_MODE_FAST = 1,
+  /* AFMM_MODE_FAST plus a reassociation inside each term: the |rep| copies of
+   * a base are summed as a doubling ladder (b, b+b, (b+b)+(b+b), ... are exact
+   * power-of-two multiples; the ones selected by the binary digits of |rep|
+   * are added into the element), i.e. floor(log2 |rep|) + popcount(|rep|)
+   * additions per term instead of |rep|, still no multiplication. Same
+   * tolerance as AFMM_MODE_FAST (fewer roundings per term). op_counts keep
+   * the reference's tallies (sum of |rep|: the additions the product stands
+   * for), not the fewer additions the device performed. */
+  AFMM_MODE_FAST_LADDER = 2
 } afmm_mode;
 
 /* op_counts.hpp:17-23 */

@@ -30,7 +30,11 @@
 
 namespace afmm::gpu {
 
-enum class Mode { OrderPreserving = AFMM_MODE_ORDER_PRESERVING, Fast = AFMM_MODE_FAST };
+enum class Mode {
+  OrderPreserving = AFMM_MODE_ORDER_PRESERVING,
+  Fast = AFMM_MODE_FAST,
+  FastLadder = AFMM_MODE_FAST_LADDER
+};
 
 enum class Partition { Work = AFMM_PARTITION_WORK, Rows = AFMM_PARTITION_ROWS };
 

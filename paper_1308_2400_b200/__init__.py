@@ -6,6 +6,7 @@ synthetic-input generators and the multi-GPU row partition used by bench.py.
 """
 from .afmm import (  # noqa: F401
     FAST,
+    FAST_LADDER,
     FORM_KERNELS,
     FORMS,
     ORDER_PRESERVING,
@@ -31,6 +32,6 @@ from .afmm import (  # noqa: F401
 __all__ = [
     "afmm_case_a", "afmm_case_b", "MultiplyResult", "OpCounts", "ShapeError", "DomainError",
     "InvalidArgument", "UnsupportedError", "DeviceError", "DeviceContext", "partition_rows",
-    "fp_add_peak", "kernel_launch_count", "ORDER_PRESERVING", "FAST", "case_a_statistics",
+    "fp_add_peak", "kernel_launch_count", "ORDER_PRESERVING", "FAST", "FAST_LADDER", "case_a_statistics",
     "model_partition_case_a", "model_slab_times_case_a", "FORMS", "FORM_KERNELS", "generate",
 ]

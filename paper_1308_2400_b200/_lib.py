@@ -31,6 +31,7 @@ F64 = 0
 F32 = 1
 MODE_ORDER_PRESERVING = 0
 MODE_FAST = 1
+MODE_FAST_LADDER = 2
 
 # afmm_error_kind
 ERRKIND_NONE = 0

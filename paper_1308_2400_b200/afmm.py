@@ -28,7 +28,9 @@ from . import _lib
 
 ORDER_PRESERVING = "order-preserving"
 FAST = "fast"
-_MODES = {ORDER_PRESERVING: _lib.MODE_ORDER_PRESERVING, FAST: _lib.MODE_FAST}
+FAST_LADDER = "fast-ladder"  # fast + each term's |rep| copies summed as a doubling ladder
+_MODES = {ORDER_PRESERVING: _lib.MODE_ORDER_PRESERVING, FAST: _lib.MODE_FAST,
+          FAST_LADDER: _lib.MODE_FAST_LADDER}
 
 
 class ShapeError(ValueError):

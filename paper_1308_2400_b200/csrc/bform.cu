@@ -172,6 +172,30 @@ struct Acc {
           for (int c = 0; c < 2 * G; ++c) a[c] = L::template add<NEG>(a[c], s.b[c]);
       }
   }
+  // AFMM_MODE_FAST_LADDER: the t copies of the step reassociated as a doubling
+  // ladder. s.b becomes b, 2b, 4b, ... (exact: power-of-two multiples, and
+  // |2^j b| <= |t b|), and the multiples picked by the binary digits of t are
+  // added into the element: floor(log2 t) + popcount(t) adds instead of t.
+  template <bool NEG>
+  __device__ __forceinline__ void add_ladder(Bases<T, G>& s, uint32_t t) {
+#pragma unroll 1
+    while (true) {
+      if (t & 1u) {
+#pragma unroll
+        for (int c = 0; c < 2 * G; ++c) a[c] = L::template add<NEG>(a[c], s.b[c]);
+      }
+      t >>= 1;
+      if (t == 0u) break;
+#pragma unroll
+      for (int c = 0; c < 2 * G; ++c) s.b[c] = L::template add<false>(s.b[c], s.b[c]);
+    }
+  }
+  __device__ __forceinline__ void run_ladder(uint32_t row_addr, int rep) {
+    Bases<T, G> s;
+    s.load(row_addr);
+    if (rep >= 0) add_ladder<false>(s, (uint32_t)rep);
+    else add_ladder<true>(s, 0u - (uint32_t)rep);
+  }
   // |rep| sequential adds of step = rep >= 0 ? base : -base (kernels.hpp:97)
   __device__ __forceinline__ void add(const Bases<T, G>& s, int rep) {
     if (rep >= 0) add_t<false>(s, (uint32_t)rep);
@@ -373,7 +397,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
             int32_t col0, int32_t ncols, const uint32_t* __restrict__ dyn_ncols,
             uint32_t nkb_total, uint32_t slice_blocks, uint64_t slice_stride,
             T* __restrict__ out, uint64_t ld_out, int vec_ok, const DevStatus* __restrict__ st,
-            int group_allow) {
+            int group_allow, int ladder) {
   using Gm = Geo<T, G>;
   extern __shared__ unsigned char smem_raw[];
   // 128-byte aligned ring (TMA destination without swizzle); pointer arithmetic
@@ -468,7 +492,8 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
     AFMM_CHECK(st, cur.kb_cur == kb && cur.stage_addr >= smem_u32(base) &&
                        cur.stage_addr + (uint32_t)Gm::STAGE_BYTES <=
                            smem_u32(base) + (uint32_t)(STAGES * Gm::STAGE_BYTES) + 32u * 16u);
-    acc.run(cur.stage_addr + (k % KB) * BOX_BYTES, e.y);
+    if (BLOCKED && ladder) acc.run_ladder(cur.stage_addr + (k % KB) * BOX_BYTES, e.y);
+    else acc.run(cur.stage_addr + (k % KB) * BOX_BYTES, e.y);
     e = ne;
   }
   cur.drain(nkb, lane);
@@ -881,7 +906,8 @@ cudaError_t launch_ring(BformLaunch& a, T* out, cudaStream_t s) {
   dim3 grid((a.nrows + rpc - 1) / rpc, tiles, a.splits);
   kern<<<grid, (CW + 1) * 32, smem, s>>>(*a.tmap, a.lists, a.cap, a.counts, a.nrows, rpc, a.col0,
                                          a.ncols, a.dyn_ncols, nkb, slice_blocks, a.slice_stride,
-                                         out, a.ld_out, vec_ok ? 1 : 0, a.st, a.group_allow);
+                                         out, a.ld_out, vec_ok ? 1 : 0, a.st, a.group_allow,
+                                         BLOCKED ? a.ladder : 0);
   note_launch();
   return cudaGetLastError();
 }

@@ -129,6 +129,7 @@ struct BformLaunch {
   uint64_t ld_out = 0;
   const DevStatus* st = nullptr;
   int group_allow = 0;          // exit when the device chose the group kernel (group_mode)
+  int ladder = 0;               // fast shape only: each term as a doubling ladder
 };
 template <class T>
 cudaError_t launch_bform(BformLaunch& a, T* out, cudaStream_t s);

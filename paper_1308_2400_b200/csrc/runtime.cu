@@ -364,10 +364,15 @@ afmm_status check_dims(int which, uint64_t n_lhs, uint64_t n_rhs, afmm_error* er
   return AFMM_OK;
 }
 
+// The reassociated modes (AFMM_MODE_FAST, AFMM_MODE_FAST_LADDER) share the
+// blocked-sum kernel shape, the k slices and the B-form-only Case A.
+inline bool is_fast(int mode) { return mode != AFMM_MODE_ORDER_PRESERVING; }
+
 afmm_status check_options(const afmm_options* o, afmm_error* err) {
   if (!o) return AFMM_OK;
-  if (o->mode != AFMM_MODE_ORDER_PRESERVING && o->mode != AFMM_MODE_FAST) {
-    set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: options.mode must be 0 or 1");
+  if (o->mode != AFMM_MODE_ORDER_PRESERVING && o->mode != AFMM_MODE_FAST &&
+      o->mode != AFMM_MODE_FAST_LADDER) {
+    set_error(err, AFMM_ERRKIND_OTHER, 0, 0, 0, 0.0, "afmm: options.mode must be 0, 1 or 2");
     return AFMM_ERR_INVALID_ARGUMENT;
   }
   if (o->split_k < 0 || o->num_devices < 0 || (o->flags & ~AFMM_FLAG_KERNEL_SEMANTICS) ||
@@ -547,7 +552,7 @@ afmm_status launch_compute(afmm_context* c, const Call& call, int shape, const T
                            DevStatus* st, int group_allow, afmm_error* err) {
   // reassociated mode: the blocked-sum kernel (bform.cu kShapeFast), k slices
   // on top when the tile grid is small
-  if (call.mode == AFMM_MODE_FAST) shape = afmm_dev::kShapeFast;
+  if (is_fast(call.mode)) shape = afmm_dev::kShapeFast;
   const ShapeGeo g = shape_geo(shape);
   const uint64_t cbytes = (uint64_t)ncols * sizeof(T);
   const uint64_t ctas = (nrows + g.rows_per_cta - 1) / g.rows_per_cta *
@@ -558,7 +563,7 @@ afmm_status launch_compute(afmm_context* c, const Call& call, int shape, const T
   // Each slice is still the exact repeated-addition chain.
   const uint64_t nkb = (kb_rows + afmm_dev::bform_kb() - 1) / afmm_dev::bform_kb();
   uint32_t splits = 1;
-  if (call.mode == AFMM_MODE_FAST) {
+  if (is_fast(call.mode)) {
     uint64_t want = (2 * slots + ctas - 1) / std::max<uint64_t>(ctas, 1);
     want = std::min<uint64_t>(want, std::max<uint64_t>(nkb / 4, 1));
     want = std::min<uint64_t>(want, 32);
@@ -583,6 +588,7 @@ afmm_status launch_compute(afmm_context* c, const Call& call, int shape, const T
   a.nk = (uint32_t)kb_rows;
   a.st = st;
   a.group_allow = group_allow;
+  a.ladder = call.mode == AFMM_MODE_FAST_LADDER ? 1 : 0;
   if (splits > 1) {
     const uint64_t ldp = round_up((uint64_t)ncols, 32);
     const uint64_t stride = (uint64_t)nrows * ldp;
@@ -605,7 +611,7 @@ afmm_status launch_compute(afmm_context* c, const Call& call, int shape, const T
 // device completes it from the validated rep statistics): fp32, the
 // order-preserving mode, and no forced k_bform shape.
 int group_allow(const afmm_context* c, const Call& call) {
-  if (call.dtype != AFMM_F32 || call.mode == AFMM_MODE_FAST || c->group_off) return 0;
+  if (call.dtype != AFMM_F32 || is_fast(call.mode) || c->group_off) return 0;
   return (c->variant == kAuto || c->variant == kAForm || c->variant == kHybrid) ? 1 : 0;
 }
 
@@ -680,7 +686,7 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
   // blocked fp64 totals bound the fp32 chain error, DESIGN 3.2; the A-form's
   // chains are the order-preserving ones, and on sparse rows of n = 8192 they
   // drift to 2.6e-5 of sum |terms|.)
-  const bool choose = call.which == AFMM_CASE_A && rows > 0 && call.mode != AFMM_MODE_FAST &&
+  const bool choose = call.which == AFMM_CASE_A && rows > 0 && !is_fast(call.mode) &&
                       (c->variant == kAForm || c->variant == kHybrid ||
                        (c->variant == kAuto && n >= 1024));
   // its statistics come out of the validation pass; the A-form's fp16 counts

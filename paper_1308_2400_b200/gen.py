@@ -101,6 +101,29 @@ def expected_additions(case: str, lhs: np.ndarray, rhs: np.ndarray) -> int:
     return int((reps.sum(axis=0) * nnz).sum())
 
 
+def ladder_additions(case: str, lhs: np.ndarray, rhs: np.ndarray) -> int:
+    """FP additions the "fast-ladder" mode PERFORMS on nonzero bases: a term of
+    |rep| copies costs floor(log2 |rep|) doublings + popcount(|rep|)
+    accumulations (the effective count, expected_additions, charges |rep|)."""
+    rep_m = rhs if case == "a" else lhs
+    reps = np.abs(np.rint(rep_m.astype(np.float64))).astype(np.int64)
+    bits = np.zeros_like(reps)
+    top = np.zeros_like(reps)
+    r = reps.copy()
+    level = 0
+    while r.any():
+        bits += r & 1
+        top = np.where(r != 0, level, top)
+        r >>= 1
+        level += 1
+    cost = np.where(reps != 0, bits + top, 0)
+    if case == "a":
+        base_nz = (lhs != 0).astype(np.int64)
+        return int((base_nz.sum(axis=0) * cost.sum(axis=1)).sum())
+    nnz = (rhs != 0).sum(axis=1).astype(np.int64)
+    return int((cost.sum(axis=0) * nnz).sum())
+
+
 def expected_counts(case: str, lhs: np.ndarray, rhs: np.ndarray) -> tuple[int, int, int]:
     """Closed-form OpCounts (additions, multiplications, zero_skips) of valid
     integer-rep operands (SURVEY.md 8.0, test_kernels.cpp:45-57, :160-173):

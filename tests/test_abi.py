@@ -76,6 +76,50 @@ def test_empty_matrix_is_invalid_argument():
     assert str(ei.value) == "DenseMatrix: dimension must be >= 1"
 
 
+def test_mode_codes_and_unknown_mode_rejected():
+    """The three modes of afmm_options.mode (include/afmm_b200.h) and an unknown
+    code: rejected by the C ABI before any device work."""
+    import ctypes
+
+    import paper_1308_2400_b200 as afmm
+    from paper_1308_2400_b200 import _lib
+
+    assert (_lib.MODE_ORDER_PRESERVING, _lib.MODE_FAST, _lib.MODE_FAST_LADDER) == (0, 1, 2)
+    assert afmm.FAST_LADDER == "fast-ladder"
+    with pytest.raises(afmm.InvalidArgument):
+        afmm.afmm_case_a(np.eye(2), np.eye(2), mode="reassociate-everything")
+    lib = _lib.load()
+    o = _lib.Options()
+    o.mode = 3
+    o.device = -1
+    x = np.eye(2)
+    z = np.empty_like(x)
+    c, e = _lib.OpCounts(), _lib.Error()
+    st = lib.afmm_case_a_f64(x.ctypes.data, 2, x.ctypes.data, 2, z.ctypes.data, ctypes.byref(o),
+                             ctypes.byref(c), ctypes.byref(e))
+    assert st == _lib.ERR_INVALID_ARGUMENT
+    assert b"options.mode" in bytes(e.message)
+
+
+def test_ladder_additions_closed_form():
+    """gen.ladder_additions (the adds the fast-ladder mode performs) against a
+    direct count: floor(log2 r) + popcount(r) per nonzero rep and nonzero base."""
+    from paper_1308_2400_b200.gen import expected_additions, ladder_additions
+
+    rng = np.random.default_rng(2)
+    n = 23
+    reps = rng.integers(-40, 41, size=(n, n)).astype(np.float64)
+    bases = rng.standard_normal((n, n)) * (rng.random((n, n)) < 0.6)
+    cost = lambda r: 0 if r == 0 else (abs(r).bit_length() - 1) + bin(abs(r)).count("1")
+    want_b = sum(cost(int(reps[i, k])) * int((bases[k] != 0).sum())
+                 for i in range(n) for k in range(n))
+    assert ladder_additions("b", reps, bases) == want_b
+    want_a = sum(cost(int(reps[k, j])) for i in range(n) for k in range(n) if bases[i, k] != 0
+                 for j in range(n))
+    assert ladder_additions("a", bases, reps) == want_a
+    assert ladder_additions("b", reps, bases) < expected_additions("b", reps, bases)
+
+
 def test_no_cpu_fallback_without_a_device():
     """Without a CUDA device the product must fail loudly, never compute on the host."""
     import torch

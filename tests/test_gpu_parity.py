@@ -323,16 +323,18 @@ def test_full_size_cfg5_rows_in_every_row_block(cuda, fastcheck):
     assert not bad, bad[:10]
 
 
+@pytest.mark.parametrize("mode", ["fast", "fast-ladder"])
 @pytest.mark.parametrize("name", ["cfg2", "cfg4"])
-def test_full_size_fast_mode_within_tolerance(cuda, fastcheck, name):
-    """Reassociated fast mode at FULL size: within 1e-12 (f64) / 1e-5 (f32) of
+def test_full_size_fast_mode_within_tolerance(cuda, fastcheck, name, mode):
+    """Reassociated fast modes at FULL size: within 1e-12 (f64) / 1e-5 (f32) of
     the fp64 reference order (the checker on the exactly widened operands),
-    normalised by sum_k |X[i,k]| |Y[k,j]|; counts unchanged."""
+    normalised by sum_k |X[i,k]| |Y[k,j]|; counts unchanged (the ladder mode
+    reports the reference's tallies, not its own fewer adds)."""
     from paper_1308_2400_b200.gen import CONFIGS, expected_counts, make_inputs
 
     cfg = CONFIGS[name]
     lhs, rhs = make_inputs(name, seed=0)
-    z, counts, _ = _device_product(cfg, lhs, rhs, mode="fast")
+    z, counts, _ = _device_product(cfg, lhs, rhs, mode=mode)
     assert (counts.additions, 0, counts.zero_skips) == expected_counts(cfg.case, lhs, rhs)
     l64, r64 = lhs.astype(np.float64), rhs.astype(np.float64)
     z64 = fastcheck.product(cfg.case, l64, r64)
@@ -533,12 +535,14 @@ def test_ragged_sizes_every_tile_shape(cuda, oracle, case, n, dt):
     assert res.counts.additions == expected_additions(case, lhs, rhs)
 
 
+@pytest.mark.parametrize("mode", ["fast", "fast-ladder"])
 @pytest.mark.parametrize("name,n,kw", [
     ("cfg1", 256, {}), ("cfg2", 1024, {}), ("cfg3", 512, {"d1": 0.5, "mu": 4}),
     ("cfg4", 384, {}), ("cfg5", 640, {}),
 ])
-def test_fast_mode_within_tolerance(cuda, oracle, name, n, kw):
-    """Reassociated fast mode (split-k): within 1e-12 (f64) / 1e-5 (f32) of the fp64
+def test_fast_mode_within_tolerance(cuda, oracle, name, n, kw, mode):
+    """Reassociated fast modes (split-k; with "fast-ladder" each term's |rep|
+    copies as a doubling ladder): within 1e-12 (f64) / 1e-5 (f32) of the fp64
     reference, normalised by sum_k |X[i,k]| |Y[k,j]| (the checker may multiply; the
     kernel may not), with the same OpCounts as the reference."""
     from paper_1308_2400_b200.gen import CONFIGS, make_inputs
@@ -547,12 +551,35 @@ def test_fast_mode_within_tolerance(cuda, oracle, name, n, kw):
     case = CONFIGS[name].case
     l64, r64 = lhs.astype(np.float64), rhs.astype(np.float64)
     z64, c64 = oracle.product_mt(case, l64, r64, 0, n, 8)
-    res = _call(case, lhs, rhs, mode="fast")
+    res = _call(case, lhs, rhs, mode=mode)
     assert (res.counts.additions, 0, res.counts.zero_skips) == c64
     norm = np.abs(l64) @ np.abs(r64)
     err = np.abs(res.product.astype(np.float64) - z64) / np.maximum(norm, 1e-300)
     tol = 1e-12 if lhs.dtype == np.float64 else 1e-5
     assert float(err.max()) <= tol, (name, float(err.max()))
+
+
+@pytest.mark.parametrize("case", ["a", "b"])
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_fast_ladder_exact_on_exact_arithmetic(cuda, oracle, case, dt):
+    """fast-ladder on inputs whose every partial sum is exactly representable
+    (small integer bases, reps of both signs up to +/-300, zeros in both
+    operands): any association gives the same bits, so the doubling ladder
+    must equal the reference's sequential chain exactly -- every rep value
+    1..300 (all binary digit patterns up to 9 bits) and both signs are hit."""
+    n = 320
+    rng = np.random.default_rng(5)
+    bases = rng.integers(-8, 9, size=(n, n)).astype(dt)
+    bases[rng.random((n, n)) < 0.2] = 0
+    reps = rng.integers(-300, 301, size=(n, n)).astype(dt)
+    reps[rng.random((n, n)) < 0.1] = 0
+    reps[0, :301] = np.arange(301)  # every ladder length
+    reps[:301, 0] = -np.arange(301)
+    lhs, rhs = (bases, reps) if case == "a" else (reps, bases)
+    z, c, _ = oracle.product(case, lhs, rhs)
+    res = _call(case, lhs, rhs, mode="fast-ladder")
+    assert (res.counts.additions, 0, res.counts.zero_skips) == c
+    assert _bits_equal(res.product, z)
 
 
 @pytest.mark.parametrize("variant", ["wide", "ring", "small", "aform", "hybrid"])
@@ -992,7 +1019,7 @@ def test_no_write_outside_the_output(cuda, oracle, monkeypatch, variant, dt):
             continue
         L = torch.from_numpy(lhs).cuda()
         R = torch.from_numpy(rhs).cuda()
-        for mode in ("order-preserving", "fast"):
+        for mode in ("order-preserving", "fast", "fast-ladder"):
             r0, r1 = 17, n - 5
             big = torch.full((r1 - r0 + 9, n + 40), sentinel, dtype=tdt, device="cuda")
             view = big[4:4 + r1 - r0, 16:16 + n]

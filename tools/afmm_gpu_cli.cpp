@@ -110,6 +110,14 @@ std::vector<std::size_t> parse_sizes(const std::string& text) {
   return sizes;
 }
 
+// --mode order-preserving | fast | fast-ladder
+afmm::gpu::Mode parse_mode(const std::string& text) {
+  if (text == "order-preserving") return afmm::gpu::Mode::OrderPreserving;
+  if (text == "fast") return afmm::gpu::Mode::Fast;
+  if (text == "fast-ladder") return afmm::gpu::Mode::FastLadder;
+  throw std::invalid_argument("unknown --mode " + text);
+}
+
 std::vector<int> parse_ints(const std::string& text) {
   std::vector<int> v;
   std::stringstream ss(text);
@@ -140,8 +148,7 @@ int bench(const Args& a) {
   if (device_time && !gpu_id) throw std::invalid_argument("--device-time needs a *-gpu kernel");
   afmm_timing timing{};
   afmm::gpu::Options o;
-  o.mode = opt(a, "mode", "order-preserving") == "fast" ? afmm::gpu::Mode::Fast
-                                                         : afmm::gpu::Mode::OrderPreserving;
+  o.mode = parse_mode(opt(a, "mode", "order-preserving"));
   o.devices = parse_ints(opt(a, "devices", ""));
   if (device_time) o.timing = &timing;
   auto call = [&](const afmm::DenseMatrix& lhs, const afmm::DenseMatrix& rhs) {
@@ -413,8 +420,7 @@ int main(int argc, char** argv) {
       const auto lhs = afmm::load_matrix(a.positional[0]);
       const auto rhs = afmm::load_matrix(a.positional[1]);
       afmm::gpu::Options o;
-      o.mode = opt(a, "mode", "order-preserving") == "fast" ? afmm::gpu::Mode::Fast
-                                                             : afmm::gpu::Mode::OrderPreserving;
+      o.mode = parse_mode(opt(a, "mode", "order-preserving"));
       const auto result = multiply(opt(a, "kernel", "afmm-a-gpu"), lhs, rhs, o);
       const std::string out = opt(a, "out", "");
       if (out.empty()) afmm::write_matrix(std::cout, result.product);

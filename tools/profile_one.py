@@ -19,7 +19,7 @@ p.add_argument("--d1", type=float, default=1.0)
 p.add_argument("--mu", type=int, default=16)
 p.add_argument("--n", type=int, default=None)
 p.add_argument("--reps", type=int, default=1)
-p.add_argument("--mode", default="order-preserving", choices=["order-preserving", "fast"])
+p.add_argument("--mode", default="order-preserving", choices=["order-preserving", "fast", "fast-ladder"])
 a = p.parse_args()
 cfg = CONFIGS[a.config]
 lhs, rhs = make_inputs(a.config, seed=0, n=a.n, d1=a.d1, mu=a.mu)
