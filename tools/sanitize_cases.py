@@ -49,7 +49,7 @@ def device(label, case, lhs, rhs, variant=None, mode="order-preserving", reps=1)
         c = ctx.product(case, L, R, O, mode=mode)
     z = O.cpu().numpy()
     ctx.close()
-    if mode == "fast":
+    if mode in ("fast", "fast-ladder"):
         want, cc, _ = oracle.product(case, lhs.astype(np.float64), rhs.astype(np.float64))
         err = np.abs(z - want).max() / max(1.0, np.abs(want).max())
         assert err < 1e-4, (label, err)
@@ -71,6 +71,8 @@ l4, r4 = make_inputs("cfg4", seed=1, n=1100)
 device("case A split (forced)", "a", l4, r4, "hybrid")
 device("case A fp32 fast mode", "a", l4, r4, mode="fast")
 device("case B fp64 fast mode", "b", l2, r2, mode="fast")
+device("case A fp32 fast-ladder mode", "a", l4, r4, mode="fast-ladder")
+device("case B fp32 fast-ladder mode", "b", l5, r5, mode="fast-ladder")
 device("case B graph replays", "b", l2, r2, reps=4)
 device("case A graph replays", "a", la, ra, reps=4)
 # the small-rep group kernel (every rep in 0..2): Case A (column groups, ragged
