@@ -208,6 +208,18 @@ int main() {
     CHECK(gpu::afmm_case_a(x, y, o).product == afmm_case_a(x, y).product);
     CHECK(gpu::afmm_case_b(x, y, o).counts == afmm_case_b(x, y).counts);
   }
+  // the reassociated modes on integer inputs: every partial sum is exact in
+  // any association, so Fast and FastLadder (each term a doubling ladder)
+  // must give the reference's product and its counts
+  for (const auto mode : {gpu::Mode::Fast, gpu::Mode::FastLadder}) {
+    gpu::Options o;
+    o.mode = mode;
+    const auto x = random_integer_matrix(90, -40, 40, 11);
+    const auto y = random_integer_matrix(90, -40, 40, 12);
+    CHECK(gpu::afmm_case_a(x, y, o).product == afmm_case_a(x, y).product);
+    CHECK(gpu::afmm_case_b(x, y, o).product == afmm_case_b(x, y).product);
+    CHECK(gpu::afmm_case_b(x, y, o).counts == afmm_case_b(x, y).counts);
+  }
   // seeded generation on the GPU: the reference's generator, bit for bit
   // (random.hpp:111-129), both roles, edge densities, and validate()'s errors
   {
