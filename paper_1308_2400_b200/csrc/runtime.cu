@@ -228,6 +228,152 @@ struct Call {
   uint32_t rep_max = 0, rep_neg = 0;
 };
 
+
+// Pageable host buffers (a std::vector-backed DenseMatrix, a numpy array): a
+// plain cudaMemcpy2DAsync stages them through the driver's own bounce buffer
+// on the calling thread at ~12 GB/s (measured: cfg5 with pageable operands
+// 2058 ms against 1842 ms with page-locked ones; 1894 ms through this
+// pipeline, cfg4 195 -> 157 ms, n = 4096 23.5 -> 12.8 ms). The stager runs the same
+// copy as a pipeline: kWorkers host threads each pack their chunks of rows
+// into their own page-locked slots (two per worker, so the memcpy of one
+// chunk overlaps the DMA of the previous one) and issue the DMAs on their own
+// streams. Only large copies come here; small ones keep the plain call.
+struct HostStager {
+  static constexpr int kMaxWorkers = 8, kSlots = 2;
+  static constexpr size_t kSlotBytes = 8u << 20;
+  static constexpr size_t kMinBytes = 16u << 20;  // below this the plain copy is as fast
+  int workers = 6;
+  int device = -1;
+  void* slot[kMaxWorkers][kSlots] = {};
+  cudaEvent_t ev[kMaxWorkers][kSlots] = {};
+  cudaStream_t st[kMaxWorkers] = {};
+  cudaEvent_t done[kMaxWorkers] = {};
+
+  // (AFMM_STAGE_WORKERS is read on every call, so a test can vary it)
+  cudaError_t ensure(int dev) {
+    if (device != dev && device >= 0) release();
+    int want = 6;  // 4 -> 6 workers: cfg5 1910 -> 1894 ms, 8 no faster (profiles/r02/pageable)
+    if (const char* v = std::getenv("AFMM_STAGE_WORKERS")) {
+      const int w = std::atoi(v);
+      if (w >= 1 && w <= kMaxWorkers) want = w;
+    }
+    for (int w = 0; w < want; ++w) {
+      if (st[w]) continue;
+      cudaError_t e = cudaStreamCreateWithFlags(&st[w], cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&done[w], cudaEventDisableTiming);
+      for (int k = 0; k < kSlots && e == cudaSuccess; ++k) {
+        e = cudaHostAlloc(&slot[w][k], kSlotBytes, cudaHostAllocDefault);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev[w][k], cudaEventDisableTiming);
+      }
+      if (e != cudaSuccess) {
+        release();
+        return e;
+      }
+    }
+    workers = want;
+    device = dev;
+    return cudaSuccess;
+  }
+  void release() {
+    for (int w = 0; w < kMaxWorkers; ++w) {
+      for (int k = 0; k < kSlots; ++k) {
+        if (slot[w][k]) cudaFreeHost(slot[w][k]);
+        if (ev[w][k]) cudaEventDestroy(ev[w][k]);
+        slot[w][k] = nullptr;
+        ev[w][k] = nullptr;
+      }
+      if (st[w]) cudaStreamDestroy(st[w]);
+      if (done[w]) cudaEventDestroy(done[w]);
+      st[w] = nullptr;
+      done[w] = nullptr;
+    }
+    device = -1;
+  }
+  // Is p ordinary pageable host memory (not page-locked, not managed)?
+  static bool pageable(const void* p) {
+    cudaPointerAttributes attr{};
+    const cudaError_t e = cudaPointerGetAttributes(&attr, p);
+    cudaGetLastError();
+    return e == cudaSuccess && attr.type == cudaMemoryTypeUnregistered;
+  }
+  static bool wants(const void* host, size_t width, size_t height) {
+    return width > 0 && width <= kSlotBytes && width * height >= kMinBytes && pageable(host);
+  }
+  // `height` rows of `width` bytes between a pageable host matrix and device
+  // memory. Host to device: returns once every DMA is enqueued; `join` (the
+  // compute stream) waits for them on the device. Device to host: the caller
+  // has synchronised the producer of `src`; returns when `dst` is complete.
+  cudaError_t copy(bool h2d, void* dst, size_t dpitch, const void* src, size_t spitch,
+                   size_t width, size_t height, cudaStream_t join) {
+    const size_t rpc = std::max<size_t>(1, kSlotBytes / width);
+    const size_t nchunks = (height + rpc - 1) / rpc;
+    const int W = (int)std::min<size_t>((size_t)workers, nchunks);
+    std::vector<cudaError_t> status((size_t)W, cudaSuccess);
+    auto pack = [&](char* to, size_t tpitch, const char* from, size_t fpitch, size_t rows) {
+      if (tpitch == width && fpitch == width) {
+        std::memcpy(to, from, rows * width);
+      } else {
+        for (size_t r = 0; r < rows; ++r) std::memcpy(to + r * tpitch, from + r * fpitch, width);
+      }
+    };
+    auto work = [&](int w) {
+      cudaError_t e = cudaSetDevice(device);
+      auto rows_of = [&](size_t i) { return std::min(rpc, height - i * rpc); };
+      if (h2d) {
+        size_t j = 0;
+        for (size_t i = (size_t)w; i < nchunks && e == cudaSuccess; i += (size_t)W, ++j) {
+          const int k = (int)(j % kSlots);
+          // the slot's last DMA, of this copy or of the previous one (an event
+          // never recorded is complete)
+          e = cudaEventSynchronize(ev[w][k]);
+          if (e != cudaSuccess) break;
+          const size_t rows = rows_of(i);
+          pack(static_cast<char*>(slot[w][k]), width, static_cast<const char*>(src) + i * rpc * spitch,
+               spitch, rows);
+          e = cudaMemcpy2DAsync(static_cast<char*>(dst) + i * rpc * dpitch, dpitch, slot[w][k], width,
+                                width, rows, cudaMemcpyHostToDevice, st[w]);
+          if (e == cudaSuccess) e = cudaEventRecord(ev[w][k], st[w]);
+        }
+        if (e == cudaSuccess) e = cudaEventRecord(done[w], st[w]);
+      } else {
+        const size_t mine = nchunks > (size_t)w ? (nchunks - (size_t)w + (size_t)W - 1) / (size_t)W : 0;
+        auto issue = [&](size_t j) {
+          const size_t i = (size_t)w + j * (size_t)W;
+          const int k = (int)(j % kSlots);
+          cudaError_t ie = cudaMemcpy2DAsync(slot[w][k], width,
+                                             static_cast<const char*>(src) + i * rpc * spitch, spitch,
+                                             width, rows_of(i), cudaMemcpyDeviceToHost, st[w]);
+          if (ie == cudaSuccess) ie = cudaEventRecord(ev[w][k], st[w]);
+          return ie;
+        };
+        if (mine > 0) e = issue(0);
+        for (size_t j = 0; j < mine && e == cudaSuccess; ++j) {
+          if (j + 1 < mine) e = issue(j + 1);  // its slot was emptied one iteration ago
+          if (e == cudaSuccess) e = cudaEventSynchronize(ev[w][j % kSlots]);
+          if (e != cudaSuccess) break;
+          const size_t i = (size_t)w + j * (size_t)W;
+          pack(static_cast<char*>(dst) + i * rpc * dpitch, dpitch,
+               static_cast<const char*>(slot[w][j % kSlots]), width, rows_of(i));
+        }
+      }
+      status[(size_t)w] = e;
+    };
+    std::vector<std::thread> threads;
+    for (int w = 1; w < W; ++w) threads.emplace_back(work, w);
+    work(0);
+    for (auto& t : threads) t.join();
+    cudaSetDevice(device);
+    for (cudaError_t e : status)
+      if (e != cudaSuccess) return e;
+    if (h2d)
+      for (int w = 0; w < W; ++w) {
+        const cudaError_t e = cudaStreamWaitEvent(join, done[w], 0);
+        if (e != cudaSuccess) return e;
+      }
+    return cudaSuccess;
+  }
+};
+
 }  // namespace
 
 struct afmm_context {
@@ -240,6 +386,7 @@ struct afmm_context {
   DevBuf gidx;  // dense group index of the small-rep group kernel (k_bgroup)
   // host-buffer API staging
   DevBuf hx, hy, hz;
+  HostStager stager;  // pageable host operands / result (created on first use)
   DevBuf gen_state, gen_draws, gen_scratch, gen_carry, gen_polys;  // seeded generation (generate.cu)
   DevStatus* status_host = nullptr;           // pinned
   unsigned long long* stats_host = nullptr;   // pinned, 4 words (multi-device Case A statistics)
@@ -1129,12 +1276,19 @@ afmm_status host_product_one(int which, const T* lhs, const T* rhs, uint64_t n, 
   if (!zdev) CK(c->hz.ensure(mat), "afmm: device allocation");
   cudaStream_t s = c->stream;
   if (time_it) CK(cudaEventRecord(c->hev[0], s), "event");
-  CK(cudaMemcpy2DAsync(c->hx.p, ld * sizeof(T), lhs, n * sizeof(T), n * sizeof(T), n,
-                       cudaMemcpyHostToDevice, s),
-     "afmm: H2D");
-  CK(cudaMemcpy2DAsync(c->hy.p, ld * sizeof(T), rhs, n * sizeof(T), n * sizeof(T), n,
-                       cudaMemcpyHostToDevice, s),
-     "afmm: H2D");
+  // pageable operands / result: the staged pipeline (HostStager); page-locked
+  // or small ones: one plain asynchronous copy each
+  auto to_device = [&](void* dst, const T* src) -> cudaError_t {
+    if (HostStager::wants(src, n * sizeof(T), n)) {
+      const cudaError_t e = c->stager.ensure(c->device);
+      if (e != cudaSuccess) return e;
+      return c->stager.copy(true, dst, ld * sizeof(T), src, n * sizeof(T), n * sizeof(T), n, s);
+    }
+    return cudaMemcpy2DAsync(dst, ld * sizeof(T), src, n * sizeof(T), n * sizeof(T), n,
+                             cudaMemcpyHostToDevice, s);
+  };
+  CK(to_device(c->hx.p, lhs), "afmm: H2D");
+  CK(to_device(c->hy.p, rhs), "afmm: H2D");
   Call call;
   call.which = which;
   call.dtype = sizeof(T) == 8 ? AFMM_F64 : AFMM_F32;
@@ -1152,9 +1306,15 @@ afmm_status host_product_one(int which, const T* lhs, const T* rhs, uint64_t n, 
   st = enqueue_call(c, call, err);
   if (st == AFMM_OK) st = finish_locked(c, counts, err);
   if (st == AFMM_OK && !zdev) {
-    CK(cudaMemcpy2DAsync(out, n * sizeof(T), c->hz.p, ld * sizeof(T), n * sizeof(T), n,
-                         cudaMemcpyDeviceToHost, s),
-       "afmm: D2H");
+    // (finish_locked has synchronised the stream: Z is complete on the device)
+    if (HostStager::wants(out, n * sizeof(T), n) && c->stager.ensure(c->device) == cudaSuccess) {
+      CK(c->stager.copy(false, out, n * sizeof(T), c->hz.p, ld * sizeof(T), n * sizeof(T), n, s),
+         "afmm: D2H");
+    } else {
+      CK(cudaMemcpy2DAsync(out, n * sizeof(T), c->hz.p, ld * sizeof(T), n * sizeof(T), n,
+                           cudaMemcpyDeviceToHost, s),
+         "afmm: D2H");
+    }
   }
   if (time_it) CK(cudaEventRecord(c->hev[1], s), "event");
   if (st == AFMM_OK) CK(cudaStreamSynchronize(s), "afmm: D2H");
@@ -1935,6 +2095,7 @@ void afmm_context_destroy(afmm_context* c) {
     for (DevBuf* b : all_bufs(c)) b->release();
     if (c->status_host) cudaFreeHost(c->status_host);
     if (c->stats_host) cudaFreeHost(c->stats_host);
+    c->stager.release();
     for (cudaEvent_t& e : c->ev)
       if (e) cudaEventDestroy(e);
     for (cudaEvent_t& e : c->hev)

@@ -707,6 +707,52 @@ def test_host_api_pinned_output_zero_copy(cuda, oracle, dt, n):
     assert np.all(out == 7.0)
 
 
+@pytest.mark.parametrize("workers", [None, "1", "3"])
+@pytest.mark.parametrize("case,dt,n", [("b", np.float32, 2100), ("a", np.float32, 2051),
+                                       ("b", np.float64, 1500)])
+def test_host_api_pageable_buffers_staged_pipeline(cuda, oracle, monkeypatch, case, dt, n,
+                                                   workers):
+    """Pageable operands and result of >= 16 MB (numpy arrays, like a
+    std::vector-backed DenseMatrix) go through the staged copy pipeline
+    (HostStager in runtime.cu: worker threads packing row chunks into
+    page-locked slots, DMAs on their own streams), with 1, 3 and the default
+    number of workers, ragged last chunks included: the product is bit-identical
+    to the same call on page-locked buffers and to the oracle on sampled rows,
+    the operands are untouched, and a failed validation leaves `out` alone."""
+    import torch
+
+    afmm = _api()
+    if workers:
+        monkeypatch.setenv("AFMM_STAGE_WORKERS", workers)  # read on every call
+    else:
+        monkeypatch.delenv("AFMM_STAGE_WORKERS", raising=False)
+    rng = np.random.default_rng(n)
+    bases = (rng.standard_normal((n, n)) * (rng.random((n, n)) < 0.7)).astype(dt)
+    reps = (rng.integers(0, 4, size=(n, n)) * (rng.random((n, n)) < 0.9)).astype(dt)
+    lhs, rhs = (bases, reps) if case == "a" else (reps, bases)
+    assert lhs.nbytes >= 16 << 20
+    l0, r0 = lhs.copy(), rhs.copy()
+    fn = afmm.afmm_case_a if case == "a" else afmm.afmm_case_b
+    out = np.full((n, n), 7.0, dtype=dt)
+    res = fn(lhs, rhs, out=out)
+    assert _bits_equal(lhs, l0) and _bits_equal(rhs, r0)
+    pl, pr = torch.from_numpy(lhs).pin_memory(), torch.from_numpy(rhs).pin_memory()
+    po = torch.empty_like(pl).pin_memory()
+    ref = fn(pl.numpy(), pr.numpy(), out=po.numpy())
+    assert res.counts == ref.counts
+    assert _bits_equal(out, po.numpy())
+    for r in (0, 1, n // 2, n - 1):
+        zr, _ = oracle.product_mt(case, lhs, rhs, r, r + 1, 1)
+        assert _bits_equal(out[r:r + 1], zr), r
+    out[:] = 7.0
+    bad = reps.copy()
+    bad[n - 1, n - 1] = 0.5
+    args = (bases, bad) if case == "a" else (bad, bases)
+    with pytest.raises(afmm.DomainError, match="is not integer-valued"):
+        fn(*args, out=out)
+    assert np.all(out == 7.0)
+
+
 @pytest.mark.parametrize("name,n", [("cfg2", 3000), ("cfg1", 2049)])
 def test_fp64_configs_at_larger_n_every_row(cuda, oracle, name, n):
     """The fp64 configurations (cfg1 Case A, cfg2 Case B) at several times
