@@ -2000,9 +2000,18 @@ afmm_status generate_host(const afmm_generator_spec* spec, uint64_t seed, T* out
     CK(c->hz.ensure(n * n * sizeof(T)), "workspace");
     afmm_status r = generate_locked<T>(c, *spec, seed, c->hz.as<T>(), n, err);
     if (r != AFMM_OK) return r;
-    CK(cudaMemcpyAsync(out, c->hz.p, n * n * sizeof(T), cudaMemcpyDeviceToHost, c->stream),
-       "result copy");
-    CK(cudaStreamSynchronize(c->stream), "result copy");
+    if (HostStager::wants(out, n * sizeof(T), n) && c->stager.ensure(c->device) == cudaSuccess) {
+      // pageable result: the staged pipeline (its threads also spread the first
+      // touch of a fresh array)
+      CK(cudaStreamSynchronize(c->stream), "generate");
+      CK(c->stager.copy(false, out, n * sizeof(T), c->hz.p, n * sizeof(T), n * sizeof(T), n,
+                        c->stream),
+         "result copy");
+    } else {
+      CK(cudaMemcpyAsync(out, c->hz.p, n * n * sizeof(T), cudaMemcpyDeviceToHost, c->stream),
+         "result copy");
+      CK(cudaStreamSynchronize(c->stream), "result copy");
+    }
     clear_error(err);
     return AFMM_OK;
   });

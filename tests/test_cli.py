@@ -53,6 +53,17 @@ def test_cli_gpu_kernels_byte_identical(cuda, tmp_path):
         assert outs[k][0] == outs["ijk"][0], k
     assert outs["afmm-a-gpu"][1] == outs["afmm-a"][1]  # identical OpCounts line
     assert outs["afmm-b-gpu"][1] == outs["afmm-b"][1]
+    # the reassociated modes: integer operands are exact in any association
+    for mode in ("fast", "fast-ladder"):
+        for k in ("afmm-a-gpu", "afmm-b-gpu"):
+            r = _run("mul", "lhs.mat", "rhs.mat", "--kernel", k, "--mode", mode, "--out",
+                     "pm.mat", cwd=tmp_path)
+            assert r.returncode == 0, r.stderr
+            assert (tmp_path / "pm.mat").read_bytes() == outs["ijk"][0], (mode, k)
+            assert r.stdout.strip() == outs[k][1]
+    r = _run("mul", "lhs.mat", "rhs.mat", "--kernel", "afmm-a-gpu", "--mode", "quick",
+             cwd=tmp_path)
+    assert r.returncode != 0 and "unknown --mode" in r.stderr
     # real-by-integer, bit-exact against the reference CPU kernel in text form
     assert _run("gen", "--n", "40", "--density", "0.8", "--seed", "3", "--out", "x.mat",
                 cwd=tmp_path).returncode == 0
