@@ -725,8 +725,11 @@ def _e2e(args, afmm, dist, torch, world, rank, local, cfg, lhs, rhs, es, job_add
             if nccl:
                 Lp[c0:c1].copy_(hl[c0:c1], non_blocking=True)
                 Rp[c0:c1].copy_(hr[c0:c1], non_blocking=True)
-                dist.all_gather_into_tensor(Lp, Lp[c0:c1].clone())
-                dist.all_gather_into_tensor(Rp, Rp[c0:c1].clone())
+                # (whole padded chunks: the last rank's is short when world
+                # does not divide n; the padding rows stay zero)
+                p0, p1 = rank * chunk, (rank + 1) * chunk
+                dist.all_gather_into_tensor(Lp, Lp[p0:p1].clone())
+                dist.all_gather_into_tensor(Rp, Rp[p0:p1].clone())
             else:  # gloo (functional test): gather host chunks, then one copy
                 for src, dst in ((hl, Lp), (hr, Rp)):
                     parts = [torch.empty_like(torch.zeros(chunk, n, dtype=src.dtype))
