@@ -1279,11 +1279,10 @@ afmm_status host_product_one(int which, const T* lhs, const T* rhs, uint64_t n, 
   // pageable operands / result: the staged pipeline (HostStager); page-locked
   // or small ones: one plain asynchronous copy each
   auto to_device = [&](void* dst, const T* src) -> cudaError_t {
-    if (HostStager::wants(src, n * sizeof(T), n)) {
-      const cudaError_t e = c->stager.ensure(c->device);
-      if (e != cudaSuccess) return e;
+    // (no page-locked memory for the slots: the plain copy still works)
+    if (HostStager::wants(src, n * sizeof(T), n) && c->stager.ensure(c->device) == cudaSuccess)
       return c->stager.copy(true, dst, ld * sizeof(T), src, n * sizeof(T), n * sizeof(T), n, s);
-    }
+    cudaGetLastError();
     return cudaMemcpy2DAsync(dst, ld * sizeof(T), src, n * sizeof(T), n * sizeof(T), n,
                              cudaMemcpyHostToDevice, s);
   };
