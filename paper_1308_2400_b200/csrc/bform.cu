@@ -40,6 +40,8 @@
 // current rep loop so its latency is hidden. Wider tiles (G = 8: 1024 fp32
 // columns, 32 accumulators per lane) amortise the per-entry overhead over
 // twice the adds, which matters for small reps (tools/sweep.py).
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -390,7 +392,11 @@ __device__ __forceinline__ uint32_t lower_bound_k(const int2* lst, uint32_t cnt,
 //   k slice: blockIdx.z selects slice z = [z*slice_blocks, (z+1)*slice_blocks)
 //   of the nkb_total k blocks and writes to out + z * slice_stride (fast-mode
 //   split-k; one slice = the whole k range in order-preserving mode).
-template <class T, int G, int CW, int STAGES, int MINB, bool SPLIT, bool BLOCKED>
+// PACKED: the lists hold 4-byte entries (common.cuh packed_mode); the packed
+// and the int2 instantiation are both launched when the host allows packing,
+// and the one the device-side decision does not pick exits at once.
+template <class T, int G, int CW, int STAGES, int MINB, bool SPLIT, bool BLOCKED,
+          bool PACKED = false>
 __global__ void __launch_bounds__((CW + 1) * 32, MINB)
     k_bform(const __grid_constant__ CUtensorMap tmap, const int2* __restrict__ lists,
             uint64_t cap, const uint32_t* __restrict__ counts, uint32_t nrows, uint32_t rpc,
@@ -409,6 +415,8 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
 
   if (status_failed(st)) return;  // validation failed: compute nothing (kernels.hpp:115,144)
   if (group_mode(st, group_allow)) return;  // the small-rep group kernel runs instead
+  static_assert(!(PACKED && (SPLIT || BLOCKED)), "packed lists: order-preserving mode only");
+  if (packed_mode(st, group_allow) != PACKED) return;  // the other list format's launch runs
   const int32_t tile_c = blockIdx.y * Gm::TILE_N;  // relative to col0
   // the whole CTA beyond the device-decided width: exit (the width is read
   // again at the store rather than kept live across the entry loop)
@@ -472,16 +480,26 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
   // prefetched into L1. (Measured against one coalesced 32-entry load per
   // chunk + SHFL broadcasts: equal at cfg5, cfg3 mu = 4 +2.6%, cfg4 +1%, rep
   // 1 -2%; fewer instructions and branches per entry.)
-  const int2* __restrict__ lp = lst;
-  int2 e = cnt ? __ldg(lp) : make_int2(0, 0);
+  // (PACKED: one 32-bit word per entry, unpacked only when the entry is taken
+  // -- unpacking the prefetched word at once would wait for its load before
+  // the current entry's adds: measured +1% at cfg5, +5% at cfg3 mu = 4)
+  using Entry = typename std::conditional<PACKED, uint32_t, int2>::type;
+  const Entry* __restrict__ lp = reinterpret_cast<const Entry*>(lst);
+  auto decode = [](Entry w) -> int2 {
+    if constexpr (PACKED) return unpack_entry(w);
+    else return w;
+  };
+  Entry raw = cnt ? __ldg(lp) : Entry{};
   for (uint32_t i = 0; i < cnt; ++i) {
+    const int2 e = decode(raw);
     const uint32_t f = i + 1;
-    const int2 ne = f < cnt ? __ldg(lp + f) : make_int2(0, 0);
+    const Entry nraw = f < cnt ? __ldg(lp + f) : Entry{};
     if (f + kListPrefetch < cnt)
       asm volatile("prefetch.global.L1 [%0];" ::"l"(lp + f + kListPrefetch));
     const uint32_t k = (uint32_t)e.x;
     const uint32_t kb = (k - k_lo) / KB;  // block index within the slice
-    AFMM_CHECK(st, k >= k_lo && kb < nkb && e.y != 0 && (i == 0 || (uint32_t)lp[i - 1].x <= k));
+    AFMM_CHECK(st, k >= k_lo && kb < nkb && e.y != 0 &&
+                       (i == 0 || (uint32_t)decode(lp[i - 1]).x <= k));
     if constexpr (BLOCKED) {
       if (kb >= flush_kb) {  // the entry starts a new block of the blocked sum
         tot.flush(acc);
@@ -494,7 +512,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, MINB)
                            smem_u32(base) + (uint32_t)(STAGES * Gm::STAGE_BYTES) + 32u * 16u);
     if (BLOCKED && ladder) acc.run_ladder(cur.stage_addr + (k % KB) * BOX_BYTES, e.y);
     else acc.run(cur.stage_addr + (k % KB) * BOX_BYTES, e.y);
-    e = ne;
+    raw = nraw;
   }
   cur.drain(nkb, lane);
   if constexpr (BLOCKED) {
@@ -904,6 +922,20 @@ cudaError_t launch_ring(BformLaunch& a, T* out, cudaStream_t s) {
   const uint32_t tiles = (a.ncols + Geo<T, G>::TILE_N - 1) / Geo<T, G>::TILE_N;
   const uint32_t rpc = balanced_rows(a.nrows, tiles * a.splits, CW, MINB);
   dim3 grid((a.nrows + rpc - 1) / rpc, tiles, a.splits);
+  if constexpr (!BLOCKED) {
+    // the packed-list instantiation first (it exits unless the device chose
+    // packed lists; the int2 one below exits when it did)
+    if ((a.group_allow & kAllowPack) && want == 1) {
+      auto pk = k_bform<T, G, CW, STAGES, MINB, false, false, true>;
+      e = cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      pk<<<grid, (CW + 1) * 32, smem, s>>>(*a.tmap, a.lists, a.cap, a.counts, a.nrows, rpc, a.col0,
+                                           a.ncols, a.dyn_ncols, nkb, slice_blocks,
+                                           a.slice_stride, out, a.ld_out, vec_ok ? 1 : 0, a.st,
+                                           a.group_allow, 0);
+      note_launch();
+    }
+  }
   kern<<<grid, (CW + 1) * 32, smem, s>>>(*a.tmap, a.lists, a.cap, a.counts, a.nrows, rpc, a.col0,
                                          a.ncols, a.dyn_ncols, nkb, slice_blocks, a.slice_stride,
                                          out, a.ld_out, vec_ok ? 1 : 0, a.st, a.group_allow,

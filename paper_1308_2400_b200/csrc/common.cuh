@@ -82,8 +82,29 @@ constexpr int kGroupRows = 5;  // B-form rows per group (one warp)
 // decided on the device from the validated rep statistics, so the choice needs
 // no host round trip. `allow` is the host's half (fp32, order-preserving mode,
 // no forced k_bform shape).
+// (`allow` carries the host's half of two device-side decisions as bits.)
+constexpr int kAllowGroup = 1;  // the small-rep group kernel may run
+constexpr int kAllowPack = 2;   // the rep lists may be written as packed 4-byte entries
 __device__ __forceinline__ bool group_mode(const DevStatus* st, int allow) {
-  return allow && st->rep_max <= kGroupMaxRep && st->rep_neg == 0;
+  return (allow & kAllowGroup) && st->rep_max <= kGroupMaxRep && st->rep_neg == 0;
+}
+
+// Packed rep lists: when every |rep| of the validated rep operand is <=
+// kPackMaxRep (rep_max saturates at 255) a list entry is one 32-bit word
+// (k << 8) | (rep & 0xff) instead of an int2 {k, rep} -- the lists are re-read
+// once per column tile, so they are most of the repeated-addition kernel's
+// DRAM traffic (cfg5: 31 of 40 GB per launch). Decided on the device like
+// group_mode; the host's half (kAllowPack) requires k < 2^24, the
+// order-preserving mode and a problem large enough to matter.
+constexpr uint32_t kPackMaxRep = 127;
+__device__ __forceinline__ bool packed_mode(const DevStatus* st, int allow) {
+  return (allow & kAllowPack) && st->rep_max <= kPackMaxRep;
+}
+__device__ __forceinline__ uint32_t pack_entry(uint32_t k, long long rep) {
+  return (k << 8) | ((uint32_t)(int)rep & 0xffu);
+}
+__device__ __forceinline__ int2 unpack_entry(uint32_t e) {
+  return make_int2((int)(e >> 8), (int)(e << 24) >> 24);
 }
 
 // kernels.hpp:31-40 on the widened value: 0 ok, 1 not integer-valued,

@@ -349,6 +349,7 @@ __global__ void k_rows(const T* __restrict__ x, uint64_t ld, uint32_t n, int whi
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   // group mode: k_bgroup reads the dense group index instead of the lists
   const bool lists_needed = lists != nullptr && !group_mode(st, group_allow);
+  const bool packed = packed_mode(st, group_allow);  // 4-byte entries (every |rep| <= 127)
   for (uint64_t i = a0 + warp; i < a1; i += nwarps) {
     const T* row = x + i * ld;
     const bool in_slab = i >= r0 && i < r1;
@@ -406,7 +407,10 @@ __global__ void k_rows(const T* __restrict__ x, uint64_t ld, uint32_t n, int whi
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             if (ne[e] == 1) {
-              if (pos < cap) out[pos] = make_int2((int)(j0 + e), (int)rep[e]);
+              if (pos < cap) {
+                if (packed) reinterpret_cast<uint32_t*>(out)[pos] = pack_entry(j0 + e, rep[e]);
+                else out[pos] = make_int2((int)(j0 + e), (int)rep[e]);
+              }
               ++pos;
             } else {
               for (uint32_t c = 0; c < ne[e]; ++c, ++pos)
@@ -447,6 +451,7 @@ __global__ void __launch_bounds__(256)
                         const uint32_t* __restrict__ skip, int group_allow) {
   if (skip && *skip == 0) return;
   if (group_mode(st, group_allow)) return;  // k_bgroup runs: no lists
+  const bool packed = packed_mode(st, group_allow);  // 4-byte entries (every |rep| <= 127)
   __shared__ T tile[32][33];
   const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const uint32_t j0 = blockIdx.x * 32;
@@ -476,11 +481,18 @@ __global__ void __launch_bounds__(256)
       const uint32_t ne = entries_for(abs_ll(rep), kMaxRep);
       uint32_t total;
       unsigned long long pos = base[q] + warp_excl_scan(ne, tx, &total);
-      if (j < n)
-        for (uint32_t c = 0; c < ne; ++c, ++pos)
-          if (pos < cap)
-            lists[(uint64_t)j * cap + pos] =
-                make_int2((int)k, (int)(ne == 1 ? rep : part_of(rep, c, kMaxRep)));
+      if (j < n) {
+        if (packed) {  // (ne <= 1: no rep is split)
+          if (ne && pos < cap)
+            reinterpret_cast<uint32_t*>(lists + (uint64_t)j * cap)[pos] = pack_entry(k, rep);
+          pos += ne;
+        } else {
+          for (uint32_t c = 0; c < ne; ++c, ++pos)
+            if (pos < cap)
+              lists[(uint64_t)j * cap + pos] =
+                  make_int2((int)k, (int)(ne == 1 ? rep : part_of(rep, c, kMaxRep)));
+        }
+      }
       base[q] += total;
     }
     __syncthreads();

@@ -89,6 +89,13 @@ bool group_off_from_env() {
   return v && std::strcmp(v, "nogroup") == 0;
 }
 
+// AFMM_BFORM=nopack: automatic choices, but the rep lists stay int2 {k, rep}
+// (never the packed 4-byte entries) -- for comparisons.
+bool pack_off_from_env() {
+  const char* v = std::getenv("AFMM_BFORM");
+  return v && std::strcmp(v, "nopack") == 0;
+}
+
 inline uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
 
 int sm_count(int device) {
@@ -395,6 +402,7 @@ struct afmm_context {
   uint64_t cap_need = 0;  // list capacity demanded by an overflowing product (re-run)
   int variant = kAuto;
   bool group_off = false;  // AFMM_BFORM=nogroup
+  bool pack_off = false;   // AFMM_BFORM=nopack
   // kernel(s) of the last call: Case A 0 B-form, 1 A-form, 2 split; + 4 when
   // the B-form part ran the small-rep group kernel (Case B: 0 or 4)
   int last_form = 0;
@@ -762,6 +770,15 @@ int group_allow(const afmm_context* c, const Call& call) {
   return (c->variant == kAuto || c->variant == kAForm || c->variant == kHybrid) ? 1 : 0;
 }
 
+// The host's half of the packed-list decision (packed_mode() on the device
+// completes it: every |rep| <= 127): the order-preserving mode, k < 2^24, and
+// a problem whose lists are worth halving (below n = 2048 the second, exiting
+// launch costs more than the bytes save). AFMM_BFORM=nopack keeps int2 lists.
+int pack_allow(const afmm_context* c, const Call& call) {
+  if (is_fast(call.mode) || c->pack_off || call.n < 2048 || call.n >= (1ull << 24)) return 0;
+  return afmm_dev::kAllowPack;
+}
+
 // Group index row length: k rounded up to whole ring stages.
 uint64_t group_ldg(uint64_t n) { return round_up(n, (uint64_t)afmm_dev::bform_kb()); }
 
@@ -817,7 +834,10 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
   afmm_dev::take_launch_error();  // (a stale one belongs to no product)
   CK(cudaMemsetAsync(st, 0, sizeof(DevStatus), s), "memset");
   const int gallow = group_allow(c, call);
-  if (call.prevalidated && gallow) {
+  // the bits the kernels combine with the validated rep statistics: the group
+  // kernel (gallow) and packed 4-byte list entries
+  const int allow = gallow | pack_allow(c, call);
+  if (call.prevalidated && allow) {
     // the shards' merged rep statistics (k_scan_stats does not run here);
     // both fields are < 256, so a one-byte memset of the low byte sets them
     CK(cudaMemsetAsync(&st->rep_max, (int)std::min<uint32_t>(call.rep_max, 255u), 1, s), "memset");
@@ -854,7 +874,7 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
     CK(c->counts.ensure(std::max<uint64_t>(rows, 1) * 4), "workspace");
     afmm_dev::launch_rows<T>(lhs, ld, n32, 1, nnz, nullptr, (uint32_t)r0, (uint32_t)r1,
                              (uint32_t)r0, (uint32_t)r1, c->lists.as<int2>(), cap,
-                             c->counts.as<uint32_t>(), nullptr, st, s, nullptr, gallow);
+                             c->counts.as<uint32_t>(), nullptr, st, s, nullptr, allow);
     if (gallow && rows > 0) {
       const uint64_t ldg = group_ldg(n), ngroups = (rows + afmm_dev::kGroupRows - 1) / afmm_dev::kGroupRows;
       CK(c->gidx.ensure(ngroups * ldg * sizeof(uint16_t)), "workspace");
@@ -874,7 +894,7 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
     c->mark(1);
     if (rows > 0) {
       afmm_status cs = launch_compute<T>(c, call, shape, base, n, n, ldb, (uint32_t)rows,
-                                         (int32_t)n, nullptr, out, ld_out, st, gallow, err);
+                                         (int32_t)n, nullptr, out, ld_out, st, allow, err);
       if (cs != AFMM_OK) return cs;
       if (gallow) {
         cs = launch_group_compute<T>(c, base, n, n, ldb, (uint32_t)rows, (int32_t)n, nullptr, out,
@@ -938,7 +958,7 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
     if (rows > 0) {
       afmm_dev::launch_transpose_compact<T>(rhs, ld, n32, c->lists.as<int2>(), cap,
                                             c->counts.as<uint32_t>(), st,
-                                            plan ? plan + 1 : nullptr, s, gallow);
+                                            plan ? plan + 1 : nullptr, s, allow);
       if (gallow) {
         const uint64_t ldg = group_ldg(n), ngroups = (n + afmm_dev::kGroupRows - 1) / afmm_dev::kGroupRows;
         CK(c->gidx.ensure(ngroups * ldg * sizeof(uint16_t)), "workspace");
@@ -965,7 +985,7 @@ afmm_status enqueue_product(afmm_context* c, const Call& call, afmm_error* err) 
       // B-form: Case A as Case B on transposed operands, Z^T = (Y^T) (x) (X^T)
       afmm_status cs = launch_compute<T>(c, call, shape, c->xt.as<T>(), n, rows, lds, n32,
                                          (int32_t)rows, plan ? plan + 1 : nullptr, c->zt.as<T>(),
-                                         lds, st, gallow, err);
+                                         lds, st, allow, err);
       if (cs != AFMM_OK) return cs;
       if (gallow) {
         cs = launch_group_compute<T>(c, c->xt.as<T>(), n, rows, lds, n32, (int32_t)rows,
@@ -2066,6 +2086,7 @@ afmm_status afmm_context_create(int32_t device, afmm_context** ctx) {
   c->device = device;
   c->variant = variant_from_env();
   c->group_off = group_off_from_env();
+  c->pack_off = pack_off_from_env();
   {
     const char* gv = std::getenv("AFMM_GRAPHS");
     c->graphs = !(gv && std::strcmp(gv, "0") == 0);

@@ -707,6 +707,49 @@ def test_host_api_pinned_output_zero_copy(cuda, oracle, dt, n):
     assert np.all(out == 7.0)
 
 
+@pytest.mark.parametrize("top", [127, 128])
+@pytest.mark.parametrize("case,dt", [("b", np.float32), ("a", np.float32), ("b", np.float64)])
+def test_packed_rep_lists_boundary(cuda, oracle, monkeypatch, case, dt, top):
+    """Rep lists as packed 4-byte entries (k << 8 | rep & 0xff; n >= 2048, every
+    |rep| <= 127: decided on the device from the validated statistics) against
+    int2 {k, rep} lists: reps of both signs up to +/-127 run packed, one rep of
+    +/-128 anywhere sends the whole product to the int2 lists; both are
+    bit-exact on sampled rows (the rows holding the extreme reps included),
+    equal to the run with packing disabled (AFMM_BFORM=nopack), and sharded
+    over two contexts."""
+    afmm = _api()
+    n = 2080
+    rng = np.random.default_rng(top)
+    bases = (rng.standard_normal((n, n)) * (rng.random((n, n)) < 0.6)).astype(dt)
+    reps = (rng.integers(-3, 4, size=(n, n)) * (rng.random((n, n)) < 0.5)).astype(dt)
+    reps[5, 7] = top
+    reps[n - 1, n - 2] = -top
+    reps[100, 0] = 127
+    reps[0, 100] = -127
+    lhs, rhs = (bases, reps) if case == "a" else (reps, bases)
+    fn = afmm.afmm_case_a if case == "a" else afmm.afmm_case_b
+    res = fn(lhs, rhs)
+    rows = [0, 5, 7, 100, n - 2, n - 1] if case == "b" else [0, 1, 5, n // 2, n - 1]
+    for r in rows:
+        zr, _ = oracle.product_mt(case, lhs, rhs, r, r + 1, 1)
+        assert _bits_equal(res.product[r:r + 1], zr), r
+    from paper_1308_2400_b200.gen import expected_counts
+
+    assert (res.counts.additions, 0, res.counts.zero_skips) == expected_counts(case, lhs, rhs)
+    sharded = fn(lhs, rhs, devices=[0, 0])
+    assert _bits_equal(sharded.product, res.product) and sharded.counts == res.counts
+    import torch
+
+    monkeypatch.setenv("AFMM_BFORM", "nopack")
+    ctx = afmm.DeviceContext(0)  # reads AFMM_BFORM at creation
+    L, R = torch.from_numpy(lhs).cuda(), torch.from_numpy(rhs).cuda()
+    O = torch.empty_like(L)
+    c = ctx.product(case, L, R, O)
+    ctx.close()
+    assert _bits_equal(O.cpu().numpy(), res.product)
+    assert (c.additions, c.zero_skips) == (res.counts.additions, res.counts.zero_skips)
+
+
 @pytest.mark.parametrize("workers", [None, "1", "3"])
 @pytest.mark.parametrize("case,dt,n", [("b", np.float32, 2100), ("a", np.float32, 2051),
                                        ("b", np.float64, 1500)])

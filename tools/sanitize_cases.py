@@ -84,6 +84,14 @@ lh, rh = make_inputs("cfg3", seed=2, n=1100, d1=0.5, mu=1)
 device("case A split with group B part (forced)", "a", lh, rh, "hybrid")
 os.environ.pop("AFMM_BFORM", None)
 
+# packed 4-byte list entries (n >= 2048, every |rep| <= 127), both cases, and
+# the int2 lists at the same size (AFMM_BFORM=nopack)
+lp, rp = make_inputs("cfg3", seed=3, n=2048, d1=0.5, mu=4)
+device("case A packed lists", "a", lp, rp)
+device("case B packed lists", "b", rp.T.copy(), lp)
+device("case B int2 lists at n = 2048", "b", rp.T.copy(), lp, "nopack")
+os.environ.pop("AFMM_BFORM", None)
+
 bad = l2.copy()
 bad[7, 3] = 0.5
 try:
