@@ -750,6 +750,36 @@ def test_packed_rep_lists_boundary(cuda, oracle, monkeypatch, case, dt, top):
     assert (c.additions, c.zero_skips) == (res.counts.additions, res.counts.zero_skips)
 
 
+def test_packed_rep_lists_redecided_on_graph_replays(cuda, oracle):
+    """The packed / int2 list choice is made on the device from each call's
+    validated statistics, so a replayed CUDA graph (device API, identical
+    calls) follows the data: reps <= 127 (packed), then one rep of 300 written
+    in place (int2 lists), then back -- sampled rows bit-exact every time."""
+    import torch
+
+    afmm = _api()
+    n = 2048
+    rng = np.random.default_rng(9)
+    reps = (rng.integers(0, 5, size=(n, n)) * (rng.random((n, n)) < 0.5)).astype(np.float32)
+    bases = (rng.standard_normal((n, n)) * (rng.random((n, n)) < 0.7)).astype(np.float32)
+    ctx = afmm.DeviceContext(0)
+    L, R = torch.from_numpy(reps).cuda(), torch.from_numpy(bases).cuda()
+    O = torch.empty_like(L)
+    cur = reps.copy()
+    for it in range(7):
+        if it == 3:
+            cur[11, 13] = 300.0
+        if it == 5:
+            cur[11, 13] = -127.0
+        L.copy_(torch.from_numpy(cur))
+        ctx.product("b", L, R, O)
+        z = O.cpu().numpy()
+        for r in (0, 11, n - 1):
+            zr, _ = oracle.product_mt("b", cur, bases, r, r + 1, 1)
+            assert _bits_equal(z[r:r + 1], zr), (it, r)
+    ctx.close()
+
+
 @pytest.mark.parametrize("workers", [None, "1", "3"])
 @pytest.mark.parametrize("case,dt,n", [("b", np.float32, 2100), ("a", np.float32, 2051),
                                        ("b", np.float64, 1500)])
