@@ -366,7 +366,13 @@ struct HostStager {
       status[(size_t)w] = e;
     };
     std::vector<std::thread> threads;
-    for (int w = 1; w < W; ++w) threads.emplace_back(work, w);
+    for (int w = 1; w < W; ++w) {
+      try {
+        threads.emplace_back(work, w);
+      } catch (...) {  // no thread to be had: this worker's chunks on the calling thread
+        work(w);
+      }
+    }
     work(0);
     for (auto& t : threads) t.join();
     cudaSetDevice(device);
