@@ -259,7 +259,10 @@ struct HostStager {
   // (AFMM_STAGE_WORKERS is read on every call, so a test can vary it)
   cudaError_t ensure(int dev) {
     if (device != dev && device >= 0) release();
-    int want = 6;  // 4 -> 6 workers: cfg5 1910 -> 1894 ms, 8 no faster (profiles/r02/pageable)
+    // 4 -> 6 workers: cfg5 1910 -> 1894 ms, 8 no faster (profiles/r02/pageable);
+    // at most half the host's hardware threads
+    const unsigned hw = std::thread::hardware_concurrency();
+    int want = hw == 0 ? 6 : (int)std::min<unsigned>(6u, std::max<unsigned>(2u, hw / 2));
     if (const char* v = std::getenv("AFMM_STAGE_WORKERS")) {
       const int w = std::atoi(v);
       if (w >= 1 && w <= kMaxWorkers) want = w;
