@@ -761,7 +761,19 @@ def _e2e(args, afmm, dist, torch, world, rank, local, cfg, lhs, rhs, es, job_add
         t = torch.tensor([secs], dtype=torch.float64, device="cpu" if on_cpu else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         secs = float(t[0])
-    return {"value": job_adds / secs, "unit": UNIT,
+    pageable = None
+    if world == 1:
+        # the same call on PAGEABLE buffers (what a std::vector-backed DenseMatrix
+        # or a numpy caller passes): the staged copy pipeline (DESIGN 5)
+        out_pg = np.empty_like(lhs)
+        fn(lhs, rhs, device=local, out=out_pg, mode=args.mode)
+        t1 = time.perf_counter()
+        for _ in range(2):
+            fn(lhs, rhs, device=local, out=out_pg, mode=args.mode)
+        secs_pg = (time.perf_counter() - t1) / 2
+        pageable = {"value": job_adds / secs_pg, "unit": UNIT, "ms_per_step": secs_pg * 1e3,
+                    "steps": 2}
+    return {"value": job_adds / secs, "unit": UNIT, "pageable_host_buffers": pageable,
             "h2d_bytes_per_step": 2 * n * n * es, "d2h_bytes_per_step": n * n * es,
             "ms_per_step": secs * 1e3, "steps": reps,
             "device_ms_per_step": statistics.median(dev_ms) if dev_ms else None,
